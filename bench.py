@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""SpecFormer decode-step benchmark (one JSON line on rank 0).
+
+A "step" = one draft_step + verify_step + accept_commit over the GPU's batch (all §8(a) rows),
+replayed from a CUDA graph through the C ABI. Workload: BASELINE.json configs[2] (7B-shaped,
+k = 4, prompt 512) at batch 64 per GPU (weak scaling across ranks); synthetic seeded weights and
+uniform-random prompts; inputs (14 GB of weights + KV) are far larger than the 126 MB L2, so no
+explicit flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--config 7b] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, max-over-ranks timing)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+A_PAPER = {"small": 1.84, "7b": 1.75, "13b": 1.71, "70b": 1.71, "tiny": 1.84}  # SURVEY §8d (T3, k=4)
+METRIC = "generated tokens/s per box (7B-shaped SpecFormer SD step, measured acceptance)"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons DURING the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, dev_index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- oracle leg
+def oracle_sample(cfg, n_steps=2, prompt_len=32):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload: ONE sequence at the
+    config's full width with the base truncated to L = 1 and L = 2 layers (same head), prompt
+    `prompt_len`, `n_steps` SD steps each. Per-step time at full depth is extrapolated linearly in
+    L: t(L) = t(1) + (L - 1) (t(2) - t(1)). The oracle computes sequences one by one, so the
+    box-level tokens/s = tokens per step per sequence / t(L_full)."""
+    import numpy as np
+    import oracle as O
+    from synth import make_prompts, make_weights
+
+    c2 = cfg.replace(n_layers=2)
+    w = make_weights(c2, seed=0, device="cpu")
+    prompt = make_prompts(1, prompt_len, cfg.vocab)[0].tolist()
+    times = {}
+    toks = {}
+    for L in (1, 2):
+        W = O.Weights(cfg.replace(n_layers=L), w)
+        # the oracle's own loop: prefill (untimed part subtracted) then n_steps SD steps
+        t0 = time.perf_counter()
+        cache = O.model._new_cache(W.cfg)
+        _, i_d, _ = O.prefill(W, prompt, cache)
+        t1 = time.perf_counter()
+        out, steps = O.sd_decode(W, prompt, 1 + n_steps)  # includes its own prefill
+        t2 = time.perf_counter()
+        # sd_decode = prefill + steps; subtract the separately timed prefill
+        times[L] = max(1e-9, ((t2 - t1) - (t1 - t0)) / max(1, len(steps)))
+        toks[L] = sum(s["m"] + 1 for s in steps) / max(1, len(steps))
+    t_full = times[1] + (cfg.n_layers - 1) * (times[2] - times[1])
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    a = toks[2]
+    return {"value": a / t_full, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"1 sequence, width {cfg.d_model}, base depth 1 and 2 of {cfg.n_layers} layers "
+                      f"(linear extrapolation in L), prompt {prompt_len}, {n_steps} SD steps each; "
+                      f"t_step(L=1)={times[1]:.3f}s t_step(L=2)={times[2]:.3f}s -> t_step(L={cfg.n_layers})="
+                      f"{t_full:.2f}s per sequence; sequences are processed one at a time",
+            "seconds_per_step_per_sequence": t_full}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state; warm-up steps are part of each sample below
+    t0 = time.perf_counter()
+    cb = oracle_sample(cfg, n_steps=max(1, min(args.steps, 3)))
+    wall = time.perf_counter() - t0
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * cb["seconds_per_step_per_sequence"] * args.batch,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded N(0,0.02) weights, uniform-random prompts)",
+            "config": {"workload": f"{cfg.name}-shaped SpecFormer decode step, batch {args.batch}/GPU, k {cfg.draft_len}",
+                       "model": cfg.name, "batch_per_gpu": args.batch, "draft_len": cfg.draft_len,
+                       "prompt_len": cfg.prompt_len, "l2": "inputs larger than L2"},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU leg
+def run_ours(args, cfg):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_20340_b200 import Engine, EngineConfig, roofline
+    from paper_2511_20340_b200 import _native as N
+    from synth import make_prompts, make_weights
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    B, k, P = args.batch, cfg.draft_len, cfg.prompt_len
+    K, W = args.steps, args.warmup
+    Kp = args.profile_steps
+    Ke = args.e2e_steps
+    max_seq = P + (W + K + Kp + 4) * (k + 1) + 32
+    max_seq = max(max_seq, P + (Ke + 4) * (k + 1) + 32)
+    max_seq = (max_seq + 15) // 16 * 16
+
+    weights = make_weights(cfg, seed=0, device="cuda")
+    ec = EngineConfig.from_model(cfg, max_batch=B, max_seq=max_seq, flags=N.SF_FLAG_CUDA_GRAPH)
+    eng = Engine(ec, weights)
+    del weights
+    torch.cuda.empty_cache()
+    prompts = make_prompts(B * world, P, cfg.vocab)[rank * B:(rank + 1) * B].contiguous()
+
+    eng.prefill(prompts.cuda())
+    eng.decode_steps(W)
+    eng.sync()
+    before = eng.capture(3, (B,), torch.int32).cpu()
+    prev_before = eng.capture(5, (B,), torch.int32).cpu()
+    acc_log = torch.zeros(K, B, dtype=torch.int32, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(eng.stream)
+        eng.decode_steps(K, None, acc_log)
+        e1.record(eng.stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    eng.sync()
+    ms = e0.elapsed_time(e1)
+    launches = eng.kernel_launches()
+    after = eng.capture(3, (B,), torch.int32).cpu()
+    tokens = int((after - before).sum())
+    stats = torch.tensor([ms, float(tokens)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        mx = stats.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = stats.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, tokens_total = float(mx[0]), float(sm[1])
+    else:
+        ms_max, tokens_total = ms, float(tokens)
+    value = tokens_total / (ms_max / 1e3)
+    steps_per_s = K / (ms_max / 1e3)
+    a_meas = tokens / (K * B)
+
+    # ---------------- roofline: per-class kernel durations from a profiled eager pass
+    hbm, tf_burst, tf_sust, peak_src = peaks()
+    lens0 = eng.capture(3, (B,), torch.int32).cpu().tolist()
+    prev0 = eng.capture(5, (B,), torch.int32).cpu().tolist()  # context layer runs at n_prev
+    acc_p = torch.zeros(Kp, B, dtype=torch.int32, device="cuda")
+    eng.profile(True)
+    ep0, ep1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ep0.record(eng.stream)
+    eng.decode_steps(Kp, None, acc_p)
+    ep1.record(eng.stream)
+    eng.sync()
+    prof_ms_total = ep0.elapsed_time(ep1)
+    cls = {c: eng.profile_read(c) for c in range(4)}
+    eng.profile(False)
+    accs = acc_p.cpu().tolist()
+    # reconstruct per-step lengths: verify at n_b, context layer at the previous n_b
+    lens, prevs = list(lens0), list(prev0)
+    attn_bytes = 0.0
+    step_bytes_tot = 0.0
+    step_flops_tot = 0.0
+    for s in range(Kp):
+        ctx_lens = prevs
+        attn_bytes += roofline.attention_kv_bytes(cfg, lens, ctx_lens, k)
+        step_bytes_tot += roofline.step_bytes(cfg, B, k, lens, ctx_lens)
+        step_flops_tot += roofline.step_flops(cfg, B, k, lens)
+        prevs = list(lens)
+        lens = [n + m + 1 for n, m in zip(lens, accs[s])]
+    gemm_ms, gemm_n, gemm_bytes = cls[0]
+    attn_ms, attn_n, _ = cls[1]
+    dominant = "gemm" if gemm_ms >= attn_ms else "attention"
+    if dominant == "gemm":
+        achieved = gemm_bytes / (gemm_ms / 1e3) / 1e9
+        dom_bytes_per_launch = gemm_bytes / max(1, gemm_n)
+        dom_ms = gemm_ms / max(1, gemm_n)
+    else:
+        achieved = attn_bytes / (attn_ms / 1e3) / 1e9
+        dom_bytes_per_launch = attn_bytes / max(1, attn_n)
+        dom_ms = attn_ms / max(1, attn_n)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(dominant)
+        except Exception:
+            traffic = None
+    prof_classes = {name: {"ms_total": cls[c][0], "launches": cls[c][1], "share_of_profiled_step":
+                           cls[c][0] / max(1e-9, prof_ms_total)}
+                    for c, name in enumerate(["gemm", "attention", "norm", "argmax"])}
+    prof_classes["gemm"]["achieved_gbs"] = gemm_bytes / max(1e-12, gemm_ms / 1e3) / 1e9
+    prof_classes["attention"]["achieved_gbs"] = attn_bytes / max(1e-12, attn_ms / 1e3) / 1e9
+    # whole-step roofline over the timed (graph) region, lengths reconstructed from the accept log
+    lens_t = before.tolist()
+    accs_t = acc_log.cpu().tolist()
+    sb = 0.0
+    prev_t = prev_before.tolist()
+    for s in range(K):
+        sb += roofline.step_bytes(cfg, B, k, lens_t, prev_t)
+        prev_t = list(lens_t)
+        lens_t = [n + m + 1 for n, m in zip(lens_t, accs_t[s])]
+    step_gbs = sb / (ms / 1e3) / 1e9
+
+    # ---------------- e2e: public C-ABI calls with pinned HOST buffers, copies inside the region
+    lib = eng.lib
+    host_prompts = prompts.clone().pin_memory()
+    g_host = torch.empty(B, dtype=torch.int32).pin_memory()
+    m_host = torch.empty(Ke, B, dtype=torch.int32).pin_memory()
+    em_host = torch.empty(Ke, B, k + 1, dtype=torch.int32).pin_memory()
+    sl_host = torch.empty(Ke, B, dtype=torch.int32).pin_memory()
+    p = lambda t: C.c_void_p(t.data_ptr())
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record(eng.stream)
+    st = lib.specformer_prefill(eng.h, p(host_prompts), B, P, p(g_host))
+    for s in range(Ke):
+        st |= lib.specformer_draft_step(eng.h, None, None)
+        st |= lib.specformer_verify_step(eng.h, None, None, None)
+        st |= lib.specformer_accept_commit(eng.h, p(m_host[s]), p(em_host[s]), p(sl_host[s]))
+    x1.record(eng.stream)
+    eng.sync()
+    if st != 0:
+        raise RuntimeError("e2e C-ABI call failed")
+    e2e_ms = x0.elapsed_time(x1)
+    e2e_tokens = B + int((em_host >= 0).sum())
+    e2 = torch.tensor([e2e_ms, float(e2e_tokens)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        mx = e2.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = e2.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        e2e_ms_max, e2e_tok = float(mx[0]), float(sm[1])
+    else:
+        e2e_ms_max, e2e_tok = e2e_ms, float(e2e_tokens)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = oracle_sample(cfg)
+        except MemoryError as ex:  # bounded sample did not fit the host
+            cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "oracle",
+                   "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded N(0,0.02) weights, uniform-random prompts)",
+            "config": {"workload": f"{cfg.name}-shaped SpecFormer decode step (draft+verify+accept), "
+                                   f"batch {B}/GPU, k {k}, prompt {P}",
+                       "model": cfg.name, "batch_per_gpu": B, "global_batch": B * world, "draft_len": k,
+                       "prompt_len": P, "parallelism": f"dp{world}", "cuda_graph": True,
+                       "l2": "inputs larger than L2 (14 GB weights + KV per step)"},
+            "verify_steps_per_s": steps_per_s, "verify_steps_per_s_box": steps_per_s * world,
+            "mean_accepted_length": a_meas,
+            "modeled_tokens_per_s_at_paper_a": steps_per_s * B * world * A_PAPER.get(cfg.name, 1.75),
+            "a_paper": A_PAPER.get(cfg.name),
+            "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
+                         "bytes_per_launch": dom_bytes_per_launch, "ms_per_launch": dom_ms,
+                         "classes": prof_classes, "profiled_steps": Kp},
+            "step_roofline": {"bound": "hbm", "achieved": step_gbs, "peak": hbm, "unit": "GB/s",
+                              "frac": step_gbs / hbm, "bytes_per_step": sb / K,
+                              "flops_per_step": step_flops_tot / max(1, Kp),
+                              "t_roof_ms": (sb / K) / (hbm * 1e9) * 1e3},
+            "e2e": {"value": e2e_tok / (e2e_ms_max / 1e3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": B * P * 4 / Ke, "d2h_bytes_per_step": B * (k + 3) * 4,
+                    "steps": Ke, "includes_prefill": True, "note": "prompt H2D amortised over the steps"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    eng.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--config", default="7b")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--profile-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    from synth import get_config
+    cfg = get_config(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,175 @@
+/*
+ * specformer.h -- C ABI of the B200-native SpecFormer speculative-decoding hot path.
+ *
+ * The three calls mirror the paper's three-step SD protocol (PAPER.md P20-23, §Intro):
+ *   specformer_draft_step   "Multi-token generation: based on information from the previous
+ *                            forward pass, the model samples multiple draft tokens"
+ *                            = SpecFormer context causal attention (Eq.8, P179-188), positional
+ *                              FFN (Eq.9, P189-193), draft bi-directional layer (Eq.10,
+ *                              P195-204), shared frozen LM head + argmax (reading C8).
+ *   specformer_verify_step  "Multi-token verification: ... evaluates all draft tokens
+ *                            simultaneously ... while also extracting and storing information
+ *                            for the next round" = one base-decoder forward over
+ *                            [last_token, d_1..d_k] that keeps the hook taps HS[0], HS[L/2],
+ *                            HS[L-1], HS[L] (P175) of those k+1 rows in the workspace.
+ *   specformer_accept_commit "Multi-token acceptance ... accordingly updates the contextual
+ *                            information" = lossless greedy accept (P25: "only draft tokens
+ *                            that exactly match the outputs of the large model") + KV commit;
+ *                            rollback moves no data (rejected rows lie beyond seq_len).
+ *
+ * Conventions (DESIGN.md §3 lists every reading of the paper):
+ *  - Tokens are int32. Matrices are row-major [out, in]; y = x W^T.
+ *  - Pointers named *_dev are device pointers; pointers documented "dev or host" may be device
+ *    memory or pinned host memory (they are moved with cudaMemcpyAsync(..., cudaMemcpyDefault)).
+ *  - Ownership: the caller allocates ALL device memory (packed weights, workspace, I/O). The
+ *    library never calls cudaMalloc/cudaFree on caller memory; it owns only host state and
+ *    CUDA graph objects. Weights and workspace must outlive the handle.
+ *  - All calls are asynchronous on the handle's stream; outputs are valid after the stream
+ *    (or specformer_sync) completes. One host thread per handle.
+ *  - Errors: argument / shape / state / capacity errors return synchronously and leave the
+ *    handle unchanged. Device-detected errors (non-finite logits) are sticky flags surfaced by
+ *    specformer_sync as SF_ERR_NONFINITE. specformer_last_error() describes the last failure.
+ *  - There is no CPU fallback: every step runs in this library's sm_100a kernels.
+ */
+#ifndef SPECFORMER_H_
+#define SPECFORMER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SF_OK = 0,
+  SF_ERR_ARG = 1,        /* bad argument value (e.g. eps <= 0, d % heads != 0, NULL handle) */
+  SF_ERR_SHAPE = 2,      /* dimension mismatch (batch > max_batch, bad prompt length ...)    */
+  SF_ERR_CAPACITY = 3,   /* seq_len + k + 1 would exceed max_seq                             */
+  SF_ERR_STATE = 4,      /* call order violated: init -> prefill -> (draft -> verify -> accept)* */
+  SF_ERR_CUDA = 5,       /* a CUDA runtime call failed                                       */
+  SF_ERR_NCCL = 6,       /* reserved (tensor-parallel path)                                  */
+  SF_ERR_NONFINITE = 7,  /* NaN/Inf met in logits (SPEC S26: an error condition)             */
+  SF_ERR_UNSUPPORTED = 8 /* configuration not supported by this build                        */
+} sf_status;
+
+typedef enum { SF_FP32 = 0, SF_BF16 = 1 } sf_dtype;
+
+/* flags */
+#define SF_FLAG_CUDA_GRAPH  (1ull << 0) /* capture draft+verify+accept as one CUDA graph for decode_steps */
+#define SF_FLAG_DRAFT_CAUSAL (1ull << 1) /* NEXT-2 ablation "+Att Mask": causal draft-slot mask (not default) */
+
+typedef struct {
+  int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab;
+  int32_t draft_len;   /* k = l_d (chain draft, no tree; PAPER P6, P37). 0 = plain greedy AR
+                          decoding through verify_step + accept_commit (no draft head), used by
+                          the GPU SD == AR losslessness test.                               */
+  int32_t max_batch;   /* B_max sequences handled by this handle                          */
+  int32_t max_seq;     /* per-sequence KV capacity (positions), multiple of kv_block      */
+  int32_t kv_block;    /* paged-KV page size in tokens; must be 16                        */
+  float rope_theta;    /* 10000 (reading C5)                                               */
+  float rms_eps;       /* 1e-6 (reading C3)                                                */
+  int32_t dtype;       /* sf_dtype: SF_FP32 (fp32 weights/activations/KV, SIMT kernels) or
+                          SF_BF16 (bf16 weights/KV, tcgen05 GEMMs, fp32 residual/accum)     */
+  int32_t tp_size, tp_rank; /* must be 1, 0 in this build                                  */
+  uint64_t flags;
+} sf_config;
+
+typedef struct {
+  char name[64];
+  int32_t ndim;
+  int64_t shape[4];
+  int64_t offset_bytes; /* from the start of the packed weight blob (256-byte aligned) */
+  int32_t dtype;        /* sf_dtype of the stored elements                              */
+} sf_tensor_desc;
+
+typedef struct sf_handle sf_handle;
+
+/* Packed weight layout. Returns the number of tensors (writes at most `cap` descriptors;
+ * out may be NULL to query the count), or -1 on an invalid config.
+ * Names: embed[V,d]; layers.<l>.{attn_norm[d] f32, wqkv[(Hq+2Hkv)hd, d] (rows q|k|v),
+ * wo[d, Hq hd], ffn_norm[d] f32, w_gu[2F,d], w_down[d,F]}; final_norm[d] f32;
+ * lm_head[V,d]; sf.group_scale[4,d] f32; sf.w_d[d,4d]; sf.ctx_norm[d] f32; sf.ctx_wqkv;
+ * sf.ctx_wo; sf.pos_norm[d] f32; sf.w_p[k d, d]; sf.b_p[k d] f32; sf.blk_attn_norm[d] f32;
+ * sf.blk_wqkv; sf.blk_wo; sf.blk_ffn_norm[d] f32; sf.blk_w_gu[2F,d]; sf.blk_w_down[d,F].
+ * w_gu interleaves the SwiGLU gate and up projections in 64-row groups: rows [128i, 128i+64)
+ * are gate rows [64i, 64i+64) and rows [128i+64, 128i+128) are up rows [64i, 64i+64)
+ * (F % 64 == 0), so one GEMM tile holds matching gate/up rows for the fused SwiGLU epilogue.
+ * Matrices are stored in the config dtype, vectors in fp32. */
+int sf_weight_table(const sf_config* cfg, sf_tensor_desc* out, int cap);
+int64_t sf_weights_bytes(const sf_config* cfg);   /* -1 on invalid config */
+int64_t sf_workspace_bytes(const sf_config* cfg); /* KV pools (L+1 layers) + activations; -1 if invalid */
+
+/* Validates cfg, carves `workspace_dev` (sf_workspace_bytes, 256-byte aligned), binds the
+ * weight pointers. `stream` is a cudaStream_t (NULL = legacy default stream). */
+sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspace_dev, void* stream,
+                          sf_handle** out);
+
+/* Setup pass (untimed): base forward over the B x P prompt tokens (dev or host, [B,P] row-major)
+ * in chunks, context layer L+1 over all P rows; first_token (dev or host, [B], may be NULL)
+ * receives g0 = argmax logits[P-1]. Afterwards seq_len = P, last_token = g0. */
+sf_status specformer_prefill(sf_handle* h, const int32_t* tokens, int32_t B, int32_t P, int32_t* first_token);
+
+/* SpecFormer draft forward. draft (dev or host [B,k], may be NULL), draft_logits (dev [B,k,V]
+ * fp32, may be NULL). The draft is also kept internally for verify_step. */
+sf_status specformer_draft_step(sf_handle* h, int32_t* draft, float* draft_logits);
+
+/* Base verify forward over [last_token, d_1..d_k] at positions seq_len..seq_len+k.
+ * draft_in: dev or host [B,k] to verify instead of the internal draft (forced/adversarial
+ * drafts), or NULL. greedy (dev or host [B,k+1]) and logits (dev [B,k+1,V] fp32) may be NULL. */
+sf_status specformer_verify_step(sf_handle* h, const int32_t* draft_in, int32_t* greedy, float* logits);
+
+/* Greedy accept + commit: m_b = longest prefix with draft[b,i] == greedy[b,i];
+ * emitted[b, 0..m_b] = greedy[b, 0..m_b] (rest -1); seq_len += m_b + 1; last_token = greedy[b,m_b].
+ * Outputs (dev or host, may be NULL): accept_len [B], emitted [B,k+1], seq_len [B]. */
+sf_status specformer_accept_commit(sf_handle* h, int32_t* accept_len, int32_t* emitted, int32_t* seq_len);
+
+/* Run n_steps x (draft -> verify -> accept) with no host synchronisation (CUDA-graph replay
+ * when SF_FLAG_CUDA_GRAPH). emitted_log (dev, [n_steps, B, k+1]) and accept_log (dev,
+ * [n_steps, B]) may be NULL. Fails with SF_ERR_CAPACITY if a step could overflow max_seq. */
+sf_status specformer_decode_steps(sf_handle* h, int32_t n_steps, int32_t* emitted_log, int32_t* accept_log);
+
+/* Stream sync + sticky device error flags -> status. */
+sf_status specformer_sync(sf_handle* h);
+const char* specformer_last_error(const sf_handle* h);
+void specformer_destroy(sf_handle* h);
+
+/* Number of kernels launched by the last call (host-side count; graph replays count their nodes). */
+int64_t specformer_kernel_launches(const sf_handle* h);
+/* Name of the library build ("sm_100a ...") for provenance. */
+const char* specformer_build_info(void);
+
+/* ------------------------------------------------------------------ test / bench hooks */
+/* Replace the page table (host [B, max_seq/kv_block] of distinct page ids < B*max_seq/kv_block).
+ * Only valid right after init (before prefill). */
+sf_status sf_debug_set_block_table(sf_handle* h, const int32_t* table_host, int32_t B, int32_t n_pages_per_seq);
+/* Copy an internal buffer to dst (dev or host). what: 0 taps [4, B(k+1), d] f32 of the last
+ * verify; 1 I_D rows used by the last draft [B, d] f32; 2 E (draft block output) [B, k, d] f32;
+ * 3 seq_len [B] i32; 4 last_token [B] i32; 5 n_prev [B] i32 (length before the last commit). Returns bytes copied via *nbytes. */
+sf_status sf_debug_capture(sf_handle* h, int32_t what, void* dst, int64_t* nbytes);
+/* Forced-acceptance drafts: overwrite the internal draft with
+ * cont[b, g + j] (j = 1..k, g = seq_len - prompt_len, cont = AR continuation with cont[b,0] = g0)
+ * and replace slot corrupt[b] (1..k; > k means none) with (token + 1) % V. Device pointers. */
+sf_status sf_debug_force_drafts(sf_handle* h, const int32_t* cont_dev, int32_t cont_len, const int32_t* corrupt_dev);
+/* Bench hook: make decode_steps overwrite each step's draft (after the draft forward ran and was
+ * paid for) with forced drafts as in sf_debug_force_drafts, slot corrupt_dev[(step % corrupt_steps) * B + b].
+ * cont_dev NULL disables. Device pointers must stay valid while enabled. */
+sf_status sf_set_forced_drafts(sf_handle* h, const int32_t* cont_dev, int32_t cont_len, const int32_t* corrupt_dev,
+                               int32_t corrupt_steps);
+/* Per-kernel-class profiling for the bench roofline: when enabled, every eager launch is bracketed
+ * by CUDA events on the handle's stream (decode_steps then runs eagerly, not from a graph).
+ * Classes: 0 GEMM, 1 paged attention (RoPE/append + partial + combine), 2 RMSNorm/embedding,
+ * 3 argmax. sf_profile(h, 1) clears and enables; sf_profile_read sums the elapsed milliseconds,
+ * launch count and host-known algorithmic bytes (GEMM: weights + activations + outputs; 0 for
+ * attention, whose KV bytes depend on device-resident lengths) of one class. */
+sf_status sf_profile(sf_handle* h, int32_t enable);
+sf_status sf_profile_read(sf_handle* h, int32_t cls, double* total_ms, int64_t* count, double* bytes);
+/* Direct GEMM entry (T-kernel parity): out[T,N] = A[T,K] W[N,K]^T in the config dtype with
+ * fp32 accumulation; A, W dev in dtype; out dev fp32. Uses the same kernels as the hot path. */
+sf_status sf_test_gemm(int32_t dtype, const void* A, const void* W, float* out, int32_t T, int32_t N, int32_t K,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECFORMER_H_ */

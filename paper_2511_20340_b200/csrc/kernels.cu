@@ -1,0 +1,619 @@
+// kernels.cu -- element-wise, normalisation, RoPE/paged-KV append, hybrid-mask attention and
+// accept kernels of the SpecFormer decode step. Every reduction uses a fixed order that depends
+// only on the row's own data and position (batch invariance, reading C23), so GPU SD == GPU AR
+// bit for bit.
+#include <cfloat>
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sf {
+
+// ------------------------------------------------------------------------ RoPE table
+// cos/sin(pos * theta^(-2i/hd)) evaluated in double, stored fp32 (reading C5).
+__global__ void rope_table_kernel(float2* tab, int max_seq, int hd, float theta) {
+  const int half = hd / 2;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= max_seq * half) return;
+  const int pos = idx / half, i = idx % half;
+  const double inv = pow((double)theta, -2.0 * i / hd);
+  double s, c;
+  sincos((double)pos * inv, &s, &c);
+  tab[idx] = make_float2((float)c, (float)s);
+}
+
+// ------------------------------------------------------------------------ row builders
+__global__ void build_verify_rows_kernel(int B, int k, const int* last_token, const int* draft, int* tok) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= B * (k + 1)) return;
+  const int b = r / (k + 1), i = r % (k + 1);
+  tok[r] = (i == 0) ? last_token[b] : draft[b * k + i - 1];
+}
+__global__ void build_prefill_rows_kernel(int B, int P, int c0, int C, const int* tokens, int* tok, int* pos0) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < B) pos0[r] = c0;
+  if (r >= B * C) return;
+  const int b = r / C, i = r % C;
+  tok[r] = tokens[(size_t)b * P + c0 + i];
+}
+
+// ------------------------------------------------------------------------ embedding (HS[0])
+template <typename TW>
+__global__ void embed_kernel(const int* tok, const TW* emb, int d, int vocab, float* resid, float* tap0) {
+  const int t = blockIdx.x;
+  int id = tok[t];
+  id = min(max(id, 0), vocab - 1);
+  const TW* src = emb + (size_t)id * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float v = Elt<TW>::to_f(src[i]);
+    resid[(size_t)t * d + i] = v;
+    if (tap0) tap0[(size_t)t * d + i] = v;
+  }
+}
+
+// ------------------------------------------------------------------------ RMSNorm
+// y = x / sqrt(mean(x^2) + eps) * g, fp32 statistics, one CTA (256 threads) per row.
+template <typename TO>
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* in, int in_ld, const float* g, float eps, int d,
+                                                      TO* out, int out_ld) {
+  __shared__ float red[8];
+  const int t = blockIdx.x;
+  const float* x = in + (size_t)t * in_ld;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += 256) ss = fmaf(x[i], x[i], ss);
+  ss = block_sum<256>(ss, red);
+  const float r = 1.0f / sqrtf(ss / (float)d + eps);
+  TO* y = out + (size_t)t * out_ld;
+  for (int i = threadIdx.x; i < d; i += 256) y[i] = Elt<TO>::from_f(x[i] * r * g[i]);
+}
+
+// Grouped RMS Norm + concat (Eq.8 I_Cat; the paper's Triton kernel KP1, P330-332):
+// out[t, g*d + i] = taps[g][t][i] / rms_g * s[g][i]
+template <typename TO>
+__global__ void __launch_bounds__(256) group_rms_kernel(const float* taps, int64_t tap_stride, const float* sc,
+                                                        float eps, int d, TO* out) {
+  __shared__ float red[8];
+  const int t = blockIdx.x;
+  for (int g = 0; g < 4; ++g) {
+    const float* x = taps + g * tap_stride + (size_t)t * d;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < d; i += 256) ss = fmaf(x[i], x[i], ss);
+    ss = block_sum<256>(ss, red);
+    const float r = 1.0f / sqrtf(ss / (float)d + eps);
+    TO* y = out + (size_t)t * 4 * d + (size_t)g * d;
+    for (int i = threadIdx.x; i < d; i += 256) y[i] = Elt<TO>::from_f(x[i] * r * sc[g * d + i]);
+  }
+}
+
+// ------------------------------------------------------------------------ RoPE + paged KV append
+// qkv row = [q (Hq*hd) | k (Hkv*hd) | v (Hkv*hd)]. Queries rotated -> q_out fp32;
+// keys rotated and values copied into the sequence's pages at their absolute positions.
+template <typename TA>
+__global__ void rope_append_kernel(const TA* qkv, int q_len, const int* pos0, const float2* rope, int Hq, int Hkv,
+                                   int hd, const int* bt, int pps, TA* Kp, TA* Vp, float* q_out) {
+  const int t = blockIdx.x;
+  const int b = t / q_len, qi = t % q_len;
+  const int pos = pos0[b] + qi;
+  const int half = hd / 2;
+  const int W = (Hq + 2 * Hkv) * hd;
+  const TA* row = qkv + (size_t)t * W;
+  const int blk = bt[b * pps + pos / 16], slot = pos % 16;
+  const float2* cs = rope + (size_t)pos * half;
+  for (int e = threadIdx.x; e < (Hq + Hkv) * half; e += blockDim.x) {
+    const int h = e / half, i = e % half;
+    const float2 c = cs[i];
+    const float x1 = Elt<TA>::to_f(row[h * hd + i]);
+    const float x2 = Elt<TA>::to_f(row[h * hd + i + half]);
+    const float y1 = x1 * c.x - x2 * c.y;
+    const float y2 = x2 * c.x + x1 * c.y;
+    if (h < Hq) {
+      q_out[((size_t)t * Hq + h) * hd + i] = y1;
+      q_out[((size_t)t * Hq + h) * hd + i + half] = y2;
+    } else {
+      const int kh = h - Hq;
+      TA* dst = Kp + (((size_t)blk * Hkv + kh) * 16 + slot) * hd;
+      dst[i] = Elt<TA>::from_f(y1);
+      dst[i + half] = Elt<TA>::from_f(y2);
+    }
+  }
+  for (int e = threadIdx.x; e < Hkv * hd; e += blockDim.x) {
+    const int kh = e / hd, i = e % hd;
+    Vp[(((size_t)blk * Hkv + kh) * 16 + slot) * hd + i] = row[(Hq + Hkv) * hd + e];
+  }
+}
+
+// ------------------------------------------------------------------------ paged attention
+// Hybrid-mask decode attention, mode CAUSAL_PREFIX: query row i of sequence b (absolute position
+// p = pos0[b] + i) attends keys 0..p of its pages. Split-KV over FIXED absolute 128-key chunks:
+// CTA (chunk c, kv head, query tile, b) writes an unnormalised partial (m, l, acc); the combine
+// kernel merges chunks in order c = 0, 1, ... . Shared-memory staged K/V via 16-byte cp.async.
+constexpr int QT = 16;  // query rows per CTA
+
+SF_DEV void cp_async16(void* smem, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
+}
+SF_DEV void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+template <typename TKV, int HD>
+__global__ void __launch_bounds__(128) attn_partial_kernel(AttnParams p) {
+  constexpr int VEC = 16 / sizeof(TKV);     // elements per 16-byte vector
+  constexpr int KLD = HD + VEC;             // padded K row (bank-conflict-free per-key reads)
+  extern __shared__ __align__(16) uint8_t sm[];
+  TKV* Ks = reinterpret_cast<TKV*>(sm);
+  TKV* Vs = Ks + kAttnChunk * KLD;
+  float* Qs = reinterpret_cast<float*>(Vs + kAttnChunk * HD);
+  float* S = Qs + QT * HD;
+
+  const int c = blockIdx.x, b = blockIdx.z;
+  const int G = p.Hq / p.Hkv;
+  const int ntiles = (p.q_len * G + QT - 1) / QT;
+  const int kvh = blockIdx.y / ntiles, qt = blockIdx.y % ntiles;
+  const int R = p.q_len * G;
+  const int r0 = qt * QT;
+  const int nr = min(QT, R - r0);
+  const int base = p.pos0[b];
+  const int kstart = c * kAttnChunk;
+  const int kmax = base + min(p.q_len - 1, (r0 + nr - 1) / G);  // largest position among this tile's rows
+  if (kstart > kmax) return;
+  const int nk = min(kAttnChunk, kmax + 1 - kstart);
+  const int tid = threadIdx.x;
+
+  // stage K, V chunk
+  const TKV* Kg = reinterpret_cast<const TKV*>(p.Kp);
+  const TKV* Vg = reinterpret_cast<const TKV*>(p.Vp);
+  for (int e = tid; e < nk * (HD / VEC); e += 128) {
+    const int j = e / (HD / VEC), part = e % (HD / VEC);
+    const int key = kstart + j;
+    const int blk = p.block_table[b * p.pages_per_seq + key / 16];
+    const size_t off = (((size_t)blk * p.Hkv + kvh) * 16 + (key % 16)) * HD + part * VEC;
+    cp_async16(Ks + j * KLD + part * VEC, Kg + off);
+    cp_async16(Vs + j * HD + part * VEC, Vg + off);
+  }
+  // queries
+  for (int e = tid; e < nr * HD; e += 128) {
+    const int r = e / HD, dd = e % HD;
+    const int rr = r0 + r, qi = rr / G, h = kvh * G + rr % G;
+    const int t = b * p.q_len + qi;
+    Qs[r * HD + dd] = p.q[((size_t)t * p.Hq + h) * HD + dd];
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  const float scale = rsqrtf((float)HD);
+  // ---- scores: thread <-> key
+  {
+    const int j = tid;
+    float acc[QT];
+#pragma unroll
+    for (int r = 0; r < QT; ++r) acc[r] = 0.f;
+    if (j < nk) {
+#pragma unroll 4
+      for (int d0 = 0; d0 < HD; d0 += VEC) {
+        float kv[VEC];
+        if constexpr (sizeof(TKV) == 2) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(Ks + j * KLD + d0);
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float2 f = __bfloat1622float2(h2[u]);
+            kv[2 * u] = f.x;
+            kv[2 * u + 1] = f.y;
+          }
+        } else {
+          const float4 raw = *reinterpret_cast<const float4*>(Ks + j * KLD + d0);
+          kv[0] = raw.x; kv[1] = raw.y; kv[2] = raw.z; kv[3] = raw.w;
+        }
+#pragma unroll
+        for (int r = 0; r < QT; ++r) {
+          if (r < nr) {
+#pragma unroll
+            for (int u = 0; u < VEC; ++u) acc[r] = fmaf(Qs[r * HD + d0 + u], kv[u], acc[r]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < QT; ++r) {
+      if (r < nr) {
+        const int pos = base + (r0 + r) / G;
+        const bool vis = (j < nk) && (kstart + j <= pos);
+        S[r * kAttnChunk + j] = vis ? acc[r] * scale : -INFINITY;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- chunk softmax (unnormalised): warp per row
+  const int warp = tid >> 5, lane = tid & 31;
+  float* ML = S + QT * kAttnChunk;
+  for (int r = warp; r < nr; r += 4) {
+    float v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = S[r * kAttnChunk + lane + 32 * i];
+    float mx = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+    mx = warp_max(mx);
+    float l = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float e = (mx == -INFINITY || v[i] == -INFINITY) ? 0.f : expf(v[i] - mx);
+      S[r * kAttnChunk + lane + 32 * i] = e;
+      l += e;
+    }
+    l = warp_sum(l);
+    if (lane == 0) {
+      ML[2 * r] = mx;
+      ML[2 * r + 1] = l;
+    }
+  }
+  __syncthreads();
+  // ---- P V: thread <-> (dim, row group)
+  {
+    constexpr int RG = 128 / HD;
+    const int dd = tid % HD, rg = tid / HD;
+    float acc[QT / RG > 0 ? QT / RG : 1];
+#pragma unroll
+    for (int i = 0; i < QT / RG; ++i) acc[i] = 0.f;
+    for (int j = 0; j < nk; ++j) {
+      const float v = Elt<TKV>::to_f(Vs[j * HD + dd]);
+#pragma unroll
+      for (int i = 0; i < QT / RG; ++i) {
+        const int r = rg + i * RG;
+        if (r < nr) acc[i] = fmaf(S[r * kAttnChunk + j], v, acc[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < QT / RG; ++i) {
+      const int r = rg + i * RG;
+      if (r < nr) {
+        const int rr = r0 + r, qi = rr / G, h = kvh * G + rr % G;
+        const int t = b * p.q_len + qi;
+        const size_t o = ((size_t)t * p.Hq + h) * p.nchunk_max + c;
+        p.part_o[o * HD + dd] = acc[i];
+        if (dd == 0) {
+          p.part_ml[2 * o] = ML[2 * r];
+          p.part_ml[2 * o + 1] = ML[2 * r + 1];
+        }
+      }
+    }
+  }
+}
+
+// combine chunks 0..pos/128 in order: M = max m_c; out = sum_c acc_c e^(m_c - M) / sum_c l_c e^(m_c - M)
+template <typename TA>
+__global__ void attn_combine_kernel(AttnParams p) {
+  const int t = blockIdx.x, h = blockIdx.y;
+  const int b = t / p.q_len, qi = t % p.q_len;
+  const int pos = p.pos0[b] + qi;
+  const int nc = pos / kAttnChunk + 1;
+  const size_t o0 = ((size_t)t * p.Hq + h) * p.nchunk_max;
+  float M = -INFINITY;
+  for (int c = 0; c < nc; ++c) M = fmaxf(M, p.part_ml[2 * (o0 + c)]);
+  float L = 0.f;
+  for (int c = 0; c < nc; ++c) L += p.part_ml[2 * (o0 + c) + 1] * expf(p.part_ml[2 * (o0 + c)] - M);
+  for (int dd = threadIdx.x; dd < p.hd; dd += blockDim.x) {
+    float acc = 0.f;
+    for (int c = 0; c < nc; ++c) acc += p.part_o[(o0 + c) * p.hd + dd] * expf(p.part_ml[2 * (o0 + c)] - M);
+    reinterpret_cast<TA*>(p.out)[((size_t)t * p.Hq + h) * p.hd + dd] = Elt<TA>::from_f(acc / L);
+  }
+}
+
+// ------------------------------------------------------------------------ draft bidirectional SA
+// Eq.10 / P204: self-attention along the k draft slots of one context row, unmasked
+// (BIDIR_LOCAL), no RoPE; effective batch B. One CTA per (b, head).
+template <typename TA>
+__global__ void bidir_attn_kernel(const TA* qkv, int k, int Hq, int Hkv, int hd, int causal, TA* out) {
+  extern __shared__ float fs[];
+  const int b = blockIdx.x, h = blockIdx.y;
+  const int G = Hq / Hkv, kh = h / G;
+  const int W = (Hq + 2 * Hkv) * hd;
+  float* q = fs;
+  float* kk = q + k * hd;
+  float* vv = kk + k * hd;
+  float* s = vv + k * hd;  // [k][k]
+  for (int e = threadIdx.x; e < k * hd; e += blockDim.x) {
+    const int i = e / hd, dd = e % hd;
+    const TA* row = qkv + (size_t)(b * k + i) * W;
+    q[e] = Elt<TA>::to_f(row[h * hd + dd]);
+    kk[e] = Elt<TA>::to_f(row[(Hq + kh) * hd + dd]);
+    vv[e] = Elt<TA>::to_f(row[(Hq + Hkv + kh) * hd + dd]);
+  }
+  __syncthreads();
+  const float scale = rsqrtf((float)hd);
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int i = e / k, j = e % k;
+    float a = 0.f;
+    for (int dd = 0; dd < hd; ++dd) a = fmaf(q[i * hd + dd], kk[j * hd + dd], a);
+    s[e] = (causal && j > i) ? -INFINITY : a * scale;
+  }
+  __syncthreads();
+  if (threadIdx.x < k) {
+    const int i = threadIdx.x;
+    float mx = -INFINITY;
+    for (int j = 0; j < k; ++j) mx = fmaxf(mx, s[i * k + j]);
+    float l = 0.f;
+    for (int j = 0; j < k; ++j) {
+      const float e = (s[i * k + j] == -INFINITY) ? 0.f : expf(s[i * k + j] - mx);
+      s[i * k + j] = e;
+      l += e;
+    }
+    for (int j = 0; j < k; ++j) s[i * k + j] /= l;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * hd; e += blockDim.x) {
+    const int i = e / hd, dd = e % hd;
+    float a = 0.f;
+    for (int j = 0; j < k; ++j) a = fmaf(s[i * k + j], vv[j * hd + dd], a);
+    out[(size_t)(b * k + i) * Hq * hd + h * hd + dd] = Elt<TA>::from_f(a);
+  }
+}
+
+// ------------------------------------------------------------------------ gather
+__global__ void gather_rows_kernel(const float* src, int q_len, const int* idx, int const_idx, int d, float* dst) {
+  const int b = blockIdx.x;
+  const int r = idx ? idx[b] : const_idx;
+  const float* s = src + ((size_t)b * q_len + r) * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) dst[(size_t)b * d + i] = s[i];
+}
+
+// ------------------------------------------------------------------------ argmax (lowest id on ties)
+constexpr int kArgmaxSlice = 2048;
+int argmax_splits(int V) { return (V + kArgmaxSlice - 1) / kArgmaxSlice; }
+
+SF_DEV void better(float& bv, int& bi, float v, int i) {
+  if (v > bv || (v == bv && i < bi)) {
+    bv = v;
+    bi = i;
+  }
+}
+__global__ void __launch_bounds__(256) argmax_partial_kernel(const float* logits, int V, int nsplit, float* pval,
+                                                             int* pidx, int* err) {
+  __shared__ float sv[8];
+  __shared__ int si[8];
+  const int row = blockIdx.y, sp = blockIdx.x;
+  const int lo = sp * kArgmaxSlice, hi = min(V, lo + kArgmaxSlice);
+  const float* x = logits + (size_t)row * V;
+  float bv = -INFINITY;
+  int bi = INT_MAX;
+  bool bad = false;
+  for (int i = lo + threadIdx.x; i < hi; i += 256) {
+    const float v = x[i];
+    if (!isfinite(v)) bad = true;
+    better(bv, bi, v, i);
+  }
+  if (bad) atomicOr(err, 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    better(bv, bi, ov, oi);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sv[w] = bv;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 1; j < 8; ++j) better(bv, bi, sv[j], si[j]);
+    pval[row * nsplit + sp] = bv;
+    pidx[row * nsplit + sp] = bi;
+  }
+}
+__global__ void argmax_final_kernel(const float* pval, const int* pidx, int R, int nsplit, int* out) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= R) return;
+  float bv = -INFINITY;
+  int bi = INT_MAX;
+  for (int s = 0; s < nsplit; ++s) better(bv, bi, pval[row * nsplit + s], pidx[row * nsplit + s]);
+  out[row] = (bi == INT_MAX) ? 0 : bi;
+}
+
+// ------------------------------------------------------------------------ accept + commit
+// P25: accept only drafts equal to the base model's greedy outputs. Single CTA (B <= 1024).
+__global__ void accept_kernel(int B, int k, const int* draft, const int* greedy, int* seq_len, int* n_prev,
+                              int* last_token, int* r_b, int* accept_len, int* emitted, int* step_counter,
+                              int* accept_log, int* emitted_log, int log_cap) {
+  const int b = threadIdx.x;
+  const int step = step_counter ? *step_counter : 0;
+  if (b < B) {
+    const int* g = greedy + b * (k + 1);
+    int m = 0;
+    while (m < k && draft[b * k + m] == g[m]) ++m;
+    for (int i = 0; i <= k; ++i) {
+      const int e = (i <= m) ? g[i] : -1;
+      emitted[b * (k + 1) + i] = e;
+      if (emitted_log && step < log_cap) emitted_log[((size_t)step * B + b) * (k + 1) + i] = e;
+    }
+    accept_len[b] = m;
+    if (accept_log && step < log_cap) accept_log[(size_t)step * B + b] = m;
+    n_prev[b] = seq_len[b];
+    seq_len[b] += m + 1;
+    last_token[b] = g[m];
+    r_b[b] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && step_counter) *step_counter = step + 1;
+}
+
+__global__ void force_drafts_kernel(int B, int k, int V, const int* cont, int cont_len, const int* corrupt,
+                                    int corrupt_steps, const int* seq_len, const int* prompt_len,
+                                    const int* step_counter, int* draft) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int gidx = seq_len[b] - prompt_len[b];
+  const int step = step_counter ? *step_counter : 0;
+  const int cs = corrupt ? corrupt[(size_t)(step % corrupt_steps) * B + b] : k + 1;
+  for (int j = 1; j <= k; ++j) {
+    const int ci = min(gidx + j, cont_len - 1);
+    int tok = cont[(size_t)b * cont_len + ci];
+    if (j == cs) tok = (tok + 1) % V;
+    draft[b * k + j - 1] = tok;
+  }
+}
+
+__global__ void fill_kernel(int* p, int n, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void prefill_finish_kernel(int B, int P, const int* greedy, int* seq_len, int* n_prev, int* last_token,
+                                      int* r_b, int* prompt_len, int* first_out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  seq_len[b] = P;
+  n_prev[b] = P;
+  last_token[b] = greedy[b];
+  r_b[b] = 0;
+  prompt_len[b] = P;
+  if (first_out) first_out[b] = greedy[b];
+}
+
+// ======================================================================== launchers
+#define SF_GRID(n, t) (((n) + (t)-1) / (t))
+
+cudaError_t launch_rope_table(float2* table, int max_seq, int hd, float theta, cudaStream_t s) {
+  const int n = max_seq * hd / 2;
+  rope_table_kernel<<<SF_GRID(n, 256), 256, 0, s>>>(table, max_seq, hd, theta);
+  return cudaGetLastError();
+}
+cudaError_t launch_build_verify_rows(int B, int k, const int* last_token, const int* draft, int* tok_rows,
+                                     cudaStream_t s) {
+  build_verify_rows_kernel<<<SF_GRID(B * (k + 1), 128), 128, 0, s>>>(B, k, last_token, draft, tok_rows);
+  return cudaGetLastError();
+}
+cudaError_t launch_build_prefill_rows(int B, int P, int c0, int C, const int* tokens, int* tok_rows, int* pos0,
+                                      cudaStream_t s) {
+  build_prefill_rows_kernel<<<SF_GRID(max(B * C, B), 128), 128, 0, s>>>(B, P, c0, C, tokens, tok_rows, pos0);
+  return cudaGetLastError();
+}
+cudaError_t launch_embed(bool bf, const int* tok, const void* embed, int T, int d, int vocab, float* resid,
+                         float* tap0, cudaStream_t s) {
+  if (bf)
+    embed_kernel<__nv_bfloat16><<<T, 256, 0, s>>>(tok, (const __nv_bfloat16*)embed, d, vocab, resid, tap0);
+  else
+    embed_kernel<float><<<T, 256, 0, s>>>(tok, (const float*)embed, d, vocab, resid, tap0);
+  return cudaGetLastError();
+}
+cudaError_t launch_rmsnorm(bool bf, const float* in, int in_ld, const float* gamma, float eps, int T, int d,
+                           void* out, int out_ld, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  if (bf)
+    rmsnorm_kernel<__nv_bfloat16><<<T, 256, 0, s>>>(in, in_ld, gamma, eps, d, (__nv_bfloat16*)out, out_ld);
+  else
+    rmsnorm_kernel<float><<<T, 256, 0, s>>>(in, in_ld, gamma, eps, d, (float*)out, out_ld);
+  return cudaGetLastError();
+}
+cudaError_t launch_group_rms(bool bf, const float* taps, int64_t tap_stride, const float* scales, float eps, int T,
+                             int d, void* out, cudaStream_t s) {
+  if (bf)
+    group_rms_kernel<__nv_bfloat16><<<T, 256, 0, s>>>(taps, tap_stride, scales, eps, d, (__nv_bfloat16*)out);
+  else
+    group_rms_kernel<float><<<T, 256, 0, s>>>(taps, tap_stride, scales, eps, d, (float*)out);
+  return cudaGetLastError();
+}
+cudaError_t launch_rope_append(bool bf, const void* qkv, int T, int q_len, const int* pos0, const float2* rope,
+                               int Hq, int Hkv, int hd, const int* bt, int pps, void* Kp, void* Vp, float* q_out,
+                               cudaStream_t s) {
+  if (bf)
+    rope_append_kernel<__nv_bfloat16><<<T, 256, 0, s>>>((const __nv_bfloat16*)qkv, q_len, pos0, rope, Hq, Hkv, hd,
+                                                         bt, pps, (__nv_bfloat16*)Kp, (__nv_bfloat16*)Vp, q_out);
+  else
+    rope_append_kernel<float><<<T, 256, 0, s>>>((const float*)qkv, q_len, pos0, rope, Hq, Hkv, hd, bt, pps,
+                                                 (float*)Kp, (float*)Vp, q_out);
+  return cudaGetLastError();
+}
+
+template <typename TKV, int HD>
+static cudaError_t attn_impl(const AttnParams& p, cudaStream_t s) {
+  constexpr int VEC = 16 / sizeof(TKV);
+  const size_t smem = (size_t)kAttnChunk * (HD + VEC) * sizeof(TKV) + (size_t)kAttnChunk * HD * sizeof(TKV) +
+                      (size_t)QT * HD * 4 + (size_t)QT * kAttnChunk * 4 + QT * 2 * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_partial_kernel<TKV, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const int G = p.Hq / p.Hkv;
+  const int ntiles = (p.q_len * G + QT - 1) / QT;
+  const int nch = (p.max_key + kAttnChunk - 1) / kAttnChunk;
+  dim3 grid(nch, p.Hkv * ntiles, p.B);
+  attn_partial_kernel<TKV, HD><<<grid, 128, smem, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 g2(p.B * p.q_len, p.Hq);
+  if (sizeof(TKV) == 2)
+    attn_combine_kernel<__nv_bfloat16><<<g2, min(HD, 128), 0, s>>>(p);
+  else
+    attn_combine_kernel<float><<<g2, min(HD, 128), 0, s>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t launch_attention(bool bf, const AttnParams& p, cudaStream_t s) {
+  if (bf) {
+    switch (p.hd) {
+      case 64: return attn_impl<__nv_bfloat16, 64>(p, s);
+      case 128: return attn_impl<__nv_bfloat16, 128>(p, s);
+      case 16: return attn_impl<__nv_bfloat16, 16>(p, s);
+    }
+  } else {
+    switch (p.hd) {
+      case 16: return attn_impl<float, 16>(p, s);
+      case 64: return attn_impl<float, 64>(p, s);
+      case 128: return attn_impl<float, 128>(p, s);
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+cudaError_t launch_bidir_attention(bool bf, const void* qkv, int B, int k, int Hq, int Hkv, int hd, bool causal,
+                                   void* out, cudaStream_t s) {
+  dim3 grid(B, Hq);
+  const size_t smem = (size_t)(3 * k * hd + k * k) * 4;
+  if (bf)
+    bidir_attn_kernel<__nv_bfloat16><<<grid, 128, smem, s>>>((const __nv_bfloat16*)qkv, k, Hq, Hkv, hd, causal,
+                                                            (__nv_bfloat16*)out);
+  else
+    bidir_attn_kernel<float><<<grid, 128, smem, s>>>((const float*)qkv, k, Hq, Hkv, hd, causal, (float*)out);
+  return cudaGetLastError();
+}
+cudaError_t launch_gather_rows(const float* src, int q_len, const int* idx, int const_idx, int B, int d, float* dst,
+                               cudaStream_t s) {
+  gather_rows_kernel<<<B, 256, 0, s>>>(src, q_len, idx, const_idx, d, dst);
+  return cudaGetLastError();
+}
+cudaError_t launch_argmax(const float* logits, int R, int V, float* pval, int* pidx, int* out, int* err,
+                          cudaStream_t s) {
+  const int ns = argmax_splits(V);
+  dim3 grid(ns, R);
+  argmax_partial_kernel<<<grid, 256, 0, s>>>(logits, V, ns, pval, pidx, err);
+  argmax_final_kernel<<<SF_GRID(R, 128), 128, 0, s>>>(pval, pidx, R, ns, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_accept(int B, int k, const int* draft, const int* greedy, int* seq_len, int* n_prev,
+                          int* last_token, int* r_b, int* accept_len, int* emitted, int* step_counter,
+                          int* accept_log, int* emitted_log, int log_cap, cudaStream_t s) {
+  const int th = ((B + 31) / 32) * 32;
+  accept_kernel<<<1, th, 0, s>>>(B, k, draft, greedy, seq_len, n_prev, last_token, r_b, accept_len, emitted,
+                                 step_counter, accept_log, emitted_log, log_cap);
+  return cudaGetLastError();
+}
+cudaError_t launch_force_drafts(int B, int k, int V, const int* cont, int cont_len, const int* corrupt,
+                                int corrupt_steps, const int* seq_len, const int* prompt_len,
+                                const int* step_counter, int* draft, cudaStream_t s) {
+  force_drafts_kernel<<<SF_GRID(B, 128), 128, 0, s>>>(B, k, V, cont, cont_len, corrupt, corrupt_steps, seq_len,
+                                                      prompt_len, step_counter, draft);
+  return cudaGetLastError();
+}
+cudaError_t launch_fill(int* p, int n, int v, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  fill_kernel<<<SF_GRID(n, 256), 256, 0, s>>>(p, n, v);
+  return cudaGetLastError();
+}
+cudaError_t launch_prefill_finish(int B, int P, const int* greedy, int* seq_len, int* n_prev, int* last_token,
+                                  int* r_b, int* prompt_len, int* first_out, cudaStream_t s) {
+  prefill_finish_kernel<<<SF_GRID(B, 128), 128, 0, s>>>(B, P, greedy, seq_len, n_prev, last_token, r_b,
+                                                         prompt_len, first_out);
+  return cudaGetLastError();
+}
+
+}  // namespace sf

@@ -1,0 +1,60 @@
+// kernels.cuh -- launchers for the non-GEMM kernels of the hot path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sf {
+
+struct AttnParams {
+  const float* q;            // [T, Hq, hd] rotated queries (fp32)
+  const void* Kp;            // paged K pool of one layer: [n_pages, Hkv, 16, hd]
+  const void* Vp;            // paged V pool
+  const int* block_table;    // [B, pages_per_seq]
+  int pages_per_seq;
+  const int* pos0;           // [B] absolute position of each sequence's first query row
+  int q_len;                 // query rows per sequence (rows b*q_len + i at pos0[b] + i)
+  int B, Hq, Hkv, hd;
+  int nchunk_max;            // partial-buffer capacity in 128-key chunks
+  float* part_o;             // [T, Hq, nchunk_max, hd]
+  float* part_ml;            // [T, Hq, nchunk_max, 2]
+  void* out;                 // [T, Hq*hd] act dtype
+  int max_key;               // upper bound of pos0[b] + q_len (grid sizing), <= max_seq
+};
+
+constexpr int kAttnChunk = 128;  // fixed absolute key-chunk size (split-KV boundaries, C23)
+
+// act dtype: bf16 (is_bf16) or fp32.
+cudaError_t launch_rope_table(float2* table, int max_seq, int hd, float theta, cudaStream_t s);
+cudaError_t launch_build_verify_rows(int B, int k, const int* last_token, const int* draft, int* tok_rows,
+                                     cudaStream_t s);
+cudaError_t launch_build_prefill_rows(int B, int P, int c0, int C, const int* tokens, int* tok_rows, int* pos0,
+                                      cudaStream_t s);
+cudaError_t launch_embed(bool is_bf16, const int* tok, const void* embed, int T, int d, int vocab, float* resid,
+                         float* tap0, cudaStream_t s);
+cudaError_t launch_rmsnorm(bool is_bf16, const float* in, int in_ld, const float* gamma, float eps, int T, int d,
+                           void* out, int out_ld, cudaStream_t s);
+cudaError_t launch_group_rms(bool is_bf16, const float* taps, int64_t tap_stride, const float* scales, float eps,
+                             int T, int d, void* out, cudaStream_t s);
+cudaError_t launch_rope_append(bool is_bf16, const void* qkv, int T, int q_len, const int* pos0,
+                               const float2* rope, int Hq, int Hkv, int hd, const int* block_table,
+                               int pages_per_seq, void* Kp, void* Vp, float* q_out, cudaStream_t s);
+cudaError_t launch_attention(bool is_bf16, const AttnParams& p, cudaStream_t s);
+cudaError_t launch_bidir_attention(bool is_bf16, const void* qkv, int B, int k, int Hq, int Hkv, int hd,
+                                   bool causal, void* out, cudaStream_t s);
+cudaError_t launch_gather_rows(const float* src, int q_len, const int* idx, int const_idx, int B, int d,
+                               float* dst, cudaStream_t s);
+cudaError_t launch_argmax(const float* logits, int R, int V, float* pval, int* pidx, int* out, int* err,
+                          cudaStream_t s);
+cudaError_t launch_accept(int B, int k, const int* draft, const int* greedy, int* seq_len, int* n_prev,
+                          int* last_token, int* r_b, int* accept_len, int* emitted, int* step_counter,
+                          int* accept_log, int* emitted_log, int log_cap, cudaStream_t s);
+cudaError_t launch_force_drafts(int B, int k, int V, const int* cont, int cont_len, const int* corrupt,
+                                int corrupt_steps, const int* seq_len, const int* prompt_len,
+                                const int* step_counter, int* draft, cudaStream_t s);
+cudaError_t launch_fill(int* p, int n, int v, cudaStream_t s);
+cudaError_t launch_prefill_finish(int B, int P, const int* greedy, int* seq_len, int* n_prev, int* last_token,
+                                  int* r_b, int* prompt_len, int* first_out, cudaStream_t s);
+
+int argmax_splits(int V);
+
+}  // namespace sf

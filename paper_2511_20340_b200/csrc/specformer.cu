@@ -1,0 +1,956 @@
+// specformer.cu -- runtime behind the C ABI (include/specformer.h): config validation, packed
+// weight table, workspace carving, the per-step launch sequences (draft / verify / accept), the
+// chunked prefill, CUDA-graph capture of the decode step and the test hooks.
+//
+// Step structure (PAPER P20-23):
+//   draft_step  : [context layer L+1 over the previous verify's k+1 rows (Eq.8) -> gather row
+//                  r_b] -> positional FFN (Eq.9) -> draft bidirectional layer (Eq.10) -> final
+//                  norm + LM head (shared, C8) -> argmax -> k draft tokens
+//   verify_step : base forward over [last, d_1..d_k] (taps HS[0, L/2, L-1, L] kept) -> LM head
+//                  -> argmax -> greedy[k+1]
+//   accept      : m = longest matching prefix, commit seq_len += m + 1 (rollback moves no data)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/specformer.h"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+using namespace sf;
+
+namespace {
+
+constexpr int64_t kAlign = 256;
+inline int64_t align_up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct TensorSpec {
+  std::string name;
+  std::vector<int64_t> shape;
+  bool matrix;  // stored in config dtype (else fp32)
+};
+
+bool valid_config(const sf_config* c, std::string* why) {
+  auto fail = [&](const char* m) {
+    if (why) *why = m;
+    return false;
+  };
+  if (!c) return fail("null config");
+  if (c->n_layers < 1 || c->d_model < 1 || c->n_heads < 1 || c->n_kv_heads < 1 || c->head_dim < 2 ||
+      c->d_ff < 1 || c->vocab < 2)
+    return fail("nonpositive dimension");
+  if (c->n_heads % c->n_kv_heads) return fail("n_heads % n_kv_heads != 0");
+  if (c->head_dim != 16 && c->head_dim != 64 && c->head_dim != 128) return fail("head_dim must be 16, 64 or 128");
+  if (c->draft_len < 0 || c->draft_len > 16) return fail("draft_len must be in [0, 16]");
+  if (c->max_batch < 1 || c->max_batch > 1024) return fail("max_batch must be in [1, 1024]");
+  if (c->kv_block != 16) return fail("kv_block must be 16");
+  if (c->max_seq < 16 || c->max_seq % 16) return fail("max_seq must be a positive multiple of 16");
+  if (!(c->rms_eps > 0.f)) return fail("rms_eps must be > 0");
+  if (!(c->rope_theta > 0.f)) return fail("rope_theta must be > 0");
+  if (c->dtype != SF_FP32 && c->dtype != SF_BF16) return fail("dtype must be SF_FP32 or SF_BF16");
+  if (c->tp_size != 1 || c->tp_rank != 0) return fail("tensor parallelism not supported in this build");
+  if (c->d_ff % 64) return fail("d_ff must be a multiple of 64 (interleaved gate/up groups)");
+  if (c->dtype == SF_BF16) {
+    const int qkv = (c->n_heads + 2 * c->n_kv_heads) * c->head_dim;
+    if (c->d_model % 128 || qkv % 128 || (2 * c->d_ff) % 128 || c->vocab % 128 ||
+        (c->n_heads * c->head_dim) % 64 || c->d_ff % 64)
+      return fail("bf16 path needs d, qkv width, 2F, V multiples of 128 and K multiples of 64");
+  }
+  return true;
+}
+
+std::vector<TensorSpec> tensor_specs(const sf_config* c) {
+  const int64_t d = c->d_model, F = c->d_ff, V = c->vocab, k = c->draft_len;
+  const int64_t qkv = (int64_t)(c->n_heads + 2 * c->n_kv_heads) * c->head_dim, ao = (int64_t)c->n_heads * c->head_dim;
+  std::vector<TensorSpec> t;
+  t.push_back({"embed", {V, d}, true});
+  for (int l = 0; l < c->n_layers; ++l) {
+    const std::string p = "layers." + std::to_string(l) + ".";
+    t.push_back({p + "attn_norm", {d}, false});
+    t.push_back({p + "wqkv", {qkv, d}, true});
+    t.push_back({p + "wo", {d, ao}, true});
+    t.push_back({p + "ffn_norm", {d}, false});
+    t.push_back({p + "w_gu", {2 * F, d}, true});
+    t.push_back({p + "w_down", {d, F}, true});
+  }
+  t.push_back({"final_norm", {d}, false});
+  t.push_back({"lm_head", {V, d}, true});
+  if (k > 0) {
+    t.push_back({"sf.group_scale", {4, d}, false});
+    t.push_back({"sf.w_d", {d, 4 * d}, true});
+    t.push_back({"sf.ctx_norm", {d}, false});
+    t.push_back({"sf.ctx_wqkv", {qkv, d}, true});
+    t.push_back({"sf.ctx_wo", {d, ao}, true});
+    t.push_back({"sf.pos_norm", {d}, false});
+    t.push_back({"sf.w_p", {k * d, d}, true});
+    t.push_back({"sf.b_p", {k * d}, false});
+    t.push_back({"sf.blk_attn_norm", {d}, false});
+    t.push_back({"sf.blk_wqkv", {qkv, d}, true});
+    t.push_back({"sf.blk_wo", {d, ao}, true});
+    t.push_back({"sf.blk_ffn_norm", {d}, false});
+    t.push_back({"sf.blk_w_gu", {2 * F, d}, true});
+    t.push_back({"sf.blk_w_down", {d, F}, true});
+  }
+  return t;
+}
+
+int64_t tensor_bytes(const sf_config* c, const TensorSpec& s) {
+  int64_t n = 1;
+  for (auto v : s.shape) n *= v;
+  return n * ((s.matrix && c->dtype == SF_BF16) ? 2 : 4);
+}
+
+// ----------------------------------------------------------------- workspace plan
+struct Plan {
+  int B, k, d, Hq, Hkv, hd, F, V, L, qkvw, ao;
+  int pps, n_pages, nchunk, rows_v, rows_d, C_pf, rows_pf, R;
+  int64_t act, kv_layer_bytes;
+  // offsets
+  int64_t o_k, o_v, o_bt, o_rope, o_resid, o_xn, o_qkv, o_qrot, o_attn, o_ffn, o_taps, o_ctx, o_idrow, o_D,
+      o_hlast, o_logits, o_dlogits, o_apo, o_apml, o_gpart, o_gcnt, o_amv, o_ami, o_ints, o_prompt;
+  int64_t gpart_elems, n_amrows;
+  int64_t total;
+};
+
+Plan make_plan(const sf_config* c) {
+  Plan p{};
+  p.B = c->max_batch;
+  p.k = c->draft_len;
+  p.d = c->d_model;
+  p.Hq = c->n_heads;
+  p.Hkv = c->n_kv_heads;
+  p.hd = c->head_dim;
+  p.F = c->d_ff;
+  p.V = c->vocab;
+  p.L = c->n_layers;
+  p.qkvw = (p.Hq + 2 * p.Hkv) * p.hd;
+  p.ao = p.Hq * p.hd;
+  p.act = c->dtype == SF_BF16 ? 2 : 4;
+  p.pps = c->max_seq / 16;
+  p.n_pages = p.B * p.pps;
+  p.nchunk = (c->max_seq + kAttnChunk - 1) / kAttnChunk;
+  p.rows_v = p.B * (p.k + 1);
+  p.rows_d = std::max(1, p.B * p.k);
+  p.C_pf = std::max(p.k + 1, std::min(64, std::max(1, 512 / p.B)));
+  p.rows_pf = p.B * p.C_pf;
+  p.R = std::max(p.rows_v, p.rows_pf);
+  p.kv_layer_bytes = (int64_t)p.n_pages * p.Hkv * 16 * p.hd * p.act;
+  // split-K partial scratch: worst case over every GEMM shape at R rows
+  const bool bf = c->dtype == SF_BF16;
+  const int shapes[][2] = {{p.qkvw, p.d}, {p.d, p.ao}, {2 * p.F, p.d}, {p.d, p.F}, {p.V, p.d},
+                           {p.d, 4 * p.d}, {std::max(1, p.k) * p.d, p.d}};
+  p.gpart_elems = 0;
+  for (auto& s : shapes) p.gpart_elems = std::max<int64_t>(p.gpart_elems, gemm_partial_elems(bf, std::min(p.R, 512), s[0], s[1]));
+  p.n_amrows = std::max(p.rows_v, std::max(p.rows_d, p.B));
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t r = o;
+    o += align_up(std::max<int64_t>(bytes, 1));
+    return r;
+  };
+  p.o_k = take(p.kv_layer_bytes * (p.L + 1));
+  p.o_v = take(p.kv_layer_bytes * (p.L + 1));
+  p.o_bt = take((int64_t)p.n_pages * 4);
+  p.o_rope = take((int64_t)c->max_seq * (p.hd / 2) * 8);
+  p.o_resid = take((int64_t)p.R * p.d * 4);
+  p.o_xn = take((int64_t)p.R * 4 * p.d * p.act);
+  p.o_qkv = take((int64_t)p.R * p.qkvw * p.act);
+  p.o_qrot = take((int64_t)p.R * p.ao * 4);
+  p.o_attn = take((int64_t)p.R * p.ao * p.act);
+  p.o_ffn = take((int64_t)p.R * p.F * p.act);
+  p.o_taps = take((int64_t)4 * p.R * p.d * 4);
+  p.o_ctx = take((int64_t)p.R * p.d * 4);
+  p.o_idrow = take((int64_t)p.B * p.d * 4);
+  p.o_D = take((int64_t)p.rows_d * p.d * 4);
+  p.o_hlast = take((int64_t)p.B * p.d * 4);
+  p.o_logits = take((int64_t)p.rows_v * p.V * 4);
+  p.o_dlogits = take((int64_t)p.rows_d * p.V * 4);
+  p.o_apo = take((int64_t)p.R * p.Hq * p.nchunk * p.hd * 4);
+  p.o_apml = take((int64_t)p.R * p.Hq * p.nchunk * 2 * 4);
+  p.o_gpart = take(p.gpart_elems * 4);
+  p.o_gcnt = take(4096 * 4);
+  p.o_amv = take(p.n_amrows * argmax_splits(p.V) * 4);
+  p.o_ami = take(p.n_amrows * argmax_splits(p.V) * 4);
+  p.o_ints = take((int64_t)(16 * p.B + 2 * p.R + 8 + p.rows_v * 2 + p.rows_d) * 4);
+  p.o_prompt = take((int64_t)p.B * c->max_seq * 4);
+  p.total = o;
+  return p;
+}
+
+enum State { ST_INIT = 0, ST_READY = 1, ST_DRAFTED = 2, ST_VERIFIED = 3 };
+
+}  // namespace
+
+struct sf_handle {
+  sf_config c{};
+  Plan p{};
+  bool bf = false;
+  cudaStream_t st = nullptr;
+  char* W = nullptr;
+  char* ws = nullptr;
+  // weights
+  struct Lw {
+    const float *attn_norm, *ffn_norm;
+    const void *wqkv, *wo, *wgu, *wdown;
+  };
+  std::vector<Lw> lw;
+  const void *embed = nullptr, *lm_head = nullptr;
+  const float* final_norm = nullptr;
+  const float *group_scale = nullptr, *ctx_norm = nullptr, *pos_norm = nullptr, *b_p = nullptr,
+              *blk_attn_norm = nullptr, *blk_ffn_norm = nullptr;
+  const void *w_d = nullptr, *ctx_wqkv = nullptr, *ctx_wo = nullptr, *w_p = nullptr, *blk_wqkv = nullptr,
+             *blk_wo = nullptr, *blk_wgu = nullptr, *blk_wdown = nullptr;
+  // workspace views
+  char *kpool = nullptr, *vpool = nullptr;
+  int* bt = nullptr;
+  float2* rope = nullptr;
+  float *resid, *qrot, *taps, *ctx, *idrow, *D, *hlast, *logits, *dlogits, *apo, *apml, *gpart, *amv;
+  void *xn, *qkv, *attn, *ffn;
+  int *gcnt, *ami;
+  int *tok_rows, *pos0_pf, *seq_len, *n_prev, *last_token, *r_b, *prompt_len, *draft, *greedy, *accept_len,
+      *emitted, *err, *step_counter, *g_pf, *prompt;
+  // state
+  int B = 0;
+  int state = ST_INIT;
+  bool ctx_pending = false;
+  int64_t launches = 0;
+  int64_t host_len_hi = 0;  // host upper bound of max(seq_len)
+  std::string err_msg;
+  // graph
+  cudaGraphExec_t gexec = nullptr;
+  int64_t graph_launches = 0;
+  int *g_acc_log = nullptr, *g_em_log = nullptr;
+  int g_log_cap = 0;
+  // per-kernel-class profiling (eager launches only; bench roofline)
+  struct Prof {
+    int cls;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  bool prof_on = false;
+  std::vector<Prof> prof;
+  std::vector<cudaEvent_t> ev_free;
+  cudaEvent_t ev_get() {
+    if (ev_free.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = ev_free.back();
+    ev_free.pop_back();
+    return e;
+  }
+  // forced drafts (bench)
+  const int *f_cont = nullptr, *f_corrupt = nullptr;
+  int f_cont_len = 0, f_corrupt_steps = 0;
+  bool forced = false;
+
+  void* kp(int layer) { return kpool + (size_t)layer * p.kv_layer_bytes; }
+  void* vp(int layer) { return vpool + (size_t)layer * p.kv_layer_bytes; }
+};
+
+// ----------------------------------------------------------------- helpers
+#define SF_TRY(expr)                                              \
+  do {                                                            \
+    cudaError_t e__ = (expr);                                     \
+    if (e__ != cudaSuccess) {                                     \
+      h->err_msg = std::string(#expr) + ": " + cudaGetErrorString(e__); \
+      return SF_ERR_CUDA;                                         \
+    }                                                             \
+  } while (0)
+
+static sf_status set_err(sf_handle* h, sf_status s, const std::string& m) {
+  if (h) h->err_msg = m;
+  return s;
+}
+
+// Kernel classes for sf_profile_read: 0 GEMM (tcgen05 / SIMT), 1 paged attention (RoPE+append,
+// partial, combine), 2 norms / embedding / gathers, 3 argmax + accept + draft attention + misc.
+struct ProfScope {
+  sf_handle* h;
+  size_t idx = (size_t)-1;
+  ProfScope(sf_handle* hh, int cls, double bytes) : h(hh) {
+    if (!h->prof_on) return;
+    sf_handle::Prof r{cls, h->ev_get(), h->ev_get(), bytes};
+    cudaEventRecord(r.a, h->st);
+    h->prof.push_back(r);
+    idx = h->prof.size() - 1;
+  }
+  ~ProfScope() {
+    if (idx != (size_t)-1) cudaEventRecord(h->prof[idx].b, h->st);
+  }
+};
+
+static cudaError_t gemm(sf_handle* h, const void* A, int lda, const void* W, int T, int N, int K, GemmEpi epi) {
+  const double wb = h->bf ? 2.0 : 4.0;
+  const double ob = (epi.mode == EPI_STORE_ACT || epi.mode == EPI_SWIGLU_ACT) ? wb : 4.0;
+  const double outc = epi.mode == EPI_SWIGLU_ACT ? N / 2 : N;
+  // algorithmic bytes: weight once + activation once + output once (+ residual read for ADD)
+  ProfScope ps(h, 0, (double)N * K * wb + (double)T * K * wb + (double)T * outc * ob * (epi.mode == EPI_ADD_F32 ? 2 : 1));
+  GemmScratch sc;
+  sc.partial = h->gpart;
+  sc.partial_elems = h->p.gpart_elems;
+  sc.counters = h->gcnt;
+  sc.n_counters = 4096;
+  h->launches += (T + 511) / 512;
+  return gemm_launch(h->bf, A, lda, W, T, N, K, epi, sc, h->st);
+}
+static GemmEpi epi_act(void* out, int ldo) {
+  GemmEpi e;
+  e.mode = EPI_STORE_ACT;
+  e.out = out;
+  e.ldo = ldo;
+  return e;
+}
+static GemmEpi epi_f32(void* out, int ldo) {
+  GemmEpi e;
+  e.mode = EPI_STORE_F32;
+  e.out = out;
+  e.ldo = ldo;
+  return e;
+}
+static GemmEpi epi_add(float* out, int ldo, float* tap) {
+  GemmEpi e;
+  e.mode = EPI_ADD_F32;
+  e.out = out;
+  e.ldo = ldo;
+  e.tap = tap;
+  return e;
+}
+
+static cudaError_t rmsnorm(sf_handle* h, const float* in, int in_ld, const float* g, int T, void* out, int out_ld) {
+  ProfScope ps(h, 2, (double)T * h->p.d * (4.0 + (h->bf ? 2.0 : 4.0)));
+  h->launches++;
+  return launch_rmsnorm(h->bf, in, in_ld, g, h->c.rms_eps, T, h->p.d, out, out_ld, h->st);
+}
+
+static const int* taps_layers(int L, int* out4) {
+  out4[0] = 0;
+  out4[1] = L / 2;
+  out4[2] = L - 1;
+  out4[3] = L;
+  return out4;
+}
+
+// One attention sub-layer's "RoPE + append + attention" for rows (T, q_len, pos0) of layer `layer`.
+static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const int* pos0, int max_key) {
+  const Plan& p = h->p;
+  ProfScope ps(h, 1, 0.0);  // KV bytes depend on device-resident lengths: the bench computes them
+  cudaError_t e = launch_rope_append(h->bf, h->qkv, T, q_len, pos0, h->rope, p.Hq, p.Hkv, p.hd, h->bt, p.pps,
+                                     h->kp(layer), h->vp(layer), h->qrot, h->st);
+  if (e != cudaSuccess) return e;
+  AttnParams ap{};
+  ap.q = h->qrot;
+  ap.Kp = h->kp(layer);
+  ap.Vp = h->vp(layer);
+  ap.block_table = h->bt;
+  ap.pages_per_seq = p.pps;
+  ap.pos0 = pos0;
+  ap.q_len = q_len;
+  ap.B = T / q_len;
+  ap.Hq = p.Hq;
+  ap.Hkv = p.Hkv;
+  ap.hd = p.hd;
+  ap.nchunk_max = p.nchunk;
+  ap.part_o = h->apo;
+  ap.part_ml = h->apml;
+  ap.out = h->attn;
+  ap.max_key = std::min(max_key, h->c.max_seq);
+  h->launches += 3;
+  return launch_attention(h->bf, ap, h->st);
+}
+
+// Base decoder forward over T rows (q_len per sequence, positions pos0[b] + i); writes resid and
+// the 4 hook taps (P175) into h->taps.
+static cudaError_t base_forward(sf_handle* h, int T, int q_len, const int* pos0, int max_key) {
+  const Plan& p = h->p;
+  const int64_t tstride = (int64_t)p.R * p.d;
+  int tl[4];
+  taps_layers(p.L, tl);
+  cudaError_t e = launch_embed(h->bf, h->tok_rows, h->embed, T, p.d, p.V, h->resid, h->taps, h->st);
+  h->launches++;
+  if (e != cudaSuccess) return e;
+  for (int g = 1; g < 4; ++g)
+    if (tl[g] == 0) cudaMemcpyAsync(h->taps + g * tstride, h->taps, (size_t)T * p.d * 4, cudaMemcpyDeviceToDevice, h->st);
+  for (int l = 0; l < p.L; ++l) {
+    const auto& w = h->lw[l];
+    if ((e = rmsnorm(h, h->resid, p.d, w.attn_norm, T, h->xn, p.d))) return e;
+    if ((e = gemm(h, h->xn, p.d, w.wqkv, T, p.qkvw, p.d, epi_act(h->qkv, p.qkvw)))) return e;
+    if ((e = attn_layer(h, l, T, q_len, pos0, max_key))) return e;
+    if ((e = gemm(h, h->attn, p.ao, w.wo, T, p.d, p.ao, epi_add(h->resid, p.d, nullptr)))) return e;
+    if ((e = rmsnorm(h, h->resid, p.d, w.ffn_norm, T, h->xn, p.d))) return e;
+    GemmEpi sw;
+    sw.mode = EPI_SWIGLU_ACT;
+    sw.out = h->ffn;
+    sw.ldo = p.F;
+    if ((e = gemm(h, h->xn, p.d, w.wgu, T, 2 * p.F, p.d, sw))) return e;
+    // residual add; the first tap slot that equals HS[l+1] is written by the epilogue
+    int first = -1;
+    for (int g = 0; g < 4; ++g)
+      if (tl[g] == l + 1 && first < 0) first = g;
+    float* tap = first >= 0 ? h->taps + first * tstride : nullptr;
+    if ((e = gemm(h, h->ffn, p.F, w.wdown, T, p.d, p.F, epi_add(h->resid, p.d, tap)))) return e;
+    for (int g = first + 1; first >= 0 && g < 4; ++g)
+      if (tl[g] == l + 1)
+        cudaMemcpyAsync(h->taps + g * tstride, tap, (size_t)T * p.d * 4, cudaMemcpyDeviceToDevice, h->st);
+  }
+  return cudaSuccess;
+}
+
+// SpecFormer context layer L+1 (Eq.8) over T rows of taps -> h->ctx (= I_D rows).
+static cudaError_t ctx_forward(sf_handle* h, int T, int q_len, const int* pos0, int max_key) {
+  const Plan& p = h->p;
+  cudaError_t e;
+  if ((e = launch_group_rms(h->bf, h->taps, (int64_t)p.R * p.d, h->group_scale, h->c.rms_eps, T, p.d, h->xn, h->st)))
+    return e;
+  h->launches++;
+  if ((e = gemm(h, h->xn, 4 * p.d, h->w_d, T, p.d, 4 * p.d, epi_f32(h->ctx, p.d)))) return e;
+  if ((e = rmsnorm(h, h->ctx, p.d, h->ctx_norm, T, h->xn, p.d))) return e;
+  if ((e = gemm(h, h->xn, p.d, h->ctx_wqkv, T, p.qkvw, p.d, epi_act(h->qkv, p.qkvw)))) return e;
+  if ((e = attn_layer(h, p.L, T, q_len, pos0, max_key))) return e;
+  return gemm(h, h->attn, p.ao, h->ctx_wo, T, p.d, p.ao, epi_add(h->ctx, p.d, nullptr));
+}
+
+// final norm + LM head + argmax over T rows of `src` (f32 [T, d])
+static cudaError_t head_argmax(sf_handle* h, const float* src, int T, float* logits, int* out) {
+  const Plan& p = h->p;
+  cudaError_t e;
+  if ((e = rmsnorm(h, src, p.d, h->final_norm, T, h->xn, p.d))) return e;
+  if ((e = gemm(h, h->xn, p.d, h->lm_head, T, p.V, p.d, epi_f32(logits, p.V)))) return e;
+  h->launches += 2;
+  ProfScope ps(h, 3, (double)T * p.V * 4.0);
+  return launch_argmax(logits, T, p.V, h->amv, h->ami, out, h->err, h->st);
+}
+
+static cudaError_t do_draft(sf_handle* h) {
+  const Plan& p = h->p;
+  const int B = h->B, k = p.k;
+  cudaError_t e;
+  if (h->ctx_pending) {
+    if ((e = ctx_forward(h, B * (k + 1), k + 1, h->n_prev, h->c.max_seq))) return e;
+    if ((e = launch_gather_rows(h->ctx, k + 1, h->r_b, 0, B, p.d, h->idrow, h->st))) return e;
+    h->launches++;
+    h->ctx_pending = false;
+  }
+  // positional FFN (Eq.9): D = W_P RMS(I_D) + b_P  -> [B, k*d] == [B*k, d]
+  if ((e = rmsnorm(h, h->idrow, p.d, h->pos_norm, B, h->xn, p.d))) return e;
+  GemmEpi eb;
+  eb.mode = EPI_BIAS_F32;
+  eb.out = h->D;
+  eb.ldo = k * p.d;
+  eb.bias = h->b_p;
+  if ((e = gemm(h, h->xn, p.d, h->w_p, B, k * p.d, p.d, eb))) return e;
+  // draft bidirectional layer (Eq.10)
+  const int Tk = B * k;
+  if ((e = rmsnorm(h, h->D, p.d, h->blk_attn_norm, Tk, h->xn, p.d))) return e;
+  if ((e = gemm(h, h->xn, p.d, h->blk_wqkv, Tk, p.qkvw, p.d, epi_act(h->qkv, p.qkvw)))) return e;
+  if ((e = launch_bidir_attention(h->bf, h->qkv, B, k, p.Hq, p.Hkv, p.hd, (h->c.flags & SF_FLAG_DRAFT_CAUSAL) != 0,
+                                  h->attn, h->st)))
+    return e;
+  h->launches++;
+  if ((e = gemm(h, h->attn, p.ao, h->blk_wo, Tk, p.d, p.ao, epi_add(h->D, p.d, nullptr)))) return e;
+  if ((e = rmsnorm(h, h->D, p.d, h->blk_ffn_norm, Tk, h->xn, p.d))) return e;
+  GemmEpi sw;
+  sw.mode = EPI_SWIGLU_ACT;
+  sw.out = h->ffn;
+  sw.ldo = p.F;
+  if ((e = gemm(h, h->xn, p.d, h->blk_wgu, Tk, 2 * p.F, p.d, sw))) return e;
+  if ((e = gemm(h, h->ffn, p.F, h->blk_wdown, Tk, p.d, p.F, epi_add(h->D, p.d, nullptr)))) return e;
+  // shared frozen final norm + LM head (C8) -> k draft tokens
+  return head_argmax(h, h->D, Tk, h->dlogits, h->draft);
+}
+
+static cudaError_t do_verify(sf_handle* h) {
+  const Plan& p = h->p;
+  const int B = h->B, k = p.k;
+  const int T = B * (k + 1);
+  cudaError_t e;
+  if ((e = launch_build_verify_rows(B, k, h->last_token, h->draft, h->tok_rows, h->st))) return e;
+  h->launches++;
+  if ((e = base_forward(h, T, k + 1, h->seq_len, h->c.max_seq))) return e;
+  return head_argmax(h, h->resid, T, h->logits, h->greedy);
+}
+
+static cudaError_t do_accept(sf_handle* h, int* acc_log, int* em_log, int log_cap) {
+  const Plan& p = h->p;
+  h->launches++;
+  cudaError_t e = launch_accept(h->B, p.k, h->draft, h->greedy, h->seq_len, h->n_prev, h->last_token, h->r_b,
+                                h->accept_len, h->emitted, h->step_counter, acc_log, em_log, log_cap, h->st);
+  if (p.k > 0) h->ctx_pending = true;
+  return e;
+}
+
+static cudaError_t copy_out(sf_handle* h, void* dst, const void* src, size_t bytes) {
+  if (!dst) return cudaSuccess;
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->st);
+}
+
+// ================================================================= C ABI
+extern "C" {
+
+int sf_weight_table(const sf_config* cfg, sf_tensor_desc* out, int cap) {
+  if (!valid_config(cfg, nullptr)) return -1;
+  auto specs = tensor_specs(cfg);
+  int64_t off = 0;
+  for (size_t i = 0; i < specs.size(); ++i) {
+    if (out && (int)i < cap) {
+      sf_tensor_desc& d = out[i];
+      memset(&d, 0, sizeof(d));
+      strncpy(d.name, specs[i].name.c_str(), sizeof(d.name) - 1);
+      d.ndim = (int32_t)specs[i].shape.size();
+      for (int j = 0; j < d.ndim; ++j) d.shape[j] = specs[i].shape[j];
+      d.offset_bytes = off;
+      d.dtype = (specs[i].matrix && cfg->dtype == SF_BF16) ? SF_BF16 : SF_FP32;
+    }
+    off += align_up(tensor_bytes(cfg, specs[i]));
+  }
+  return (int)specs.size();
+}
+
+int64_t sf_weights_bytes(const sf_config* cfg) {
+  if (!valid_config(cfg, nullptr)) return -1;
+  int64_t off = 0;
+  for (auto& s : tensor_specs(cfg)) off += align_up(tensor_bytes(cfg, s));
+  return off;
+}
+
+int64_t sf_workspace_bytes(const sf_config* cfg) {
+  if (!valid_config(cfg, nullptr)) return -1;
+  return make_plan(cfg).total;
+}
+
+const char* specformer_build_info(void) {
+  return "specformer sm_100a (tcgen05/TMA bf16 GEMM, SIMT fp32 mode), built " __DATE__ " " __TIME__;
+}
+
+sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspace_dev, void* stream,
+                          sf_handle** out) {
+  if (!out) return SF_ERR_ARG;
+  *out = nullptr;
+  std::string why;
+  if (!valid_config(cfg, &why)) return SF_ERR_ARG;
+  if (!weights_dev || !workspace_dev) return SF_ERR_ARG;
+  if (((uintptr_t)weights_dev | (uintptr_t)workspace_dev) % kAlign) return SF_ERR_ARG;
+  auto* h = new sf_handle();
+  h->c = *cfg;
+  h->p = make_plan(cfg);
+  h->bf = cfg->dtype == SF_BF16;
+  h->st = (cudaStream_t)stream;
+  h->W = (char*)weights_dev;
+  h->ws = (char*)workspace_dev;
+  // bind weights
+  auto specs = tensor_specs(cfg);
+  int64_t off = 0;
+  std::vector<std::pair<std::string, char*>> ptrs;
+  for (auto& s : specs) {
+    ptrs.push_back({s.name, h->W + off});
+    off += align_up(tensor_bytes(cfg, s));
+  }
+  auto get = [&](const std::string& n) -> char* {
+    for (auto& pr : ptrs)
+      if (pr.first == n) return pr.second;
+    return nullptr;
+  };
+  h->lw.resize(cfg->n_layers);
+  for (int l = 0; l < cfg->n_layers; ++l) {
+    const std::string p = "layers." + std::to_string(l) + ".";
+    h->lw[l].attn_norm = (const float*)get(p + "attn_norm");
+    h->lw[l].ffn_norm = (const float*)get(p + "ffn_norm");
+    h->lw[l].wqkv = get(p + "wqkv");
+    h->lw[l].wo = get(p + "wo");
+    h->lw[l].wgu = get(p + "w_gu");
+    h->lw[l].wdown = get(p + "w_down");
+  }
+  h->embed = get("embed");
+  h->final_norm = (const float*)get("final_norm");
+  h->lm_head = get("lm_head");
+  if (cfg->draft_len > 0) {
+    h->group_scale = (const float*)get("sf.group_scale");
+    h->w_d = get("sf.w_d");
+    h->ctx_norm = (const float*)get("sf.ctx_norm");
+    h->ctx_wqkv = get("sf.ctx_wqkv");
+    h->ctx_wo = get("sf.ctx_wo");
+    h->pos_norm = (const float*)get("sf.pos_norm");
+    h->w_p = get("sf.w_p");
+    h->b_p = (const float*)get("sf.b_p");
+    h->blk_attn_norm = (const float*)get("sf.blk_attn_norm");
+    h->blk_wqkv = get("sf.blk_wqkv");
+    h->blk_wo = get("sf.blk_wo");
+    h->blk_ffn_norm = (const float*)get("sf.blk_ffn_norm");
+    h->blk_wgu = get("sf.blk_w_gu");
+    h->blk_wdown = get("sf.blk_w_down");
+  }
+  // carve workspace
+  const Plan& p = h->p;
+  char* w = h->ws;
+  h->kpool = w + p.o_k;
+  h->vpool = w + p.o_v;
+  h->bt = (int*)(w + p.o_bt);
+  h->rope = (float2*)(w + p.o_rope);
+  h->resid = (float*)(w + p.o_resid);
+  h->xn = w + p.o_xn;
+  h->qkv = w + p.o_qkv;
+  h->qrot = (float*)(w + p.o_qrot);
+  h->attn = w + p.o_attn;
+  h->ffn = w + p.o_ffn;
+  h->taps = (float*)(w + p.o_taps);
+  h->ctx = (float*)(w + p.o_ctx);
+  h->idrow = (float*)(w + p.o_idrow);
+  h->D = (float*)(w + p.o_D);
+  h->hlast = (float*)(w + p.o_hlast);
+  h->logits = (float*)(w + p.o_logits);
+  h->dlogits = (float*)(w + p.o_dlogits);
+  h->apo = (float*)(w + p.o_apo);
+  h->apml = (float*)(w + p.o_apml);
+  h->gpart = (float*)(w + p.o_gpart);
+  h->gcnt = (int*)(w + p.o_gcnt);
+  h->amv = (float*)(w + p.o_amv);
+  h->ami = (int*)(w + p.o_ami);
+  int* ip = (int*)(w + p.o_ints);
+  auto ints = [&](int n) {
+    int* r = ip;
+    ip += n;
+    return r;
+  };
+  h->tok_rows = ints(p.R);
+  h->pos0_pf = ints(p.B);
+  h->seq_len = ints(p.B);
+  h->n_prev = ints(p.B);
+  h->last_token = ints(p.B);
+  h->r_b = ints(p.B);
+  h->prompt_len = ints(p.B);
+  h->draft = ints(p.rows_d);
+  h->greedy = ints(p.rows_v);
+  h->accept_len = ints(p.B);
+  h->emitted = ints(p.rows_v);
+  h->err = ints(1);
+  h->step_counter = ints(1);
+  h->g_pf = ints(p.B);
+  h->prompt = (int*)(w + p.o_prompt);
+  cudaError_t e = cudaSuccess;
+  // page table: identity (sequence b owns pages [b*pps, (b+1)*pps)); tests may permute it
+  std::vector<int> bt(p.n_pages);
+  for (int i = 0; i < p.n_pages; ++i) bt[i] = i;
+  e = cudaMemcpyAsync(h->bt, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice, h->st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->gcnt, 0, 4096 * 4, h->st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->ws + p.o_ints, 0, (16 * p.B + 2 * p.R + 8 + p.rows_v * 2 + p.rows_d) * 4, h->st);
+  if (e == cudaSuccess) e = launch_rope_table(h->rope, cfg->max_seq, p.hd, cfg->rope_theta, h->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->st);  // host vector bt must outlive the copy
+  if (e != cudaSuccess) {
+    delete h;
+    return SF_ERR_CUDA;
+  }
+  *out = h;
+  return SF_OK;
+}
+
+sf_status sf_debug_set_block_table(sf_handle* h, const int32_t* table_host, int32_t B, int32_t n_pages_per_seq) {
+  if (!h || !table_host) return SF_ERR_ARG;
+  if (h->state != ST_INIT) return set_err(h, SF_ERR_STATE, "block table can only be set before prefill");
+  if (B != h->p.B || n_pages_per_seq != h->p.pps) return set_err(h, SF_ERR_SHAPE, "block table shape");
+  std::vector<char> seen(h->p.n_pages, 0);
+  for (int i = 0; i < B * n_pages_per_seq; ++i) {
+    const int v = table_host[i];
+    if (v < 0 || v >= h->p.n_pages || seen[v]) return set_err(h, SF_ERR_ARG, "block table not a permutation");
+    seen[v] = 1;
+  }
+  SF_TRY(cudaMemcpyAsync(h->bt, table_host, (size_t)B * n_pages_per_seq * 4, cudaMemcpyHostToDevice, h->st));
+  SF_TRY(cudaStreamSynchronize(h->st));
+  return SF_OK;
+}
+
+sf_status specformer_prefill(sf_handle* h, const int32_t* tokens, int32_t B, int32_t P, int32_t* first_token) {
+  if (!h || !tokens) return SF_ERR_ARG;
+  if (B < 1 || B > h->p.B) return set_err(h, SF_ERR_SHAPE, "batch out of range");
+  if (P < 1) return set_err(h, SF_ERR_SHAPE, "empty prompt");
+  if (P + h->p.k + 1 > h->c.max_seq) return set_err(h, SF_ERR_CAPACITY, "prompt exceeds max_seq");
+  h->launches = 0;
+  h->B = B;
+  const Plan& p = h->p;
+  SF_TRY(cudaMemcpyAsync(h->prompt, tokens, (size_t)B * P * 4, cudaMemcpyDefault, h->st));
+  SF_TRY(cudaMemsetAsync(h->err, 0, 4, h->st));
+  const int C = p.C_pf;
+  int Cc = 0;
+  for (int c0 = 0; c0 < P; c0 += C) {
+    Cc = std::min(C, P - c0);
+    SF_TRY(launch_build_prefill_rows(B, P, c0, Cc, h->prompt, h->tok_rows, h->pos0_pf, h->st));
+    SF_TRY(base_forward(h, B * Cc, Cc, h->pos0_pf, c0 + Cc));
+    if (p.k > 0) SF_TRY(ctx_forward(h, B * Cc, Cc, h->pos0_pf, c0 + Cc));
+  }
+  // last prompt row per sequence: I_D row (draft input) and LM head -> g0
+  if (p.k > 0) SF_TRY(launch_gather_rows(h->ctx, Cc, nullptr, Cc - 1, B, p.d, h->idrow, h->st));
+  SF_TRY(launch_gather_rows(h->resid, Cc, nullptr, Cc - 1, B, p.d, h->hlast, h->st));
+  SF_TRY(head_argmax(h, h->hlast, B, h->logits, h->g_pf));
+  SF_TRY(launch_prefill_finish(B, P, h->g_pf, h->seq_len, h->n_prev, h->last_token, h->r_b, h->prompt_len, nullptr,
+                               h->st));
+  SF_TRY(copy_out(h, first_token, h->g_pf, (size_t)B * 4));
+  h->ctx_pending = false;
+  h->host_len_hi = P;
+  h->state = ST_READY;
+  return SF_OK;
+}
+
+sf_status specformer_draft_step(sf_handle* h, int32_t* draft, float* draft_logits) {
+  if (!h) return SF_ERR_ARG;
+  if (h->p.k == 0) return set_err(h, SF_ERR_UNSUPPORTED, "draft_len == 0 (AR mode) has no draft head");
+  if (h->state != ST_READY) return set_err(h, SF_ERR_STATE, "draft_step needs prefill or accept_commit first");
+  h->launches = 0;
+  SF_TRY(do_draft(h));
+  SF_TRY(copy_out(h, draft, h->draft, (size_t)h->B * h->p.k * 4));
+  SF_TRY(copy_out(h, draft_logits, h->dlogits, (size_t)h->B * h->p.k * h->p.V * 4));
+  h->state = ST_DRAFTED;
+  return SF_OK;
+}
+
+sf_status specformer_verify_step(sf_handle* h, const int32_t* draft_in, int32_t* greedy, float* logits) {
+  if (!h) return SF_ERR_ARG;
+  const int k = h->p.k;
+  const bool ok_state = h->state == ST_DRAFTED || (h->state == ST_READY && (k == 0 || draft_in));
+  if (!ok_state) return set_err(h, SF_ERR_STATE, "verify_step needs a draft (draft_step or draft_in)");
+  if (h->host_len_hi + k + 1 > h->c.max_seq) {
+    // refresh the host bound from the device lengths before failing
+    std::vector<int> sl(h->B);
+    SF_TRY(cudaMemcpyAsync(sl.data(), h->seq_len, (size_t)h->B * 4, cudaMemcpyDeviceToHost, h->st));
+    SF_TRY(cudaStreamSynchronize(h->st));
+    h->host_len_hi = *std::max_element(sl.begin(), sl.end());
+    if (h->host_len_hi + k + 1 > h->c.max_seq) return set_err(h, SF_ERR_CAPACITY, "seq_len + k + 1 > max_seq");
+  }
+  if (h->state == ST_READY && k > 0 && h->ctx_pending) {
+    // forced draft without a draft step: the context layer still has to see the previous rows
+    h->launches = 0;
+    SF_TRY(ctx_forward(h, h->B * (k + 1), k + 1, h->n_prev, h->c.max_seq));
+    SF_TRY(launch_gather_rows(h->ctx, k + 1, h->r_b, 0, h->B, h->p.d, h->idrow, h->st));
+    h->ctx_pending = false;
+  } else if (h->state != ST_READY) {
+    h->launches = 0;
+  } else {
+    h->launches = 0;
+  }
+  if (draft_in && k > 0) SF_TRY(cudaMemcpyAsync(h->draft, draft_in, (size_t)h->B * k * 4, cudaMemcpyDefault, h->st));
+  SF_TRY(do_verify(h));
+  SF_TRY(copy_out(h, greedy, h->greedy, (size_t)h->B * (k + 1) * 4));
+  SF_TRY(copy_out(h, logits, h->logits, (size_t)h->B * (k + 1) * h->p.V * 4));
+  h->state = ST_VERIFIED;
+  return SF_OK;
+}
+
+sf_status specformer_accept_commit(sf_handle* h, int32_t* accept_len, int32_t* emitted, int32_t* seq_len) {
+  if (!h) return SF_ERR_ARG;
+  if (h->state != ST_VERIFIED) return set_err(h, SF_ERR_STATE, "accept_commit needs verify_step first");
+  SF_TRY(do_accept(h, nullptr, nullptr, 0));
+  const int k = h->p.k;
+  SF_TRY(copy_out(h, accept_len, h->accept_len, (size_t)h->B * 4));
+  SF_TRY(copy_out(h, emitted, h->emitted, (size_t)h->B * (k + 1) * 4));
+  SF_TRY(copy_out(h, seq_len, h->seq_len, (size_t)h->B * 4));
+  h->host_len_hi += k + 1;
+  h->state = ST_READY;
+  return SF_OK;
+}
+
+static cudaError_t one_step(sf_handle* h, int* acc_log, int* em_log, int cap) {
+  cudaError_t e;
+  if (h->p.k > 0) {
+    if ((e = do_draft(h))) return e;
+    if (h->forced) {
+      h->launches++;
+      if ((e = launch_force_drafts(h->B, h->p.k, h->p.V, h->f_cont, h->f_cont_len, h->f_corrupt,
+                                   h->f_corrupt_steps, h->seq_len, h->prompt_len, h->step_counter, h->draft, h->st)))
+        return e;
+    }
+  }
+  if ((e = do_verify(h))) return e;
+  return do_accept(h, acc_log, em_log, cap);
+}
+
+sf_status specformer_decode_steps(sf_handle* h, int32_t n_steps, int32_t* emitted_log, int32_t* accept_log) {
+  if (!h) return SF_ERR_ARG;
+  if (n_steps < 0) return SF_ERR_ARG;
+  if (h->state != ST_READY) return set_err(h, SF_ERR_STATE, "decode_steps needs prefill or accept_commit first");
+  const int k = h->p.k;
+  if (h->host_len_hi + (int64_t)n_steps * (k + 1) > h->c.max_seq) {
+    std::vector<int> sl(h->B);
+    SF_TRY(cudaMemcpyAsync(sl.data(), h->seq_len, (size_t)h->B * 4, cudaMemcpyDeviceToHost, h->st));
+    SF_TRY(cudaStreamSynchronize(h->st));
+    h->host_len_hi = *std::max_element(sl.begin(), sl.end());
+    if (h->host_len_hi + (int64_t)n_steps * (k + 1) > h->c.max_seq)
+      return set_err(h, SF_ERR_CAPACITY, "decode_steps could exceed max_seq");
+  }
+  h->launches = 0;
+  SF_TRY(cudaMemsetAsync(h->step_counter, 0, 4, h->st));
+  int done = 0;
+  if (k > 0 && !h->ctx_pending && n_steps > 0) {  // first step after prefill: no context pass
+    SF_TRY(one_step(h, accept_log, emitted_log, n_steps));
+    done = 1;
+  }
+  const bool use_graph = (h->c.flags & SF_FLAG_CUDA_GRAPH) != 0 && !h->prof_on;
+  if (use_graph && done < n_steps) {
+    if (h->gexec && (h->g_acc_log != accept_log || h->g_em_log != emitted_log || h->g_log_cap < n_steps)) {
+      cudaGraphExecDestroy(h->gexec);
+      h->gexec = nullptr;
+    }
+    if (!h->gexec) {
+      cudaGraph_t g;
+      const int64_t before = h->launches;
+      SF_TRY(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+      cudaError_t e = one_step(h, accept_log, emitted_log, n_steps);
+      cudaError_t e2 = cudaStreamEndCapture(h->st, &g);
+      if (e != cudaSuccess || e2 != cudaSuccess) {
+        h->err_msg = std::string("graph capture failed: ") + cudaGetErrorString(e != cudaSuccess ? e : e2);
+        return SF_ERR_CUDA;
+      }
+      SF_TRY(cudaGraphInstantiate(&h->gexec, g, 0));
+      cudaGraphDestroy(g);
+      h->graph_launches = h->launches - before;
+      h->launches = before;
+      h->g_acc_log = accept_log;
+      h->g_em_log = emitted_log;
+      h->g_log_cap = n_steps;
+    }
+    for (int s = done; s < n_steps; ++s) {
+      SF_TRY(cudaGraphLaunch(h->gexec, h->st));
+      h->launches += h->graph_launches;
+    }
+    h->ctx_pending = k > 0;
+  } else {
+    for (int s = done; s < n_steps; ++s) SF_TRY(one_step(h, accept_log, emitted_log, n_steps));
+  }
+  h->host_len_hi += (int64_t)n_steps * (k + 1);
+  h->state = ST_READY;
+  return SF_OK;
+}
+
+sf_status specformer_sync(sf_handle* h) {
+  if (!h) return SF_ERR_ARG;
+  SF_TRY(cudaStreamSynchronize(h->st));
+  int err = 0;
+  SF_TRY(cudaMemcpy(&err, h->err, 4, cudaMemcpyDeviceToHost));
+  if (err & 1) return set_err(h, SF_ERR_NONFINITE, "non-finite logits");
+  return SF_OK;
+}
+
+const char* specformer_last_error(const sf_handle* h) { return h ? h->err_msg.c_str() : "null handle"; }
+
+void specformer_destroy(sf_handle* h) {
+  if (!h) return;
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  for (auto& r : h->prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : h->ev_free) cudaEventDestroy(e);
+  delete h;
+}
+
+int64_t specformer_kernel_launches(const sf_handle* h) { return h ? h->launches : -1; }
+
+sf_status sf_debug_capture(sf_handle* h, int32_t what, void* dst, int64_t* nbytes) {
+  if (!h || !dst) return SF_ERR_ARG;
+  const Plan& p = h->p;
+  const int B = h->B, k = p.k;
+  const void* src = nullptr;
+  size_t bytes = 0;
+  switch (what) {
+    case 0: {  // taps [4, B(k+1), d]
+      for (int g = 0; g < 4; ++g)
+        SF_TRY(cudaMemcpyAsync((char*)dst + (size_t)g * B * (k + 1) * p.d * 4, h->taps + (size_t)g * p.R * p.d,
+                               (size_t)B * (k + 1) * p.d * 4, cudaMemcpyDefault, h->st));
+      bytes = (size_t)4 * B * (k + 1) * p.d * 4;
+      break;
+    }
+    case 1: src = h->idrow; bytes = (size_t)B * p.d * 4; break;
+    case 2: src = h->D; bytes = (size_t)B * k * p.d * 4; break;
+    case 3: src = h->seq_len; bytes = (size_t)B * 4; break;
+    case 4: src = h->last_token; bytes = (size_t)B * 4; break;
+    case 5: src = h->n_prev; bytes = (size_t)B * 4; break;
+    default: return set_err(h, SF_ERR_ARG, "unknown capture id");
+  }
+  if (src) SF_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->st));
+  SF_TRY(cudaStreamSynchronize(h->st));
+  if (nbytes) *nbytes = (int64_t)bytes;
+  return SF_OK;
+}
+
+sf_status sf_debug_force_drafts(sf_handle* h, const int32_t* cont_dev, int32_t cont_len, const int32_t* corrupt_dev) {
+  if (!h || !cont_dev || cont_len < 1) return SF_ERR_ARG;
+  if (h->state != ST_DRAFTED && h->state != ST_READY) return set_err(h, SF_ERR_STATE, "force_drafts before verify");
+  SF_TRY(launch_force_drafts(h->B, h->p.k, h->p.V, cont_dev, cont_len, corrupt_dev, 1, h->seq_len, h->prompt_len,
+                             nullptr, h->draft, h->st));
+  h->state = ST_DRAFTED;
+  return SF_OK;
+}
+
+sf_status sf_set_forced_drafts(sf_handle* h, const int32_t* cont_dev, int32_t cont_len, const int32_t* corrupt_dev,
+                               int32_t corrupt_steps) {
+  if (!h) return SF_ERR_ARG;
+  if (h->gexec) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  h->forced = cont_dev != nullptr;
+  h->f_cont = cont_dev;
+  h->f_cont_len = cont_len;
+  h->f_corrupt = corrupt_dev;
+  h->f_corrupt_steps = std::max(1, corrupt_steps);
+  return SF_OK;
+}
+
+sf_status sf_profile(sf_handle* h, int32_t enable) {
+  if (!h) return SF_ERR_ARG;
+  SF_TRY(cudaStreamSynchronize(h->st));
+  for (auto& r : h->prof) {
+    h->ev_free.push_back(r.a);
+    h->ev_free.push_back(r.b);
+  }
+  h->prof.clear();
+  h->prof_on = enable != 0;
+  return SF_OK;
+}
+
+sf_status sf_profile_read(sf_handle* h, int32_t cls, double* total_ms, int64_t* count, double* bytes) {
+  if (!h || !total_ms || !count || !bytes) return SF_ERR_ARG;
+  SF_TRY(cudaStreamSynchronize(h->st));
+  double ms = 0, by = 0;
+  int64_t n = 0;
+  for (auto& r : h->prof) {
+    if (r.cls != cls) continue;
+    float t = 0;
+    SF_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+    ms += t;
+    by += r.bytes;
+    ++n;
+  }
+  *total_ms = ms;
+  *count = n;
+  *bytes = by;
+  return SF_OK;
+}
+
+sf_status sf_test_gemm(int32_t dtype, const void* A, const void* W, float* out, int32_t T, int32_t N, int32_t K,
+                       void* stream) {
+  if (!A || !W || !out || T < 1 || N < 1 || K < 1) return SF_ERR_ARG;
+  const bool bf = dtype == SF_BF16;
+  cudaStream_t st = (cudaStream_t)stream;
+  GemmScratch sc;
+  const int64_t pe = gemm_partial_elems(bf, std::min(T, 512), N, K);
+  if (pe > 0) {
+    if (cudaMallocAsync((void**)&sc.partial, pe * 4, st) != cudaSuccess) return SF_ERR_CUDA;
+    sc.partial_elems = pe;
+  }
+  if (cudaMallocAsync((void**)&sc.counters, 4096 * 4, st) != cudaSuccess) return SF_ERR_CUDA;
+  cudaMemsetAsync(sc.counters, 0, 4096 * 4, st);
+  sc.n_counters = 4096;
+  GemmEpi e;
+  e.mode = EPI_STORE_F32;
+  e.out = out;
+  e.ldo = N;
+  cudaError_t err = gemm_launch(bf, A, K, W, T, N, K, e, sc, st);
+  if (sc.partial) cudaFreeAsync(sc.partial, st);
+  cudaFreeAsync(sc.counters, st);
+  return err == cudaSuccess ? SF_OK : SF_ERR_CUDA;
+}
+
+}  // extern "C"

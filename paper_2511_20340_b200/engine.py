@@ -1,0 +1,240 @@
+"""Thin Python binding over the C ABI: device memory via torch, marshalling only.
+
+Every step of the decode path (draft, verify, accept) runs inside libspecformer.so's sm_100a
+kernels; this module allocates the packed weight blob / workspace with torch, packs the caller's
+weight dict into the layout `sf_weight_table` reports (concatenating q|k|v rows and interleaving
+gate/up rows in 64-row groups) and forwards calls.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as N
+
+
+@dataclass
+class EngineConfig:
+    n_layers: int
+    d_model: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    d_ff: int
+    vocab: int
+    draft_len: int
+    max_batch: int
+    max_seq: int
+    dtype: str = "bf16"          # "bf16" | "fp32"
+    rope_theta: float = 10000.0
+    rms_eps: float = 1e-6
+    kv_block: int = 16
+    flags: int = 0
+
+    @classmethod
+    def from_model(cls, m, max_batch=None, max_seq=None, draft_len=None, flags=0):
+        """Build from any object with the model-shape attributes (e.g. synth.ModelConfig)."""
+        return cls(m.n_layers, m.d_model, m.n_heads, m.n_kv_heads, m.head_dim, m.d_ff, m.vocab,
+                   m.draft_len if draft_len is None else draft_len, max_batch or m.batch,
+                   max_seq or m.max_seq, m.dtype, m.rope_theta, m.rms_eps, m.kv_block, flags)
+
+    def to_c(self) -> N.sf_config:
+        return N.sf_config(self.n_layers, self.d_model, self.n_heads, self.n_kv_heads, self.head_dim, self.d_ff,
+                           self.vocab, self.draft_len, self.max_batch, self.max_seq, self.kv_block,
+                           self.rope_theta, self.rms_eps, N.SF_BF16 if self.dtype == "bf16" else N.SF_FP32,
+                           1, 0, self.flags)
+
+
+def weight_table(cfg: EngineConfig):
+    lib = N.lib()
+    c = cfg.to_c()
+    n = lib.sf_weight_table(C.byref(c), None, 0)
+    if n < 0:
+        raise N.SpecFormerError(N.SF_ERR_ARG, "invalid config")
+    arr = (N.sf_tensor_desc * n)()
+    lib.sf_weight_table(C.byref(c), arr, n)
+    return [(d.name.decode(), tuple(d.shape[: d.ndim]), d.offset_bytes, d.dtype) for d in arr]
+
+
+def _interleave_gu(gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
+    F, d = gate.shape
+    return torch.stack([gate.reshape(F // 64, 64, d), up.reshape(F // 64, 64, d)], dim=1).reshape(2 * F, d)
+
+
+def _source_tensor(name: str, w: dict) -> torch.Tensor:
+    """Map a packed-table name to the caller's canonical tensors (see synth/weights.py)."""
+    pre, _, leaf = name.rpartition(".")
+    pre = pre + "." if pre else ""
+    if leaf.endswith("wqkv"):
+        p = pre + leaf[:-4]
+        return torch.cat([w[p + "wq"], w[p + "wk"], w[p + "wv"]], dim=0)
+    if leaf.endswith("w_gu"):
+        p = pre + leaf[:-4]
+        return _interleave_gu(w[p + "w_gate"], w[p + "w_up"])
+    return w[name]
+
+
+def pack_weights(cfg: EngineConfig, weights: dict, device="cuda") -> torch.Tensor:
+    lib = N.lib()
+    c = cfg.to_c()
+    nbytes = lib.sf_weights_bytes(C.byref(c))
+    blob = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    for name, shape, off, dt in weight_table(cfg):
+        t = _source_tensor(name, weights)
+        tdtype = torch.bfloat16 if dt == N.SF_BF16 else torch.float32
+        if tuple(t.shape) != shape:
+            raise ValueError(f"{name}: expected {shape}, got {tuple(t.shape)}")
+        n = t.numel() * (2 if dt == N.SF_BF16 else 4)
+        blob[off: off + n].view(tdtype).view(shape).copy_(t.to(device=device, dtype=tdtype))
+    return blob
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class Engine:
+    """One handle over B_max sequences on the current CUDA device."""
+
+    def __init__(self, cfg: EngineConfig, weights: dict, device="cuda", stream: torch.cuda.Stream | None = None):
+        self.cfg = cfg
+        self.lib = N.lib()
+        self.device = torch.device(device)
+        self.stream = stream or torch.cuda.Stream(device=self.device)
+        self._c = cfg.to_c()
+        self.weights = pack_weights(cfg, weights, self.device)
+        ws = self.lib.sf_workspace_bytes(C.byref(self._c))
+        if ws < 0:
+            raise N.SpecFormerError(N.SF_ERR_ARG, "invalid config")
+        self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
+        torch.cuda.synchronize(self.device)
+        h = C.c_void_p()
+        st = self.lib.specformer_init(C.byref(self._c), _ptr(self.weights), _ptr(self.workspace),
+                                      C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        if st != N.SF_OK:
+            raise N.SpecFormerError(st, "specformer_init")
+        self.h = h
+        self.B = 0
+
+    # ---------------------------------------------------------------- helpers
+    def _enter(self):
+        # inputs produced on torch's current stream must be visible to the engine stream
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+
+    def _exit(self):
+        # outputs written on the engine stream become visible to torch's current stream
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
+
+    def _check(self, st, what):
+        self._exit()
+        if st != N.SF_OK:
+            msg = self.lib.specformer_last_error(self.h)
+            raise N.SpecFormerError(st, f"{what}: {msg.decode() if msg else ''}")
+
+    def _i32(self, *shape):
+        return torch.empty(*shape, dtype=torch.int32, device=self.device)
+
+    @property
+    def k(self):
+        return self.cfg.draft_len
+
+    # ---------------------------------------------------------------- API
+    def prefill(self, tokens: torch.Tensor):
+        """tokens: int32 [B, P] (device or pinned host). Returns g0 [B] (device int32)."""
+        tokens = tokens.to(torch.int32).contiguous()
+        B, P = tokens.shape
+        first = self._i32(B)
+        self._enter()
+        self._check(self.lib.specformer_prefill(self.h, _ptr(tokens), B, P, _ptr(first)), "prefill")
+        self.B = B
+        return first
+
+    def draft_step(self, want_logits=False):
+        d = self._i32(self.B, self.k)
+        lg = torch.empty(self.B, self.k, self.cfg.vocab, device=self.device) if want_logits else None
+        self._enter()
+        self._check(self.lib.specformer_draft_step(self.h, _ptr(d), _ptr(lg)), "draft_step")
+        return (d, lg) if want_logits else d
+
+    def verify_step(self, draft: torch.Tensor | None = None, want_logits=False):
+        g = self._i32(self.B, self.k + 1)
+        lg = torch.empty(self.B, self.k + 1, self.cfg.vocab, device=self.device) if want_logits else None
+        if draft is not None:
+            draft = draft.to(torch.int32).contiguous()
+        self._enter()
+        self._check(self.lib.specformer_verify_step(self.h, _ptr(draft), _ptr(g), _ptr(lg)), "verify_step")
+        return (g, lg) if want_logits else g
+
+    def accept_commit(self):
+        m, em, sl = self._i32(self.B), self._i32(self.B, self.k + 1), self._i32(self.B)
+        self._enter()
+        self._check(self.lib.specformer_accept_commit(self.h, _ptr(m), _ptr(em), _ptr(sl)), "accept_commit")
+        return m, em, sl
+
+    def decode_steps(self, n: int, emitted_log: torch.Tensor | None = None, accept_log: torch.Tensor | None = None):
+        self._enter()
+        self._check(self.lib.specformer_decode_steps(self.h, n, _ptr(emitted_log), _ptr(accept_log)),
+                    "decode_steps")
+
+    def sync(self):
+        self._check(self.lib.specformer_sync(self.h), "sync")
+
+    def set_block_table(self, table: torch.Tensor):
+        t = table.to(torch.int32).contiguous().cpu()
+        self._check(self.lib.sf_debug_set_block_table(self.h, C.c_void_p(t.data_ptr()), t.shape[0], t.shape[1]),
+                    "set_block_table")
+
+    def capture(self, what: int, shape, dtype=torch.float32):
+        out = torch.empty(*shape, dtype=dtype, device=self.device)
+        nb = C.c_int64()
+        self._check(self.lib.sf_debug_capture(self.h, what, _ptr(out), C.byref(nb)), "capture")
+        return out
+
+    def set_forced_drafts(self, cont: torch.Tensor | None, corrupt: torch.Tensor | None = None):
+        self._forced = (cont, corrupt)  # keep alive
+        if cont is None:
+            self._check(self.lib.sf_set_forced_drafts(self.h, None, 0, None, 1), "set_forced_drafts")
+            return
+        cs = corrupt.shape[0] if corrupt is not None else 1
+        self._enter()
+        self._check(self.lib.sf_set_forced_drafts(self.h, _ptr(cont), cont.shape[1], _ptr(corrupt), cs),
+                    "set_forced_drafts")
+
+    def profile(self, enable: bool):
+        self._check(self.lib.sf_profile(self.h, 1 if enable else 0), "profile")
+
+    def profile_read(self, cls: int):
+        ms, n, by = C.c_double(), C.c_int64(), C.c_double()
+        self._check(self.lib.sf_profile_read(self.h, cls, C.byref(ms), C.byref(n), C.byref(by)), "profile_read")
+        return ms.value, n.value, by.value
+
+    def kernel_launches(self) -> int:
+        return int(self.lib.specformer_kernel_launches(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.specformer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_gemm(A: torch.Tensor, W: torch.Tensor, stream=None) -> torch.Tensor:
+    """out[T,N] = A[T,K] W[N,K]^T through the hot path's GEMM kernels (T-kernel parity hook)."""
+    lib = N.lib()
+    T, K = A.shape
+    Nn = W.shape[0]
+    out = torch.empty(T, Nn, dtype=torch.float32, device=A.device)
+    dt = N.SF_BF16 if A.dtype == torch.bfloat16 else N.SF_FP32
+    s = stream or torch.cuda.current_stream(A.device)
+    st = lib.sf_test_gemm(dt, _ptr(A.contiguous()), _ptr(W.contiguous()), _ptr(out), T, Nn, K,
+                          C.c_void_p(s.cuda_stream))
+    if st != N.SF_OK:
+        raise N.SpecFormerError(st, "sf_test_gemm")
+    return out

@@ -1,0 +1,54 @@
+"""Algorithmic bytes / FLOPs of one decode step.
+
+Counted once per pass: every weight byte of the base model (verify) and of the SpecFormer head +
+shared LM head (draft), every KV byte once per (sequence, layer) -- the k+1 query rows share one
+KV stream -- and the fp32 logits once written and once read. Not counted: re-reads, padded MMA
+rows, split-K / split-KV partials, L2 hits.
+"""
+from __future__ import annotations
+
+
+def _attn_params(c):
+    d, hq, hkv, hd = c.d_model, c.n_heads, c.n_kv_heads, c.head_dim
+    return d * (hq + 2 * hkv) * hd + hq * hd * d
+
+
+def base_linear_params(c):
+    return c.n_layers * (_attn_params(c) + 3 * c.d_model * c.d_ff)
+
+
+def head_params(c, k):
+    d = c.d_model
+    return 4 * d * d + _attn_params(c) + k * d * d + _attn_params(c) + 3 * d * c.d_ff
+
+
+def kv_bytes_per_token_layer(c, elt=2):
+    return 2 * c.n_kv_heads * c.head_dim * elt
+
+
+def attention_kv_bytes(c, lens_verify, lens_ctx, k, elt=2):
+    """KV bytes read by the paged-attention launches of one step: base layers at positions
+    0..n_b+k (verify), context layer L+1 at 0..n_prev_b+k (draft)."""
+    per = kv_bytes_per_token_layer(c, elt)
+    return per * (c.n_layers * sum(n + k + 1 for n in lens_verify) + sum(n + k + 1 for n in lens_ctx))
+
+
+def step_bytes(c, B, k, lens_verify, lens_ctx, elt=2):
+    V, d = c.vocab, c.d_model
+    w = (base_linear_params(c) + V * d) * elt          # verify: base + LM head
+    w += (head_params(c, k) + V * d) * elt             # draft: head + LM head again
+    kv = attention_kv_bytes(c, lens_verify, lens_ctx, k, elt)
+    logits = (B * (k + 1) + B * k) * V * 4 * 2
+    return w + kv + logits
+
+
+def step_flops(c, B, k, lens_verify):
+    T = B * (k + 1)
+    V, d = c.vocab, c.d_model
+    f = 2 * T * (base_linear_params(c) + V * d)
+    f += 2 * T * (4 * d * d + _attn_params(c))                 # W_D + context QKV/O
+    f += 2 * B * k * d * d                                      # W_P
+    f += 2 * B * k * (_attn_params(c) + 3 * d * c.d_ff + V * d)  # draft block + LM head
+    ctx = sum(lens_verify) / max(1, len(lens_verify)) + k + 1
+    f += 4 * T * ctx * c.n_heads * c.head_dim * (c.n_layers + 1)
+    return f

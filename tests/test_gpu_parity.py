@@ -1,0 +1,187 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, and GPU-side invariants.
+
+Tolerances (reading C21 of SURVEY §8c):
+  fp32 mode: logits |gpu - oracle| <= 1e-5 (abs) + 1e-5 rel; tokens, drafts, accept lengths bit-exact.
+  bf16 mode (Small): per-step logits rel-L2 <= 1.5e-2 and >= 99% of elements within 2e-2 rel / 1e-2 abs;
+    greedy and draft tokens bit-exact wherever the oracle's top-1/top-2 margin > 5e-2;
+    accept lengths == oracle accept(gpu draft, gpu greedy) (integer logic, always exact).
+  GPU SD == GPU AR (k = 0 loop) bit-exact (batch-invariant kernels, reading C23).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from gpu_helpers import make_engine, oracle_replay, rel_l2, run_gpu, setup
+from paper_2511_20340_b200 import _native as N
+from paper_2511_20340_b200 import run_gemm
+from synth import get_config, make_prompts
+
+pytestmark = pytest.mark.gpu
+
+TINY = get_config("tiny")
+SMALL = get_config("small")
+
+
+# ------------------------------------------------------------------ GEMM kernel parity
+@pytest.mark.parametrize("T,Nn,K", [(1, 128, 64), (5, 256, 128), (16, 384, 4096), (40, 768, 768), (77, 2304, 768),
+                                    (320, 4096, 4096), (600, 1024, 256), (8, 32000, 768), (257, 512, 11008)])
+def test_gemm_bf16_tcgen05(T, Nn, K):
+    g = torch.Generator().manual_seed(T * 7 + Nn + K)
+    A = torch.randn(T, K, generator=g).to(torch.bfloat16)
+    W = (0.02 * torch.randn(Nn, K, generator=g)).to(torch.bfloat16)
+    ref = (A.double() @ W.double().T)
+    out = run_gemm(A.cuda(), W.cuda()).cpu().double()
+    torch.cuda.synchronize()
+    err = (out - ref).abs()
+    tol = 2e-5 * (A.double().abs() @ W.double().abs().T) + 1e-6
+    assert (err <= tol).all(), f"max err {err.max().item()} worst ratio {(err / tol).max().item()}"
+
+
+@pytest.mark.parametrize("T,Nn,K", [(1, 64, 16), (5, 512, 64), (33, 100, 70)])
+def test_gemm_fp32_simt(T, Nn, K):
+    g = torch.Generator().manual_seed(1)
+    A, W = torch.randn(T, K, generator=g), torch.randn(Nn, K, generator=g)
+    out = run_gemm(A.cuda(), W.cuda()).cpu().double()
+    ref = A.double() @ W.double().T
+    assert torch.allclose(out, ref, rtol=1e-5, atol=1e-5)
+
+
+# ------------------------------------------------------------------ Tiny fp32 end to end
+def _check_fp32(cfg, w, prompts, res, atol=1e-5):
+    for b in range(prompts.shape[0]):
+        plog, rep = oracle_replay(cfg, w, prompts[b].tolist(), res["steps"], b)
+        for s, r in zip(res["steps"], rep):
+            gl = s["logits"][b]
+            assert np.all(np.abs(gl - r["logits"]) <= atol + 1e-5 * np.abs(r["logits"])), \
+                np.abs(gl - r["logits"]).max()
+            dl = s["draft_logits"][b]
+            assert np.all(np.abs(dl - r["draft_logits"]) <= atol + 1e-5 * np.abs(r["draft_logits"])), \
+                np.abs(dl - r["draft_logits"]).max()
+            assert list(s["greedy"][b]) == r["greedy"]
+            assert list(s["draft"][b]) == [O.argmax_lowest(x) for x in r["draft_logits"]]
+            m, _ = O.accept(s["draft"][b], s["greedy"][b])
+            assert m == s["m"][b]
+
+
+@pytest.mark.parametrize("seed,jitter", [(0, 0.0), (3, 0.1)])
+def test_tiny_fp32_matches_oracle(seed, jitter):
+    w, prompts = setup(TINY, seed=seed, jitter=jitter)
+    res = run_gpu(TINY, w, prompts, TINY.gen_len, want_logits=True)
+    _check_fp32(TINY, w, prompts, res)
+    W = O.Weights(TINY, w)
+    assert res["tokens"][0] == O.decode_greedy(W, prompts[0].tolist(), TINY.gen_len)
+
+
+def test_tiny_fp32_batch_and_paged_permutation():
+    cfg = TINY.replace(batch=3)
+    w, prompts = setup(cfg, seed=5, B=3)
+    res = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True)
+    _check_fp32(cfg, w, prompts, res)
+    eng = res["engine"]
+    pps = eng.cfg.max_seq // 16
+    perm = torch.randperm(3 * pps, generator=torch.Generator().manual_seed(9)).reshape(3, pps)
+    res2 = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True, block_table=perm)
+    assert res2["tokens"] == res["tokens"]
+    for s1, s2 in zip(res["steps"], res2["steps"]):
+        assert np.array_equal(s1["logits"], s2["logits"])
+
+
+def test_tiny_gpu_sd_equals_gpu_ar():
+    cfg = TINY.replace(batch=2)
+    w, prompts = setup(cfg, seed=2, B=2)
+    sd = run_gpu(cfg, w, prompts, cfg.gen_len)
+    ar = run_gpu(cfg, w, prompts, cfg.gen_len, k=0)
+    assert sd["tokens"] == ar["tokens"]
+    assert all(len(s["m"]) == 2 for s in ar["steps"])
+
+
+# ------------------------------------------------------------------ Small bf16
+@pytest.fixture(scope="module")
+def small_run():
+    w, prompts = setup(SMALL, seed=0)
+    res = run_gpu(SMALL, w, prompts, 48, want_logits=True)
+    return w, prompts, res
+
+
+def test_small_bf16_logits_and_tokens(small_run):
+    w, prompts, res = small_run
+    flips = checked = 0
+    for b in (0, 5):
+        _, rep = oracle_replay(SMALL, w, prompts[b].tolist(), res["steps"], b)
+        for s, r in zip(res["steps"], rep):
+            gl, ol = s["logits"][b].astype(np.float64), r["logits"]
+            assert rel_l2(gl, ol) <= 1.5e-2
+            ok = np.abs(gl - ol) <= 1e-2 + 2e-2 * np.abs(ol)
+            assert ok.mean() >= 0.99
+            for i in range(SMALL.draft_len + 1):
+                if O.top2_margin(ol[i]) > 5e-2:
+                    checked += 1
+                    assert s["greedy"][b][i] == r["greedy"][i]
+            dl, odl = s["draft_logits"][b].astype(np.float64), r["draft_logits"]
+            for j in range(SMALL.draft_len):
+                if O.top2_margin(odl[j]) > 5e-2:
+                    assert s["draft"][b][j] == O.argmax_lowest(odl[j])
+            m, _ = O.accept(s["draft"][b], s["greedy"][b])
+            assert m == s["m"][b]
+    assert checked > 50
+
+
+def test_small_bf16_sd_equals_ar_and_batch_invariance(small_run):
+    w, prompts, res = small_run
+    ar = run_gpu(SMALL, w, prompts, 48, k=0)
+    assert ar["tokens"] == res["tokens"]
+    solo = run_gpu(SMALL.replace(batch=1), w, prompts[3:4], 48)
+    assert solo["tokens"][0] == res["tokens"][3]
+
+
+def test_forced_perfect_drafts_accept_all():
+    """Drafts replaced by the GPU's own AR continuation => every step accepts k (C11 step count)."""
+    cfg = TINY
+    w, prompts = setup(cfg, seed=1)
+    N_ = cfg.gen_len
+    ar = run_gpu(cfg, w, prompts, N_ + 2 * cfg.draft_len + 2, k=0)
+    cont = torch.tensor(ar["tokens"], dtype=torch.int32).cuda()
+    eng = make_engine(cfg, w, 1, N_)
+    eng.prefill(prompts.cuda())
+    eng.set_forced_drafts(cont, None)
+    n_steps = -(-(N_ - 1) // (cfg.draft_len + 1))
+    acc = torch.zeros(n_steps, 1, dtype=torch.int32, device="cuda")
+    eng.decode_steps(n_steps, None, acc)
+    eng.sync()
+    assert (acc == cfg.draft_len).all()
+
+
+# ------------------------------------------------------------------ errors
+def test_state_machine_and_nonfinite():
+    cfg = TINY
+    w, prompts = setup(cfg, seed=0)
+    eng = make_engine(cfg, w, 1, 32)
+    with pytest.raises(N.SpecFormerError) as e:
+        eng.draft_step()
+    assert e.value.status == N.SF_ERR_STATE
+    eng.prefill(prompts.cuda())
+    with pytest.raises(N.SpecFormerError) as e:
+        eng.accept_commit()
+    assert e.value.status == N.SF_ERR_STATE
+    with pytest.raises(N.SpecFormerError) as e:
+        eng.prefill(torch.zeros(2, 4, dtype=torch.int32).cuda())
+    assert e.value.status == N.SF_ERR_SHAPE
+    w2 = dict(w)
+    w2["lm_head"] = w["lm_head"].clone()
+    w2["lm_head"][7, 3] = float("nan")
+    eng2 = make_engine(cfg, w2, 1, 32)
+    eng2.prefill(prompts.cuda())
+    with pytest.raises(N.SpecFormerError) as e:
+        eng2.sync()
+    assert e.value.status == N.SF_ERR_NONFINITE
+
+
+def test_capacity_error():
+    cfg = TINY
+    w, prompts = setup(cfg, seed=0)
+    eng = make_engine(cfg, w, 1, 4)
+    eng.prefill(prompts.cuda())
+    with pytest.raises(N.SpecFormerError) as e:
+        eng.decode_steps(100)
+    assert e.value.status == N.SF_ERR_CAPACITY
