@@ -363,8 +363,17 @@ static cudaError_t gemm_launch_chunk(bool is_bf16, const void* A, int lda, const
   p.tmem_cols = 32;
   while ((int)p.tmem_cols < cols) p.tmem_cols <<= 1;
   const int stage_bytes = BM * BK * 2 + p.n_sub * p.NT * BK * 2;
-  const int budget = 200 * 1024;
-  p.stages = std::max(2, std::min(8, budget / stage_bytes));
+  // Size the ring so that every CTA of the launch is resident at once (no tail wave): a
+  // memory-bound launch then shares HBM evenly across all its weight streams.
+  const int ctas = (N / BM) * p.splits;
+  int per_sm = std::min(4, (ctas + 147) / 148);
+  int stages = 0;
+  for (; per_sm >= 1; --per_sm) {
+    const int budget = (226 * 1024) / per_sm - 2048;
+    stages = std::min(8, budget / stage_bytes);
+    if (stages >= 3 || per_sm == 1) break;
+  }
+  p.stages = std::max(2, stages);
   const size_t smem = (size_t)p.stages * stage_bytes + 1024 + (2 * p.stages + 1) * 8 + 16;
   if (!g_attr_set) {
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

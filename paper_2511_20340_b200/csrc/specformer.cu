@@ -934,23 +934,30 @@ sf_status sf_test_gemm(int32_t dtype, const void* A, const void* W, float* out, 
   if (!A || !W || !out || T < 1 || N < 1 || K < 1) return SF_ERR_ARG;
   const bool bf = dtype == SF_BF16;
   cudaStream_t st = (cudaStream_t)stream;
-  GemmScratch sc;
+  // test-only scratch, grown on demand and kept (counters stay zeroed: kernels re-arm them)
+  static float* partial = nullptr;
+  static int64_t partial_cap = 0;
+  static int* counters = nullptr;
   const int64_t pe = gemm_partial_elems(bf, std::min(T, 512), N, K);
-  if (pe > 0) {
-    if (cudaMallocAsync((void**)&sc.partial, pe * 4, st) != cudaSuccess) return SF_ERR_CUDA;
-    sc.partial_elems = pe;
+  if (pe > partial_cap) {
+    if (partial) cudaFree(partial);
+    if (cudaMalloc((void**)&partial, pe * 4) != cudaSuccess) return SF_ERR_CUDA;
+    partial_cap = pe;
   }
-  if (cudaMallocAsync((void**)&sc.counters, 4096 * 4, st) != cudaSuccess) return SF_ERR_CUDA;
-  cudaMemsetAsync(sc.counters, 0, 4096 * 4, st);
+  if (!counters) {
+    if (cudaMalloc((void**)&counters, 4096 * 4) != cudaSuccess) return SF_ERR_CUDA;
+    cudaMemset(counters, 0, 4096 * 4);
+  }
+  GemmScratch sc;
+  sc.partial = partial;
+  sc.partial_elems = partial_cap;
+  sc.counters = counters;
   sc.n_counters = 4096;
   GemmEpi e;
   e.mode = EPI_STORE_F32;
   e.out = out;
   e.ldo = N;
-  cudaError_t err = gemm_launch(bf, A, K, W, T, N, K, e, sc, st);
-  if (sc.partial) cudaFreeAsync(sc.partial, st);
-  cudaFreeAsync(sc.counters, st);
-  return err == cudaSuccess ? SF_OK : SF_ERR_CUDA;
+  return gemm_launch(bf, A, K, W, T, N, K, e, sc, st) == cudaSuccess ? SF_OK : SF_ERR_CUDA;
 }
 
 }  // extern "C"

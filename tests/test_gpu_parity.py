@@ -185,3 +185,44 @@ def test_capacity_error():
     with pytest.raises(N.SpecFormerError) as e:
         eng.decode_steps(100)
     assert e.value.status == N.SF_ERR_CAPACITY
+
+
+# ------------------------------------------------------------------ hd=128 bf16 (tensor-core attention path)
+MID = SMALL.replace(name="mid", n_layers=2, d_model=512, n_heads=4, n_kv_heads=4, head_dim=128, d_ff=1408,
+                    vocab=4096, batch=4, prompt_len=300, gen_len=24)
+GQA = MID.replace(name="gqa", d_model=1024, n_heads=8, n_kv_heads=2, prompt_len=200, batch=3)
+
+
+def _check_bf16(cfg, w, prompts, res, seqs, rel_tol=1.5e-2):
+    checked = 0
+    for b in seqs:
+        _, rep = oracle_replay(cfg, w, prompts[b].tolist(), res["steps"], b)
+        for s, r in zip(res["steps"], rep):
+            gl, ol = s["logits"][b].astype(np.float64), r["logits"]
+            assert rel_l2(gl, ol) <= rel_tol, rel_l2(gl, ol)
+            for i in range(cfg.draft_len + 1):
+                if O.top2_margin(ol[i]) > 5e-2:
+                    checked += 1
+                    assert s["greedy"][b][i] == r["greedy"][i]
+            odl = r["draft_logits"]
+            assert rel_l2(s["draft_logits"][b].astype(np.float64), odl) <= rel_tol
+            for j in range(cfg.draft_len):
+                if O.top2_margin(odl[j]) > 5e-2:
+                    assert s["draft"][b][j] == O.argmax_lowest(odl[j])
+            assert O.accept(s["draft"][b], s["greedy"][b])[0] == s["m"][b]
+    return checked
+
+
+@pytest.mark.parametrize("cfg", [MID, GQA], ids=["mha128", "gqa4"])
+def test_hd128_bf16_matches_oracle_and_sd_equals_ar(cfg):
+    w, prompts = setup(cfg, seed=4, jitter=0.1)
+    res = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True)
+    assert _check_bf16(cfg, w, prompts, res, seqs=(0, cfg.batch - 1)) > 20
+    ar = run_gpu(cfg, w, prompts, cfg.gen_len, k=0)
+    assert ar["tokens"] == res["tokens"]
+    eng = res["engine"]
+    pps = eng.cfg.max_seq // 16
+    perm = torch.randperm(cfg.batch * pps, generator=torch.Generator().manual_seed(3)).reshape(cfg.batch, pps)
+    res2 = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True, block_table=perm)
+    for s1, s2 in zip(res["steps"], res2["steps"]):
+        assert np.array_equal(s1["logits"], s2["logits"])
