@@ -81,6 +81,8 @@ typedef struct {
   int64_t shape[4];
   int64_t offset_bytes; /* from the start of the packed weight blob (256-byte aligned) */
   int32_t dtype;        /* sf_dtype of the stored elements                              */
+  int32_t layout;       /* 0: row-major [out, in]; 1: tile-contiguous bf16 GEMM layout written
+                           by sf_pack_matrix (128 x 64 tiles, 128B-swizzled, t-major then k) */
 } sf_tensor_desc;
 
 typedef struct sf_handle sf_handle;
@@ -95,7 +97,8 @@ typedef struct sf_handle sf_handle;
  * w_gu interleaves the SwiGLU gate and up projections in 64-row groups: rows [128i, 128i+64)
  * are gate rows [64i, 64i+64) and rows [128i+64, 128i+128) are up rows [64i, 64i+64)
  * (F % 64 == 0), so one GEMM tile holds matching gate/up rows for the fused SwiGLU epilogue.
- * Matrices are stored in the config dtype, vectors in fp32. */
+ * Matrices are stored in the config dtype, vectors in fp32. In bf16 mode every matrix except
+ * `embed` uses layout 1: fill it with sf_pack_matrix from a row-major device copy. */
 int sf_weight_table(const sf_config* cfg, sf_tensor_desc* out, int cap);
 int64_t sf_weights_bytes(const sf_config* cfg);   /* -1 on invalid config */
 int64_t sf_workspace_bytes(const sf_config* cfg); /* KV pools (L+1 layers) + activations; -1 if invalid */
@@ -164,8 +167,15 @@ sf_status sf_set_forced_drafts(sf_handle* h, const int32_t* cont_dev, int32_t co
  * attention, whose KV bytes depend on device-resident lengths) of one class. */
 sf_status sf_profile(sf_handle* h, int32_t enable);
 sf_status sf_profile_read(sf_handle* h, int32_t cls, double* total_ms, int64_t* count, double* bytes);
-/* Direct GEMM entry (T-kernel parity): out[T,N] = A[T,K] W[N,K]^T in the config dtype with
- * fp32 accumulation; A, W dev in dtype; out dev fp32. Uses the same kernels as the hot path. */
+/* Write row-major bf16 src[N, K] (device) into the tile-contiguous layout 1 at dst (device, N*K*2
+ * bytes): 128-row x 64-column tiles stored contiguously (tile (t, k) at ((t * K/64) + k) * 16 KB)
+ * as the exact image of a 128-byte-swizzled K-major shared-memory tile, so each GEMM pipeline
+ * stage is one contiguous bulk copy and a stream-K range is one contiguous stretch of HBM.
+ * Requires N % 128 == 0, K % 64 == 0. Asynchronous on `stream`. */
+sf_status sf_pack_matrix(int32_t dtype, const void* src_dev, void* dst_dev, int64_t N, int64_t K, void* stream);
+/* Direct GEMM entry (T-kernel parity): out[T,N] = A[T,K] W[N,K]^T with fp32 accumulation;
+ * dtype SF_FP32 (A, W fp32), SF_BF16 (A, W bf16 row-major; W is packed to layout 1 internally) or
+ * 2 (A bf16, W already in layout 1). out dev fp32. Uses the same kernels as the hot path. */
 sf_status sf_test_gemm(int32_t dtype, const void* A, const void* W, float* out, int32_t T, int32_t N, int32_t K,
                        void* stream);
 

@@ -30,7 +30,7 @@ class sf_config(C.Structure):
 
 class sf_tensor_desc(C.Structure):
     _fields_ = [("name", C.c_char * 64), ("ndim", C.c_int32), ("shape", C.c_int64 * 4),
-                ("offset_bytes", C.c_int64), ("dtype", C.c_int32)]
+                ("offset_bytes", C.c_int64), ("dtype", C.c_int32), ("layout", C.c_int32)]
 
 
 # every symbol include/specformer.h declares: (name, restype, argtypes)
@@ -58,6 +58,7 @@ SIGNATURES = [
     ("sf_profile", C.c_int, [_P, C.c_int32]),
     ("sf_profile_read", C.c_int, [_P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                   C.POINTER(C.c_double)]),
+    ("sf_pack_matrix", C.c_int, [C.c_int32, _P, _P, C.c_int64, C.c_int64, _P]),
     ("sf_test_gemm", C.c_int, [C.c_int32, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, _P]),
 ]
 

@@ -1,20 +1,21 @@
 // gemm.cu -- the dense contractions of the hot path (QKV / O / SwiGLU / down / W_D / W_P /
 // LM head; PAPER Eq.7-10 and the base decoder).
 //
-// bf16: a swap-AB tcgen05 GEMM. The weight W[N, K] is the MMA "A" operand (M = 128 weight rows
-// per CTA), the skinny activation block X[T, K] (T = B(k+1) = 5..512 rows) is the MMA "B"
-// operand (N = T rounded to 16, up to 2 x 256 accumulators), so the weight -- the bytes that
-// bound the step at small batch -- streams through shared memory exactly once per launch.
-// TMA (128B swizzle) feeds a multi-stage mbarrier ring; one thread issues tcgen05.mma into a
-// TMEM fp32 accumulator; 4 epilogue warps read TMEM with tcgen05.ld and apply the fused
-// epilogue. Split-K (a function of the weight shape only -> batch-invariant, reading C23) is
-// reduced deterministically by the last-arriving CTA in split order.
+// bf16: a swap-AB, persistent stream-K tcgen05 GEMM. The weight W[N, K] is the MMA "A" operand
+// (M = 128 weight rows per tile), the skinny activation block X[T, K] (T = B(k+1) = 5..512 rows)
+// is the MMA "B" operand (N = T rounded to 16, up to 2 x 256 accumulator columns), so the weight
+// -- the bytes that bound the step at small batch -- streams through shared memory exactly once
+// per launch, from a tile-contiguous pre-swizzled HBM layout (one 16 KB bulk copy per stage).
+// An mbarrier ring feeds one MMA-issuing thread; TMEM holds the fp32 accumulators; 4 epilogue
+// warps read them with tcgen05.ld and apply the fused epilogue.
 // fp32: a plain smem-tiled SIMT kernel (the fp32 parity mode; no TF32).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -24,20 +25,6 @@ namespace sf {
 
 constexpr int BM = 128;  // weight rows per CTA (MMA M)
 constexpr int BK = 64;   // K per stage (one 128-byte swizzle atom of bf16)
-
-struct TcParams {
-  int T, N, K;
-  int NT;          // MMA N (columns per accumulator), multiple of 16
-  int n_sub;       // accumulators (n_sub * NT >= T)
-  int stages;
-  int kb_total;
-  int splits;
-  uint32_t tmem_cols;
-  GemmEpi epi;
-  float* partial;
-  int* counters;
-};
-
 template <typename TA>
 SF_DEV void epi_apply(const GemmEpi& e, int t, int n, float v) {
   const size_t off = (size_t)t * e.ldo + n;
@@ -57,8 +44,36 @@ SF_DEV void epi_apply(const GemmEpi& e, int t, int n, float v) {
 SF_DEV float silu_f(float g) { return g / (1.f + expf(-g)); }
 
 // ------------------------------------------------------------------------ tcgen05 kernel
-__global__ void __launch_bounds__(128, 1)
-gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA, const TcParams p) {
+// ------------------------------------------------------------------------ persistent stream-K kernel
+// Grid = G CTAs (G = min(#SMs, units), a function of (N, K) only). The (128-row tile, 64-wide
+// k-block) units of the whole GEMM are split into G contiguous equal ranges, so every SM streams
+// the same number of weight bytes (no wave quantisation). A tile cut between CTAs is finished by
+// the CTA owning its k = 0 segment, which adds the other segments' fp32 partials in k order:
+// segment boundaries depend only on (N, K, G) -> the same rounding for every T (batch invariance).
+// Warps: 0 = TMA producer, 1 = MMA issuer, 2 = TMEM allocator, 4..7 = epilogue (TMEM lanes 32(w-4)..).
+// Two TMEM accumulator buffers (when they fit) let the epilogue of one segment overlap the MMAs
+// of the next.
+struct SkParams {
+  int T, N, K;
+  int NT, n_sub, stages, kb_total, n_tiles, G, nbuf, w_tiled;
+  int cgrp;  // ring slots released per tcgen05.commit (a commit drains the tensor pipe)
+  uint32_t tmem_cols;
+  const __nv_bfloat16* w_tiles;  // tile-contiguous weights (w_tiled)
+  GemmEpi epi;
+  float* partial;  // [G][T][128]
+  int* flags;      // [G]
+};
+
+SF_DEV void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+SF_DEV int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+SF_DEV void st_release(int* p, int v) { asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
+
+__global__ void __launch_bounds__(256, 1)
+gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA, const SkParams p) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
@@ -66,25 +81,29 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   const int stage_bytes = BM * BK * 2 + a_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * stage_bytes);
   uint64_t* empty = full + p.stages;
-  uint64_t* accum = empty + p.stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
-  int* flag_s = reinterpret_cast<int*>(tmem_slot + 1);
+  uint64_t* accf = empty + p.stages;  // [2]
+  uint64_t* acce = accf + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+  float* xch = reinterpret_cast<float*>(tmem_slot + 4);  // [64][17] SwiGLU exchange
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile_n = blockIdx.x, split = blockIdx.y;
-  const int n0 = tile_n * BM;
-  const int kb_per = p.kb_total / p.splits, kb_rem = p.kb_total % p.splits;
-  const int kb_begin = split * kb_per + min(split, kb_rem);
-  const int kb_count = kb_per + (split < kb_rem ? 1 : 0);
+  const int c = blockIdx.x;
+  const int kb = p.kb_total;
+  const long long U = (long long)p.n_tiles * kb;
+  const long long u0 = U * c / p.G, u1 = U * (c + 1) / p.G;
+  const int cols = p.n_sub * p.NT;
 
   if (threadIdx.x == 0) {
-    prefetch_tmap(&tmW);
+    if (!p.w_tiled) prefetch_tmap(&tmW);
     prefetch_tmap(&tmA);
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accum, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
@@ -93,112 +112,152 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer
-    for (int i = 0; i < kb_count; ++i) {
+  if (warp == 0) {
+    // ---- TMA producer warp (converged; one elected lane issues)
+    int i = 0;
+    int t = (int)(u0 / kb), k = (int)(u0 % kb);
+    for (long long u = u0; u < u1; ++u, ++i) {
       const int s = i % p.stages;
       const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
-      mbar_wait(&empty[s], ph ^ 1u);
-      uint8_t* st = smem + (size_t)s * stage_bytes;
-      mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
-      const int kc = (kb_begin + i) * BK;
-      tma_load_2d(st, &tmW, &full[s], kc, n0, kEvictFirst);
-      for (int j = 0; j < p.n_sub; ++j)
-        tma_load_2d(st + BM * BK * 2 + j * p.NT * BK * 2, &tmA, &full[s], kc, j * p.NT, kEvictLast);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer (single thread)
-    const uint32_t idesc = idesc_bf16_f32(BM, p.NT);
-    for (int i = 0; i < kb_count; ++i) {
-      const int s = i % p.stages;
-      const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
-      mbar_wait(&full[s], ph);
-      tc_fence_after();
-      const uint32_t wa = smem_u32(smem + (size_t)s * stage_bytes);
-      const uint64_t dw = sw128_kmajor_desc(wa);
-#pragma unroll
-      for (int kk = 0; kk < BK / 16; ++kk) {
-        for (int j = 0; j < p.n_sub; ++j) {
-          const uint64_t da = sw128_kmajor_desc(wa + BM * BK * 2 + j * p.NT * BK * 2);
-          umma_bf16(tmem + (uint32_t)(j * p.NT), dw + (uint64_t)(kk * 2), da + (uint64_t)(kk * 2), idesc,
-                    (i > 0 || kk > 0) ? 1u : 0u);
-        }
+      mbar_wait(&empty[(s / p.cgrp) * p.cgrp + p.cgrp - 1], ph ^ 1u);  // slot group released
+      if (elect_one()) {
+        uint8_t* st = smem + (size_t)s * stage_bytes;
+        mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
+        if (p.w_tiled)  // tile-contiguous, pre-swizzled weights: one 16 KB bulk copy per stage
+          bulk_load(st, p.w_tiles + ((size_t)t * kb + k) * (BM * BK), BM * BK * 2, &full[s], kEvictFirst);
+        else
+          tma_load_2d(st, &tmW, &full[s], k * BK, t * BM, kEvictFirst);
+        for (int j = 0; j < p.n_sub; ++j)
+          tma_load_2d(st + BM * BK * 2 + j * p.NT * BK * 2, &tmA, &full[s], k * BK, j * p.NT, kEvictLast);
       }
-      umma_commit(&empty[s]);  // frees the smem slot once these MMAs have read it
+      __syncwarp();
+      if (++k == kb) {
+        k = 0;
+        ++t;
+      }
     }
-    umma_commit(accum);
-  }
-  __syncwarp();
-
-  // ---- epilogue: all 4 warps; thread owns accumulator row m = weight row n0 + m
-  mbar_wait(accum, 0);
-  tc_fence_after();
-  const int m = warp * 32 + lane;
-  const int n = n0 + m;
-  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
-  bool do_epi = true;
-  if (p.splits > 1) {
-    for (int c0 = 0; c0 < p.T; c0 += 16) {
-      float v[16];
-      tmem_ld16(t_row + (uint32_t)c0, v);
+  } else if (warp == 1) {
+    // ---- MMA warp (converged; one elected lane issues every tcgen05 op so commits track them)
+    const uint32_t idesc = idesc_bf16_f32(BM, p.NT);
+    const uint32_t a_off = (uint32_t)(BM * BK * 2) >> 4;       // B-operand tile offset (16 B units)
+    const uint32_t sub_off = (uint32_t)(p.NT * BK * 2) >> 4;   // between activation sub-tiles
+    int i = 0, seg = 0;
+    long long u = u0;
+    int t = (int)(u0 / kb);
+    while (u < u1) {
+      const long long se = min(u1, (long long)(t + 1) * kb);
+      const int b = seg % p.nbuf;
+      mbar_wait(&acce[b], ((uint32_t)(seg / p.nbuf) & 1u) ^ 1u);
+      tc_fence_after();
+      const uint32_t dacc = tmem + (uint32_t)(b * cols);
+      for (long long uu = u; uu < se; ++uu, ++i) {
+        const int s = i % p.stages;
+        const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t dw = sw128_kmajor_desc(smem_u32(smem + (size_t)s * stage_bytes));
+          const uint64_t da = dw + a_off;
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
-        if (c0 + c < p.T) p.partial[((size_t)split * p.T + c0 + c) * p.N + n] = v[c];
+          for (int kk = 0; kk < BK / 16; ++kk)
+            for (int j = 0; j < p.n_sub; ++j)
+              umma_bf16(dacc + (uint32_t)(j * p.NT), dw + (uint64_t)(kk * 2), da + (uint64_t)(j * sub_off + kk * 2),
+                        idesc, (uu > u || kk > 0) ? 1u : 0u);
+          if (s % p.cgrp == p.cgrp - 1) umma_commit(&empty[s]);  // frees slots s-cgrp+1..s
+        }
+        __syncwarp();
+      }
+      if (elect_one()) umma_commit(&accf[b]);
+      __syncwarp();
+      u = se;
+      ++seg;
+      ++t;
     }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int old = atomicAdd(&p.counters[tile_n], 1);
-      const int last = (old == p.splits - 1);
-      if (last) p.counters[tile_n] = 0;  // re-arm for the next launch (stream-ordered)
-      *flag_s = last;
-    }
-    __syncthreads();
-    do_epi = *flag_s != 0;
-    __threadfence();
-  }
-  if (do_epi) {
-    float* xch = reinterpret_cast<float*>(smem);  // stage buffers are idle now
+  } else if (warp >= 4) {
+    // ---- epilogue warps
+    const int ew = warp - 4;
+    const int m = ew * 32 + lane;
+    const int etid = threadIdx.x - 128;
     const bool swiglu = p.epi.mode == EPI_SWIGLU_ACT;
-    for (int c0 = 0; c0 < p.T; c0 += 16) {
-      float v[16];
-      tmem_ld16(t_row + (uint32_t)c0, v);
-      if (p.splits > 1) {
-        float acc[16];
+    int seg = 0;
+    long long u = u0;
+    while (u < u1) {
+      const int t = (int)(u / kb);
+      const long long ts = (long long)t * kb, te = ts + kb;
+      const long long se = min(u1, te);
+      const int b = seg % p.nbuf;
+      mbar_wait_sleep(&accf[b], (uint32_t)(seg / p.nbuf) & 1u);
+      tc_fence_after();
+      const uint32_t t_row = tmem + (uint32_t)(b * cols) + ((uint32_t)(ew * 32) << 16);
+      const int n = t * BM + m;
+      const bool is_full = (u == ts) && (se == te);
+      const bool is_head = (u == ts) && !is_full;
+      if (!is_full && !is_head) {
+        // publish this segment's fp32 partial (slot = this CTA; at most one per CTA)
+        float* dst = p.partial + (size_t)c * p.T * BM;
+        for (int c0 = 0; c0 < p.T; c0 += 16) {
+          float v[16];
+          tmem_ld16(t_row + (uint32_t)c0, v);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) acc[c] = 0.f;
-        for (int s = 0; s < p.splits; ++s) {  // fixed order 0..S-1
+          for (int cc = 0; cc < 16; ++cc)
+            if (c0 + cc < p.T) dst[(size_t)(c0 + cc) * BM + m] = v[cc];
+        }
+        __threadfence();
+        named_sync(1, 128);
+        if (etid == 0) st_release(&p.flags[c], 1);
+      } else {
+        // owners of the other k segments of this tile (they publish them first thing)
+        int c_lo = c + 1, c_hi = c;
+        if (is_head) {
+          const long long ul = te - 1;
+          c_hi = (int)(((ul + 1) * p.G + U - 1) / U) - 1;
+          if (etid == 0)
+            for (int cc = c_lo; cc <= c_hi; ++cc)
+              while (ld_acquire(&p.flags[cc]) == 0) {
+              }
+          named_sync(1, 128);
+        }
+        for (int c0 = 0; c0 < p.T; c0 += 16) {
+          float v[16];
+          tmem_ld16(t_row + (uint32_t)c0, v);
+          for (int cc = c_lo; cc <= c_hi; ++cc) {  // fixed k order
+            const float* src = p.partial + (size_t)cc * p.T * BM;
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            float x = v[c];
-            if (s != split)
-              x = (c0 + c < p.T) ? __ldcg(&p.partial[((size_t)s * p.T + c0 + c) * p.N + n]) : 0.f;
-            acc[c] = (s == 0) ? x : acc[c] + x;
+            for (int q = 0; q < 16; ++q)
+              if (c0 + q < p.T) v[q] += __ldcg(&src[(size_t)(c0 + q) * BM + m]);
+          }
+          if (!swiglu) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (c0 + q < p.T) epi_apply<__nv_bfloat16>(p.epi, c0 + q, n, v[q]);
+          } else {
+            named_sync(1, 128);
+            if (m >= 64) {
+#pragma unroll
+              for (int q = 0; q < 16; ++q) xch[(m - 64) * 17 + q] = v[q];
+            }
+            named_sync(1, 128);
+            if (m < 64) {
+              const int f = t * 64 + m;
+              __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.epi.out);
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                if (c0 + q < p.T)
+                  o[(size_t)(c0 + q) * p.epi.ldo + f] = __float2bfloat16_rn(silu_f(v[q]) * xch[m * 17 + q]);
+            }
           }
         }
-#pragma unroll
-        for (int c = 0; c < 16; ++c) v[c] = acc[c];
-      }
-      if (!swiglu) {
-#pragma unroll
-        for (int c = 0; c < 16; ++c)
-          if (c0 + c < p.T) epi_apply<__nv_bfloat16>(p.epi, c0 + c, n, v[c]);
-      } else {
-        __syncthreads();
-        if (m >= 64) {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) xch[(m - 64) * 17 + c] = v[c];
-        }
-        __syncthreads();
-        if (m < 64) {
-          const int f = tile_n * 64 + m;
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.epi.out);
-#pragma unroll
-          for (int c = 0; c < 16; ++c)
-            if (c0 + c < p.T)
-              o[(size_t)(c0 + c) * p.epi.ldo + f] = __float2bfloat16_rn(silu_f(v[c]) * xch[m * 17 + c]);
+        if (is_head) {
+          named_sync(1, 128);
+          if (etid == 0)
+            for (int cc = c_lo; cc <= c_hi; ++cc) p.flags[cc] = 0;  // re-arm for the next launch
         }
       }
+      tc_fence_before();
+      named_sync(1, 128);
+      if (etid == 0) mbar_arrive(&acce[b]);
+      u = se;
+      ++seg;
     }
   }
   tc_fence_before();
@@ -258,9 +317,10 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
 }
 
 // ------------------------------------------------------------------------ host side
+
+// ------------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static std::once_flag g_once;
-static bool g_attr_set = false;
 
 static bool ensure_encode() {
   std::call_once(g_once, [] {
@@ -284,15 +344,6 @@ static bool make_map(CUtensorMap* m, const void* ptr, int rows, int K, int ld_el
   return r == CUDA_SUCCESS;
 }
 
-int gemm_splits(int N, int K) {
-  const int tiles = N / BM;
-  const int kb = K / BK;
-  if (tiles >= 148) return 1;
-  int s = (int)std::lround(148.0 / tiles);
-  s = std::max(1, std::min(s, kb / 4));
-  return std::max(1, s);
-}
-
 static void tc_shape(int T, int* NT, int* n_sub) {
   const int Tp = std::max(16, (T + 15) / 16 * 16);
   if (Tp <= 256) {
@@ -304,34 +355,100 @@ static void tc_shape(int T, int* NT, int* n_sub) {
   }
 }
 
-int64_t gemm_partial_elems(bool is_bf16, int T, int N, int K) {
-  if (!is_bf16) return 0;
-  const int s = gemm_splits(N, K);
-  return s > 1 ? (int64_t)s * T * N : 0;
-}
-
-static cudaError_t gemm_launch_chunk(bool is_bf16, const void* A, int lda, const void* W, int T, int N, int K,
-                                     const GemmEpi& epi, const GemmScratch& scratch, cudaStream_t st);
-
-// Rows beyond 512 (the two 256-column TMEM accumulators) are processed as independent column
-// chunks; per-element arithmetic is unchanged, so results do not depend on the chunking.
-cudaError_t gemm_launch(bool is_bf16, const void* A, int lda, const void* W, int T, int N, int K,
-                        const GemmEpi& epi, const GemmScratch& scratch, cudaStream_t st) {
-  if (!is_bf16 || T <= 512) return gemm_launch_chunk(is_bf16, A, lda, W, T, N, K, epi, scratch, st);
-  for (int t0 = 0; t0 < T; t0 += 512) {
-    GemmEpi e = epi;
-    const size_t out_elt = (epi.mode == EPI_STORE_ACT || epi.mode == EPI_SWIGLU_ACT) ? 2 : 4;
-    e.out = (char*)epi.out + (size_t)t0 * epi.ldo * out_elt;
-    if (epi.tap) e.tap = epi.tap + (size_t)t0 * epi.ldo;
-    cudaError_t r = gemm_launch_chunk(true, (const char*)A + (size_t)t0 * lda * 2, lda, W, std::min(512, T - t0), N,
-                                      K, e, scratch, st);
-    if (r != cudaSuccess) return r;
+constexpr int kMaxSMs = 160;
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    n = std::min(std::max(n, 1), kMaxSMs);
   }
-  return cudaSuccess;
+  return n;
 }
 
-static cudaError_t gemm_launch_chunk(bool is_bf16, const void* A, int lda, const void* W, int T, int N, int K,
-                                     const GemmEpi& epi, const GemmScratch& scratch, cudaStream_t st) {
+int64_t gemm_partial_elems(bool is_bf16, int T, int N, int K) {
+  (void)N;
+  (void)K;
+  if (!is_bf16) return 0;
+  return (int64_t)kMaxSMs * BM * std::min(T, 512);
+}
+
+// Tile-contiguous weight layout: block (t, k) = rows [128t, +128) x cols [64k, +64) stored as the
+// exact 16 KB shared-memory image of a 128B-swizzled K-major tile (16-byte chunk c of row r at
+// chunk position c ^ (r & 7)); blocks ordered t-major then k. A stream-K range of consecutive
+// (t, k) units is then one contiguous stretch of HBM.
+__global__ void pack_tiled_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst, int K) {
+  const int kb = K / BK;
+  const int blk = blockIdx.x;
+  const int t = blk / kb, k = blk % kb;
+  const int r = threadIdx.x;  // 128 rows
+  const uint4* s = reinterpret_cast<const uint4*>(src + ((size_t)t * BM + r) * K + (size_t)k * BK);
+  uint4* d = reinterpret_cast<uint4*>(dst + (size_t)blk * BM * BK + (size_t)r * BK);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) d[c ^ (r & 7)] = s[c];
+}
+
+cudaError_t gemm_pack_weight(const void* src, void* dst, int N, int K, cudaStream_t st) {
+  if (N % BM || K % BK) return cudaErrorInvalidValue;
+  pack_tiled_kernel<<<(N / BM) * (K / BK), BM, 0, st>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, K);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled, int T, int N, int K,
+                             const GemmEpi& epi, const GemmScratch& scratch, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  SkParams p{};
+  p.T = T;
+  p.N = N;
+  p.K = K;
+  tc_shape(T, &p.NT, &p.n_sub);
+  p.kb_total = K / BK;
+  p.n_tiles = N / BM;
+  const long long U = (long long)p.n_tiles * p.kb_total;
+  p.G = (int)std::min<long long>(num_sms(), U);  // depends on (N, K) only
+  const int cols = p.n_sub * p.NT;
+  p.nbuf = (2 * cols <= 512) ? 2 : 1;
+  p.tmem_cols = 32;
+  while ((int)p.tmem_cols < p.nbuf * cols) p.tmem_cols <<= 1;
+  const int stage_bytes = BM * BK * 2 + p.n_sub * p.NT * BK * 2;
+  // deep ring: ~200 KB in flight per SM covers loaded-HBM latency (Little's law)
+  static const int env_st = getenv("SF_GEMM_STAGES") ? atoi(getenv("SF_GEMM_STAGES")) : 0;
+  p.stages = std::max(2, std::min(16, (216 * 1024) / stage_bytes));
+  if (env_st >= 2 && env_st * stage_bytes <= 216 * 1024) p.stages = env_st;
+  // release slots in groups of cgrp (>= 3 groups in the ring; cgrp divides stages)
+  static const int env_cg = getenv("SF_GEMM_CGRP") ? atoi(getenv("SF_GEMM_CGRP")) : 0;
+  p.cgrp = 1;
+  for (int c = 8; c >= 2; c >>= 1)
+    if (c * 3 <= p.stages || (c * 2 <= p.stages && c == 2)) {
+      p.cgrp = c;
+      break;
+    }
+  if (env_cg >= 1 && env_cg * 2 <= p.stages) p.cgrp = env_cg;
+  p.stages = (p.stages / p.cgrp) * p.cgrp;
+  p.epi = epi;
+  p.partial = scratch.partial;
+  p.flags = scratch.counters;
+  p.w_tiled = w_tiled ? 1 : 0;
+  p.w_tiles = (const __nv_bfloat16*)W;
+  if (!scratch.partial || scratch.partial_elems < (int64_t)p.G * T * BM || scratch.n_counters < p.G)
+    return cudaErrorInvalidValue;
+  const size_t smem = (size_t)p.stages * stage_bytes + 1024 + (2 * p.stages + 4) * 8 + 16 + 64 * 17 * 4;
+  CUtensorMap mw, ma;
+  memset(&mw, 0, sizeof(mw));
+  if (!w_tiled && !make_map(&mw, W, N, K, K, BM)) return cudaErrorInvalidValue;
+  if (!make_map(&ma, A, T, K, lda, p.NT)) return cudaErrorInvalidValue;
+  gemm_sk_kernel<<<p.G, 256, smem, st>>>(mw, ma, p);
+  return cudaGetLastError();
+}
+
+static cudaError_t gemm_launch_chunk(bool is_bf16, const void* A, int lda, const void* W, bool w_tiled, int T,
+                                     int N, int K, const GemmEpi& epi, const GemmScratch& scratch,
+                                     cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
   if (!is_bf16) {
     const int Nout = epi.mode == EPI_SWIGLU_ACT ? N / 2 : N;
@@ -344,47 +461,24 @@ static cudaError_t gemm_launch_chunk(bool is_bf16, const void* A, int lda, const
   }
   if (N % BM || K % BK || T > 512) return cudaErrorInvalidValue;
   if (!ensure_encode()) return cudaErrorNotSupported;
-  TcParams p{};
-  p.T = T;
-  p.N = N;
-  p.K = K;
-  tc_shape(T, &p.NT, &p.n_sub);
-  p.kb_total = K / BK;
-  p.splits = gemm_splits(N, K);
-  p.epi = epi;
-  p.partial = scratch.partial;
-  p.counters = scratch.counters;
-  if (p.splits > 1) {
-    if (!scratch.partial || scratch.partial_elems < (int64_t)p.splits * T * N || !scratch.counters ||
-        scratch.n_counters < N / BM)
-      return cudaErrorInvalidValue;
+  return launch_sk(A, lda, W, w_tiled, T, N, K, epi, scratch, st);
+}
+
+// Rows beyond 512 (the TMEM accumulator capacity) are processed as independent column chunks;
+// per-element arithmetic is unchanged, so results do not depend on the chunking.
+cudaError_t gemm_launch(bool is_bf16, const void* A, int lda, const void* W, bool w_tiled, int T, int N, int K,
+                        const GemmEpi& epi, const GemmScratch& scratch, cudaStream_t st) {
+  if (!is_bf16 || T <= 512) return gemm_launch_chunk(is_bf16, A, lda, W, w_tiled, T, N, K, epi, scratch, st);
+  for (int t0 = 0; t0 < T; t0 += 512) {
+    GemmEpi e = epi;
+    const size_t out_elt = (epi.mode == EPI_STORE_ACT || epi.mode == EPI_SWIGLU_ACT) ? 2 : 4;
+    e.out = (char*)epi.out + (size_t)t0 * epi.ldo * out_elt;
+    if (epi.tap) e.tap = epi.tap + (size_t)t0 * epi.ldo;
+    cudaError_t r = gemm_launch_chunk(true, (const char*)A + (size_t)t0 * lda * 2, lda, W, w_tiled,
+                                      std::min(512, T - t0), N, K, e, scratch, st);
+    if (r != cudaSuccess) return r;
   }
-  const int cols = p.n_sub * p.NT;
-  p.tmem_cols = 32;
-  while ((int)p.tmem_cols < cols) p.tmem_cols <<= 1;
-  const int stage_bytes = BM * BK * 2 + p.n_sub * p.NT * BK * 2;
-  // Size the ring so that every CTA of the launch is resident at once (no tail wave): a
-  // memory-bound launch then shares HBM evenly across all its weight streams.
-  const int ctas = (N / BM) * p.splits;
-  int per_sm = std::min(4, (ctas + 147) / 148);
-  int stages = 0;
-  for (; per_sm >= 1; --per_sm) {
-    const int budget = (226 * 1024) / per_sm - 2048;
-    stages = std::min(8, budget / stage_bytes);
-    if (stages >= 3 || per_sm == 1) break;
-  }
-  p.stages = std::max(2, stages);
-  const size_t smem = (size_t)p.stages * stage_bytes + 1024 + (2 * p.stages + 1) * 8 + 16;
-  if (!g_attr_set) {
-    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    g_attr_set = true;
-  }
-  CUtensorMap mw, ma;
-  if (!make_map(&mw, W, N, K, K, BM)) return cudaErrorInvalidValue;
-  if (!make_map(&ma, A, T, K, lda, p.NT)) return cudaErrorInvalidValue;
-  dim3 grid(N / BM, p.splits);
-  gemm_tc_kernel<<<grid, 128, smem, st>>>(mw, ma, p);
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 }  // namespace sf

@@ -29,15 +29,14 @@ struct GemmScratch {
   int n_counters = 0;
 };
 
-// Number of K splits used for an (N, K) weight: a function of the weight shape ONLY, so every
-// output element has the same reduction order for any row count T (batch invariance, C23).
-int gemm_splits(int N, int K);
-
 // out = A[T, K] . W[N, K]^T with fp32 accumulation.
-// is_bf16: A, W bf16 (tcgen05 path, requires N % 128 == 0, K % 64 == 0, T <= 512);
-// otherwise fp32 (SIMT path). act outputs are in the same dtype as A.
-cudaError_t gemm_launch(bool is_bf16, const void* A, int lda, const void* W, int T, int N, int K,
+// is_bf16: A, W bf16 (tcgen05 path, requires N % 128 == 0, K % 64 == 0); W either row-major
+// [N, K] (w_tiled = false) or in the tile-contiguous layout written by gemm_pack_weight.
+// Otherwise fp32 (SIMT path, W row-major). act outputs are in the same dtype as A.
+cudaError_t gemm_launch(bool is_bf16, const void* A, int lda, const void* W, bool w_tiled, int T, int N, int K,
                         const GemmEpi& epi, const GemmScratch& scratch, cudaStream_t s);
+// Row-major bf16 W[N, K] -> tile-contiguous 128x64 pre-swizzled layout (same byte count).
+cudaError_t gemm_pack_weight(const void* src, void* dst, int N, int K, cudaStream_t s);
 
 // scratch floats needed by gemm_launch for (T, N, K)
 int64_t gemm_partial_elems(bool is_bf16, int T, int N, int K);

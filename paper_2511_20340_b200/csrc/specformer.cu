@@ -297,7 +297,7 @@ static cudaError_t gemm(sf_handle* h, const void* A, int lda, const void* W, int
   sc.counters = h->gcnt;
   sc.n_counters = 4096;
   h->launches += (T + 511) / 512;
-  return gemm_launch(h->bf, A, lda, W, T, N, K, epi, sc, h->st);
+  return gemm_launch(h->bf, A, lda, W, h->bf, T, N, K, epi, sc, h->st);
 }
 static GemmEpi epi_act(void* out, int ldo) {
   GemmEpi e;
@@ -505,6 +505,7 @@ int sf_weight_table(const sf_config* cfg, sf_tensor_desc* out, int cap) {
       for (int j = 0; j < d.ndim; ++j) d.shape[j] = specs[i].shape[j];
       d.offset_bytes = off;
       d.dtype = (specs[i].matrix && cfg->dtype == SF_BF16) ? SF_BF16 : SF_FP32;
+      d.layout = (specs[i].matrix && cfg->dtype == SF_BF16 && specs[i].name != "embed") ? 1 : 0;
     }
     off += align_up(tensor_bytes(cfg, specs[i]));
   }
@@ -932,12 +933,15 @@ sf_status sf_profile_read(sf_handle* h, int32_t cls, double* total_ms, int64_t* 
 sf_status sf_test_gemm(int32_t dtype, const void* A, const void* W, float* out, int32_t T, int32_t N, int32_t K,
                        void* stream) {
   if (!A || !W || !out || T < 1 || N < 1 || K < 1) return SF_ERR_ARG;
-  const bool bf = dtype == SF_BF16;
+  const bool pretiled = dtype == 2;  // bf16 W already in layout 1 (sf_pack_matrix)
+  const bool bf = dtype == SF_BF16 || pretiled;
   cudaStream_t st = (cudaStream_t)stream;
-  // test-only scratch, grown on demand and kept (counters stay zeroed: kernels re-arm them)
+  // test-only scratch, grown on demand and kept (flags stay zeroed: kernels re-arm them)
   static float* partial = nullptr;
   static int64_t partial_cap = 0;
   static int* counters = nullptr;
+  static void* wt = nullptr;
+  static int64_t wt_cap = 0;
   const int64_t pe = gemm_partial_elems(bf, std::min(T, 512), N, K);
   if (pe > partial_cap) {
     if (partial) cudaFree(partial);
@@ -948,6 +952,17 @@ sf_status sf_test_gemm(int32_t dtype, const void* A, const void* W, float* out, 
     if (cudaMalloc((void**)&counters, 4096 * 4) != cudaSuccess) return SF_ERR_CUDA;
     cudaMemset(counters, 0, 4096 * 4);
   }
+  const void* Wuse = W;
+  if (bf && !pretiled) {  // the hot path stores bf16 weights tile-contiguous: pack into scratch
+    const int64_t wb = (int64_t)N * K * 2;
+    if (wb > wt_cap) {
+      if (wt) cudaFree(wt);
+      if (cudaMalloc(&wt, wb) != cudaSuccess) return SF_ERR_CUDA;
+      wt_cap = wb;
+    }
+    if (gemm_pack_weight(W, wt, N, K, st) != cudaSuccess) return SF_ERR_ARG;
+    Wuse = wt;
+  }
   GemmScratch sc;
   sc.partial = partial;
   sc.partial_elems = partial_cap;
@@ -957,7 +972,13 @@ sf_status sf_test_gemm(int32_t dtype, const void* A, const void* W, float* out, 
   e.mode = EPI_STORE_F32;
   e.out = out;
   e.ldo = N;
-  return gemm_launch(bf, A, K, W, T, N, K, e, sc, st) == cudaSuccess ? SF_OK : SF_ERR_CUDA;
+  return gemm_launch(bf, A, K, Wuse, bf, T, N, K, e, sc, st) == cudaSuccess ? SF_OK : SF_ERR_CUDA;
+}
+
+sf_status sf_pack_matrix(int32_t dtype, const void* src_dev, void* dst_dev, int64_t N, int64_t K, void* stream) {
+  if (!src_dev || !dst_dev || N < 1 || K < 1) return SF_ERR_ARG;
+  if (dtype != SF_BF16) return SF_ERR_UNSUPPORTED;
+  return gemm_pack_weight(src_dev, dst_dev, (int)N, (int)K, (cudaStream_t)stream) == cudaSuccess ? SF_OK : SF_ERR_SHAPE;
 }
 
 }  // extern "C"

@@ -55,7 +55,7 @@ def weight_table(cfg: EngineConfig):
         raise N.SpecFormerError(N.SF_ERR_ARG, "invalid config")
     arr = (N.sf_tensor_desc * n)()
     lib.sf_weight_table(C.byref(c), arr, n)
-    return [(d.name.decode(), tuple(d.shape[: d.ndim]), d.offset_bytes, d.dtype) for d in arr]
+    return [(d.name.decode(), tuple(d.shape[: d.ndim]), d.offset_bytes, d.dtype, d.layout) for d in arr]
 
 
 def _interleave_gu(gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
@@ -77,17 +77,28 @@ def _source_tensor(name: str, w: dict) -> torch.Tensor:
 
 
 def pack_weights(cfg: EngineConfig, weights: dict, device="cuda") -> torch.Tensor:
+    """Copy the caller's tensors into the packed blob; layout-1 matrices go through the library's
+    sf_pack_matrix kernel (tile-contiguous GEMM layout)."""
     lib = N.lib()
     c = cfg.to_c()
     nbytes = lib.sf_weights_bytes(C.byref(c))
     blob = torch.empty(nbytes, dtype=torch.uint8, device=device)
-    for name, shape, off, dt in weight_table(cfg):
+    stream = torch.cuda.current_stream(device)
+    for name, shape, off, dt, layout in weight_table(cfg):
         t = _source_tensor(name, weights)
         tdtype = torch.bfloat16 if dt == N.SF_BF16 else torch.float32
         if tuple(t.shape) != shape:
             raise ValueError(f"{name}: expected {shape}, got {tuple(t.shape)}")
         n = t.numel() * (2 if dt == N.SF_BF16 else 4)
-        blob[off: off + n].view(tdtype).view(shape).copy_(t.to(device=device, dtype=tdtype))
+        src = t.to(device=device, dtype=tdtype).contiguous()
+        if layout == 1:
+            st = lib.sf_pack_matrix(dt, C.c_void_p(src.data_ptr()), C.c_void_p(blob.data_ptr() + off), shape[0],
+                                    shape[1], C.c_void_p(stream.cuda_stream))
+            if st != N.SF_OK:
+                raise N.SpecFormerError(st, f"sf_pack_matrix({name})")
+            torch.cuda.current_stream(device).synchronize()  # src may be freed after this iteration
+        else:
+            blob[off: off + n].view(tdtype).view(shape).copy_(src)
     return blob
 
 
@@ -225,13 +236,24 @@ class Engine:
             pass
 
 
-def run_gemm(A: torch.Tensor, W: torch.Tensor, stream=None) -> torch.Tensor:
-    """out[T,N] = A[T,K] W[N,K]^T through the hot path's GEMM kernels (T-kernel parity hook)."""
+def pack_matrix(W: torch.Tensor) -> torch.Tensor:
+    """Row-major bf16 W[N, K] (device) -> layout-1 copy (same shape/bytes, tile-contiguous)."""
+    out = torch.empty_like(W)
+    st = N.lib().sf_pack_matrix(N.SF_BF16, _ptr(W.contiguous()), _ptr(out), W.shape[0], W.shape[1],
+                                C.c_void_p(torch.cuda.current_stream(W.device).cuda_stream))
+    if st != N.SF_OK:
+        raise N.SpecFormerError(st, "sf_pack_matrix")
+    return out
+
+
+def run_gemm(A: torch.Tensor, W: torch.Tensor, stream=None, w_tiled: bool = False) -> torch.Tensor:
+    """out[T,N] = A[T,K] W[N,K]^T through the hot path's GEMM kernels (T-kernel parity hook).
+    w_tiled: W was produced by pack_matrix."""
     lib = N.lib()
     T, K = A.shape
     Nn = W.shape[0]
     out = torch.empty(T, Nn, dtype=torch.float32, device=A.device)
-    dt = N.SF_BF16 if A.dtype == torch.bfloat16 else N.SF_FP32
+    dt = (2 if w_tiled else N.SF_BF16) if A.dtype == torch.bfloat16 else N.SF_FP32
     s = stream or torch.cuda.current_stream(A.device)
     st = lib.sf_test_gemm(dt, _ptr(A.contiguous()), _ptr(W.contiguous()), _ptr(out), T, Nn, K,
                           C.c_void_p(s.cuda_stream))

@@ -49,7 +49,8 @@ def test_weight_table_layout(lib, name):
     esz = 2 if m.dtype == "bf16" else 4
     prev_end = 0
     n_params = 0
-    for nm, shape, off, dt in tab:
+    for nm, shape, off, dt, layout in tab:
+        assert layout == (1 if (dt == N.SF_BF16 and nm != 'embed') else 0)
         assert off % 256 == 0 and off >= prev_end
         n = 1
         for s in shape:

@@ -2,7 +2,7 @@
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-from paper_2511_20340_b200 import run_gemm
+from paper_2511_20340_b200.engine import run_gemm, pack_matrix
 
 shapes = {"qkv": (12288, 4096), "o": (4096, 4096), "gu": (22016, 4096), "down": (4096, 11008), "lm": (32000, 4096)}
 Ts = [int(x) for x in os.environ.get("TS", "5,80,320").split(",")]
@@ -12,16 +12,16 @@ res = {}
 for name, (N, K) in shapes.items():
     if only and name not in only.split(","):
         continue
-    W = (0.02 * torch.randn(N, K, device="cuda")).to(torch.bfloat16)
+    W = pack_matrix((0.02 * torch.randn(N, K, device="cuda")).to(torch.bfloat16))
     for T in Ts:
         A = torch.randn(T, K, device="cuda").to(torch.bfloat16)
         for _ in range(3):
-            run_gemm(A, W)
+            run_gemm(A, W, w_tiled=True)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record()
         for _ in range(iters):
-            run_gemm(A, W)
+            run_gemm(A, W, w_tiled=True)
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / iters
         by = N * K * 2 + T * K * 2 + T * N * 4
