@@ -114,12 +114,11 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 
   if (warp == 0) {
     // ---- TMA producer warp (converged; one elected lane issues)
-    int i = 0;
     int t = (int)(u0 / kb), k = (int)(u0 % kb);
-    for (long long u = u0; u < u1; ++u, ++i) {
-      const int s = i % p.stages;
-      const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
-      mbar_wait(&empty[(s / p.cgrp) * p.cgrp + p.cgrp - 1], ph ^ 1u);  // slot group released
+    int s = 0, grp_last = p.cgrp - 1;  // ring slot and the last slot of its release group
+    uint32_t ph = 0;
+    for (long long u = u0; u < u1; ++u) {
+      mbar_wait(&empty[grp_last], ph ^ 1u);  // slot group released
       if (elect_one()) {
         uint8_t* st = smem + (size_t)s * stage_bytes;
         mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
@@ -135,6 +134,12 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         k = 0;
         ++t;
       }
+      if (++s == p.stages) {
+        s = 0;
+        ph ^= 1u;
+      }
+      if (s > grp_last) grp_last += p.cgrp;
+      if (s == 0) grp_last = p.cgrp - 1;
     }
   } else if (warp == 1) {
     // ---- MMA warp (converged; one elected lane issues every tcgen05 op so commits track them)
@@ -142,18 +147,33 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     const uint32_t a_off = (uint32_t)(BM * BK * 2) >> 4;       // B-operand tile offset (16 B units)
     const uint32_t sub_off = (uint32_t)(p.NT * BK * 2) >> 4;   // between activation sub-tiles
     int i = 0, seg = 0;
+    int s = 0, gcnt = 0;
+    uint32_t ph = 0;
     long long u = u0;
     int t = (int)(u0 / kb);
+#ifdef SF_GEMM_PROFILE
+    long long tm0 = clock64(), twf = 0, twa = 0;
+#endif
     while (u < u1) {
       const long long se = min(u1, (long long)(t + 1) * kb);
       const int b = seg % p.nbuf;
+#ifdef SF_GEMM_PROFILE
+      long long ta = clock64();
+#endif
       mbar_wait(&acce[b], ((uint32_t)(seg / p.nbuf) & 1u) ^ 1u);
+#ifdef SF_GEMM_PROFILE
+      twa += clock64() - ta;
+#endif
       tc_fence_after();
       const uint32_t dacc = tmem + (uint32_t)(b * cols);
       for (long long uu = u; uu < se; ++uu, ++i) {
-        const int s = i % p.stages;
-        const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
+#ifdef SF_GEMM_PROFILE
+        long long tf = clock64();
+#endif
         mbar_wait(&full[s], ph);
+#ifdef SF_GEMM_PROFILE
+        twf += clock64() - tf;
+#endif
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dw = sw128_kmajor_desc(smem_u32(smem + (size_t)s * stage_bytes));
@@ -163,9 +183,14 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
             for (int j = 0; j < p.n_sub; ++j)
               umma_bf16(dacc + (uint32_t)(j * p.NT), dw + (uint64_t)(kk * 2), da + (uint64_t)(j * sub_off + kk * 2),
                         idesc, (uu > u || kk > 0) ? 1u : 0u);
-          if (s % p.cgrp == p.cgrp - 1) umma_commit(&empty[s]);  // frees slots s-cgrp+1..s
+          if (++gcnt == p.cgrp) umma_commit(&empty[s]);  // frees slots s-cgrp+1..s
         }
         __syncwarp();
+        if (gcnt == p.cgrp) gcnt = 0;
+        if (++s == p.stages) {
+          s = 0;
+          ph ^= 1u;
+        }
       }
       if (elect_one()) umma_commit(&accf[b]);
       __syncwarp();
@@ -173,6 +198,11 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       ++seg;
       ++t;
     }
+#ifdef SF_GEMM_PROFILE
+    if (lane == 0 && (c == 0 || c == p.G / 2))
+      printf("T=%d cta %d: %d kb, %.0f cyc/kb total, wait-full %.0f/kb, wait-acc %lld\n", p.T, c, i,
+             (double)(clock64() - tm0) / max(i, 1), (double)twf / max(i, 1), twa);
+#endif
   } else if (warp >= 4) {
     // ---- epilogue warps
     const int ew = warp - 4;
