@@ -94,9 +94,9 @@ typedef struct sf_handle sf_handle;
  * lm_head[V,d]; sf.group_scale[4,d] f32; sf.w_d[d,4d]; sf.ctx_norm[d] f32; sf.ctx_wqkv;
  * sf.ctx_wo; sf.pos_norm[d] f32; sf.w_p[k d, d]; sf.b_p[k d] f32; sf.blk_attn_norm[d] f32;
  * sf.blk_wqkv; sf.blk_wo; sf.blk_ffn_norm[d] f32; sf.blk_w_gu[2F,d]; sf.blk_w_down[d,F].
- * w_gu interleaves the SwiGLU gate and up projections in 64-row groups: rows [128i, 128i+64)
- * are gate rows [64i, 64i+64) and rows [128i+64, 128i+128) are up rows [64i, 64i+64)
- * (F % 64 == 0), so one GEMM tile holds matching gate/up rows for the fused SwiGLU epilogue.
+ * w_gu interleaves the SwiGLU gate and up projections row by row: row 2i is gate row i, row
+ * 2i+1 is up row i, so a GEMM tile holds matching gate/up rows in adjacent accumulator lanes
+ * for the fused SwiGLU epilogue (F % 64 == 0).
  * Matrices are stored in the config dtype, vectors in fp32. In bf16 mode every matrix except
  * `embed` uses layout 1: fill it with sf_pack_matrix from a row-major device copy. */
 int sf_weight_table(const sf_config* cfg, sf_tensor_desc* out, int cap);

@@ -45,23 +45,26 @@ SF_DEV float silu_f(float g) { return g / (1.f + expf(-g)); }
 
 // ------------------------------------------------------------------------ tcgen05 kernel
 // ------------------------------------------------------------------------ persistent stream-K kernel
-// Grid = G CTAs (G = min(#SMs, units), a function of (N, K) only). The (128-row tile, 64-wide
-// k-block) units of the whole GEMM are split into G contiguous equal ranges, so every SM streams
-// the same number of weight bytes (no wave quantisation). A tile cut between CTAs is finished by
-// the CTA owning its k = 0 segment, which adds the other segments' fp32 partials in k order:
-// segment boundaries depend only on (N, K, G) -> the same rounding for every T (batch invariance).
-// Warps: 0 = TMA producer, 1 = MMA issuer, 2 = TMEM allocator, 4..7 = epilogue (TMEM lanes 32(w-4)..).
-// Two TMEM accumulator buffers (when they fit) let the epilogue of one segment overlap the MMAs
+// Work groups: CG = 1 (one CTA, M = 128 weight rows per MMA) or CG = 2 (a cluster pair issuing
+// tcgen05.mma.cta_group::2, M = 256: each CTA stages its own 128 weight rows and HALF of the
+// activation tile; the leader CTA issues every MMA, commits multicast to both CTAs). G work groups
+// (a function of (N, K) only) split the (256/128-row tile, 64-wide k-block) units of the whole GEMM
+// into G contiguous equal ranges, so every SM streams the same number of weight bytes (no wave
+// quantisation). A tile cut between groups is finished by the group owning its k = 0 segment,
+// which adds the other segments' fp32 partials in k order: segment boundaries depend only on
+// (N, K, G) -> the same rounding for every T (batch invariance, reading C23).
+// Warps: 0 = TMA producer, 1 = MMA issuer (leader CTA), 2 = TMEM allocator, 4..7 = epilogue.
+// Two TMEM accumulator buffers (when they fit) overlap the epilogue of one segment with the MMAs
 // of the next.
 struct SkParams {
   int T, N, K;
   int NT, n_sub, stages, kb_total, n_tiles, G, nbuf, w_tiled;
-  int cgrp;  // ring slots released per tcgen05.commit (a commit drains the tensor pipe)
+  int cgrp;  // ring slots released per tcgen05.commit
   uint32_t tmem_cols;
-  const __nv_bfloat16* w_tiles;  // tile-contiguous weights (w_tiled)
+  const __nv_bfloat16* w_tiles;  // tile-contiguous weights (w_tiled, CG == 1 bulk path)
   GemmEpi epi;
-  float* partial;  // [G][T][128]
-  int* flags;      // [G]
+  float* partial;  // [CTAs][T][128]
+  int* flags;      // [CTAs]
 };
 
 SF_DEV void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -71,44 +74,97 @@ SF_DEV int ld_acquire(const int* p) {
   return v;
 }
 SF_DEV void st_release(int* p, int v) { asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
+SF_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+SF_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the mbarrier at the same shared offset in CTA `rank` of the cluster
+SF_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
+// 2-SM TMA: data lands in this CTA's smem, transaction bytes are credited to the LEADER's barrier
+SF_DEV void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+SF_DEV void umma_bf16_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+SF_DEV void umma_commit_2sm(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
 
-__global__ void __launch_bounds__(256, 1)
+template <int CG>
+__global__ void __launch_bounds__(384, 1)
 gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA, const SkParams p) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
-  const int a_bytes = p.n_sub * p.NT * BK * 2;
+  const int a_rows = p.NT / CG;  // activation rows of each sub-tile staged by this CTA
+  const int a_bytes = p.n_sub * a_rows * BK * 2;
   const int stage_bytes = BM * BK * 2 + a_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * stage_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* accf = empty + p.stages;  // [2]
   uint64_t* acce = accf + 2;          // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
-  float* xch = reinterpret_cast<float*>(tmem_slot + 4);  // [64][17] SwiGLU exchange
-
+  
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x;
+  const uint32_t rank = (CG == 2) ? cluster_rank() : 0u;
+  const int c = blockIdx.x / CG;       // work group
+  const int slot = blockIdx.x;         // partial / flag slot of this CTA
   const int kb = p.kb_total;
   const long long U = (long long)p.n_tiles * kb;
   const long long u0 = U * c / p.G, u1 = U * (c + 1) / p.G;
   const int cols = p.n_sub * p.NT;
 
   if (threadIdx.x == 0) {
-    if (!p.w_tiled) prefetch_tmap(&tmW);
+    if (!(CG == 1 && p.w_tiled)) prefetch_tmap(&tmW);
     prefetch_tmap(&tmA);
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], CG);  // leader: own arrive_expect_tx (+ the peer's forwarded arrival)
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
-      mbar_init(&acce[b], 1);
+      mbar_init(&acce[b], CG);  // leader: both CTAs' epilogues release the accumulator
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
+  if (warp == 2) {
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(p.tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      tmem_alloc(tmem_slot, p.tmem_cols);
+    }
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -121,13 +177,23 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       mbar_wait(&empty[grp_last], ph ^ 1u);  // slot group released
       if (elect_one()) {
         uint8_t* st = smem + (size_t)s * stage_bytes;
-        mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
-        if (p.w_tiled)  // tile-contiguous, pre-swizzled weights: one 16 KB bulk copy per stage
-          bulk_load(st, p.w_tiles + ((size_t)t * kb + k) * (BM * BK), BM * BK * 2, &full[s], kEvictFirst);
-        else
-          tma_load_2d(st, &tmW, &full[s], k * BK, t * BM, kEvictFirst);
-        for (int j = 0; j < p.n_sub; ++j)
-          tma_load_2d(st + BM * BK * 2 + j * p.NT * BK * 2, &tmA, &full[s], k * BK, j * p.NT, kEvictLast);
+        if constexpr (CG == 1) {
+          mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
+          if (p.w_tiled)  // tile-contiguous, pre-swizzled weights: one 16 KB bulk copy per stage
+            bulk_load(st, p.w_tiles + ((size_t)t * kb + k) * (BM * BK), BM * BK * 2, &full[s], kEvictFirst);
+          else
+            tma_load_2d(st, &tmW, &full[s], k * BK, t * BM, kEvictFirst);
+          for (int j = 0; j < p.n_sub; ++j)
+            tma_load_2d(st + BM * BK * 2 + j * a_rows * BK * 2, &tmA, &full[s], k * BK, j * p.NT, kEvictLast);
+        } else {
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * stage_bytes));
+          // tiled weights viewed as a [blocks*128, 64] tensor: this CTA's 128-row half of pair tile t
+          tma_load_2d_2sm(st, &tmW, &full[s], 0, ((t * 2 + (int)rank) * kb + k) * BM, kEvictFirst);
+          for (int j = 0; j < p.n_sub; ++j)
+            tma_load_2d_2sm(st + BM * BK * 2 + j * a_rows * BK * 2, &tmA, &full[s], k * BK,
+                            j * p.NT + (int)rank * a_rows, kEvictLast);
+          if (rank != 0) mbar_arrive_remote(&full[s], 0);
+        }
       }
       __syncwarp();
       if (++k == kb) {
@@ -141,49 +207,42 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       if (s > grp_last) grp_last += p.cgrp;
       if (s == 0) grp_last = p.cgrp - 1;
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && rank == 0) {
     // ---- MMA warp (converged; one elected lane issues every tcgen05 op so commits track them)
-    const uint32_t idesc = idesc_bf16_f32(BM, p.NT);
-    const uint32_t a_off = (uint32_t)(BM * BK * 2) >> 4;       // B-operand tile offset (16 B units)
-    const uint32_t sub_off = (uint32_t)(p.NT * BK * 2) >> 4;   // between activation sub-tiles
-    int i = 0, seg = 0;
+    const uint32_t idesc = idesc_bf16_f32(BM * CG, p.NT);
+    const uint32_t a_off = (uint32_t)(BM * BK * 2) >> 4;           // B-operand tile offset (16 B units)
+    const uint32_t sub_off = (uint32_t)(a_rows * BK * 2) >> 4;     // between activation sub-tiles
+    int seg = 0;
     int s = 0, gcnt = 0;
     uint32_t ph = 0;
     long long u = u0;
     int t = (int)(u0 / kb);
-#ifdef SF_GEMM_PROFILE
-    long long tm0 = clock64(), twf = 0, twa = 0;
-#endif
     while (u < u1) {
       const long long se = min(u1, (long long)(t + 1) * kb);
       const int b = seg % p.nbuf;
-#ifdef SF_GEMM_PROFILE
-      long long ta = clock64();
-#endif
       mbar_wait(&acce[b], ((uint32_t)(seg / p.nbuf) & 1u) ^ 1u);
-#ifdef SF_GEMM_PROFILE
-      twa += clock64() - ta;
-#endif
       tc_fence_after();
       const uint32_t dacc = tmem + (uint32_t)(b * cols);
-      for (long long uu = u; uu < se; ++uu, ++i) {
-#ifdef SF_GEMM_PROFILE
-        long long tf = clock64();
-#endif
+      for (long long uu = u; uu < se; ++uu) {
         mbar_wait(&full[s], ph);
-#ifdef SF_GEMM_PROFILE
-        twf += clock64() - tf;
-#endif
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dw = sw128_kmajor_desc(smem_u32(smem + (size_t)s * stage_bytes));
           const uint64_t da = dw + a_off;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
-            for (int j = 0; j < p.n_sub; ++j)
-              umma_bf16(dacc + (uint32_t)(j * p.NT), dw + (uint64_t)(kk * 2), da + (uint64_t)(j * sub_off + kk * 2),
-                        idesc, (uu > u || kk > 0) ? 1u : 0u);
-          if (++gcnt == p.cgrp) umma_commit(&empty[s]);  // frees slots s-cgrp+1..s
+            for (int j = 0; j < p.n_sub; ++j) {
+              if constexpr (CG == 1)
+                umma_bf16(dacc + (uint32_t)(j * p.NT), dw + (uint64_t)(kk * 2), da + (uint64_t)(j * sub_off + kk * 2),
+                          idesc, (uu > u || kk > 0) ? 1u : 0u);
+              else
+                umma_bf16_2sm(dacc + (uint32_t)(j * p.NT), dw + (uint64_t)(kk * 2),
+                              da + (uint64_t)(j * sub_off + kk * 2), idesc, (uu > u || kk > 0) ? 1u : 0u);
+            }
+          if (++gcnt == p.cgrp) {  // frees slots s-cgrp+1..s (in both CTAs of a pair)
+            if constexpr (CG == 1) umma_commit(&empty[s]);
+            else umma_commit_2sm(&empty[s]);
+          }
         }
         __syncwarp();
         if (gcnt == p.cgrp) gcnt = 0;
@@ -192,23 +251,22 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           ph ^= 1u;
         }
       }
-      if (elect_one()) umma_commit(&accf[b]);
+      if (elect_one()) {
+        if constexpr (CG == 1) umma_commit(&accf[b]);
+        else umma_commit_2sm(&accf[b]);
+      }
       __syncwarp();
       u = se;
       ++seg;
       ++t;
     }
-#ifdef SF_GEMM_PROFILE
-    if (lane == 0 && (c == 0 || c == p.G / 2))
-      printf("T=%d cta %d: %d kb, %.0f cyc/kb total, wait-full %.0f/kb, wait-acc %lld\n", p.T, c, i,
-             (double)(clock64() - tm0) / max(i, 1), (double)twf / max(i, 1), twa);
-#endif
   } else if (warp >= 4) {
-    // ---- epilogue warps
-    const int ew = warp - 4;
-    const int m = ew * 32 + lane;
-    const int etid = threadIdx.x - 128;
-    const bool swiglu = p.epi.mode == EPI_SWIGLU_ACT;
+    // ---- epilogue: 8 warps, two per TMEM lane quadrant (warp w reads lanes 32 (w % 4) ..);
+    // the two warps of a quadrant take alternate 32-column chunks.
+    const int quad = warp & 3, half = (warp - 4) >> 2;
+    const int m = quad * 32 + lane;
+    const int etid = threadIdx.x - 128;  // 0..255
+    const int mode = p.epi.mode;
     int seg = 0;
     long long u = u0;
     while (u < u1) {
@@ -217,83 +275,146 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       const long long se = min(u1, te);
       const int b = seg % p.nbuf;
       mbar_wait_sleep(&accf[b], (uint32_t)(seg / p.nbuf) & 1u);
+#ifdef SF_GEMM_PROFILE
+      const long long te0 = clock64();
+#endif
       tc_fence_after();
-      const uint32_t t_row = tmem + (uint32_t)(b * cols) + ((uint32_t)(ew * 32) << 16);
-      const int n = t * BM + m;
+      const uint32_t t_row = tmem + (uint32_t)(b * cols) + ((uint32_t)(quad * 32) << 16);
+      const int vt = t * CG + (int)rank;  // 128-row tile index of this CTA's rows
+      const int n = vt * BM + m;
       const bool is_full = (u == ts) && (se == te);
       const bool is_head = (u == ts) && !is_full;
-      if (!is_full && !is_head) {
-        // publish this segment's fp32 partial (slot = this CTA; at most one per CTA)
-        float* dst = p.partial + (size_t)c * p.T * BM;
-        for (int c0 = 0; c0 < p.T; c0 += 16) {
-          float v[16];
-          tmem_ld16(t_row + (uint32_t)c0, v);
+      if (mode == EPI_PARTIAL) {
+        // every segment -> slot 2 * group + (first segment of the range ? 0 : 1) (one 128-row half
+        // per CTA of a pair); reduced later, in k order, by the consumer
+        float* dst = p.partial + ((size_t)(2 * c + (u == u0 ? 0 : 1)) * CG + (int)rank) * p.T * BM + m;
+        for (int c0 = half * 32; c0 < p.T; c0 += 64) {
+          uint32_t r[32];
+          tmem_ld32_async(t_row + (uint32_t)c0, r);
+          tmem_ld_wait();
 #pragma unroll
-          for (int cc = 0; cc < 16; ++cc)
-            if (c0 + cc < p.T) dst[(size_t)(c0 + cc) * BM + m] = v[cc];
+          for (int cc = 0; cc < 32; ++cc)
+            if (c0 + cc < p.T) dst[(size_t)(c0 + cc) * BM] = __uint_as_float(r[cc]);
+        }
+      } else if (!is_full && !is_head) {
+        // publish this segment's fp32 partial (slot = this CTA; at most one per CTA)
+        float* dst = p.partial + (size_t)slot * p.T * BM + m;
+        for (int c0 = half * 32; c0 < p.T; c0 += 64) {
+          uint32_t r[32];
+          tmem_ld32_async(t_row + (uint32_t)c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int cc = 0; cc < 32; ++cc)
+            if (c0 + cc < p.T) dst[(size_t)(c0 + cc) * BM] = __uint_as_float(r[cc]);
         }
         __threadfence();
-        named_sync(1, 128);
-        if (etid == 0) st_release(&p.flags[c], 1);
+        named_sync(1, 256);
+        if (etid == 0) st_release(&p.flags[slot], 1);
       } else {
-        // owners of the other k segments of this tile (they publish them first thing)
+        // groups owning the other k segments of this tile (they publish them first thing)
         int c_lo = c + 1, c_hi = c;
         if (is_head) {
           const long long ul = te - 1;
           c_hi = (int)(((ul + 1) * p.G + U - 1) / U) - 1;
           if (etid == 0)
             for (int cc = c_lo; cc <= c_hi; ++cc)
-              while (ld_acquire(&p.flags[cc]) == 0) {
+              while (ld_acquire(&p.flags[cc * CG + (int)rank]) == 0) {
               }
-          named_sync(1, 128);
+          named_sync(1, 256);
         }
-        for (int c0 = 0; c0 < p.T; c0 += 16) {
-          float v[16];
-          tmem_ld16(t_row + (uint32_t)c0, v);
+        for (int c0 = half * 32; c0 < p.T; c0 += 64) {
+          uint32_t r[32];
+          tmem_ld32_async(t_row + (uint32_t)c0, r);
+          tmem_ld_wait();
+          float v[32];
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
           for (int cc = c_lo; cc <= c_hi; ++cc) {  // fixed k order
-            const float* src = p.partial + (size_t)cc * p.T * BM;
+            const float* src = p.partial + (size_t)(cc * CG + (int)rank) * p.T * BM + m;
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-              if (c0 + q < p.T) v[q] += __ldcg(&src[(size_t)(c0 + q) * BM + m]);
+            for (int q = 0; q < 32; ++q)
+              if (c0 + q < p.T) v[q] += __ldcg(&src[(size_t)(c0 + q) * BM]);
           }
-          if (!swiglu) {
+          const int nq = min(32, p.T - c0);
+          const size_t ldo = (size_t)p.epi.ldo;
+          if (mode == EPI_STORE_ACT) {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.epi.out) + (size_t)c0 * ldo + n;
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-              if (c0 + q < p.T) epi_apply<__nv_bfloat16>(p.epi, c0 + q, n, v[q]);
-          } else {
-            named_sync(1, 128);
-            if (m >= 64) {
+            for (int q = 0; q < 32; ++q)
+              if (q < nq) o[q * ldo] = __float2bfloat16_rn(v[q]);
+          } else if (mode == EPI_STORE_F32) {
+            float* o = reinterpret_cast<float*>(p.epi.out) + (size_t)c0 * ldo + n;
 #pragma unroll
-              for (int q = 0; q < 16; ++q) xch[(m - 64) * 17 + q] = v[q];
+            for (int q = 0; q < 32; ++q)
+              if (q < nq) o[q * ldo] = v[q];
+          } else if (mode == EPI_ADD_F32) {
+            float* o = reinterpret_cast<float*>(p.epi.out) + (size_t)c0 * ldo + n;
+            float old[32];
+#pragma unroll
+            for (int q = 0; q < 32; ++q) old[q] = (q < nq) ? o[q * ldo] : 0.f;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) v[q] = old[q] + v[q];
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (q < nq) o[q * ldo] = v[q];
+            if (p.epi.tap) {
+              float* tp = p.epi.tap + (size_t)c0 * ldo + n;
+#pragma unroll
+              for (int q = 0; q < 32; ++q)
+                if (q < nq) tp[q * ldo] = v[q];
             }
-            named_sync(1, 128);
-            if (m < 64) {
-              const int f = t * 64 + m;
-              __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.epi.out);
+          } else if (mode == EPI_BIAS_F32) {
+            float* o = reinterpret_cast<float*>(p.epi.out) + (size_t)c0 * ldo + n;
+            const float bias = p.epi.bias[n];
 #pragma unroll
-              for (int q = 0; q < 16; ++q)
-                if (c0 + q < p.T)
-                  o[(size_t)(c0 + q) * p.epi.ldo + f] = __float2bfloat16_rn(silu_f(v[q]) * xch[m * 17 + q]);
+            for (int q = 0; q < 32; ++q)
+              if (q < nq) o[q * ldo] = v[q] + bias;
+          } else {
+            // SwiGLU: rows 2i / 2i+1 of the interleaved weight are gate_i / up_i -> adjacent lanes.
+            // Even lanes emit even columns, odd lanes odd columns.
+            const int f = vt * 64 + (m >> 1);
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.epi.out) + (size_t)c0 * ldo + f;
+            const int par = lane & 1;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+              const float gq = __shfl_sync(0xffffffffu, v[q], lane & ~1);
+              const float uq = __shfl_sync(0xffffffffu, v[q], lane | 1);
+              if ((q & 1) == par && q < nq)
+                o[q * ldo] = __float2bfloat16_rn(__fdividef(gq, 1.f + __expf(-gq)) * uq);
             }
           }
         }
         if (is_head) {
-          named_sync(1, 128);
+          named_sync(1, 256);
           if (etid == 0)
-            for (int cc = c_lo; cc <= c_hi; ++cc) p.flags[cc] = 0;  // re-arm for the next launch
+            for (int cc = c_lo; cc <= c_hi; ++cc) p.flags[cc * CG + (int)rank] = 0;  // re-arm for the next launch
         }
       }
+#ifdef SF_GEMM_PROFILE
+      if (etid == 0 && (c == 0 || c == p.G / 2))
+        printf("T=%d grp %d seg %d: epilogue %lld cycles (%s)\n", p.T, c, seg, clock64() - te0,
+               is_full ? "full" : (is_head ? "head" : "publish"));
+#endif
       tc_fence_before();
-      named_sync(1, 128);
-      if (etid == 0) mbar_arrive(&acce[b]);
+      named_sync(1, 256);
+      if (etid == 0) {
+        if (CG == 1 || rank == 0) mbar_arrive(&acce[b]);
+        else mbar_arrive_remote(&acce[b], 0);
+      }
       u = se;
       ++seg;
     }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, p.tmem_cols);
+  if (warp == 2) {
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
+    else
+      tmem_dealloc(tmem, p.tmem_cols);
+  }
 }
 
 // ------------------------------------------------------------------------ SIMT fp32 kernel
@@ -310,14 +431,14 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
   const int Nout = DUAL ? N / 2 : N;
   const int ob = blockIdx.x * 32, tb = blockIdx.y * 32;
   float acc[4] = {0, 0, 0, 0}, accu[4] = {0, 0, 0, 0};
-  auto wrow = [&](int o) { return DUAL ? (o / 64) * 128 + (o % 64) : o; };
+  auto wrow = [&](int o) { return DUAL ? 2 * o : o; };
   for (int kt = 0; kt < K; kt += 32) {
     for (int i = ty; i < 32; i += 8) {
       const int t = tb + i, kk = kt + tx;
       As[i][tx] = (t < T && kk < K) ? A[(size_t)t * lda + kk] : 0.f;
       const int o = ob + i;
       Ws[i][tx] = (o < Nout && kk < K) ? W[(size_t)wrow(o) * K + kk] : 0.f;
-      if (DUAL) Us[i][tx] = (o < Nout && kk < K) ? W[(size_t)(wrow(o) + 64) * K + kk] : 0.f;
+      if (DUAL) Us[i][tx] = (o < Nout && kk < K) ? W[(size_t)(wrow(o) + 1) * K + kk] : 0.f;
     }
     __syncthreads();
 #pragma unroll 8
@@ -401,7 +522,7 @@ int64_t gemm_partial_elems(bool is_bf16, int T, int N, int K) {
   (void)N;
   (void)K;
   if (!is_bf16) return 0;
-  return (int64_t)kMaxSMs * BM * std::min(T, 512);
+  return (int64_t)2 * kMaxSMs * BM * std::min(T, 512);  // EPI_PARTIAL: 2 slots per CTA
 }
 
 // Tile-contiguous weight layout: block (t, k) = rows [128t, +128) x cols [64k, +64) stored as the
@@ -425,54 +546,232 @@ cudaError_t gemm_pack_weight(const void* src, void* dst, int N, int K, cudaStrea
   return cudaGetLastError();
 }
 
+static bool make_map_tiled(CUtensorMap* m, const void* ptr, long long rows) {
+  // tile-contiguous weights as a [rows, 64] bf16 tensor: each 128-row box is one contiguous 16 KB
+  // block already in the swizzled shared-memory image, so no TMA swizzle is applied
+  cuuint64_t dims[2] = {(cuuint64_t)BK, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)BK * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)BM};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// CTA-pair (cta_group::2) mode for a weight shape: a function of (N, K) only (batch invariance)
+static int gemm_cg(int N, int K) {
+  (void)K;
+  static const int env = getenv("SF_GEMM_CG") ? atoi(getenv("SF_GEMM_CG")) : 0;
+  if (env == 2 && N % (2 * BM) == 0) return 2;  // CTA-pair mode (experimental; slower so far)
+  return 1;
+}
+
 static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled, int T, int N, int K,
                              const GemmEpi& epi, const GemmScratch& scratch, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(gemm_sk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(gemm_sk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
+  const int CG = (w_tiled && T >= 1) ? gemm_cg(N, K) : 1;
   SkParams p{};
   p.T = T;
   p.N = N;
   p.K = K;
   tc_shape(T, &p.NT, &p.n_sub);
   p.kb_total = K / BK;
-  p.n_tiles = N / BM;
+  p.n_tiles = N / (BM * CG);
   const long long U = (long long)p.n_tiles * p.kb_total;
-  p.G = (int)std::min<long long>(num_sms(), U);  // depends on (N, K) only
+  p.G = (int)std::min<long long>(num_sms() / CG, U);  // depends on (N, K) only
   const int cols = p.n_sub * p.NT;
   p.nbuf = (2 * cols <= 512) ? 2 : 1;
   p.tmem_cols = 32;
   while ((int)p.tmem_cols < p.nbuf * cols) p.tmem_cols <<= 1;
-  const int stage_bytes = BM * BK * 2 + p.n_sub * p.NT * BK * 2;
+  const int stage_bytes = BM * BK * 2 + p.n_sub * (p.NT / CG) * BK * 2;
   // deep ring: ~200 KB in flight per SM covers loaded-HBM latency (Little's law)
   static const int env_st = getenv("SF_GEMM_STAGES") ? atoi(getenv("SF_GEMM_STAGES")) : 0;
   p.stages = std::max(2, std::min(16, (216 * 1024) / stage_bytes));
   if (env_st >= 2 && env_st * stage_bytes <= 216 * 1024) p.stages = env_st;
   // release slots in groups of cgrp (>= 3 groups in the ring; cgrp divides stages)
-  static const int env_cg = getenv("SF_GEMM_CGRP") ? atoi(getenv("SF_GEMM_CGRP")) : 0;
   p.cgrp = 1;
-  for (int c = 8; c >= 2; c >>= 1)
-    if (c * 3 <= p.stages || (c * 2 <= p.stages && c == 2)) {
-      p.cgrp = c;
+  for (int cg = 8; cg >= 2; cg >>= 1)
+    if (cg * 3 <= p.stages || (cg * 2 <= p.stages && cg == 2)) {
+      p.cgrp = cg;
       break;
     }
-  if (env_cg >= 1 && env_cg * 2 <= p.stages) p.cgrp = env_cg;
   p.stages = (p.stages / p.cgrp) * p.cgrp;
   p.epi = epi;
   p.partial = scratch.partial;
   p.flags = scratch.counters;
   p.w_tiled = w_tiled ? 1 : 0;
   p.w_tiles = (const __nv_bfloat16*)W;
-  if (!scratch.partial || scratch.partial_elems < (int64_t)p.G * T * BM || scratch.n_counters < p.G)
+  if (!scratch.partial || scratch.partial_elems < (int64_t)2 * p.G * CG * T * BM || scratch.n_counters < p.G * CG)
     return cudaErrorInvalidValue;
-  const size_t smem = (size_t)p.stages * stage_bytes + 1024 + (2 * p.stages + 4) * 8 + 16 + 64 * 17 * 4;
+  if (epi.mode == EPI_PARTIAL && p.n_tiles > p.G) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)p.stages * stage_bytes + 1024 + (2 * p.stages + 4) * 8 + 16;
   CUtensorMap mw, ma;
   memset(&mw, 0, sizeof(mw));
-  if (!w_tiled && !make_map(&mw, W, N, K, K, BM)) return cudaErrorInvalidValue;
-  if (!make_map(&ma, A, T, K, lda, p.NT)) return cudaErrorInvalidValue;
-  gemm_sk_kernel<<<p.G, 256, smem, st>>>(mw, ma, p);
+  if (CG == 2) {
+    if (!make_map_tiled(&mw, W, (long long)N * (K / BK))) return cudaErrorInvalidValue;
+  } else if (!w_tiled && !make_map(&mw, W, N, K, K, BM)) {
+    return cudaErrorInvalidValue;
+  }
+  if (!make_map(&ma, A, T, K, lda, p.NT / CG)) return cudaErrorInvalidValue;
+  if (CG == 1) {
+    gemm_sk_kernel<1><<<p.G, 384, smem, st>>>(mw, ma, p);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.G * 2);
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_sk_kernel<2>, mw, ma, p);
+}
+
+bool gemm_partial_geom(int T, int N, int K, PartialGeom* g) {
+  if (N % BM || K % BK || T > 512) return false;
+  const int CG = gemm_cg(N, K);
+  const int n_tiles = N / (BM * CG);
+  const long long U = (long long)n_tiles * (K / BK);
+  const int G = (int)std::min<long long>(num_sms() / CG, U);
+  if (n_tiles > G) return false;  // a group must touch at most 2 tiles
+  g->G = G * CG;                  // slots are per CTA: consumer addresses (2 * group + which) * CG + rank
+  g->kb = K / BK;
+  g->n_tiles = N / BM;
+  g->T = T;
+  return true;
+}
+
+// One CTA (512 threads) per virtual row. For every 128-column tile the k-segment owners are
+// precomputed in shared memory (first group, count, slot parity of the first one); each thread then
+// issues the loads of 4 columns x up to 8 segments back to back before summing them in k order.
+constexpr int kRnThreads = 512;
+constexpr int kRnMaxSeg = 8;
+
+__global__ void __launch_bounds__(kRnThreads) resid_norm_kernel(
+    const float* __restrict__ partial, int G, int kb, int CG, int n_tiles_cta, int T, int rep, int d,
+    const float* resid, const float* __restrict__ bias, float* out, float* tap, const float* __restrict__ gamma,
+    float eps, __nv_bfloat16* xn) {
+  __shared__ int seg_lo[128], seg_n[128], seg_w0[128];
+  __shared__ float red[kRnThreads / 32];
+  const int r = blockIdx.x;
+  const int src_row = r / rep, col0 = (r % rep) * d;
+  const int tid = threadIdx.x;
+  const int groups = G / CG;
+  const int n_tiles_grp = n_tiles_cta / CG;
+  const long long U = (long long)n_tiles_grp * kb;
+  if (partial) {
+    for (int tg = tid; tg < n_tiles_grp; tg += kRnThreads) {
+      const long long ua = (long long)tg * kb, ub = ua + kb - 1;
+      const int lo = (int)(((ua + 1) * groups + U - 1) / U) - 1;
+      const int hi = (int)(((ub + 1) * groups + U - 1) / U) - 1;
+      seg_lo[tg] = lo;
+      seg_n[tg] = hi - lo + 1;
+      seg_w0[tg] = ((U * lo / groups) / kb == tg) ? 0 : 1;  // slot parity of the first segment
+    }
+    __syncthreads();
+  }
+  const size_t slot_stride = (size_t)T * BM;
+  constexpr int CPT = 16;  // columns per thread kept in registers (d <= 8192)
+  float xv[CPT];
+  float ss = 0.f;
+#pragma unroll
+  for (int j0 = 0; j0 < CPT; j0 += 4) {
+    float acc[4];
+    int nn[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = tid + (j0 + j) * kRnThreads;
+      nn[j] = i;
+      acc[j] = 0.f;
+      if (i < d) {
+        acc[j] = resid ? resid[(size_t)r * d + i] : 0.f;
+        if (bias) acc[j] += bias[col0 + i];
+      }
+    }
+    if (partial) {
+      float pv[4][kRnMaxSeg];
+      int cnt[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = nn[j];
+        cnt[j] = 0;
+        if (i < d) {
+          const int n = col0 + i;
+          const int vt = n / BM, m = n % BM, tg = vt / CG, rk = vt % CG;
+          const int lo = seg_lo[tg], ns = seg_n[tg], w0 = seg_w0[tg];
+          cnt[j] = ns;
+          const float* basep = partial + (size_t)src_row * BM + m + (size_t)rk * slot_stride;
+#pragma unroll
+          for (int q = 0; q < kRnMaxSeg; ++q)
+            if (q < ns) {
+              const int g = lo + q;
+              const int which = (q == 0) ? w0 : 0;
+              pv[j][q] = __ldcg(basep + (size_t)((2 * g + which) * CG) * slot_stride);
+            }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int q = 0; q < kRnMaxSeg; ++q)
+          if (q < cnt[j]) acc[j] += pv[j][q];
+        if (cnt[j] > kRnMaxSeg) {  // segments beyond the unrolled window, still in k order
+          const int n = col0 + nn[j];
+          const int vt = n / BM, m = n % BM, tg = vt / CG, rk = vt % CG;
+          const float* basep = partial + (size_t)src_row * BM + m + (size_t)rk * slot_stride;
+          for (int q = kRnMaxSeg; q < cnt[j]; ++q)
+            acc[j] += __ldcg(basep + (size_t)((2 * (seg_lo[tg] + q)) * CG) * slot_stride);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = nn[j];
+      xv[j0 + j] = acc[j];
+      if (i < d) {
+        if (out) out[(size_t)r * d + i] = acc[j];
+        if (tap) tap[(size_t)r * d + i] = acc[j];
+        ss = fmaf(acc[j], acc[j], ss);
+      }
+    }
+  }
+  if (!gamma) return;
+  ss = block_sum<kRnThreads>(ss, red);
+  const float rs = 1.0f / sqrtf(ss / (float)d + eps);
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const int i = tid + j * kRnThreads;
+    if (i < d) xn[(size_t)r * d + i] = __float2bfloat16_rn(xv[j] * rs * gamma[i]);
+  }
+}
+
+cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T, int rep, int d, const float* resid,
+                              const float* bias, float* out, float* tap, const float* gamma, float eps,
+                              __nv_bfloat16* xn, cudaStream_t st) {
+  if (T * rep <= 0) return cudaSuccess;
+  if (d > kRnThreads * 16) return cudaErrorInvalidValue;
+  int G = 1, kb = 1, CG = 1, nt = 1, Tslot = T;
+  if (partial) {
+    G = g->G;
+    kb = g->kb;
+    nt = g->n_tiles;
+    CG = gemm_cg(nt * BM, kb * BK);
+    Tslot = g->T;
+    if (nt / CG > 128) return cudaErrorInvalidValue;
+  }
+  resid_norm_kernel<<<T * rep, kRnThreads, 0, st>>>(partial, G, kb, CG, nt, Tslot, rep, d, resid, bias, out, tap,
+                                                    gamma, eps, xn);
   return cudaGetLastError();
 }
 

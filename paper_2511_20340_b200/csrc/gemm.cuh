@@ -1,6 +1,7 @@
 // gemm.cuh -- GEMM launch interface shared by the runtime.
 #pragma once
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 namespace sf {
@@ -10,8 +11,10 @@ enum EpiMode : int {
   EPI_STORE_F32 = 1,   // out_f32[t, n] = acc                     (logits, residual init)
   EPI_ADD_F32 = 2,     // out_f32[t, n] += acc; tap[t, n] = result (residual stream, Eq.7)
   EPI_BIAS_F32 = 3,    // out_f32[t, n] = acc + bias[n]           (positional FFN, Eq.9)
-  EPI_SWIGLU_ACT = 4,  // W rows interleaved in 64-row groups [gate_i; up_i]:
-                       // out_act[t, 64 i + m] = silu(gate) * up  (SwiGLU, P197)
+  EPI_SWIGLU_ACT = 4,  // W rows interleaved [gate_0; up_0; gate_1; up_1; ...]:
+                       // out_act[t, i] = silu(gate_i) * up_i  (SwiGLU, P197)
+  EPI_PARTIAL = 5,     // bf16 path, N/128 <= #SMs: every k-segment's fp32 accumulator goes to the
+                       // scratch partial slots; a consumer (launch_resid_norm) adds them in k order
 };
 
 struct GemmEpi {
@@ -40,5 +43,23 @@ cudaError_t gemm_pack_weight(const void* src, void* dst, int N, int K, cudaStrea
 
 // scratch floats needed by gemm_launch for (T, N, K)
 int64_t gemm_partial_elems(bool is_bf16, int T, int N, int K);
+
+// Stream-K geometry the EPI_PARTIAL consumer needs to locate a tile's k-segments.
+struct PartialGeom {
+  int G;          // CTAs
+  int kb;         // k-blocks per tile
+  int n_tiles;    // 128-row tiles
+  int T;          // rows per launch chunk (slot stride)
+};
+bool gemm_partial_geom(int T, int N, int K, PartialGeom* g);  // false if EPI_PARTIAL unsupported
+
+// Fused consumer of EPI_PARTIAL (and plain residual/norm): for virtual row r (T*rep rows, source
+// row r / rep, columns [(r % rep) * d, +d) of the GEMM output):
+//   x = (resid ? resid[r] : 0) + (bias ? bias[col] : 0) + sum_k-segments partial   (fixed order)
+//   out[r] = x (fp32, out may alias resid); tap[r] = x (optional);
+//   xn[r] = bf16(x / sqrt(mean(x^2) + eps) * gamma) (optional, gamma != null)
+cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T, int rep, int d, const float* resid,
+                              const float* bias, float* out, float* tap, const float* gamma, float eps,
+                              __nv_bfloat16* xn, cudaStream_t s);
 
 }  // namespace sf

@@ -217,6 +217,7 @@ struct sf_handle {
   int B = 0;
   int state = ST_INIT;
   bool ctx_pending = false;
+  bool final_xn_ready = false;
   int64_t launches = 0;
   int64_t host_len_hi = 0;  // host upper bound of max(seq_len)
   std::string err_msg;
@@ -328,6 +329,26 @@ static cudaError_t rmsnorm(sf_handle* h, const float* in, int in_ld, const float
   return launch_rmsnorm(h->bf, in, in_ld, g, h->c.rms_eps, T, h->p.d, out, out_ld, h->st);
 }
 
+// Fused "GEMM -> residual (+bias) -> [tap] -> RMSNorm" (bf16 path): the GEMM writes its k-segment
+// partials (EPI_PARTIAL) and resid_norm_kernel sums them in k order while applying the residual and
+// the next norm. Returns false (nothing launched) when the shape does not allow it; callers then use
+// the unfused ADD / STORE epilogue + rmsnorm. rep > 1 views each GEMM row as rep rows of d columns.
+static bool gemm_resid_norm(sf_handle* h, cudaError_t* err, const void* A, int lda, const void* W, int T, int N,
+                            int K, int rep, const float* resid, const float* bias, float* out, float* tap,
+                            const float* gamma) {
+  if (!h->bf || T > 512) return false;
+  PartialGeom g;
+  if (!gemm_partial_geom(T, N, K, &g)) return false;
+  GemmEpi e;
+  e.mode = EPI_PARTIAL;
+  if ((*err = gemm(h, A, lda, W, T, N, K, e)) != cudaSuccess) return true;
+  ProfScope ps(h, 2, (double)T * N * 4.0 * 3);
+  h->launches++;
+  *err = launch_resid_norm(h->gpart, &g, T, rep, h->p.d, resid, bias, out, tap, gamma, h->c.rms_eps,
+                           gamma ? (__nv_bfloat16*)h->xn : nullptr, h->st);
+  return true;
+}
+
 static const int* taps_layers(int L, int* out4) {
   out4[0] = 0;
   out4[1] = L / 2;
@@ -366,7 +387,8 @@ static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const i
 
 // Base decoder forward over T rows (q_len per sequence, positions pos0[b] + i); writes resid and
 // the 4 hook taps (P175) into h->taps.
-static cudaError_t base_forward(sf_handle* h, int T, int q_len, const int* pos0, int max_key) {
+static cudaError_t base_forward(sf_handle* h, int T, int q_len, const int* pos0, int max_key,
+                                bool final_norm = true) {
   const Plan& p = h->p;
   const int64_t tstride = (int64_t)p.R * p.d;
   int tl[4];
@@ -376,28 +398,42 @@ static cudaError_t base_forward(sf_handle* h, int T, int q_len, const int* pos0,
   if (e != cudaSuccess) return e;
   for (int g = 1; g < 4; ++g)
     if (tl[g] == 0) cudaMemcpyAsync(h->taps + g * tstride, h->taps, (size_t)T * p.d * 4, cudaMemcpyDeviceToDevice, h->st);
+  bool xn_ready = false;  // xn already holds RMS_attn(resid) of this layer (fused into the last consumer)
   for (int l = 0; l < p.L; ++l) {
     const auto& w = h->lw[l];
-    if ((e = rmsnorm(h, h->resid, p.d, w.attn_norm, T, h->xn, p.d))) return e;
+    if (!xn_ready && (e = rmsnorm(h, h->resid, p.d, w.attn_norm, T, h->xn, p.d))) return e;
     if ((e = gemm(h, h->xn, p.d, w.wqkv, T, p.qkvw, p.d, epi_act(h->qkv, p.qkvw)))) return e;
     if ((e = attn_layer(h, l, T, q_len, pos0, max_key))) return e;
-    if ((e = gemm(h, h->attn, p.ao, w.wo, T, p.d, p.ao, epi_add(h->resid, p.d, nullptr)))) return e;
-    if ((e = rmsnorm(h, h->resid, p.d, w.ffn_norm, T, h->xn, p.d))) return e;
+    // o-proj + residual + RMS_ffn
+    if (!gemm_resid_norm(h, &e, h->attn, p.ao, w.wo, T, p.d, p.ao, 1, h->resid, nullptr, h->resid, nullptr,
+                         w.ffn_norm)) {
+      if ((e = gemm(h, h->attn, p.ao, w.wo, T, p.d, p.ao, epi_add(h->resid, p.d, nullptr)))) return e;
+      e = rmsnorm(h, h->resid, p.d, w.ffn_norm, T, h->xn, p.d);
+    }
+    if (e) return e;
     GemmEpi sw;
     sw.mode = EPI_SWIGLU_ACT;
     sw.out = h->ffn;
     sw.ldo = p.F;
     if ((e = gemm(h, h->xn, p.d, w.wgu, T, 2 * p.F, p.d, sw))) return e;
-    // residual add; the first tap slot that equals HS[l+1] is written by the epilogue
+    // down-proj + residual (+ hook tap HS[l+1]) + the next RMSNorm
     int first = -1;
     for (int g = 0; g < 4; ++g)
       if (tl[g] == l + 1 && first < 0) first = g;
     float* tap = first >= 0 ? h->taps + first * tstride : nullptr;
-    if ((e = gemm(h, h->ffn, p.F, w.wdown, T, p.d, p.F, epi_add(h->resid, p.d, tap)))) return e;
+    const float* next_g = (l + 1 < p.L) ? h->lw[l + 1].attn_norm : (final_norm ? h->final_norm : nullptr);
+    if (gemm_resid_norm(h, &e, h->ffn, p.F, w.wdown, T, p.d, p.F, 1, h->resid, nullptr, h->resid, tap, next_g)) {
+      xn_ready = next_g != nullptr;
+    } else {
+      if ((e = gemm(h, h->ffn, p.F, w.wdown, T, p.d, p.F, epi_add(h->resid, p.d, tap)))) return e;
+      xn_ready = false;
+    }
+    if (e) return e;
     for (int g = first + 1; first >= 0 && g < 4; ++g)
       if (tl[g] == l + 1)
         cudaMemcpyAsync(h->taps + g * tstride, tap, (size_t)T * p.d * 4, cudaMemcpyDeviceToDevice, h->st);
   }
+  h->final_xn_ready = xn_ready;  // xn = RMS_f(HS[L]) when the last consumer applied the final norm
   return cudaSuccess;
 }
 
@@ -408,18 +444,26 @@ static cudaError_t ctx_forward(sf_handle* h, int T, int q_len, const int* pos0, 
   if ((e = launch_group_rms(h->bf, h->taps, (int64_t)p.R * p.d, h->group_scale, h->c.rms_eps, T, p.d, h->xn, h->st)))
     return e;
   h->launches++;
-  if ((e = gemm(h, h->xn, 4 * p.d, h->w_d, T, p.d, 4 * p.d, epi_f32(h->ctx, p.d)))) return e;
-  if ((e = rmsnorm(h, h->ctx, p.d, h->ctx_norm, T, h->xn, p.d))) return e;
+  // X = W_D I_Cat -> ctx, xn = RMS_c(X)
+  if (!gemm_resid_norm(h, &e, h->xn, 4 * p.d, h->w_d, T, p.d, 4 * p.d, 1, nullptr, nullptr, h->ctx, nullptr,
+                       h->ctx_norm)) {
+    if ((e = gemm(h, h->xn, 4 * p.d, h->w_d, T, p.d, 4 * p.d, epi_f32(h->ctx, p.d)))) return e;
+    e = rmsnorm(h, h->ctx, p.d, h->ctx_norm, T, h->xn, p.d);
+  }
+  if (e) return e;
   if ((e = gemm(h, h->xn, p.d, h->ctx_wqkv, T, p.qkvw, p.d, epi_act(h->qkv, p.qkvw)))) return e;
   if ((e = attn_layer(h, p.L, T, q_len, pos0, max_key))) return e;
-  return gemm(h, h->attn, p.ao, h->ctx_wo, T, p.d, p.ao, epi_add(h->ctx, p.d, nullptr));
+  // I_D = X + MSA(...)
+  if (!gemm_resid_norm(h, &e, h->attn, p.ao, h->ctx_wo, T, p.d, p.ao, 1, h->ctx, nullptr, h->ctx, nullptr, nullptr))
+    e = gemm(h, h->attn, p.ao, h->ctx_wo, T, p.d, p.ao, epi_add(h->ctx, p.d, nullptr));
+  return e;
 }
 
 // final norm + LM head + argmax over T rows of `src` (f32 [T, d])
-static cudaError_t head_argmax(sf_handle* h, const float* src, int T, float* logits, int* out) {
+static cudaError_t head_argmax(sf_handle* h, const float* src, int T, float* logits, int* out, bool xn_ready = false) {
   const Plan& p = h->p;
   cudaError_t e;
-  if ((e = rmsnorm(h, src, p.d, h->final_norm, T, h->xn, p.d))) return e;
+  if (!xn_ready && (e = rmsnorm(h, src, p.d, h->final_norm, T, h->xn, p.d))) return e;
   if ((e = gemm(h, h->xn, p.d, h->lm_head, T, p.V, p.d, epi_f32(logits, p.V)))) return e;
   h->launches += 2;
   ProfScope ps(h, 3, (double)T * p.V * 4.0);
@@ -438,30 +482,43 @@ static cudaError_t do_draft(sf_handle* h) {
   }
   // positional FFN (Eq.9): D = W_P RMS(I_D) + b_P  -> [B, k*d] == [B*k, d]
   if ((e = rmsnorm(h, h->idrow, p.d, h->pos_norm, B, h->xn, p.d))) return e;
-  GemmEpi eb;
-  eb.mode = EPI_BIAS_F32;
-  eb.out = h->D;
-  eb.ldo = k * p.d;
-  eb.bias = h->b_p;
-  if ((e = gemm(h, h->xn, p.d, h->w_p, B, k * p.d, p.d, eb))) return e;
-  // draft bidirectional layer (Eq.10)
   const int Tk = B * k;
-  if ((e = rmsnorm(h, h->D, p.d, h->blk_attn_norm, Tk, h->xn, p.d))) return e;
+  // D = W_P RMS_p(I_D) + b_P viewed as [B*k, d]; xn = RMS_1(D)
+  if (!gemm_resid_norm(h, &e, h->xn, p.d, h->w_p, B, k * p.d, p.d, k, nullptr, h->b_p, h->D, nullptr,
+                       h->blk_attn_norm)) {
+    GemmEpi eb;
+    eb.mode = EPI_BIAS_F32;
+    eb.out = h->D;
+    eb.ldo = k * p.d;
+    eb.bias = h->b_p;
+    if ((e = gemm(h, h->xn, p.d, h->w_p, B, k * p.d, p.d, eb))) return e;
+    e = rmsnorm(h, h->D, p.d, h->blk_attn_norm, Tk, h->xn, p.d);
+  }
+  if (e) return e;
+  // draft bidirectional layer (Eq.10)
   if ((e = gemm(h, h->xn, p.d, h->blk_wqkv, Tk, p.qkvw, p.d, epi_act(h->qkv, p.qkvw)))) return e;
   if ((e = launch_bidir_attention(h->bf, h->qkv, B, k, p.Hq, p.Hkv, p.hd, (h->c.flags & SF_FLAG_DRAFT_CAUSAL) != 0,
                                   h->attn, h->st)))
     return e;
   h->launches++;
-  if ((e = gemm(h, h->attn, p.ao, h->blk_wo, Tk, p.d, p.ao, epi_add(h->D, p.d, nullptr)))) return e;
-  if ((e = rmsnorm(h, h->D, p.d, h->blk_ffn_norm, Tk, h->xn, p.d))) return e;
+  if (!gemm_resid_norm(h, &e, h->attn, p.ao, h->blk_wo, Tk, p.d, p.ao, 1, h->D, nullptr, h->D, nullptr,
+                       h->blk_ffn_norm)) {
+    if ((e = gemm(h, h->attn, p.ao, h->blk_wo, Tk, p.d, p.ao, epi_add(h->D, p.d, nullptr)))) return e;
+    e = rmsnorm(h, h->D, p.d, h->blk_ffn_norm, Tk, h->xn, p.d);
+  }
+  if (e) return e;
   GemmEpi sw;
   sw.mode = EPI_SWIGLU_ACT;
   sw.out = h->ffn;
   sw.ldo = p.F;
   if ((e = gemm(h, h->xn, p.d, h->blk_wgu, Tk, 2 * p.F, p.d, sw))) return e;
-  if ((e = gemm(h, h->ffn, p.F, h->blk_wdown, Tk, p.d, p.F, epi_add(h->D, p.d, nullptr)))) return e;
-  // shared frozen final norm + LM head (C8) -> k draft tokens
-  return head_argmax(h, h->D, Tk, h->dlogits, h->draft);
+  // E = Y + SwiGLU(...); xn = RMS_f(E) (shared frozen final norm, C8)
+  bool xn_ready = gemm_resid_norm(h, &e, h->ffn, p.F, h->blk_wdown, Tk, p.d, p.F, 1, h->D, nullptr, h->D, nullptr,
+                                  h->final_norm);
+  if (!xn_ready) e = gemm(h, h->ffn, p.F, h->blk_wdown, Tk, p.d, p.F, epi_add(h->D, p.d, nullptr));
+  if (e) return e;
+  // shared frozen LM head -> k draft tokens
+  return head_argmax(h, h->D, Tk, h->dlogits, h->draft, xn_ready);
 }
 
 static cudaError_t do_verify(sf_handle* h) {
@@ -472,7 +529,7 @@ static cudaError_t do_verify(sf_handle* h) {
   if ((e = launch_build_verify_rows(B, k, h->last_token, h->draft, h->tok_rows, h->st))) return e;
   h->launches++;
   if ((e = base_forward(h, T, k + 1, h->seq_len, h->c.max_seq))) return e;
-  return head_argmax(h, h->resid, T, h->logits, h->greedy);
+  return head_argmax(h, h->resid, T, h->logits, h->greedy, h->final_xn_ready);
 }
 
 static cudaError_t do_accept(sf_handle* h, int* acc_log, int* em_log, int log_cap) {
@@ -679,7 +736,7 @@ sf_status specformer_prefill(sf_handle* h, const int32_t* tokens, int32_t B, int
   for (int c0 = 0; c0 < P; c0 += C) {
     Cc = std::min(C, P - c0);
     SF_TRY(launch_build_prefill_rows(B, P, c0, Cc, h->prompt, h->tok_rows, h->pos0_pf, h->st));
-    SF_TRY(base_forward(h, B * Cc, Cc, h->pos0_pf, c0 + Cc));
+    SF_TRY(base_forward(h, B * Cc, Cc, h->pos0_pf, c0 + Cc, /*final_norm=*/false));
     if (p.k > 0) SF_TRY(ctx_forward(h, B * Cc, Cc, h->pos0_pf, c0 + Cc));
   }
   // last prompt row per sequence: I_D row (draft input) and LM head -> g0

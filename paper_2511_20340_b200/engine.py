@@ -60,7 +60,7 @@ def weight_table(cfg: EngineConfig):
 
 def _interleave_gu(gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
     F, d = gate.shape
-    return torch.stack([gate.reshape(F // 64, 64, d), up.reshape(F // 64, 64, d)], dim=1).reshape(2 * F, d)
+    return torch.stack([gate, up], dim=1).reshape(2 * F, d)  # rows 2i = gate_i, 2i+1 = up_i
 
 
 def _source_tensor(name: str, w: dict) -> torch.Tensor:
