@@ -5,12 +5,15 @@
 // attn_combine_kernel), so every row's result is independent of batch size, block length and
 // split count (batch invariance, reading C23).
 //
-// Persistent CTAs (4 warps) walk a static list of (sequence, kv head, query tile, chunk range)
-// items; a 3-stage cp.async ring streams each 128-key K/V chunk (64 KB, XOR-swizzled 16-byte
-// chunks -> conflict-free ldmatrix) while the previous chunk is computed:
+// Persistent CTAs walk a static list of (sequence, kv head, query tile, chunk range) items. A
+// producer warp streams each 128-key K/V chunk (64 KB) with TMA: one 2-D box per (16-key page,
+// 64-dim half) of the paged cache, 128-byte swizzled (conflict-free ldmatrix), into a 3-stage
+// mbarrier ring, while 4 compute warps work on the previous chunk:
 //   S = Q K^T   : warp w owns keys 32w..32w+31, mma.sync m16n8k16 bf16 -> fp32
 //   chunk softmax: row max / sum across the 4 warps in fixed order (exact zeros for masked keys)
 //   O = P V     : P (bf16) exchanged through smem, warp w owns output dims 32w..32w+31
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -28,7 +31,7 @@ constexpr int NST = 3;           // pipeline stages
 constexpr int KV_BYTES = CH * HD * 2;            // one of K or V per stage: 32 KB
 constexpr int STAGE_BYTES = 2 * KV_BYTES;        // 64 KB
 constexpr int PLD = CH + 8;                      // padded P row (bf16 elements)
-constexpr int SMEM = NST * STAGE_BYTES + 16 * PLD * 2 + 2 * 4 * 16 * 4 + 64;
+constexpr int SMEM = NST * STAGE_BYTES + 16 * PLD * 2 + 2 * 4 * 16 * 4 + 2 * NST * 8 + 1024 + 64;
 
 SF_DEV void cp_async16_zfill(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
@@ -59,8 +62,12 @@ SF_DEV uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
-// byte offset of 16-byte chunk c (0..15) of key row j inside a swizzled [128][128] bf16 tile
-SF_DEV uint32_t swz(int j, int c) { return (uint32_t)(j * (HD * 2) + ((c ^ (j & 7)) << 4)); }
+// byte offset of 16-byte chunk c (0..15) of key row j in a [2 halves][128 keys][128 B] tile, each
+// 128-byte row 128B-swizzled exactly as TMA SWIZZLE_128B writes it (chunk c' at c' ^ (j % 8))
+SF_DEV uint32_t swz(int j, int c) {
+  return (uint32_t)((c >> 3) * (CH * 128) + j * 128 + (((c & 7) ^ (j & 7)) << 4));
+}
+SF_DEV void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 struct Item {
   int b, kvh, qt, c0, c1;
@@ -69,19 +76,24 @@ struct Item {
 }  // namespace
 
 // Work list is implicit: item = ((b * Hkv + kvh) * ntiles + qt) * nsplit + split.
-__global__ void __launch_bounds__(128, 1) attn_mma_kernel(AttnParams p, int ntiles, int nsplit, int n_items) {
-  extern __shared__ __align__(128) uint8_t sm[];
+// Warps 0..3 compute, warp 4 produces (TMA).
+__global__ void __launch_bounds__(160, 1) attn_mma_kernel(const __grid_constant__ CUtensorMap tmK,
+                                                         const __grid_constant__ CUtensorMap tmV, AttnParams p,
+                                                         int ntiles, int nsplit, int n_items) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  const uint32_t raw = smem_u32(sm_raw);
+  uint8_t* sm = sm_raw + (((raw + 1023u) & ~1023u) - raw);
   const uint32_t sbase = smem_u32(sm);
   __nv_bfloat16* Ps = reinterpret_cast<__nv_bfloat16*>(sm + NST * STAGE_BYTES);
   float* red_m = reinterpret_cast<float*>(sm + NST * STAGE_BYTES + 16 * PLD * 2);
   float* red_l = red_m + 4 * 16;
+  uint64_t* full = reinterpret_cast<uint64_t*>(red_l + 4 * 16);
+  uint64_t* empty = full + NST;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int G = p.Hq / p.Hkv;
   const int R = p.q_len * G;
-  const __nv_bfloat16* Kg = reinterpret_cast<const __nv_bfloat16*>(p.Kp);
-  const __nv_bfloat16* Vg = reinterpret_cast<const __nv_bfloat16*>(p.Vp);
 
   auto item_of = [&](int idx, Item& it) -> bool {
     int r = idx;
@@ -101,51 +113,60 @@ __global__ void __launch_bounds__(128, 1) attn_mma_kernel(AttnParams p, int ntil
     return it.c0 < it.c1;
   };
 
-  // ---- flattened (item, chunk) task stream of this CTA
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);  // one arrival per compute warp
+    }
+    fence_barrier_init();
+  }
+  // Pages past a sequence's last key are not loaded: their (masked, p = 0) V rows must still be
+  // finite, so the ring starts zeroed; afterwards it only ever holds real (finite) K/V values.
+  for (int i = tid; i < NST * STAGE_BYTES / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(sm)[i] = make_uint4(0u, 0u, 0u, 0u);
+  fence_proxy_async();
+  __syncthreads();
+
+  if (warp == 4) {
+    // ---- TMA producer
+    int seq = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      Item it;
+      if (!item_of(item, it)) continue;
+      const int r0 = it.qt * 16;
+      const int nr = min(16, R - r0);
+      const int kmax = min(p.pos0[it.b] + min(p.q_len - 1, (r0 + nr - 1) / G), p.max_key - 1);
+      for (int c = it.c0; c < it.c1; ++c, ++seq) {
+        const int st = seq % NST;
+        mbar_wait(&empty[st], ((uint32_t)(seq / NST) & 1u) ^ 1u);
+        const int kstart = c * CH;
+        const int npages = (min(CH, kmax + 1 - kstart) + 15) / 16;
+        const int pg = (lane < npages) ? p.block_table[it.b * p.pages_per_seq + kstart / 16 + lane] : 0;
+        if (lane == 0) mbar_arrive_expect_tx(&full[st], (uint32_t)(npages * 4 * 16 * 128));
+        __syncwarp();
+        // page ids broadcast warp-wide, then the elected lane issues the boxes
+        for (int i = 0; i < npages; ++i) {
+          const int blk = __shfl_sync(0xffffffffu, pg, i);
+          if (lane == 0) {
+            const int row = (blk * p.Hkv + it.kvh) * 16;
+            uint8_t* kb = sm + st * STAGE_BYTES;
+            uint8_t* vb = kb + KV_BYTES;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              tma_load_2d(kb + hf * (CH * 128) + i * 16 * 128, &tmK, &full[st], hf * 64, row, kEvictFirst);
+              tma_load_2d(vb + hf * (CH * 128) + i * 16 * 128, &tmV, &full[st], hf * 64, row, kEvictFirst);
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
+
   int cur_item = blockIdx.x;
   Item cur{};
   while (cur_item < n_items && !item_of(cur_item, cur)) cur_item += gridDim.x;
-  if (cur_item >= n_items) return;
-  // loader cursor (runs NST-1 tasks ahead)
-  int ld_item = cur_item, ld_chunk = cur.c0;
-  Item ld = cur;
-  int ld_seq = 0;  // number of chunk loads issued
-  auto issue_load = [&]() {
-    if (ld_item >= n_items) {
-      cp_commit();  // keep group accounting uniform
-      return;
-    }
-    const int stage = ld_seq % NST;
-    const uint32_t kb = sbase + stage * STAGE_BYTES, vb = kb + KV_BYTES;
-    const int r0 = ld.qt * 16;
-    const int nr = min(16, R - r0);
-    const int kmax = min(p.pos0[ld.b] + min(p.q_len - 1, (r0 + nr - 1) / G), p.max_key - 1);
-    const int kstart = ld_chunk * CH;
-    const int nk = min(CH, kmax + 1 - kstart);
-    // 128 keys x 16 chunks x 2 (K,V) = 4096 x 16 B, 32 per thread
-#pragma unroll 4
-    for (int e = tid; e < CH * 16; e += 128) {
-      const int j = e >> 4, c = e & 15;
-      const bool valid = j < nk;
-      const int key = kstart + (valid ? j : 0);
-      const int blk = p.block_table[ld.b * p.pages_per_seq + key / 16];
-      const size_t off = (((size_t)blk * p.Hkv + ld.kvh) * 16 + (key % 16)) * HD + c * 8;
-      cp_async16_zfill(kb + swz(j, c), Kg + off, valid);
-      cp_async16_zfill(vb + swz(j, c), Vg + off, valid);
-    }
-    cp_commit();
-    ++ld_seq;
-    // advance loader cursor
-    if (++ld_chunk >= ld.c1) {
-      do {
-        ld_item += gridDim.x;
-      } while (ld_item < n_items && !item_of(ld_item, ld));
-      if (ld_item < n_items) ld_chunk = ld.c0;
-    }
-  };
-#pragma unroll
-  for (int s = 0; s < NST - 1; ++s) issue_load();
-
   int use_seq = 0;
   uint32_t qa[8][4];  // Q A-fragments (bf16) for 8 k-steps of 16 dims
   int q_item = -1;
@@ -173,10 +194,8 @@ __global__ void __launch_bounds__(128, 1) attn_mma_kernel(AttnParams p, int ntil
       q_item = cur_item;
     }
     for (int c = cur.c0; c < cur.c1; ++c) {
-      issue_load();            // keep NST-1 loads in flight
-      cp_wait<NST - 1>();      // the chunk to consume has landed (this thread's copies)
-      __syncthreads();         // ... and everyone else's
       const int stage = use_seq % NST;
+      mbar_wait(&full[stage], (uint32_t)(use_seq / NST) & 1u);  // this chunk's K/V landed
       const uint32_t kb = sbase + stage * STAGE_BYTES, vb = kb + KV_BYTES;
       const int kstart = c * CH;
       // ---- S = Q K^T over this warp's 32 keys
@@ -222,7 +241,7 @@ __global__ void __launch_bounds__(128, 1) attn_mma_kernel(AttnParams p, int ntil
         red_m[warp * 16 + g] = mlo;
         red_m[warp * 16 + g + 8] = mhi;
       }
-      __syncthreads();
+      named_bar(1, 128);
       const float Mlo = fmaxf(fmaxf(red_m[g], red_m[16 + g]), fmaxf(red_m[32 + g], red_m[48 + g]));
       const float Mhi =
           fmaxf(fmaxf(red_m[8 + g], red_m[24 + g]), fmaxf(red_m[40 + g], red_m[56 + g]));
@@ -250,7 +269,7 @@ __global__ void __launch_bounds__(128, 1) attn_mma_kernel(AttnParams p, int ntil
         red_l[warp * 16 + g] = llo;
         red_l[warp * 16 + g + 8] = lhi;
       }
-      __syncthreads();
+      named_bar(1, 128);
       // ---- O = P V for this warp's 32 output dims (n-tiles 4w..4w+3)
       float o[4][4];
 #pragma unroll
@@ -277,6 +296,8 @@ __global__ void __launch_bounds__(128, 1) attn_mma_kernel(AttnParams p, int ntil
           mma16816(o[2 * np + 1], a, b2, b3);
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);  // this warp is done reading the stage
       // ---- write the chunk partial
 #pragma unroll
       for (int hr = 0; hr < 2; ++hr) {
@@ -299,16 +320,36 @@ __global__ void __launch_bounds__(128, 1) attn_mma_kernel(AttnParams p, int ntil
         }
       }
       ++use_seq;
-      __syncthreads();  // stage + Ps + red buffers free for reuse
+      named_bar(1, 128);  // Ps + red buffers free for reuse
     }
     do {
       cur_item += gridDim.x;
     } while (cur_item < n_items && !item_of(cur_item, cur));
   }
-  cp_wait<0>();
 }
 
 static int g_num_sms = 0;
+
+// 2-D view of one layer's paged K (or V) pool: [n_pages * Hkv * 16 rows, 128 dims] bf16; a box is
+// one 16-key page x 64 dims (128 B rows), 128B-swizzled.
+static bool encode_kv_map(CUtensorMap* m, const void* base, long long rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)HD, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)HD * 2};
+  cuuint32_t box[2] = {64, 16};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 cudaError_t launch_attention_mma(const AttnParams& p, cudaStream_t s) {
   static bool attr = false;
@@ -328,7 +369,10 @@ cudaError_t launch_attention_mma(const AttnParams& p, cudaStream_t s) {
   while (nsplit < nch && pairs * nsplit < 2 * g_num_sms) ++nsplit;
   const int n_items = pairs * nsplit;
   const int grid = std::min(n_items, g_num_sms);
-  attn_mma_kernel<<<grid, 128, SMEM, s>>>(p, ntiles, nsplit, n_items);
+  CUtensorMap mk, mv;
+  const long long rows = (long long)p.n_pages * p.Hkv * 16;
+  if (!encode_kv_map(&mk, p.Kp, rows) || !encode_kv_map(&mv, p.Vp, rows)) return cudaErrorInvalidValue;
+  attn_mma_kernel<<<grid, 160, SMEM, s>>>(mk, mv, p, ntiles, nsplit, n_items);
   return cudaGetLastError();
 }
 

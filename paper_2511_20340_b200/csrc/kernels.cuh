@@ -19,6 +19,7 @@ struct AttnParams {
   float* part_ml;            // [T, Hq, nchunk_max, 2]
   void* out;                 // [T, Hq*hd] act dtype
   int max_key;               // upper bound of pos0[b] + q_len (grid sizing), <= max_seq
+  int n_pages;               // pages in the pool (TMA tensor-map extent)
 };
 
 constexpr int kAttnChunk = 128;  // fixed absolute key-chunk size (split-KV boundaries, C23)

@@ -381,6 +381,7 @@ static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const i
   ap.part_ml = h->apml;
   ap.out = h->attn;
   ap.max_key = std::min(max_key, h->c.max_seq);
+  ap.n_pages = p.n_pages;
   h->launches += 3;
   return launch_attention(h->bf, ap, h->st);
 }
@@ -695,6 +696,10 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
   for (int i = 0; i < p.n_pages; ++i) bt[i] = i;
   e = cudaMemcpyAsync(h->bt, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice, h->st);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->gcnt, 0, 4096 * 4, h->st);
+  // whole 16-key pages are staged by TMA: never-written slots must hold finite values (masked keys
+  // get probability exactly 0, and 0 * finite = 0)
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->kpool, 0, (size_t)p.kv_layer_bytes * (p.L + 1), h->st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->vpool, 0, (size_t)p.kv_layer_bytes * (p.L + 1), h->st);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->ws + p.o_ints, 0, (16 * p.B + 2 * p.R + 8 + p.rows_v * 2 + p.rows_d) * 4, h->st);
   if (e == cudaSuccess) e = launch_rope_table(h->rope, cfg->max_seq, p.hd, cfg->rope_theta, h->st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->st);  // host vector bt must outlive the copy

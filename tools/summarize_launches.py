@@ -9,7 +9,7 @@ for r in rows[1:]:
     name = r[ki].split("(")[0].replace("void ", "")[:60]
     v = float(r[vi].replace(",", ""))
     unit = r[hdr.index("Metric Unit")]
-    v = v / 1e3 if unit == "nsecond" else v * (1e3 if unit == "msecond" else 1)
+    v = v / 1e3 if unit in ("nsecond", "ns") else v * (1e3 if unit in ("msecond", "ms") else 1)
     tot[name] += v; cnt[name] += 1
 steps = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 S = sum(tot.values())
