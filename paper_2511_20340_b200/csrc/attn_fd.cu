@@ -1,0 +1,350 @@
+// attn_fd.cu -- bf16 hybrid-mask paged decode attention (mode CAUSAL_PREFIX), flash-decoding form.
+//
+// One CTA item = (sequence b, kv head, 16-row query tile); persistent CTAs walk the items. A
+// producer warp streams the item's 128-key K/V chunks with TMA (one 2-D 128B-swizzled box per
+// (16-key page, 64-dim half)) into a 3-stage mbarrier ring. Compute warp w owns keys
+// [32w, 32w+32) of every chunk and keeps its own online-softmax state (m, l, O[16x128]) across
+// the chunks -- no cross-warp synchronisation per chunk, P never leaves registers:
+//   S = Q K_w^T (mma.sync m16n8k16 bf16 -> fp32), masked (key <= row position), m_new = max,
+//   O = O e^(m_old - m_new) + P V_w,  l = l e^(m_old - m_new) + sum P.
+// At the end of the item the 4 warp states are merged in the fixed order w = 0..3 and normalised.
+// Every row's arithmetic (chunk boundaries at fixed absolute 128-key positions, per-warp key
+// slices, merge order) is independent of batch size and block length (batch invariance, C23).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sf {
+namespace {
+
+constexpr int HD = 128;
+constexpr int CH = 128;
+constexpr int NST = 3;
+constexpr int KV_BYTES = CH * HD * 2;      // 32 KB
+constexpr int STAGE_BYTES = 2 * KV_BYTES;  // 64 KB
+constexpr int MERGE_BYTES = 4 * 16 * (HD + 2) * 4;  // per-warp O, m, l for the final merge
+constexpr int SMEM = NST * STAGE_BYTES + MERGE_BYTES + 2 * NST * 8 + 1024 + 64;
+
+SF_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+SF_DEV void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+SF_DEV void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+SF_DEV uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// 16-byte chunk c (0..15) of key row j in a [2 halves][128 keys][128 B] tile, 128B-swizzled the
+// way TMA SWIZZLE_128B writes each 128-byte row (chunk c' at c' ^ (j % 8))
+SF_DEV uint32_t swz(int j, int c) {
+  return (uint32_t)((c >> 3) * (CH * 128) + j * 128 + (((c & 7) ^ (j & 7)) << 4));
+}
+SF_DEV void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+struct Item {
+  int b, kvh, qt, nch;
+};
+
+}  // namespace
+
+// item = (b * Hkv + kvh) * ntiles + qt. Warps 0..3 compute, warp 4 produces.
+__global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__ CUtensorMap tmK,
+                                                        const __grid_constant__ CUtensorMap tmV, AttnParams p,
+                                                        int ntiles, int n_items) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  const uint32_t raw = smem_u32(sm_raw);
+  uint8_t* sm = sm_raw + (((raw + 1023u) & ~1023u) - raw);
+  const uint32_t sbase = smem_u32(sm);
+  float* mrg = reinterpret_cast<float*>(sm + NST * STAGE_BYTES);  // [4][16][HD] O, then [4][16] m, l
+  float* mrg_m = mrg + 4 * 16 * HD;
+  float* mrg_l = mrg_m + 4 * 16;
+  uint64_t* full = reinterpret_cast<uint64_t*>(mrg_l + 4 * 16);
+  uint64_t* empty = full + NST;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int G = p.Hq / p.Hkv;
+  const int R = p.q_len * G;
+
+  auto item_of = [&](int idx, Item& it) {
+    int r = idx;
+    it.qt = r % ntiles;
+    r /= ntiles;
+    it.kvh = r % p.Hkv;
+    it.b = r / p.Hkv;
+    const int r0 = it.qt * 16;
+    const int nr = min(16, R - r0);
+    const int kmax = min(p.pos0[it.b] + min(p.q_len - 1, (r0 + nr - 1) / G), p.max_key - 1);
+    it.nch = kmax / CH + 1;
+    return kmax;
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);  // one arrival per compute warp
+    }
+    fence_barrier_init();
+  }
+  // pages past a sequence's last key are not loaded; their (masked, p = 0) V rows must be finite
+  for (int i = tid; i < NST * STAGE_BYTES / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(sm)[i] = make_uint4(0u, 0u, 0u, 0u);
+  fence_proxy_async();
+  __syncthreads();
+
+  if (warp == 4) {
+    // ---- TMA producer
+    int seq = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      Item it;
+      const int kmax = item_of(item, it);
+      for (int c = 0; c < it.nch; ++c, ++seq) {
+        const int st = seq % NST;
+        mbar_wait(&empty[st], ((uint32_t)(seq / NST) & 1u) ^ 1u);
+        const int kstart = c * CH;
+        const int npages = (min(CH, kmax + 1 - kstart) + 15) / 16;
+        const int pg = (lane < npages) ? p.block_table[it.b * p.pages_per_seq + kstart / 16 + lane] : 0;
+        if (lane == 0) mbar_arrive_expect_tx(&full[st], (uint32_t)(npages * 4 * 16 * 128));
+        __syncwarp();
+        for (int i = 0; i < npages; ++i) {
+          const int blk = __shfl_sync(0xffffffffu, pg, i);
+          if (lane == 0) {
+            const int row = (blk * p.Hkv + it.kvh) * 16;
+            uint8_t* kb = sm + st * STAGE_BYTES;
+            uint8_t* vb = kb + KV_BYTES;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              tma_load_2d(kb + hf * (CH * 128) + i * 16 * 128, &tmK, &full[st], hf * 64, row, kEvictFirst);
+              tma_load_2d(vb + hf * (CH * 128) + i * 16 * 128, &tmV, &full[st], hf * 64, row, kEvictFirst);
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
+
+  // ---- compute warps
+  const float scale_log2 = 0.08838834764831845f * 1.4426950408889634f;  // log2(e) / sqrt(128)
+  int seq = 0;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    Item it;
+    item_of(item, it);
+    const int r0 = it.qt * 16;
+    const int nr = min(16, R - r0);
+    const int base = p.pos0[it.b];
+    // Q fragments (rows g, g+8 of the tile) from the fp32 rotated queries
+    uint32_t qa[8][4];
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      const int r = g + 8 * hr;
+      const bool ok = r < nr;
+      const int rr = r0 + (ok ? r : 0), qi = rr / G, h = it.kvh * G + rr % G;
+      const float* qrow = p.q + ((size_t)(it.b * p.q_len + qi) * p.Hq + h) * HD;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int d0 = kk * 16 + 2 * t4;
+        const float2 x0 = ok ? *reinterpret_cast<const float2*>(qrow + d0) : make_float2(0.f, 0.f);
+        const float2 x1 = ok ? *reinterpret_cast<const float2*>(qrow + d0 + 8) : make_float2(0.f, 0.f);
+        qa[kk][hr] = pack_bf16(x0.x, x0.y);
+        qa[kk][2 + hr] = pack_bf16(x1.x, x1.y);
+      }
+    }
+    const int pos_lo = base + (r0 + g) / G, pos_hi = base + (r0 + g + 8) / G;
+    const bool row_lo = g < nr, row_hi = g + 8 < nr;
+    float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;  // log2-domain running max
+    float o[16][4];
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[nt][i] = 0.f;
+
+    for (int c = 0; c < it.nch; ++c, ++seq) {
+      const int st = seq % NST;
+      mbar_wait(&full[st], (uint32_t)(seq / NST) & 1u);
+      const uint32_t kb = sbase + st * STAGE_BYTES, vb = kb + KV_BYTES;
+      const int kstart = c * CH + warp * 32;
+      // S = Q K_w^T for this warp's 32 keys
+      float s[4][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s[nt][i] = 0.f;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int key = warp * 32 + nt * 8 + (lane & 7);
+#pragma unroll
+        for (int kp = 0; kp < 4; ++kp) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(kb + swz(key, kp * 4 + (lane >> 3)), b0, b1, b2, b3);
+          mma16816(s[nt], qa[2 * kp], b0, b1);
+          mma16816(s[nt], qa[2 * kp + 1], b2, b3);
+        }
+      }
+      // mask, new running max (exact; masked entries excluded)
+      float cm_lo = -INFINITY, cm_hi = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int key = kstart + nt * 8 + 2 * t4 + (i & 1);
+          const bool hi = i >= 2;
+          const bool vis = hi ? (row_hi && key <= pos_hi) : (row_lo && key <= pos_lo);
+          const float v = vis ? s[nt][i] * scale_log2 : -INFINITY;
+          s[nt][i] = v;
+          if (hi) cm_hi = fmaxf(cm_hi, v); else cm_lo = fmaxf(cm_lo, v);
+        }
+#pragma unroll
+      for (int off = 1; off <= 2; off <<= 1) {
+        cm_lo = fmaxf(cm_lo, __shfl_xor_sync(0xffffffffu, cm_lo, off));
+        cm_hi = fmaxf(cm_hi, __shfl_xor_sync(0xffffffffu, cm_hi, off));
+      }
+      const float mn_lo = fmaxf(m_lo, cm_lo), mn_hi = fmaxf(m_hi, cm_hi);
+      const float a_lo = (mn_lo == -INFINITY) ? 1.f : exp2f(m_lo - mn_lo);
+      const float a_hi = (mn_hi == -INFINITY) ? 1.f : exp2f(m_hi - mn_hi);
+      m_lo = mn_lo;
+      m_hi = mn_hi;
+      // P (bf16 A fragments straight from the S accumulators) and its row sums
+      uint32_t pa[2][4];
+      float ps_lo = 0.f, ps_hi = 0.f;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        float e[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float M = i >= 2 ? mn_hi : mn_lo;
+          e[i] = (s[nt][i] == -INFINITY) ? 0.f : exp2f(s[nt][i] - M);
+        }
+        ps_lo += e[0] + e[1];
+        ps_hi += e[2] + e[3];
+        // k-step kk = nt/2 (16 keys): a0,a1 = n-tile 2kk (rows g, g+8); a2,a3 = n-tile 2kk+1
+        pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(e[0], e[1]);
+        pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(e[2], e[3]);
+      }
+#pragma unroll
+      for (int off = 1; off <= 2; off <<= 1) {
+        ps_lo += __shfl_xor_sync(0xffffffffu, ps_lo, off);
+        ps_hi += __shfl_xor_sync(0xffffffffu, ps_hi, off);
+      }
+      l_lo = l_lo * a_lo + ps_lo;
+      l_hi = l_hi * a_hi + ps_hi;
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt) {
+        o[nt][0] *= a_lo;
+        o[nt][1] *= a_lo;
+        o[nt][2] *= a_hi;
+        o[nt][3] *= a_hi;
+      }
+      // O += P V_w: 2 k-steps (this warp's 32 keys) x 16 n-tiles (128 dims)
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const uint32_t a[4] = {pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3]};
+#pragma unroll
+        for (int np = 0; np < 8; ++np) {
+          const int mi = lane >> 3, ri = lane & 7;
+          const int key = warp * 32 + kk * 16 + (mi & 1) * 8 + ri;
+          const int chunk = np * 2 + (mi >> 1);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(vb + swz(key, chunk), b0, b1, b2, b3);
+          mma16816(o[2 * np], a, b0, b1);
+          mma16816(o[2 * np + 1], a, b2, b3);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
+    }
+    // ---- merge the 4 warp states in fixed order and normalise
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      const int d = nt * 8 + 2 * t4;
+      *reinterpret_cast<float2*>(mrg + (warp * 16 + g) * HD + d) = make_float2(o[nt][0], o[nt][1]);
+      *reinterpret_cast<float2*>(mrg + (warp * 16 + g + 8) * HD + d) = make_float2(o[nt][2], o[nt][3]);
+    }
+    if (t4 == 0) {
+      mrg_m[warp * 16 + g] = m_lo;
+      mrg_m[warp * 16 + g + 8] = m_hi;
+      mrg_l[warp * 16 + g] = l_lo;
+      mrg_l[warp * 16 + g + 8] = l_hi;
+    }
+    named_bar(1, 128);
+    for (int e = tid; e < 16 * HD; e += 128) {
+      const int r = e / HD, d = e % HD;
+      if (r < nr) {
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, mrg_m[w * 16 + r]);
+        float L = 0.f, acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const float f = (mrg_m[w * 16 + r] == -INFINITY) ? 0.f : exp2f(mrg_m[w * 16 + r] - M);
+          L += mrg_l[w * 16 + r] * f;
+          acc += mrg[(w * 16 + r) * HD + d] * f;
+        }
+        const int rr = r0 + r, qi = rr / G, h = it.kvh * G + rr % G;
+        const int t = it.b * p.q_len + qi;
+        reinterpret_cast<__nv_bfloat16*>(p.out)[((size_t)t * p.Hq + h) * HD + d] = __float2bfloat16_rn(acc / L);
+      }
+    }
+    named_bar(1, 128);
+  }
+}
+
+static bool encode_kv_map(CUtensorMap* m, const void* base, long long rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)HD, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)HD * 2};
+  cuuint32_t box[2] = {64, 16};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
+  static bool attr = false;
+  static int num_sms = 148;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_fd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    attr = true;
+  }
+  const int G = p.Hq / p.Hkv;
+  const int ntiles = (p.q_len * G + 15) / 16;
+  const int n_items = p.B * p.Hkv * ntiles;
+  const int grid = std::min(n_items, num_sms);
+  CUtensorMap mk, mv;
+  const long long rows = (long long)p.n_pages * p.Hkv * 16;
+  if (!encode_kv_map(&mk, p.Kp, rows) || !encode_kv_map(&mv, p.Vp, rows)) return cudaErrorInvalidValue;
+  attn_fd_kernel<<<grid, 160, SMEM, s>>>(mk, mv, p, ntiles, n_items);
+  return cudaGetLastError();
+}
+
+}  // namespace sf

@@ -550,13 +550,7 @@ static cudaError_t attn_impl(const AttnParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 cudaError_t launch_attention(bool bf, const AttnParams& p, cudaStream_t s) {
-  if (bf && p.hd == 128) {
-    cudaError_t e = launch_attention_mma(p, s);
-    if (e != cudaSuccess) return e;
-    dim3 g2(p.B * p.q_len, p.Hq);
-    attn_combine_kernel<__nv_bfloat16><<<g2, 128, 0, s>>>(p);
-    return cudaGetLastError();
-  }
+  if (bf && p.hd == 128) return launch_attention_fd(p, s);  // flash-decoding, no split-KV partials
   if (bf) {
     switch (p.hd) {
       case 64: return attn_impl<__nv_bfloat16, 64>(p, s);

@@ -40,7 +40,8 @@ cudaError_t launch_rope_append(bool is_bf16, const void* qkv, int T, int q_len, 
                                const float2* rope, int Hq, int Hkv, int hd, const int* block_table,
                                int pages_per_seq, void* Kp, void* Vp, float* q_out, cudaStream_t s);
 cudaError_t launch_attention(bool is_bf16, const AttnParams& p, cudaStream_t s);
-cudaError_t launch_attention_mma(const AttnParams& p, cudaStream_t s);  // bf16, hd 128
+cudaError_t launch_attention_mma(const AttnParams& p, cudaStream_t s);  // bf16, hd 128 (split-KV)
+cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s);   // bf16, hd 128 (flash-decoding)
 cudaError_t launch_bidir_attention(bool is_bf16, const void* qkv, int B, int k, int Hq, int Hkv, int hd,
                                    bool causal, void* out, cudaStream_t s);
 cudaError_t launch_gather_rows(const float* src, int q_len, const int* idx, int const_idx, int B, int d,
