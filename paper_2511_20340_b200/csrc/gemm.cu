@@ -652,107 +652,102 @@ bool gemm_partial_geom(int T, int N, int K, PartialGeom* g) {
   return true;
 }
 
-// One CTA (512 threads) per virtual row. For every 128-column tile the k-segment owners are
-// precomputed in shared memory (first group, count, slot parity of the first one); each thread then
-// issues the loads of 4 columns x up to 8 segments back to back before summing them in k order.
-constexpr int kRnThreads = 512;
-constexpr int kRnMaxSeg = 8;
+// One CTA (256 threads) per virtual row; thread t owns the float4 column groups 4t + 1024 j. Per
+// 128-column tile the k-segment slot offsets are precomputed in shared memory; all loads of a
+// thread (residual + up to 8 segments x 4 groups, 16-byte vectors) are issued before the k-ordered
+// sums, so the kernel streams at memory speed.
+constexpr int kRnThreads = 256;
+constexpr int rn_max_seg(int NG) { return NG >= 8 ? 4 : 32 / NG; }  // register budget: NG x segs float4
 
+template <int NG>  // float4 groups per thread (d = 1024 NG)
 __global__ void __launch_bounds__(kRnThreads) resid_norm_kernel(
     const float* __restrict__ partial, int G, int kb, int CG, int n_tiles_cta, int T, int rep, int d,
     const float* resid, const float* __restrict__ bias, float* out, float* tap, const float* __restrict__ gamma,
     float eps, __nv_bfloat16* xn) {
-  __shared__ int seg_lo[128], seg_n[128], seg_w0[128];
+  constexpr int kRnMaxSeg = rn_max_seg(NG);
+  __shared__ int seg_n[128];
+  __shared__ int seg_off[128][kRnMaxSeg];  // slot * T * 128 (the tile's k segments, k order)
   __shared__ float red[kRnThreads / 32];
   const int r = blockIdx.x;
   const int src_row = r / rep, col0 = (r % rep) * d;
   const int tid = threadIdx.x;
-  const int groups = G / CG;
-  const int n_tiles_grp = n_tiles_cta / CG;
-  const long long U = (long long)n_tiles_grp * kb;
   if (partial) {
-    for (int tg = tid; tg < n_tiles_grp; tg += kRnThreads) {
+    const int groups = G / CG;
+    const int n_tiles_grp = n_tiles_cta / CG;
+    const long long U = (long long)n_tiles_grp * kb;
+    for (int vt = tid; vt < n_tiles_cta; vt += kRnThreads) {
+      const int tg = vt / CG, rk = vt % CG;
       const long long ua = (long long)tg * kb, ub = ua + kb - 1;
       const int lo = (int)(((ua + 1) * groups + U - 1) / U) - 1;
       const int hi = (int)(((ub + 1) * groups + U - 1) / U) - 1;
-      seg_lo[tg] = lo;
-      seg_n[tg] = hi - lo + 1;
-      seg_w0[tg] = ((U * lo / groups) / kb == tg) ? 0 : 1;  // slot parity of the first segment
+      const int w0 = ((U * lo / groups) / kb == tg) ? 0 : 1;
+      seg_n[vt] = hi - lo + 1;
+      for (int q = 0; q < kRnMaxSeg && lo + q <= hi; ++q)
+        seg_off[vt][q] = ((2 * (lo + q) + (q == 0 ? w0 : 0)) * CG + rk) * T * BM;
     }
     __syncthreads();
   }
-  const size_t slot_stride = (size_t)T * BM;
-  constexpr int CPT = 16;  // columns per thread kept in registers (d <= 8192)
-  float xv[CPT];
+  float4 x[NG];
   float ss = 0.f;
 #pragma unroll
-  for (int j0 = 0; j0 < CPT; j0 += 4) {
-    float acc[4];
-    int nn[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int i = tid + (j0 + j) * kRnThreads;
-      nn[j] = i;
-      acc[j] = 0.f;
-      if (i < d) {
-        acc[j] = resid ? resid[(size_t)r * d + i] : 0.f;
-        if (bias) acc[j] += bias[col0 + i];
-      }
+  for (int j = 0; j < NG; ++j) {
+    const int i = 4 * tid + 1024 * j;  // column within the virtual row
+    x[j] = resid ? *reinterpret_cast<const float4*>(resid + (size_t)r * d + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (bias) {
+      const float4 bb = *reinterpret_cast<const float4*>(bias + col0 + i);
+      x[j].x += bb.x;
+      x[j].y += bb.y;
+      x[j].z += bb.z;
+      x[j].w += bb.w;
     }
-    if (partial) {
-      float pv[4][kRnMaxSeg];
-      int cnt[4];
+  }
+  if (partial) {
+    float4 pv[NG][kRnMaxSeg];
+    int ns[NG];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int i = nn[j];
-        cnt[j] = 0;
-        if (i < d) {
-          const int n = col0 + i;
-          const int vt = n / BM, m = n % BM, tg = vt / CG, rk = vt % CG;
-          const int lo = seg_lo[tg], ns = seg_n[tg], w0 = seg_w0[tg];
-          cnt[j] = ns;
-          const float* basep = partial + (size_t)src_row * BM + m + (size_t)rk * slot_stride;
+    for (int j = 0; j < NG; ++j) {
+      const int n = col0 + 4 * tid + 1024 * j;
+      const int vt = n / BM, m = n % BM;
+      ns[j] = seg_n[vt];
+      const float* bp = partial + (size_t)src_row * BM + m;
 #pragma unroll
-          for (int q = 0; q < kRnMaxSeg; ++q)
-            if (q < ns) {
-              const int g = lo + q;
-              const int which = (q == 0) ? w0 : 0;
-              pv[j][q] = __ldcg(basep + (size_t)((2 * g + which) * CG) * slot_stride);
-            }
+      for (int q = 0; q < kRnMaxSeg; ++q)
+        if (q < ns[j]) pv[j][q] = __ldcg(reinterpret_cast<const float4*>(bp + seg_off[vt][q]));
+    }
+#pragma unroll
+    for (int j = 0; j < NG; ++j)
+#pragma unroll
+      for (int q = 0; q < kRnMaxSeg; ++q)
+        if (q < ns[j]) {  // k order
+          x[j].x += pv[j][q].x;
+          x[j].y += pv[j][q].y;
+          x[j].z += pv[j][q].z;
+          x[j].w += pv[j][q].w;
         }
-      }
+  }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-#pragma unroll
-        for (int q = 0; q < kRnMaxSeg; ++q)
-          if (q < cnt[j]) acc[j] += pv[j][q];
-        if (cnt[j] > kRnMaxSeg) {  // segments beyond the unrolled window, still in k order
-          const int n = col0 + nn[j];
-          const int vt = n / BM, m = n % BM, tg = vt / CG, rk = vt % CG;
-          const float* basep = partial + (size_t)src_row * BM + m + (size_t)rk * slot_stride;
-          for (int q = kRnMaxSeg; q < cnt[j]; ++q)
-            acc[j] += __ldcg(basep + (size_t)((2 * (seg_lo[tg] + q)) * CG) * slot_stride);
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int i = nn[j];
-      xv[j0 + j] = acc[j];
-      if (i < d) {
-        if (out) out[(size_t)r * d + i] = acc[j];
-        if (tap) tap[(size_t)r * d + i] = acc[j];
-        ss = fmaf(acc[j], acc[j], ss);
-      }
-    }
+  for (int j = 0; j < NG; ++j) {
+    const int i = 4 * tid + 1024 * j;
+    if (out) *reinterpret_cast<float4*>(out + (size_t)r * d + i) = x[j];
+    if (tap) *reinterpret_cast<float4*>(tap + (size_t)r * d + i) = x[j];
+    ss = fmaf(x[j].x, x[j].x, ss);
+    ss = fmaf(x[j].y, x[j].y, ss);
+    ss = fmaf(x[j].z, x[j].z, ss);
+    ss = fmaf(x[j].w, x[j].w, ss);
   }
   if (!gamma) return;
   ss = block_sum<kRnThreads>(ss, red);
   const float rs = 1.0f / sqrtf(ss / (float)d + eps);
 #pragma unroll
-  for (int j = 0; j < CPT; ++j) {
-    const int i = tid + j * kRnThreads;
-    if (i < d) xn[(size_t)r * d + i] = __float2bfloat16_rn(xv[j] * rs * gamma[i]);
+  for (int j = 0; j < NG; ++j) {
+    const int i = 4 * tid + 1024 * j;
+    const float4 gg = *reinterpret_cast<const float4*>(gamma + i);
+    __nv_bfloat162 lo = __floats2bfloat162_rn(x[j].x * rs * gg.x, x[j].y * rs * gg.y);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(x[j].z * rs * gg.z, x[j].w * rs * gg.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(xn + (size_t)r * d + i) = pk;
   }
 }
 
@@ -760,7 +755,7 @@ cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T,
                               const float* bias, float* out, float* tap, const float* gamma, float eps,
                               __nv_bfloat16* xn, cudaStream_t st) {
   if (T * rep <= 0) return cudaSuccess;
-  if (d > kRnThreads * 16) return cudaErrorInvalidValue;
+  if (d % 1024 || d > 8192) return cudaErrorInvalidValue;  // caller falls back to the unfused path
   int G = 1, kb = 1, CG = 1, nt = 1, Tslot = T;
   if (partial) {
     G = g->G;
@@ -768,11 +763,34 @@ cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T,
     nt = g->n_tiles;
     CG = gemm_cg(nt * BM, kb * BK);
     Tslot = g->T;
-    if (nt / CG > 128) return cudaErrorInvalidValue;
+    if (nt > 128) return cudaErrorInvalidValue;
+    // every tile must have <= rn_max_seg k segments
+    const int groups = G / CG;
+    if ((groups + nt / CG - 1) / (nt / CG) + 1 > rn_max_seg(d / 1024)) return cudaErrorInvalidValue;
   }
-  resid_norm_kernel<<<T * rep, kRnThreads, 0, st>>>(partial, G, kb, CG, nt, Tslot, rep, d, resid, bias, out, tap,
-                                                    gamma, eps, xn);
+#define SF_RN(NG)                                                                                               \
+  resid_norm_kernel<NG><<<T * rep, kRnThreads, 0, st>>>(partial, G, kb, CG, nt, Tslot, rep, d, resid, bias, out, \
+                                                        tap, gamma, eps, xn)
+  switch (d / 1024) {
+    case 1: SF_RN(1); break;
+    case 2: SF_RN(2); break;
+    case 4: SF_RN(4); break;
+    case 5: SF_RN(5); break;
+    case 8: SF_RN(8); break;
+    default: return cudaErrorInvalidValue;
+  }
+#undef SF_RN
   return cudaGetLastError();
+}
+
+// Whether the fused consumer supports this (d, N, K): callers use the unfused path otherwise.
+bool resid_norm_supported(int d, int T, int N, int K) {
+  if (d % 1024 || d > 8192 || (d / 1024 == 3) || (d / 1024 == 6) || (d / 1024 == 7)) return false;
+  PartialGeom g;
+  if (!gemm_partial_geom(T, N, K, &g)) return false;
+  const int CG = gemm_cg(N, K);
+  const int groups = g.G / CG, ntg = g.n_tiles / CG;
+  return (groups + ntg - 1) / ntg + 1 <= rn_max_seg(d / 1024) && g.n_tiles <= 128;
 }
 
 static cudaError_t gemm_launch_chunk(bool is_bf16, const void* A, int lda, const void* W, bool w_tiled, int T,

@@ -58,6 +58,7 @@ bool gemm_partial_geom(int T, int N, int K, PartialGeom* g);  // false if EPI_PA
 //   x = (resid ? resid[r] : 0) + (bias ? bias[col] : 0) + sum_k-segments partial   (fixed order)
 //   out[r] = x (fp32, out may alias resid); tap[r] = x (optional);
 //   xn[r] = bf16(x / sqrt(mean(x^2) + eps) * gamma) (optional, gamma != null)
+bool resid_norm_supported(int d, int T, int N, int K);
 cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T, int rep, int d, const float* resid,
                               const float* bias, float* out, float* tap, const float* gamma, float eps,
                               __nv_bfloat16* xn, cudaStream_t s);

@@ -337,6 +337,7 @@ static bool gemm_resid_norm(sf_handle* h, cudaError_t* err, const void* A, int l
                             int K, int rep, const float* resid, const float* bias, float* out, float* tap,
                             const float* gamma) {
   if (!h->bf || T > 512) return false;
+  if (!resid_norm_supported(h->p.d, T, N, K)) return false;
   PartialGeom g;
   if (!gemm_partial_geom(T, N, K, &g)) return false;
   GemmEpi e;

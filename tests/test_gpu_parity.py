@@ -226,3 +226,21 @@ def test_hd128_bf16_matches_oracle_and_sd_equals_ar(cfg):
     res2 = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True, block_table=perm)
     for s1, s2 in zip(res["steps"], res2["steps"]):
         assert np.array_equal(s1["logits"], s2["logits"])
+
+
+# ------------------------------------------------------------------ 7B width, depth 2 (fused paths)
+W7D2 = get_config("7b").replace(name="7b-d2", n_layers=2, batch=3, prompt_len=200, gen_len=10)
+GQA2K = get_config("70b").replace(name="70b-w2k", n_layers=2, d_model=2048, n_heads=16, n_kv_heads=2,
+                                  d_ff=5632, batch=2, prompt_len=150, gen_len=8)
+
+
+@pytest.mark.parametrize("cfg", [W7D2, GQA2K], ids=["7b_width_depth2", "gqa_d2048"])
+def test_full_width_depth2_bf16(cfg):
+    """Reading C21 (iii)/(iv): full-width bf16 at depth 2 -- logits rel-L2 <= 2.2e-2 and tokens exact
+    where the oracle margin > 5e-2; GPU SD == GPU AR bit-exact; exercises the fused partial-GEMM ->
+    residual/RMSNorm consumer and the flash-decoding attention at d = 4096 / GQA."""
+    w, prompts = setup(cfg, seed=7, jitter=0.1)
+    res = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True)
+    assert _check_bf16(cfg, w, prompts, res, seqs=(0,), rel_tol=2.2e-2) > 10
+    ar = run_gpu(cfg, w, prompts, cfg.gen_len, k=0)
+    assert ar["tokens"] == res["tokens"]
