@@ -88,39 +88,40 @@ class ClockSampler:
 # --------------------------------------------------------------------------- oracle leg
 def oracle_sample(cfg, n_steps=2, prompt_len=32):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload: ONE sequence at the
-    config's full width with the base truncated to L = 1 and L = 2 layers (same head), prompt
-    `prompt_len`, `n_steps` SD steps each. Per-step time at full depth is extrapolated linearly in
-    L: t(L) = t(1) + (L - 1) (t(2) - t(1)). The oracle computes sequences one by one, so the
-    box-level tokens/s = tokens per step per sequence / t(L_full)."""
-    import numpy as np
+    config's full width with the base truncated to L = 1 and L = 2 layers (same SpecFormer head),
+    prompt `prompt_len`. For each depth, oracle.sd_decode runs twice -- 1 + s1 and 1 + s1 + s2
+    tokens -- and the difference of the two wall times divided by the difference of their step
+    counts is the per-step time (the prefill cancels). Full depth is extrapolated linearly in L:
+    t(L) = t(1) + (L - 1) (t(2) - t(1)). The oracle computes sequences one by one, so the box-level
+    tokens/s = tokens per step per sequence / t(L_full)."""
     import oracle as O
     from synth import make_prompts, make_weights
 
     c2 = cfg.replace(n_layers=2)
     w = make_weights(c2, seed=0, device="cpu")
     prompt = make_prompts(1, prompt_len, cfg.vocab)[0].tolist()
-    times = {}
-    toks = {}
+    times, toks = {}, {}
+    s1, s2 = 1, n_steps
     for L in (1, 2):
         W = O.Weights(cfg.replace(n_layers=L), w)
-        # the oracle's own loop: prefill (untimed part subtracted) then n_steps SD steps
+        O.sd_decode(W, prompt, 2)  # warm the fp64 weight cache (upcast) outside the timing
         t0 = time.perf_counter()
-        cache = O.model._new_cache(W.cfg)
-        _, i_d, _ = O.prefill(W, prompt, cache)
+        _, st_a = O.sd_decode(W, prompt, 1 + s1)
         t1 = time.perf_counter()
-        out, steps = O.sd_decode(W, prompt, 1 + n_steps)  # includes its own prefill
+        _, st_b = O.sd_decode(W, prompt, 1 + s1 + s2)
         t2 = time.perf_counter()
-        # sd_decode = prefill + steps; subtract the separately timed prefill
-        times[L] = max(1e-9, ((t2 - t1) - (t1 - t0)) / max(1, len(steps)))
-        toks[L] = sum(s["m"] + 1 for s in steps) / max(1, len(steps))
-    t_full = times[1] + (cfg.n_layers - 1) * (times[2] - times[1])
+        dsteps = max(1, len(st_b) - len(st_a))
+        times[L] = max(1e-6, ((t2 - t1) - (t1 - t0)) / dsteps)
+        toks[L] = sum(s["m"] + 1 for s in st_b) / max(1, len(st_b))
+    t_full = times[1] + (cfg.n_layers - 1) * max(0.0, times[2] - times[1])
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     a = toks[2]
     return {"value": a / t_full, "unit": "tokens/s", "cores": cores, "kind": "oracle",
             "sample": f"1 sequence, width {cfg.d_model}, base depth 1 and 2 of {cfg.n_layers} layers "
-                      f"(linear extrapolation in L), prompt {prompt_len}, {n_steps} SD steps each; "
-                      f"t_step(L=1)={times[1]:.3f}s t_step(L=2)={times[2]:.3f}s -> t_step(L={cfg.n_layers})="
-                      f"{t_full:.2f}s per sequence; sequences are processed one at a time",
+                      f"(linear extrapolation in L), prompt {prompt_len}, per-step time from the difference "
+                      f"of {1 + s1} vs {1 + s1 + s2} generated tokens; t_step(L=1)={times[1]:.3f}s "
+                      f"t_step(L=2)={times[2]:.3f}s -> t_step(L={cfg.n_layers})={t_full:.2f}s per sequence; "
+                      f"sequences are processed one at a time (numpy fp64, BLAS threads = {cores})",
             "seconds_per_step_per_sequence": t_full}
 
 
@@ -131,7 +132,7 @@ def run_reference(args, cfg):
     for _ in range(args.warmup):
         pass  # the oracle has no warm-up state; warm-up steps are part of each sample below
     t0 = time.perf_counter()
-    cb = oracle_sample(cfg, n_steps=max(1, min(args.steps, 3)))
+    cb = oracle_sample(cfg, n_steps=max(2, min(args.steps, 4)))
     wall = time.perf_counter() - t0
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -154,7 +155,7 @@ def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
 
-    from paper_2511_20340_b200 import Engine, EngineConfig, roofline
+    from paper_2511_20340_b200 import Engine, EngineConfig, dp, roofline
     from paper_2511_20340_b200 import _native as N
     from synth import make_prompts, make_weights
 
@@ -177,7 +178,7 @@ def run_ours(args, cfg):
     eng = Engine(ec, weights)
     del weights
     torch.cuda.empty_cache()
-    prompts = make_prompts(B * world, P, cfg.vocab)[rank * B:(rank + 1) * B].contiguous()
+    prompts = dp.shard_rows(make_prompts(B * world, P, cfg.vocab), rank, world)  # weak scaling
 
     eng.prefill(prompts.cuda())
     eng.decode_steps(W)
@@ -201,15 +202,7 @@ def run_ours(args, cfg):
     launches = eng.kernel_launches()
     after = eng.capture(3, (B,), torch.int32).cpu()
     tokens = int((after - before).sum())
-    stats = torch.tensor([ms, float(tokens)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        mx = stats.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = stats.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms_max, tokens_total = float(mx[0]), float(sm[1])
-    else:
-        ms_max, tokens_total = ms, float(tokens)
+    ms_max, tokens_total = dp.reduce_timing(ms, float(tokens), device="cuda")
     value = tokens_total / (ms_max / 1e3)
     steps_per_s = K / (ms_max / 1e3)
     a_meas = tokens / (K * B)
@@ -243,12 +236,31 @@ def run_ours(args, cfg):
         lens = [n + m + 1 for n, m in zip(lens, accs[s])]
     gemm_ms, gemm_n, gemm_bytes = cls[0]
     attn_ms, attn_n, _ = cls[1]
+    # GEMM FLOPs of the profiled steps (2 T N K summed over the step's contractions)
+    gemm_flops = 0.0
+    d_, F_, V_ = cfg.d_model, cfg.d_ff, cfg.vocab
+    qkv_ = (cfg.n_heads + 2 * cfg.n_kv_heads) * cfg.head_dim
+    ao_ = cfg.n_heads * cfg.head_dim
+    Tv, Td = B * (k + 1), B * k
+    per_layer = qkv_ * d_ + d_ * ao_ + 2 * F_ * d_ + d_ * F_
+    gemm_flops = 2.0 * Kp * (Tv * (cfg.n_layers * per_layer + V_ * d_)
+                             + Tv * (4 * d_ * d_ + qkv_ * d_ + d_ * ao_)
+                             + B * k * d_ * d_ + Td * (qkv_ * d_ + d_ * ao_ + 3 * F_ * d_ + V_ * d_))
     dominant = "gemm" if gemm_ms >= attn_ms else "attention"
     if dominant == "gemm":
-        achieved = gemm_bytes / (gemm_ms / 1e3) / 1e9
-        dom_bytes_per_launch = gemm_bytes / max(1, gemm_n)
+        t_hbm = gemm_bytes / (hbm * 1e9)
+        t_tc = gemm_flops / (tf_sust * 1e12)
+        if t_tc > t_hbm:  # compute-bound at this batch: judge against the sustained bf16 peak
+            bound, unit, achieved, peak_v = "tensor", "TFLOP/s", gemm_flops / (gemm_ms / 1e3) / 1e12, tf_sust
+            peak_src = peak_src + " (bf16_tflops_sustained: kernel timed inside the step)"
+            dom_units = gemm_flops
+        else:
+            bound, unit, achieved, peak_v = "hbm", "GB/s", gemm_bytes / (gemm_ms / 1e3) / 1e9, hbm
+            dom_units = gemm_bytes
+        dom_bytes_per_launch = dom_units / max(1, gemm_n)
         dom_ms = gemm_ms / max(1, gemm_n)
     else:
+        bound, unit, peak_v = "hbm", "GB/s", hbm
         achieved = attn_bytes / (attn_ms / 1e3) / 1e9
         dom_bytes_per_launch = attn_bytes / max(1, attn_n)
         dom_ms = attn_ms / max(1, attn_n)
@@ -263,6 +275,7 @@ def run_ours(args, cfg):
                            cls[c][0] / max(1e-9, prof_ms_total)}
                     for c, name in enumerate(["gemm", "attention", "norm", "argmax"])}
     prof_classes["gemm"]["achieved_gbs"] = gemm_bytes / max(1e-12, gemm_ms / 1e3) / 1e9
+    prof_classes["gemm"]["achieved_tflops"] = gemm_flops / max(1e-12, gemm_ms / 1e3) / 1e12
     prof_classes["attention"]["achieved_gbs"] = attn_bytes / max(1e-12, attn_ms / 1e3) / 1e9
     # whole-step roofline over the timed (graph) region, lengths reconstructed from the accept log
     lens_t = before.tolist()
@@ -299,15 +312,7 @@ def run_ours(args, cfg):
         raise RuntimeError("e2e C-ABI call failed")
     e2e_ms = x0.elapsed_time(x1)
     e2e_tokens = B + int((em_host >= 0).sum())
-    e2 = torch.tensor([e2e_ms, float(e2e_tokens)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        mx = e2.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = e2.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        e2e_ms_max, e2e_tok = float(mx[0]), float(sm[1])
-    else:
-        e2e_ms_max, e2e_tok = e2e_ms, float(e2e_tokens)
+    e2e_ms_max, e2e_tok = dp.reduce_timing(e2e_ms, float(e2e_tokens), device="cuda")
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -331,9 +336,9 @@ def run_ours(args, cfg):
             "mean_accepted_length": a_meas,
             "modeled_tokens_per_s_at_paper_a": steps_per_s * B * world * A_PAPER.get(cfg.name, 1.75),
             "a_paper": A_PAPER.get(cfg.name),
-            "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                         "bytes_per_launch": dom_bytes_per_launch, "ms_per_launch": dom_ms,
+            "roofline": {"bound": bound, "kernel": dominant, "achieved": achieved, "peak": peak_v, "unit": unit,
+                         "frac": achieved / peak_v, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_units_per_launch": dom_bytes_per_launch, "ms_per_launch": dom_ms,
                          "classes": prof_classes, "profiled_steps": Kp},
             "step_roofline": {"bound": "hbm", "achieved": step_gbs, "peak": hbm, "unit": "GB/s",
                               "frac": step_gbs / hbm, "bytes_per_step": sb / K,
