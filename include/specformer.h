@@ -178,6 +178,16 @@ sf_status sf_pack_matrix(int32_t dtype, const void* src_dev, void* dst_dev, int6
  * 2 (A bf16, W already in layout 1). out dev fp32. Uses the same kernels as the hot path. */
 sf_status sf_test_gemm(int32_t dtype, const void* A, const void* W, float* out, int32_t T, int32_t N, int32_t K,
                        void* stream);
+/* Tools only: when the process ran with SF_GEMM_TRACE=1, copy (and clear) the per-CTA %globaltimer
+ * timeline (ns; [CTA][64] uint64, slot map in csrc/gemm.cu) of the last tcgen05 GEMM launches into
+ * host memory dst_host (cap entries). Returns the number of entries copied, 0 if tracing is off. */
+int32_t sf_debug_gemm_trace(uint64_t* dst_host, int32_t cap);
+/* Tools only: when the process ran with SF_KTRACE=1, copy (and clear) the kernel timeline: one
+ * 40-byte record per CTA of every kernel launched since the last call -- {uint32 kind<<24|param,
+ * uint32 smid, uint64 start_ns, uint64 dependency_resolved_ns, uint64 end_ns, uint64 0} -- into
+ * host memory dst_host (cap records). Synchronises the device. Returns the number of records
+ * copied, 0 if tracing is off. */
+int32_t sf_debug_ktrace(void* dst_host, int32_t cap);
 
 #ifdef __cplusplus
 }

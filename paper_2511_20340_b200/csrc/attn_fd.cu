@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
   uint64_t* full = reinterpret_cast<uint64_t*>(mrg_l + 4 * 16);
   uint64_t* empty = full + NST;
 
+  KtScope kt_(KT_ATTN, (uint32_t)p.q_len);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int G = p.Hq / p.Hkv;
@@ -108,6 +109,9 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
     reinterpret_cast<uint4*>(sm)[i] = make_uint4(0u, 0u, 0u, 0u);
   fence_proxy_async();
   __syncthreads();
+  pdl_wait();  // queries, lengths and the new KV rows come from the previous kernels
+  kt_.mark();
+  pdl_trigger();
 
   if (warp == 4) {
     // ---- TMA producer
@@ -343,8 +347,16 @@ cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
   CUtensorMap mk, mv;
   const long long rows = (long long)p.n_pages * p.Hkv * 16;
   if (!encode_kv_map(&mk, p.Kp, rows) || !encode_kv_map(&mv, p.Vp, rows)) return cudaErrorInvalidValue;
-  attn_fd_kernel<<<grid, 160, SMEM, s>>>(mk, mv, p, ntiles, n_items);
+  launch_k(attn_fd_kernel, dim3(grid), dim3(160), SMEM, s, mk, mv, p, ntiles, n_items);
   return cudaGetLastError();
+}
+
+cudaError_t kt_setup_attn_fd(void* rec, unsigned* cnt, unsigned cap) {
+  KtBuf b;
+  b.rec = reinterpret_cast<KtRec*>(rec);
+  b.cnt = cnt;
+  b.cap = cap;
+  return kt_setup_tu(b);
 }
 
 }  // namespace sf

@@ -80,6 +80,10 @@ struct Item {
 __global__ void __launch_bounds__(160, 1) attn_mma_kernel(const __grid_constant__ CUtensorMap tmK,
                                                          const __grid_constant__ CUtensorMap tmV, AttnParams p,
                                                          int ntiles, int nsplit, int n_items) {
+  KtScope kt_(KT_ATTN, (uint32_t)(1));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   const uint32_t raw = smem_u32(sm_raw);
   uint8_t* sm = sm_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -372,8 +376,16 @@ cudaError_t launch_attention_mma(const AttnParams& p, cudaStream_t s) {
   CUtensorMap mk, mv;
   const long long rows = (long long)p.n_pages * p.Hkv * 16;
   if (!encode_kv_map(&mk, p.Kp, rows) || !encode_kv_map(&mv, p.Vp, rows)) return cudaErrorInvalidValue;
-  attn_mma_kernel<<<grid, 160, SMEM, s>>>(mk, mv, p, ntiles, nsplit, n_items);
+  launch_k(attn_mma_kernel, dim3(grid), dim3(160), SMEM, s, mk, mv, p, ntiles, nsplit, n_items);
   return cudaGetLastError();
+}
+
+cudaError_t kt_setup_attn_mma(void* rec, unsigned* cnt, unsigned cap) {
+  KtBuf b;
+  b.rec = reinterpret_cast<KtRec*>(rec);
+  b.cnt = cnt;
+  b.cap = cap;
+  return kt_setup_tu(b);
 }
 
 }  // namespace sf

@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <utility>
+
 #define SF_DEV __device__ __forceinline__
 
 namespace sf {
@@ -52,6 +55,93 @@ SF_DEV float block_sum(float v, float* red /* >= NT/32 floats */) {
   __syncthreads();
   return red[0];
 }
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of the step is launched with programmatic stream serialisation: it may start while
+// its predecessor drains, does only dependency-free work (barrier init, TMEM alloc, smem clears,
+// weight prefetch) before pdl_wait(), and lets its own successor launch once all of its CTAs have
+// passed pdl_wait() (pdl_trigger()). pdl_wait() returns when every prerequisite grid has completed
+// and its memory is visible, so the chain stays fully ordered. No-ops without the launch attribute.
+SF_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SF_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = !(getenv("SF_NO_PDL") && atoi(getenv("SF_NO_PDL")) > 0);
+  return on;
+}
+// <<<grid, block, smem, stream>>> with the PDL attribute (and an optional cluster shape).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// ---------------------------------------------------------------- kernel timeline (tools only)
+// With SF_KTRACE=1 every kernel's recorder thread appends (kernel id, SM, start, dependency
+// resolved, end) %globaltimer stamps to a device log (tools/ktrace.py reconstructs the per-launch
+// timeline of a CUDA-graph step). Off by default: one predicated load per CTA.
+enum KtKind : uint32_t {
+  KT_GEMM = 1, KT_RESID_NORM, KT_ROPE, KT_ATTN, KT_RMSNORM, KT_GROUP_RMS, KT_EMBED, KT_ARGMAX_P, KT_ARGMAX_F,
+  KT_ACCEPT, KT_BIDIR, KT_GATHER, KT_ROWS, KT_GEMM_SIMT, KT_ATTN_PART, KT_ATTN_COMB, KT_MISC
+};
+struct KtRec {
+  uint32_t kid, smid;
+  unsigned long long t0, tw, t1;
+  unsigned long long pad;
+};
+struct KtBuf {
+  KtRec* rec;
+  unsigned* cnt;
+  unsigned cap;
+};
+static __device__ KtBuf g_kt;  // one per translation unit, set by kt_setup_*()
+SF_DEV unsigned long long kt_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct KtScope {
+  unsigned long long t0 = 0, tw = 0;
+  uint32_t kid = 0;
+  bool on = false;
+  SF_DEV KtScope(uint32_t kind, uint32_t param, int who = 0) {
+    if (g_kt.rec && (int)threadIdx.x == who) {
+      on = true;
+      kid = (kind << 24) | (param & 0xFFFFFFu);
+      t0 = kt_now();
+    }
+  }
+  SF_DEV void mark() {
+    if (on) tw = kt_now();
+  }
+  SF_DEV ~KtScope() {
+    if (!on) return;
+    const unsigned i = atomicAdd(g_kt.cnt, 1u);
+    if (i < g_kt.cap) {
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      KtRec r;
+      r.kid = kid;
+      r.smid = sm;
+      r.t0 = t0;
+      r.tw = tw ? tw : t0;
+      r.t1 = kt_now();
+      r.pad = 0;
+      g_kt.rec[i] = r;
+    }
+  }
+};
+static inline cudaError_t kt_setup_tu(const KtBuf& b) { return cudaMemcpyToSymbol(g_kt, &b, sizeof(b)); }
 
 // ---------------------------------------------------------------- PTX wrappers (sm_100a)
 SF_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }

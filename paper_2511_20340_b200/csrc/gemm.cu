@@ -58,14 +58,29 @@ SF_DEV float silu_f(float g) { return g / (1.f + expf(-g)); }
 // of the next.
 struct SkParams {
   int T, N, K;
-  int NT, n_sub, stages, kb_total, n_tiles, G, nbuf, w_tiled;
+  int Tp;  // T rounded up to 32 (row stride of the fixup partial slots)
+  int NT, n_sub, stages, kb_total, n_tiles, G, nbuf, w_tiled, w_tma, stage_ok, bulk_ok;
   int cgrp;  // ring slots released per tcgen05.commit
   uint32_t tmem_cols;
   const __nv_bfloat16* w_tiles;  // tile-contiguous weights (w_tiled, CG == 1 bulk path)
   GemmEpi epi;
   float* partial;  // [CTAs][T][128]
   int* flags;      // [CTAs]
+  unsigned long long* trace;  // optional per-CTA timeline (SF_GEMM_TRACE=1, tools only): [CTA][64]
 };
+
+SF_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// trace slots: 0 start, 1 setup done, 2 producer first issue, 3 MMA first full, 4 MMA last issue,
+// 5 epilogue done, 8 + 4 s + {0 MMA seg start, 1 MMA seg issued, 2 epi seg ready, 3 epi seg done}
+// (s < 4), 24 + i: MMA full-barrier pass of unit i (i < 40)
+#define SF_TR(i) \
+  do {           \
+    if (p.trace) p.trace[(size_t)blockIdx.x * 128 + (i)] = gtimer(); \
+  } while (0)
 
 SF_DEV void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 SF_DEV int ld_acquire(const int* p) {
@@ -128,7 +143,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   uint64_t* empty = full + p.stages;
   uint64_t* accf = empty + p.stages;  // [2]
   uint64_t* acce = accf + 2;          // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+  uint64_t* fixb = acce + 2;           // bulk fixup loads (last-segment heads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 3);
   
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = (CG == 2) ? cluster_rank() : 0u;
@@ -138,18 +154,21 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   const long long U = (long long)p.n_tiles * kb;
   const long long u0 = U * c / p.G, u1 = U * (c + 1) / p.G;
   const int cols = p.n_sub * p.NT;
+  if (threadIdx.x == 0) SF_TR(0);
+  KtScope kt_(KT_GEMM, (uint32_t)p.N, 128);
 
   if (threadIdx.x == 0) {
-    if (!(CG == 1 && p.w_tiled)) prefetch_tmap(&tmW);
+    if (!(CG == 1 && p.w_tiled && !p.w_tma)) prefetch_tmap(&tmW);
     prefetch_tmap(&tmA);
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(&full[s], CG);  // leader: own arrive_expect_tx (+ the peer's forwarded arrival)
+      mbar_init(&full[s], 1);  // leader: one arrive_expect_tx covering both CTAs' bytes
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
       mbar_init(&acce[b], CG);  // leader: both CTAs' epilogues release the accumulator
     }
+    mbar_init(fixb, 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -167,22 +186,51 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   if constexpr (CG == 2) cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) SF_TR(1);
 
   if (warp == 0) {
     // ---- TMA producer warp (converged; one elected lane issues)
+    // The weights do not depend on the previous kernel: the first ring's worth of weight tiles is
+    // requested before the grid dependency resolves (PDL), the activation tiles after it.
+    const long long npre = (CG == 1 && p.w_tiled) ? min((long long)p.stages, u1 - u0) : 0;
+    if (npre > 0 && elect_one()) {
+      int tp = (int)(u0 / kb), kp = (int)(u0 % kb);
+      for (int i = 0; i < (int)npre; ++i) {
+        uint8_t* st = smem + (size_t)i * stage_bytes;
+        mbar_arrive_expect_tx(&full[i], (uint32_t)stage_bytes);
+        if (p.w_tma)
+          tma_load_2d(st, &tmW, &full[i], 0, (tp * kb + kp) * BM, kEvictFirst);
+        else
+          bulk_load(st, p.w_tiles + ((size_t)tp * kb + kp) * (BM * BK), BM * BK * 2, &full[i], kEvictFirst);
+        if (++kp == kb) {
+          kp = 0;
+          ++tp;
+        }
+      }
+    }
+    __syncwarp();
+    pdl_wait();
+    pdl_trigger();
     int t = (int)(u0 / kb), k = (int)(u0 % kb);
     int s = 0, grp_last = p.cgrp - 1;  // ring slot and the last slot of its release group
     uint32_t ph = 0;
     for (long long u = u0; u < u1; ++u) {
-      mbar_wait(&empty[grp_last], ph ^ 1u);  // slot group released
+      const bool pre = (u - u0) < npre;  // weights already requested, slot known free
+      if (!pre) mbar_wait(&empty[grp_last], ph ^ 1u);  // slot group released
+      if (u == u0 && lane == 0) SF_TR(2);
+      if (lane == 0 && u - u0 < 40) SF_TR(64 + (int)(u - u0));
       if (elect_one()) {
         uint8_t* st = smem + (size_t)s * stage_bytes;
         if constexpr (CG == 1) {
-          mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
-          if (p.w_tiled)  // tile-contiguous, pre-swizzled weights: one 16 KB bulk copy per stage
-            bulk_load(st, p.w_tiles + ((size_t)t * kb + k) * (BM * BK), BM * BK * 2, &full[s], kEvictFirst);
-          else
-            tma_load_2d(st, &tmW, &full[s], k * BK, t * BM, kEvictFirst);
+          if (!pre) {
+            mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
+            if (p.w_tiled && p.w_tma)  // tiled weights through a 2-D TMA box
+              tma_load_2d(st, &tmW, &full[s], 0, (t * kb + k) * BM, kEvictFirst);
+            else if (p.w_tiled)  // tile-contiguous, pre-swizzled weights: one 16 KB bulk copy per stage
+              bulk_load(st, p.w_tiles + ((size_t)t * kb + k) * (BM * BK), BM * BK * 2, &full[s], kEvictFirst);
+            else
+              tma_load_2d(st, &tmW, &full[s], k * BK, t * BM, kEvictFirst);
+          }
           for (int j = 0; j < p.n_sub; ++j)
             tma_load_2d(st + BM * BK * 2 + j * a_rows * BK * 2, &tmA, &full[s], k * BK, j * p.NT, kEvictLast);
         } else {
@@ -192,7 +240,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           for (int j = 0; j < p.n_sub; ++j)
             tma_load_2d_2sm(st + BM * BK * 2 + j * a_rows * BK * 2, &tmA, &full[s], k * BK,
                             j * p.NT + (int)rank * a_rows, kEvictLast);
-          if (rank != 0) mbar_arrive_remote(&full[s], 0);
+          // no arrival from the peer: its bytes complete_tx on the leader's barrier, which the leader
+          // armed for both CTAs; they cannot land before that phase (the slot was released first)
         }
       }
       __syncwarp();
@@ -222,10 +271,15 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       const int b = seg % p.nbuf;
       mbar_wait(&acce[b], ((uint32_t)(seg / p.nbuf) & 1u) ^ 1u);
       tc_fence_after();
+      if (lane == 0 && seg < 4) SF_TR(8 + 4 * seg);
       const uint32_t dacc = tmem + (uint32_t)(b * cols);
       for (long long uu = u; uu < se; ++uu) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
+        if (lane == 0) {
+          if (uu == u0) SF_TR(3);
+          if (uu - u0 < 40) SF_TR(24 + (int)(uu - u0));
+        }
         if (elect_one()) {
           const uint64_t dw = sw128_kmajor_desc(smem_u32(smem + (size_t)s * stage_bytes));
           const uint64_t da = dw + a_off;
@@ -256,6 +310,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         else umma_commit_2sm(&accf[b]);
       }
       __syncwarp();
+      if (lane == 0) {
+        if (seg < 4) SF_TR(8 + 4 * seg + 1);
+        if (se == u1) SF_TR(4);
+      }
       u = se;
       ++seg;
       ++t;
@@ -263,6 +321,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   } else if (warp >= 4) {
     // ---- epilogue: 8 warps, two per TMEM lane quadrant (warp w reads lanes 32 (w % 4) ..);
     // the two warps of a quadrant take alternate 32-column chunks.
+    pdl_wait();  // outputs / partial slots / flags may still be in use by the previous kernel
+    kt_.mark();
+    uint32_t fix_ph = 0;
     const int quad = warp & 3, half = (warp - 4) >> 2;
     const int m = quad * 32 + lane;
     const int etid = threadIdx.x - 128;  // 0..255
@@ -275,6 +336,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       const long long se = min(u1, te);
       const int b = seg % p.nbuf;
       mbar_wait_sleep(&accf[b], (uint32_t)(seg / p.nbuf) & 1u);
+      if (etid == 0 && seg < 4) SF_TR(8 + 4 * seg + 2);
 #ifdef SF_GEMM_PROFILE
       const long long te0 = clock64();
 #endif
@@ -297,8 +359,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
             if (c0 + cc < p.T) dst[(size_t)(c0 + cc) * BM] = __uint_as_float(r[cc]);
         }
       } else if (!is_full && !is_head) {
-        // publish this segment's fp32 partial (slot = this CTA; at most one per CTA)
-        float* dst = p.partial + (size_t)slot * p.T * BM + m;
+        // publish this segment's fp32 partial (slot = this CTA; at most one per CTA): [T][128],
+        // each warp store one coalesced 128-byte line
+        float* dst = p.partial + (size_t)slot * p.Tp * BM + m;
         for (int c0 = half * 32; c0 < p.T; c0 += 64) {
           uint32_t r[32];
           tmem_ld32_async(t_row + (uint32_t)c0, r);
@@ -321,23 +384,135 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
               while (ld_acquire(&p.flags[cc * CG + (int)rank]) == 0) {
               }
           named_sync(1, 256);
+          if (etid == 0 && se == u1) SF_TR(104);
         }
-        for (int c0 = half * 32; c0 < p.T; c0 += 64) {
+        // A head that is this CTA's last segment finds the smem ring idle (every MMA has completed):
+        // the other segments' partials are then bulk-copied into it (TMA engine, full lines) instead
+        // of being gathered with per-thread loads that compete with the other CTAs' weight streams.
+        const int n_o = c_hi - c_lo + 1;
+        int Tc = p.T;
+        bool bulk = p.bulk_ok && is_head && se == u1 && n_o > 0;
+        if (bulk) {
+          Tc = ((p.stages * stage_bytes) / (n_o * BM * 4)) / 64 * 64;
+          bulk = Tc >= 64;
+        }
+        // output staging (ring idle): 2 x 16 KB at the end of the ring, one per epilogue half
+        constexpr int kStageBytes = 16384;
+        const int ring_bytes = p.stages * stage_bytes;
+        const int out_elt = mode == EPI_STORE_F32 ? 4 : 2;
+        const bool stage_out = se == u1 &&
+                               ((mode == EPI_STORE_ACT && (p.stage_ok & 1)) || (mode == EPI_STORE_F32 && (p.stage_ok & 2)) ||
+                                (mode == EPI_SWIGLU_ACT && (p.stage_ok & 4))) &&
+                               ((size_t)p.epi.ldo * out_elt) % 16 == 0 && ring_bytes >= 2 * kStageBytes + 64 * BM * 4 * n_o;
+        uint8_t* stg = smem + ring_bytes - 2 * kStageBytes;
+        if (stage_out && bulk) Tc = ((ring_bytes - 2 * kStageBytes) / (n_o * BM * 4)) / 64 * 64;
+        const float* smf = reinterpret_cast<const float*>(smem);
+        for (int P0 = 0; P0 < p.T; P0 += (bulk ? Tc : p.T)) {
+        const int P1 = bulk ? min(p.T, P0 + Tc) : p.T;
+        if (bulk) {
+          if (etid == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            mbar_arrive_expect_tx(fixb, (uint32_t)(n_o * (P1 - P0) * BM * 4));
+            for (int o = 0; o < n_o; ++o)
+              bulk_load(smem + (size_t)o * (P1 - P0) * BM * 4,
+                        p.partial + (size_t)((c_lo + o) * CG + (int)rank) * p.Tp * BM + (size_t)P0 * BM,
+                        (uint32_t)((P1 - P0) * BM * 4), fixb, kEvictFirst);
+          }
+          mbar_wait(fixb, fix_ph);
+          fix_ph ^= 1u;
+          if (etid == 0 && P0 == 0) SF_TR(105);
+        }
+        for (int c0 = P0 + half * 32; c0 < P1; c0 += 64) {
           uint32_t r[32];
           tmem_ld32_async(t_row + (uint32_t)c0, r);
           tmem_ld_wait();
           float v[32];
 #pragma unroll
           for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
-          for (int cc = c_lo; cc <= c_hi; ++cc) {  // fixed k order
-            const float* src = p.partial + (size_t)(cc * CG + (int)rank) * p.T * BM + m;
+          if (bulk) {
+            for (int o = 0; o < n_o; ++o) {  // fixed k order
+              const float* sp = smf + (size_t)o * (P1 - P0) * BM + (size_t)(c0 - P0) * BM + m;
 #pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (c0 + q < p.T) v[q] += __ldcg(&src[(size_t)(c0 + q) * BM]);
+              for (int q = 0; q < 32; ++q)
+                if (c0 + q < p.T) v[q] += sp[q * BM];
+            }
+          } else
+          for (int cc = c_lo; cc <= c_hi; cc += 2) {  // fixed k order; two segments' loads in flight
+            const float* s0 = p.partial + (size_t)(cc * CG + (int)rank) * p.Tp * BM + m;
+            const bool two = cc + 1 <= c_hi;
+            const float* s1 = s0 + (two ? (size_t)CG * p.Tp * BM : 0);
+            float a0[32], a1[32];
+#pragma unroll
+            for (int q = 0; q < 32; ++q) a0[q] = (c0 + q < p.T) ? __ldcg(&s0[(size_t)(c0 + q) * BM]) : 0.f;
+            if (two) {
+#pragma unroll
+              for (int q = 0; q < 32; ++q) a1[q] = (c0 + q < p.T) ? __ldcg(&s1[(size_t)(c0 + q) * BM]) : 0.f;
+            }
+#pragma unroll
+            for (int q = 0; q < 32; ++q) v[q] += a0[q];
+            if (two) {
+#pragma unroll
+              for (int q = 0; q < 32; ++q) v[q] += a1[q];
+            }
           }
+          if (etid == 0 && bulk && c0 < 128) SF_TR(107 + (c0 >> 6));  // chunk's TMEM + adds done
           const int nq = min(32, p.T - c0);
           const size_t ldo = (size_t)p.epi.ldo;
-          if (mode == EPI_STORE_ACT) {
+          if (stage_out) {
+            // stage the chunk [32 tokens][tile columns] in smem, then write whole rows with
+            // 16-byte vectors (per-thread column stores are 32-byte sectors 10-100 KB apart)
+            uint8_t* sb = stg + (size_t)half * kStageBytes;
+            const int rowb = mode == EPI_SWIGLU_ACT ? 128 : (mode == EPI_STORE_ACT ? 256 : 512);
+            if (mode == EPI_STORE_ACT) {
+#pragma unroll
+              for (int q = 0; q < 32; ++q)
+                reinterpret_cast<__nv_bfloat16*>(sb + q * 256)[m] = __float2bfloat16_rn(v[q]);
+            } else if (mode == EPI_STORE_F32) {
+#pragma unroll
+              for (int q = 0; q < 32; ++q) reinterpret_cast<float*>(sb + q * 512)[m] = v[q];
+            } else {
+              // even lane 2i holds gate_i, odd lane up_i (interleaved rows): the even lane forms all
+              // 32 tokens of feature i
+              if (etid == 0 && c0 < 64) SF_TR(111);
+              __nv_bfloat16* srow = reinterpret_cast<__nv_bfloat16*>(sb) + quad * 16 + (lane >> 1);
+              // batches of 8 independent shuffle / exp / divide chains (the per-element chain is
+              // ~100 cycles of latency; one element at a time the warp would mostly wait)
+#pragma unroll
+              for (int q0 = 0; q0 < 32; q0 += 8) {
+                float u[8], e[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) u[j] = __shfl_down_sync(0xffffffffu, v[q0 + j], 1);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) e[j] = __expf(-v[q0 + j]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) e[j] = __fdividef(v[q0 + j], 1.f + e[j]) * u[j];
+                if (!(lane & 1)) {
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) srow[(q0 + j) * 64] = __float2bfloat16_rn(e[j]);
+                }
+              }
+            }
+            if (etid == 0 && c0 < 64) SF_TR(112);
+            named_sync(2 + half, 128);
+            if (etid == 0 && c0 < 64) SF_TR(113);
+            const int elt = mode == EPI_STORE_F32 ? 4 : 2;
+            const int col0 = mode == EPI_SWIGLU_ACT ? vt * 64 : vt * BM;
+            uint8_t* gbase = reinterpret_cast<uint8_t*>(p.epi.out) + ((size_t)c0 * ldo + col0) * elt;
+            const int vpr = rowb / 16, ht = etid & 127;
+            for (int i = ht; i < nq * vpr; i += 128) {
+              const int q = i / vpr, x = i % vpr;
+#ifdef SF_GEMM_CHECK
+              if ((((uintptr_t)(gbase + (size_t)q * ldo * elt + x * 16)) & 15) || (((uintptr_t)(sb + q * rowb + x * 16)) & 15)) {
+                printf("misaligned: mode %d out %p ldo %d c0 %d col0 %d q %d x %d sb %p T %d N %d K %d\n", mode, p.epi.out,
+                       (int)ldo, c0, col0, q, x, sb, p.T, p.N, p.K);
+                __trap();
+              }
+#endif
+              *reinterpret_cast<uint4*>(gbase + (size_t)q * ldo * elt + x * 16) =
+                  *reinterpret_cast<const uint4*>(sb + q * rowb + x * 16);
+            }
+            named_sync(2 + half, 128);
+          } else if (mode == EPI_STORE_ACT) {
             __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.epi.out) + (size_t)c0 * ldo + n;
 #pragma unroll
             for (int q = 0; q < 32; ++q)
@@ -374,16 +549,27 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
             // Even lanes emit even columns, odd lanes odd columns.
             const int f = vt * 64 + (m >> 1);
             __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.epi.out) + (size_t)c0 * ldo + f;
-            const int par = lane & 1;
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
-              const float gq = __shfl_sync(0xffffffffu, v[q], lane & ~1);
-              const float uq = __shfl_sync(0xffffffffu, v[q], lane | 1);
-              if ((q & 1) == par && q < nq)
-                o[q * ldo] = __float2bfloat16_rn(__fdividef(gq, 1.f + __expf(-gq)) * uq);
+            for (int q0 = 0; q0 < 32; q0 += 8) {
+              float u[8], e[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) u[j] = __shfl_down_sync(0xffffffffu, v[q0 + j], 1);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) e[j] = __expf(-v[q0 + j]);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) e[j] = __fdividef(v[q0 + j], 1.f + e[j]) * u[j];
+              if (!(lane & 1)) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  if (q0 + j < nq) o[(q0 + j) * ldo] = __float2bfloat16_rn(e[j]);
+              }
             }
           }
+          if (etid == 0 && bulk && c0 < 128) SF_TR(109 + (c0 >> 6));  // chunk's stores issued
         }
+        if (bulk) named_sync(1, 256);  // smem pass consumed before the next one overwrites it
+        if (etid == 0 && P0 == 0) SF_TR(106);
+        }  // passes
         if (is_head) {
           named_sync(1, 256);
           if (etid == 0)
@@ -397,6 +583,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 #endif
       tc_fence_before();
       named_sync(1, 256);
+      if (etid == 0 && seg < 4) SF_TR(8 + 4 * seg + 3);
+      if (etid == 0 && se == u1) SF_TR(5);
       if (etid == 0) {
         if (CG == 1 || rank == 0) mbar_arrive(&acce[b]);
         else mbar_arrive_remote(&acce[b], 0);
@@ -424,6 +612,10 @@ template <bool DUAL>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict__ A, int lda,
                                                          const float* __restrict__ W, int T, int N, int K,
                                                          GemmEpi epi) {
+  KtScope kt_(KT_GEMM_SIMT, (uint32_t)(N));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   __shared__ float As[32][33];
   __shared__ float Ws[32][33];
   __shared__ float Us[DUAL ? 32 : 1][33];
@@ -507,6 +699,24 @@ static void tc_shape(int T, int* NT, int* n_sub) {
 }
 
 constexpr int kMaxSMs = 160;
+// Optional per-CTA timeline of the last GEMM launch (SF_GEMM_TRACE=1; tools/gemm_trace.py only).
+static unsigned long long* g_trace_buf = nullptr;
+static unsigned long long* gemm_trace_buffer() {
+  static const bool on = getenv("SF_GEMM_TRACE") && atoi(getenv("SF_GEMM_TRACE")) > 0;
+  if (!on) return nullptr;
+  if (!g_trace_buf) {
+    if (cudaMalloc((void**)&g_trace_buf, (size_t)2 * kMaxSMs * 128 * 8) != cudaSuccess) return nullptr;
+    cudaMemset(g_trace_buf, 0, (size_t)2 * kMaxSMs * 128 * 8);
+  }
+  return g_trace_buf;
+}
+int gemm_trace_copy(unsigned long long* host, int n) {
+  if (!g_trace_buf) return 0;
+  n = std::min(n, 2 * kMaxSMs * 128);
+  if (cudaMemcpy(host, g_trace_buf, (size_t)n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  cudaMemset(g_trace_buf, 0, (size_t)2 * kMaxSMs * 128 * 8);
+  return n;
+}
 static int num_sms() {
   static int n = 0;
   if (!n) {
@@ -522,7 +732,7 @@ int64_t gemm_partial_elems(bool is_bf16, int T, int N, int K) {
   (void)N;
   (void)K;
   if (!is_bf16) return 0;
-  return (int64_t)2 * kMaxSMs * BM * std::min(T, 512);  // EPI_PARTIAL: 2 slots per CTA
+  return (int64_t)2 * kMaxSMs * BM * std::min((T + 31) / 32 * 32, 512);  // 2 slots per CTA
 }
 
 // Tile-contiguous weight layout: block (t, k) = rows [128t, +128) x cols [64k, +64) stored as the
@@ -530,6 +740,11 @@ int64_t gemm_partial_elems(bool is_bf16, int T, int N, int K) {
 // chunk position c ^ (r & 7)); blocks ordered t-major then k. A stream-K range of consecutive
 // (t, k) units is then one contiguous stretch of HBM.
 __global__ void pack_tiled_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst, int K) {
+  KtScope kt_(KT_MISC, (uint32_t)(5));
+  pdl_wait();
+  kt_.mark();
+  // no pdl_trigger(): a GEMM may prefetch these weights before its grid dependency resolves, so
+  // dependents launch only once the packed weights are complete
   const int kb = K / BK;
   const int blk = blockIdx.x;
   const int t = blk / kb, k = blk % kb;
@@ -540,9 +755,15 @@ __global__ void pack_tiled_kernel(const __nv_bfloat16* __restrict__ src, __nv_bf
   for (int c = 0; c < 8; ++c) d[c ^ (r & 7)] = s[c];
 }
 
+// Launched WITHOUT the PDL attribute after weight packing: it starts only when the pack kernel has
+// fully completed, so a following GEMM that prefetches weights before its own grid dependency
+// resolves (launched with PDL relative to this kernel) can never observe a partially packed tile.
+__global__ void stream_fence_kernel() {}
+
 cudaError_t gemm_pack_weight(const void* src, void* dst, int N, int K, cudaStream_t st) {
   if (N % BM || K % BK) return cudaErrorInvalidValue;
-  pack_tiled_kernel<<<(N / BM) * (K / BK), BM, 0, st>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, K);
+  launch_k(pack_tiled_kernel, dim3((N / BM) * (K / BK)), dim3(BM), 0, st, (const __nv_bfloat16*)src, (__nv_bfloat16*)dst, K);
+  stream_fence_kernel<<<1, 32, 0, st>>>();
   return cudaGetLastError();
 }
 
@@ -560,10 +781,12 @@ static bool make_map_tiled(CUtensorMap* m, const void* ptr, long long rows) {
 }
 
 // CTA-pair (cta_group::2) mode for a weight shape: a function of (N, K) only (batch invariance)
+// CTA-pair mode halves each SM's share of the activation tile (the MMA reads the B operand from
+// both CTAs' shared memory), the L2->SM traffic that bounds the skinny GEMM at large T.
 static int gemm_cg(int N, int K) {
   (void)K;
-  static const int env = getenv("SF_GEMM_CG") ? atoi(getenv("SF_GEMM_CG")) : 0;
-  if (env == 2 && N % (2 * BM) == 0) return 2;  // CTA-pair mode (experimental; slower so far)
+  static const int env = getenv("SF_GEMM_CG") ? atoi(getenv("SF_GEMM_CG")) : 2;
+  if (env == 2 && N % (2 * BM) == 0) return 2;
   return 1;
 }
 
@@ -580,6 +803,7 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   p.T = T;
   p.N = N;
   p.K = K;
+  p.Tp = (T + 31) / 32 * 32;
   tc_shape(T, &p.NT, &p.n_sub);
   p.kb_total = K / BK;
   p.n_tiles = N / (BM * CG);
@@ -607,20 +831,29 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   p.flags = scratch.counters;
   p.w_tiled = w_tiled ? 1 : 0;
   p.w_tiles = (const __nv_bfloat16*)W;
-  if (!scratch.partial || scratch.partial_elems < (int64_t)2 * p.G * CG * T * BM || scratch.n_counters < p.G * CG)
+  p.trace = gemm_trace_buffer();
+  // bit0 bulk fixup loads; bits 1..3 smem-staged stores for ACT / F32 / SwiGLU outputs
+  static const int env_epi = getenv("SF_GEMM_EPI") ? atoi(getenv("SF_GEMM_EPI")) : 15;
+  p.bulk_ok = env_epi & 1;
+  p.stage_ok = (env_epi >> 1) & 7;
+  static const int trace_n = getenv("SF_GEMM_TRACE_N") ? atoi(getenv("SF_GEMM_TRACE_N")) : 0;
+  if (trace_n && trace_n != N) p.trace = nullptr;  // trace one weight shape only
+  if (!scratch.partial || scratch.partial_elems < (int64_t)2 * p.G * CG * p.Tp * BM || scratch.n_counters < p.G * CG)
     return cudaErrorInvalidValue;
   if (epi.mode == EPI_PARTIAL && p.n_tiles > p.G) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)p.stages * stage_bytes + 1024 + (2 * p.stages + 4) * 8 + 16;
+  const size_t smem = (size_t)p.stages * stage_bytes + 1024 + (2 * p.stages + 5) * 8 + 16;
   CUtensorMap mw, ma;
   memset(&mw, 0, sizeof(mw));
-  if (CG == 2) {
+  static const int env_wtma = getenv("SF_GEMM_WTMA") ? atoi(getenv("SF_GEMM_WTMA")) : 0;
+  p.w_tma = (CG == 1 && w_tiled && env_wtma) ? 1 : 0;
+  if (CG == 2 || p.w_tma) {
     if (!make_map_tiled(&mw, W, (long long)N * (K / BK))) return cudaErrorInvalidValue;
   } else if (!w_tiled && !make_map(&mw, W, N, K, K, BM)) {
     return cudaErrorInvalidValue;
   }
   if (!make_map(&ma, A, T, K, lda, p.NT / CG)) return cudaErrorInvalidValue;
   if (CG == 1) {
-    gemm_sk_kernel<1><<<p.G, 384, smem, st>>>(mw, ma, p);
+    launch_k(gemm_sk_kernel<1>, dim3(p.G), dim3(384), smem, st, mw, ma, p);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg{};
@@ -628,13 +861,15 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   cfg.blockDim = dim3(384);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attrs[1];
+  cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
   attrs[0].val.clusterDim.x = 2;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, gemm_sk_kernel<2>, mw, ma, p);
 }
 
@@ -652,30 +887,36 @@ bool gemm_partial_geom(int T, int N, int K, PartialGeom* g) {
   return true;
 }
 
-// One CTA (256 threads) per virtual row; thread t owns the float4 column groups 4t + 1024 j. Per
-// 128-column tile the k-segment slot offsets are precomputed in shared memory; all loads of a
-// thread (residual + up to 8 segments x 4 groups, 16-byte vectors) are issued before the k-ordered
-// sums, so the kernel streams at memory speed.
-constexpr int kRnThreads = 256;
-constexpr int rn_max_seg(int NG) { return NG >= 8 ? 4 : 32 / NG; }  // register budget: NG x segs float4
+// One CTA per virtual row, d / (4 NG) threads (<= 1024): thread t owns the float4 column groups
+// 4t + 4 nthr j (j < NG). Per 128-column tile the k-segment slot offsets are precomputed in shared
+// memory; the segments' 16-byte partial loads are issued in batches of kRnBatch before the k-ordered
+// sums, so a row streams at memory speed and a few rows (B = 1) still spread over many warps.
+constexpr int kRnMaxSeg = 16;  // k segments per 128-column tile (stream-K: <= G / n_tiles + 2)
+constexpr int kRnMaxTiles = 128;
+static int rn_ng(int d) {  // float4 groups per thread
+  for (int ng = 1; ng <= 4; ++ng)
+    if (d % (4 * ng * 32) == 0 && d / (4 * ng) <= 1024) return ng;
+  return 0;
+}
 
-template <int NG>  // float4 groups per thread (d = 1024 NG)
-__global__ void __launch_bounds__(kRnThreads) resid_norm_kernel(
+template <int NG>
+__global__ void __launch_bounds__(1024) resid_norm_kernel(
     const float* __restrict__ partial, int G, int kb, int CG, int n_tiles_cta, int T, int rep, int d,
     const float* resid, const float* __restrict__ bias, float* out, float* tap, const float* __restrict__ gamma,
     float eps, __nv_bfloat16* xn) {
-  constexpr int kRnMaxSeg = rn_max_seg(NG);
-  __shared__ int seg_n[128];
-  __shared__ int seg_off[128][kRnMaxSeg];  // slot * T * 128 (the tile's k segments, k order)
-  __shared__ float red[kRnThreads / 32];
+  constexpr int kRnBatch = 8 / NG;
+  __shared__ int seg_n[kRnMaxTiles];
+  __shared__ int seg_off[kRnMaxTiles][kRnMaxSeg];  // slot * T * 128 (the tile's k segments, k order)
+  __shared__ float red[32];
+  const int nthr = blockDim.x;
   const int r = blockIdx.x;
   const int src_row = r / rep, col0 = (r % rep) * d;
   const int tid = threadIdx.x;
-  if (partial) {
+  if (partial) {  // geometry only (no dependency on the previous kernel)
     const int groups = G / CG;
     const int n_tiles_grp = n_tiles_cta / CG;
     const long long U = (long long)n_tiles_grp * kb;
-    for (int vt = tid; vt < n_tiles_cta; vt += kRnThreads) {
+    for (int vt = tid; vt < n_tiles_cta; vt += nthr) {
       const int tg = vt / CG, rk = vt % CG;
       const long long ua = (long long)tg * kb, ub = ua + kb - 1;
       const int lo = (int)(((ua + 1) * groups + U - 1) / U) - 1;
@@ -687,11 +928,15 @@ __global__ void __launch_bounds__(kRnThreads) resid_norm_kernel(
     }
     __syncthreads();
   }
+  KtScope kt_(KT_RESID_NORM, (uint32_t)(d));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   float4 x[NG];
   float ss = 0.f;
 #pragma unroll
   for (int j = 0; j < NG; ++j) {
-    const int i = 4 * tid + 1024 * j;  // column within the virtual row
+    const int i = 4 * tid + 4 * nthr * j;  // column within the virtual row
     x[j] = resid ? *reinterpret_cast<const float4*>(resid + (size_t)r * d + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     if (bias) {
       const float4 bb = *reinterpret_cast<const float4*>(bias + col0 + i);
@@ -702,32 +947,31 @@ __global__ void __launch_bounds__(kRnThreads) resid_norm_kernel(
     }
   }
   if (partial) {
-    float4 pv[NG][kRnMaxSeg];
-    int ns[NG];
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
-      const int n = col0 + 4 * tid + 1024 * j;
+      const int n = col0 + 4 * tid + 4 * nthr * j;
       const int vt = n / BM, m = n % BM;
-      ns[j] = seg_n[vt];
+      const int ns = seg_n[vt];
       const float* bp = partial + (size_t)src_row * BM + m;
+      for (int q0 = 0; q0 < ns; q0 += kRnBatch) {
+        float4 pv[kRnBatch];
 #pragma unroll
-      for (int q = 0; q < kRnMaxSeg; ++q)
-        if (q < ns[j]) pv[j][q] = __ldcg(reinterpret_cast<const float4*>(bp + seg_off[vt][q]));
+        for (int q = 0; q < kRnBatch; ++q)
+          if (q0 + q < ns) pv[q] = __ldcg(reinterpret_cast<const float4*>(bp + seg_off[vt][q0 + q]));
+#pragma unroll
+        for (int q = 0; q < kRnBatch; ++q)
+          if (q0 + q < ns) {  // k order
+            x[j].x += pv[q].x;
+            x[j].y += pv[q].y;
+            x[j].z += pv[q].z;
+            x[j].w += pv[q].w;
+          }
+      }
     }
-#pragma unroll
-    for (int j = 0; j < NG; ++j)
-#pragma unroll
-      for (int q = 0; q < kRnMaxSeg; ++q)
-        if (q < ns[j]) {  // k order
-          x[j].x += pv[j][q].x;
-          x[j].y += pv[j][q].y;
-          x[j].z += pv[j][q].z;
-          x[j].w += pv[j][q].w;
-        }
   }
 #pragma unroll
   for (int j = 0; j < NG; ++j) {
-    const int i = 4 * tid + 1024 * j;
+    const int i = 4 * tid + 4 * nthr * j;
     if (out) *reinterpret_cast<float4*>(out + (size_t)r * d + i) = x[j];
     if (tap) *reinterpret_cast<float4*>(tap + (size_t)r * d + i) = x[j];
     ss = fmaf(x[j].x, x[j].x, ss);
@@ -736,11 +980,20 @@ __global__ void __launch_bounds__(kRnThreads) resid_norm_kernel(
     ss = fmaf(x[j].w, x[j].w, ss);
   }
   if (!gamma) return;
-  ss = block_sum<kRnThreads>(ss, red);
-  const float rs = 1.0f / sqrtf(ss / (float)d + eps);
+  // fixed reduction tree (depends on d only): warp shuffles, then warp 0 over the warp sums
+  ss = warp_sum(ss);
+  if ((tid & 31) == 0) red[tid >> 5] = ss;
+  __syncthreads();
+  if (tid < 32) {
+    float v = (tid < (nthr >> 5)) ? red[tid] : 0.f;
+    v = warp_sum(v);
+    if (tid == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float rs = 1.0f / sqrtf(red[0] / (float)d + eps);
 #pragma unroll
   for (int j = 0; j < NG; ++j) {
-    const int i = 4 * tid + 1024 * j;
+    const int i = 4 * tid + 4 * nthr * j;
     const float4 gg = *reinterpret_cast<const float4*>(gamma + i);
     __nv_bfloat162 lo = __floats2bfloat162_rn(x[j].x * rs * gg.x, x[j].y * rs * gg.y);
     __nv_bfloat162 hi = __floats2bfloat162_rn(x[j].z * rs * gg.z, x[j].w * rs * gg.w);
@@ -755,7 +1008,8 @@ cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T,
                               const float* bias, float* out, float* tap, const float* gamma, float eps,
                               __nv_bfloat16* xn, cudaStream_t st) {
   if (T * rep <= 0) return cudaSuccess;
-  if (d % 1024 || d > 8192) return cudaErrorInvalidValue;  // caller falls back to the unfused path
+  const int ng = rn_ng(d);
+  if (!ng) return cudaErrorInvalidValue;
   int G = 1, kb = 1, CG = 1, nt = 1, Tslot = T;
   if (partial) {
     G = g->G;
@@ -763,34 +1017,31 @@ cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T,
     nt = g->n_tiles;
     CG = gemm_cg(nt * BM, kb * BK);
     Tslot = g->T;
-    if (nt > 128) return cudaErrorInvalidValue;
-    // every tile must have <= rn_max_seg k segments
+    if (nt > kRnMaxTiles) return cudaErrorInvalidValue;
     const int groups = G / CG;
-    if ((groups + nt / CG - 1) / (nt / CG) + 1 > rn_max_seg(d / 1024)) return cudaErrorInvalidValue;
+    if ((groups + nt / CG - 1) / (nt / CG) + 1 > kRnMaxSeg) return cudaErrorInvalidValue;
   }
-#define SF_RN(NG)                                                                                               \
-  resid_norm_kernel<NG><<<T * rep, kRnThreads, 0, st>>>(partial, G, kb, CG, nt, Tslot, rep, d, resid, bias, out, \
-                                                        tap, gamma, eps, xn)
-  switch (d / 1024) {
-    case 1: SF_RN(1); break;
-    case 2: SF_RN(2); break;
-    case 4: SF_RN(4); break;
-    case 5: SF_RN(5); break;
-    case 8: SF_RN(8); break;
-    default: return cudaErrorInvalidValue;
+  const dim3 grid(T * rep), block(d / (4 * ng));
+  switch (ng) {
+    case 1: return launch_k(resid_norm_kernel<1>, grid, block, 0, st, partial, G, kb, CG, nt, Tslot, rep, d, resid,
+                            bias, out, tap, gamma, eps, xn);
+    case 2: return launch_k(resid_norm_kernel<2>, grid, block, 0, st, partial, G, kb, CG, nt, Tslot, rep, d, resid,
+                            bias, out, tap, gamma, eps, xn);
+    case 3: return launch_k(resid_norm_kernel<3>, grid, block, 0, st, partial, G, kb, CG, nt, Tslot, rep, d, resid,
+                            bias, out, tap, gamma, eps, xn);
+    default: return launch_k(resid_norm_kernel<4>, grid, block, 0, st, partial, G, kb, CG, nt, Tslot, rep, d, resid,
+                             bias, out, tap, gamma, eps, xn);
   }
-#undef SF_RN
-  return cudaGetLastError();
 }
 
 // Whether the fused consumer supports this (d, N, K): callers use the unfused path otherwise.
 bool resid_norm_supported(int d, int T, int N, int K) {
-  if (d % 1024 || d > 8192 || (d / 1024 == 3) || (d / 1024 == 6) || (d / 1024 == 7)) return false;
+  if (!rn_ng(d)) return false;
   PartialGeom g;
   if (!gemm_partial_geom(T, N, K, &g)) return false;
   const int CG = gemm_cg(N, K);
   const int groups = g.G / CG, ntg = g.n_tiles / CG;
-  return (groups + ntg - 1) / ntg + 1 <= rn_max_seg(d / 1024) && g.n_tiles <= 128;
+  return (groups + ntg - 1) / ntg + 1 <= kRnMaxSeg && g.n_tiles <= kRnMaxTiles;
 }
 
 static cudaError_t gemm_launch_chunk(bool is_bf16, const void* A, int lda, const void* W, bool w_tiled, int T,
@@ -801,9 +1052,9 @@ static cudaError_t gemm_launch_chunk(bool is_bf16, const void* A, int lda, const
     const int Nout = epi.mode == EPI_SWIGLU_ACT ? N / 2 : N;
     dim3 grid((Nout + 31) / 32, (T + 31) / 32), block(32, 8);
     if (epi.mode == EPI_SWIGLU_ACT)
-      gemm_simt_kernel<true><<<grid, block, 0, st>>>((const float*)A, lda, (const float*)W, T, N, K, epi);
+      launch_k(gemm_simt_kernel<true>, dim3(grid), dim3(block), 0, st, (const float*)A, lda, (const float*)W, T, N, K, epi);
     else
-      gemm_simt_kernel<false><<<grid, block, 0, st>>>((const float*)A, lda, (const float*)W, T, N, K, epi);
+      launch_k(gemm_simt_kernel<false>, dim3(grid), dim3(block), 0, st, (const float*)A, lda, (const float*)W, T, N, K, epi);
     return cudaGetLastError();
   }
   if (N % BM || K % BK || T > 512) return cudaErrorInvalidValue;
@@ -826,6 +1077,14 @@ cudaError_t gemm_launch(bool is_bf16, const void* A, int lda, const void* W, boo
     if (r != cudaSuccess) return r;
   }
   return cudaSuccess;
+}
+
+cudaError_t kt_setup_gemm(void* rec, unsigned* cnt, unsigned cap) {
+  KtBuf b;
+  b.rec = reinterpret_cast<KtRec*>(rec);
+  b.cnt = cnt;
+  b.cap = cap;
+  return kt_setup_tu(b);
 }
 
 }  // namespace sf

@@ -41,6 +41,10 @@ cudaError_t gemm_launch(bool is_bf16, const void* A, int lda, const void* W, boo
 // Row-major bf16 W[N, K] -> tile-contiguous 128x64 pre-swizzled layout (same byte count).
 cudaError_t gemm_pack_weight(const void* src, void* dst, int N, int K, cudaStream_t s);
 
+// Copies (and clears) the per-CTA timeline of GEMM launches made with SF_GEMM_TRACE=1 set
+// (tools only); returns the number of 64-bit entries copied (0 when tracing is off).
+int gemm_trace_copy(unsigned long long* host, int n);
+
 // scratch floats needed by gemm_launch for (T, N, K)
 int64_t gemm_partial_elems(bool is_bf16, int T, int N, int K);
 

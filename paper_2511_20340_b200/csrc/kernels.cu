@@ -13,6 +13,10 @@ namespace sf {
 // ------------------------------------------------------------------------ RoPE table
 // cos/sin(pos * theta^(-2i/hd)) evaluated in double, stored fp32 (reading C5).
 __global__ void rope_table_kernel(float2* tab, int max_seq, int hd, float theta) {
+  KtScope kt_(KT_MISC, (uint32_t)(4));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   const int half = hd / 2;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= max_seq * half) return;
@@ -25,12 +29,20 @@ __global__ void rope_table_kernel(float2* tab, int max_seq, int hd, float theta)
 
 // ------------------------------------------------------------------------ row builders
 __global__ void build_verify_rows_kernel(int B, int k, const int* last_token, const int* draft, int* tok) {
+  KtScope kt_(KT_ROWS, (uint32_t)(0));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= B * (k + 1)) return;
   const int b = r / (k + 1), i = r % (k + 1);
   tok[r] = (i == 0) ? last_token[b] : draft[b * k + i - 1];
 }
 __global__ void build_prefill_rows_kernel(int B, int P, int c0, int C, const int* tokens, int* tok, int* pos0) {
+  KtScope kt_(KT_ROWS, (uint32_t)(1));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < B) pos0[r] = c0;
   if (r >= B * C) return;
@@ -41,6 +53,10 @@ __global__ void build_prefill_rows_kernel(int B, int P, int c0, int C, const int
 // ------------------------------------------------------------------------ embedding (HS[0])
 template <typename TW>
 __global__ void embed_kernel(const int* tok, const TW* emb, int d, int vocab, float* resid, float* tap0) {
+  KtScope kt_(KT_EMBED, (uint32_t)(d));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   const int t = blockIdx.x;
   int id = tok[t];
   id = min(max(id, 0), vocab - 1);
@@ -57,6 +73,10 @@ __global__ void embed_kernel(const int* tok, const TW* emb, int d, int vocab, fl
 template <typename TO>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* in, int in_ld, const float* g, float eps, int d,
                                                       TO* out, int out_ld) {
+  KtScope kt_(KT_RMSNORM, (uint32_t)(d));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   __shared__ float red[8];
   const int t = blockIdx.x;
   const float* x = in + (size_t)t * in_ld;
@@ -73,6 +93,10 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* in, int in_ld
 template <typename TO>
 __global__ void __launch_bounds__(256) group_rms_kernel(const float* taps, int64_t tap_stride, const float* sc,
                                                         float eps, int d, TO* out) {
+  KtScope kt_(KT_GROUP_RMS, (uint32_t)(d));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   __shared__ float red[8];
   const int t = blockIdx.x;
   for (int g = 0; g < 4; ++g) {
@@ -89,37 +113,83 @@ __global__ void __launch_bounds__(256) group_rms_kernel(const float* taps, int64
 // ------------------------------------------------------------------------ RoPE + paged KV append
 // qkv row = [q (Hq*hd) | k (Hkv*hd) | v (Hkv*hd)]. Queries rotated -> q_out fp32;
 // keys rotated and values copied into the sequence's pages at their absolute positions.
-template <typename TA>
-__global__ void rope_append_kernel(const TA* qkv, int q_len, const int* pos0, const float2* rope, int Hq, int Hkv,
-                                   int hd, const int* bt, int pps, TA* Kp, TA* Vp, float* q_out) {
+// One warp per (row, head slot) -- grid (T, ceil((Hq + 2 Hkv) / 4)), 4 warps per CTA -- so even a
+// 5-row verify block spreads over hundreds of warps; lane l owns the rotate-half pairs
+// (i, i + hd/2) for i = VEC l .. VEC l + VEC - 1 (+ 32 VEC j), VEC = 2 when hd/2 is a multiple of 64.
+template <typename TA, int VEC>
+__global__ void __launch_bounds__(128) rope_append_kernel(const TA* qkv, int q_len, const int* pos0,
+                                                          const float2* rope, int Hq, int Hkv, int hd,
+                                                          const int* bt, int pps, TA* Kp, TA* Vp, float* q_out) {
+  KtScope kt_(KT_ROPE, (uint32_t)(Hq));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   const int t = blockIdx.x;
+  const int h = blockIdx.y * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (h >= Hq + 2 * Hkv) return;
   const int b = t / q_len, qi = t % q_len;
   const int pos = pos0[b] + qi;
   const int half = hd / 2;
   const int W = (Hq + 2 * Hkv) * hd;
-  const TA* row = qkv + (size_t)t * W;
+  const TA* row = qkv + (size_t)t * W + (size_t)h * hd;
   const int blk = bt[b * pps + pos / 16], slot = pos % 16;
-  const float2* cs = rope + (size_t)pos * half;
-  for (int e = threadIdx.x; e < (Hq + Hkv) * half; e += blockDim.x) {
-    const int h = e / half, i = e % half;
-    const float2 c = cs[i];
-    const float x1 = Elt<TA>::to_f(row[h * hd + i]);
-    const float x2 = Elt<TA>::to_f(row[h * hd + i + half]);
-    const float y1 = x1 * c.x - x2 * c.y;
-    const float y2 = x2 * c.x + x1 * c.y;
-    if (h < Hq) {
-      q_out[((size_t)t * Hq + h) * hd + i] = y1;
-      q_out[((size_t)t * Hq + h) * hd + i + half] = y2;
-    } else {
-      const int kh = h - Hq;
-      TA* dst = Kp + (((size_t)blk * Hkv + kh) * 16 + slot) * hd;
-      dst[i] = Elt<TA>::from_f(y1);
-      dst[i + half] = Elt<TA>::from_f(y2);
+  if (h >= Hq + Hkv) {  // value head: plain copy into the page
+    TA* dst = Vp + (((size_t)blk * Hkv + (h - Hq - Hkv)) * 16 + slot) * hd;
+    for (int i = lane * VEC; i < hd; i += 32 * VEC) {
+      if constexpr (VEC == 2 && sizeof(TA) == 2) {
+        *reinterpret_cast<__nv_bfloat162*>(dst + i) = *reinterpret_cast<const __nv_bfloat162*>(row + i);
+      } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) dst[i + v] = row[i + v];
+      }
     }
+    return;
   }
-  for (int e = threadIdx.x; e < Hkv * hd; e += blockDim.x) {
-    const int kh = e / hd, i = e % hd;
-    Vp[(((size_t)blk * Hkv + kh) * 16 + slot) * hd + i] = row[(Hq + Hkv) * hd + e];
+  const float2* cs = rope + (size_t)pos * half;
+  for (int i = lane * VEC; i < half; i += 32 * VEC) {
+    float x1[VEC], x2[VEC], y1[VEC], y2[VEC];
+    float2 c[VEC];
+    if constexpr (VEC == 2 && sizeof(TA) == 2) {
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(row + i));
+      const float2 bb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(row + i + half));
+      const float4 cc = *reinterpret_cast<const float4*>(cs + i);
+      x1[0] = a.x, x1[1] = a.y, x2[0] = bb.x, x2[1] = bb.y;
+      c[0] = make_float2(cc.x, cc.y), c[1] = make_float2(cc.z, cc.w);
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        c[v] = cs[i + v];
+        x1[v] = Elt<TA>::to_f(row[i + v]);
+        x2[v] = Elt<TA>::to_f(row[i + v + half]);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      y1[v] = x1[v] * c[v].x - x2[v] * c[v].y;
+      y2[v] = x2[v] * c[v].x + x1[v] * c[v].y;
+    }
+    if (h < Hq) {
+      float* q = q_out + ((size_t)t * Hq + h) * hd;
+      if constexpr (VEC == 2) {
+        *reinterpret_cast<float2*>(q + i) = make_float2(y1[0], y1[1]);
+        *reinterpret_cast<float2*>(q + i + half) = make_float2(y2[0], y2[1]);
+      } else {
+        q[i] = y1[0];
+        q[i + half] = y2[0];
+      }
+    } else {
+      TA* dst = Kp + (((size_t)blk * Hkv + (h - Hq)) * 16 + slot) * hd;
+      if constexpr (VEC == 2 && sizeof(TA) == 2) {
+        *reinterpret_cast<__nv_bfloat162*>(dst + i) = __floats2bfloat162_rn(y1[0], y1[1]);
+        *reinterpret_cast<__nv_bfloat162*>(dst + i + half) = __floats2bfloat162_rn(y2[0], y2[1]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          dst[i + v] = Elt<TA>::from_f(y1[v]);
+          dst[i + v + half] = Elt<TA>::from_f(y2[v]);
+        }
+      }
+    }
   }
 }
 
@@ -139,6 +209,10 @@ SF_DEV void cp_async_wait_all() {
 
 template <typename TKV, int HD>
 __global__ void __launch_bounds__(128) attn_partial_kernel(AttnParams p) {
+  KtScope kt_(KT_ATTN_PART, (uint32_t)(HD));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   constexpr int VEC = 16 / sizeof(TKV);     // elements per 16-byte vector
   constexpr int KLD = HD + VEC;             // padded K row (bank-conflict-free per-key reads)
   extern __shared__ __align__(16) uint8_t sm[];
@@ -283,6 +357,10 @@ __global__ void __launch_bounds__(128) attn_partial_kernel(AttnParams p) {
 // combine chunks 0..pos/128 in order: M = max m_c; out = sum_c acc_c e^(m_c - M) / sum_c l_c e^(m_c - M)
 template <typename TA>
 __global__ void attn_combine_kernel(AttnParams p) {
+  KtScope kt_(KT_ATTN_COMB, (uint32_t)(0));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   const int t = blockIdx.x, h = blockIdx.y;
   const int b = t / p.q_len, qi = t % p.q_len;
   const int pos = p.pos0[b] + qi;
@@ -304,6 +382,10 @@ __global__ void attn_combine_kernel(AttnParams p) {
 // (BIDIR_LOCAL), no RoPE; effective batch B. One CTA per (b, head).
 template <typename TA>
 __global__ void bidir_attn_kernel(const TA* qkv, int k, int Hq, int Hkv, int hd, int causal, TA* out) {
+  KtScope kt_(KT_BIDIR, (uint32_t)(k));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   extern __shared__ float fs[];
   const int b = blockIdx.x, h = blockIdx.y;
   const int G = Hq / Hkv, kh = h / G;
@@ -351,6 +433,10 @@ __global__ void bidir_attn_kernel(const TA* qkv, int k, int Hq, int Hkv, int hd,
 
 // ------------------------------------------------------------------------ gather
 __global__ void gather_rows_kernel(const float* src, int q_len, const int* idx, int const_idx, int d, float* dst) {
+  KtScope kt_(KT_GATHER, (uint32_t)(d));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   const int b = blockIdx.x;
   const int r = idx ? idx[b] : const_idx;
   const float* s = src + ((size_t)b * q_len + r) * d;
@@ -369,6 +455,10 @@ SF_DEV void better(float& bv, int& bi, float v, int i) {
 }
 __global__ void __launch_bounds__(256) argmax_partial_kernel(const float* logits, int V, int nsplit, float* pval,
                                                              int* pidx, int* err) {
+  KtScope kt_(KT_ARGMAX_P, (uint32_t)(V));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   __shared__ float sv[8];
   __shared__ int si[8];
   const int row = blockIdx.y, sp = blockIdx.x;
@@ -402,6 +492,10 @@ __global__ void __launch_bounds__(256) argmax_partial_kernel(const float* logits
   }
 }
 __global__ void argmax_final_kernel(const float* pval, const int* pidx, int R, int nsplit, int* out) {
+  KtScope kt_(KT_ARGMAX_F, (uint32_t)(nsplit));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= R) return;
   float bv = -INFINITY;
@@ -415,6 +509,10 @@ __global__ void argmax_final_kernel(const float* pval, const int* pidx, int R, i
 __global__ void accept_kernel(int B, int k, const int* draft, const int* greedy, int* seq_len, int* n_prev,
                               int* last_token, int* r_b, int* accept_len, int* emitted, int* step_counter,
                               int* accept_log, int* emitted_log, int log_cap) {
+  KtScope kt_(KT_ACCEPT, (uint32_t)(k));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   const int b = threadIdx.x;
   const int step = step_counter ? *step_counter : 0;
   if (b < B) {
@@ -440,6 +538,10 @@ __global__ void accept_kernel(int B, int k, const int* draft, const int* greedy,
 __global__ void force_drafts_kernel(int B, int k, int V, const int* cont, int cont_len, const int* corrupt,
                                     int corrupt_steps, const int* seq_len, const int* prompt_len,
                                     const int* step_counter, int* draft) {
+  KtScope kt_(KT_MISC, (uint32_t)(1));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const int gidx = seq_len[b] - prompt_len[b];
@@ -454,12 +556,20 @@ __global__ void force_drafts_kernel(int B, int k, int V, const int* cont, int co
 }
 
 __global__ void fill_kernel(int* p, int n, int v) {
+  KtScope kt_(KT_MISC, (uint32_t)(2));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
 }
 
 __global__ void prefill_finish_kernel(int B, int P, const int* greedy, int* seq_len, int* n_prev, int* last_token,
                                       int* r_b, int* prompt_len, int* first_out) {
+  KtScope kt_(KT_MISC, (uint32_t)(3));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   seq_len[b] = P;
@@ -475,54 +585,57 @@ __global__ void prefill_finish_kernel(int B, int P, const int* greedy, int* seq_
 
 cudaError_t launch_rope_table(float2* table, int max_seq, int hd, float theta, cudaStream_t s) {
   const int n = max_seq * hd / 2;
-  rope_table_kernel<<<SF_GRID(n, 256), 256, 0, s>>>(table, max_seq, hd, theta);
+  launch_k(rope_table_kernel, dim3(SF_GRID(n, 256)), dim3(256), 0, s, table, max_seq, hd, theta);
   return cudaGetLastError();
 }
 cudaError_t launch_build_verify_rows(int B, int k, const int* last_token, const int* draft, int* tok_rows,
                                      cudaStream_t s) {
-  build_verify_rows_kernel<<<SF_GRID(B * (k + 1), 128), 128, 0, s>>>(B, k, last_token, draft, tok_rows);
+  launch_k(build_verify_rows_kernel, dim3(SF_GRID(B * (k + 1), 128)), dim3(128), 0, s, B, k, last_token, draft, tok_rows);
   return cudaGetLastError();
 }
 cudaError_t launch_build_prefill_rows(int B, int P, int c0, int C, const int* tokens, int* tok_rows, int* pos0,
                                       cudaStream_t s) {
-  build_prefill_rows_kernel<<<SF_GRID(max(B * C, B), 128), 128, 0, s>>>(B, P, c0, C, tokens, tok_rows, pos0);
+  launch_k(build_prefill_rows_kernel, dim3(SF_GRID(max(B * C, B), 128)), dim3(128), 0, s, B, P, c0, C, tokens, tok_rows, pos0);
   return cudaGetLastError();
 }
 cudaError_t launch_embed(bool bf, const int* tok, const void* embed, int T, int d, int vocab, float* resid,
                          float* tap0, cudaStream_t s) {
   if (bf)
-    embed_kernel<__nv_bfloat16><<<T, 256, 0, s>>>(tok, (const __nv_bfloat16*)embed, d, vocab, resid, tap0);
+    launch_k(embed_kernel<__nv_bfloat16>, dim3(T), dim3(256), 0, s, tok, (const __nv_bfloat16*)embed, d, vocab, resid, tap0);
   else
-    embed_kernel<float><<<T, 256, 0, s>>>(tok, (const float*)embed, d, vocab, resid, tap0);
+    launch_k(embed_kernel<float>, dim3(T), dim3(256), 0, s, tok, (const float*)embed, d, vocab, resid, tap0);
   return cudaGetLastError();
 }
 cudaError_t launch_rmsnorm(bool bf, const float* in, int in_ld, const float* gamma, float eps, int T, int d,
                            void* out, int out_ld, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   if (bf)
-    rmsnorm_kernel<__nv_bfloat16><<<T, 256, 0, s>>>(in, in_ld, gamma, eps, d, (__nv_bfloat16*)out, out_ld);
+    launch_k(rmsnorm_kernel<__nv_bfloat16>, dim3(T), dim3(256), 0, s, in, in_ld, gamma, eps, d, (__nv_bfloat16*)out, out_ld);
   else
-    rmsnorm_kernel<float><<<T, 256, 0, s>>>(in, in_ld, gamma, eps, d, (float*)out, out_ld);
+    launch_k(rmsnorm_kernel<float>, dim3(T), dim3(256), 0, s, in, in_ld, gamma, eps, d, (float*)out, out_ld);
   return cudaGetLastError();
 }
 cudaError_t launch_group_rms(bool bf, const float* taps, int64_t tap_stride, const float* scales, float eps, int T,
                              int d, void* out, cudaStream_t s) {
   if (bf)
-    group_rms_kernel<__nv_bfloat16><<<T, 256, 0, s>>>(taps, tap_stride, scales, eps, d, (__nv_bfloat16*)out);
+    launch_k(group_rms_kernel<__nv_bfloat16>, dim3(T), dim3(256), 0, s, taps, tap_stride, scales, eps, d, (__nv_bfloat16*)out);
   else
-    group_rms_kernel<float><<<T, 256, 0, s>>>(taps, tap_stride, scales, eps, d, (float*)out);
+    launch_k(group_rms_kernel<float>, dim3(T), dim3(256), 0, s, taps, tap_stride, scales, eps, d, (float*)out);
   return cudaGetLastError();
 }
 cudaError_t launch_rope_append(bool bf, const void* qkv, int T, int q_len, const int* pos0, const float2* rope,
                                int Hq, int Hkv, int hd, const int* bt, int pps, void* Kp, void* Vp, float* q_out,
                                cudaStream_t s) {
-  if (bf)
-    rope_append_kernel<__nv_bfloat16><<<T, 256, 0, s>>>((const __nv_bfloat16*)qkv, q_len, pos0, rope, Hq, Hkv, hd,
-                                                         bt, pps, (__nv_bfloat16*)Kp, (__nv_bfloat16*)Vp, q_out);
-  else
-    rope_append_kernel<float><<<T, 256, 0, s>>>((const float*)qkv, q_len, pos0, rope, Hq, Hkv, hd, bt, pps,
-                                                 (float*)Kp, (float*)Vp, q_out);
-  return cudaGetLastError();
+  const dim3 grid(T, (Hq + 2 * Hkv + 3) / 4);
+  const bool v2 = (hd / 2) % 64 == 0;
+  if (bf) {
+    auto k = v2 ? rope_append_kernel<__nv_bfloat16, 2> : rope_append_kernel<__nv_bfloat16, 1>;
+    return launch_k(k, grid, dim3(128), 0, s, (const __nv_bfloat16*)qkv, q_len, pos0, rope, Hq, Hkv, hd, bt, pps,
+                    (__nv_bfloat16*)Kp, (__nv_bfloat16*)Vp, q_out);
+  }
+  auto k = v2 ? rope_append_kernel<float, 2> : rope_append_kernel<float, 1>;
+  return launch_k(k, grid, dim3(128), 0, s, (const float*)qkv, q_len, pos0, rope, Hq, Hkv, hd, bt, pps, (float*)Kp,
+                  (float*)Vp, q_out);
 }
 
 template <typename TKV, int HD>
@@ -539,14 +652,14 @@ static cudaError_t attn_impl(const AttnParams& p, cudaStream_t s) {
   const int ntiles = (p.q_len * G + QT - 1) / QT;
   const int nch = (p.max_key + kAttnChunk - 1) / kAttnChunk;
   dim3 grid(nch, p.Hkv * ntiles, p.B);
-  attn_partial_kernel<TKV, HD><<<grid, 128, smem, s>>>(p);
+  launch_k(attn_partial_kernel<TKV, HD>, dim3(grid), dim3(128), smem, s, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   dim3 g2(p.B * p.q_len, p.Hq);
   if (sizeof(TKV) == 2)
-    attn_combine_kernel<__nv_bfloat16><<<g2, min(HD, 128), 0, s>>>(p);
+    launch_k(attn_combine_kernel<__nv_bfloat16>, dim3(g2), dim3(min(HD, 128)), 0, s, p);
   else
-    attn_combine_kernel<float><<<g2, min(HD, 128), 0, s>>>(p);
+    launch_k(attn_combine_kernel<float>, dim3(g2), dim3(min(HD, 128)), 0, s, p);
   return cudaGetLastError();
 }
 cudaError_t launch_attention(bool bf, const AttnParams& p, cudaStream_t s) {
@@ -571,50 +684,58 @@ cudaError_t launch_bidir_attention(bool bf, const void* qkv, int B, int k, int H
   dim3 grid(B, Hq);
   const size_t smem = (size_t)(3 * k * hd + k * k) * 4;
   if (bf)
-    bidir_attn_kernel<__nv_bfloat16><<<grid, 128, smem, s>>>((const __nv_bfloat16*)qkv, k, Hq, Hkv, hd, causal,
+    launch_k(bidir_attn_kernel<__nv_bfloat16>, dim3(grid), dim3(128), smem, s, (const __nv_bfloat16*)qkv, k, Hq, Hkv, hd, causal,
                                                             (__nv_bfloat16*)out);
   else
-    bidir_attn_kernel<float><<<grid, 128, smem, s>>>((const float*)qkv, k, Hq, Hkv, hd, causal, (float*)out);
+    launch_k(bidir_attn_kernel<float>, dim3(grid), dim3(128), smem, s, (const float*)qkv, k, Hq, Hkv, hd, causal, (float*)out);
   return cudaGetLastError();
 }
 cudaError_t launch_gather_rows(const float* src, int q_len, const int* idx, int const_idx, int B, int d, float* dst,
                                cudaStream_t s) {
-  gather_rows_kernel<<<B, 256, 0, s>>>(src, q_len, idx, const_idx, d, dst);
+  launch_k(gather_rows_kernel, dim3(B), dim3(256), 0, s, src, q_len, idx, const_idx, d, dst);
   return cudaGetLastError();
 }
 cudaError_t launch_argmax(const float* logits, int R, int V, float* pval, int* pidx, int* out, int* err,
                           cudaStream_t s) {
   const int ns = argmax_splits(V);
   dim3 grid(ns, R);
-  argmax_partial_kernel<<<grid, 256, 0, s>>>(logits, V, ns, pval, pidx, err);
-  argmax_final_kernel<<<SF_GRID(R, 128), 128, 0, s>>>(pval, pidx, R, ns, out);
+  launch_k(argmax_partial_kernel, dim3(grid), dim3(256), 0, s, logits, V, ns, pval, pidx, err);
+  launch_k(argmax_final_kernel, dim3(SF_GRID(R, 128)), dim3(128), 0, s, pval, pidx, R, ns, out);
   return cudaGetLastError();
 }
 cudaError_t launch_accept(int B, int k, const int* draft, const int* greedy, int* seq_len, int* n_prev,
                           int* last_token, int* r_b, int* accept_len, int* emitted, int* step_counter,
                           int* accept_log, int* emitted_log, int log_cap, cudaStream_t s) {
   const int th = ((B + 31) / 32) * 32;
-  accept_kernel<<<1, th, 0, s>>>(B, k, draft, greedy, seq_len, n_prev, last_token, r_b, accept_len, emitted,
+  launch_k(accept_kernel, dim3(1), dim3(th), 0, s, B, k, draft, greedy, seq_len, n_prev, last_token, r_b, accept_len, emitted,
                                  step_counter, accept_log, emitted_log, log_cap);
   return cudaGetLastError();
 }
 cudaError_t launch_force_drafts(int B, int k, int V, const int* cont, int cont_len, const int* corrupt,
                                 int corrupt_steps, const int* seq_len, const int* prompt_len,
                                 const int* step_counter, int* draft, cudaStream_t s) {
-  force_drafts_kernel<<<SF_GRID(B, 128), 128, 0, s>>>(B, k, V, cont, cont_len, corrupt, corrupt_steps, seq_len,
+  launch_k(force_drafts_kernel, dim3(SF_GRID(B, 128)), dim3(128), 0, s, B, k, V, cont, cont_len, corrupt, corrupt_steps, seq_len,
                                                       prompt_len, step_counter, draft);
   return cudaGetLastError();
 }
 cudaError_t launch_fill(int* p, int n, int v, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  fill_kernel<<<SF_GRID(n, 256), 256, 0, s>>>(p, n, v);
+  launch_k(fill_kernel, dim3(SF_GRID(n, 256)), dim3(256), 0, s, p, n, v);
   return cudaGetLastError();
 }
 cudaError_t launch_prefill_finish(int B, int P, const int* greedy, int* seq_len, int* n_prev, int* last_token,
                                   int* r_b, int* prompt_len, int* first_out, cudaStream_t s) {
-  prefill_finish_kernel<<<SF_GRID(B, 128), 128, 0, s>>>(B, P, greedy, seq_len, n_prev, last_token, r_b,
+  launch_k(prefill_finish_kernel, dim3(SF_GRID(B, 128)), dim3(128), 0, s, B, P, greedy, seq_len, n_prev, last_token, r_b,
                                                          prompt_len, first_out);
   return cudaGetLastError();
+}
+
+cudaError_t kt_setup_kernels(void* rec, unsigned* cnt, unsigned cap) {
+  KtBuf b;
+  b.rec = reinterpret_cast<KtRec*>(rec);
+  b.cnt = cnt;
+  b.cap = cap;
+  return kt_setup_tu(b);
 }
 
 }  // namespace sf

@@ -60,4 +60,11 @@ cudaError_t launch_prefill_finish(int B, int P, const int* greedy, int* seq_len,
 
 int argmax_splits(int V);
 
+// kernel timeline (SF_KTRACE=1, tools only): point every translation unit's device log at rec/cnt
+cudaError_t kt_setup_kernels(void* rec, unsigned* cnt, unsigned cap);
+cudaError_t kt_setup_gemm(void* rec, unsigned* cnt, unsigned cap);
+cudaError_t kt_setup_attn_mma(void* rec, unsigned* cnt, unsigned cap);
+cudaError_t kt_setup_attn_fd(void* rec, unsigned* cnt, unsigned cap);
+constexpr int kKtRecBytes = 40;
+
 }  // namespace sf

@@ -286,6 +286,15 @@ struct ProfScope {
   }
 };
 
+// SF_DEBUG_SYNC=1 (debugging only): synchronise after every launch group and name the first failure
+static cudaError_t dbg_sync(sf_handle* h, const char* what, cudaError_t e) {
+  static const bool on = getenv("SF_DEBUG_SYNC") && atoi(getenv("SF_DEBUG_SYNC")) > 0;
+  if (!on || e != cudaSuccess) return e;
+  cudaError_t r = cudaStreamSynchronize(h->st);
+  if (r != cudaSuccess) fprintf(stderr, "SF_DEBUG_SYNC: %s failed: %s\n", what, cudaGetErrorString(r));
+  return r;
+}
+
 static cudaError_t gemm(sf_handle* h, const void* A, int lda, const void* W, int T, int N, int K, GemmEpi epi) {
   const double wb = h->bf ? 2.0 : 4.0;
   const double ob = (epi.mode == EPI_STORE_ACT || epi.mode == EPI_SWIGLU_ACT) ? wb : 4.0;
@@ -298,7 +307,9 @@ static cudaError_t gemm(sf_handle* h, const void* A, int lda, const void* W, int
   sc.counters = h->gcnt;
   sc.n_counters = 4096;
   h->launches += (T + 511) / 512;
-  return gemm_launch(h->bf, A, lda, W, h->bf, T, N, K, epi, sc, h->st);
+  char nm[96];
+  snprintf(nm, sizeof nm, "gemm T=%d N=%d K=%d mode=%d", T, N, K, epi.mode);
+  return dbg_sync(h, nm, gemm_launch(h->bf, A, lda, W, h->bf, T, N, K, epi, sc, h->st));
 }
 static GemmEpi epi_act(void* out, int ldo) {
   GemmEpi e;
@@ -345,8 +356,8 @@ static bool gemm_resid_norm(sf_handle* h, cudaError_t* err, const void* A, int l
   if ((*err = gemm(h, A, lda, W, T, N, K, e)) != cudaSuccess) return true;
   ProfScope ps(h, 2, (double)T * N * 4.0 * 3);
   h->launches++;
-  *err = launch_resid_norm(h->gpart, &g, T, rep, h->p.d, resid, bias, out, tap, gamma, h->c.rms_eps,
-                           gamma ? (__nv_bfloat16*)h->xn : nullptr, h->st);
+  *err = dbg_sync(h, "resid_norm", launch_resid_norm(h->gpart, &g, T, rep, h->p.d, resid, bias, out, tap, gamma,
+                                                     h->c.rms_eps, gamma ? (__nv_bfloat16*)h->xn : nullptr, h->st));
   return true;
 }
 
@@ -384,7 +395,8 @@ static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const i
   ap.max_key = std::min(max_key, h->c.max_seq);
   ap.n_pages = p.n_pages;
   h->launches += 3;
-  return launch_attention(h->bf, ap, h->st);
+  if ((e = dbg_sync(h, "rope_append", e)) != cudaSuccess) return e;
+  return dbg_sync(h, "attention", launch_attention(h->bf, ap, h->st));
 }
 
 // Base decoder forward over T rows (q_len per sequence, positions pos0[b] + i); writes resid and
@@ -549,6 +561,25 @@ static cudaError_t copy_out(sf_handle* h, void* dst, const void* src, size_t byt
 }
 
 // ================================================================= C ABI
+// ---- kernel timeline (SF_KTRACE=1; tools/ktrace.py)
+static void* g_kt_rec = nullptr;
+static unsigned* g_kt_cnt = nullptr;
+static constexpr unsigned kKtCap = 1u << 21;
+static bool kt_enable() {
+  static const bool on = getenv("SF_KTRACE") && atoi(getenv("SF_KTRACE")) > 0;
+  if (!on) return false;
+  if (!g_kt_rec) {
+    if (cudaMalloc(&g_kt_rec, (size_t)kKtCap * kKtRecBytes) != cudaSuccess) return false;
+    if (cudaMalloc((void**)&g_kt_cnt, 4) != cudaSuccess) return false;
+    cudaMemset(g_kt_cnt, 0, 4);
+    kt_setup_kernels(g_kt_rec, g_kt_cnt, kKtCap);
+    kt_setup_gemm(g_kt_rec, g_kt_cnt, kKtCap);
+    kt_setup_attn_mma(g_kt_rec, g_kt_cnt, kKtCap);
+    kt_setup_attn_fd(g_kt_rec, g_kt_cnt, kKtCap);
+  }
+  return true;
+}
+
 extern "C" {
 
 int sf_weight_table(const sf_config* cfg, sf_tensor_desc* out, int cap) {
@@ -595,6 +626,7 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
   if (!valid_config(cfg, &why)) return SF_ERR_ARG;
   if (!weights_dev || !workspace_dev) return SF_ERR_ARG;
   if (((uintptr_t)weights_dev | (uintptr_t)workspace_dev) % kAlign) return SF_ERR_ARG;
+  kt_enable();  // no-op unless SF_KTRACE=1
   auto* h = new sf_handle();
   h->c = *cfg;
   h->p = make_plan(cfg);
@@ -991,6 +1023,22 @@ sf_status sf_profile_read(sf_handle* h, int32_t cls, double* total_ms, int64_t* 
   *count = n;
   *bytes = by;
   return SF_OK;
+}
+
+int32_t sf_debug_ktrace(void* dst_host, int32_t cap) {
+  if (!kt_enable() || !dst_host || cap <= 0) return 0;
+  cudaDeviceSynchronize();
+  unsigned n = 0;
+  cudaMemcpy(&n, g_kt_cnt, 4, cudaMemcpyDeviceToHost);
+  n = std::min<unsigned>(std::min<unsigned>(n, kKtCap), (unsigned)cap);
+  cudaMemcpy(dst_host, g_kt_rec, (size_t)n * kKtRecBytes, cudaMemcpyDeviceToHost);
+  cudaMemset(g_kt_cnt, 0, 4);
+  return (int32_t)n;
+}
+
+int32_t sf_debug_gemm_trace(uint64_t* dst_host, int32_t cap) {
+  if (!dst_host || cap <= 0) return 0;
+  return gemm_trace_copy(reinterpret_cast<unsigned long long*>(dst_host), cap);
 }
 
 sf_status sf_test_gemm(int32_t dtype, const void* A, const void* W, float* out, int32_t T, int32_t N, int32_t K,

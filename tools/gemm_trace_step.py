@@ -1,0 +1,40 @@
+"""Per-CTA timeline of the last in-step (CUDA graph) GEMM launch of weight shape N=SF_GEMM_TRACE_N.
+  SF_GEMM_TRACE=1 SF_GEMM_TRACE_N=22016 B=64 python tools/gemm_trace_step.py"""
+import os, sys, ctypes as C
+os.environ.setdefault("SF_GEMM_TRACE", "1")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2511_20340_b200 import Engine, EngineConfig
+from paper_2511_20340_b200 import _native as N
+from synth import get_config, make_prompts, make_weights
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
+cfg = get_config(os.environ.get("CFG", "7b")); B = int(os.environ.get("B", "64"))
+w = make_weights(cfg, seed=0, device="cuda")
+eng = Engine(EngineConfig.from_model(cfg, max_batch=B, max_seq=cfg.prompt_len + 32 * (cfg.draft_len + 1),
+                                     flags=N.SF_FLAG_CUDA_GRAPH), w)
+del w
+eng.prefill(make_prompts(B, cfg.prompt_len, cfg.vocab).cuda())
+eng.decode_steps(4); eng.sync()
+buf = np.zeros(2 * 160 * 128, dtype=np.uint64)
+N.lib().sf_debug_gemm_trace(buf.ctypes.data_as(C.c_void_p), buf.size)
+eng.decode_steps(1); eng.sync()
+N.lib().sf_debug_gemm_trace(buf.ctypes.data_as(C.c_void_p), buf.size)
+tr = buf.reshape(-1, 128).astype(np.int64); tr = tr[tr[:, 0] > 0]
+t0 = tr[:, 0].min(); R = np.where(tr > 0, (tr - t0) / 1e3, np.nan)
+print(f"== in-step GEMM N={os.environ.get('SF_GEMM_TRACE_N')} B={B}: {len(tr)} CTAs, span {np.nanmax(R):.2f} us")
+for k, c in {"start": 0, "setup": 1, "prod0": 2, "mma_full0": 3, "mma_last": 4, "epi_done": 5}.items():
+    v = R[:, c]; print(f"  {k:10s} min {np.nanmin(v):7.2f} med {np.nanmedian(v):7.2f} max {np.nanmax(v):7.2f} us")
+for sg in range(4):
+    v = R[:, 8 + 4 * sg: 12 + 4 * sg]
+    if np.all(np.isnan(v)): continue
+    print(f"  seg{sg}: mma_start/issued/epi_ready/epi_done med " + " ".join(f"{np.nanmedian(v[:, j]):7.2f}" for j in range(4)) +
+          "   max " + " ".join(f"{np.nanmax(v[:, j]):7.2f}" for j in range(4)))
+u = R[:, 24:64]; d = np.diff(u, axis=1)
+print("  per-unit full-barrier interval (us): med %.3f  p90 %.3f" % (np.nanmedian(d), np.nanpercentile(d, 90)))
+print("  unit pass times CTA0:", " ".join(f"{x:.2f}" for x in u[0, :20]))
+print("  producer issue CTA0: ", " ".join(f"{x:.2f}" for x in R[0, 64:84]))
+print("  last-seg head: flags-acquired / bulk-landed / pass0-done (med, max):",
+      " ".join(f"{np.nanmedian(R[:, c]):.2f}/{np.nanmax(R[:, c]):.2f}" for c in (104, 105, 106)))
+print("  head chunk0 adds/stores, chunk1 adds/stores (med):", " ".join(f"{np.nanmedian(R[:, c]):.2f}" for c in (107, 109, 108, 110)))
+print("  swiglu chunk0: pre-math / staged / barrier (med):", " ".join(f"{np.nanmedian(R[:, c]):.2f}" for c in (111, 112, 113)))
