@@ -1,15 +1,20 @@
 // attn_fd.cu -- bf16 hybrid-mask paged decode attention (mode CAUSAL_PREFIX), flash-decoding form.
 //
-// One CTA item = (sequence b, kv head, 16-row query tile); persistent CTAs walk the items. A
+// One CTA item = (sequence b, kv head, 16-row query tile, 512-key segment); persistent CTAs walk the
+// items, so even a single sequence spreads over (heads x segments) SMs. A
 // producer warp streams the item's 128-key K/V chunks with TMA (one 2-D 128B-swizzled box per
 // (16-key page, 64-dim half)) into a 3-stage mbarrier ring. Compute warp w owns keys
 // [32w, 32w+32) of every chunk and keeps its own online-softmax state (m, l, O[16x128]) across
 // the chunks -- no cross-warp synchronisation per chunk, P never leaves registers:
 //   S = Q K_w^T (mma.sync m16n8k16 bf16 -> fp32), masked (key <= row position), m_new = max,
 //   O = O e^(m_old - m_new) + P V_w,  l = l e^(m_old - m_new) + sum P.
-// At the end of the item the 4 warp states are merged in the fixed order w = 0..3 and normalised.
-// Every row's arithmetic (chunk boundaries at fixed absolute 128-key positions, per-warp key
-// slices, merge order) is independent of batch size and block length (batch invariance, C23).
+// At the end of the item the 4 warp states are merged in the fixed order w = 0..3 into the
+// segment's unnormalised (M, L, acc). A row whose keys span one segment is normalised directly;
+// otherwise each segment is written to the partial buffer and the CTA that completes the last
+// segment of the (b, kv head, tile) group (arrival counter) merges segments 0, 1, ... in order:
+// out = sum_s acc_s 2^(M_s - M) / sum_s L_s 2^(M_s - M) -- for one segment exactly acc / L.
+// Every row's arithmetic (chunk and segment boundaries at fixed absolute key positions, per-warp
+// key slices, merge orders) is independent of batch size and block length (batch invariance, C23).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -28,7 +33,7 @@ constexpr int NST = 3;
 constexpr int KV_BYTES = CH * HD * 2;      // 32 KB
 constexpr int STAGE_BYTES = 2 * KV_BYTES;  // 64 KB
 constexpr int MERGE_BYTES = 4 * 16 * (HD + 2) * 4;  // per-warp O, m, l for the final merge
-constexpr int SMEM = NST * STAGE_BYTES + MERGE_BYTES + 2 * NST * 8 + 1024 + 64;
+constexpr int SMEM = NST * STAGE_BYTES + MERGE_BYTES + 2 * NST * 8 + 1024 + 64 + 16;
 
 SF_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -59,7 +64,7 @@ SF_DEV uint32_t swz(int j, int c) {
 SF_DEV void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 struct Item {
-  int b, kvh, qt, nch;
+  int b, kvh, qt, seg, c0, c1, nseg;  // chunks [c0, c1) of segment seg (of nseg) of group (b, kvh, qt)
 };
 
 }  // namespace
@@ -67,7 +72,7 @@ struct Item {
 // item = (b * Hkv + kvh) * ntiles + qt. Warps 0..3 compute, warp 4 produces.
 __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__ CUtensorMap tmK,
                                                         const __grid_constant__ CUtensorMap tmV, AttnParams p,
-                                                        int ntiles, int n_items) {
+                                                        int ntiles, int nseg_max, int seg_keys, int n_items) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   const uint32_t raw = smem_u32(sm_raw);
   uint8_t* sm = sm_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -77,6 +82,7 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
   float* mrg_l = mrg_m + 4 * 16;
   uint64_t* full = reinterpret_cast<uint64_t*>(mrg_l + 4 * 16);
   uint64_t* empty = full + NST;
+  int* mrg_flag = reinterpret_cast<int*>(empty + NST);
 
   KtScope kt_(KT_ATTN, (uint32_t)p.q_len);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -84,8 +90,13 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
   const int G = p.Hq / p.Hkv;
   const int R = p.q_len * G;
 
+  // segment-major item order: consecutive CTAs take different groups' segment s, so the long
+  // (full) and short (tail) segments spread evenly over the persistent CTAs
+  const int n_groups = p.B * p.Hkv * ntiles;
+  const int seg_ch = seg_keys / CH;
   auto item_of = [&](int idx, Item& it) {
-    int r = idx;
+    int r = idx % n_groups;
+    it.seg = idx / n_groups;
     it.qt = r % ntiles;
     r /= ntiles;
     it.kvh = r % p.Hkv;
@@ -93,7 +104,10 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
     const int r0 = it.qt * 16;
     const int nr = min(16, R - r0);
     const int kmax = min(p.pos0[it.b] + min(p.q_len - 1, (r0 + nr - 1) / G), p.max_key - 1);
-    it.nch = kmax / CH + 1;
+    const int nch = kmax / CH + 1;
+    it.nseg = (nch + seg_ch - 1) / seg_ch;
+    it.c0 = it.seg * seg_ch;
+    it.c1 = min(nch, it.c0 + seg_ch);  // empty when seg >= nseg
     return kmax;
   };
 
@@ -119,7 +133,7 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       Item it;
       const int kmax = item_of(item, it);
-      for (int c = 0; c < it.nch; ++c, ++seq) {
+      for (int c = it.c0; c < it.c1; ++c, ++seq) {
         const int st = seq % NST;
         mbar_wait(&empty[st], ((uint32_t)(seq / NST) & 1u) ^ 1u);
         const int kstart = c * CH;
@@ -152,6 +166,8 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     Item it;
     item_of(item, it);
+    if (it.c0 >= it.c1) continue;  // segment beyond this group's keys
+    const unsigned long long ti0 = g_kt.rec ? kt_now() : 0ull;
     const int r0 = it.qt * 16;
     const int nr = min(16, R - r0);
     const int base = p.pos0[it.b];
@@ -181,7 +197,7 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
 #pragma unroll
       for (int i = 0; i < 4; ++i) o[nt][i] = 0.f;
 
-    for (int c = 0; c < it.nch; ++c, ++seq) {
+    for (int c = it.c0; c < it.c1; ++c, ++seq) {
       const int st = seq % NST;
       mbar_wait(&full[st], (uint32_t)(seq / NST) & 1u);
       const uint32_t kb = sbase + st * STAGE_BYTES, vb = kb + KV_BYTES;
@@ -275,6 +291,7 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
     }
+    const unsigned long long ti1 = g_kt.rec ? kt_now() : 0ull;
     // ---- merge the 4 warp states in fixed order and normalise
 #pragma unroll
     for (int nt = 0; nt < 16; ++nt) {
@@ -289,6 +306,7 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
       mrg_l[warp * 16 + g + 8] = l_hi;
     }
     named_bar(1, 128);
+    const int group = (it.b * p.Hkv + it.kvh) * ntiles + it.qt;
     for (int e = tid; e < 16 * HD; e += 128) {
       const int r = e / HD, d = e % HD;
       if (r < nr) {
@@ -304,10 +322,50 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
         }
         const int rr = r0 + r, qi = rr / G, h = it.kvh * G + rr % G;
         const int t = it.b * p.q_len + qi;
-        reinterpret_cast<__nv_bfloat16*>(p.out)[((size_t)t * p.Hq + h) * HD + d] = __float2bfloat16_rn(acc / L);
+        if (it.nseg == 1) {
+          reinterpret_cast<__nv_bfloat16*>(p.out)[((size_t)t * p.Hq + h) * HD + d] = __float2bfloat16_rn(acc / L);
+        } else {
+          const size_t slot = ((size_t)t * p.Hq + h) * p.nchunk_max + it.seg;
+          p.part_o[slot * HD + d] = acc;
+          if (d == 0) {
+            p.part_ml[2 * slot] = M;
+            p.part_ml[2 * slot + 1] = L;
+          }
+        }
+      }
+    }
+    if (it.nseg > 1) {
+      // one gpu-scope release per item (cumulative over the compute warps' partial writes, which
+      // the CTA barrier orders before it) instead of a fence in every thread
+      named_bar(1, 128);
+      if (tid == 0) {
+        int prev;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(p.seg_cnt + group) : "memory");
+        mrg_flag[0] = prev == it.nseg - 1;
+      }
+      named_bar(1, 128);
+      if (mrg_flag[0]) {  // every segment of the group has landed: merge them in segment order
+        for (int e = tid; e < nr * HD; e += 128) {
+          const int r = e / HD, d = e % HD;
+          const int rr = r0 + r, qi = rr / G, h = it.kvh * G + rr % G;
+          const int t = it.b * p.q_len + qi;
+          const size_t s0 = ((size_t)t * p.Hq + h) * p.nchunk_max;
+          float M = -INFINITY;
+          for (int sg = 0; sg < it.nseg; ++sg) M = fmaxf(M, __ldcg(&p.part_ml[2 * (s0 + sg)]));
+          float L = 0.f, acc = 0.f;
+          for (int sg = 0; sg < it.nseg; ++sg) {
+            const float ms = __ldcg(&p.part_ml[2 * (s0 + sg)]);
+            const float f = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
+            L += __ldcg(&p.part_ml[2 * (s0 + sg) + 1]) * f;
+            acc += __ldcg(&p.part_o[(s0 + sg) * HD + d]) * f;
+          }
+          reinterpret_cast<__nv_bfloat16*>(p.out)[((size_t)t * p.Hq + h) * HD + d] = __float2bfloat16_rn(acc / L);
+        }
+        if (tid == 0) p.seg_cnt[group] = 0;  // re-arm for the next launch
       }
     }
     named_bar(1, 128);
+    if (tid == 0 && g_kt.rec) kt_item((uint32_t)(it.seg | (it.nseg << 8) | ((it.c1 - it.c0) << 16)), ti0, ti1, kt_now());
   }
 }
 
@@ -342,12 +400,16 @@ cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
   }
   const int G = p.Hq / p.Hkv;
   const int ntiles = (p.q_len * G + 15) / 16;
-  const int n_items = p.B * p.Hkv * ntiles;
+  static const int env_seg = getenv("SF_ATTN_SEG") ? atoi(getenv("SF_ATTN_SEG")) : 0;  // experiments
+  const int seg_keys = (env_seg >= CH && env_seg % CH == 0) ? env_seg : kAttnSeg;
+  const int nseg_max = (p.max_key + seg_keys - 1) / seg_keys;
+  if (nseg_max > p.nchunk_max || !p.seg_cnt) return cudaErrorInvalidValue;
+  const int n_items = p.B * p.Hkv * ntiles * nseg_max;
   const int grid = std::min(n_items, num_sms);
   CUtensorMap mk, mv;
   const long long rows = (long long)p.n_pages * p.Hkv * 16;
   if (!encode_kv_map(&mk, p.Kp, rows) || !encode_kv_map(&mv, p.Vp, rows)) return cudaErrorInvalidValue;
-  launch_k(attn_fd_kernel, dim3(grid), dim3(160), SMEM, s, mk, mv, p, ntiles, n_items);
+  launch_k(attn_fd_kernel, dim3(grid), dim3(160), SMEM, s, mk, mv, p, ntiles, nseg_max, seg_keys, n_items);
   return cudaGetLastError();
 }
 

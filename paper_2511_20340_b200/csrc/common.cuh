@@ -92,8 +92,9 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
 // timeline of a CUDA-graph step). Off by default: one predicated load per CTA.
 enum KtKind : uint32_t {
   KT_GEMM = 1, KT_RESID_NORM, KT_ROPE, KT_ATTN, KT_RMSNORM, KT_GROUP_RMS, KT_EMBED, KT_ARGMAX_P, KT_ARGMAX_F,
-  KT_ACCEPT, KT_BIDIR, KT_GATHER, KT_ROWS, KT_GEMM_SIMT, KT_ATTN_PART, KT_ATTN_COMB, KT_MISC
+  KT_ACCEPT, KT_BIDIR, KT_GATHER, KT_ROWS, KT_GEMM_SIMT, KT_ATTN_PART, KT_ATTN_COMB, KT_MISC, KT_ITEM
 };
+
 struct KtRec {
   uint32_t kid, smid;
   unsigned long long t0, tw, t1;
@@ -141,6 +142,20 @@ struct KtScope {
     }
   }
 };
+// one free-form record (t0, tw, t1) -- e.g. a work item inside a persistent kernel
+SF_DEV void kt_item(uint32_t param, unsigned long long t0, unsigned long long tw, unsigned long long t1) {
+  if (!g_kt.rec) return;
+  const unsigned i = atomicAdd(g_kt.cnt, 1u);
+  if (i >= g_kt.cap) return;
+  KtRec r;
+  r.kid = (KT_ITEM << 24) | (param & 0xFFFFFFu);
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r.smid));
+  r.t0 = t0;
+  r.tw = tw;
+  r.t1 = t1;
+  r.pad = 0;
+  g_kt.rec[i] = r;
+}
 static inline cudaError_t kt_setup_tu(const KtBuf& b) { return cudaMemcpyToSymbol(g_kt, &b, sizeof(b)); }
 
 // ---------------------------------------------------------------- PTX wrappers (sm_100a)

@@ -130,7 +130,10 @@ SF_DEV void umma_commit_2sm(uint64_t* bar) {
       : "memory");
 }
 
-template <int CG>
+// MODE = the epilogue (EpiMode), a template parameter so each instantiation carries only its own
+// store path: the kernel's code is executed cold once per CTA in the final phase, and every
+// instruction-cache line it does not need is a fetch that competes with the weight stream.
+template <int CG, int MODE>
 __global__ void __launch_bounds__(384, 1)
 gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA, const SkParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -192,16 +195,23 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     // ---- TMA producer warp (converged; one elected lane issues)
     // The weights do not depend on the previous kernel: the first ring's worth of weight tiles is
     // requested before the grid dependency resolves (PDL), the activation tiles after it.
-    const long long npre = (CG == 1 && p.w_tiled) ? min((long long)p.stages, u1 - u0) : 0;
+    const long long npre = p.w_tiled ? min((long long)p.stages, u1 - u0) : 0;
     if (npre > 0 && elect_one()) {
       int tp = (int)(u0 / kb), kp = (int)(u0 % kb);
       for (int i = 0; i < (int)npre; ++i) {
         uint8_t* st = smem + (size_t)i * stage_bytes;
-        mbar_arrive_expect_tx(&full[i], (uint32_t)stage_bytes);
-        if (p.w_tma)
-          tma_load_2d(st, &tmW, &full[i], 0, (tp * kb + kp) * BM, kEvictFirst);
-        else
-          bulk_load(st, p.w_tiles + ((size_t)tp * kb + kp) * (BM * BK), BM * BK * 2, &full[i], kEvictFirst);
+        if constexpr (CG == 1) {
+          mbar_arrive_expect_tx(&full[i], (uint32_t)stage_bytes);
+          if (p.w_tma)
+            tma_load_2d(st, &tmW, &full[i], 0, (tp * kb + kp) * BM, kEvictFirst);
+          else
+            bulk_load(st, p.w_tiles + ((size_t)tp * kb + kp) * (BM * BK), BM * BK * 2, &full[i], kEvictFirst);
+        } else {
+          // the leader arms the barrier for both CTAs' bytes; a fresh phase cannot complete before
+          // that arrival, so the peer's bytes may land first
+          if (rank == 0) mbar_arrive_expect_tx(&full[i], (uint32_t)(2 * stage_bytes));
+          tma_load_2d_2sm(st, &tmW, &full[i], 0, ((tp * 2 + (int)rank) * kb + kp) * BM, kEvictFirst);
+        }
         if (++kp == kb) {
           kp = 0;
           ++tp;
@@ -234,9 +244,11 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           for (int j = 0; j < p.n_sub; ++j)
             tma_load_2d(st + BM * BK * 2 + j * a_rows * BK * 2, &tmA, &full[s], k * BK, j * p.NT, kEvictLast);
         } else {
-          if (rank == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * stage_bytes));
-          // tiled weights viewed as a [blocks*128, 64] tensor: this CTA's 128-row half of pair tile t
-          tma_load_2d_2sm(st, &tmW, &full[s], 0, ((t * 2 + (int)rank) * kb + k) * BM, kEvictFirst);
+          if (!pre) {
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * stage_bytes));
+            // tiled weights viewed as a [blocks*128, 64] tensor: this CTA's 128-row half of pair tile t
+            tma_load_2d_2sm(st, &tmW, &full[s], 0, ((t * 2 + (int)rank) * kb + k) * BM, kEvictFirst);
+          }
           for (int j = 0; j < p.n_sub; ++j)
             tma_load_2d_2sm(st + BM * BK * 2 + j * a_rows * BK * 2, &tmA, &full[s], k * BK,
                             j * p.NT + (int)rank * a_rows, kEvictLast);
@@ -318,111 +330,206 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       ++seg;
       ++t;
     }
-  } else if (warp >= 4) {
-    // ---- epilogue: 8 warps, two per TMEM lane quadrant (warp w reads lanes 32 (w % 4) ..);
-    // the two warps of a quadrant take alternate 32-column chunks.
-    pdl_wait();  // outputs / partial slots / flags may still be in use by the previous kernel
-    kt_.mark();
+  }
+  {
+    // ---- epilogue (named barriers: 1 = the 8 loop warps, 5 = all 12 in the final phase, 2..4 = the
+    // final phase's three groups). Segments before the last: warps 4..11 (two groups of 4 = one warp per TMEM
+    // lane quadrant each, warp w reads lanes 32 (w % 4) ..), alternate 32-column chunks, while the
+    // MMA streams the next segment. The last segment and a parked full tile ("final phase"): all 12
+    // warps (warps 0..3 are done producing / issuing by then) in three groups.
+    if (warp >= 4) pdl_wait();  // outputs / partial slots / flags may still be in use by the previous kernel
+    if (warp >= 4) kt_.mark();
     uint32_t fix_ph = 0;
-    const int quad = warp & 3, half = (warp - 4) >> 2;
+    const int quad = warp & 3;
     const int m = quad * 32 + lane;
-    const int etid = threadIdx.x - 128;  // 0..255
-    const int mode = p.epi.mode;
-    int seg = 0;
-    long long u = u0;
-    while (u < u1) {
-      const int t = (int)(u / kb);
+    const bool lead = threadIdx.x == 128;  // first epilogue thread: flags, barriers' single-thread work
+    constexpr int mode = MODE;
+    const size_t ldo = (size_t)p.epi.ldo;
+    // smem ring reuse once every MMA of the CTA has completed (final phase): partial staging
+    // [0, ring - 48 KB) and three 16 KB output staging buffers at the end
+    constexpr int kStageBytes = 16384;
+    const int ring_bytes = p.stages * stage_bytes;
+    const int out_elt = mode == EPI_STORE_F32 ? 4 : 2;
+    constexpr bool kStageable = MODE == EPI_STORE_ACT || MODE == EPI_STORE_F32 || MODE == EPI_SWIGLU_ACT;
+    const bool can_stage = kStageable && p.stage_ok &&
+                           (ldo * out_elt) % 16 == 0 && ring_bytes >= 3 * kStageBytes + 64 * BM * 4;
+    const int fix_bytes = can_stage ? ring_bytes - 3 * kStageBytes : ring_bytes;
+    uint8_t* stg = smem + ring_bytes - 3 * kStageBytes;
+    const float* smf = reinterpret_cast<const float*>(smem);
+    float* const slot_base = p.partial + (size_t)slot * p.Tp * BM;                    // published tail
+    float* const defer_base = p.partial + (size_t)(p.G * CG + slot) * p.Tp * BM;  // parked full tile
+
+    // one 32-token chunk of this thread's row m: stage [32 tokens][tile columns] in smem, then
+    // write whole rows with 16-byte vectors (per-thread column stores would be 32-byte sectors
+    // 10-100 KB apart)
+    auto staged_store = [&](float (&v)[32], int c0, int nq, int vt_, int gid) {
+      uint8_t* sb = stg + (size_t)gid * kStageBytes;
+      const int rowb = mode == EPI_SWIGLU_ACT ? 128 : (mode == EPI_STORE_ACT ? 256 : 512);
+      if (mode == EPI_STORE_ACT) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) reinterpret_cast<__nv_bfloat16*>(sb + q * 256)[m] = __float2bfloat16_rn(v[q]);
+      } else if (mode == EPI_STORE_F32) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) reinterpret_cast<float*>(sb + q * 512)[m] = v[q];
+      } else {
+        // lane 2i holds gate_i, lane 2i+1 up_i (row-interleaved weight): the even lane forms the 32
+        // tokens of feature i, in batches of 8 independent shuffle / exp / divide chains
+        __nv_bfloat16* srow = reinterpret_cast<__nv_bfloat16*>(sb) + quad * 16 + (lane >> 1);
+#pragma unroll
+        for (int q0 = 0; q0 < 32; q0 += 8) {
+          float uu[8], e[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) uu[j] = __shfl_down_sync(0xffffffffu, v[q0 + j], 1);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) e[j] = __expf(-v[q0 + j]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) e[j] = __fdividef(v[q0 + j], 1.f + e[j]) * uu[j];
+          if (!(lane & 1)) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) srow[(q0 + j) * 64] = __float2bfloat16_rn(e[j]);
+          }
+        }
+      }
+      named_sync(2 + gid, 128);
+      const int col0 = mode == EPI_SWIGLU_ACT ? vt_ * 64 : vt_ * BM;
+      uint8_t* gbase = reinterpret_cast<uint8_t*>(p.epi.out) + ((size_t)c0 * ldo + col0) * out_elt;
+      const int vpr = rowb / 16, ht = quad * 32 + lane;
+      for (int i = ht; i < nq * vpr; i += 128) {
+        const int q = i / vpr, x = i % vpr;
+        *reinterpret_cast<uint4*>(gbase + (size_t)q * ldo * out_elt + x * 16) =
+            *reinterpret_cast<const uint4*>(sb + q * rowb + x * 16);
+      }
+      named_sync(2 + gid, 128);
+    };
+    // per-thread column stores (segments that end while the ring is still streaming)
+    auto direct_store = [&](float (&v)[32], int c0, int nq, int vt_) {
+      const int n = vt_ * BM + m;
+      if (mode == EPI_STORE_ACT) {
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.epi.out) + (size_t)c0 * ldo + n;
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (q < nq) o[q * ldo] = __float2bfloat16_rn(v[q]);
+      } else if (mode == EPI_STORE_F32) {
+        float* o = reinterpret_cast<float*>(p.epi.out) + (size_t)c0 * ldo + n;
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (q < nq) o[q * ldo] = v[q];
+      } else if (mode == EPI_ADD_F32) {
+        float* o = reinterpret_cast<float*>(p.epi.out) + (size_t)c0 * ldo + n;
+        float old[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) old[q] = (q < nq) ? o[q * ldo] : 0.f;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = old[q] + v[q];
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (q < nq) o[q * ldo] = v[q];
+        if (p.epi.tap) {
+          float* tp = p.epi.tap + (size_t)c0 * ldo + n;
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (q < nq) tp[q * ldo] = v[q];
+        }
+      } else if (mode == EPI_BIAS_F32) {
+        float* o = reinterpret_cast<float*>(p.epi.out) + (size_t)c0 * ldo + n;
+        const float bias = p.epi.bias[n];
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (q < nq) o[q * ldo] = v[q] + bias;
+      } else {  // SwiGLU (see staged_store)
+        const int f = vt_ * 64 + (m >> 1);
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.epi.out) + (size_t)c0 * ldo + f;
+#pragma unroll
+        for (int q0 = 0; q0 < 32; q0 += 8) {
+          if (q0 >= nq) break;  // (warp-uniform)
+          float uu[8], e[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) uu[j] = __shfl_down_sync(0xffffffffu, v[q0 + j], 1);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) e[j] = __expf(-v[q0 + j]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) e[j] = __fdividef(v[q0 + j], 1.f + e[j]) * uu[j];
+          if (!(lane & 1)) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (q0 + j < nq) o[(q0 + j) * ldo] = __float2bfloat16_rn(e[j]);
+          }
+        }
+      }
+    };
+    // bulk-copy n_src [rows P0..P1) x 128 fp32 partial slots into the idle ring (one TMA request each)
+    auto bulk_rows = [&](const float* const* srcs, int n_src, int P0, int P1) {
+      if (lead) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        mbar_arrive_expect_tx(fixb, (uint32_t)(n_src * (P1 - P0) * BM * 4));
+        for (int o = 0; o < n_src; ++o)
+          bulk_load(smem + (size_t)o * (P1 - P0) * BM * 4, srcs[o] + (size_t)P0 * BM, (uint32_t)((P1 - P0) * BM * 4),
+                    fixb, kEvictFirst);
+      }
+      mbar_wait(fixb, fix_ph);
+      fix_ph ^= 1u;
+    };
+
+    // Epilogue of segment [u, se) of tile t from TMEM buffer b by ng groups (this thread: group
+    // gid, barrier over nthr threads). final: every MMA of the CTA has completed (ring idle).
+    auto segment_epilogue = [&](long long u, int t, long long se, int b, int gid, int ng, int nthr, bool final,
+                                int& defer_vt) {
       const long long ts = (long long)t * kb, te = ts + kb;
-      const long long se = min(u1, te);
-      const int b = seg % p.nbuf;
-      mbar_wait_sleep(&accf[b], (uint32_t)(seg / p.nbuf) & 1u);
-      if (etid == 0 && seg < 4) SF_TR(8 + 4 * seg + 2);
-#ifdef SF_GEMM_PROFILE
-      const long long te0 = clock64();
-#endif
-      tc_fence_after();
       const uint32_t t_row = tmem + (uint32_t)(b * cols) + ((uint32_t)(quad * 32) << 16);
       const int vt = t * CG + (int)rank;  // 128-row tile index of this CTA's rows
-      const int n = vt * BM + m;
       const bool is_full = (u == ts) && (se == te);
       const bool is_head = (u == ts) && !is_full;
-      if (mode == EPI_PARTIAL) {
-        // every segment -> slot 2 * group + (first segment of the range ? 0 : 1) (one 128-row half
-        // per CTA of a pair); reduced later, in k order, by the consumer
-        float* dst = p.partial + ((size_t)(2 * c + (u == u0 ? 0 : 1)) * CG + (int)rank) * p.T * BM + m;
-        for (int c0 = half * 32; c0 < p.T; c0 += 64) {
+      const int cstep = 32 * ng;
+      if (mode == EPI_PARTIAL || (!is_full && !is_head) || (is_full && !final && can_stage && p.T >= 64)) {
+        // fp32 accumulator -> [T][128] slot (each warp store is one 128-byte line):
+        //  EPI_PARTIAL: slot 2 group + (first segment of the range ? 0 : 1), reduced in k order by
+        //    the consumer; tail of a tile owned by another group: this CTA's slot, then its flag;
+        //  full tile in mid-range: parked, finished in the final phase instead of stalling the MMA
+        const bool tail = mode != EPI_PARTIAL && !is_full && !is_head;
+        float* dst = mode == EPI_PARTIAL
+                         ? p.partial + ((size_t)(2 * c + (u == u0 ? 0 : 1)) * CG + (int)rank) * p.T * BM
+                         : (tail ? slot_base : defer_base);
+        for (int c0 = gid * 32; c0 < p.T; c0 += cstep) {
           uint32_t r[32];
           tmem_ld32_async(t_row + (uint32_t)c0, r);
           tmem_ld_wait();
 #pragma unroll
           for (int cc = 0; cc < 32; ++cc)
-            if (c0 + cc < p.T) dst[(size_t)(c0 + cc) * BM] = __uint_as_float(r[cc]);
+            if (c0 + cc < p.T) dst[(size_t)(c0 + cc) * BM + m] = __uint_as_float(r[cc]);
         }
-      } else if (!is_full && !is_head) {
-        // publish this segment's fp32 partial (slot = this CTA; at most one per CTA): [T][128],
-        // each warp store one coalesced 128-byte line
-        float* dst = p.partial + (size_t)slot * p.Tp * BM + m;
-        for (int c0 = half * 32; c0 < p.T; c0 += 64) {
-          uint32_t r[32];
-          tmem_ld32_async(t_row + (uint32_t)c0, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int cc = 0; cc < 32; ++cc)
-            if (c0 + cc < p.T) dst[(size_t)(c0 + cc) * BM] = __uint_as_float(r[cc]);
+        if (tail) {
+          __threadfence();
+          named_sync(final ? 5 : 1, nthr);
+          if (lead) st_release(&p.flags[slot], 1);
         }
-        __threadfence();
-        named_sync(1, 256);
-        if (etid == 0) st_release(&p.flags[slot], 1);
-      } else {
-        // groups owning the other k segments of this tile (they publish them first thing)
-        int c_lo = c + 1, c_hi = c;
-        if (is_head) {
-          const long long ul = te - 1;
-          c_hi = (int)(((ul + 1) * p.G + U - 1) / U) - 1;
-          if (etid == 0)
-            for (int cc = c_lo; cc <= c_hi; ++cc)
-              while (ld_acquire(&p.flags[cc * CG + (int)rank]) == 0) {
-              }
-          named_sync(1, 256);
-          if (etid == 0 && se == u1) SF_TR(104);
-        }
-        // A head that is this CTA's last segment finds the smem ring idle (every MMA has completed):
-        // the other segments' partials are then bulk-copied into it (TMA engine, full lines) instead
-        // of being gathered with per-thread loads that compete with the other CTAs' weight streams.
-        const int n_o = c_hi - c_lo + 1;
-        int Tc = p.T;
-        bool bulk = p.bulk_ok && is_head && se == u1 && n_o > 0;
-        if (bulk) {
-          Tc = ((p.stages * stage_bytes) / (n_o * BM * 4)) / 64 * 64;
-          bulk = Tc >= 64;
-        }
-        // output staging (ring idle): 2 x 16 KB at the end of the ring, one per epilogue half
-        constexpr int kStageBytes = 16384;
-        const int ring_bytes = p.stages * stage_bytes;
-        const int out_elt = mode == EPI_STORE_F32 ? 4 : 2;
-        const bool stage_out = se == u1 &&
-                               ((mode == EPI_STORE_ACT && (p.stage_ok & 1)) || (mode == EPI_STORE_F32 && (p.stage_ok & 2)) ||
-                                (mode == EPI_SWIGLU_ACT && (p.stage_ok & 4))) &&
-                               ((size_t)p.epi.ldo * out_elt) % 16 == 0 && ring_bytes >= 2 * kStageBytes + 64 * BM * 4 * n_o;
-        uint8_t* stg = smem + ring_bytes - 2 * kStageBytes;
-        if (stage_out && bulk) Tc = ((ring_bytes - 2 * kStageBytes) / (n_o * BM * 4)) / 64 * 64;
-        const float* smf = reinterpret_cast<const float*>(smem);
-        for (int P0 = 0; P0 < p.T; P0 += (bulk ? Tc : p.T)) {
-        const int P1 = bulk ? min(p.T, P0 + Tc) : p.T;
-        if (bulk) {
-          if (etid == 0) {
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            mbar_arrive_expect_tx(fixb, (uint32_t)(n_o * (P1 - P0) * BM * 4));
-            for (int o = 0; o < n_o; ++o)
-              bulk_load(smem + (size_t)o * (P1 - P0) * BM * 4,
-                        p.partial + (size_t)((c_lo + o) * CG + (int)rank) * p.Tp * BM + (size_t)P0 * BM,
-                        (uint32_t)((P1 - P0) * BM * 4), fixb, kEvictFirst);
-          }
-          mbar_wait(fixb, fix_ph);
-          fix_ph ^= 1u;
-          if (etid == 0 && P0 == 0) SF_TR(105);
-        }
-        for (int c0 = P0 + half * 32; c0 < P1; c0 += 64) {
+        if (mode != EPI_PARTIAL && is_full) defer_vt = vt;
+        return;
+      }
+      // head or full tile: add the other groups' k segments of this tile (they publish them first
+      // thing), in k order, then the output epilogue
+      int c_lo = c + 1, c_hi = c;
+      if (is_head) {
+        const long long ul = te - 1;
+        c_hi = (int)(((ul + 1) * p.G + U - 1) / U) - 1;
+        if (lead)
+          for (int cc = c_lo; cc <= c_hi; ++cc)
+            while (ld_acquire(&p.flags[cc * CG + (int)rank]) == 0) {
+            }
+        named_sync(final ? 5 : 1, nthr);
+      }
+      if (lead && final) SF_TR(104);
+      const int n_o = c_hi - c_lo + 1;
+      // (small T: a few rows -- direct loads / stores beat the TMA round trip and the staging barriers)
+      const bool stage_out = final && can_stage && p.T >= 64;
+      const bool bulk = final && p.bulk_ok && p.T >= 64 && n_o > 0 && n_o <= 8 && fix_bytes >= 64 * BM * 4 * n_o;
+      const int Tc = bulk ? (fix_bytes / (n_o * BM * 4)) / 64 * 64 : p.T;
+      const float* srcs[8];
+      for (int o = 0; o < n_o && o < 8; ++o) srcs[o] = p.partial + (size_t)((c_lo + o) * CG + (int)rank) * p.Tp * BM;
+      for (int P0 = 0; P0 < p.T; P0 += Tc) {
+        const int P1 = min(p.T, P0 + Tc);
+        if (bulk) bulk_rows(srcs, n_o, P0, P1);
+        if (lead && final && P0 == 0) SF_TR(105);
+        for (int c0 = P0 + gid * 32; c0 < P1; c0 += cstep) {
           uint32_t r[32];
           tmem_ld32_async(t_row + (uint32_t)c0, r);
           tmem_ld_wait();
@@ -436,161 +543,112 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
               for (int q = 0; q < 32; ++q)
                 if (c0 + q < p.T) v[q] += sp[q * BM];
             }
-          } else
-          for (int cc = c_lo; cc <= c_hi; cc += 2) {  // fixed k order; two segments' loads in flight
-            const float* s0 = p.partial + (size_t)(cc * CG + (int)rank) * p.Tp * BM + m;
-            const bool two = cc + 1 <= c_hi;
-            const float* s1 = s0 + (two ? (size_t)CG * p.Tp * BM : 0);
-            float a0[32], a1[32];
-#pragma unroll
-            for (int q = 0; q < 32; ++q) a0[q] = (c0 + q < p.T) ? __ldcg(&s0[(size_t)(c0 + q) * BM]) : 0.f;
-            if (two) {
-#pragma unroll
-              for (int q = 0; q < 32; ++q) a1[q] = (c0 + q < p.T) ? __ldcg(&s1[(size_t)(c0 + q) * BM]) : 0.f;
-            }
-#pragma unroll
-            for (int q = 0; q < 32; ++q) v[q] += a0[q];
-            if (two) {
-#pragma unroll
-              for (int q = 0; q < 32; ++q) v[q] += a1[q];
-            }
-          }
-          if (etid == 0 && bulk && c0 < 128) SF_TR(107 + (c0 >> 6));  // chunk's TMEM + adds done
-          const int nq = min(32, p.T - c0);
-          const size_t ldo = (size_t)p.epi.ldo;
-          if (stage_out) {
-            // stage the chunk [32 tokens][tile columns] in smem, then write whole rows with
-            // 16-byte vectors (per-thread column stores are 32-byte sectors 10-100 KB apart)
-            uint8_t* sb = stg + (size_t)half * kStageBytes;
-            const int rowb = mode == EPI_SWIGLU_ACT ? 128 : (mode == EPI_STORE_ACT ? 256 : 512);
-            if (mode == EPI_STORE_ACT) {
-#pragma unroll
-              for (int q = 0; q < 32; ++q)
-                reinterpret_cast<__nv_bfloat16*>(sb + q * 256)[m] = __float2bfloat16_rn(v[q]);
-            } else if (mode == EPI_STORE_F32) {
-#pragma unroll
-              for (int q = 0; q < 32; ++q) reinterpret_cast<float*>(sb + q * 512)[m] = v[q];
-            } else {
-              // even lane 2i holds gate_i, odd lane up_i (interleaved rows): the even lane forms all
-              // 32 tokens of feature i
-              if (etid == 0 && c0 < 64) SF_TR(111);
-              __nv_bfloat16* srow = reinterpret_cast<__nv_bfloat16*>(sb) + quad * 16 + (lane >> 1);
-              // batches of 8 independent shuffle / exp / divide chains (the per-element chain is
-              // ~100 cycles of latency; one element at a time the warp would mostly wait)
-#pragma unroll
-              for (int q0 = 0; q0 < 32; q0 += 8) {
-                float u[8], e[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) u[j] = __shfl_down_sync(0xffffffffu, v[q0 + j], 1);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) e[j] = __expf(-v[q0 + j]);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) e[j] = __fdividef(v[q0 + j], 1.f + e[j]) * u[j];
-                if (!(lane & 1)) {
-#pragma unroll
-                  for (int j = 0; j < 8; ++j) srow[(q0 + j) * 64] = __float2bfloat16_rn(e[j]);
-                }
-              }
-            }
-            if (etid == 0 && c0 < 64) SF_TR(112);
-            named_sync(2 + half, 128);
-            if (etid == 0 && c0 < 64) SF_TR(113);
-            const int elt = mode == EPI_STORE_F32 ? 4 : 2;
-            const int col0 = mode == EPI_SWIGLU_ACT ? vt * 64 : vt * BM;
-            uint8_t* gbase = reinterpret_cast<uint8_t*>(p.epi.out) + ((size_t)c0 * ldo + col0) * elt;
-            const int vpr = rowb / 16, ht = etid & 127;
-            for (int i = ht; i < nq * vpr; i += 128) {
-              const int q = i / vpr, x = i % vpr;
-#ifdef SF_GEMM_CHECK
-              if ((((uintptr_t)(gbase + (size_t)q * ldo * elt + x * 16)) & 15) || (((uintptr_t)(sb + q * rowb + x * 16)) & 15)) {
-                printf("misaligned: mode %d out %p ldo %d c0 %d col0 %d q %d x %d sb %p T %d N %d K %d\n", mode, p.epi.out,
-                       (int)ldo, c0, col0, q, x, sb, p.T, p.N, p.K);
-                __trap();
-              }
-#endif
-              *reinterpret_cast<uint4*>(gbase + (size_t)q * ldo * elt + x * 16) =
-                  *reinterpret_cast<const uint4*>(sb + q * rowb + x * 16);
-            }
-            named_sync(2 + half, 128);
-          } else if (mode == EPI_STORE_ACT) {
-            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.epi.out) + (size_t)c0 * ldo + n;
-#pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (q < nq) o[q * ldo] = __float2bfloat16_rn(v[q]);
-          } else if (mode == EPI_STORE_F32) {
-            float* o = reinterpret_cast<float*>(p.epi.out) + (size_t)c0 * ldo + n;
-#pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (q < nq) o[q * ldo] = v[q];
-          } else if (mode == EPI_ADD_F32) {
-            float* o = reinterpret_cast<float*>(p.epi.out) + (size_t)c0 * ldo + n;
-            float old[32];
-#pragma unroll
-            for (int q = 0; q < 32; ++q) old[q] = (q < nq) ? o[q * ldo] : 0.f;
-#pragma unroll
-            for (int q = 0; q < 32; ++q) v[q] = old[q] + v[q];
-#pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (q < nq) o[q * ldo] = v[q];
-            if (p.epi.tap) {
-              float* tp = p.epi.tap + (size_t)c0 * ldo + n;
-#pragma unroll
-              for (int q = 0; q < 32; ++q)
-                if (q < nq) tp[q * ldo] = v[q];
-            }
-          } else if (mode == EPI_BIAS_F32) {
-            float* o = reinterpret_cast<float*>(p.epi.out) + (size_t)c0 * ldo + n;
-            const float bias = p.epi.bias[n];
-#pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (q < nq) o[q * ldo] = v[q] + bias;
           } else {
-            // SwiGLU: rows 2i / 2i+1 of the interleaved weight are gate_i / up_i -> adjacent lanes.
-            // Even lanes emit even columns, odd lanes odd columns.
-            const int f = vt * 64 + (m >> 1);
-            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.epi.out) + (size_t)c0 * ldo + f;
+            for (int cc = c_lo; cc <= c_hi; cc += 2) {  // fixed k order; two segments' loads in flight
+              const float* s0 = p.partial + (size_t)(cc * CG + (int)rank) * p.Tp * BM + m;
+              const bool two = cc + 1 <= c_hi;
+              const float* s1 = s0 + (two ? (size_t)CG * p.Tp * BM : 0);
+              float a0[32], a1[32];
 #pragma unroll
-            for (int q0 = 0; q0 < 32; q0 += 8) {
-              float u[8], e[8];
+              for (int q = 0; q < 32; ++q) a0[q] = (c0 + q < p.T) ? __ldcg(&s0[(size_t)(c0 + q) * BM]) : 0.f;
+              if (two) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) u[j] = __shfl_down_sync(0xffffffffu, v[q0 + j], 1);
+                for (int q = 0; q < 32; ++q) a1[q] = (c0 + q < p.T) ? __ldcg(&s1[(size_t)(c0 + q) * BM]) : 0.f;
+              }
 #pragma unroll
-              for (int j = 0; j < 8; ++j) e[j] = __expf(-v[q0 + j]);
+              for (int q = 0; q < 32; ++q) v[q] += a0[q];
+              if (two) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) e[j] = __fdividef(v[q0 + j], 1.f + e[j]) * u[j];
-              if (!(lane & 1)) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                  if (q0 + j < nq) o[(q0 + j) * ldo] = __float2bfloat16_rn(e[j]);
+                for (int q = 0; q < 32; ++q) v[q] += a1[q];
               }
             }
           }
-          if (etid == 0 && bulk && c0 < 128) SF_TR(109 + (c0 >> 6));  // chunk's stores issued
+          const int nq = min(32, p.T - c0);
+          if (lead && final && c0 < 4 * cstep) SF_TR(106 + 2 * (c0 / cstep));  // TMEM + adds done
+          if constexpr (kStageable) {
+            if (stage_out) staged_store(v, c0, nq, vt, gid);
+            else direct_store(v, c0, nq, vt);
+          } else {
+            direct_store(v, c0, nq, vt);
+          }
+          if (lead && final && c0 < 4 * cstep) SF_TR(107 + 2 * (c0 / cstep));  // stored
         }
-        if (bulk) named_sync(1, 256);  // smem pass consumed before the next one overwrites it
-        if (etid == 0 && P0 == 0) SF_TR(106);
-        }  // passes
-        if (is_head) {
-          named_sync(1, 256);
-          if (etid == 0)
-            for (int cc = c_lo; cc <= c_hi; ++cc) p.flags[cc * CG + (int)rank] = 0;  // re-arm for the next launch
-        }
+        if (bulk) named_sync(final ? 5 : 1, nthr);  // smem pass consumed before the next one overwrites it
       }
-#ifdef SF_GEMM_PROFILE
-      if (etid == 0 && (c == 0 || c == p.G / 2))
-        printf("T=%d grp %d seg %d: epilogue %lld cycles (%s)\n", p.T, c, seg, clock64() - te0,
-               is_full ? "full" : (is_head ? "head" : "publish"));
-#endif
-      tc_fence_before();
-      named_sync(1, 256);
-      if (etid == 0 && seg < 4) SF_TR(8 + 4 * seg + 3);
-      if (etid == 0 && se == u1) SF_TR(5);
-      if (etid == 0) {
-        if (CG == 1 || rank == 0) mbar_arrive(&acce[b]);
-        else mbar_arrive_remote(&acce[b], 0);
+      if (is_head) {
+        named_sync(final ? 5 : 1, nthr);
+        if (lead)
+          for (int cc = c_lo; cc <= c_hi; ++cc) p.flags[cc * CG + (int)rank] = 0;  // re-arm for the next launch
+      }
+    };
+
+    // segments of [u0, u1): all but the last by the 8 epilogue warps while the MMA streams on; the
+    // last one (and a parked full tile) by all 12 warps -- one inlined copy of the epilogue
+    int nseg_total = 0;
+    for (long long uu = u0; uu < u1; uu = min(u1, (uu / kb + 1) * kb)) ++nseg_total;
+    int defer_vt = -1;
+    long long u = u0;
+    int gid = 0;
+    for (int seg = 0; seg < nseg_total; ++seg) {
+      const int t = (int)(u / kb);
+      const long long se = min(u1, (long long)(t + 1) * kb);
+      // the 12-warp final phase pays off for large T only (small T: a few rows per chunk, the
+      // extra barriers would dominate)
+      const bool final = seg == nseg_total - 1 && p.T >= 64;
+      if (warp >= 4 || final) {
+        const int b = seg % p.nbuf;
+        int ng = 2, nthr = 256;
+        gid = warp >= 4 ? (warp - 4) >> 2 : 0;
+        if (final) {
+          if (warp < 4) pdl_wait();  // (already resolved: the producer waited before its first load)
+          int* s_defer = reinterpret_cast<int*>(tmem_slot + 1);  // share the parked tile index
+          if (lead) *s_defer = defer_vt;
+          named_sync(5, 384);
+          defer_vt = *s_defer;
+          ng = 3;
+          nthr = 384;
+          gid = warp < 4 ? 2 : gid;
+        }
+        mbar_wait_sleep(&accf[b], (uint32_t)(seg / p.nbuf) & 1u);
+        if (lead && seg < 4) SF_TR(8 + 4 * seg + 2);
+        tc_fence_after();
+        segment_epilogue(u, t, se, b, gid, ng, nthr, final, defer_vt);
+        if (!final) {
+          tc_fence_before();
+          named_sync(1, 256);
+          if (lead && seg < nseg_total - 1) {  // (the MMA never waits for the last buffer)
+            if (CG == 1 || rank == 0) mbar_arrive(&acce[b]);
+            else mbar_arrive_remote(&acce[b], 0);
+          }
+        } else {
+          named_sync(5, 384);
+          if (lead) SF_TR(5);
+        }
+        if (lead && seg < 4) SF_TR(8 + 4 * seg + 3);
       }
       u = se;
-      ++seg;
+    }
+    if constexpr (kStageable) {
+      if (defer_vt >= 0) {
+        // the parked full tile, through the idle ring
+        __threadfence();
+        named_sync(5, 384);
+        const int Tc = (fix_bytes / (BM * 4)) / 64 * 64;
+        const float* src = defer_base;
+        for (int P0 = 0; P0 < p.T; P0 += Tc) {
+          const int P1 = min(p.T, P0 + Tc);
+          bulk_rows(&src, 1, P0, P1);
+          for (int c0 = P0 + gid * 32; c0 < P1; c0 += 96) {
+            float v[32];
+            const float* sp = smf + (size_t)(c0 - P0) * BM + m;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) v[q] = (c0 + q < p.T) ? sp[q * BM] : 0.f;
+            staged_store(v, c0, min(32, p.T - c0), defer_vt, gid);
+          }
+          named_sync(5, 384);
+        }
+        if (lead) SF_TR(6);
+      }
     }
   }
   tc_fence_before();
@@ -790,12 +848,29 @@ static int gemm_cg(int N, int K) {
   return 1;
 }
 
+using SkKernel = void (*)(const CUtensorMap, const CUtensorMap, const SkParams);
+static SkKernel sk_kernel_for(int cg, int mode) {
+#define SF_SK(CGV)                                              \
+  switch (mode) {                                               \
+    case EPI_STORE_ACT: return gemm_sk_kernel<CGV, EPI_STORE_ACT>;   \
+    case EPI_STORE_F32: return gemm_sk_kernel<CGV, EPI_STORE_F32>;   \
+    case EPI_ADD_F32: return gemm_sk_kernel<CGV, EPI_ADD_F32>;       \
+    case EPI_BIAS_F32: return gemm_sk_kernel<CGV, EPI_BIAS_F32>;     \
+    case EPI_SWIGLU_ACT: return gemm_sk_kernel<CGV, EPI_SWIGLU_ACT>; \
+    default: return gemm_sk_kernel<CGV, EPI_PARTIAL>;           \
+  }
+  if (cg == 2) SF_SK(2);
+  SF_SK(1);
+#undef SF_SK
+}
+
 static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled, int T, int N, int K,
                              const GemmEpi& epi, const GemmScratch& scratch, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_sk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(gemm_sk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    for (int cg = 1; cg <= 2; ++cg)
+      for (int md = 0; md <= EPI_PARTIAL; ++md)
+        cudaFuncSetAttribute(sk_kernel_for(cg, md), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   const int CG = (w_tiled && T >= 1) ? gemm_cg(N, K) : 1;
@@ -853,7 +928,7 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   }
   if (!make_map(&ma, A, T, K, lda, p.NT / CG)) return cudaErrorInvalidValue;
   if (CG == 1) {
-    launch_k(gemm_sk_kernel<1>, dim3(p.G), dim3(384), smem, st, mw, ma, p);
+    launch_k(sk_kernel_for(1, epi.mode), dim3(p.G), dim3(384), smem, st, mw, ma, p);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg{};
@@ -870,7 +945,7 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   attrs[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, gemm_sk_kernel<2>, mw, ma, p);
+  return cudaLaunchKernelEx(&cfg, sk_kernel_for(2, epi.mode), mw, ma, p);
 }
 
 bool gemm_partial_geom(int T, int N, int K, PartialGeom* g) {

@@ -20,9 +20,11 @@ struct AttnParams {
   void* out;                 // [T, Hq*hd] act dtype
   int max_key;               // upper bound of pos0[b] + q_len (grid sizing), <= max_seq
   int n_pages;               // pages in the pool (TMA tensor-map extent)
+  int* seg_cnt;              // [B * Hkv * query tiles] zeroed arrival counters (bf16 hd=128 kernel)
 };
 
 constexpr int kAttnChunk = 128;  // fixed absolute key-chunk size (split-KV boundaries, C23)
+constexpr int kAttnSeg = 1024;   // flash-decoding key segment: one work item (fixed absolute bounds)
 
 // act dtype: bf16 (is_bf16) or fp32.
 cudaError_t launch_rope_table(float2* table, int max_seq, int hd, float theta, cudaStream_t s);

@@ -111,7 +111,8 @@ struct Plan {
   int64_t act, kv_layer_bytes;
   // offsets
   int64_t o_k, o_v, o_bt, o_rope, o_resid, o_xn, o_qkv, o_qrot, o_attn, o_ffn, o_taps, o_ctx, o_idrow, o_D,
-      o_hlast, o_logits, o_dlogits, o_apo, o_apml, o_gpart, o_gcnt, o_amv, o_ami, o_ints, o_prompt;
+      o_hlast, o_logits, o_dlogits, o_apo, o_apml, o_gpart, o_gcnt, o_amv, o_ami, o_ints, o_prompt, o_acnt;
+  int64_t n_acnt;
   int64_t gpart_elems, n_amrows;
   int64_t total;
 };
@@ -171,6 +172,9 @@ Plan make_plan(const sf_config* c) {
   p.o_dlogits = take((int64_t)p.rows_d * p.V * 4);
   p.o_apo = take((int64_t)p.R * p.Hq * p.nchunk * p.hd * 4);
   p.o_apml = take((int64_t)p.R * p.Hq * p.nchunk * 2 * 4);
+  // split-KV arrival counters: one per (sequence, kv head, 16-row query tile) at the longest block
+  p.n_acnt = (int64_t)p.B * p.Hkv * ((std::max(p.k + 1, p.C_pf) * (p.Hq / p.Hkv) + 15) / 16);
+  p.o_acnt = take(p.n_acnt * 4);
   p.o_gpart = take(p.gpart_elems * 4);
   p.o_gcnt = take(4096 * 4);
   p.o_amv = take(p.n_amrows * argmax_splits(p.V) * 4);
@@ -210,7 +214,7 @@ struct sf_handle {
   float2* rope = nullptr;
   float *resid, *qrot, *taps, *ctx, *idrow, *D, *hlast, *logits, *dlogits, *apo, *apml, *gpart, *amv;
   void *xn, *qkv, *attn, *ffn;
-  int *gcnt, *ami;
+  int *gcnt, *ami, *acnt;
   int *tok_rows, *pos0_pf, *seq_len, *n_prev, *last_token, *r_b, *prompt_len, *draft, *greedy, *accept_len,
       *emitted, *err, *step_counter, *g_pf, *prompt;
   // state
@@ -391,6 +395,7 @@ static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const i
   ap.nchunk_max = p.nchunk;
   ap.part_o = h->apo;
   ap.part_ml = h->apml;
+  ap.seg_cnt = h->acnt;
   ap.out = h->attn;
   ap.max_key = std::min(max_key, h->c.max_seq);
   ap.n_pages = p.n_pages;
@@ -698,6 +703,7 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
   h->dlogits = (float*)(w + p.o_dlogits);
   h->apo = (float*)(w + p.o_apo);
   h->apml = (float*)(w + p.o_apml);
+  h->acnt = (int*)(w + p.o_acnt);
   h->gpart = (float*)(w + p.o_gpart);
   h->gcnt = (int*)(w + p.o_gcnt);
   h->amv = (float*)(w + p.o_amv);
@@ -729,6 +735,7 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
   for (int i = 0; i < p.n_pages; ++i) bt[i] = i;
   e = cudaMemcpyAsync(h->bt, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice, h->st);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->gcnt, 0, 4096 * 4, h->st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->acnt, 0, (size_t)p.n_acnt * 4, h->st);
   // whole 16-key pages are staged by TMA: never-written slots must hold finite values (masked keys
   // get probability exactly 0, and 0 * finite = 0)
   if (e == cudaSuccess) e = cudaMemsetAsync(h->kpool, 0, (size_t)p.kv_layer_bytes * (p.L + 1), h->st);

@@ -34,7 +34,13 @@ u = R[:, 24:64]; d = np.diff(u, axis=1)
 print("  per-unit full-barrier interval (us): med %.3f  p90 %.3f" % (np.nanmedian(d), np.nanpercentile(d, 90)))
 print("  unit pass times CTA0:", " ".join(f"{x:.2f}" for x in u[0, :20]))
 print("  producer issue CTA0: ", " ".join(f"{x:.2f}" for x in R[0, 64:84]))
-print("  last-seg head: flags-acquired / bulk-landed / pass0-done (med, max):",
-      " ".join(f"{np.nanmedian(R[:, c]):.2f}/{np.nanmax(R[:, c]):.2f}" for c in (104, 105, 106)))
-print("  head chunk0 adds/stores, chunk1 adds/stores (med):", " ".join(f"{np.nanmedian(R[:, c]):.2f}" for c in (107, 109, 108, 110)))
-print("  swiglu chunk0: pre-math / staged / barrier (med):", " ".join(f"{np.nanmedian(R[:, c]):.2f}" for c in (111, 112, 113)))
+print("  final phase (med): flags %.2f bulk %.2f chunks(tmem+add/stored): %s" % (np.nanmedian(R[:, 104]), np.nanmedian(R[:, 105]),
+      " ".join(f"{np.nanmedian(R[:, c]):.2f}/{np.nanmedian(R[:, c + 1]):.2f}" for c in (106, 108, 110, 112))))
+order = np.argsort(-np.nan_to_num(R[:, 4]))
+print("  slowest CTAs (mma_last): cta: seg(mma_start, issued, epi_ready, epi_done)...")
+for i in list(order[:6]) + list(order[len(order) // 2: len(order) // 2 + 2]):
+    segs = []
+    for sg in range(4):
+        v = R[i, 8 + 4 * sg: 12 + 4 * sg]
+        if not np.all(np.isnan(v)): segs.append("(" + ",".join(f"{x:.1f}" for x in v) + ")")
+    print(f"    cta {i:3d} full0 {R[i,3]:.1f} mma_last {R[i,4]:.1f} epi_done {R[i,5]:.1f}: " + " ".join(segs))

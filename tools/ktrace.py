@@ -11,7 +11,7 @@ from synth import get_config, make_prompts, make_weights
 
 KIND = {1: "gemm", 2: "resid_norm", 3: "rope", 4: "attn", 5: "rmsnorm", 6: "group_rms", 7: "embed", 8: "argmax_p",
         9: "argmax_f", 10: "accept", 11: "bidir", 12: "gather", 13: "rows", 14: "gemm_simt", 15: "attn_part",
-        16: "attn_comb", 17: "misc"}
+        16: "attn_comb", 17: "misc", 18: "item"}
 REC = np.dtype([("kid", "<u4"), ("sm", "<u4"), ("t0", "<u8"), ("tw", "<u8"), ("t1", "<u8"), ("pad", "<u8")])
 
 
@@ -53,7 +53,18 @@ def main():
     e0.record(eng.stream); eng.decode_steps(steps); e1.record(eng.stream); eng.sync()
     ms = e0.elapsed_time(e1)
     n = lib.sf_debug_ktrace(buf.ctypes.data_as(C.c_void_p), buf.size)
-    Ls = launches(buf[:n])
+    items = buf[:n][(buf[:n]["kid"] >> 24) == 18]
+    rest = buf[:n][(buf[:n]["kid"] >> 24) != 18]
+    if len(items):
+        par = items["kid"] & 0xFFFFFF
+        seg, nseg, nch = par & 0xFF, (par >> 8) & 0xFF, par >> 16
+        dt_c = (items["tw"] - items["t0"]) / 1e3; dt_m = (items["t1"] - items["tw"]) / 1e3
+        for sg in sorted(set(seg.tolist())):
+            msk = seg == sg
+            print(f"  attention items seg {sg}: n={msk.sum()} chunks med {np.median(nch[msk]):.0f} "
+                  f"chunk-loop med {np.median(dt_c[msk]):.2f} us (per chunk {np.median(dt_c[msk] / nch[msk]):.2f}) "
+                  f"merge/publish med {np.median(dt_m[msk]):.2f} p90 {np.percentile(dt_m[msk], 90):.2f} us")
+    Ls = launches(rest)
     t_first = Ls[0]["tw"]
     span = (max(L["t1"] for L in Ls) - t_first) / 1e3
     exposed = collections.defaultdict(float); dur = collections.defaultdict(float); cnt = collections.Counter()
