@@ -56,6 +56,23 @@ SF_DEV float block_sum(float v, float* red /* >= NT/32 floats */) {
   return red[0];
 }
 
+// Block-wide sum for a runtime blockDim (multiple of 32, <= 1024) with a fixed tree: warp shuffles,
+// then warp 0 over the per-warp sums in warp order (depends on blockDim only -> batch-invariant).
+SF_DEV float block_sum_dyn(float v, float* red /* >= 32 floats */) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    float s = (l < (int)(blockDim.x >> 5)) ? red[l] : 0.f;
+    s = warp_sum(s);
+    if (l == 0) red[0] = s;
+  }
+  __syncthreads();
+  return red[0];
+}
+
 // ---------------------------------------------------------------- programmatic dependent launch
 // Every kernel of the step is launched with programmatic stream serialisation: it may start while
 // its predecessor drains, does only dependency-free work (barrier init, TMEM alloc, smem clears,

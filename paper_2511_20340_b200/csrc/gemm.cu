@@ -59,7 +59,7 @@ SF_DEV float silu_f(float g) { return g / (1.f + expf(-g)); }
 struct SkParams {
   int T, N, K;
   int Tp;  // T rounded up to 32 (row stride of the fixup partial slots)
-  int NT, n_sub, stages, kb_total, n_tiles, G, nbuf, w_tiled, w_tma, stage_ok, bulk_ok;
+  int NT, n_sub, stages, kb_total, n_tiles, G, nbuf, w_tiled, w_tma, stage_ok, bulk_ok, npre;
   int cgrp;  // ring slots released per tcgen05.commit
   uint32_t tmem_cols;
   const __nv_bfloat16* w_tiles;  // tile-contiguous weights (w_tiled, CG == 1 bulk path)
@@ -195,7 +195,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     // ---- TMA producer warp (converged; one elected lane issues)
     // The weights do not depend on the previous kernel: the first ring's worth of weight tiles is
     // requested before the grid dependency resolves (PDL), the activation tiles after it.
-    const long long npre = p.w_tiled ? min((long long)p.stages, u1 - u0) : 0;
+    const long long npre = p.w_tiled ? min((long long)p.npre, u1 - u0) : 0;
     if (npre > 0 && elect_one()) {
       int tp = (int)(u0 / kb), kp = (int)(u0 % kb);
       for (int i = 0; i < (int)npre; ++i) {
@@ -508,9 +508,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       // head or full tile: add the other groups' k segments of this tile (they publish them first
       // thing), in k order, then the output epilogue
       int c_lo = c + 1, c_hi = c;
+      if (is_head) c_hi = (int)((te * p.G + U - 1) / U) - 1;
       if (is_head) {
-        const long long ul = te - 1;
-        c_hi = (int)(((ul + 1) * p.G + U - 1) / U) - 1;
         if (lead)
           for (int cc = c_lo; cc <= c_hi; ++cc)
             while (ld_acquire(&p.flags[cc * CG + (int)rank]) == 0) {
@@ -910,6 +909,10 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   // bit0 bulk fixup loads; bits 1..3 smem-staged stores for ACT / F32 / SwiGLU outputs
   static const int env_epi = getenv("SF_GEMM_EPI") ? atoi(getenv("SF_GEMM_EPI")) : 15;
   p.bulk_ok = env_epi & 1;
+  // weight stages requested before the grid dependency resolves: a few, not the whole ring -- the
+  // first activation tile is served behind them, and it gates the first MMA
+  static const int env_npre = getenv("SF_GEMM_NPRE") ? atoi(getenv("SF_GEMM_NPRE")) : 4;
+  p.npre = std::max(1, std::min(env_npre, p.stages));
   p.stage_ok = (env_epi >> 1) & 7;
   static const int trace_n = getenv("SF_GEMM_TRACE_N") ? atoi(getenv("SF_GEMM_TRACE_N")) : 0;
   if (trace_n && trace_n != N) p.trace = nullptr;  // trace one weight shape only

@@ -2,6 +2,7 @@
 // accept kernels of the SpecFormer decode step. Every reduction uses a fixed order that depends
 // only on the row's own data and position (batch invariance, reading C23), so GPU SD == GPU AR
 // bit for bit.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 
@@ -107,6 +108,79 @@ __global__ void __launch_bounds__(256) group_rms_kernel(const float* taps, int64
     const float r = 1.0f / sqrtf(ss / (float)d + eps);
     TO* y = out + (size_t)t * 4 * d + (size_t)g * d;
     for (int i = threadIdx.x; i < d; i += 256) y[i] = Elt<TO>::from_f(x[i] * r * sc[g * d + i]);
+  }
+}
+
+// ------------------------------------------------------------------------ vectorised row kernels
+// bf16 path, d % 128 == 0: one CTA of d / (4 NG) threads per row, thread t owns the float4 groups
+// 4t + 4 nthr j (j < NG): every load / store is 16 bytes and even a 5-row step spreads over
+// thousands of threads.
+static int row_ng(int d) {
+  for (int ng = 1; ng <= 4; ++ng)
+    if (d % (128 * ng) == 0 && d / (4 * ng) <= 1024) return ng;
+  return 0;
+}
+SF_DEV void st_bf16x4(__nv_bfloat16* p, float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 pk;
+  pk.x = *reinterpret_cast<uint32_t*>(&lo);
+  pk.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(p) = pk;
+}
+// y = x / sqrt(mean(x^2) + eps) * g  (grid.y > 1: grouped form, group g = blockIdx.y reads taps
+// + g * x_stride, scales g_ + g * d, writes columns [g d, (g+1) d) of a [T, 4d] row -- Eq.8 I_Cat)
+template <int NG>
+__global__ void __launch_bounds__(1024) rms_rows_kernel(const float* x_, int64_t x_stride, int in_ld, const float* g_,
+                                                        float eps, int d, __nv_bfloat16* out, int out_ld) {
+  KtScope kt_(gridDim.y > 1 ? KT_GROUP_RMS : KT_RMSNORM, (uint32_t)(d));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
+  __shared__ float red[32];
+  const int t = blockIdx.x, grp = blockIdx.y, nthr = blockDim.x;
+  const float* x = x_ + grp * x_stride + (size_t)t * in_ld;
+  const float* gm = g_ + (size_t)grp * d;
+  float4 v[NG];
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < NG; ++j) {
+    v[j] = *reinterpret_cast<const float4*>(x + 4 * threadIdx.x + 4 * nthr * j);
+    ss = fmaf(v[j].x, v[j].x, ss);
+    ss = fmaf(v[j].y, v[j].y, ss);
+    ss = fmaf(v[j].z, v[j].z, ss);
+    ss = fmaf(v[j].w, v[j].w, ss);
+  }
+  ss = block_sum_dyn(ss, red);
+  const float r = 1.0f / sqrtf(ss / (float)d + eps);
+  __nv_bfloat16* y = out + (size_t)t * out_ld + (size_t)grp * d;
+#pragma unroll
+  for (int j = 0; j < NG; ++j) {
+    const int i = 4 * threadIdx.x + 4 * nthr * j;
+    const float4 gg = *reinterpret_cast<const float4*>(gm + i);
+    st_bf16x4(y + i, v[j].x * r * gg.x, v[j].y * r * gg.y, v[j].z * r * gg.z, v[j].w * r * gg.w);
+  }
+}
+// embedding rows (bf16 table) -> fp32 residual stream (+ tap HS[0]), 8 elements per thread
+__global__ void __launch_bounds__(1024) embed_v_kernel(const int* tok, const __nv_bfloat16* emb, int d, int vocab,
+                                                       float* resid, float* tap0) {
+  KtScope kt_(KT_EMBED, (uint32_t)(d));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
+  const int t = blockIdx.x;
+  const int id = min(max(tok[t], 0), vocab - 1);
+  for (int i = 8 * threadIdx.x; i < d; i += 8 * blockDim.x) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(emb + (size_t)id * d + i);
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+    const float2 a = __bfloat1622float2(h2[0]), b = __bfloat1622float2(h2[1]), c = __bfloat1622float2(h2[2]),
+                 e = __bfloat1622float2(h2[3]);
+    const float4 lo = make_float4(a.x, a.y, b.x, b.y), hi = make_float4(c.x, c.y, e.x, e.y);
+    *reinterpret_cast<float4*>(resid + (size_t)t * d + i) = lo;
+    *reinterpret_cast<float4*>(resid + (size_t)t * d + i + 4) = hi;
+    if (tap0) {
+      *reinterpret_cast<float4*>(tap0 + (size_t)t * d + i) = lo;
+      *reinterpret_cast<float4*>(tap0 + (size_t)t * d + i + 4) = hi;
+    }
   }
 }
 
@@ -379,9 +453,12 @@ __global__ void attn_combine_kernel(AttnParams p) {
 
 // ------------------------------------------------------------------------ draft bidirectional SA
 // Eq.10 / P204: self-attention along the k draft slots of one context row, unmasked
-// (BIDIR_LOCAL), no RoPE; effective batch B. One CTA per (b, head).
+// (BIDIR_LOCAL), no RoPE; effective batch B. One CTA per (b, head); warp w takes query slots
+// i = w, w + 4, ...: scores by lane-parallel dot products + warp sums, softmax over the k slots in
+// registers, then each lane forms hd/32 output dimensions.
 template <typename TA>
-__global__ void bidir_attn_kernel(const TA* qkv, int k, int Hq, int Hkv, int hd, int causal, TA* out) {
+__global__ void __launch_bounds__(128) bidir_attn_kernel(const TA* qkv, int k, int Hq, int Hkv, int hd, int causal,
+                                                         TA* out) {
   KtScope kt_(KT_BIDIR, (uint32_t)(k));
   pdl_wait();
   kt_.mark();
@@ -393,7 +470,6 @@ __global__ void bidir_attn_kernel(const TA* qkv, int k, int Hq, int Hkv, int hd,
   float* q = fs;
   float* kk = q + k * hd;
   float* vv = kk + k * hd;
-  float* s = vv + k * hd;  // [k][k]
   for (int e = threadIdx.x; e < k * hd; e += blockDim.x) {
     const int i = e / hd, dd = e % hd;
     const TA* row = qkv + (size_t)(b * k + i) * W;
@@ -403,31 +479,35 @@ __global__ void bidir_attn_kernel(const TA* qkv, int k, int Hq, int Hkv, int hd,
   }
   __syncthreads();
   const float scale = rsqrtf((float)hd);
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-    const int i = e / k, j = e % k;
-    float a = 0.f;
-    for (int dd = 0; dd < hd; ++dd) a = fmaf(q[i * hd + dd], kk[j * hd + dd], a);
-    s[e] = (causal && j > i) ? -INFINITY : a * scale;
-  }
-  __syncthreads();
-  if (threadIdx.x < k) {
-    const int i = threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = warp; i < k; i += nw) {
+    float sc[16];
     float mx = -INFINITY;
-    for (int j = 0; j < k; ++j) mx = fmaxf(mx, s[i * k + j]);
-    float l = 0.f;
-    for (int j = 0; j < k; ++j) {
-      const float e = (s[i * k + j] == -INFINITY) ? 0.f : expf(s[i * k + j] - mx);
-      s[i * k + j] = e;
-      l += e;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j >= k) break;
+      float a = 0.f;
+      for (int dd = lane; dd < hd; dd += 32) a = fmaf(q[i * hd + dd], kk[j * hd + dd], a);
+      a = warp_sum(a) * scale;
+      sc[j] = (causal && j > i) ? -INFINITY : a;
+      mx = fmaxf(mx, sc[j]);
     }
-    for (int j = 0; j < k; ++j) s[i * k + j] /= l;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < k * hd; e += blockDim.x) {
-    const int i = e / hd, dd = e % hd;
-    float a = 0.f;
-    for (int j = 0; j < k; ++j) a = fmaf(s[i * k + j], vv[j * hd + dd], a);
-    out[(size_t)(b * k + i) * Hq * hd + h * hd + dd] = Elt<TA>::from_f(a);
+    float l = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j >= k) break;
+      sc[j] = (sc[j] == -INFINITY) ? 0.f : expf(sc[j] - mx);
+      l += sc[j];
+    }
+    for (int dd = lane; dd < hd; dd += 32) {
+      float a = 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j >= k) break;
+        a = fmaf(sc[j] / l, vv[j * hd + dd], a);
+      }
+      out[(size_t)(b * k + i) * Hq * hd + h * hd + dd] = Elt<TA>::from_f(a);
+    }
   }
 }
 
@@ -439,8 +519,13 @@ __global__ void gather_rows_kernel(const float* src, int q_len, const int* idx, 
   pdl_trigger();
   const int b = blockIdx.x;
   const int r = idx ? idx[b] : const_idx;
-  const float* s = src + ((size_t)b * q_len + r) * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) dst[(size_t)b * d + i] = s[i];
+  const float* sr = src + ((size_t)b * q_len + r) * d;
+  if (d % 4 == 0) {
+    for (int i = 4 * threadIdx.x; i < d; i += 4 * blockDim.x)
+      *reinterpret_cast<float4*>(dst + (size_t)b * d + i) = *reinterpret_cast<const float4*>(sr + i);
+  } else {
+    for (int i = threadIdx.x; i < d; i += blockDim.x) dst[(size_t)b * d + i] = sr[i];
+  }
 }
 
 // ------------------------------------------------------------------------ argmax (lowest id on ties)
@@ -600,15 +685,31 @@ cudaError_t launch_build_prefill_rows(int B, int P, int c0, int C, const int* to
 }
 cudaError_t launch_embed(bool bf, const int* tok, const void* embed, int T, int d, int vocab, float* resid,
                          float* tap0, cudaStream_t s) {
+  if (bf && d % 8 == 0)
+    return launch_k(embed_v_kernel, dim3(T), dim3(std::min(1024, d / 8)), 0, s, tok, (const __nv_bfloat16*)embed, d,
+                    vocab, resid, tap0);
   if (bf)
     launch_k(embed_kernel<__nv_bfloat16>, dim3(T), dim3(256), 0, s, tok, (const __nv_bfloat16*)embed, d, vocab, resid, tap0);
   else
     launch_k(embed_kernel<float>, dim3(T), dim3(256), 0, s, tok, (const float*)embed, d, vocab, resid, tap0);
   return cudaGetLastError();
 }
+static cudaError_t launch_rms_rows(const float* x, int64_t x_stride, int in_ld, const float* g, float eps, int T,
+                                   int groups, int d, __nv_bfloat16* out, int out_ld, cudaStream_t s) {
+  const int ng = row_ng(d);
+  const dim3 grid(T, groups), block(d / (4 * ng));
+  switch (ng) {
+    case 1: return launch_k(rms_rows_kernel<1>, grid, block, 0, s, x, x_stride, in_ld, g, eps, d, out, out_ld);
+    case 2: return launch_k(rms_rows_kernel<2>, grid, block, 0, s, x, x_stride, in_ld, g, eps, d, out, out_ld);
+    case 3: return launch_k(rms_rows_kernel<3>, grid, block, 0, s, x, x_stride, in_ld, g, eps, d, out, out_ld);
+    default: return launch_k(rms_rows_kernel<4>, grid, block, 0, s, x, x_stride, in_ld, g, eps, d, out, out_ld);
+  }
+}
 cudaError_t launch_rmsnorm(bool bf, const float* in, int in_ld, const float* gamma, float eps, int T, int d,
                            void* out, int out_ld, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
+  if (bf && row_ng(d) && in_ld % 4 == 0 && out_ld % 4 == 0)
+    return launch_rms_rows(in, 0, in_ld, gamma, eps, T, 1, d, (__nv_bfloat16*)out, out_ld, s);
   if (bf)
     launch_k(rmsnorm_kernel<__nv_bfloat16>, dim3(T), dim3(256), 0, s, in, in_ld, gamma, eps, d, (__nv_bfloat16*)out, out_ld);
   else
@@ -617,6 +718,8 @@ cudaError_t launch_rmsnorm(bool bf, const float* in, int in_ld, const float* gam
 }
 cudaError_t launch_group_rms(bool bf, const float* taps, int64_t tap_stride, const float* scales, float eps, int T,
                              int d, void* out, cudaStream_t s) {
+  if (bf && row_ng(d) && tap_stride % 4 == 0)
+    return launch_rms_rows(taps, tap_stride, d, scales, eps, T, 4, d, (__nv_bfloat16*)out, 4 * d, s);
   if (bf)
     launch_k(group_rms_kernel<__nv_bfloat16>, dim3(T), dim3(256), 0, s, taps, tap_stride, scales, eps, d, (__nv_bfloat16*)out);
   else
@@ -682,7 +785,7 @@ cudaError_t launch_attention(bool bf, const AttnParams& p, cudaStream_t s) {
 cudaError_t launch_bidir_attention(bool bf, const void* qkv, int B, int k, int Hq, int Hkv, int hd, bool causal,
                                    void* out, cudaStream_t s) {
   dim3 grid(B, Hq);
-  const size_t smem = (size_t)(3 * k * hd + k * k) * 4;
+  const size_t smem = (size_t)(3 * k * hd) * 4;
   if (bf)
     launch_k(bidir_attn_kernel<__nv_bfloat16>, dim3(grid), dim3(128), smem, s, (const __nv_bfloat16*)qkv, k, Hq, Hkv, hd, causal,
                                                             (__nv_bfloat16*)out);
@@ -692,7 +795,8 @@ cudaError_t launch_bidir_attention(bool bf, const void* qkv, int B, int k, int H
 }
 cudaError_t launch_gather_rows(const float* src, int q_len, const int* idx, int const_idx, int B, int d, float* dst,
                                cudaStream_t s) {
-  launch_k(gather_rows_kernel, dim3(B), dim3(256), 0, s, src, q_len, idx, const_idx, d, dst);
+  launch_k(gather_rows_kernel, dim3(B), dim3(std::max(32, std::min(1024, d / 4 / 32 * 32))), 0, s, src, q_len, idx,
+           const_idx, d, dst);
   return cudaGetLastError();
 }
 cudaError_t launch_argmax(const float* logits, int R, int V, float* pval, int* pidx, int* out, int* err,
