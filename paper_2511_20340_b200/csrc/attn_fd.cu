@@ -178,14 +178,14 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
       const int r = g + 8 * hr;
       const bool ok = r < nr;
       const int rr = r0 + (ok ? r : 0), qi = rr / G, h = it.kvh * G + rr % G;
-      const float* qrow = p.q + ((size_t)(it.b * p.q_len + qi) * p.Hq + h) * HD;
+      // bf16 rotated queries (rope_append rounded them RNE)
+      const uint32_t* qrow = reinterpret_cast<const uint32_t*>(reinterpret_cast<const __nv_bfloat16*>(p.q) +
+                                                               ((size_t)(it.b * p.q_len + qi) * p.Hq + h) * HD);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const int d0 = kk * 16 + 2 * t4;
-        const float2 x0 = ok ? *reinterpret_cast<const float2*>(qrow + d0) : make_float2(0.f, 0.f);
-        const float2 x1 = ok ? *reinterpret_cast<const float2*>(qrow + d0 + 8) : make_float2(0.f, 0.f);
-        qa[kk][hr] = pack_bf16(x0.x, x0.y);
-        qa[kk][2 + hr] = pack_bf16(x1.x, x1.y);
+        qa[kk][hr] = ok ? qrow[d0 / 2] : 0u;
+        qa[kk][2 + hr] = ok ? qrow[(d0 + 8) / 2] : 0u;
       }
     }
     const int pos_lo = base + (r0 + g) / G, pos_hi = base + (r0 + g + 8) / G;

@@ -268,6 +268,15 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       if (s > grp_last) grp_last += p.cgrp;
       if (s == 0) grp_last = p.cgrp - 1;
     }
+    if (p.epi.pf && p.epi.pf_bytes >= 16 * gridDim.x && elect_one()) {
+      // this CTA's slice of the next GEMM's weights -> L2, while the last stages drain and the
+      // epilogue runs (the DRAM would otherwise idle through the tail)
+      const size_t per = (p.epi.pf_bytes / gridDim.x) & ~(size_t)15;
+      const char* base = reinterpret_cast<const char*>(p.epi.pf) + per * blockIdx.x;
+      for (size_t off = 0; off < per; off += 65536)
+        prefetch_l2(base + off, (uint32_t)std::min<size_t>(65536, per - off), kEvictLast);
+    }
+    __syncwarp();
   } else if (warp == 1 && rank == 0) {
     // ---- MMA warp (converged; one elected lane issues every tcgen05 op so commits track them)
     const uint32_t idesc = idesc_bf16_f32(BM * CG, p.NT);

@@ -23,6 +23,10 @@ struct GemmEpi {
   int ldo = 0;             // row stride of out (elements)
   const float* bias = nullptr;
   float* tap = nullptr;    // optional extra copy (ADD_F32 only), row stride ldo
+  // optional: the next GEMM's weights; once this launch has issued its own loads, each CTA
+  // prefetches a slice of them into L2 so the DRAM keeps streaming through the epilogue tail
+  const void* pf = nullptr;
+  size_t pf_bytes = 0;
 };
 
 struct GemmScratch {

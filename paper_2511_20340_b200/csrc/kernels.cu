@@ -190,16 +190,19 @@ __global__ void __launch_bounds__(1024) embed_v_kernel(const int* tok, const __n
 // One warp per (row, head slot) -- grid (T, ceil((Hq + 2 Hkv) / 4)), 4 warps per CTA -- so even a
 // 5-row verify block spreads over hundreds of warps; lane l owns the rotate-half pairs
 // (i, i + hd/2) for i = VEC l .. VEC l + VEC - 1 (+ 32 VEC j), VEC = 2 when hd/2 is a multiple of 64.
-template <typename TA, int VEC>
-__global__ void __launch_bounds__(128) rope_append_kernel(const TA* qkv, int q_len, const int* pos0,
+template <typename TA, int VEC, bool QB>
+__global__ void __launch_bounds__(256) rope_append_kernel(const TA* qkv, int q_len, const int* pos0,
                                                           const float2* rope, int Hq, int Hkv, int hd,
-                                                          const int* bt, int pps, TA* Kp, TA* Vp, float* q_out) {
+                                                          const int* bt, int pps, TA* Kp, TA* Vp, void* q_out,
+                                                          int hpw) {
   KtScope kt_(KT_ROPE, (uint32_t)(Hq));
   pdl_wait();
   kt_.mark();
   pdl_trigger();
   const int t = blockIdx.x;
-  const int h = blockIdx.y * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
+  for (int hh = 0; hh < hpw; ++hh) {
+  const int h = (blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5)) * hpw + hh;
   if (h >= Hq + 2 * Hkv) return;
   const int b = t / q_len, qi = t % q_len;
   const int pos = pos0[b] + qi;
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(128) rope_append_kernel(const TA* qkv, int q_l
         for (int v = 0; v < VEC; ++v) dst[i + v] = row[i + v];
       }
     }
-    return;
+    continue;
   }
   const float2* cs = rope + (size_t)pos * half;
   for (int i = lane * VEC; i < half; i += 32 * VEC) {
@@ -243,7 +246,16 @@ __global__ void __launch_bounds__(128) rope_append_kernel(const TA* qkv, int q_l
       y2[v] = x2[v] * c[v].x + x1[v] * c[v].y;
     }
     if (h < Hq) {
-      float* q = q_out + ((size_t)t * Hq + h) * hd;
+      if constexpr (QB) {  // bf16 queries (RNE: the same bits the attention kernel would round to)
+        __nv_bfloat16* qb = reinterpret_cast<__nv_bfloat16*>(q_out) + ((size_t)t * Hq + h) * hd;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          qb[i + v] = __float2bfloat16_rn(y1[v]);
+          qb[i + v + half] = __float2bfloat16_rn(y2[v]);
+        }
+        continue;
+      }
+      float* q = reinterpret_cast<float*>(q_out) + ((size_t)t * Hq + h) * hd;
       if constexpr (VEC == 2) {
         *reinterpret_cast<float2*>(q + i) = make_float2(y1[0], y1[1]);
         *reinterpret_cast<float2*>(q + i + half) = make_float2(y2[0], y2[1]);
@@ -265,6 +277,7 @@ __global__ void __launch_bounds__(128) rope_append_kernel(const TA* qkv, int q_l
       }
     }
   }
+  }  // heads of this warp
 }
 
 // ------------------------------------------------------------------------ paged attention
@@ -727,18 +740,21 @@ cudaError_t launch_group_rms(bool bf, const float* taps, int64_t tap_stride, con
   return cudaGetLastError();
 }
 cudaError_t launch_rope_append(bool bf, const void* qkv, int T, int q_len, const int* pos0, const float2* rope,
-                               int Hq, int Hkv, int hd, const int* bt, int pps, void* Kp, void* Vp, float* q_out,
-                               cudaStream_t s) {
-  const dim3 grid(T, (Hq + 2 * Hkv + 3) / 4);
+                               int Hq, int Hkv, int hd, const int* bt, int pps, void* Kp, void* Vp, void* q_out,
+                               bool q_bf16, cudaStream_t s) {
+  const int hpw = 1;                      // heads per warp
+  const int wpc = T >= 64 ? 8 : 4;          // warps per CTA: fewer, fuller CTAs for long blocks
+  const dim3 grid(T, (Hq + 2 * Hkv + wpc * hpw - 1) / (wpc * hpw));
   const bool v2 = (hd / 2) % 64 == 0;
   if (bf) {
-    auto k = v2 ? rope_append_kernel<__nv_bfloat16, 2> : rope_append_kernel<__nv_bfloat16, 1>;
-    return launch_k(k, grid, dim3(128), 0, s, (const __nv_bfloat16*)qkv, q_len, pos0, rope, Hq, Hkv, hd, bt, pps,
-                    (__nv_bfloat16*)Kp, (__nv_bfloat16*)Vp, q_out);
+    auto k = q_bf16 ? (v2 ? rope_append_kernel<__nv_bfloat16, 2, true> : rope_append_kernel<__nv_bfloat16, 1, true>)
+                    : (v2 ? rope_append_kernel<__nv_bfloat16, 2, false> : rope_append_kernel<__nv_bfloat16, 1, false>);
+    return launch_k(k, grid, dim3(32 * wpc), 0, s, (const __nv_bfloat16*)qkv, q_len, pos0, rope, Hq, Hkv, hd, bt, pps,
+                    (__nv_bfloat16*)Kp, (__nv_bfloat16*)Vp, q_out, hpw);
   }
-  auto k = v2 ? rope_append_kernel<float, 2> : rope_append_kernel<float, 1>;
-  return launch_k(k, grid, dim3(128), 0, s, (const float*)qkv, q_len, pos0, rope, Hq, Hkv, hd, bt, pps, (float*)Kp,
-                  (float*)Vp, q_out);
+  auto k = v2 ? rope_append_kernel<float, 2, false> : rope_append_kernel<float, 1, false>;
+  return launch_k(k, grid, dim3(32 * wpc), 0, s, (const float*)qkv, q_len, pos0, rope, Hq, Hkv, hd, bt, pps, (float*)Kp,
+                  (float*)Vp, q_out, hpw);
 }
 
 template <typename TKV, int HD>

@@ -6,7 +6,7 @@
 namespace sf {
 
 struct AttnParams {
-  const float* q;            // [T, Hq, hd] rotated queries (fp32)
+  const float* q;            // [T, Hq, hd] rotated queries (fp32; bf16 for the bf16 hd=128 kernel)
   const void* Kp;            // paged K pool of one layer: [n_pages, Hkv, 16, hd]
   const void* Vp;            // paged V pool
   const int* block_table;    // [B, pages_per_seq]
@@ -38,11 +38,11 @@ cudaError_t launch_rmsnorm(bool is_bf16, const float* in, int in_ld, const float
                            void* out, int out_ld, cudaStream_t s);
 cudaError_t launch_group_rms(bool is_bf16, const float* taps, int64_t tap_stride, const float* scales, float eps,
                              int T, int d, void* out, cudaStream_t s);
+// q_bf16: rotated queries written as bf16 (the flash-decoding attention's operand precision)
 cudaError_t launch_rope_append(bool is_bf16, const void* qkv, int T, int q_len, const int* pos0,
                                const float2* rope, int Hq, int Hkv, int hd, const int* block_table,
-                               int pages_per_seq, void* Kp, void* Vp, float* q_out, cudaStream_t s);
+                               int pages_per_seq, void* Kp, void* Vp, void* q_out, bool q_bf16, cudaStream_t s);
 cudaError_t launch_attention(bool is_bf16, const AttnParams& p, cudaStream_t s);
-cudaError_t launch_attention_mma(const AttnParams& p, cudaStream_t s);  // bf16, hd 128 (split-KV)
 cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s);   // bf16, hd 128 (flash-decoding)
 cudaError_t launch_bidir_attention(bool is_bf16, const void* qkv, int B, int k, int Hq, int Hkv, int hd,
                                    bool causal, void* out, cudaStream_t s);
@@ -65,7 +65,6 @@ int argmax_splits(int V);
 // kernel timeline (SF_KTRACE=1, tools only): point every translation unit's device log at rec/cnt
 cudaError_t kt_setup_kernels(void* rec, unsigned* cnt, unsigned cap);
 cudaError_t kt_setup_gemm(void* rec, unsigned* cnt, unsigned cap);
-cudaError_t kt_setup_attn_mma(void* rec, unsigned* cnt, unsigned cap);
 cudaError_t kt_setup_attn_fd(void* rec, unsigned* cnt, unsigned cap);
 constexpr int kKtRecBytes = 40;
 

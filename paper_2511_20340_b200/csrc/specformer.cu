@@ -249,6 +249,9 @@ struct sf_handle {
     ev_free.pop_back();
     return e;
   }
+  // GEMM weights in launch order (draft, verify): the successor of each launch is prefetched to L2
+  std::vector<std::pair<const void*, size_t>> wchain;
+  size_t wchain_pos = 0;
   // forced drafts (bench)
   const int *f_cont = nullptr, *f_corrupt = nullptr;
   int f_cont_len = 0, f_corrupt_steps = 0;
@@ -305,6 +308,22 @@ static cudaError_t gemm(sf_handle* h, const void* A, int lda, const void* W, int
   const double outc = epi.mode == EPI_SWIGLU_ACT ? N / 2 : N;
   // algorithmic bytes: weight once + activation once + output once (+ residual read for ADD)
   ProfScope ps(h, 0, (double)N * K * wb + (double)T * K * wb + (double)T * outc * ob * (epi.mode == EPI_ADD_F32 ? 2 : 1));
+  static const size_t cap = (size_t)(getenv("SF_GEMM_PF_MB") ? atof(getenv("SF_GEMM_PF_MB")) : 0.0) * (1 << 20);
+  if (h->bf && !h->wchain.empty() && cap > 0) {
+    // (measured: prefetching the successor's weights into L2 during the tail loses at every batch --
+    // it competes with the tail's own loads -- so it is off unless SF_GEMM_PF_MB asks for it)
+    const size_t n = h->wchain.size();
+    for (size_t i = 0; i < n; ++i) {  // forward search from the last position: launch order is fixed
+      const size_t j = (h->wchain_pos + i) % n;
+      if (h->wchain[j].first == W) {
+        const auto& nx = h->wchain[(j + 1) % n];
+        epi.pf = nx.first;
+        epi.pf_bytes = std::min(nx.second, cap);
+        h->wchain_pos = j + 1;
+        break;
+      }
+    }
+  }
   GemmScratch sc;
   sc.partial = h->gpart;
   sc.partial_elems = h->p.gpart_elems;
@@ -378,7 +397,7 @@ static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const i
   const Plan& p = h->p;
   ProfScope ps(h, 1, 0.0);  // KV bytes depend on device-resident lengths: the bench computes them
   cudaError_t e = launch_rope_append(h->bf, h->qkv, T, q_len, pos0, h->rope, p.Hq, p.Hkv, p.hd, h->bt, p.pps,
-                                     h->kp(layer), h->vp(layer), h->qrot, h->st);
+                                     h->kp(layer), h->vp(layer), h->qrot, h->bf && p.hd == 128, h->st);
   if (e != cudaSuccess) return e;
   AttnParams ap{};
   ap.q = h->qrot;
@@ -579,7 +598,6 @@ static bool kt_enable() {
     cudaMemset(g_kt_cnt, 0, 4);
     kt_setup_kernels(g_kt_rec, g_kt_cnt, kKtCap);
     kt_setup_gemm(g_kt_rec, g_kt_cnt, kKtCap);
-    kt_setup_attn_mma(g_kt_rec, g_kt_cnt, kKtCap);
     kt_setup_attn_fd(g_kt_rec, g_kt_cnt, kKtCap);
   }
   return true;
@@ -680,7 +698,33 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
     h->blk_ffn_norm = (const float*)get("sf.blk_ffn_norm");
     h->blk_wgu = get("sf.blk_w_gu");
     h->blk_wdown = get("sf.blk_w_down");
+  }  {
+    // GEMM weight chain in launch order: draft (W_D, ctx QKV/O, W_P, block QKV/O/gate-up/down, LM
+    // head), then verify (per layer QKV, O, gate-up, down; LM head), then the next step's draft
+    const int64_t d = cfg->d_model, F = cfg->d_ff, V = cfg->vocab, k = cfg->draft_len;
+    const int64_t qkv = (int64_t)(cfg->n_heads + 2 * cfg->n_kv_heads) * cfg->head_dim,
+                  ao = (int64_t)cfg->n_heads * cfg->head_dim;
+    auto add = [&](const void* w, int64_t n, int64_t kk) { h->wchain.push_back({w, (size_t)(n * kk * 2)}); };
+    if (k > 0) {
+      add(h->w_d, d, 4 * d);
+      add(h->ctx_wqkv, qkv, d);
+      add(h->ctx_wo, d, ao);
+      add(h->w_p, k * d, d);
+      add(h->blk_wqkv, qkv, d);
+      add(h->blk_wo, d, ao);
+      add(h->blk_wgu, 2 * F, d);
+      add(h->blk_wdown, d, F);
+      add(h->lm_head, V, d);
+    }
+    for (int l = 0; l < cfg->n_layers; ++l) {
+      add(h->lw[l].wqkv, qkv, d);
+      add(h->lw[l].wo, d, ao);
+      add(h->lw[l].wgu, 2 * F, d);
+      add(h->lw[l].wdown, d, F);
+    }
+    add(h->lm_head, V, d);
   }
+
   // carve workspace
   const Plan& p = h->p;
   char* w = h->ws;
