@@ -168,9 +168,13 @@ def run_ours(args, cfg):
     B, k, P = args.batch, cfg.draft_len, cfg.prompt_len
     K, W = args.steps, args.warmup
     Kp = args.profile_steps
-    Ke = args.e2e_steps
+    Ke = args.e2e_steps if args.e2e_steps > 0 else cfg.gen_len - 1  # default: one full generation
+    Kf = max(0, args.forced_steps) if k > 0 else 0
+    n_cont = (W + Kf + 2) * (k + 1) + k + 2  # greedy-continuation tokens the forced window can consume
     max_seq = P + (W + K + Kp + 4) * (k + 1) + 32
     max_seq = max(max_seq, P + (Ke + 4) * (k + 1) + 32)
+    if Kf:
+        max_seq = max(max_seq, P + (n_cont + 2) * (k + 1) + 32)
     max_seq = (max_seq + 15) // 16 * 16
 
     weights = make_weights(cfg, seed=0, device="cuda")
@@ -181,11 +185,11 @@ def run_ours(args, cfg):
     prompts = dp.shard_rows(make_prompts(B * world, P, cfg.vocab), rank, world)  # weak scaling
 
     eng.prefill(prompts.cuda())
-    eng.decode_steps(W)
+    acc_log = torch.zeros(max(K, W), B, dtype=torch.int32, device="cuda")
+    eng.decode_steps(W, None, acc_log)  # warm-up; also captures the step graph the timed window replays
     eng.sync()
     before = eng.capture(3, (B,), torch.int32).cpu()
     prev_before = eng.capture(5, (B,), torch.int32).cpu()
-    acc_log = torch.zeros(K, B, dtype=torch.int32, device="cuda")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -314,6 +318,59 @@ def run_ours(args, cfg):
     e2e_tokens = B + int((em_host >= 0).sum())
     e2e_ms_max, e2e_tok = dp.reduce_timing(e2e_ms, float(e2e_tokens), device="cuda")
 
+    # ---------------- forced acceptance: drafts replaced -- after the draft step has run
+    # and been paid for -- by the GPU's own greedy continuation, corrupted at slot j with
+    # P(j) = alpha^(j-1) (1 - alpha) (none with alpha^k), alpha set so E[tokens/step] = a_paper
+    forced = None
+    if Kf:
+        a_target = A_PAPER.get(cfg.name, 1.75)
+        lo, hi = 0.0, 0.999
+        for _ in range(60):
+            mid = (lo + hi) / 2
+            if (1 - mid ** (k + 1)) / (1 - mid) < a_target: lo = mid
+            else: hi = mid
+        alpha = (lo + hi) / 2
+        # the continuation: lossless SD with measured acceptance emits the greedy sequence
+        g0 = eng.prefill(prompts.cuda())
+        n_gen = n_cont
+        em_log = torch.full((n_gen, B, k + 1), -1, dtype=torch.int32, device="cuda")
+        eng.decode_steps(n_gen, em_log, None)
+        eng.sync()
+        em = em_log.cpu()
+        cont = torch.zeros(B, n_cont, dtype=torch.int32)
+        g0c = g0.cpu()
+        for b in range(B):
+            toks = [int(g0c[b])] + [int(t) for t in em[:, b, :].reshape(-1) if int(t) >= 0]
+            toks = (toks + [toks[-1]] * n_cont)[:n_cont]
+            cont[b] = torch.tensor(toks, dtype=torch.int32)
+        gen = torch.Generator().manual_seed(2)  # per (step, global sequence): identical at any GPU count
+        n_cs = W + Kf + 2
+        u = torch.rand(n_cs, B * world, generator=gen)[:, rank * B:(rank + 1) * B]
+        cdf = torch.tensor([sum(alpha ** (i - 1) * (1 - alpha) for i in range(1, j + 1)) for j in range(1, k + 1)])
+        corrupt = (torch.searchsorted(cdf, u.contiguous()) + 1).to(torch.int32)  # k + 1 = no corruption
+        eng.prefill(prompts.cuda())
+        eng.set_forced_drafts(cont.cuda(), corrupt.cuda())
+        f_log = torch.zeros(max(Kf, W), B, dtype=torch.int32, device="cuda")
+        eng.decode_steps(W, None, f_log)
+        eng.sync()
+        fb = eng.capture(3, (B,), torch.int32).cpu()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        f0.record(eng.stream)
+        eng.decode_steps(Kf, None, f_log)
+        f1.record(eng.stream)
+        eng.sync()
+        fa = eng.capture(3, (B,), torch.int32).cpu()
+        f_ms, f_tok = dp.reduce_timing(f0.elapsed_time(f1), float(int((fa - fb).sum())), device="cuda")
+        eng.set_forced_drafts(None)
+        forced = {"tokens_per_s": f_tok / (f_ms / 1e3), "verify_steps_per_s_per_gpu": Kf / (f_ms / 1e3),
+                  "ms_per_step": f_ms / Kf, "mean_accepted_length": f_tok / (Kf * B * world),
+                  "a_target": a_target, "alpha": alpha, "steps": Kf,
+                  "note": "drafts = GPU greedy continuation corrupted at an i.i.d. slot (seed 2); the draft "
+                          "forward still runs every step"}
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
@@ -334,6 +391,7 @@ def run_ours(args, cfg):
                        "l2": "inputs larger than L2 (14 GB weights + KV per step)"},
             "verify_steps_per_s": steps_per_s, "verify_steps_per_s_box": steps_per_s * world,
             "mean_accepted_length": a_meas,
+            "forced_acceptance": forced,
             "modeled_tokens_per_s_at_paper_a": steps_per_s * B * world * A_PAPER.get(cfg.name, 1.75),
             "a_paper": A_PAPER.get(cfg.name),
             "roofline": {"bound": bound, "kernel": dominant, "achieved": achieved, "peak": peak_v, "unit": unit,
@@ -346,7 +404,10 @@ def run_ours(args, cfg):
                               "t_roof_ms": (sb / K) / (hbm * 1e9) * 1e3},
             "e2e": {"value": e2e_tok / (e2e_ms_max / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": B * P * 4 / Ke, "d2h_bytes_per_step": B * (k + 3) * 4,
-                    "steps": Ke, "includes_prefill": True, "note": "prompt H2D amortised over the steps"},
+                    "steps": Ke, "includes_prefill": True,
+                    "note": "one generation through the public C ABI with pinned host buffers: prompt H2D + "
+                            "prefill + Ke draft/verify/accept calls, each step's accept lengths / emitted tokens / "
+                            "lengths read back to the host; prompt bytes amortised over the steps"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
@@ -367,7 +428,8 @@ def main():
     ap.add_argument("--config", default="7b")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--profile-steps", type=int, default=4)
-    ap.add_argument("--e2e-steps", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = the config's generation length - 1")
+    ap.add_argument("--forced-steps", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -606,13 +606,14 @@ __global__ void argmax_final_kernel(const float* pval, const int* pidx, int R, i
 // P25: accept only drafts equal to the base model's greedy outputs. Single CTA (B <= 1024).
 __global__ void accept_kernel(int B, int k, const int* draft, const int* greedy, int* seq_len, int* n_prev,
                               int* last_token, int* r_b, int* accept_len, int* emitted, int* step_counter,
-                              int* accept_log, int* emitted_log, int log_cap) {
+                              int* accept_log, int* emitted_log, const int* log_cap_dev) {
   KtScope kt_(KT_ACCEPT, (uint32_t)(k));
   pdl_wait();
   kt_.mark();
   pdl_trigger();
   const int b = threadIdx.x;
   const int step = step_counter ? *step_counter : 0;
+  const int log_cap = (accept_log || emitted_log) && log_cap_dev ? *log_cap_dev : 0;
   if (b < B) {
     const int* g = greedy + b * (k + 1);
     int m = 0;
@@ -825,7 +826,7 @@ cudaError_t launch_argmax(const float* logits, int R, int V, float* pval, int* p
 }
 cudaError_t launch_accept(int B, int k, const int* draft, const int* greedy, int* seq_len, int* n_prev,
                           int* last_token, int* r_b, int* accept_len, int* emitted, int* step_counter,
-                          int* accept_log, int* emitted_log, int log_cap, cudaStream_t s) {
+                          int* accept_log, int* emitted_log, const int* log_cap, cudaStream_t s) {
   const int th = ((B + 31) / 32) * 32;
   launch_k(accept_kernel, dim3(1), dim3(th), 0, s, B, k, draft, greedy, seq_len, n_prev, last_token, r_b, accept_len, emitted,
                                  step_counter, accept_log, emitted_log, log_cap);

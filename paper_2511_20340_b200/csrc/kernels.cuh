@@ -52,7 +52,7 @@ cudaError_t launch_argmax(const float* logits, int R, int V, float* pval, int* p
                           cudaStream_t s);
 cudaError_t launch_accept(int B, int k, const int* draft, const int* greedy, int* seq_len, int* n_prev,
                           int* last_token, int* r_b, int* accept_len, int* emitted, int* step_counter,
-                          int* accept_log, int* emitted_log, int log_cap, cudaStream_t s);
+                          int* accept_log, int* emitted_log, const int* log_cap /* device */, cudaStream_t s);
 cudaError_t launch_force_drafts(int B, int k, int V, const int* cont, int cont_len, const int* corrupt,
                                 int corrupt_steps, const int* seq_len, const int* prompt_len,
                                 const int* step_counter, int* draft, cudaStream_t s);

@@ -216,7 +216,7 @@ struct sf_handle {
   void *xn, *qkv, *attn, *ffn;
   int *gcnt, *ami, *acnt;
   int *tok_rows, *pos0_pf, *seq_len, *n_prev, *last_token, *r_b, *prompt_len, *draft, *greedy, *accept_len,
-      *emitted, *err, *step_counter, *g_pf, *prompt;
+      *emitted, *err, *step_counter, *g_pf, *prompt, *d_logcap;
   // state
   int B = 0;
   int state = ST_INIT;
@@ -229,7 +229,6 @@ struct sf_handle {
   cudaGraphExec_t gexec = nullptr;
   int64_t graph_launches = 0;
   int *g_acc_log = nullptr, *g_em_log = nullptr;
-  int g_log_cap = 0;
   // per-kernel-class profiling (eager launches only; bench roofline)
   struct Prof {
     int cls;
@@ -570,11 +569,11 @@ static cudaError_t do_verify(sf_handle* h) {
   return head_argmax(h, h->resid, T, h->logits, h->greedy, h->final_xn_ready);
 }
 
-static cudaError_t do_accept(sf_handle* h, int* acc_log, int* em_log, int log_cap) {
+static cudaError_t do_accept(sf_handle* h, int* acc_log, int* em_log) {
   const Plan& p = h->p;
   h->launches++;
   cudaError_t e = launch_accept(h->B, p.k, h->draft, h->greedy, h->seq_len, h->n_prev, h->last_token, h->r_b,
-                                h->accept_len, h->emitted, h->step_counter, acc_log, em_log, log_cap, h->st);
+                                h->accept_len, h->emitted, h->step_counter, acc_log, em_log, h->d_logcap, h->st);
   if (p.k > 0) h->ctx_pending = true;
   return e;
 }
@@ -771,6 +770,7 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
   h->emitted = ints(p.rows_v);
   h->err = ints(1);
   h->step_counter = ints(1);
+  h->d_logcap = ints(1);
   h->g_pf = ints(p.B);
   h->prompt = (int*)(w + p.o_prompt);
   cudaError_t e = cudaSuccess;
@@ -888,7 +888,7 @@ sf_status specformer_verify_step(sf_handle* h, const int32_t* draft_in, int32_t*
 sf_status specformer_accept_commit(sf_handle* h, int32_t* accept_len, int32_t* emitted, int32_t* seq_len) {
   if (!h) return SF_ERR_ARG;
   if (h->state != ST_VERIFIED) return set_err(h, SF_ERR_STATE, "accept_commit needs verify_step first");
-  SF_TRY(do_accept(h, nullptr, nullptr, 0));
+  SF_TRY(do_accept(h, nullptr, nullptr));
   const int k = h->p.k;
   SF_TRY(copy_out(h, accept_len, h->accept_len, (size_t)h->B * 4));
   SF_TRY(copy_out(h, emitted, h->emitted, (size_t)h->B * (k + 1) * 4));
@@ -898,7 +898,7 @@ sf_status specformer_accept_commit(sf_handle* h, int32_t* accept_len, int32_t* e
   return SF_OK;
 }
 
-static cudaError_t one_step(sf_handle* h, int* acc_log, int* em_log, int cap) {
+static cudaError_t one_step(sf_handle* h, int* acc_log, int* em_log) {
   cudaError_t e;
   if (h->p.k > 0) {
     if ((e = do_draft(h))) return e;
@@ -910,7 +910,7 @@ static cudaError_t one_step(sf_handle* h, int* acc_log, int* em_log, int cap) {
     }
   }
   if ((e = do_verify(h))) return e;
-  return do_accept(h, acc_log, em_log, cap);
+  return do_accept(h, acc_log, em_log);
 }
 
 sf_status specformer_decode_steps(sf_handle* h, int32_t n_steps, int32_t* emitted_log, int32_t* accept_log) {
@@ -928,14 +928,16 @@ sf_status specformer_decode_steps(sf_handle* h, int32_t n_steps, int32_t* emitte
   }
   h->launches = 0;
   SF_TRY(cudaMemsetAsync(h->step_counter, 0, 4, h->st));
+  if (accept_log || emitted_log) SF_TRY(launch_fill(h->d_logcap, 1, n_steps, h->st));  // logs hold n_steps rows
   int done = 0;
   if (k > 0 && !h->ctx_pending && n_steps > 0) {  // first step after prefill: no context pass
-    SF_TRY(one_step(h, accept_log, emitted_log, n_steps));
+    SF_TRY(one_step(h, accept_log, emitted_log));
     done = 1;
   }
   const bool use_graph = (h->c.flags & SF_FLAG_CUDA_GRAPH) != 0 && !h->prof_on;
   if (use_graph && done < n_steps) {
-    if (h->gexec && (h->g_acc_log != accept_log || h->g_em_log != emitted_log || h->g_log_cap < n_steps)) {
+    // the graph depends on the log pointers only (the log capacity is read on the device)
+    if (h->gexec && (h->g_acc_log != accept_log || h->g_em_log != emitted_log)) {
       cudaGraphExecDestroy(h->gexec);
       h->gexec = nullptr;
     }
@@ -943,7 +945,7 @@ sf_status specformer_decode_steps(sf_handle* h, int32_t n_steps, int32_t* emitte
       cudaGraph_t g;
       const int64_t before = h->launches;
       SF_TRY(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
-      cudaError_t e = one_step(h, accept_log, emitted_log, n_steps);
+      cudaError_t e = one_step(h, accept_log, emitted_log);
       cudaError_t e2 = cudaStreamEndCapture(h->st, &g);
       if (e != cudaSuccess || e2 != cudaSuccess) {
         h->err_msg = std::string("graph capture failed: ") + cudaGetErrorString(e != cudaSuccess ? e : e2);
@@ -955,7 +957,6 @@ sf_status specformer_decode_steps(sf_handle* h, int32_t n_steps, int32_t* emitte
       h->launches = before;
       h->g_acc_log = accept_log;
       h->g_em_log = emitted_log;
-      h->g_log_cap = n_steps;
     }
     for (int s = done; s < n_steps; ++s) {
       SF_TRY(cudaGraphLaunch(h->gexec, h->st));
@@ -963,7 +964,7 @@ sf_status specformer_decode_steps(sf_handle* h, int32_t n_steps, int32_t* emitte
     }
     h->ctx_pending = k > 0;
   } else {
-    for (int s = done; s < n_steps; ++s) SF_TRY(one_step(h, accept_log, emitted_log, n_steps));
+    for (int s = done; s < n_steps; ++s) SF_TRY(one_step(h, accept_log, emitted_log));
   }
   h->host_len_hi += (int64_t)n_steps * (k + 1);
   h->state = ST_READY;
