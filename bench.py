@@ -195,10 +195,12 @@ def run_ours(args, cfg):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        torch.cuda.cudart().cudaProfilerStart()  # ncu --profile-from-start off: the timed window only
         e0.record(eng.stream)
         eng.decode_steps(K, None, acc_log)
         e1.record(eng.stream)
         torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
     if world > 1:
         dist.barrier()
     eng.sync()
@@ -268,11 +270,13 @@ def run_ours(args, cfg):
         achieved = attn_bytes / (attn_ms / 1e3) / 1e9
         dom_bytes_per_launch = attn_bytes / max(1, attn_n)
         dom_ms = attn_ms / max(1, attn_n)
+    # DRAM bytes per launch of the dominant kernel class from the committed ncu launch list of this
+    # command at this batch (profiles/ncu_traffic.json, written by tools/profile_summary.py)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(dominant)
+            traffic = json.load(open(tp)).get(f"{cfg.name}_b{B}", {}).get("traffic_bytes_per_launch", {}).get(dominant)
         except Exception:
             traffic = None
     prof_classes = {name: {"ms_total": cls[c][0], "launches": cls[c][1], "share_of_profiled_step":

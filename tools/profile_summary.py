@@ -36,10 +36,14 @@ def main(path, steps, out_txt, out_json=None):
     open(out_txt, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     if out_json:
-        traffic = {}
+        traffic, tot = {}, collections.defaultdict(lambda: [0, 0.0])
         for k, (n, t, b) in agg.items():
-            if k.startswith("gemm_sk_kernel"): traffic["gemm"] = b / n
-            if k.startswith("attn_fd_kernel") or k.startswith("attn_mma_kernel"): traffic["attention"] = b / n
+            cls = "gemm" if k.startswith("gemm_sk_kernel") else ("attention" if k.startswith("attn_fd_kernel") else None)
+            if cls:
+                tot[cls][0] += n
+                tot[cls][1] += b
+        for cls, (n, b) in tot.items():
+            traffic[cls] = b / n  # DRAM bytes per launch, averaged over the class's launches
         json.dump({"traffic_bytes_per_launch": traffic, "source": path}, open(out_json, "w"), indent=1)
 
 if __name__ == "__main__":
