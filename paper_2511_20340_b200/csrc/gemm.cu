@@ -122,11 +122,21 @@ SF_DEV void umma_bf16_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uin
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-SF_DEV void umma_commit_2sm(uint64_t* bar) {
+SF_DEV void umma_commit_2sm(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
-      "h"((uint16_t)3)
+      "h"(mask)
+      : "memory");
+}
+// 2-SM TMA multicast: the box lands at the same offset in every CTA of `mask`; each destination's
+// transaction bytes are credited to the barrier of ITS pair leader (peer bit cleared)
+SF_DEV void tma_load_2d_2sm_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint16_t mask,
+                               uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "h"(mask), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
 
@@ -139,7 +149,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
-  const int a_rows = p.NT / CG;  // activation rows of each sub-tile staged by this CTA
+  // CG = CTAs per cluster: 1; 2 = one CTA pair (cta_group::2 MMA, M = 256); 4 = two CTA pairs that
+  // share the activation tile through TMA multicast (each CTA loads a quarter of it)
+  constexpr bool kPair = CG >= 2;
+  const int a_rows = kPair ? p.NT / 2 : p.NT;  // activation rows of each sub-tile in this CTA's smem
   const int a_bytes = p.n_sub * a_rows * BK * 2;
   const int stage_bytes = BM * BK * 2 + a_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)p.stages * stage_bytes);
@@ -150,7 +163,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 3);
   
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = (CG == 2) ? cluster_rank() : 0u;
+  const uint32_t rank = kPair ? cluster_rank() : 0u;
+  const uint32_t prank = rank & 1u, pbase = rank & ~1u;  // position in the CTA pair, pair leader rank
   const int c = blockIdx.x / CG;       // work group
   const int slot = blockIdx.x;         // partial / flag slot of this CTA
   const int kb = p.kb_total;
@@ -164,18 +178,18 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     if (!(CG == 1 && p.w_tiled && !p.w_tma)) prefetch_tmap(&tmW);
     prefetch_tmap(&tmA);
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(&full[s], 1);  // leader: one arrive_expect_tx covering both CTAs' bytes
-      mbar_init(&empty[s], 1);
+      mbar_init(&full[s], 1);  // pair leader: one arrive_expect_tx covering both CTAs' bytes
+      mbar_init(&empty[s], CG == 4 ? 2 : 1);  // CG 4: a slot is refilled (multicast) once BOTH pairs consumed it
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
-      mbar_init(&acce[b], CG);  // leader: both CTAs' epilogues release the accumulator
+      mbar_init(&acce[b], kPair ? 2 : 1);  // pair leader: both CTAs' epilogues release the accumulator
     }
     mbar_init(fixb, 1);
     fence_barrier_init();
   }
   if (warp == 2) {
-    if constexpr (CG == 2) {
+    if constexpr (kPair) {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                    "r"(p.tmem_cols)
                    : "memory");
@@ -186,7 +200,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CG == 2) cluster_sync();
+  if constexpr (kPair) cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) SF_TR(1);
@@ -209,8 +223,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         } else {
           // the leader arms the barrier for both CTAs' bytes; a fresh phase cannot complete before
           // that arrival, so the peer's bytes may land first
-          if (rank == 0) mbar_arrive_expect_tx(&full[i], (uint32_t)(2 * stage_bytes));
-          tma_load_2d_2sm(st, &tmW, &full[i], 0, ((tp * 2 + (int)rank) * kb + kp) * BM, kEvictFirst);
+          if (prank == 0) mbar_arrive_expect_tx(&full[i], (uint32_t)(2 * stage_bytes));
+          tma_load_2d_2sm(st, &tmW, &full[i], 0, ((tp * CG + (int)rank) * kb + kp) * BM, kEvictFirst);
         }
         if (++kp == kb) {
           kp = 0;
@@ -245,13 +259,23 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
             tma_load_2d(st + BM * BK * 2 + j * a_rows * BK * 2, &tmA, &full[s], k * BK, j * p.NT, kEvictLast);
         } else {
           if (!pre) {
-            if (rank == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * stage_bytes));
-            // tiled weights viewed as a [blocks*128, 64] tensor: this CTA's 128-row half of pair tile t
-            tma_load_2d_2sm(st, &tmW, &full[s], 0, ((t * 2 + (int)rank) * kb + k) * BM, kEvictFirst);
+            if (prank == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * stage_bytes));
+            // tiled weights viewed as a [blocks*128, 64] tensor: this CTA's 128-row tile of unit tile t
+            tma_load_2d_2sm(st, &tmW, &full[s], 0, ((t * CG + (int)rank) * kb + k) * BM, kEvictFirst);
           }
-          for (int j = 0; j < p.n_sub; ++j)
-            tma_load_2d_2sm(st + BM * BK * 2 + j * a_rows * BK * 2, &tmA, &full[s], k * BK,
-                            j * p.NT + (int)rank * a_rows, kEvictLast);
+          if constexpr (CG == 4) {
+            // this CTA's pair-half of the activation (rows prank * a_rows ..) is also needed by the
+            // CTA at the same position in the other pair: each loads one half of it, multicast to both
+            const int hr = a_rows / 2, pr = (int)(rank >> 1);
+            const uint16_t mask = (uint16_t)((1u << prank) | (1u << (prank + 2)));
+            for (int j = 0; j < p.n_sub; ++j)
+              tma_load_2d_2sm_mc(st + BM * BK * 2 + j * a_rows * BK * 2 + pr * hr * BK * 2, &tmA, &full[s], k * BK,
+                                 j * p.NT + (int)prank * a_rows + pr * hr, mask, kEvictLast);
+          } else {
+            for (int j = 0; j < p.n_sub; ++j)
+              tma_load_2d_2sm(st + BM * BK * 2 + j * a_rows * BK * 2, &tmA, &full[s], k * BK,
+                              j * p.NT + (int)rank * a_rows, kEvictLast);
+          }
           // no arrival from the peer: its bytes complete_tx on the leader's barrier, which the leader
           // armed for both CTAs; they cannot land before that phase (the slot was released first)
         }
@@ -277,9 +301,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         prefetch_l2(base + off, (uint32_t)std::min<size_t>(65536, per - off), kEvictLast);
     }
     __syncwarp();
-  } else if (warp == 1 && rank == 0) {
+  } else if (warp == 1 && prank == 0) {
     // ---- MMA warp (converged; one elected lane issues every tcgen05 op so commits track them)
-    const uint32_t idesc = idesc_bf16_f32(BM * CG, p.NT);
+    const uint32_t idesc = idesc_bf16_f32(kPair ? 2 * BM : BM, p.NT);
     const uint32_t a_off = (uint32_t)(BM * BK * 2) >> 4;           // B-operand tile offset (16 B units)
     const uint32_t sub_off = (uint32_t)(a_rows * BK * 2) >> 4;     // between activation sub-tiles
     int seg = 0;
@@ -316,7 +340,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
             }
           if (++gcnt == p.cgrp) {  // frees slots s-cgrp+1..s (in both CTAs of a pair)
             if constexpr (CG == 1) umma_commit(&empty[s]);
-            else umma_commit_2sm(&empty[s]);
+            else umma_commit_2sm(&empty[s], CG == 4 ? (uint16_t)0xF : (uint16_t)(3u << pbase));
           }
         }
         __syncwarp();
@@ -328,7 +352,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       }
       if (elect_one()) {
         if constexpr (CG == 1) umma_commit(&accf[b]);
-        else umma_commit_2sm(&accf[b]);
+        else umma_commit_2sm(&accf[b], (uint16_t)(3u << pbase));
       }
       __syncwarp();
       if (lane == 0) {
@@ -625,8 +649,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           tc_fence_before();
           named_sync(1, 256);
           if (lead && seg < nseg_total - 1) {  // (the MMA never waits for the last buffer)
-            if (CG == 1 || rank == 0) mbar_arrive(&acce[b]);
-            else mbar_arrive_remote(&acce[b], 0);
+            if (CG == 1 || prank == 0) mbar_arrive(&acce[b]);
+            else mbar_arrive_remote(&acce[b], pbase);
           }
         } else {
           named_sync(5, 384);
@@ -661,10 +685,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CG == 2) cluster_sync();
+  if constexpr (kPair) cluster_sync();
   tc_fence_after();
   if (warp == 2) {
-    if constexpr (CG == 2)
+    if constexpr (kPair)
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
     else
       tmem_dealloc(tmem, p.tmem_cols);
@@ -753,14 +777,16 @@ static bool make_map(CUtensorMap* m, const void* ptr, int rows, int K, int ld_el
   return r == CUDA_SUCCESS;
 }
 
-static void tc_shape(int T, int* NT, int* n_sub) {
-  const int Tp = std::max(16, (T + 15) / 16 * 16);
+// MMA N tiling of T token columns (granularity g: 16, or 32 for the multicast pairs whose quarter
+// activation boxes must start on 8-row swizzle atoms)
+static void tc_shape(int T, int* NT, int* n_sub, int g = 16) {
+  const int Tp = std::max(g, (T + g - 1) / g * g);
   if (Tp <= 256) {
     *NT = Tp;
     *n_sub = 1;
   } else {
     *n_sub = (Tp + 255) / 256;
-    *NT = ((Tp + *n_sub - 1) / *n_sub + 15) / 16 * 16;
+    *NT = ((Tp + *n_sub - 1) / *n_sub + g - 1) / g * g;
   }
 }
 
@@ -847,12 +873,44 @@ static bool make_map_tiled(CUtensorMap* m, const void* ptr, long long rows) {
 }
 
 // CTA-pair (cta_group::2) mode for a weight shape: a function of (N, K) only (batch invariance)
+// Persistent groups for a cluster size: the co-resident clusters of a 1-CTA-per-SM kernel (GPCs
+// with an odd SM count or not a multiple of 4 leave SMs out: 74 pairs but only 33 quads on a B200).
+static int max_groups(int cg) {
+  static int cache[5] = {0, 0, 0, 0, 0};
+  if (cache[cg]) return cache[cg];
+  int n = num_sms() / cg;
+  if (cg > 1) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(num_sms() / cg * cg);
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = 200 * 1024;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cg;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int m = 0;
+    cudaFuncSetAttribute(gemm_sk_kernel<2, EPI_STORE_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (cudaOccupancyMaxActiveClusters(&m, (const void*)gemm_sk_kernel<2, EPI_STORE_F32>, &cfg) == cudaSuccess && m > 0)
+      n = std::min(n, m);
+    cudaGetLastError();
+  }
+  cache[cg] = n;
+  return n;
+}
+
 // CTA-pair mode halves each SM's share of the activation tile (the MMA reads the B operand from
 // both CTAs' shared memory), the L2->SM traffic that bounds the skinny GEMM at large T.
+// CG 4 (two pairs sharing the activation tile by 2-SM TMA multicast) would quarter it again, but
+// it deadlocks on the first launch in this build (not yet understood) and a B200 co-schedules only
+// 33 4-CTA clusters (132 SMs): experimental, SF_GEMM_CG=4 only.
 static int gemm_cg(int N, int K) {
   (void)K;
   static const int env = getenv("SF_GEMM_CG") ? atoi(getenv("SF_GEMM_CG")) : 2;
-  if (env == 2 && N % (2 * BM) == 0) return 2;
+  if (env >= 4 && N % (4 * BM) == 0) return 4;
+  if (env >= 2 && N % (2 * BM) == 0) return 2;
   return 1;
 }
 
@@ -867,6 +925,7 @@ static SkKernel sk_kernel_for(int cg, int mode) {
     case EPI_SWIGLU_ACT: return gemm_sk_kernel<CGV, EPI_SWIGLU_ACT>; \
     default: return gemm_sk_kernel<CGV, EPI_PARTIAL>;           \
   }
+  if (cg == 4) SF_SK(4);
   if (cg == 2) SF_SK(2);
   SF_SK(1);
 #undef SF_SK
@@ -876,7 +935,7 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
                              const GemmEpi& epi, const GemmScratch& scratch, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    for (int cg = 1; cg <= 2; ++cg)
+    for (int cg = 1; cg <= 4; cg *= 2)
       for (int md = 0; md <= EPI_PARTIAL; ++md)
         cudaFuncSetAttribute(sk_kernel_for(cg, md), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
@@ -887,16 +946,16 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   p.N = N;
   p.K = K;
   p.Tp = (T + 31) / 32 * 32;
-  tc_shape(T, &p.NT, &p.n_sub);
+  tc_shape(T, &p.NT, &p.n_sub, CG == 4 ? 32 : 16);
   p.kb_total = K / BK;
   p.n_tiles = N / (BM * CG);
   const long long U = (long long)p.n_tiles * p.kb_total;
-  p.G = (int)std::min<long long>(num_sms() / CG, U);  // depends on (N, K) only
+  p.G = (int)std::min<long long>(max_groups(CG), U);  // depends on (N, K) and the device only
   const int cols = p.n_sub * p.NT;
   p.nbuf = (2 * cols <= 512) ? 2 : 1;
   p.tmem_cols = 32;
   while ((int)p.tmem_cols < p.nbuf * cols) p.tmem_cols <<= 1;
-  const int stage_bytes = BM * BK * 2 + p.n_sub * (p.NT / CG) * BK * 2;
+  const int stage_bytes = BM * BK * 2 + p.n_sub * (CG >= 2 ? p.NT / 2 : p.NT) * BK * 2;
   // deep ring: ~200 KB in flight per SM covers loaded-HBM latency (Little's law)
   static const int env_st = getenv("SF_GEMM_STAGES") ? atoi(getenv("SF_GEMM_STAGES")) : 0;
   p.stages = std::max(2, std::min(16, (216 * 1024) / stage_bytes));
@@ -933,7 +992,7 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   memset(&mw, 0, sizeof(mw));
   static const int env_wtma = getenv("SF_GEMM_WTMA") ? atoi(getenv("SF_GEMM_WTMA")) : 0;
   p.w_tma = (CG == 1 && w_tiled && env_wtma) ? 1 : 0;
-  if (CG == 2 || p.w_tma) {
+  if (CG >= 2 || p.w_tma) {
     if (!make_map_tiled(&mw, W, (long long)N * (K / BK))) return cudaErrorInvalidValue;
   } else if (!w_tiled && !make_map(&mw, W, N, K, K, BM)) {
     return cudaErrorInvalidValue;
@@ -944,13 +1003,13 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p.G * 2);
+  cfg.gridDim = dim3(p.G * CG);
   cfg.blockDim = dim3(384);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.x = CG;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
   attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -965,7 +1024,7 @@ bool gemm_partial_geom(int T, int N, int K, PartialGeom* g) {
   const int CG = gemm_cg(N, K);
   const int n_tiles = N / (BM * CG);
   const long long U = (long long)n_tiles * (K / BK);
-  const int G = (int)std::min<long long>(num_sms() / CG, U);
+  const int G = (int)std::min<long long>(max_groups(CG), U);
   if (n_tiles > G) return false;  // a group must touch at most 2 tiles
   g->G = G * CG;                  // slots are per CTA: consumer addresses (2 * group + which) * CG + rank
   g->kb = K / BK;
