@@ -71,7 +71,9 @@ struct Item {
 
 // item = (b * Hkv + kvh) * ntiles + qt. Warps 0..3 compute, warp 4 produces.
 __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__ CUtensorMap tmK,
-                                                        const __grid_constant__ CUtensorMap tmV, AttnParams p,
+                                                        const __grid_constant__ CUtensorMap tmV,
+                                                        const __grid_constant__ CUtensorMap tmK4,
+                                                        const __grid_constant__ CUtensorMap tmV4, AttnParams p,
                                                         int ntiles, int nseg_max, int seg_keys, int n_items) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   const uint32_t raw = smem_u32(sm_raw);
@@ -139,6 +141,25 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
         const int kstart = c * CH;
         const int npages = (min(CH, kmax + 1 - kstart) + 15) / 16;
         const int pg = (lane < npages) ? p.block_table[it.b * p.pages_per_seq + kstart / 16 + lane] : 0;
+        const int pg0 = __shfl_sync(0xffffffffu, pg, 0);
+        // the chunk's pages are consecutive in the pool (the identity page table, and any run of a
+        // permuted one): 4 TMA boxes of 8 pages x 16 keys x 64 dims instead of 32 one-page boxes
+        // (pages past the sequence's last key are masked; the pool is zero-initialised, so they are finite)
+        const bool run = __all_sync(0xffffffffu, lane >= npages || pg == pg0 + lane);
+        if (run) {
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&full[st], (uint32_t)(4 * 8 * 16 * 128));
+            uint8_t* kb = sm + st * STAGE_BYTES;
+            uint8_t* vb = kb + KV_BYTES;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              tma_load_4d(kb + hf * (CH * 128), &tmK4, &full[st], hf * 64, 0, it.kvh, pg0, kEvictFirst);
+              tma_load_4d(vb + hf * (CH * 128), &tmV4, &full[st], hf * 64, 0, it.kvh, pg0, kEvictFirst);
+            }
+          }
+          __syncwarp();
+          continue;
+        }
         if (lane == 0) mbar_arrive_expect_tx(&full[st], (uint32_t)(npages * 4 * 16 * 128));
         __syncwarp();
         for (int i = 0; i < npages; ++i) {
@@ -388,6 +409,26 @@ static bool encode_kv_map(CUtensorMap* m, const void* base, long long rows) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// the pool as [pages][Hkv][16 keys][hd]: box = 8 consecutive pages x 16 keys x 1 head x 64 dims
+static bool encode_kv_map4(CUtensorMap* m, const void* base, int Hkv, long long n_pages) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)HD, 16, (cuuint64_t)Hkv, (cuuint64_t)n_pages};
+  cuuint64_t strides[3] = {(cuuint64_t)HD * 2, (cuuint64_t)16 * HD * 2, (cuuint64_t)Hkv * 16 * HD * 2};
+  cuuint32_t box[4] = {64, 16, 1, 8};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
   static bool attr = false;
   static int num_sms = 148;
@@ -408,8 +449,11 @@ cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
   const int grid = std::min(n_items, num_sms);
   CUtensorMap mk, mv;
   const long long rows = (long long)p.n_pages * p.Hkv * 16;
+  CUtensorMap mk4, mv4;
   if (!encode_kv_map(&mk, p.Kp, rows) || !encode_kv_map(&mv, p.Vp, rows)) return cudaErrorInvalidValue;
-  launch_k(attn_fd_kernel, dim3(grid), dim3(160), SMEM, s, mk, mv, p, ntiles, nseg_max, seg_keys, n_items);
+  if (!encode_kv_map4(&mk4, p.Kp, p.Hkv, p.n_pages) || !encode_kv_map4(&mv4, p.Vp, p.Hkv, p.n_pages))
+    return cudaErrorInvalidValue;
+  launch_k(attn_fd_kernel, dim3(grid), dim3(160), SMEM, s, mk, mv, mk4, mv4, p, ntiles, nseg_max, seg_keys, n_items);
   return cudaGetLastError();
 }
 
