@@ -171,11 +171,13 @@ def run_ours(args, cfg):
     Ke = args.e2e_steps if args.e2e_steps > 0 else cfg.gen_len - 1  # default: one full generation
     Kf = max(0, args.forced_steps) if k > 0 else 0
     n_cont = (W + Kf + 2) * (k + 1) + k + 2  # greedy-continuation tokens the forced window can consume
-    max_seq = P + (W + K + Kp + 4) * (k + 1) + 32
-    max_seq = max(max_seq, P + (Ke + 4) * (k + 1) + 32)
+    # capacity: every phase restarts from a prefill; a decode_steps call of n steps needs n (k + 1)
+    # positions of headroom over the actual length (a ~= 1 with random weights, so lengths grow ~1 per step)
+    GEN_CHUNK = 16
+    grow = max(W + K * (k + 1), W + K + Kp * (k + 1), Ke + k + 1)
     if Kf:
-        max_seq = max(max_seq, P + (n_cont + 2) * (k + 1) + 32)
-    max_seq = (max_seq + 15) // 16 * 16
+        grow = max(grow, n_cont + GEN_CHUNK * (k + 1), (W + Kf) * (k + 1))
+    max_seq = (P + grow + 32 + 15) // 16 * 16
 
     weights = make_weights(cfg, seed=0, device="cuda")
     ec = EngineConfig.from_model(cfg, max_batch=B, max_seq=max_seq, flags=N.SF_FLAG_CUDA_GRAPH)
@@ -338,7 +340,8 @@ def run_ours(args, cfg):
         g0 = eng.prefill(prompts.cuda())
         n_gen = n_cont
         em_log = torch.full((n_gen, B, k + 1), -1, dtype=torch.int32, device="cuda")
-        eng.decode_steps(n_gen, em_log, None)
+        for s0 in range(0, n_gen, GEN_CHUNK):  # chunked: each call needs only GEN_CHUNK (k+1) of headroom
+            eng.decode_steps(min(GEN_CHUNK, n_gen - s0), em_log[s0:], None)
         eng.sync()
         em = em_log.cpu()
         cont = torch.zeros(B, n_cont, dtype=torch.int32)
@@ -434,12 +437,15 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = the config's generation length - 1")
     ap.add_argument("--forced-steps", type=int, default=32)
+    ap.add_argument("--draft-len", type=int, default=None, help="override k (13B sweep: 4 / 6 / 8)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     from synth import get_config
     cfg = get_config(args.config)
+    if args.draft_len is not None:
+        cfg = cfg.replace(draft_len=args.draft_len)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

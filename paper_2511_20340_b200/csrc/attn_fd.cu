@@ -441,7 +441,8 @@ cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
   }
   const int G = p.Hq / p.Hkv;
   const int ntiles = (p.q_len * G + 15) / 16;
-  static const int env_seg = getenv("SF_ATTN_SEG") ? atoi(getenv("SF_ATTN_SEG")) : 0;  // experiments
+  // segment size override (tests exercise the multi-segment fold at short contexts; read per launch)
+  const int env_seg = getenv("SF_ATTN_SEG") ? atoi(getenv("SF_ATTN_SEG")) : 0;
   const int seg_keys = (env_seg >= CH && env_seg % CH == 0) ? env_seg : kAttnSeg;
   const int nseg_max = (p.max_key + seg_keys - 1) / seg_keys;
   if (nseg_max > p.nchunk_max || !p.seg_cnt) return cudaErrorInvalidValue;

@@ -24,7 +24,7 @@ struct AttnParams {
 };
 
 constexpr int kAttnChunk = 128;  // fixed absolute key-chunk size (split-KV boundaries, C23)
-constexpr int kAttnSeg = 1024;   // flash-decoding key segment: one work item (fixed absolute bounds)
+constexpr int kAttnSeg = 2048;   // flash-decoding key segment: one work item (fixed absolute bounds)
 
 // act dtype: bf16 (is_bf16) or fp32.
 cudaError_t launch_rope_table(float2* table, int max_seq, int hd, float theta, cudaStream_t s);

@@ -244,3 +244,24 @@ def test_full_width_depth2_bf16(cfg):
     assert _check_bf16(cfg, w, prompts, res, seqs=(0,), rel_tol=2.2e-2) > 10
     ar = run_gpu(cfg, w, prompts, cfg.gen_len, k=0)
     assert ar["tokens"] == res["tokens"]
+
+
+# ------------------------------------------------------------------ multi-segment flash-decoding
+@pytest.mark.parametrize("cfg", [MID, GQA], ids=["mha128", "gqa4"])
+def test_attention_segments_fold(cfg, monkeypatch):
+    """Attention keys split into fixed 128-key segments (SF_ATTN_SEG; the default segment exceeds every
+    BASELINE context but the 70B one): segment states are published and folded in segment order by the
+    CTA that completes a (sequence, head, tile) group's last segment. Oracle parity, GPU SD == GPU AR
+    bit-exact, and paged == identity page tables bit-exact (the per-page TMA fallback) under it."""
+    monkeypatch.setenv("SF_ATTN_SEG", "128")
+    w, prompts = setup(cfg, seed=5, jitter=0.1)
+    res = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True)
+    assert _check_bf16(cfg, w, prompts, res, seqs=(0, cfg.batch - 1)) > 20
+    ar = run_gpu(cfg, w, prompts, cfg.gen_len, k=0)
+    assert ar["tokens"] == res["tokens"]
+    eng = res["engine"]
+    pps = eng.cfg.max_seq // 16
+    perm = torch.randperm(cfg.batch * pps, generator=torch.Generator().manual_seed(4)).reshape(cfg.batch, pps)
+    res2 = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True, block_table=perm)
+    for s1, s2 in zip(res["steps"], res2["steps"]):
+        assert np.array_equal(s1["logits"], s2["logits"])
