@@ -314,11 +314,15 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
     }
     const unsigned long long ti1 = g_kt.rec ? kt_now() : 0ull;
     // ---- merge the 4 warp states in fixed order and normalise
+    if (g < nr) {  // (rows of the tile past the block's rows are never read)
 #pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-      const int d = nt * 8 + 2 * t4;
-      *reinterpret_cast<float2*>(mrg + (warp * 16 + g) * HD + d) = make_float2(o[nt][0], o[nt][1]);
-      *reinterpret_cast<float2*>(mrg + (warp * 16 + g + 8) * HD + d) = make_float2(o[nt][2], o[nt][3]);
+      for (int nt = 0; nt < 16; ++nt)
+        *reinterpret_cast<float2*>(mrg + (warp * 16 + g) * HD + nt * 8 + 2 * t4) = make_float2(o[nt][0], o[nt][1]);
+    }
+    if (g + 8 < nr) {
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt)
+        *reinterpret_cast<float2*>(mrg + (warp * 16 + g + 8) * HD + nt * 8 + 2 * t4) = make_float2(o[nt][2], o[nt][3]);
     }
     if (t4 == 0) {
       mrg_m[warp * 16 + g] = m_lo;
@@ -327,31 +331,41 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
       mrg_l[warp * 16 + g + 8] = l_hi;
     }
     named_bar(1, 128);
+    // per-row merge factors once (row r: thread r): M = max_w m_w, f_w = 2^(m_w - M), L = sum_w l_w f_w
+    // (same values and order as forming them per element)
+    if (tid < nr) {
+      const int r = tid;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) M = fmaxf(M, mrg_m[w * 16 + r]);
+      float L = 0.f;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float f = (mrg_m[w * 16 + r] == -INFINITY) ? 0.f : exp2f(mrg_m[w * 16 + r] - M);
+        L += mrg_l[w * 16 + r] * f;
+        mrg_m[w * 16 + r] = f;
+      }
+      mrg_l[r] = L;
+      mrg_l[16 + r] = M;
+    }
+    named_bar(1, 128);
     const int group = (it.b * p.Hkv + it.kvh) * ntiles + it.qt;
-    for (int e = tid; e < 16 * HD; e += 128) {
+    for (int e = tid; e < nr * HD; e += 128) {
       const int r = e / HD, d = e % HD;
-      if (r < nr) {
-        float M = -INFINITY;
+      float acc = 0.f;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) M = fmaxf(M, mrg_m[w * 16 + r]);
-        float L = 0.f, acc = 0.f;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const float f = (mrg_m[w * 16 + r] == -INFINITY) ? 0.f : exp2f(mrg_m[w * 16 + r] - M);
-          L += mrg_l[w * 16 + r] * f;
-          acc += mrg[(w * 16 + r) * HD + d] * f;
-        }
-        const int rr = r0 + r, qi = rr / G, h = it.kvh * G + rr % G;
-        const int t = it.b * p.q_len + qi;
-        if (it.nseg == 1) {
-          reinterpret_cast<__nv_bfloat16*>(p.out)[((size_t)t * p.Hq + h) * HD + d] = __float2bfloat16_rn(acc / L);
-        } else {
-          const size_t slot = ((size_t)t * p.Hq + h) * p.nchunk_max + it.seg;
-          p.part_o[slot * HD + d] = acc;
-          if (d == 0) {
-            p.part_ml[2 * slot] = M;
-            p.part_ml[2 * slot + 1] = L;
-          }
+      for (int w = 0; w < 4; ++w) acc += mrg[(w * 16 + r) * HD + d] * mrg_m[w * 16 + r];
+      const float L = mrg_l[r];
+      const int rr = r0 + r, qi = rr / G, h = it.kvh * G + rr % G;
+      const int t = it.b * p.q_len + qi;
+      if (it.nseg == 1) {
+        reinterpret_cast<__nv_bfloat16*>(p.out)[((size_t)t * p.Hq + h) * HD + d] = __float2bfloat16_rn(acc / L);
+      } else {
+        const size_t slot = ((size_t)t * p.Hq + h) * p.nchunk_max + it.seg;
+        p.part_o[slot * HD + d] = acc;
+        if (d == 0) {
+          p.part_ml[2 * slot] = mrg_l[16 + r];
+          p.part_ml[2 * slot + 1] = L;
         }
       }
     }
