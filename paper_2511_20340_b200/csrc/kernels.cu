@@ -280,6 +280,64 @@ __global__ void __launch_bounds__(256) rope_append_kernel(const TA* qkv, int q_l
   }  // heads of this warp
 }
 
+// bf16, hd = 128, bf16 queries (the flash-decoding path): persistent warps walk the (row, head)
+// items two at a time (loads of both in flight), lane l owns the rotate-half pairs (2l, 2l+1) and
+// (2l + 64, 2l + 65). A few hundred resident CTAs instead of T x heads / 8 short ones.
+__global__ void __launch_bounds__(256) rope_append128_kernel(const __nv_bfloat16* qkv, int T, int q_len,
+                                                             const int* pos0, const float2* rope, int Hq, int Hkv,
+                                                             const int* bt, int pps, __nv_bfloat16* Kp,
+                                                             __nv_bfloat16* Vp, __nv_bfloat16* q_out) {
+  KtScope kt_(KT_ROPE, (uint32_t)(Hq));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
+  const int H = Hq + 2 * Hkv, W = H * 128;
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const int items = T * H;
+  for (int i0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i0 < items; i0 += 2 * nw) {
+    uint32_t a[2], bb[2];
+    float4 cs[2];
+    int t[2], h[2], pos[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int it = min(i0 + u * nw, items - 1);
+      t[u] = it / H;
+      h[u] = it % H;
+      pos[u] = pos0[t[u] / q_len] + t[u] % q_len;
+      const __nv_bfloat16* row = qkv + (size_t)t[u] * W + (size_t)h[u] * 128;
+      a[u] = *reinterpret_cast<const uint32_t*>(row + 2 * lane);
+      bb[u] = *reinterpret_cast<const uint32_t*>(row + 64 + 2 * lane);
+      cs[u] = *reinterpret_cast<const float4*>(rope + (size_t)pos[u] * 64 + 2 * lane);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (i0 + u * nw >= items) break;
+      const int b = t[u] / q_len;
+      if (h[u] >= Hq + Hkv) {  // value head: plain copy into the page
+        const int blk = bt[b * pps + pos[u] / 16], slot = pos[u] % 16;
+        __nv_bfloat16* dst = Vp + (((size_t)blk * Hkv + (h[u] - Hq - Hkv)) * 16 + slot) * 128;
+        *reinterpret_cast<uint32_t*>(dst + 2 * lane) = a[u];
+        *reinterpret_cast<uint32_t*>(dst + 64 + 2 * lane) = bb[u];
+        continue;
+      }
+      const float2 x1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a[u]));
+      const float2 x2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bb[u]));
+      const float y10 = x1.x * cs[u].x - x2.x * cs[u].y, y20 = x2.x * cs[u].x + x1.x * cs[u].y;
+      const float y11 = x1.y * cs[u].z - x2.y * cs[u].w, y21 = x2.y * cs[u].z + x1.y * cs[u].w;
+      __nv_bfloat16* dst;
+      if (h[u] < Hq) {
+        dst = q_out + ((size_t)t[u] * Hq + h[u]) * 128;
+      } else {
+        const int blk = bt[b * pps + pos[u] / 16], slot = pos[u] % 16;
+        dst = Kp + (((size_t)blk * Hkv + (h[u] - Hq)) * 16 + slot) * 128;
+      }
+      *reinterpret_cast<__nv_bfloat162*>(dst + 2 * lane) = __floats2bfloat162_rn(y10, y11);
+      *reinterpret_cast<__nv_bfloat162*>(dst + 64 + 2 * lane) = __floats2bfloat162_rn(y20, y21);
+    }
+  }
+}
+
 // ------------------------------------------------------------------------ paged attention
 // Hybrid-mask decode attention, mode CAUSAL_PREFIX: query row i of sequence b (absolute position
 // p = pos0[b] + i) attends keys 0..p of its pages. Split-KV over FIXED absolute 128-key chunks:
@@ -743,6 +801,12 @@ cudaError_t launch_group_rms(bool bf, const float* taps, int64_t tap_stride, con
 cudaError_t launch_rope_append(bool bf, const void* qkv, int T, int q_len, const int* pos0, const float2* rope,
                                int Hq, int Hkv, int hd, const int* bt, int pps, void* Kp, void* Vp, void* q_out,
                                bool q_bf16, cudaStream_t s) {
+  if (bf && q_bf16 && hd == 128) {
+    const int items = T * (Hq + 2 * Hkv);
+    const int grid = std::max(1, std::min((items + 15) / 16, 148 * 4));
+    return launch_k(rope_append128_kernel, dim3(grid), dim3(256), 0, s, (const __nv_bfloat16*)qkv, T, q_len, pos0, rope,
+                    Hq, Hkv, bt, pps, (__nv_bfloat16*)Kp, (__nv_bfloat16*)Vp, (__nv_bfloat16*)q_out);
+  }
   const int hpw = 1;                      // heads per warp
   const int wpc = T >= 64 ? 8 : 4;          // warps per CTA: fewer, fuller CTAs for long blocks
   const dim3 grid(T, (Hq + 2 * Hkv + wpc * hpw - 1) / (wpc * hpw));
