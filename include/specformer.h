@@ -96,7 +96,11 @@ typedef struct sf_handle sf_handle;
  * sf.blk_wqkv; sf.blk_wo; sf.blk_ffn_norm[d] f32; sf.blk_w_gu[2F,d]; sf.blk_w_down[d,F].
  * w_gu interleaves the SwiGLU gate and up projections row by row: row 2i is gate row i, row
  * 2i+1 is up row i, so a GEMM tile holds matching gate/up rows in adjacent accumulator lanes
- * for the fused SwiGLU epilogue (F % 64 == 0).
+ * for the fused SwiGLU epilogue (F % 64 == 0). In bf16 mode with head_dim 128, the rows of
+ * layers.<l>.wqkv and sf.ctx_wqkv are pair-interleaved within each 128-row head: row 2i of a head is
+ * its dimension i, row 2i+1 its dimension i + 64 (the rotate-half RoPE partners land in adjacent
+ * accumulator lanes of the fused RoPE / KV-append epilogue); sf.blk_wqkv (no RoPE) keeps the
+ * natural order.
  * Matrices are stored in the config dtype, vectors in fp32. In bf16 mode every matrix except
  * `embed` uses layout 1: fill it with sf_pack_matrix from a row-major device copy. */
 int sf_weight_table(const sf_config* cfg, sf_tensor_desc* out, int cap);

@@ -26,6 +26,13 @@ template <> struct Elt<__nv_bfloat16> {
 template <typename T> SF_DEV float ld_f(const T* p) { return Elt<T>::to_f(*p); }
 template <typename T> SF_DEV void st_f(T* p, float v) { *p = Elt<T>::from_f(v); }
 
+// ---------------------------------------------------------------- RoPE (reading C5)
+// Rotate-half pair (x1 = dim i, x2 = dim i + hd/2) at angle (c, s), with explicitly rounded
+// operations (no FMA contraction) so every kernel that applies it -- the RoPE/append kernels and
+// the QKV GEMM's fused epilogue -- produces the same bits from the same bf16 inputs.
+SF_DEV float rope_y1(float x1, float x2, float c, float s) { return __fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, s)); }
+SF_DEV float rope_y2(float x1, float x2, float c, float s) { return __fadd_rn(__fmul_rn(x2, c), __fmul_rn(x1, s)); }
+
 // ---------------------------------------------------------------- warp reductions
 SF_DEV float warp_sum(float v) {
 #pragma unroll

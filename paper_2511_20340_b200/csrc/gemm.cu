@@ -383,7 +383,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     constexpr int kStageBytes = 16384;
     const int ring_bytes = p.stages * stage_bytes;
     const int out_elt = mode == EPI_STORE_F32 ? 4 : 2;
-    constexpr bool kStageable = MODE == EPI_STORE_ACT || MODE == EPI_STORE_F32 || MODE == EPI_SWIGLU_ACT;
+    constexpr bool kStageable =
+        MODE == EPI_STORE_ACT || MODE == EPI_STORE_F32 || MODE == EPI_SWIGLU_ACT || MODE == EPI_QKV_ROPE;
     const bool can_stage = kStageable && p.stage_ok &&
                            (ldo * out_elt) % 16 == 0 && ring_bytes >= 3 * kStageBytes + 64 * BM * 4;
     const int fix_bytes = can_stage ? ring_bytes - 3 * kStageBytes : ring_bytes;
@@ -392,12 +393,72 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     float* const slot_base = p.partial + (size_t)slot * p.Tp * BM;                    // published tail
     float* const defer_base = p.partial + (size_t)(p.G * CG + slot) * p.Tp * BM;  // parked full tile
 
+    // EPI_QKV_ROPE: destination row (128 bf16) of token t for head tile vt_: q heads -> q_out,
+    // k / v heads -> the token's page slot
+    auto rope_dst_row = [&](int tl, int vt_) -> __nv_bfloat16* {
+      const RopeEpi& R = p.epi.rope;
+      const int t = tl + R.t0;
+      const int b = t / R.q_len, pos = R.pos0[b] + t % R.q_len;
+      if (vt_ < R.Hq) return reinterpret_cast<__nv_bfloat16*>(R.q_out) + ((size_t)t * R.Hq + vt_) * 128;
+      const bool isk = vt_ < R.Hq + R.Hkv;
+      const int kvh = isk ? vt_ - R.Hq : vt_ - R.Hq - R.Hkv;
+      const int blk = R.bt[b * R.pps + pos / 16];
+      return reinterpret_cast<__nv_bfloat16*>(isk ? R.Kp : R.Vp) + (((size_t)blk * R.Hkv + kvh) * 16 + pos % 16) * 128;
+    };
+    // RoPE on this thread's (dim, token) values: lane pair (2i, 2i+1) holds dims (i, i + 64) of the head
+    // (pair-interleaved weight rows). The accumulator is rounded to bf16 first -- exactly the values
+    // the unfused path (bf16 QKV output, then the RoPE kernel) rotates -- so both paths give the same
+    // bits. Lane l resolves token c0 + l's position and destination row once; emit(q, dim, y, row).
+    auto rope_rows = [&](float (&v)[32], int c0, int nq, int vt_, auto emit) {
+      const RopeEpi& R = p.epi.rope;
+      const bool odd = lane & 1;
+      const int i = m >> 1, dim = odd ? 64 + i : i;
+      const bool rot = vt_ < R.Hq + R.Hkv;
+      int my_pos = 0;
+      unsigned long long my_row = 0;
+      if (lane < nq) {
+        const int t = c0 + lane + R.t0;
+        my_pos = R.pos0[t / R.q_len] + t % R.q_len;
+        my_row = reinterpret_cast<unsigned long long>(rope_dst_row(c0 + lane, vt_));
+      }
+#pragma unroll 8
+      for (int q = 0; q < 32; ++q) {
+        if (q >= nq) break;  // (warp-uniform)
+        const int pos = __shfl_sync(0xffffffffu, my_pos, q);
+        const unsigned long long row = __shfl_sync(0xffffffffu, my_row, q);
+        const float x = __bfloat162float(__float2bfloat16_rn(v[q]));
+        const float xo = __shfl_xor_sync(0xffffffffu, x, 1);
+        float y = x;
+        if (rot) {
+          const float2 cs = R.table[(size_t)pos * 64 + i];
+          y = odd ? rope_y2(xo, x, cs.x, cs.y) : rope_y1(x, xo, cs.x, cs.y);
+        }
+        emit(q, dim, y, reinterpret_cast<__nv_bfloat16*>(row));
+      }
+    };
     // one 32-token chunk of this thread's row m: stage [32 tokens][tile columns] in smem, then
     // write whole rows with 16-byte vectors (per-thread column stores would be 32-byte sectors
     // 10-100 KB apart)
     auto staged_store = [&](float (&v)[32], int c0, int nq, int vt_, int gid) {
       uint8_t* sb = stg + (size_t)gid * kStageBytes;
-      const int rowb = mode == EPI_SWIGLU_ACT ? 128 : (mode == EPI_STORE_ACT ? 256 : 512);
+      const int rowb = mode == EPI_SWIGLU_ACT ? 128 : ((mode == EPI_STORE_ACT || mode == EPI_QKV_ROPE) ? 256 : 512);
+      if constexpr (MODE == EPI_QKV_ROPE) {
+        // rows: [32][256 B] values, then the 32 destination row pointers (8 KB + 256 B < 16 KB)
+        unsigned long long* rows = reinterpret_cast<unsigned long long*>(sb + 32 * 256);
+        rope_rows(v, c0, nq, vt_, [&](int q, int dim, float y, __nv_bfloat16* row) {
+          reinterpret_cast<__nv_bfloat16*>(sb + q * 256)[dim] = __float2bfloat16_rn(y);
+          if (m == 0) rows[q] = reinterpret_cast<unsigned long long>(row);
+        });
+        named_sync(2 + gid, 128);
+        const int ht = quad * 32 + lane;
+        for (int i = ht; i < nq * 16; i += 128) {
+          const int q = i >> 4, x = i & 15;
+          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(rows[q]) + x * 8) =
+              *reinterpret_cast<const uint4*>(sb + q * 256 + x * 16);
+        }
+        named_sync(2 + gid, 128);
+        return;
+      }
       if (mode == EPI_STORE_ACT) {
 #pragma unroll
         for (int q = 0; q < 32; ++q) reinterpret_cast<__nv_bfloat16*>(sb + q * 256)[m] = __float2bfloat16_rn(v[q]);
@@ -436,6 +497,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     };
     // per-thread column stores (segments that end while the ring is still streaming)
     auto direct_store = [&](float (&v)[32], int c0, int nq, int vt_) {
+      if constexpr (MODE == EPI_QKV_ROPE) {
+        rope_rows(v, c0, nq, vt_, [&](int q, int dim, float y, __nv_bfloat16* row) { row[dim] = __float2bfloat16_rn(y); });
+        return;
+      }
       const int n = vt_ * BM + m;
       if (mode == EPI_STORE_ACT) {
         __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.epi.out) + (size_t)c0 * ldo + n;
@@ -923,6 +988,7 @@ static SkKernel sk_kernel_for(int cg, int mode) {
     case EPI_ADD_F32: return gemm_sk_kernel<CGV, EPI_ADD_F32>;       \
     case EPI_BIAS_F32: return gemm_sk_kernel<CGV, EPI_BIAS_F32>;     \
     case EPI_SWIGLU_ACT: return gemm_sk_kernel<CGV, EPI_SWIGLU_ACT>; \
+    case EPI_QKV_ROPE: return gemm_sk_kernel<CGV, EPI_QKV_ROPE>;     \
     default: return gemm_sk_kernel<CGV, EPI_PARTIAL>;           \
   }
   if (cg == 4) SF_SK(4);
@@ -936,7 +1002,7 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   static bool attr = false;
   if (!attr) {
     for (int cg = 1; cg <= 4; cg *= 2)
-      for (int md = 0; md <= EPI_PARTIAL; ++md)
+      for (int md = 0; md <= EPI_QKV_ROPE; ++md)
         cudaFuncSetAttribute(sk_kernel_for(cg, md), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
@@ -1216,7 +1282,8 @@ cudaError_t gemm_launch(bool is_bf16, const void* A, int lda, const void* W, boo
   for (int t0 = 0; t0 < T; t0 += 512) {
     GemmEpi e = epi;
     const size_t out_elt = (epi.mode == EPI_STORE_ACT || epi.mode == EPI_SWIGLU_ACT) ? 2 : 4;
-    e.out = (char*)epi.out + (size_t)t0 * epi.ldo * out_elt;
+    if (epi.mode == EPI_QKV_ROPE) e.rope.t0 = epi.rope.t0 + t0;
+    else e.out = (char*)epi.out + (size_t)t0 * epi.ldo * out_elt;
     if (epi.tap) e.tap = epi.tap + (size_t)t0 * epi.ldo;
     cudaError_t r = gemm_launch_chunk(true, (const char*)A + (size_t)t0 * lda * 2, lda, W, w_tiled,
                                       std::min(512, T - t0), N, K, e, scratch, st);

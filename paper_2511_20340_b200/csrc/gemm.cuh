@@ -15,6 +15,21 @@ enum EpiMode : int {
                        // out_act[t, i] = silu(gate_i) * up_i  (SwiGLU, P197)
   EPI_PARTIAL = 5,     // bf16 path, N/128 <= #SMs: every k-segment's fp32 accumulator goes to the
                        // scratch partial slots; a consumer (launch_resid_norm) adds them in k order
+  EPI_QKV_ROPE = 6,    // bf16, head_dim 128 (one head per 128-row tile), W rows pair-interleaved per
+                       // head (row 2i = dim i, 2i+1 = dim i+64): RoPE on q / k heads at the rows'
+                       // positions, q -> rope.q_out [T, Hq, 128] bf16, k / v -> their page slots
+};
+struct RopeEpi {
+  const int* pos0 = nullptr;   // [B] position of each sequence's first row; row t = b q_len + i
+  int q_len = 1;
+  const float2* table = nullptr;  // [max_seq, 64] (cos, sin)
+  int Hq = 0, Hkv = 0;
+  const int* bt = nullptr;     // [B, pps] page table
+  int pps = 0;
+  void* Kp = nullptr;          // [pages, Hkv, 16, 128] bf16
+  void* Vp = nullptr;
+  void* q_out = nullptr;       // [T, Hq, 128] bf16
+  int t0 = 0;                  // row offset of this launch chunk (T > 512 runs in chunks)
 };
 
 struct GemmEpi {
@@ -27,6 +42,7 @@ struct GemmEpi {
   // prefetches a slice of them into L2 so the DRAM keeps streaming through the epilogue tail
   const void* pf = nullptr;
   size_t pf_bytes = 0;
+  RopeEpi rope;  // EPI_QKV_ROPE only
 };
 
 struct GemmScratch {

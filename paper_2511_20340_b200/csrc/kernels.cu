@@ -242,8 +242,8 @@ __global__ void __launch_bounds__(256) rope_append_kernel(const TA* qkv, int q_l
     }
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
-      y1[v] = x1[v] * c[v].x - x2[v] * c[v].y;
-      y2[v] = x2[v] * c[v].x + x1[v] * c[v].y;
+      y1[v] = rope_y1(x1[v], x2[v], c[v].x, c[v].y);
+      y2[v] = rope_y2(x1[v], x2[v], c[v].x, c[v].y);
     }
     if (h < Hq) {
       if constexpr (QB) {  // bf16 queries (RNE: the same bits the attention kernel would round to)
@@ -280,9 +280,10 @@ __global__ void __launch_bounds__(256) rope_append_kernel(const TA* qkv, int q_l
   }  // heads of this warp
 }
 
-// bf16, hd = 128, bf16 queries (the flash-decoding path): persistent warps walk the (row, head)
-// items two at a time (loads of both in flight), lane l owns the rotate-half pairs (2l, 2l+1) and
-// (2l + 64, 2l + 65). A few hundred resident CTAs instead of T x heads / 8 short ones.
+// bf16, hd = 128, bf16 queries (the flash-decoding path; the QKV weight rows are pair-interleaved
+// per head, so its output is too): persistent warps walk the (row, head) items two at a time
+// (loads of both in flight), lane l owns the rotate-half pairs (2l, 2l+64) and (2l+1, 2l+65).
+// A few hundred resident CTAs instead of T x heads / 8 short ones.
 __global__ void __launch_bounds__(256) rope_append128_kernel(const __nv_bfloat16* qkv, int T, int q_len,
                                                              const int* pos0, const float2* rope, int Hq, int Hkv,
                                                              const int* bt, int pps, __nv_bfloat16* Kp,
@@ -305,9 +306,16 @@ __global__ void __launch_bounds__(256) rope_append128_kernel(const __nv_bfloat16
       t[u] = it / H;
       h[u] = it % H;
       pos[u] = pos0[t[u] / q_len] + t[u] % q_len;
+      // pair-interleaved head rows (include/specformer.h): position 2d holds dim d, 2d+1 dim d + 64;
+      // lane l reads positions 4l..4l+3 = dims (2l, 2l+64, 2l+1, 2l+65)
       const __nv_bfloat16* row = qkv + (size_t)t[u] * W + (size_t)h[u] * 128;
-      a[u] = *reinterpret_cast<const uint32_t*>(row + 2 * lane);
-      bb[u] = *reinterpret_cast<const uint32_t*>(row + 64 + 2 * lane);
+      const uint2 raw = *reinterpret_cast<const uint2*>(row + 4 * lane);
+      const __nv_bfloat162 p0 = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);  // (2l, 2l+64)
+      const __nv_bfloat162 p1 = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);  // (2l+1, 2l+65)
+      const __nv_bfloat162 lo = __halves2bfloat162(__low2bfloat16(p0), __low2bfloat16(p1));
+      const __nv_bfloat162 hi = __halves2bfloat162(__high2bfloat16(p0), __high2bfloat16(p1));
+      a[u] = *reinterpret_cast<const uint32_t*>(&lo);   // dims 2l, 2l+1
+      bb[u] = *reinterpret_cast<const uint32_t*>(&hi);  // dims 2l+64, 2l+65
       cs[u] = *reinterpret_cast<const float4*>(rope + (size_t)pos[u] * 64 + 2 * lane);
     }
 #pragma unroll
@@ -323,8 +331,8 @@ __global__ void __launch_bounds__(256) rope_append128_kernel(const __nv_bfloat16
       }
       const float2 x1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a[u]));
       const float2 x2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bb[u]));
-      const float y10 = x1.x * cs[u].x - x2.x * cs[u].y, y20 = x2.x * cs[u].x + x1.x * cs[u].y;
-      const float y11 = x1.y * cs[u].z - x2.y * cs[u].w, y21 = x2.y * cs[u].z + x1.y * cs[u].w;
+      const float y10 = rope_y1(x1.x, x2.x, cs[u].x, cs[u].y), y20 = rope_y2(x1.x, x2.x, cs[u].x, cs[u].y);
+      const float y11 = rope_y1(x1.y, x2.y, cs[u].z, cs[u].w), y21 = rope_y2(x1.y, x2.y, cs[u].z, cs[u].w);
       __nv_bfloat16* dst;
       if (h[u] < Hq) {
         dst = q_out + ((size_t)t[u] * Hq + h[u]) * 128;

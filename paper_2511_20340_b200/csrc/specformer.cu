@@ -392,11 +392,43 @@ static const int* taps_layers(int L, int* out4) {
 }
 
 // One attention sub-layer's "RoPE + append + attention" for rows (T, q_len, pos0) of layer `layer`.
+// bf16, head_dim 128, blocks of < 64 rows: RoPE and the paged K/V append run in the QKV GEMM's
+// epilogue (EPI_QKV_ROPE; one launch fewer per attention). Both paths rotate the same bf16-rounded
+// projections with the same operations, so the choice per T keeps every row's bits (batch
+// invariance); SF_ROPE_FUSE_T (read per call; tests) moves the threshold.
+static bool fused_rope(const sf_handle* h, int T) {
+  const char* e = getenv("SF_ROPE_FUSE_T");
+  const int thr = e ? atoi(e) : 64;
+  return h->bf && h->p.hd == 128 && T < thr;
+}
+
+// QKV projection of layer `layer` (its KV pool): fused RoPE / append, else the plain GEMM (rope later)
+static cudaError_t qkv_gemm(sf_handle* h, const void* W, int layer, int T, int q_len, const int* pos0) {
+  const Plan& p = h->p;
+  if (!fused_rope(h, T)) return gemm(h, h->xn, p.d, W, T, p.qkvw, p.d, epi_act(h->qkv, p.qkvw));
+  GemmEpi e;
+  e.mode = EPI_QKV_ROPE;
+  e.ldo = 128;
+  e.rope.pos0 = pos0;
+  e.rope.q_len = q_len;
+  e.rope.table = h->rope;
+  e.rope.Hq = p.Hq;
+  e.rope.Hkv = p.Hkv;
+  e.rope.bt = h->bt;
+  e.rope.pps = p.pps;
+  e.rope.Kp = h->kp(layer);
+  e.rope.Vp = h->vp(layer);
+  e.rope.q_out = h->qrot;
+  return gemm(h, h->xn, p.d, W, T, p.qkvw, p.d, e);
+}
+
 static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const int* pos0, int max_key) {
   const Plan& p = h->p;
   ProfScope ps(h, 1, 0.0);  // KV bytes depend on device-resident lengths: the bench computes them
-  cudaError_t e = launch_rope_append(h->bf, h->qkv, T, q_len, pos0, h->rope, p.Hq, p.Hkv, p.hd, h->bt, p.pps,
-                                     h->kp(layer), h->vp(layer), h->qrot, h->bf && p.hd == 128, h->st);
+  cudaError_t e = cudaSuccess;
+  if (!fused_rope(h, T))
+    e = launch_rope_append(h->bf, h->qkv, T, q_len, pos0, h->rope, p.Hq, p.Hkv, p.hd, h->bt, p.pps, h->kp(layer),
+                           h->vp(layer), h->qrot, h->bf && p.hd == 128, h->st);
   if (e != cudaSuccess) return e;
   AttnParams ap{};
   ap.q = h->qrot;
@@ -439,7 +471,7 @@ static cudaError_t base_forward(sf_handle* h, int T, int q_len, const int* pos0,
   for (int l = 0; l < p.L; ++l) {
     const auto& w = h->lw[l];
     if (!xn_ready && (e = rmsnorm(h, h->resid, p.d, w.attn_norm, T, h->xn, p.d))) return e;
-    if ((e = gemm(h, h->xn, p.d, w.wqkv, T, p.qkvw, p.d, epi_act(h->qkv, p.qkvw)))) return e;
+    if ((e = qkv_gemm(h, w.wqkv, l, T, q_len, pos0))) return e;
     if ((e = attn_layer(h, l, T, q_len, pos0, max_key))) return e;
     // o-proj + residual + RMS_ffn
     if (!gemm_resid_norm(h, &e, h->attn, p.ao, w.wo, T, p.d, p.ao, 1, h->resid, nullptr, h->resid, nullptr,
@@ -488,7 +520,7 @@ static cudaError_t ctx_forward(sf_handle* h, int T, int q_len, const int* pos0, 
     e = rmsnorm(h, h->ctx, p.d, h->ctx_norm, T, h->xn, p.d);
   }
   if (e) return e;
-  if ((e = gemm(h, h->xn, p.d, h->ctx_wqkv, T, p.qkvw, p.d, epi_act(h->qkv, p.qkvw)))) return e;
+  if ((e = qkv_gemm(h, h->ctx_wqkv, p.L, T, q_len, pos0))) return e;
   if ((e = attn_layer(h, p.L, T, q_len, pos0, max_key))) return e;
   // I_D = X + MSA(...)
   if (!gemm_resid_norm(h, &e, h->attn, p.ao, h->ctx_wo, T, p.d, p.ao, 1, h->ctx, nullptr, h->ctx, nullptr, nullptr))

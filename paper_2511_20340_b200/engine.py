@@ -63,13 +63,25 @@ def _interleave_gu(gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
     return torch.stack([gate, up], dim=1).reshape(2 * F, d)  # rows 2i = gate_i, 2i+1 = up_i
 
 
-def _source_tensor(name: str, w: dict) -> torch.Tensor:
-    """Map a packed-table name to the caller's canonical tensors (see synth/weights.py)."""
+def _pair_interleave_heads(W: torch.Tensor, hd: int) -> torch.Tensor:
+    """Rows of each hd-row head reordered [0, hd/2, 1, hd/2 + 1, ...] (include/specformer.h)."""
+    n = W.shape[0] // hd
+    half = hd // 2
+    idx = torch.arange(hd, device=W.device).view(2, half).t().reshape(-1)  # 0, 64, 1, 65, ...
+    return W.view(n, hd, -1)[:, idx, :].reshape(W.shape)
+
+
+def _source_tensor(name: str, w: dict, rope_pairs: int = 0) -> torch.Tensor:
+    """Map a packed-table name to the caller's canonical tensors (see synth/weights.py).
+    rope_pairs = head_dim when the RoPE'd QKV projections are pair-interleaved (bf16, hd 128)."""
     pre, _, leaf = name.rpartition(".")
     pre = pre + "." if pre else ""
     if leaf.endswith("wqkv"):
         p = pre + leaf[:-4]
-        return torch.cat([w[p + "wq"], w[p + "wk"], w[p + "wv"]], dim=0)
+        W = torch.cat([w[p + "wq"], w[p + "wk"], w[p + "wv"]], dim=0)
+        if rope_pairs and not leaf.startswith("blk_"):
+            W = _pair_interleave_heads(W, rope_pairs)
+        return W
     if leaf.endswith("w_gu"):
         p = pre + leaf[:-4]
         return _interleave_gu(w[p + "w_gate"], w[p + "w_up"])
@@ -84,8 +96,9 @@ def pack_weights(cfg: EngineConfig, weights: dict, device="cuda") -> torch.Tenso
     nbytes = lib.sf_weights_bytes(C.byref(c))
     blob = torch.empty(nbytes, dtype=torch.uint8, device=device)
     stream = torch.cuda.current_stream(device)
+    rope_pairs = cfg.head_dim if (cfg.dtype == "bf16" and cfg.head_dim == 128) else 0
     for name, shape, off, dt, layout in weight_table(cfg):
-        t = _source_tensor(name, weights)
+        t = _source_tensor(name, weights, rope_pairs)
         tdtype = torch.bfloat16 if dt == N.SF_BF16 else torch.float32
         if tuple(t.shape) != shape:
             raise ValueError(f"{name}: expected {shape}, got {tuple(t.shape)}")

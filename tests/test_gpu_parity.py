@@ -265,3 +265,20 @@ def test_attention_segments_fold(cfg, monkeypatch):
     res2 = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True, block_table=perm)
     for s1, s2 in zip(res["steps"], res2["steps"]):
         assert np.array_equal(s1["logits"], s2["logits"])
+
+
+@pytest.mark.parametrize("cfg", [MID, GQA], ids=["mha128", "gqa4"])
+def test_fused_rope_epilogue_bit_exact(cfg, monkeypatch):
+    """The QKV GEMM's fused RoPE / paged-append epilogue (small blocks) and the separate RoPE kernel
+    (large blocks) rotate the same bf16 projections with the same operations: forcing either path
+    for every block gives bit-identical logits, drafts and tokens (so choosing it per T keeps SD ==
+    AR and batch invariance)."""
+    w, prompts = setup(cfg, seed=6, jitter=0.1)
+    monkeypatch.setenv("SF_ROPE_FUSE_T", "0")
+    unfused = run_gpu(cfg, w, prompts, 12, want_logits=True)
+    monkeypatch.setenv("SF_ROPE_FUSE_T", "100000")
+    fused = run_gpu(cfg, w, prompts, 12, want_logits=True)
+    assert fused["tokens"] == unfused["tokens"]
+    for s1, s2 in zip(unfused["steps"], fused["steps"]):
+        assert np.array_equal(s1["logits"], s2["logits"])
+        assert np.array_equal(s1["draft_logits"], s2["draft_logits"])
