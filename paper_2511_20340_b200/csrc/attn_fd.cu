@@ -1,20 +1,18 @@
 // attn_fd.cu -- bf16 hybrid-mask paged decode attention (mode CAUSAL_PREFIX), flash-decoding form.
 //
-// One CTA item = (sequence b, kv head, 16-row query tile, 512-key segment); persistent CTAs walk the
-// items, so even a single sequence spreads over (heads x segments) SMs. A
-// producer warp streams the item's 128-key K/V chunks with TMA (one 2-D 128B-swizzled box per
-// (16-key page, 64-dim half)) into a 3-stage mbarrier ring. Compute warp w owns keys
-// [32w, 32w+32) of every chunk and keeps its own online-softmax state (m, l, O[16x128]) across
-// the chunks -- no cross-warp synchronisation per chunk, P never leaves registers:
-//   S = Q K_w^T (mma.sync m16n8k16 bf16 -> fp32), masked (key <= row position), m_new = max,
-//   O = O e^(m_old - m_new) + P V_w,  l = l e^(m_old - m_new) + sum P.
-// At the end of the item the 4 warp states are merged in the fixed order w = 0..3 into the
-// segment's unnormalised (M, L, acc). A row whose keys span one segment is normalised directly;
-// otherwise each segment is written to the partial buffer and the CTA that completes the last
-// segment of the (b, kv head, tile) group (arrival counter) merges segments 0, 1, ... in order:
-// out = sum_s acc_s 2^(M_s - M) / sum_s L_s 2^(M_s - M) -- for one segment exactly acc / L.
-// Every row's arithmetic (chunk and segment boundaries at fixed absolute key positions, per-warp
-// key slices, merge orders) is independent of batch size and block length (batch invariance, C23).
+// Work: (sequence b, kv head, 16-row query tile) groups. Keys are cut into fixed SEG-key segments
+// (absolute positions) and the arithmetic is defined segment-wise:
+//   per segment s and warp w: an online softmax over w's 32-key slice of each of the segment's
+//     128-key chunks, starting fresh -> (m, l, O)_{s,w}   (S = Q K^T and O += P V by mma.sync bf16,
+//     masked keys excluded, P kept in registers);
+//   per warp: fold the segment states in order s = 0, 1, ...: M = max, f = 2^(m - M),
+//     l = l_a f_a + l_b f_b, O = O_a f_a + O_b f_b (explicitly rounded products);
+//   across warps: the same merge in the fixed order w = 0..3, then out = acc / L.
+// Two schedules compute exactly this (bit-identical results): a CTA per group walking all its
+// segments (folds in registers; large batches), or a CTA per (group, segment) for small batches,
+// which publishes its four warp states; the CTA completing a group's last segment (arrival
+// counter) folds them and merges. A producer warp streams the chunks with TMA into a 3-stage ring.
+// Every row's arithmetic depends only on its own keys (batch invariance, C23).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -74,7 +72,8 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
                                                         const __grid_constant__ CUtensorMap tmV,
                                                         const __grid_constant__ CUtensorMap tmK4,
                                                         const __grid_constant__ CUtensorMap tmV4, AttnParams p,
-                                                        int ntiles, int nseg_max, int seg_keys, int n_items) {
+                                                        int ntiles, int nseg_max, int seg_keys, int n_items,
+                                                        int split) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   const uint32_t raw = smem_u32(sm_raw);
   uint8_t* sm = sm_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -98,7 +97,7 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
   const int seg_ch = seg_keys / CH;
   auto item_of = [&](int idx, Item& it) {
     int r = idx % n_groups;
-    it.seg = idx / n_groups;
+    it.seg = split ? idx / n_groups : 0;
     it.qt = r % ntiles;
     r /= ntiles;
     it.kvh = r % p.Hkv;
@@ -108,8 +107,8 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
     const int kmax = min(p.pos0[it.b] + min(p.q_len - 1, (r0 + nr - 1) / G), p.max_key - 1);
     const int nch = kmax / CH + 1;
     it.nseg = (nch + seg_ch - 1) / seg_ch;
-    it.c0 = it.seg * seg_ch;
-    it.c1 = min(nch, it.c0 + seg_ch);  // empty when seg >= nseg
+    it.c0 = split ? it.seg * seg_ch : 0;
+    it.c1 = split ? min(nch, it.c0 + seg_ch) : nch;  // empty when seg >= nseg
     return kmax;
   };
 
@@ -217,8 +216,40 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
     for (int nt = 0; nt < 16; ++nt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) o[nt][i] = 0.f;
+    // this warp's fold of its finished segments (starts empty: fold(empty, x) == x exactly)
+    float tm_lo = -INFINITY, tm_hi = -INFINITY, tl_lo = 0.f, tl_hi = 0.f;
+    float to[16][4];
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) to[nt][i] = 0.f;
+    auto fold_segment = [&]() {
+      const float M_lo = fmaxf(tm_lo, m_lo), M_hi = fmaxf(tm_hi, m_hi);
+      const float ft_lo = (tm_lo == -INFINITY) ? 0.f : exp2f(tm_lo - M_lo);
+      const float fc_lo = (m_lo == -INFINITY) ? 0.f : exp2f(m_lo - M_lo);
+      const float ft_hi = (tm_hi == -INFINITY) ? 0.f : exp2f(tm_hi - M_hi);
+      const float fc_hi = (m_hi == -INFINITY) ? 0.f : exp2f(m_hi - M_hi);
+      tl_lo = __fadd_rn(__fmul_rn(tl_lo, ft_lo), __fmul_rn(l_lo, fc_lo));
+      tl_hi = __fadd_rn(__fmul_rn(tl_hi, ft_hi), __fmul_rn(l_hi, fc_hi));
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt) {
+        to[nt][0] = __fadd_rn(__fmul_rn(to[nt][0], ft_lo), __fmul_rn(o[nt][0], fc_lo));
+        to[nt][1] = __fadd_rn(__fmul_rn(to[nt][1], ft_lo), __fmul_rn(o[nt][1], fc_lo));
+        to[nt][2] = __fadd_rn(__fmul_rn(to[nt][2], ft_hi), __fmul_rn(o[nt][2], fc_hi));
+        to[nt][3] = __fadd_rn(__fmul_rn(to[nt][3], ft_hi), __fmul_rn(o[nt][3], fc_hi));
+      }
+      tm_lo = M_lo;
+      tm_hi = M_hi;
+      m_lo = m_hi = -INFINITY;
+      l_lo = l_hi = 0.f;
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[nt][i] = 0.f;
+    };
 
     for (int c = it.c0; c < it.c1; ++c, ++seq) {
+      if (c != it.c0 && c % seg_ch == 0) fold_segment();  // segment boundary (group schedule)
       const int st = seq % NST;
       mbar_wait(&full[st], (uint32_t)(seq / NST) & 1u);
       const uint32_t kb = sbase + st * STAGE_BYTES, vb = kb + KV_BYTES;
@@ -313,22 +344,109 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
       if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
     }
     const unsigned long long ti1 = g_kt.rec ? kt_now() : 0ull;
-    // ---- merge the 4 warp states in fixed order and normalise
-    if (g < nr) {  // (rows of the tile past the block's rows are never read)
+    fold_segment();
+    const int group = (it.b * p.Hkv + it.kvh) * ntiles + it.qt;
+    auto row_slot = [&](int r) {  // (token, head) of tile row r
+      const int rr = r0 + r, qi = rr / G, h = it.kvh * G + rr % G;
+      return (size_t)(it.b * p.q_len + qi) * p.Hq + h;
+    };
+    if (split && it.nseg > 1) {
+      // ---- segment schedule: publish this segment's four warp states
+      auto pub = [&](int r, int hsel) {
+        const size_t base = (row_slot(r) * p.nchunk_max + it.seg) * 4 + warp;
 #pragma unroll
-      for (int nt = 0; nt < 16; ++nt)
-        *reinterpret_cast<float2*>(mrg + (warp * 16 + g) * HD + nt * 8 + 2 * t4) = make_float2(o[nt][0], o[nt][1]);
-    }
-    if (g + 8 < nr) {
+        for (int nt = 0; nt < 16; ++nt)
+          *reinterpret_cast<float2*>(p.part_o + base * HD + nt * 8 + 2 * t4) =
+              make_float2(to[nt][2 * hsel], to[nt][2 * hsel + 1]);
+        if (t4 == 0) {
+          p.part_ml[2 * base] = hsel ? tm_hi : tm_lo;
+          p.part_ml[2 * base + 1] = hsel ? tl_hi : tl_lo;
+        }
+      };
+      if (g < nr) pub(g, 0);
+      if (g + 8 < nr) pub(g + 8, 1);
+      named_bar(1, 128);
+      if (tid == 0) {
+        int prev;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(p.seg_cnt + group) : "memory");
+        mrg_flag[0] = prev == it.nseg - 1;
+        if (prev == it.nseg - 1) p.seg_cnt[group] = 0;  // re-arm for the next launch
+      }
+      named_bar(1, 128);
+      if (!mrg_flag[0]) continue;
+      // the group's last segment: fold every warp slot's segment states in segment order (the same
+      // operations as the in-register fold). Step factors per (warp, row) first (one thread each),
+      // then every thread (one dimension) streams the O values, all segments of 4 (warp, row)
+      // pairs in flight at a time.
+      constexpr int SMAX = 8;
+      float* fa_s = mrg;                   // [4][16][SMAX] factor of the running state, then
+      float* fb_s = mrg + 4 * 16 * SMAX;   // of segment s; the O fold overwrites mrg[] afterwards
+      const int nsg = min(it.nseg, SMAX);
+      if (tid < 4 * nr) {
+        const int w = tid / nr, r = tid % nr;
+        const size_t s0 = row_slot(r) * p.nchunk_max;
+        float m = -INFINITY, l = 0.f;
+        for (int sg = 0; sg < nsg; ++sg) {
+          const size_t bs = (s0 + sg) * 4 + w;
+          const float ms = __ldcg(&p.part_ml[2 * bs]), ls = __ldcg(&p.part_ml[2 * bs + 1]);
+          const float M = fmaxf(m, ms);
+          const float fa = (m == -INFINITY) ? 0.f : exp2f(m - M);
+          const float fb = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
+          l = __fadd_rn(__fmul_rn(l, fa), __fmul_rn(ls, fb));
+          m = M;
+          fa_s[(w * 16 + r) * SMAX + sg] = fa;
+          fb_s[(w * 16 + r) * SMAX + sg] = fb;
+        }
+        mrg_m[w * 16 + r] = m;
+        mrg_l[w * 16 + r] = l;
+      }
+      named_bar(1, 128);
+      float Ofold[64];  // (warp, row) pairs x this thread's dimension d = tid
+      for (int q0 = 0; q0 < 4 * nr; q0 += 4) {
+        float Os[4][SMAX];
 #pragma unroll
-      for (int nt = 0; nt < 16; ++nt)
-        *reinterpret_cast<float2*>(mrg + (warp * 16 + g + 8) * HD + nt * 8 + 2 * t4) = make_float2(o[nt][2], o[nt][3]);
-    }
-    if (t4 == 0) {
-      mrg_m[warp * 16 + g] = m_lo;
-      mrg_m[warp * 16 + g + 8] = m_hi;
-      mrg_l[warp * 16 + g] = l_lo;
-      mrg_l[warp * 16 + g + 8] = l_hi;
+        for (int j = 0; j < 4; ++j) {
+          const int q = min(q0 + j, 4 * nr - 1), w = q / nr, r = q % nr;
+          const size_t s0 = row_slot(r) * p.nchunk_max;
+#pragma unroll
+          for (int sg = 0; sg < SMAX; ++sg)
+            Os[j][sg] = (sg < nsg) ? __ldcg(&p.part_o[((s0 + sg) * 4 + w) * HD + tid]) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int q = min(q0 + j, 4 * nr - 1), w = q / nr, r = q % nr;
+          float O = 0.f;
+#pragma unroll
+          for (int sg = 0; sg < SMAX; ++sg)
+            if (sg < nsg)
+              O = __fadd_rn(__fmul_rn(O, fa_s[(w * 16 + r) * SMAX + sg]), __fmul_rn(Os[j][sg], fb_s[(w * 16 + r) * SMAX + sg]));
+          if (q0 + j < 4 * nr) Ofold[q0 + j] = O;
+        }
+      }
+      named_bar(1, 128);  // factors consumed before mrg[] is overwritten
+      for (int q = 0; q < 4 * nr; ++q) {
+        const int w = q / nr, r = q % nr;
+        mrg[(w * 16 + r) * HD + tid] = Ofold[q];
+      }
+    } else {
+      // ---- merge the 4 warp states in fixed order and normalise
+      if (g < nr) {  // (rows of the tile past the block's rows are never read)
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt)
+          *reinterpret_cast<float2*>(mrg + (warp * 16 + g) * HD + nt * 8 + 2 * t4) = make_float2(to[nt][0], to[nt][1]);
+      }
+      if (g + 8 < nr) {
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt)
+          *reinterpret_cast<float2*>(mrg + (warp * 16 + g + 8) * HD + nt * 8 + 2 * t4) =
+              make_float2(to[nt][2], to[nt][3]);
+      }
+      if (t4 == 0) {
+        mrg_m[warp * 16 + g] = tm_lo;
+        mrg_m[warp * 16 + g + 8] = tm_hi;
+        mrg_l[warp * 16 + g] = tl_lo;
+        mrg_l[warp * 16 + g + 8] = tl_hi;
+      }
     }
     named_bar(1, 128);
     // per-row merge factors once (row r: thread r): M = max_w m_w, f_w = 2^(m_w - M), L = sum_w l_w f_w
@@ -349,55 +467,12 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
       mrg_l[16 + r] = M;
     }
     named_bar(1, 128);
-    const int group = (it.b * p.Hkv + it.kvh) * ntiles + it.qt;
     for (int e = tid; e < nr * HD; e += 128) {
       const int r = e / HD, d = e % HD;
       float acc = 0.f;
 #pragma unroll
       for (int w = 0; w < 4; ++w) acc += mrg[(w * 16 + r) * HD + d] * mrg_m[w * 16 + r];
-      const float L = mrg_l[r];
-      const int rr = r0 + r, qi = rr / G, h = it.kvh * G + rr % G;
-      const int t = it.b * p.q_len + qi;
-      if (it.nseg == 1) {
-        reinterpret_cast<__nv_bfloat16*>(p.out)[((size_t)t * p.Hq + h) * HD + d] = __float2bfloat16_rn(acc / L);
-      } else {
-        const size_t slot = ((size_t)t * p.Hq + h) * p.nchunk_max + it.seg;
-        p.part_o[slot * HD + d] = acc;
-        if (d == 0) {
-          p.part_ml[2 * slot] = mrg_l[16 + r];
-          p.part_ml[2 * slot + 1] = L;
-        }
-      }
-    }
-    if (it.nseg > 1) {
-      // one gpu-scope release per item (cumulative over the compute warps' partial writes, which
-      // the CTA barrier orders before it) instead of a fence in every thread
-      named_bar(1, 128);
-      if (tid == 0) {
-        int prev;
-        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(p.seg_cnt + group) : "memory");
-        mrg_flag[0] = prev == it.nseg - 1;
-      }
-      named_bar(1, 128);
-      if (mrg_flag[0]) {  // every segment of the group has landed: merge them in segment order
-        for (int e = tid; e < nr * HD; e += 128) {
-          const int r = e / HD, d = e % HD;
-          const int rr = r0 + r, qi = rr / G, h = it.kvh * G + rr % G;
-          const int t = it.b * p.q_len + qi;
-          const size_t s0 = ((size_t)t * p.Hq + h) * p.nchunk_max;
-          float M = -INFINITY;
-          for (int sg = 0; sg < it.nseg; ++sg) M = fmaxf(M, __ldcg(&p.part_ml[2 * (s0 + sg)]));
-          float L = 0.f, acc = 0.f;
-          for (int sg = 0; sg < it.nseg; ++sg) {
-            const float ms = __ldcg(&p.part_ml[2 * (s0 + sg)]);
-            const float f = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
-            L += __ldcg(&p.part_ml[2 * (s0 + sg) + 1]) * f;
-            acc += __ldcg(&p.part_o[(s0 + sg) * HD + d]) * f;
-          }
-          reinterpret_cast<__nv_bfloat16*>(p.out)[((size_t)t * p.Hq + h) * HD + d] = __float2bfloat16_rn(acc / L);
-        }
-        if (tid == 0) p.seg_cnt[group] = 0;  // re-arm for the next launch
-      }
+      reinterpret_cast<__nv_bfloat16*>(p.out)[row_slot(r) * HD + d] = __float2bfloat16_rn(acc / mrg_l[r]);
     }
     named_bar(1, 128);
     if (tid == 0 && g_kt.rec) kt_item((uint32_t)(it.seg | (it.nseg << 8) | ((it.c1 - it.c0) << 16)), ti0, ti1, kt_now());
@@ -460,7 +535,13 @@ cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
   const int seg_keys = (env_seg >= CH && env_seg % CH == 0) ? env_seg : kAttnSeg;
   const int nseg_max = (p.max_key + seg_keys - 1) / seg_keys;
   if (nseg_max > p.nchunk_max || !p.seg_cnt) return cudaErrorInvalidValue;
-  const int n_items = p.B * p.Hkv * ntiles * nseg_max;
+  // schedule (the arithmetic is the same): a CTA per (group, segment) when the groups alone would
+  // leave most SMs idle, else a CTA per group folding its segments in registers
+  const int n_groups = p.B * p.Hkv * ntiles;
+  const char* env_split = getenv("SF_ATTN_SPLIT");  // tests force either schedule
+  const int split = (nseg_max > 1 && nseg_max <= 8) &&  // (the publishing fold holds <= 8 segments)
+                    (env_split ? atoi(env_split) > 0 : 2 * n_groups <= num_sms);
+  const int n_items = split ? n_groups * nseg_max : n_groups;
   const int grid = std::min(n_items, num_sms);
   CUtensorMap mk, mv;
   const long long rows = (long long)p.n_pages * p.Hkv * 16;
@@ -468,7 +549,8 @@ cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
   if (!encode_kv_map(&mk, p.Kp, rows) || !encode_kv_map(&mv, p.Vp, rows)) return cudaErrorInvalidValue;
   if (!encode_kv_map4(&mk4, p.Kp, p.Hkv, p.n_pages) || !encode_kv_map4(&mv4, p.Vp, p.Hkv, p.n_pages))
     return cudaErrorInvalidValue;
-  launch_k(attn_fd_kernel, dim3(grid), dim3(160), SMEM, s, mk, mv, mk4, mv4, p, ntiles, nseg_max, seg_keys, n_items);
+  launch_k(attn_fd_kernel, dim3(grid), dim3(160), SMEM, s, mk, mv, mk4, mv4, p, ntiles, nseg_max, seg_keys, n_items,
+           split);
   return cudaGetLastError();
 }
 

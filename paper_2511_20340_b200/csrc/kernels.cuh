@@ -15,8 +15,8 @@ struct AttnParams {
   int q_len;                 // query rows per sequence (rows b*q_len + i at pos0[b] + i)
   int B, Hq, Hkv, hd;
   int nchunk_max;            // partial-buffer capacity in 128-key chunks
-  float* part_o;             // [T, Hq, nchunk_max, hd]
-  float* part_ml;            // [T, Hq, nchunk_max, 2]
+  float* part_o;             // [T, Hq, nchunk_max, 4, hd] (flash-decoding: per segment and warp slot)
+  float* part_ml;            // [T, Hq, nchunk_max, 4, 2]
   void* out;                 // [T, Hq*hd] act dtype
   int max_key;               // upper bound of pos0[b] + q_len (grid sizing), <= max_seq
   int n_pages;               // pages in the pool (TMA tensor-map extent)
@@ -24,7 +24,7 @@ struct AttnParams {
 };
 
 constexpr int kAttnChunk = 128;  // fixed absolute key-chunk size (split-KV boundaries, C23)
-constexpr int kAttnSeg = 2048;   // flash-decoding key segment: one work item (fixed absolute bounds)
+constexpr int kAttnSeg = 2048;   // flash-decoding key segment (fixed absolute bounds; defines the arithmetic)
 
 // act dtype: bf16 (is_bf16) or fp32.
 cudaError_t launch_rope_table(float2* table, int max_seq, int hd, float theta, cudaStream_t s);

@@ -170,8 +170,8 @@ Plan make_plan(const sf_config* c) {
   p.o_hlast = take((int64_t)p.B * p.d * 4);
   p.o_logits = take((int64_t)p.rows_v * p.V * 4);
   p.o_dlogits = take((int64_t)p.rows_d * p.V * 4);
-  p.o_apo = take((int64_t)p.R * p.Hq * p.nchunk * p.hd * 4);
-  p.o_apml = take((int64_t)p.R * p.Hq * p.nchunk * 2 * 4);
+  p.o_apo = take((int64_t)p.R * p.Hq * p.nchunk * 4 * p.hd * 4);
+  p.o_apml = take((int64_t)p.R * p.Hq * p.nchunk * 4 * 2 * 4);
   // split-KV arrival counters: one per (sequence, kv head, 16-row query tile) at the longest block
   p.n_acnt = (int64_t)p.B * p.Hkv * ((std::max(p.k + 1, p.C_pf) * (p.Hq / p.Hkv) + 15) / 16);
   p.o_acnt = take(p.n_acnt * 4);

@@ -282,3 +282,20 @@ def test_fused_rope_epilogue_bit_exact(cfg, monkeypatch):
     for s1, s2 in zip(unfused["steps"], fused["steps"]):
         assert np.array_equal(s1["logits"], s2["logits"])
         assert np.array_equal(s1["draft_logits"], s2["draft_logits"])
+
+
+@pytest.mark.parametrize("cfg", [MID, GQA], ids=["mha128", "gqa4"])
+def test_attention_schedules_bit_exact(cfg, monkeypatch):
+    """The two flash-decoding schedules -- a CTA per (group, segment) that publishes its warp states
+    (small batches) and a CTA per group folding its segments in registers (large batches) -- compute
+    the same per-segment / per-warp folds: bit-identical logits and tokens with both forced."""
+    monkeypatch.setenv("SF_ATTN_SEG", "128")
+    w, prompts = setup(cfg, seed=8, jitter=0.1)
+    monkeypatch.setenv("SF_ATTN_SPLIT", "1")
+    a = run_gpu(cfg, w, prompts, 12, want_logits=True)
+    monkeypatch.setenv("SF_ATTN_SPLIT", "0")
+    b = run_gpu(cfg, w, prompts, 12, want_logits=True)
+    assert a["tokens"] == b["tokens"]
+    for s1, s2 in zip(a["steps"], b["steps"]):
+        assert np.array_equal(s1["logits"], s2["logits"])
+        assert np.array_equal(s1["draft_logits"], s2["draft_logits"])
