@@ -155,7 +155,9 @@ def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
 
-    from paper_2511_20340_b200 import Engine, EngineConfig, dp, roofline
+    import numpy as np
+
+    from paper_2511_20340_b200 import Engine, EngineConfig, dp, roofline, timeline
     from paper_2511_20340_b200 import _native as N
     from synth import make_prompts, make_weights
 
@@ -174,7 +176,7 @@ def run_ours(args, cfg):
     # capacity: every phase restarts from a prefill; a decode_steps call of n steps needs n (k + 1)
     # positions of headroom over the actual length (a ~= 1 with random weights, so lengths grow ~1 per step)
     GEN_CHUNK = 16
-    grow = max(W + K * (k + 1), W + K + Kp * (k + 1), Ke + k + 1)
+    grow = max(W + K * (k + 1), W + K + (args.timeline_steps + Kp) * (k + 1), Ke + k + 1)
     if Kf:
         grow = max(grow, n_cont + GEN_CHUNK * (k + 1), (W + Kf) * (k + 1))
     max_seq = (P + grow + 32 + 15) // 16 * 16
@@ -215,8 +217,56 @@ def run_ours(args, cfg):
     steps_per_s = K / (ms_max / 1e3)
     a_meas = tokens / (K * B)
 
-    # ---------------- roofline: per-class kernel durations from a profiled eager pass
+    # ---------------- whole-step roofline over the timed (graph) region, lengths from the accept log
+    lens_t = before.tolist()
+    accs_t = acc_log.cpu().tolist()
+    sb = 0.0
+    prev_t = prev_before.tolist()
+    for s in range(K):
+        sb += roofline.step_bytes(cfg, B, k, lens_t, prev_t)
+        prev_t = list(lens_t)
+        lens_t = [n + m + 1 for n, m in zip(lens_t, accs_t[s])]
+    step_gbs = sb / (ms / 1e3) / 1e9
+
+    def replay_lengths(lens0, prev0, accs):
+        """algorithmic KV bytes / step bytes / step flops of the steps whose accept rows are accs"""
+        lens, prevs, kv, by, fl = list(lens0), list(prev0), 0.0, 0.0, 0.0
+        for a in accs:
+            kv += roofline.attention_kv_bytes(cfg, lens, prevs, k)
+            by += roofline.step_bytes(cfg, B, k, lens, prevs)
+            fl += roofline.step_flops(cfg, B, k, lens)
+            prevs = list(lens)
+            lens = [n + m + 1 for n, m in zip(lens, a)]
+        return kv, by, fl
+
+    # ---------------- kernel timeline: Kt replays of the timed step graph with the per-CTA
+    # %globaltimer probes switched on; the step's critical path is attributed to kernel classes
     hbm, tf_burst, tf_sust, peak_src = peaks()
+    Kt = args.timeline_steps
+    tl = None
+    if Kt > 0 and N.lib().sf_debug_ktrace_enable(1) == 0:
+        lt0 = eng.capture(3, (B,), torch.int32).cpu().tolist()
+        pt0 = eng.capture(5, (B,), torch.int32).cpu().tolist()
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0e.record(eng.stream)
+        eng.decode_steps(Kt, None, acc_log)  # the same graph the timed window replayed
+        t1e.record(eng.stream)
+        eng.sync()
+        buf = np.zeros(1 << 21, dtype=timeline.REC)
+        n_rec = N.lib().sf_debug_ktrace(C.c_void_p(buf.ctypes.data), buf.size)
+        N.lib().sf_debug_ktrace_enable(0)
+        cp = timeline.critical_path(buf[:n_rec], key=timeline.kclass)
+        kv_t, _, _ = replay_lengths(lt0, pt0, acc_log[:Kt].cpu().tolist())
+        tl = {"steps": Kt, "cta_records": int(n_rec), "events_ms_per_step": t0e.elapsed_time(t1e) / Kt,
+              "span_ms_per_step": cp["span_us"] / 1e3 / Kt, "idle_gap_ms_per_step": cp["gap_us"] / 1e3 / Kt,
+              "classes": {c: {"exposed_ms_per_step": cp["exposed"][c] / 1e3 / Kt,
+                              "launches_per_step": cp["count"][c] / Kt,
+                              "share_of_step": cp["exposed"][c] / max(1e-9, cp["span_us"])}
+                          for c in cp["exposed"]},
+              "attention_kv_bytes": kv_t}
+
+    # ---------------- per-class CUDA-event times: the step graph re-captured with an event-record
+    # node around every launch (Kp replays); also gives the host-known GEMM bytes per launch
     lens0 = eng.capture(3, (B,), torch.int32).cpu().tolist()
     prev0 = eng.capture(5, (B,), torch.int32).cpu().tolist()  # context layer runs at n_prev
     acc_p = torch.zeros(Kp, B, dtype=torch.int32, device="cuda")
@@ -229,49 +279,51 @@ def run_ours(args, cfg):
     prof_ms_total = ep0.elapsed_time(ep1)
     cls = {c: eng.profile_read(c) for c in range(4)}
     eng.profile(False)
-    accs = acc_p.cpu().tolist()
-    # reconstruct per-step lengths: verify at n_b, context layer at the previous n_b
-    lens, prevs = list(lens0), list(prev0)
-    attn_bytes = 0.0
-    step_bytes_tot = 0.0
-    step_flops_tot = 0.0
-    for s in range(Kp):
-        ctx_lens = prevs
-        attn_bytes += roofline.attention_kv_bytes(cfg, lens, ctx_lens, k)
-        step_bytes_tot += roofline.step_bytes(cfg, B, k, lens, ctx_lens)
-        step_flops_tot += roofline.step_flops(cfg, B, k, lens)
-        prevs = list(lens)
-        lens = [n + m + 1 for n, m in zip(lens, accs[s])]
+    attn_bytes, step_bytes_tot, step_flops_tot = replay_lengths(lens0, prev0, acc_p.cpu().tolist())
     gemm_ms, gemm_n, gemm_bytes = cls[0]
     attn_ms, attn_n, _ = cls[1]
-    # GEMM FLOPs of the profiled steps (2 T N K summed over the step's contractions)
-    gemm_flops = 0.0
+    # GEMM FLOPs of one step (2 T N K summed over the step's contractions)
     d_, F_, V_ = cfg.d_model, cfg.d_ff, cfg.vocab
     qkv_ = (cfg.n_heads + 2 * cfg.n_kv_heads) * cfg.head_dim
     ao_ = cfg.n_heads * cfg.head_dim
     Tv, Td = B * (k + 1), B * k
     per_layer = qkv_ * d_ + d_ * ao_ + 2 * F_ * d_ + d_ * F_
-    gemm_flops = 2.0 * Kp * (Tv * (cfg.n_layers * per_layer + V_ * d_)
+    gemm_flops_step = 2.0 * (Tv * (cfg.n_layers * per_layer + V_ * d_)
                              + Tv * (4 * d_ * d_ + qkv_ * d_ + d_ * ao_)
                              + B * k * d_ * d_ + Td * (qkv_ * d_ + d_ * ao_ + 3 * F_ * d_ + V_ * d_))
-    dominant = "gemm" if gemm_ms >= attn_ms else "attention"
+    gemm_bytes_step = gemm_bytes / max(1, Kp)
+    gemm_n_step = gemm_n / max(1, Kp)
+    # the dominant class and its per-launch duration: from the timeline (graph replay, PDL overlap
+    # intact, exposed critical-path time per launch) when it ran, else from the event-node graph
+    if tl is not None:
+        ex = {c: tl["classes"].get(c, {}).get("exposed_ms_per_step", 0.0) for c in ("gemm", "attention")}
+        dominant = "gemm" if ex["gemm"] >= ex["attention"] else "attention"
+        n_dom = tl["classes"][dominant]["launches_per_step"]
+        dom_ms = ex[dominant] / max(1e-9, n_dom)
+        dur_source = "kernel timeline: exposed critical-path time per launch over graph replays"
+        attn_bytes_step = tl["attention_kv_bytes"] / Kt
+    else:
+        dominant = "gemm" if gemm_ms >= attn_ms else "attention"
+        n_dom = (gemm_n if dominant == "gemm" else attn_n) / max(1, Kp)
+        dom_ms = (gemm_ms if dominant == "gemm" else attn_ms) / max(1, Kp) / max(1e-9, n_dom)
+        dur_source = "CUDA event-record nodes around each launch (no PDL overlap)"
+        attn_bytes_step = attn_bytes / max(1, Kp)
     if dominant == "gemm":
-        t_hbm = gemm_bytes / (hbm * 1e9)
-        t_tc = gemm_flops / (tf_sust * 1e12)
+        t_hbm = gemm_bytes_step / (hbm * 1e9)
+        t_tc = gemm_flops_step / (tf_sust * 1e12)
         if t_tc > t_hbm:  # compute-bound at this batch: judge against the sustained bf16 peak
-            bound, unit, achieved, peak_v = "tensor", "TFLOP/s", gemm_flops / (gemm_ms / 1e3) / 1e12, tf_sust
+            bound, unit, peak_v = "tensor", "TFLOP/s", tf_sust
             peak_src = peak_src + " (bf16_tflops_sustained: kernel timed inside the step)"
-            dom_units = gemm_flops
+            dom_units = gemm_flops_step / max(1e-9, n_dom)
+            achieved = dom_units / (dom_ms / 1e3) / 1e12
         else:
-            bound, unit, achieved, peak_v = "hbm", "GB/s", gemm_bytes / (gemm_ms / 1e3) / 1e9, hbm
-            dom_units = gemm_bytes
-        dom_bytes_per_launch = dom_units / max(1, gemm_n)
-        dom_ms = gemm_ms / max(1, gemm_n)
+            bound, unit, peak_v = "hbm", "GB/s", hbm
+            dom_units = gemm_bytes_step / max(1e-9, n_dom)
+            achieved = dom_units / (dom_ms / 1e3) / 1e9
     else:
         bound, unit, peak_v = "hbm", "GB/s", hbm
-        achieved = attn_bytes / (attn_ms / 1e3) / 1e9
-        dom_bytes_per_launch = attn_bytes / max(1, attn_n)
-        dom_ms = attn_ms / max(1, attn_n)
+        dom_units = attn_bytes_step / max(1e-9, n_dom)
+        achieved = dom_units / (dom_ms / 1e3) / 1e9
     # DRAM bytes per launch of the dominant kernel class from the committed ncu launch list of this
     # command at this batch (profiles/ncu_traffic.json, written by tools/profile_summary.py)
     traffic = None
@@ -285,18 +337,8 @@ def run_ours(args, cfg):
                            cls[c][0] / max(1e-9, prof_ms_total)}
                     for c, name in enumerate(["gemm", "attention", "norm", "argmax"])}
     prof_classes["gemm"]["achieved_gbs"] = gemm_bytes / max(1e-12, gemm_ms / 1e3) / 1e9
-    prof_classes["gemm"]["achieved_tflops"] = gemm_flops / max(1e-12, gemm_ms / 1e3) / 1e12
+    prof_classes["gemm"]["achieved_tflops"] = gemm_flops_step * Kp / max(1e-12, gemm_ms / 1e3) / 1e12
     prof_classes["attention"]["achieved_gbs"] = attn_bytes / max(1e-12, attn_ms / 1e3) / 1e9
-    # whole-step roofline over the timed (graph) region, lengths reconstructed from the accept log
-    lens_t = before.tolist()
-    accs_t = acc_log.cpu().tolist()
-    sb = 0.0
-    prev_t = prev_before.tolist()
-    for s in range(K):
-        sb += roofline.step_bytes(cfg, B, k, lens_t, prev_t)
-        prev_t = list(lens_t)
-        lens_t = [n + m + 1 for n, m in zip(lens_t, accs_t[s])]
-    step_gbs = sb / (ms / 1e3) / 1e9
 
     # ---------------- e2e: public C-ABI calls with pinned HOST buffers, copies inside the region
     lib = eng.lib
@@ -403,8 +445,9 @@ def run_ours(args, cfg):
             "a_paper": A_PAPER.get(cfg.name),
             "roofline": {"bound": bound, "kernel": dominant, "achieved": achieved, "peak": peak_v, "unit": unit,
                          "frac": achieved / peak_v, "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_units_per_launch": dom_bytes_per_launch, "ms_per_launch": dom_ms,
-                         "classes": prof_classes, "profiled_steps": Kp},
+                         "algorithmic_units_per_launch": dom_units, "ms_per_launch": dom_ms,
+                         "launches_per_step": n_dom, "duration_source": dur_source,
+                         "timeline": tl, "event_classes": prof_classes, "event_profiled_steps": Kp},
             "step_roofline": {"bound": "hbm", "achieved": step_gbs, "peak": hbm, "unit": "GB/s",
                               "frac": step_gbs / hbm, "bytes_per_step": sb / K,
                               "flops_per_step": step_flops_tot / max(1, Kp),
@@ -437,6 +480,7 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = the config's generation length - 1")
     ap.add_argument("--forced-steps", type=int, default=32)
+    ap.add_argument("--timeline-steps", type=int, default=2, help="graph steps replayed with the kernel timeline on")
     ap.add_argument("--draft-len", type=int, default=None, help="override k (13B sweep: 4 / 6 / 8)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -163,8 +163,11 @@ sf_status sf_debug_force_drafts(sf_handle* h, const int32_t* cont_dev, int32_t c
  * cont_dev NULL disables. Device pointers must stay valid while enabled. */
 sf_status sf_set_forced_drafts(sf_handle* h, const int32_t* cont_dev, int32_t cont_len, const int32_t* corrupt_dev,
                                int32_t corrupt_steps);
-/* Per-kernel-class profiling for the bench roofline: when enabled, every eager launch is bracketed
- * by CUDA events on the handle's stream (decode_steps then runs eagerly, not from a graph).
+/* Per-kernel-class profiling for the bench roofline: when enabled, every launch is bracketed by
+ * CUDA events on the handle's stream. With SF_FLAG_CUDA_GRAPH, decode_steps captures a profiling
+ * copy of the step graph whose event records are graph nodes (cudaEventRecordExternal) and replays
+ * it one step at a time, so the times carry no host launch gaps (a record node between two launches
+ * does remove their programmatic overlap); without the flag the launches are eager.
  * Classes: 0 GEMM, 1 paged attention (RoPE/append + partial + combine), 2 RMSNorm/embedding,
  * 3 argmax. sf_profile(h, 1) clears and enables; sf_profile_read sums the elapsed milliseconds,
  * launch count and host-known algorithmic bytes (GEMM: weights + activations + outputs; 0 for
@@ -192,6 +195,11 @@ int32_t sf_debug_gemm_trace(uint64_t* dst_host, int32_t cap);
  * host memory dst_host (cap records). Synchronises the device. Returns the number of records
  * copied, 0 if tracing is off. */
 int32_t sf_debug_ktrace(void* dst_host, int32_t cap);
+/* Turn the kernel timeline on (1) or off (0) at run time (bench.py's timeline pass; SF_KTRACE=1
+ * turns it on at the first handle). Takes effect for launches -- graph replays included -- made
+ * after the call: the probes read a device-global record pointer, null when off. Synchronises
+ * the device and clears the log. Returns 0, or -1 if the 80 MB log cannot be allocated. */
+int32_t sf_debug_ktrace_enable(int32_t on);
 
 #ifdef __cplusplus
 }

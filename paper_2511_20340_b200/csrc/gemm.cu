@@ -56,11 +56,37 @@ SF_DEV float silu_f(float g) { return g / (1.f + expf(-g)); }
 // Warps: 0 = TMA producer, 1 = MMA issuer (leader CTA), 2 = TMEM allocator, 4..7 = epilogue.
 // Two TMEM accumulator buffers (when they fit) overlap the epilogue of one segment with the MMAs
 // of the next.
+// Stream-K partition with a tile-entry cost. Group g of G owns the units [sk_begin(g), sk_begin(g+1))
+// of the n_tiles x kb (tile, k-block) sequence. Every tile is preceded by `drain` virtual units --
+// the MMA stall a group pays when its range enters a new tile after finishing another one (the
+// accumulator's epilogue must drain TMEM first; one TMEM buffer at T > 256) -- and the virtual
+// sequence is cut evenly, so a range that crosses a tile boundary gets fewer real units. The cut
+// depends on (n_tiles, kb, G, drain) only: the same k segmentation at every T (batch invariance).
+__host__ __device__ inline long long sk_real(long long v, int kb, int drain) {
+  const long long t = v / (kb + drain), o = v % (kb + drain);
+  return t * kb + (o > drain ? o - drain : 0);
+}
+__host__ __device__ inline long long sk_begin(int g, int G, int n_tiles, int kb, int drain) {
+  const long long V = (long long)n_tiles * (kb + drain);
+  return sk_real(V * g / G, kb, drain);
+}
+// the group whose (non-empty) range holds unit u: the largest g with sk_begin(g) <= u
+__host__ __device__ inline int sk_group_of(long long u, int G, int n_tiles, int kb, int drain) {
+  const long long V = (long long)n_tiles * (kb + drain);
+  const long long v = (u / kb) * (kb + drain) + drain + u % kb;
+  return (int)(((v + 1) * G + V - 1) / V) - 1;
+}
+static int sk_drain() {
+  static const int d = getenv("SF_GEMM_DRAIN") ? std::max(0, atoi(getenv("SF_GEMM_DRAIN"))) : 8;
+  return d;
+}
+
 struct SkParams {
   int T, N, K;
   int Tp;  // T rounded up to 32 (row stride of the fixup partial slots)
   int NT, n_sub, stages, kb_total, n_tiles, G, nbuf, w_tiled, w_tma, stage_ok, bulk_ok, npre;
   int cgrp;  // ring slots released per tcgen05.commit
+  int drain; // tile-entry cost of the stream-K partition (sk_begin)
   uint32_t tmem_cols;
   const __nv_bfloat16* w_tiles;  // tile-contiguous weights (w_tiled, CG == 1 bulk path)
   GemmEpi epi;
@@ -168,8 +194,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   const int c = blockIdx.x / CG;       // work group
   const int slot = blockIdx.x;         // partial / flag slot of this CTA
   const int kb = p.kb_total;
-  const long long U = (long long)p.n_tiles * kb;
-  const long long u0 = U * c / p.G, u1 = U * (c + 1) / p.G;
+  const long long u0 = sk_begin(c, p.G, p.n_tiles, kb, p.drain), u1 = sk_begin(c + 1, p.G, p.n_tiles, kb, p.drain);
   const int cols = p.n_sub * p.NT;
   if (threadIdx.x == 0) SF_TR(0);
   KtScope kt_(KT_GEMM, (uint32_t)p.N, 128);
@@ -606,7 +631,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       // head or full tile: add the other groups' k segments of this tile (they publish them first
       // thing), in k order, then the output epilogue
       int c_lo = c + 1, c_hi = c;
-      if (is_head) c_hi = (int)((te * p.G + U - 1) / U) - 1;
+      if (is_head) c_hi = sk_group_of(te - 1, p.G, p.n_tiles, kb, p.drain);
       if (is_head) {
         if (lead)
           for (int cc = c_lo; cc <= c_hi; ++cc)
@@ -1047,6 +1072,7 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   // first activation tile is served behind them, and it gates the first MMA
   static const int env_npre = getenv("SF_GEMM_NPRE") ? atoi(getenv("SF_GEMM_NPRE")) : 4;
   p.npre = std::max(1, std::min(env_npre, p.stages));
+  p.drain = sk_drain();
   p.stage_ok = (env_epi >> 1) & 7;
   static const int trace_n = getenv("SF_GEMM_TRACE_N") ? atoi(getenv("SF_GEMM_TRACE_N")) : 0;
   if (trace_n && trace_n != N) p.trace = nullptr;  // trace one weight shape only
@@ -1096,6 +1122,7 @@ bool gemm_partial_geom(int T, int N, int K, PartialGeom* g) {
   g->kb = K / BK;
   g->n_tiles = N / BM;
   g->T = T;
+  g->drain = sk_drain();
   return true;
 }
 
@@ -1113,7 +1140,7 @@ static int rn_ng(int d) {  // float4 groups per thread
 
 template <int NG>
 __global__ void __launch_bounds__(1024) resid_norm_kernel(
-    const float* __restrict__ partial, int G, int kb, int CG, int n_tiles_cta, int T, int rep, int d,
+    const float* __restrict__ partial, int G, int kb, int drain, int CG, int n_tiles_cta, int T, int rep, int d,
     const float* resid, const float* __restrict__ bias, float* out, float* tap, const float* __restrict__ gamma,
     float eps, __nv_bfloat16* xn) {
   constexpr int kRnBatch = 8 / NG;
@@ -1127,13 +1154,12 @@ __global__ void __launch_bounds__(1024) resid_norm_kernel(
   if (partial) {  // geometry only (no dependency on the previous kernel)
     const int groups = G / CG;
     const int n_tiles_grp = n_tiles_cta / CG;
-    const long long U = (long long)n_tiles_grp * kb;
     for (int vt = tid; vt < n_tiles_cta; vt += nthr) {
       const int tg = vt / CG, rk = vt % CG;
       const long long ua = (long long)tg * kb, ub = ua + kb - 1;
-      const int lo = (int)(((ua + 1) * groups + U - 1) / U) - 1;
-      const int hi = (int)(((ub + 1) * groups + U - 1) / U) - 1;
-      const int w0 = ((U * lo / groups) / kb == tg) ? 0 : 1;
+      const int lo = sk_group_of(ua, groups, n_tiles_grp, kb, drain);
+      const int hi = sk_group_of(ub, groups, n_tiles_grp, kb, drain);
+      const int w0 = (sk_begin(lo, groups, n_tiles_grp, kb, drain) / kb == tg) ? 0 : 1;
       seg_n[vt] = hi - lo + 1;
       for (int q = 0; q < kRnMaxSeg && lo + q <= hi; ++q)
         seg_off[vt][q] = ((2 * (lo + q) + (q == 0 ? w0 : 0)) * CG + rk) * T * BM;
@@ -1222,10 +1248,11 @@ cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T,
   if (T * rep <= 0) return cudaSuccess;
   const int ng = rn_ng(d);
   if (!ng) return cudaErrorInvalidValue;
-  int G = 1, kb = 1, CG = 1, nt = 1, Tslot = T;
+  int G = 1, kb = 1, CG = 1, nt = 1, Tslot = T, drain = 0;
   if (partial) {
     G = g->G;
     kb = g->kb;
+    drain = g->drain;
     nt = g->n_tiles;
     CG = gemm_cg(nt * BM, kb * BK);
     Tslot = g->T;
@@ -1235,13 +1262,13 @@ cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T,
   }
   const dim3 grid(T * rep), block(d / (4 * ng));
   switch (ng) {
-    case 1: return launch_k(resid_norm_kernel<1>, grid, block, 0, st, partial, G, kb, CG, nt, Tslot, rep, d, resid,
+    case 1: return launch_k(resid_norm_kernel<1>, grid, block, 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, d, resid,
                             bias, out, tap, gamma, eps, xn);
-    case 2: return launch_k(resid_norm_kernel<2>, grid, block, 0, st, partial, G, kb, CG, nt, Tslot, rep, d, resid,
+    case 2: return launch_k(resid_norm_kernel<2>, grid, block, 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, d, resid,
                             bias, out, tap, gamma, eps, xn);
-    case 3: return launch_k(resid_norm_kernel<3>, grid, block, 0, st, partial, G, kb, CG, nt, Tslot, rep, d, resid,
+    case 3: return launch_k(resid_norm_kernel<3>, grid, block, 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, d, resid,
                             bias, out, tap, gamma, eps, xn);
-    default: return launch_k(resid_norm_kernel<4>, grid, block, 0, st, partial, G, kb, CG, nt, Tslot, rep, d, resid,
+    default: return launch_k(resid_norm_kernel<4>, grid, block, 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, d, resid,
                              bias, out, tap, gamma, eps, xn);
   }
 }

@@ -74,6 +74,7 @@ struct PartialGeom {
   int kb;         // k-blocks per tile
   int n_tiles;    // 128-row tiles
   int T;          // rows per launch chunk (slot stride)
+  int drain;      // tile-entry cost of the stream-K partition
 };
 bool gemm_partial_geom(int T, int N, int K, PartialGeom* g);  // false if EPI_PARTIAL unsupported
 

@@ -236,7 +236,10 @@ struct sf_handle {
     double bytes;
   };
   bool prof_on = false;
+  bool prof_capture = false;  // records become external event-record nodes of the profiling graph
   std::vector<Prof> prof;
+  double prof_ms[4] = {0, 0, 0, 0}, prof_bytes[4] = {0, 0, 0, 0};  // graph replays, accumulated
+  int64_t prof_n[4] = {0, 0, 0, 0};
   std::vector<cudaEvent_t> ev_free;
   cudaEvent_t ev_get() {
     if (ev_free.empty()) {
@@ -283,12 +286,18 @@ struct ProfScope {
   ProfScope(sf_handle* hh, int cls, double bytes) : h(hh) {
     if (!h->prof_on) return;
     sf_handle::Prof r{cls, h->ev_get(), h->ev_get(), bytes};
-    cudaEventRecord(r.a, h->st);
+    ev_record(r.a);
     h->prof.push_back(r);
     idx = h->prof.size() - 1;
   }
   ~ProfScope() {
-    if (idx != (size_t)-1) cudaEventRecord(h->prof[idx].b, h->st);
+    if (idx != (size_t)-1) ev_record(h->prof[idx].b);
+  }
+  void ev_record(cudaEvent_t e) {
+    if (h->prof_capture)
+      cudaEventRecordWithFlags(e, h->st, cudaEventRecordExternal);
+    else
+      cudaEventRecord(e, h->st);
   }
 };
 
@@ -620,18 +629,27 @@ static cudaError_t copy_out(sf_handle* h, void* dst, const void* src, size_t byt
 static void* g_kt_rec = nullptr;
 static unsigned* g_kt_cnt = nullptr;
 static constexpr unsigned kKtCap = 1u << 21;
-static bool kt_enable() {
-  static const bool on = getenv("SF_KTRACE") && atoi(getenv("SF_KTRACE")) > 0;
-  if (!on) return false;
-  if (!g_kt_rec) {
+static bool g_kt_on = false;
+static bool kt_set(bool on) {
+  if (on && !g_kt_rec) {
     if (cudaMalloc(&g_kt_rec, (size_t)kKtCap * kKtRecBytes) != cudaSuccess) return false;
     if (cudaMalloc((void**)&g_kt_cnt, 4) != cudaSuccess) return false;
-    cudaMemset(g_kt_cnt, 0, 4);
-    kt_setup_kernels(g_kt_rec, g_kt_cnt, kKtCap);
-    kt_setup_gemm(g_kt_rec, g_kt_cnt, kKtCap);
-    kt_setup_attn_fd(g_kt_rec, g_kt_cnt, kKtCap);
   }
+  if (!g_kt_rec) return !on;
+  cudaDeviceSynchronize();
+  cudaMemset(g_kt_cnt, 0, 4);
+  void* rec = on ? g_kt_rec : nullptr;  // a null record pointer turns every probe off
+  kt_setup_kernels(rec, g_kt_cnt, kKtCap);
+  kt_setup_gemm(rec, g_kt_cnt, kKtCap);
+  kt_setup_attn_fd(rec, g_kt_cnt, kKtCap);
+  cudaDeviceSynchronize();
+  g_kt_on = on;
   return true;
+}
+static bool kt_enable() {  // SF_KTRACE=1: on from the first handle on
+  static const bool env = getenv("SF_KTRACE") && atoi(getenv("SF_KTRACE")) > 0;
+  if (env && !g_kt_on) kt_set(true);
+  return g_kt_on;
 }
 
 extern "C" {
@@ -966,8 +984,49 @@ sf_status specformer_decode_steps(sf_handle* h, int32_t n_steps, int32_t* emitte
     SF_TRY(one_step(h, accept_log, emitted_log));
     done = 1;
   }
-  const bool use_graph = (h->c.flags & SF_FLAG_CUDA_GRAPH) != 0 && !h->prof_on;
-  if (use_graph && done < n_steps) {
+  const bool use_graph = (h->c.flags & SF_FLAG_CUDA_GRAPH) != 0;
+  if (use_graph && h->prof_on && done < n_steps) {
+    // profiling: the step graph re-captured with an event-record node around every launch (this
+    // serialises the launches -- no PDL overlap across a record node), replayed one step at a time
+    // with each replay's per-launch times accumulated per kernel class
+    cudaGraph_t g;
+    cudaGraphExec_t ge = nullptr;
+    const size_t r0 = h->prof.size();
+    const int64_t before = h->launches;
+    h->prof_capture = true;
+    SF_TRY(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = one_step(h, accept_log, emitted_log);
+    cudaError_t e2 = cudaStreamEndCapture(h->st, &g);
+    h->prof_capture = false;
+    if (e != cudaSuccess || e2 != cudaSuccess) {
+      h->err_msg = std::string("profiling graph capture failed: ") + cudaGetErrorString(e != cudaSuccess ? e : e2);
+      return SF_ERR_CUDA;
+    }
+    SF_TRY(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    const int64_t per_step = h->launches - before;
+    h->launches = before;
+    std::vector<sf_handle::Prof> recs(h->prof.begin() + r0, h->prof.end());
+    h->prof.resize(r0);
+    for (int s = done; s < n_steps; ++s) {
+      SF_TRY(cudaGraphLaunch(ge, h->st));
+      SF_TRY(cudaStreamSynchronize(h->st));
+      h->launches += per_step;
+      for (auto& r : recs) {
+        float t = 0;
+        SF_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+        h->prof_ms[r.cls] += t;
+        h->prof_bytes[r.cls] += r.bytes;
+        h->prof_n[r.cls] += 1;
+      }
+    }
+    cudaGraphExecDestroy(ge);
+    for (auto& r : recs) {
+      h->ev_free.push_back(r.a);
+      h->ev_free.push_back(r.b);
+    }
+    h->ctx_pending = k > 0;
+  } else if (use_graph && done < n_steps) {
     // the graph depends on the log pointers only (the log capacity is read on the device)
     if (h->gexec && (h->g_acc_log != accept_log || h->g_em_log != emitted_log)) {
       cudaGraphExecDestroy(h->gexec);
@@ -1086,6 +1145,7 @@ sf_status sf_profile(sf_handle* h, int32_t enable) {
     h->ev_free.push_back(r.b);
   }
   h->prof.clear();
+  for (int c = 0; c < 4; ++c) h->prof_ms[c] = h->prof_bytes[c] = 0, h->prof_n[c] = 0;
   h->prof_on = enable != 0;
   return SF_OK;
 }
@@ -1093,8 +1153,9 @@ sf_status sf_profile(sf_handle* h, int32_t enable) {
 sf_status sf_profile_read(sf_handle* h, int32_t cls, double* total_ms, int64_t* count, double* bytes) {
   if (!h || !total_ms || !count || !bytes) return SF_ERR_ARG;
   SF_TRY(cudaStreamSynchronize(h->st));
-  double ms = 0, by = 0;
-  int64_t n = 0;
+  if (cls < 0 || cls > 3) return SF_ERR_ARG;
+  double ms = h->prof_ms[cls], by = h->prof_bytes[cls];
+  int64_t n = h->prof_n[cls];
   for (auto& r : h->prof) {
     if (r.cls != cls) continue;
     float t = 0;
@@ -1108,6 +1169,8 @@ sf_status sf_profile_read(sf_handle* h, int32_t cls, double* total_ms, int64_t* 
   *bytes = by;
   return SF_OK;
 }
+
+int32_t sf_debug_ktrace_enable(int32_t on) { return kt_set(on != 0) ? 0 : -1; }
 
 int32_t sf_debug_ktrace(void* dst_host, int32_t cap) {
   if (!kt_enable() || !dst_host || cap <= 0) return 0;
