@@ -76,9 +76,13 @@ __host__ __device__ inline int sk_group_of(long long u, int G, int n_tiles, int 
   const long long v = (u / kb) * (kb + drain) + drain + u % kb;
   return (int)(((v + 1) * G + V - 1) / V) - 1;
 }
-static int sk_drain() {
+// Measured on the 7B shapes (profiles/r01/drain_sweep.txt): the entry cost pays off where the
+// epilogue of a piece is a plain fp32 publish or a SwiGLU tile (EPI_PARTIAL, EPI_SWIGLU_ACT: -3..-5 us
+// per launch at T = 320, +0.5 us at T = 5); for the fixup-heavy ACT / F32 / QKV launches it does not.
+// Depends on the epilogue mode only, never on T.
+static int sk_drain(int mode) {
   static const int d = getenv("SF_GEMM_DRAIN") ? std::max(0, atoi(getenv("SF_GEMM_DRAIN"))) : 8;
-  return d;
+  return (mode == EPI_PARTIAL || mode == EPI_SWIGLU_ACT) ? d : 0;
 }
 
 struct SkParams {
@@ -87,6 +91,7 @@ struct SkParams {
   int NT, n_sub, stages, kb_total, n_tiles, G, nbuf, w_tiled, w_tma, stage_ok, bulk_ok, npre;
   int cgrp;  // ring slots released per tcgen05.commit
   int drain; // tile-entry cost of the stream-K partition (sk_begin)
+  int park;  // park mid-range full tiles (T >= 64) for the final phase
   uint32_t tmem_cols;
   const __nv_bfloat16* w_tiles;  // tile-contiguous weights (w_tiled, CG == 1 bulk path)
   GemmEpi epi;
@@ -196,8 +201,13 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   const int kb = p.kb_total;
   const long long u0 = sk_begin(c, p.G, p.n_tiles, kb, p.drain), u1 = sk_begin(c + 1, p.G, p.n_tiles, kb, p.drain);
   const int cols = p.n_sub * p.NT;
+  // the range's segments: its pieces of consecutive 128-row tiles, in k order
+  const int t_first = (int)(u0 / kb);
+  const int nseg = u1 > u0 ? (int)((u1 - 1) / kb) - t_first + 1 : 0;
+  auto seg_lo = [=](int i) -> long long { return max(u0, (long long)(t_first + i) * kb); };
+  auto seg_hi = [=](int i) -> long long { return min(u1, (long long)(t_first + i + 1) * kb); };
   if (threadIdx.x == 0) SF_TR(0);
-  KtScope kt_(KT_GEMM, (uint32_t)p.N, 128);
+  KtScope kt_(KT_GEMM, (uint32_t)p.N | ((uint32_t)min(kb, 511) << 15), 128);  // param: N | (K / 64) << 15
 
   if (threadIdx.x == 0) {
     if (!(CG == 1 && p.w_tiled && !p.w_tma)) prefetch_tmap(&tmW);
@@ -236,8 +246,12 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     // requested before the grid dependency resolves (PDL), the activation tiles after it.
     const long long npre = p.w_tiled ? min((long long)p.npre, u1 - u0) : 0;
     if (npre > 0 && elect_one()) {
-      int tp = (int)(u0 / kb), kp = (int)(u0 % kb);
+      int si = 0;
+      long long up = seg_lo(0);
       for (int i = 0; i < (int)npre; ++i) {
+        if (up == seg_hi(si)) up = seg_lo(++si);
+        const int tp = (int)(up / kb), kp = (int)(up % kb);
+        ++up;
         uint8_t* st = smem + (size_t)i * stage_bytes;
         if constexpr (CG == 1) {
           mbar_arrive_expect_tx(&full[i], (uint32_t)stage_bytes);
@@ -251,23 +265,21 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           if (prank == 0) mbar_arrive_expect_tx(&full[i], (uint32_t)(2 * stage_bytes));
           tma_load_2d_2sm(st, &tmW, &full[i], 0, ((tp * CG + (int)rank) * kb + kp) * BM, kEvictFirst);
         }
-        if (++kp == kb) {
-          kp = 0;
-          ++tp;
-        }
       }
     }
     __syncwarp();
     pdl_wait();
     pdl_trigger();
-    int t = (int)(u0 / kb), k = (int)(u0 % kb);
     int s = 0, grp_last = p.cgrp - 1;  // ring slot and the last slot of its release group
     uint32_t ph = 0;
-    for (long long u = u0; u < u1; ++u) {
-      const bool pre = (u - u0) < npre;  // weights already requested, slot known free
+    long long j = 0;  // units issued
+    for (int si = 0; si < nseg; ++si)
+    for (long long u = seg_lo(si); u < seg_hi(si); ++u, ++j) {
+      const int t = (int)(u / kb), k = (int)(u % kb);
+      const bool pre = j < npre;  // weights already requested, slot known free
       if (!pre) mbar_wait(&empty[grp_last], ph ^ 1u);  // slot group released
-      if (u == u0 && lane == 0) SF_TR(2);
-      if (lane == 0 && u - u0 < 40) SF_TR(64 + (int)(u - u0));
+      if (j == 0 && lane == 0) SF_TR(2);
+      if (lane == 0 && j < 40) SF_TR(64 + (int)j);
       if (elect_one()) {
         uint8_t* st = smem + (size_t)s * stage_bytes;
         if constexpr (CG == 1) {
@@ -306,10 +318,6 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         }
       }
       __syncwarp();
-      if (++k == kb) {
-        k = 0;
-        ++t;
-      }
       if (++s == p.stages) {
         s = 0;
         ph ^= 1u;
@@ -331,13 +339,11 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     const uint32_t idesc = idesc_bf16_f32(kPair ? 2 * BM : BM, p.NT);
     const uint32_t a_off = (uint32_t)(BM * BK * 2) >> 4;           // B-operand tile offset (16 B units)
     const uint32_t sub_off = (uint32_t)(a_rows * BK * 2) >> 4;     // between activation sub-tiles
-    int seg = 0;
     int s = 0, gcnt = 0;
     uint32_t ph = 0;
-    long long u = u0;
-    int t = (int)(u0 / kb);
-    while (u < u1) {
-      const long long se = min(u1, (long long)(t + 1) * kb);
+    long long j = 0;  // units consumed
+    for (int seg = 0; seg < nseg; ++seg) {
+      const long long u = seg_lo(seg), se = seg_hi(seg);
       const int b = seg % p.nbuf;
       mbar_wait(&acce[b], ((uint32_t)(seg / p.nbuf) & 1u) ^ 1u);
       tc_fence_after();
@@ -347,9 +353,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         mbar_wait(&full[s], ph);
         tc_fence_after();
         if (lane == 0) {
-          if (uu == u0) SF_TR(3);
-          if (uu - u0 < 40) SF_TR(24 + (int)(uu - u0));
+          if (j == 0) SF_TR(3);
+          if (j < 40) SF_TR(24 + (int)j);
         }
+        ++j;
         if (elect_one()) {
           const uint64_t dw = sw128_kmajor_desc(smem_u32(smem + (size_t)s * stage_bytes));
           const uint64_t da = dw + a_off;
@@ -382,11 +389,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       __syncwarp();
       if (lane == 0) {
         if (seg < 4) SF_TR(8 + 4 * seg + 1);
-        if (se == u1) SF_TR(4);
+        if (seg == nseg - 1) SF_TR(4);
       }
-      u = se;
-      ++seg;
-      ++t;
     }
   }
   {
@@ -603,7 +607,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       const bool is_full = (u == ts) && (se == te);
       const bool is_head = (u == ts) && !is_full;
       const int cstep = 32 * ng;
-      if (mode == EPI_PARTIAL || (!is_full && !is_head) || (is_full && !final && can_stage && p.T >= 64)) {
+      if (mode == EPI_PARTIAL || (!is_full && !is_head) || (is_full && !final && can_stage && p.park && p.T >= 64)) {
         // fp32 accumulator -> [T][128] slot (each warp store is one 128-byte line):
         //  EPI_PARTIAL: slot 2 group + (first segment of the range ? 0 : 1), reduced in k order by
         //    the consumer; tail of a tile owned by another group: this CTA's slot, then its flag;
@@ -706,14 +710,12 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 
     // segments of [u0, u1): all but the last by the 8 epilogue warps while the MMA streams on; the
     // last one (and a parked full tile) by all 12 warps -- one inlined copy of the epilogue
-    int nseg_total = 0;
-    for (long long uu = u0; uu < u1; uu = min(u1, (uu / kb + 1) * kb)) ++nseg_total;
+    const int nseg_total = nseg;
     int defer_vt = -1;
-    long long u = u0;
     int gid = 0;
     for (int seg = 0; seg < nseg_total; ++seg) {
+      const long long u = seg_lo(seg), se = seg_hi(seg);
       const int t = (int)(u / kb);
-      const long long se = min(u1, (long long)(t + 1) * kb);
       // the 12-warp final phase pays off for large T only (small T: a few rows per chunk, the
       // extra barriers would dominate)
       const bool final = seg == nseg_total - 1 && p.T >= 64;
@@ -748,7 +750,6 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         }
         if (lead && seg < 4) SF_TR(8 + 4 * seg + 3);
       }
-      u = se;
     }
     if constexpr (kStageable) {
       if (defer_vt >= 0) {
@@ -1065,14 +1066,16 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   p.w_tiled = w_tiled ? 1 : 0;
   p.w_tiles = (const __nv_bfloat16*)W;
   p.trace = gemm_trace_buffer();
-  // bit0 bulk fixup loads; bits 1..3 smem-staged stores for ACT / F32 / SwiGLU outputs
-  static const int env_epi = getenv("SF_GEMM_EPI") ? atoi(getenv("SF_GEMM_EPI")) : 15;
+  // bit0 bulk fixup loads; bits 1..3 smem-staged stores for ACT / F32 / SwiGLU outputs; bit 4 park
+  // mid-range full tiles (T >= 64) for the final phase
+  static const int env_epi = getenv("SF_GEMM_EPI") ? atoi(getenv("SF_GEMM_EPI")) : 31;
   p.bulk_ok = env_epi & 1;
   // weight stages requested before the grid dependency resolves: a few, not the whole ring -- the
   // first activation tile is served behind them, and it gates the first MMA
   static const int env_npre = getenv("SF_GEMM_NPRE") ? atoi(getenv("SF_GEMM_NPRE")) : 4;
   p.npre = std::max(1, std::min(env_npre, p.stages));
-  p.drain = sk_drain();
+  p.drain = sk_drain(epi.mode);
+  p.park = (env_epi >> 4) & 1;
   p.stage_ok = (env_epi >> 1) & 7;
   static const int trace_n = getenv("SF_GEMM_TRACE_N") ? atoi(getenv("SF_GEMM_TRACE_N")) : 0;
   if (trace_n && trace_n != N) p.trace = nullptr;  // trace one weight shape only
@@ -1122,7 +1125,7 @@ bool gemm_partial_geom(int T, int N, int K, PartialGeom* g) {
   g->kb = K / BK;
   g->n_tiles = N / BM;
   g->T = T;
-  g->drain = sk_drain();
+  g->drain = sk_drain(EPI_PARTIAL);
   return true;
 }
 

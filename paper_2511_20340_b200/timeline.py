@@ -27,7 +27,7 @@ CLASS = {"gemm": "gemm", "gemm_simt": "gemm", "attn": "attention", "rope": "atte
 def name(kid: int) -> str:
     k, p = kid >> 24, kid & 0xFFFFFF
     n = KIND.get(k, str(k))
-    return f"{n}[N={p}]" if n == "gemm" else n
+    return f"{n}[N={p & 0x7FFF},K={64 * (p >> 15)}]" if n == "gemm" else n
 
 
 def kclass(kid: int) -> str:
