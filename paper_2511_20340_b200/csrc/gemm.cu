@@ -62,19 +62,24 @@ SF_DEV float silu_f(float g) { return g / (1.f + expf(-g)); }
 // accumulator's epilogue must drain TMEM first; one TMEM buffer at T > 256) -- and the virtual
 // sequence is cut evenly, so a range that crosses a tile boundary gets fewer real units. The cut
 // depends on (n_tiles, kb, G, drain) only: the same k segmentation at every T (batch invariance).
-__host__ __device__ inline long long sk_real(long long v, int kb, int drain) {
-  const long long t = v / (kb + drain), o = v % (kb + drain);
+// (32-bit arithmetic: n_tiles (kb + drain) G < 2^31 for every supported shape, checked at launch)
+__host__ __device__ inline int sk_real(int v, int kb, int drain) {
+  const int t = v / (kb + drain), o = v - t * (kb + drain);
   return t * kb + (o > drain ? o - drain : 0);
 }
-__host__ __device__ inline long long sk_begin(int g, int G, int n_tiles, int kb, int drain) {
-  const long long V = (long long)n_tiles * (kb + drain);
+__host__ __device__ inline int sk_begin(int g, int G, int n_tiles, int kb, int drain) {
+  const int V = n_tiles * (kb + drain);
   return sk_real(V * g / G, kb, drain);
 }
 // the group whose (non-empty) range holds unit u: the largest g with sk_begin(g) <= u
-__host__ __device__ inline int sk_group_of(long long u, int G, int n_tiles, int kb, int drain) {
-  const long long V = (long long)n_tiles * (kb + drain);
-  const long long v = (u / kb) * (kb + drain) + drain + u % kb;
-  return (int)(((v + 1) * G + V - 1) / V) - 1;
+__host__ __device__ inline int sk_group_of(int u, int G, int n_tiles, int kb, int drain) {
+  const int V = n_tiles * (kb + drain);
+  const int t = u / kb;
+  const int v = t * (kb + drain) + drain + (u - t * kb);
+  return ((v + 1) * G + V - 1) / V - 1;
+}
+static bool sk_fits(int G, int n_tiles, int kb, int drain) {
+  return (long long)n_tiles * (kb + drain) * (G + 1) + G < (1ll << 31);
 }
 // Measured on the 7B shapes (profiles/r01/drain_sweep.txt): the entry cost pays off where the
 // epilogue of a piece is a plain fp32 publish or a SwiGLU tile (EPI_PARTIAL, EPI_SWIGLU_ACT: -3..-5 us
@@ -274,8 +279,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     uint32_t ph = 0;
     long long j = 0;  // units issued
     for (int si = 0; si < nseg; ++si)
-    for (long long u = seg_lo(si); u < seg_hi(si); ++u, ++j) {
-      const int t = (int)(u / kb), k = (int)(u % kb);
+    for (int t = t_first + si, k = (int)(seg_lo(si) - (long long)t * kb), ke = (int)(seg_hi(si) - (long long)t * kb);
+         k < ke; ++k, ++j) {
       const bool pre = j < npre;  // weights already requested, slot known free
       if (!pre) mbar_wait(&empty[grp_last], ph ^ 1u);  // slot group released
       if (j == 0 && lane == 0) SF_TR(2);
@@ -514,6 +519,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         }
       }
       named_sync(2 + gid, 128);
+      if (lead && c0 < 2 * 96) SF_TR(116 + 4 * (c0 / 96));  // staged in smem
       const int col0 = mode == EPI_SWIGLU_ACT ? vt_ * 64 : vt_ * BM;
       uint8_t* gbase = reinterpret_cast<uint8_t*>(p.epi.out) + ((size_t)c0 * ldo + col0) * out_elt;
       const int vpr = rowb / 16, ht = quad * 32 + lane;
@@ -635,7 +641,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       // head or full tile: add the other groups' k segments of this tile (they publish them first
       // thing), in k order, then the output epilogue
       int c_lo = c + 1, c_hi = c;
-      if (is_head) c_hi = sk_group_of(te - 1, p.G, p.n_tiles, kb, p.drain);
+      if (is_head) c_hi = sk_group_of((int)(te - 1), p.G, p.n_tiles, kb, p.drain);
       if (is_head) {
         if (lead)
           for (int cc = c_lo; cc <= c_hi; ++cc)
@@ -659,6 +665,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           uint32_t r[32];
           tmem_ld32_async(t_row + (uint32_t)c0, r);
           tmem_ld_wait();
+          if (lead && final && c0 < 2 * cstep) SF_TR(114 + 4 * (c0 / cstep));  // TMEM loaded
           float v[32];
 #pragma unroll
           for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
@@ -1074,7 +1081,8 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   // first activation tile is served behind them, and it gates the first MMA
   static const int env_npre = getenv("SF_GEMM_NPRE") ? atoi(getenv("SF_GEMM_NPRE")) : 4;
   p.npre = std::max(1, std::min(env_npre, p.stages));
-  p.drain = sk_drain(epi.mode);
+  p.drain = epi.drain >= 0 ? epi.drain : sk_drain(epi.mode);
+  if (!sk_fits(p.G, p.n_tiles, p.kb_total, p.drain)) return cudaErrorInvalidValue;
   p.park = (env_epi >> 4) & 1;
   p.stage_ok = (env_epi >> 1) & 7;
   static const int trace_n = getenv("SF_GEMM_TRACE_N") ? atoi(getenv("SF_GEMM_TRACE_N")) : 0;
@@ -1114,7 +1122,7 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   return cudaLaunchKernelEx(&cfg, sk_kernel_for(2, epi.mode), mw, ma, p);
 }
 
-bool gemm_partial_geom(int T, int N, int K, PartialGeom* g) {
+bool gemm_partial_geom(int T, int N, int K, PartialGeom* g, int drain) {
   if (N % BM || K % BK || T > 512) return false;
   const int CG = gemm_cg(N, K);
   const int n_tiles = N / (BM * CG);
@@ -1125,7 +1133,8 @@ bool gemm_partial_geom(int T, int N, int K, PartialGeom* g) {
   g->kb = K / BK;
   g->n_tiles = N / BM;
   g->T = T;
-  g->drain = sk_drain(EPI_PARTIAL);
+  g->drain = drain >= 0 ? drain : sk_drain(EPI_PARTIAL);
+  if (!sk_fits(G, n_tiles, K / BK, g->drain)) return false;
   return true;
 }
 
@@ -1159,7 +1168,7 @@ __global__ void __launch_bounds__(1024) resid_norm_kernel(
     const int n_tiles_grp = n_tiles_cta / CG;
     for (int vt = tid; vt < n_tiles_cta; vt += nthr) {
       const int tg = vt / CG, rk = vt % CG;
-      const long long ua = (long long)tg * kb, ub = ua + kb - 1;
+      const int ua = tg * kb, ub = ua + kb - 1;
       const int lo = sk_group_of(ua, groups, n_tiles_grp, kb, drain);
       const int hi = sk_group_of(ub, groups, n_tiles_grp, kb, drain);
       const int w0 = (sk_begin(lo, groups, n_tiles_grp, kb, drain) / kb == tg) ? 0 : 1;
@@ -1284,6 +1293,122 @@ bool resid_norm_supported(int d, int T, int N, int K) {
   const int CG = gemm_cg(N, K);
   const int groups = g.G / CG, ntg = g.n_tiles / CG;
   return (groups + ntg - 1) / ntg + 1 <= kRnMaxSeg && g.n_tiles <= kRnMaxTiles;
+}
+
+// ------------------------------------------------------------------------ QKV partial consumer
+// One warp per (row, head) item (persistent grid, two items in flight per warp); lane l owns the
+// pair-interleaved positions 4l..4l+3 = dims (2l, 2l+64, 2l+1, 2l+65) of the head.
+__global__ void __launch_bounds__(256) rope_partial_kernel(const float* __restrict__ partial, int G, int kb, int drain,
+                                                           int CG, int H, int Tslot, int T, int q_len,
+                                                           const int* __restrict__ pos0, const float2* __restrict__ rope,
+                                                           int Hq, int Hkv, const int* __restrict__ bt, int pps,
+                                                           __nv_bfloat16* Kp, __nv_bfloat16* Vp, __nv_bfloat16* q_out) {
+  __shared__ int seg_n[kRnMaxTiles];
+  __shared__ int seg_off[kRnMaxTiles][kRnMaxSeg];  // slot * Tslot * 128, k order
+  {  // geometry only (no dependency on the previous kernel)
+    const int groups = G / CG, n_tiles_grp = H / CG;
+    for (int vt = threadIdx.x; vt < H; vt += blockDim.x) {
+      const int tg = vt / CG, rk = vt % CG;
+      const int ua = tg * kb, ub = ua + kb - 1;
+      const int lo = sk_group_of(ua, groups, n_tiles_grp, kb, drain);
+      const int hi = sk_group_of(ub, groups, n_tiles_grp, kb, drain);
+      const int w0 = (sk_begin(lo, groups, n_tiles_grp, kb, drain) / kb == tg) ? 0 : 1;
+      seg_n[vt] = hi - lo + 1;
+      for (int q = 0; q < kRnMaxSeg && lo + q <= hi; ++q)
+        seg_off[vt][q] = ((2 * (lo + q) + (q == 0 ? w0 : 0)) * CG + rk) * Tslot * BM;
+    }
+    __syncthreads();
+  }
+  KtScope kt_(KT_ROPE, (uint32_t)Hq);
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const int items = T * H;
+  for (int i0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i0 < items; i0 += 2 * nw) {
+    uint32_t a[2], bb[2];
+    float4 cs[2];
+    int t[2], h[2], pos[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int it = min(i0 + u * nw, items - 1);
+      t[u] = it / H;
+      h[u] = it % H;
+      pos[u] = pos0[t[u] / q_len] + t[u] % q_len;
+      const float* base = partial + (size_t)t[u] * BM + 4 * lane;
+      const int ns = seg_n[h[u]];
+      float4 x = __ldcg(reinterpret_cast<const float4*>(base + seg_off[h[u]][0]));
+      for (int q0 = 1; q0 < ns; q0 += 4) {  // k order; up to four loads in flight
+        float4 pv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q0 + q < ns) pv[q] = __ldcg(reinterpret_cast<const float4*>(base + seg_off[h[u]][q0 + q]));
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q0 + q < ns) {
+            x.x += pv[q].x;
+            x.y += pv[q].y;
+            x.z += pv[q].z;
+            x.w += pv[q].w;
+          }
+      }
+      // positions (4l, 4l+1, 4l+2, 4l+3) = dims (2l, 2l+64, 2l+1, 2l+65), rounded as the GEMM would
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.z);  // dims 2l, 2l+1
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(x.y, x.w);  // dims 2l+64, 2l+65
+      a[u] = *reinterpret_cast<const uint32_t*>(&lo);
+      bb[u] = *reinterpret_cast<const uint32_t*>(&hi);
+      cs[u] = *reinterpret_cast<const float4*>(rope + (size_t)pos[u] * 64 + 2 * lane);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (i0 + u * nw >= items) break;
+      const int b = t[u] / q_len;
+      if (h[u] >= Hq + Hkv) {  // value head: plain copy into the page
+        const int blk = bt[b * pps + pos[u] / 16], slot = pos[u] % 16;
+        __nv_bfloat16* dst = Vp + (((size_t)blk * Hkv + (h[u] - Hq - Hkv)) * 16 + slot) * 128;
+        *reinterpret_cast<uint32_t*>(dst + 2 * lane) = a[u];
+        *reinterpret_cast<uint32_t*>(dst + 64 + 2 * lane) = bb[u];
+        continue;
+      }
+      const float2 x1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a[u]));
+      const float2 x2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bb[u]));
+      const float y10 = rope_y1(x1.x, x2.x, cs[u].x, cs[u].y), y20 = rope_y2(x1.x, x2.x, cs[u].x, cs[u].y);
+      const float y11 = rope_y1(x1.y, x2.y, cs[u].z, cs[u].w), y21 = rope_y2(x1.y, x2.y, cs[u].z, cs[u].w);
+      __nv_bfloat16* dst;
+      if (h[u] < Hq) {
+        dst = q_out + ((size_t)t[u] * Hq + h[u]) * 128;
+      } else {
+        const int blk = bt[b * pps + pos[u] / 16], slot = pos[u] % 16;
+        dst = Kp + (((size_t)blk * Hkv + (h[u] - Hq)) * 16 + slot) * 128;
+      }
+      *reinterpret_cast<__nv_bfloat162*>(dst + 2 * lane) = __floats2bfloat162_rn(y10, y11);
+      *reinterpret_cast<__nv_bfloat162*>(dst + 64 + 2 * lane) = __floats2bfloat162_rn(y20, y21);
+    }
+  }
+}
+
+bool rope_partial_supported(int T, int N, int K, int Hq, int Hkv, int drain) {
+  PartialGeom g;
+  if (N != (Hq + 2 * Hkv) * BM || !gemm_partial_geom(T, N, K, &g, drain)) return false;
+  const int CG = gemm_cg(N, K);
+  const int groups = g.G / CG, ntg = g.n_tiles / CG;
+  return (groups + ntg - 1) / ntg + 1 <= kRnMaxSeg && g.n_tiles <= kRnMaxTiles;
+}
+
+cudaError_t launch_rope_partial(const float* partial, const PartialGeom* g, int T, int q_len, const int* pos0,
+                                const float2* rope, int Hq, int Hkv, const int* bt, int pps, void* Kp, void* Vp,
+                                void* q_out, cudaStream_t st) {
+  const int H = Hq + 2 * Hkv;
+  if (!partial || !g || g->n_tiles != H || H > kRnMaxTiles || T < 1) return cudaErrorInvalidValue;
+  const int CG = gemm_cg(g->n_tiles * BM, g->kb * BK);
+  const int groups = g->G / CG;
+  if ((groups + H / CG - 1) / (H / CG) + 1 > kRnMaxSeg) return cudaErrorInvalidValue;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = std::max(1, std::min(6 * sms, (T * H + 15) / 16));
+  return launch_k(rope_partial_kernel, dim3(grid), dim3(256), 0, st, partial, g->G, g->kb, g->drain, CG, H, g->T, T,
+                  q_len, pos0, rope, Hq, Hkv, bt, pps, (__nv_bfloat16*)Kp, (__nv_bfloat16*)Vp, (__nv_bfloat16*)q_out);
 }
 
 static cudaError_t gemm_launch_chunk(bool is_bf16, const void* A, int lda, const void* W, bool w_tiled, int T,

@@ -43,6 +43,10 @@ struct GemmEpi {
   const void* pf = nullptr;
   size_t pf_bytes = 0;
   RopeEpi rope;  // EPI_QKV_ROPE only
+  // tile-entry cost of the stream-K partition (k segmentation); < 0: the mode's default. Launches
+  // whose results must agree bit for bit across modes (the QKV projection: EPI_QKV_ROPE for short
+  // blocks, EPI_PARTIAL + launch_rope_partial for long ones) pass the same value.
+  int drain = -1;
 };
 
 struct GemmScratch {
@@ -76,7 +80,8 @@ struct PartialGeom {
   int T;          // rows per launch chunk (slot stride)
   int drain;      // tile-entry cost of the stream-K partition
 };
-bool gemm_partial_geom(int T, int N, int K, PartialGeom* g);  // false if EPI_PARTIAL unsupported
+// false if EPI_PARTIAL unsupported; drain as GemmEpi::drain
+bool gemm_partial_geom(int T, int N, int K, PartialGeom* g, int drain = -1);
 
 // Fused consumer of EPI_PARTIAL (and plain residual/norm): for virtual row r (T*rep rows, source
 // row r / rep, columns [(r % rep) * d, +d) of the GEMM output):
@@ -87,5 +92,16 @@ bool resid_norm_supported(int d, int T, int N, int K);
 cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T, int rep, int d, const float* resid,
                               const float* bias, float* out, float* tap, const float* gamma, float eps,
                               __nv_bfloat16* xn, cudaStream_t s);
+
+// Consumer of an EPI_PARTIAL QKV projection (bf16, head_dim 128, one 128-row tile per head, rows
+// pair-interleaved per head as for EPI_QKV_ROPE): for every (row t, head h) the head's k-segment
+// partials are summed in k order (the first segment, then the others: the same additions as the
+// GEMM's own head-tile fixup), rounded to bf16, and -- exactly as launch_rope_append's 128-wide
+// kernel does with the bf16 projection -- q / k heads rotated at position pos0[t / q_len] + t % q_len
+// (q -> q_out [T, Hq, 128], k -> its page slot) and v heads copied to their page slot.
+bool rope_partial_supported(int T, int N, int K, int Hq, int Hkv, int drain);
+cudaError_t launch_rope_partial(const float* partial, const PartialGeom* g, int T, int q_len, const int* pos0,
+                                const float2* rope, int Hq, int Hkv, const int* bt, int pps, void* Kp, void* Vp,
+                                void* q_out, cudaStream_t s);
 
 }  // namespace sf

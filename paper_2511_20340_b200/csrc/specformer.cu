@@ -411,11 +411,37 @@ static bool fused_rope(const sf_handle* h, int T) {
   return h->bf && h->p.hd == 128 && T < thr;
 }
 
-// QKV projection of layer `layer` (its KV pool): fused RoPE / append, else the plain GEMM (rope later)
+// The QKV projection's stream-K k segmentation is the same in every mode it runs in (fused RoPE,
+// partials + rope_partial, plain): a row's bits do not depend on the block size.
+constexpr int kQkvDrain = 0;
+// bf16, head_dim 128, blocks too long for the fused epilogue: the GEMM publishes its k-segment
+// partials and launch_rope_partial reduces them while rotating / appending (no fixup tail in the
+// GEMM). SF_QKV_PARTIAL=0 (read per call; tests) selects the plain GEMM + rope_append instead.
+static bool qkv_partial(const sf_handle* h, int T) {
+  const char* e = getenv("SF_QKV_PARTIAL");
+  if (e && atoi(e) == 0) return false;
+  const Plan& p = h->p;
+  return h->bf && p.hd == 128 && !fused_rope(h, T) && T <= 512 &&
+         rope_partial_supported(T, p.qkvw, p.d, p.Hq, p.Hkv, kQkvDrain);
+}
+
+// QKV projection of layer `layer` (its KV pool): fused RoPE / append, partials for rope_partial, or
+// the plain GEMM (rope later)
 static cudaError_t qkv_gemm(sf_handle* h, const void* W, int layer, int T, int q_len, const int* pos0) {
   const Plan& p = h->p;
-  if (!fused_rope(h, T)) return gemm(h, h->xn, p.d, W, T, p.qkvw, p.d, epi_act(h->qkv, p.qkvw));
+  if (qkv_partial(h, T)) {
+    GemmEpi e;
+    e.mode = EPI_PARTIAL;
+    e.drain = kQkvDrain;
+    return gemm(h, h->xn, p.d, W, T, p.qkvw, p.d, e);
+  }
+  if (!fused_rope(h, T)) {
+    GemmEpi e = epi_act(h->qkv, p.qkvw);
+    e.drain = kQkvDrain;
+    return gemm(h, h->xn, p.d, W, T, p.qkvw, p.d, e);
+  }
   GemmEpi e;
+  e.drain = kQkvDrain;
   e.mode = EPI_QKV_ROPE;
   e.ldo = 128;
   e.rope.pos0 = pos0;
@@ -435,9 +461,16 @@ static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const i
   const Plan& p = h->p;
   ProfScope ps(h, 1, 0.0);  // KV bytes depend on device-resident lengths: the bench computes them
   cudaError_t e = cudaSuccess;
-  if (!fused_rope(h, T))
+  if (qkv_partial(h, T)) {
+    PartialGeom g;
+    e = gemm_partial_geom(T, p.qkvw, p.d, &g, kQkvDrain)
+            ? launch_rope_partial(h->gpart, &g, T, q_len, pos0, (const float2*)h->rope, p.Hq, p.Hkv, h->bt, p.pps,
+                                  h->kp(layer), h->vp(layer), h->qrot, h->st)
+            : cudaErrorInvalidValue;
+  } else if (!fused_rope(h, T)) {
     e = launch_rope_append(h->bf, h->qkv, T, q_len, pos0, h->rope, p.Hq, p.Hkv, p.hd, h->bt, p.pps, h->kp(layer),
                            h->vp(layer), h->qrot, h->bf && p.hd == 128, h->st);
+  }
   if (e != cudaSuccess) return e;
   AttnParams ap{};
   ap.q = h->qrot;

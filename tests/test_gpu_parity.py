@@ -272,16 +272,23 @@ def test_fused_rope_epilogue_bit_exact(cfg, monkeypatch):
     """The QKV GEMM's fused RoPE / paged-append epilogue (small blocks) and the separate RoPE kernel
     (large blocks) rotate the same bf16 projections with the same operations: forcing either path
     for every block gives bit-identical logits, drafts and tokens (so choosing it per T keeps SD ==
-    AR and batch invariance)."""
+    AR and batch invariance).
+    The unfused path comes in two forms -- the GEMM's own head-tile fixup + the RoPE kernel, and
+    k-segment partials reduced by the RoPE kernel (launch_rope_partial) -- with the same additions
+    in the same order: all three agree bit for bit."""
     w, prompts = setup(cfg, seed=6, jitter=0.1)
     monkeypatch.setenv("SF_ROPE_FUSE_T", "0")
+    monkeypatch.setenv("SF_QKV_PARTIAL", "1")
+    partial = run_gpu(cfg, w, prompts, 12, want_logits=True)
+    monkeypatch.setenv("SF_QKV_PARTIAL", "0")
     unfused = run_gpu(cfg, w, prompts, 12, want_logits=True)
     monkeypatch.setenv("SF_ROPE_FUSE_T", "100000")
     fused = run_gpu(cfg, w, prompts, 12, want_logits=True)
-    assert fused["tokens"] == unfused["tokens"]
-    for s1, s2 in zip(unfused["steps"], fused["steps"]):
-        assert np.array_equal(s1["logits"], s2["logits"])
+    assert fused["tokens"] == unfused["tokens"] == partial["tokens"]
+    for s1, s2, s3 in zip(unfused["steps"], fused["steps"], partial["steps"]):
+        assert np.array_equal(s1["logits"], s2["logits"]) and np.array_equal(s1["logits"], s3["logits"])
         assert np.array_equal(s1["draft_logits"], s2["draft_logits"])
+        assert np.array_equal(s1["draft_logits"], s3["draft_logits"])
 
 
 @pytest.mark.parametrize("cfg", [MID, GQA], ids=["mha128", "gqa4"])

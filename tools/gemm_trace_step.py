@@ -44,3 +44,10 @@ for i in list(order[:6]) + list(order[len(order) // 2: len(order) // 2 + 2]):
         v = R[i, 8 + 4 * sg: 12 + 4 * sg]
         if not np.all(np.isnan(v)): segs.append("(" + ",".join(f"{x:.1f}" for x in v) + ")")
     print(f"    cta {i:3d} full0 {R[i,3]:.1f} mma_last {R[i,4]:.1f} epi_done {R[i,5]:.1f}: " + " ".join(segs))
+print("  final phase per CTA (flags, bulk, chunk0 add/stored, chunk1 add/stored, ...), epi_done:")
+for i in list(order[:6]) + list(order[len(order) // 2: len(order) // 2 + 2]):
+    print(f"    cta {i:3d}: " + " ".join(f"{x:.2f}" for x in R[i, 104:114]) + f"  | {R[i, 5]:.2f}")
+print("  chunk detail per CTA (c0=0: tmem, add, staged, stored | c0=96: tmem, add, staged, stored):")
+for i in list(order[:6]) + list(order[len(order) // 2: len(order) // 2 + 2]):
+    print(f"    cta {i:3d}: " + " ".join(f"{x:.2f}" for x in [R[i,114], R[i,106], R[i,116], R[i,107]]) + " | " +
+          " ".join(f"{x:.2f}" for x in [R[i,118], R[i,108], R[i,120], R[i,109]]))
