@@ -12,7 +12,7 @@ echo "launch list rc=$?"
 if [ -n "$FULL" ]; then
   $CMD > $OUT/plain2_b$B.log 2>&1 && \
   ncu --profile-from-start off --set full --clock-control none --import-source on \
-      -k "regex:gemm_sk_kernel|attn_fd_kernel|resid_norm|rope_append" -s ${SKIP:-12} -c ${COUNT:-6} \
+      -k "regex:gemm_sk_kernel|attn_fd_kernel|resid_norm|rope_append|rope_partial" -s ${SKIP:-12} -c ${COUNT:-6} \
       -o $OUT/full_b$B -f $CMD > $OUT/ncu_full_b$B.log 2>&1
   echo "full rc=$?"
 fi
