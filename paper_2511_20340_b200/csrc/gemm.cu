@@ -227,6 +227,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     }
     mbar_init(fixb, 1);
     fence_barrier_init();
+    SF_TR(125);
   }
   if (warp == 2) {
     if constexpr (kPair) {
@@ -237,9 +238,11 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     } else {
       tmem_alloc(tmem_slot, p.tmem_cols);
     }
+    if (lane == 0) SF_TR(126);
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) SF_TR(127);
   if constexpr (kPair) cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
@@ -443,14 +446,35 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     // (pair-interleaved weight rows). The accumulator is rounded to bf16 first -- exactly the values
     // the unfused path (bf16 QKV output, then the RoPE kernel) rotates -- so both paths give the same
     // bits. Lane l resolves token c0 + l's position and destination row once; emit(q, dim, y, row).
+    // (small T) token c0 + lane's position and destination row for tile vt_, resolved while the MMA
+    // still runs, and the RoPE table lines of the chunk's tokens pulled into L1: the epilogue then
+    // starts from the accumulator instead of a pos -> page table -> table chain of L2 round trips
+    int pre_pos = 0, pre_c0 = -1, pre_vt = -1;
+    unsigned long long pre_row = 0;
+    auto rope_prefetch = [&](int c0, int vt_) {
+      const RopeEpi& R = p.epi.rope;
+      const int nq = min(32, p.T - c0);
+      pre_c0 = c0;
+      pre_vt = vt_;
+      if (lane < nq) {
+        const int t = c0 + lane + R.t0;
+        pre_pos = R.pos0[t / R.q_len] + t % R.q_len;
+        pre_row = reinterpret_cast<unsigned long long>(rope_dst_row(c0 + lane, vt_));
+      }
+      if (vt_ < R.Hq + R.Hkv)
+        for (int q = 0; q < nq; ++q) {
+          const int pq = __shfl_sync(0xffffffffu, pre_pos, q);
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(R.table + (size_t)pq * 64 + (m >> 1)));
+        }
+    };
     auto rope_rows = [&](float (&v)[32], int c0, int nq, int vt_, auto emit) {
       const RopeEpi& R = p.epi.rope;
       const bool odd = lane & 1;
       const int i = m >> 1, dim = odd ? 64 + i : i;
       const bool rot = vt_ < R.Hq + R.Hkv;
-      int my_pos = 0;
-      unsigned long long my_row = 0;
-      if (lane < nq) {
+      int my_pos = pre_pos;
+      unsigned long long my_row = pre_row;
+      if (lane < nq && (c0 != pre_c0 || vt_ != pre_vt)) {
         const int t = c0 + lane + R.t0;
         my_pos = R.pos0[t / R.q_len] + t % R.q_len;
         my_row = reinterpret_cast<unsigned long long>(rope_dst_row(c0 + lane, vt_));
@@ -603,6 +627,12 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       fix_ph ^= 1u;
     };
 
+    // (small T, head pieces with one or two partner segments) the partners' partials of this
+    // thread's chunk, loaded while the MMA still runs -- see the driver loop
+    constexpr int kPreT = 8;  // rows (T <= kPreT: B = 1 verify / draft blocks)
+    float pf1[kPreT], pf2[kPreT];
+    bool pre_fix = false;
+
     // Epilogue of segment [u, se) of tile t from TMEM buffer b by ng groups (this thread: group
     // gid, barrier over nthr threads). final: every MMA of the CTA has completed (ring idle).
     auto segment_epilogue = [&](long long u, int t, long long se, int b, int gid, int ng, int nthr, bool final,
@@ -642,13 +672,14 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       // thing), in k order, then the output epilogue
       int c_lo = c + 1, c_hi = c;
       if (is_head) c_hi = sk_group_of((int)(te - 1), p.G, p.n_tiles, kb, p.drain);
-      if (is_head) {
+      if (is_head && !pre_fix) {
         if (lead)
           for (int cc = c_lo; cc <= c_hi; ++cc)
             while (ld_acquire(&p.flags[cc * CG + (int)rank]) == 0) {
             }
         named_sync(final ? 5 : 1, nthr);
       }
+      if (lead && !final) SF_TR(122);  // (small T) partners' partials published
       if (lead && final) SF_TR(104);
       const int n_o = c_hi - c_lo + 1;
       // (small T: a few rows -- direct loads / stores beat the TMA round trip and the staging barriers)
@@ -676,6 +707,13 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
               for (int q = 0; q < 32; ++q)
                 if (c0 + q < p.T) v[q] += sp[q * BM];
             }
+          } else if (pre_fix) {  // fixed k order
+#pragma unroll
+            for (int q = 0; q < kPreT; ++q) v[q] += pf1[q];
+            if (n_o == 2) {
+#pragma unroll
+              for (int q = 0; q < kPreT; ++q) v[q] += pf2[q];
+            }
           } else {
             for (int cc = c_lo; cc <= c_hi; cc += 2) {  // fixed k order; two segments' loads in flight
               const float* s0 = p.partial + (size_t)(cc * CG + (int)rank) * p.Tp * BM + m;
@@ -697,6 +735,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
             }
           }
           const int nq = min(32, p.T - c0);
+          if (lead && !final && c0 == 0) SF_TR(123);
           if (lead && final && c0 < 4 * cstep) SF_TR(106 + 2 * (c0 / cstep));  // TMEM + adds done
           if constexpr (kStageable) {
             if (stage_out) staged_store(v, c0, nq, vt, gid);
@@ -704,6 +743,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           } else {
             direct_store(v, c0, nq, vt);
           }
+          if (lead && !final && c0 == 0) SF_TR(124);
           if (lead && final && c0 < 4 * cstep) SF_TR(107 + 2 * (c0 / cstep));  // stored
         }
         if (bulk) named_sync(final ? 5 : 1, nthr);  // smem pass consumed before the next one overwrites it
@@ -739,6 +779,33 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           ng = 3;
           nthr = 384;
           gid = warp < 4 ? 2 : gid;
+        }
+        if constexpr (MODE == EPI_QKV_ROPE) {
+          const bool out_seg = u == (long long)t * kb;  // head or full tile: this CTA writes the rows
+          if (!final && out_seg && gid * 32 < p.T) rope_prefetch(gid * 32, t * CG + (int)rank);
+        }
+        // small T, a head piece with one or two partner segments: wait for the partners' flags and
+        // load their partials of this thread's chunk now, off the critical path after the last MMA
+        pre_fix = false;
+        if (mode != EPI_PARTIAL && !final && p.T <= kPreT && u == (long long)t * kb && se < (long long)(t + 1) * kb) {
+          const int c_hi = sk_group_of(t * kb + kb - 1, p.G, p.n_tiles, kb, p.drain);
+          const int n_o = c_hi - c;
+          if (n_o >= 1 && n_o <= 2) {
+            for (int cc = c + 1; cc <= c_hi; ++cc)
+              while (ld_acquire(&p.flags[cc * CG + (int)rank]) == 0) {
+              }
+            if (gid == 0) {
+              const float* s0 = p.partial + (size_t)((c + 1) * CG + (int)rank) * p.Tp * BM + m;
+              const float* s1 = s0 + (size_t)CG * p.Tp * BM;
+#pragma unroll
+              for (int q = 0; q < kPreT; ++q) pf1[q] = q < p.T ? __ldcg(&s0[(size_t)q * BM]) : 0.f;
+              if (n_o == 2) {
+#pragma unroll
+                for (int q = 0; q < kPreT; ++q) pf2[q] = q < p.T ? __ldcg(&s1[(size_t)q * BM]) : 0.f;
+              }
+            }
+            pre_fix = true;
+          }
         }
         mbar_wait_sleep(&accf[b], (uint32_t)(seg / p.nbuf) & 1u);
         if (lead && seg < 4) SF_TR(8 + 4 * seg + 2);

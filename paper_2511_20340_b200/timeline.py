@@ -74,3 +74,18 @@ def critical_path(rec: np.ndarray, key=name) -> dict:
     span = (max(L["t1"] for L in Ls) - t_first) / 1e3
     return {"span_us": span, "gap_us": gap, "exposed": dict(exposed), "dur": dict(dur), "count": dict(cnt),
             "launches": len(Ls), "_launches": Ls, "_t_first": t_first}
+
+
+def spans_between(rec: np.ndarray, start_kid: int, end_kind: int) -> list[float]:
+    """Per occurrence: dependency release of a launch with kid == start_kid -> dependency release of
+    the next launch of kind end_kind (us). E.g. the verify forward of a decode step: the verify-row
+    builder (kind 13, param 0) to the accept kernel (kind 10)."""
+    Ls = launches(rec[(rec["kid"] >> 24) != KT_ITEM])
+    out, start = [], None
+    for L in Ls:
+        if L["kid"] == start_kid:
+            start = L["tw"]
+        elif (L["kid"] >> 24) == end_kind and start is not None:
+            out.append((L["tw"] - start) / 1e3)
+            start = None
+    return out

@@ -27,3 +27,12 @@ def test_critical_path_partitions_span():
     assert abs(sum(cp["exposed"].values()) + cp["gap_us"] - cp["span_us"]) < 1e-9
     by_class = tl.critical_path(rec, key=tl.kclass)
     assert set(by_class["exposed"]) == {"gemm", "norm", "attention"}
+
+
+def test_spans_between():
+    us = 1000
+    rows, acc = 13 << 24, 10 << 24
+    rec = _rec([(13, 0, 0, 1 * us, 2 * us), (1, 4096 | (64 << 15), 2 * us, 2 * us, 9 * us), (10, 4, 9 * us, 10 * us, 11 * us),
+                (13, 1, 11 * us, 11 * us, 12 * us),  # prefill row builder: not a verify start
+                (13, 0, 20 * us, 20 * us, 21 * us), (10, 4, 24 * us, 25 * us, 26 * us)])
+    assert tl.spans_between(rec, rows, acc >> 24) == [9.0, 5.0]

@@ -51,3 +51,13 @@ print("  chunk detail per CTA (c0=0: tmem, add, staged, stored | c0=96: tmem, ad
 for i in list(order[:6]) + list(order[len(order) // 2: len(order) // 2 + 2]):
     print(f"    cta {i:3d}: " + " ".join(f"{x:.2f}" for x in [R[i,114], R[i,106], R[i,116], R[i,107]]) + " | " +
           " ".join(f"{x:.2f}" for x in [R[i,118], R[i,108], R[i,120], R[i,109]]))
+print("  small-T head epilogue per CTA (epi_ready(last seg), flags, tmem+fixup, stored, epi_done):")
+for i in list(order[:6]) + list(order[len(order) // 2: len(order) // 2 + 2]):
+    ns = [sg for sg in range(4) if not np.isnan(R[i, 10 + 4 * sg])]
+    er = R[i, 10 + 4 * ns[-1]] if ns else np.nan
+    print(f"    cta {i:3d}: " + " ".join(f"{x:.2f}" for x in [er, R[i,122], R[i,123], R[i,124], R[i, 11 + 4 * ns[-1]] if ns else np.nan]))
+print("  setup detail (start, barriers init, tmem alloc, syncthreads, cluster sync = setup) med: " +
+      " ".join(f"{np.nanmedian(R[:, c]):.2f}" for c in (0, 125, 126, 127, 1)))
+late = np.argsort(-np.nan_to_num(R[:, 0]))[:4]
+for i in late:
+    print(f"    late cta {i:3d}: " + " ".join(f"{R[i, c]:.2f}" for c in (0, 125, 126, 127, 1, 2, 3)))
