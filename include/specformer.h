@@ -48,7 +48,7 @@ typedef enum {
   SF_ERR_CAPACITY = 3,   /* seq_len + k + 1 would exceed max_seq                             */
   SF_ERR_STATE = 4,      /* call order violated: init -> prefill -> (draft -> verify -> accept)* */
   SF_ERR_CUDA = 5,       /* a CUDA runtime call failed                                       */
-  SF_ERR_NCCL = 6,       /* reserved (tensor-parallel path)                                  */
+  SF_ERR_NCCL = 6,       /* NCCL communicator setup failed (tensor-parallel path)            */
   SF_ERR_NONFINITE = 7,  /* NaN/Inf met in logits (SPEC S26: an error condition)             */
   SF_ERR_UNSUPPORTED = 8 /* configuration not supported by this build                        */
 } sf_status;
@@ -71,7 +71,7 @@ typedef struct {
   float rms_eps;       /* 1e-6 (reading C3)                                                */
   int32_t dtype;       /* sf_dtype: SF_FP32 (fp32 weights/activations/KV, SIMT kernels) or
                           SF_BF16 (bf16 weights/KV, tcgen05 GEMMs, fp32 residual/accum)     */
-  int32_t tp_size, tp_rank; /* must be 1, 0 in this build                                  */
+  int32_t tp_size, tp_rank; /* tensor parallelism (see sf_nccl_attach); 1, 0 = one GPU        */
   uint64_t flags;
 } sf_config;
 
@@ -200,6 +200,33 @@ int32_t sf_debug_ktrace(void* dst_host, int32_t cap);
  * after the call: the probes read a device-global record pointer, null when off. Synchronises
  * the device and clears the log. Returns 0, or -1 if the 80 MB log cannot be allocated. */
 int32_t sf_debug_ktrace_enable(int32_t on);
+
+/* ---- Tensor parallelism (Megatron-style; sf_config.tp_size > 1, bf16 only) ----
+ * Rank r of tp holds: q / kv heads [r H/tp, (r+1) H/tp) of every attention (QKV rows and O columns
+ * sliced alike; the KV pools hold the rank's kv heads), FFN rows [r F/tp, ..) of gate/up and the
+ * matching down-proj columns, the LM head's vocabulary rows [v0, v1) (whole 128-row tiles split as
+ * evenly as possible; sf_weight_table reports the rank's shapes), W_D's input columns [r 4d/tp, ..)
+ * (the rank's slice of I_Cat); embedding, norms, W_P / b_P and the residual stream are replicated.
+ * The row-parallel outputs (base O / down, context W_D / O, draft O / down) are summed over the
+ * ranks in fp32 before the residual add; the argmax max-reduces per-row packed keys
+ * (orderable float logit << 32 | ~global id: largest logit, lowest id on ties). Every rank computes
+ * the same tokens. Logits copied out (verify_step / draft_step) are the rank's vocabulary shard
+ * [rows, v1 - v0]. One of the two collectives below must be attached before prefill. */
+/* 128-byte NCCL unique id for sf_nccl_attach (rank 0 creates it; the caller broadcasts it).
+ * Returns 0, -1 if NCCL is unavailable in this build. */
+int32_t sf_nccl_unique_id(uint8_t* out_128);
+/* Create this handle's NCCL communicator (nranks == tp_size, rank == tp_rank; call on the handle's
+ * device). Reductions run as ncclAllReduce on the handle's stream and are captured by
+ * SF_FLAG_CUDA_GRAPH. Errors: SF_ERR_ARG, SF_ERR_STATE (already attached), SF_ERR_NCCL. */
+sf_status sf_nccl_attach(sf_handle* h, const uint8_t* id_128, int32_t nranks, int32_t rank);
+/* Tests without a second GPU: n (<= 8) handles of one process on one device, each driven by its
+ * own host thread, reduce through device memory with host barriers (rank order sums). Handles on
+ * a local group run eagerly (decode_steps does not capture). The group owns its device scratch;
+ * destroy it after its handles. */
+typedef struct sf_local_group sf_local_group;
+sf_local_group* sf_local_group_create(int32_t n);
+void sf_local_group_destroy(sf_local_group* g);
+sf_status sf_local_group_attach(sf_handle* h, sf_local_group* g, int32_t rank);
 
 #ifdef __cplusplus
 }

@@ -63,6 +63,11 @@ SIGNATURES = [
     ("sf_debug_gemm_trace", C.c_int32, [_P, C.c_int32]),
     ("sf_debug_ktrace", C.c_int32, [_P, C.c_int32]),
     ("sf_debug_ktrace_enable", C.c_int32, [C.c_int32]),
+    ("sf_nccl_unique_id", C.c_int32, [_P]),
+    ("sf_nccl_attach", C.c_int, [_P, _P, C.c_int32, C.c_int32]),
+    ("sf_local_group_create", _P, [C.c_int32]),
+    ("sf_local_group_destroy", None, [_P]),
+    ("sf_local_group_attach", C.c_int, [_P, _P, C.c_int32]),
 ]
 
 

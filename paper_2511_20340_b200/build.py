@@ -10,6 +10,23 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libspecformer.so")
 SOURCES = ["gemm.cu", "kernels.cu", "attn_fd.cu", "specformer.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir():
+    """The NCCL that ships with the torch wheel (nvidia/nccl: include/nccl.h, lib/libnccl.so.2)."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        roots = list(spec.submodule_search_locations) if spec and spec.submodule_search_locations else []
+    except Exception:
+        roots = []
+    for r in roots:
+        if os.path.exists(os.path.join(r, "include", "nccl.h")) and os.path.exists(os.path.join(r, "lib", "libnccl.so.2")):
+            return r
+    return None
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr"]
 
@@ -33,6 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in SOURCES:
         obj = os.path.join(odir, src.replace(".cu", ".o"))
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        if NCCL and src == "specformer.cu":
+            cmd[1:1] = ["-DSF_WITH_NCCL", "-I" + os.path.join(NCCL, "include")]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
@@ -45,6 +64,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(out)
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
+    if NCCL:
+        lib = os.path.join(NCCL, "lib")
+        cmd += ["-L" + lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

@@ -1220,8 +1220,8 @@ static int rn_ng(int d) {  // float4 groups per thread
 template <int NG>
 __global__ void __launch_bounds__(1024) resid_norm_kernel(
     const float* __restrict__ partial, int G, int kb, int drain, int CG, int n_tiles_cta, int T, int rep, int d,
-    const float* resid, const float* __restrict__ bias, float* out, float* tap, const float* __restrict__ gamma,
-    float eps, __nv_bfloat16* xn) {
+    const float* resid, const float* __restrict__ add, const float* __restrict__ bias, float* out, float* tap,
+    const float* __restrict__ gamma, float eps, __nv_bfloat16* xn) {
   constexpr int kRnBatch = 8 / NG;
   __shared__ int seg_n[kRnMaxTiles];
   __shared__ int seg_off[kRnMaxTiles][kRnMaxSeg];  // slot * T * 128 (the tile's k segments, k order)
@@ -1255,6 +1255,13 @@ __global__ void __launch_bounds__(1024) resid_norm_kernel(
   for (int j = 0; j < NG; ++j) {
     const int i = 4 * tid + 4 * nthr * j;  // column within the virtual row
     x[j] = resid ? *reinterpret_cast<const float4*>(resid + (size_t)r * d + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (add) {  // (tensor parallelism: the all-reduced row-parallel GEMM output)
+      const float4 a = *reinterpret_cast<const float4*>(add + (size_t)r * d + i);
+      x[j].x += a.x;
+      x[j].y += a.y;
+      x[j].z += a.z;
+      x[j].w += a.w;
+    }
     if (bias) {
       const float4 bb = *reinterpret_cast<const float4*>(bias + col0 + i);
       x[j].x += bb.x;
@@ -1322,8 +1329,8 @@ __global__ void __launch_bounds__(1024) resid_norm_kernel(
 }
 
 cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T, int rep, int d, const float* resid,
-                              const float* bias, float* out, float* tap, const float* gamma, float eps,
-                              __nv_bfloat16* xn, cudaStream_t st) {
+                              const float* add, const float* bias, float* out, float* tap, const float* gamma,
+                              float eps, __nv_bfloat16* xn, cudaStream_t st) {
   if (T * rep <= 0) return cudaSuccess;
   const int ng = rn_ng(d);
   if (!ng) return cudaErrorInvalidValue;
@@ -1342,13 +1349,13 @@ cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T,
   const dim3 grid(T * rep), block(d / (4 * ng));
   switch (ng) {
     case 1: return launch_k(resid_norm_kernel<1>, grid, block, 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, d, resid,
-                            bias, out, tap, gamma, eps, xn);
+                            add, bias, out, tap, gamma, eps, xn);
     case 2: return launch_k(resid_norm_kernel<2>, grid, block, 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, d, resid,
-                            bias, out, tap, gamma, eps, xn);
+                            add, bias, out, tap, gamma, eps, xn);
     case 3: return launch_k(resid_norm_kernel<3>, grid, block, 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, d, resid,
-                            bias, out, tap, gamma, eps, xn);
+                            add, bias, out, tap, gamma, eps, xn);
     default: return launch_k(resid_norm_kernel<4>, grid, block, 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, d, resid,
-                             bias, out, tap, gamma, eps, xn);
+                             add, bias, out, tap, gamma, eps, xn);
   }
 }
 

@@ -85,13 +85,14 @@ bool gemm_partial_geom(int T, int N, int K, PartialGeom* g, int drain = -1);
 
 // Fused consumer of EPI_PARTIAL (and plain residual/norm): for virtual row r (T*rep rows, source
 // row r / rep, columns [(r % rep) * d, +d) of the GEMM output):
-//   x = (resid ? resid[r] : 0) + (bias ? bias[col] : 0) + sum_k-segments partial   (fixed order)
+//   x = (resid ? resid[r] : 0) + (add ? add[r] : 0) + (bias ? bias[col] : 0) + sum_k-segments partial
+//   (fixed order; partial may be null -- add carries a tensor-parallel all-reduced GEMM output)
 //   out[r] = x (fp32, out may alias resid); tap[r] = x (optional);
 //   xn[r] = bf16(x / sqrt(mean(x^2) + eps) * gamma) (optional, gamma != null)
 bool resid_norm_supported(int d, int T, int N, int K);
 cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T, int rep, int d, const float* resid,
-                              const float* bias, float* out, float* tap, const float* gamma, float eps,
-                              __nv_bfloat16* xn, cudaStream_t s);
+                              const float* add, const float* bias, float* out, float* tap, const float* gamma,
+                              float eps, __nv_bfloat16* xn, cudaStream_t s);
 
 // Consumer of an EPI_PARTIAL QKV projection (bf16, head_dim 128, one 128-row tile per head, rows
 // pair-interleaved per head as for EPI_QKV_ROPE): for every (row t, head h) the head's k-segment

@@ -668,6 +668,39 @@ __global__ void argmax_final_kernel(const float* pval, const int* pidx, int R, i
   out[row] = (bi == INT_MAX) ? 0 : bi;
 }
 
+// Tensor parallelism (vocabulary-sharded LM head): each rank packs its rows' best (logit, id) as
+// key = orderable(logit) << 32 | (0xFFFFFFFF - (v0 + id)), the ranks max-reduce the keys (largest
+// logit, lowest id on ties -- the same rule as above over the whole vocabulary), and the winner's id
+// is unpacked.
+SF_DEV unsigned long long argmax_key(float v, unsigned id) {
+  unsigned u = __float_as_uint(v);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // order-preserving map of the finite floats
+  return ((unsigned long long)u << 32) | (0xFFFFFFFFu - id);
+}
+__global__ void argmax_key_kernel(const float* pval, const int* pidx, int R, int nsplit, int v0,
+                                  unsigned long long* keys) {
+  KtScope kt_(KT_ARGMAX_F, (uint32_t)(nsplit));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= R) return;
+  float bv = -INFINITY;
+  int bi = INT_MAX;
+  for (int s = 0; s < nsplit; ++s) better(bv, bi, pval[row * nsplit + s], pidx[row * nsplit + s]);
+  keys[row] = (bi == INT_MAX) ? 0ull : argmax_key(bv, (unsigned)(v0 + bi));
+}
+__global__ void argmax_unkey_kernel(const unsigned long long* keys, int R, int* out) {
+  KtScope kt_(KT_ARGMAX_F, 0u);
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= R) return;
+  const unsigned long long k = keys[row];
+  out[row] = k ? (int)(0xFFFFFFFFu - (unsigned)(k & 0xFFFFFFFFull)) : 0;
+}
+
 // ------------------------------------------------------------------------ accept + commit
 // P25: accept only drafts equal to the base model's greedy outputs. Single CTA (B <= 1024).
 __global__ void accept_kernel(int B, int k, const int* draft, const int* greedy, int* seq_len, int* n_prev,
@@ -888,6 +921,43 @@ cudaError_t launch_gather_rows(const float* src, int q_len, const int* idx, int 
            const_idx, d, dst);
   return cudaGetLastError();
 }
+struct BufList {
+  const void* p[8];
+};
+__global__ void reduce_bufs_kernel(BufList bl, int n, int64_t count, int max_u64, void* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    if (max_u64) {
+      unsigned long long m = 0;
+      for (int q = 0; q < n; ++q) m = max(m, reinterpret_cast<const unsigned long long*>(bl.p[q])[i]);
+      reinterpret_cast<unsigned long long*>(out)[i] = m;
+    } else {
+      float a = reinterpret_cast<const float*>(bl.p[0])[i];
+      for (int q = 1; q < n; ++q) a += reinterpret_cast<const float*>(bl.p[q])[i];  // buffer (rank) order
+      reinterpret_cast<float*>(out)[i] = a;
+    }
+  }
+}
+cudaError_t launch_reduce_bufs(const void* const* bufs, int n, int64_t count, bool max_u64, void* out,
+                               cudaStream_t s) {
+  if (n < 1 || n > 8) return cudaErrorInvalidValue;
+  BufList bl{};
+  for (int q = 0; q < n; ++q) bl.p[q] = bufs[q];
+  const int grid = (int)std::min<int64_t>(1184, (count + 255) / 256);
+  reduce_bufs_kernel<<<std::max(grid, 1), 256, 0, s>>>(bl, n, count, max_u64 ? 1 : 0, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_argmax_key(const float* logits, int R, int V, int v0, float* pval, int* pidx,
+                              unsigned long long* keys, int* err, cudaStream_t s) {
+  const int ns = argmax_splits(V);
+  const dim3 grid(ns, R);
+  launch_k(argmax_partial_kernel, dim3(grid), dim3(256), 0, s, logits, V, ns, pval, pidx, err);
+  return launch_k(argmax_key_kernel, dim3(SF_GRID(R, 128)), dim3(128), 0, s, pval, pidx, R, ns, v0, keys);
+}
+cudaError_t launch_argmax_unkey(const unsigned long long* keys, int R, int* out, cudaStream_t s) {
+  return launch_k(argmax_unkey_kernel, dim3(SF_GRID(R, 128)), dim3(128), 0, s, keys, R, out);
+}
+
 cudaError_t launch_argmax(const float* logits, int R, int V, float* pval, int* pidx, int* out, int* err,
                           cudaStream_t s) {
   const int ns = argmax_splits(V);

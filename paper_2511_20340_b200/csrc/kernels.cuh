@@ -50,6 +50,14 @@ cudaError_t launch_gather_rows(const float* src, int q_len, const int* idx, int 
                                float* dst, cudaStream_t s);
 cudaError_t launch_argmax(const float* logits, int R, int V, float* pval, int* pidx, int* out, int* err,
                           cudaStream_t s);
+// tensor parallelism: per-row packed (logit, v0 + id) keys of this vocabulary shard / their unpacking
+cudaError_t launch_argmax_key(const float* logits, int R, int V, int v0, float* pval, int* pidx,
+                              unsigned long long* keys, int* err, cudaStream_t s);
+cudaError_t launch_argmax_unkey(const unsigned long long* keys, int R, int* out, cudaStream_t s);
+// tensor parallelism, tests (one process, several handles): out[i] = sum / max over the n buffers in
+// buffer order
+cudaError_t launch_reduce_bufs(const void* const* bufs, int n, int64_t count, bool max_u64, void* out,
+                               cudaStream_t s);
 cudaError_t launch_accept(int B, int k, const int* draft, const int* greedy, int* seq_len, int* n_prev,
                           int* last_token, int* r_b, int* accept_len, int* emitted, int* step_counter,
                           int* accept_log, int* emitted_log, const int* log_cap /* device */, cudaStream_t s);

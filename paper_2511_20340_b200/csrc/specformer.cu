@@ -9,6 +9,11 @@
 //   verify_step : base forward over [last, d_1..d_k] (taps HS[0, L/2, L-1, L] kept) -> LM head
 //                  -> argmax -> greedy[k+1]
 //   accept      : m = longest matching prefix, commit seq_len += m + 1 (rollback moves no data)
+#include <condition_variable>
+#include <mutex>
+#ifdef SF_WITH_NCCL
+#include <nccl.h>
+#endif
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -52,7 +57,15 @@ bool valid_config(const sf_config* c, std::string* why) {
   if (!(c->rms_eps > 0.f)) return fail("rms_eps must be > 0");
   if (!(c->rope_theta > 0.f)) return fail("rope_theta must be > 0");
   if (c->dtype != SF_FP32 && c->dtype != SF_BF16) return fail("dtype must be SF_FP32 or SF_BF16");
-  if (c->tp_size != 1 || c->tp_rank != 0) return fail("tensor parallelism not supported in this build");
+  if (c->tp_size < 1 || c->tp_rank < 0 || c->tp_rank >= c->tp_size) return fail("need 0 <= tp_rank < tp_size");
+  if (c->tp_size > 1) {  // Megatron TP: heads / FFN / vocab / W_D input split over the ranks
+    const int tp = c->tp_size;
+    if (c->dtype != SF_BF16) return fail("tensor parallelism needs the bf16 path");
+    if (c->n_heads % tp || c->n_kv_heads % tp) return fail("n_heads and n_kv_heads must divide by tp_size");
+    if (c->d_ff % (64 * tp)) return fail("d_ff must be a multiple of 64 tp_size");
+    if ((4 * c->d_model) % (64 * tp)) return fail("4 d_model must be a multiple of 64 tp_size");
+    if (c->vocab % 128 || c->vocab / 128 < tp) return fail("vocab must be a multiple of 128 with >= tp_size tiles");
+  }
   if (c->d_ff % 64) return fail("d_ff must be a multiple of 64 (interleaved gate/up groups)");
   if (c->dtype == SF_BF16) {
     const int qkv = (c->n_heads + 2 * c->n_kv_heads) * c->head_dim;
@@ -63,9 +76,28 @@ bool valid_config(const sf_config* c, std::string* why) {
   return true;
 }
 
+// Tensor-parallel rank r of tp: q / kv heads [r H/tp, (r+1) H/tp), FFN rows [r F/tp, ..), the LM head's
+// vocabulary rows [v0, v1) (whole 128-row tiles, as even as possible), W_D's input columns
+// [r 4d/tp, ..). tp = 1: everything.
+static int tp_of(const sf_config* c) { return c->tp_size > 1 ? c->tp_size : 1; }
+static void vocab_shard(const sf_config* c, int* v0, int* v1) {
+  const int tp = tp_of(c), r = tp > 1 ? c->tp_rank : 0, tiles = c->vocab / 128;
+  if (tp == 1) {
+    *v0 = 0;
+    *v1 = c->vocab;
+    return;
+  }
+  *v0 = (int)((int64_t)tiles * r / tp) * 128;
+  *v1 = (int)((int64_t)tiles * (r + 1) / tp) * 128;
+}
+
 std::vector<TensorSpec> tensor_specs(const sf_config* c) {
-  const int64_t d = c->d_model, F = c->d_ff, V = c->vocab, k = c->draft_len;
-  const int64_t qkv = (int64_t)(c->n_heads + 2 * c->n_kv_heads) * c->head_dim, ao = (int64_t)c->n_heads * c->head_dim;
+  const int tp = tp_of(c);
+  int v0, v1;
+  vocab_shard(c, &v0, &v1);
+  const int64_t d = c->d_model, F = c->d_ff / tp, V = c->vocab, Vl = v1 - v0, k = c->draft_len;
+  const int64_t qkv = (int64_t)(c->n_heads + 2 * c->n_kv_heads) / tp * c->head_dim,
+                ao = (int64_t)c->n_heads / tp * c->head_dim;
   std::vector<TensorSpec> t;
   t.push_back({"embed", {V, d}, true});
   for (int l = 0; l < c->n_layers; ++l) {
@@ -78,10 +110,10 @@ std::vector<TensorSpec> tensor_specs(const sf_config* c) {
     t.push_back({p + "w_down", {d, F}, true});
   }
   t.push_back({"final_norm", {d}, false});
-  t.push_back({"lm_head", {V, d}, true});
+  t.push_back({"lm_head", {Vl, d}, true});
   if (k > 0) {
     t.push_back({"sf.group_scale", {4, d}, false});
-    t.push_back({"sf.w_d", {d, 4 * d}, true});
+    t.push_back({"sf.w_d", {d, 4 * d / tp}, true});
     t.push_back({"sf.ctx_norm", {d}, false});
     t.push_back({"sf.ctx_wqkv", {qkv, d}, true});
     t.push_back({"sf.ctx_wo", {d, ao}, true});
@@ -106,12 +138,14 @@ int64_t tensor_bytes(const sf_config* c, const TensorSpec& s) {
 
 // ----------------------------------------------------------------- workspace plan
 struct Plan {
-  int B, k, d, Hq, Hkv, hd, F, V, L, qkvw, ao;
+  int B, k, d, Hq, Hkv, hd, F, V, L, qkvw, ao;  // Hq, Hkv, F, V: this rank's share (tensor parallelism)
+  int tp, tp_rank, V_full, v0, wd_k;            // ranks, full vocabulary, vocab shard offset, W_D input width
   int pps, n_pages, nchunk, rows_v, rows_d, C_pf, rows_pf, R;
   int64_t act, kv_layer_bytes;
   // offsets
   int64_t o_k, o_v, o_bt, o_rope, o_resid, o_xn, o_qkv, o_qrot, o_attn, o_ffn, o_taps, o_ctx, o_idrow, o_D,
-      o_hlast, o_logits, o_dlogits, o_apo, o_apml, o_gpart, o_gcnt, o_amv, o_ami, o_ints, o_prompt, o_acnt;
+      o_hlast, o_logits, o_dlogits, o_apo, o_apml, o_gpart, o_gcnt, o_amv, o_ami, o_ints, o_prompt, o_acnt,
+      o_tpbuf, o_tpkey;
   int64_t n_acnt;
   int64_t gpart_elems, n_amrows;
   int64_t total;
@@ -122,11 +156,17 @@ Plan make_plan(const sf_config* c) {
   p.B = c->max_batch;
   p.k = c->draft_len;
   p.d = c->d_model;
-  p.Hq = c->n_heads;
-  p.Hkv = c->n_kv_heads;
+  p.tp = tp_of(c);
+  p.tp_rank = p.tp > 1 ? c->tp_rank : 0;
+  p.Hq = c->n_heads / p.tp;
+  p.Hkv = c->n_kv_heads / p.tp;
   p.hd = c->head_dim;
-  p.F = c->d_ff;
-  p.V = c->vocab;
+  p.F = c->d_ff / p.tp;
+  int v1 = 0;
+  vocab_shard(c, &p.v0, &v1);
+  p.V = v1 - p.v0;
+  p.V_full = c->vocab;
+  p.wd_k = 4 * c->d_model / p.tp;
   p.L = c->n_layers;
   p.qkvw = (p.Hq + 2 * p.Hkv) * p.hd;
   p.ao = p.Hq * p.hd;
@@ -143,7 +183,7 @@ Plan make_plan(const sf_config* c) {
   // split-K partial scratch: worst case over every GEMM shape at R rows
   const bool bf = c->dtype == SF_BF16;
   const int shapes[][2] = {{p.qkvw, p.d}, {p.d, p.ao}, {2 * p.F, p.d}, {p.d, p.F}, {p.V, p.d},
-                           {p.d, 4 * p.d}, {std::max(1, p.k) * p.d, p.d}};
+                           {p.d, p.wd_k}, {std::max(1, p.k) * p.d, p.d}};
   p.gpart_elems = 0;
   for (auto& s : shapes) p.gpart_elems = std::max<int64_t>(p.gpart_elems, gemm_partial_elems(bf, std::min(p.R, 512), s[0], s[1]));
   p.n_amrows = std::max(p.rows_v, std::max(p.rows_d, p.B));
@@ -181,6 +221,8 @@ Plan make_plan(const sf_config* c) {
   p.o_ami = take(p.n_amrows * argmax_splits(p.V) * 4);
   p.o_ints = take((int64_t)(16 * p.B + 2 * p.R + 8 + p.rows_v * 2 + p.rows_d) * 4);
   p.o_prompt = take((int64_t)p.B * c->max_seq * 4);
+  p.o_tpbuf = p.tp > 1 ? take((int64_t)p.R * p.d * 4) : 0;   // row-parallel GEMM output, all-reduced
+  p.o_tpkey = p.tp > 1 ? take(p.n_amrows * 8) : 0;           // packed (logit, id) argmax keys, max-reduced
   p.total = o;
   return p;
 }
@@ -215,6 +257,16 @@ struct sf_handle {
   float *resid, *qrot, *taps, *ctx, *idrow, *D, *hlast, *logits, *dlogits, *apo, *apml, *gpart, *amv;
   void *xn, *qkv, *attn, *ffn;
   int *gcnt, *ami, *acnt;
+  // tensor parallelism: row-parallel GEMM output / argmax keys, and the collective that reduces them
+  float* tpbuf = nullptr;
+  unsigned long long* tpkey = nullptr;
+  struct Coll {
+    cudaError_t (*sum_f32)(void* ctx, float* buf, int64_t n, cudaStream_t s) = nullptr;
+    cudaError_t (*max_u64)(void* ctx, unsigned long long* buf, int64_t n, cudaStream_t s) = nullptr;
+    void* ctx = nullptr;
+    bool graph_safe = false;  // only device work is enqueued (NCCL): decode_steps may capture it
+  } coll;
+  void* nccl_comm = nullptr;
   int *tok_rows, *pos0_pf, *seq_len, *n_prev, *last_token, *r_b, *prompt_len, *draft, *greedy, *accept_len,
       *emitted, *err, *step_counter, *g_pf, *prompt, *d_logcap;
   // state
@@ -375,9 +427,40 @@ static cudaError_t rmsnorm(sf_handle* h, const float* in, int in_ld, const float
 // partials (EPI_PARTIAL) and resid_norm_kernel sums them in k order while applying the residual and
 // the next norm. Returns false (nothing launched) when the shape does not allow it; callers then use
 // the unfused ADD / STORE epilogue + rmsnorm. rep > 1 views each GEMM row as rep rows of d columns.
+// Tensor parallelism: every rank holds the full residual stream and a K-slice of the row-parallel
+// weights (O, down, W_D: row_parallel = true); its GEMM output is a partial sum over the ranks, so
+// the rank writes it dense (fp32), the collective sums it over the ranks (rank order / NCCL's), and
+// the consumer adds it to the residual before the norm.
+static cudaError_t tp_sum(sf_handle* h, float* buf, int64_t n) {
+  if (!h->coll.sum_f32) {
+    h->err_msg = "tensor parallelism: no collective attached (sf_nccl_attach / sf_local_group_attach)";
+    return cudaErrorNotReady;
+  }
+  h->launches++;
+  return h->coll.sum_f32(h->coll.ctx, buf, n, h->st);
+}
+static cudaError_t tp_max(sf_handle* h, unsigned long long* buf, int64_t n) {
+  if (!h->coll.max_u64) {
+    h->err_msg = "tensor parallelism: no collective attached (sf_nccl_attach / sf_local_group_attach)";
+    return cudaErrorNotReady;
+  }
+  h->launches++;
+  return h->coll.max_u64(h->coll.ctx, buf, n, h->st);
+}
+
 static bool gemm_resid_norm(sf_handle* h, cudaError_t* err, const void* A, int lda, const void* W, int T, int N,
                             int K, int rep, const float* resid, const float* bias, float* out, float* tap,
-                            const float* gamma) {
+                            const float* gamma, bool row_parallel = false) {
+  if (row_parallel && h->p.tp > 1) {
+    if ((*err = gemm(h, A, lda, W, T, N, K, epi_f32(h->tpbuf, N))) != cudaSuccess) return true;
+    if ((*err = tp_sum(h, h->tpbuf, (int64_t)T * N)) != cudaSuccess) return true;
+    ProfScope ps(h, 2, (double)T * N * 4.0 * 3);
+    h->launches++;
+    *err = dbg_sync(h, "resid_norm(tp)", launch_resid_norm(nullptr, nullptr, T, rep, h->p.d, resid, h->tpbuf, bias, out,
+                                                          tap, gamma, h->c.rms_eps,
+                                                          gamma ? (__nv_bfloat16*)h->xn : nullptr, h->st));
+    return true;
+  }
   if (!h->bf || T > 512) return false;
   if (!resid_norm_supported(h->p.d, T, N, K)) return false;
   PartialGeom g;
@@ -387,8 +470,8 @@ static bool gemm_resid_norm(sf_handle* h, cudaError_t* err, const void* A, int l
   if ((*err = gemm(h, A, lda, W, T, N, K, e)) != cudaSuccess) return true;
   ProfScope ps(h, 2, (double)T * N * 4.0 * 3);
   h->launches++;
-  *err = dbg_sync(h, "resid_norm", launch_resid_norm(h->gpart, &g, T, rep, h->p.d, resid, bias, out, tap, gamma,
-                                                     h->c.rms_eps, gamma ? (__nv_bfloat16*)h->xn : nullptr, h->st));
+  *err = dbg_sync(h, "resid_norm", launch_resid_norm(h->gpart, &g, T, rep, h->p.d, resid, nullptr, bias, out, tap,
+                                                     gamma, h->c.rms_eps, gamma ? (__nv_bfloat16*)h->xn : nullptr, h->st));
   return true;
 }
 
@@ -504,7 +587,7 @@ static cudaError_t base_forward(sf_handle* h, int T, int q_len, const int* pos0,
   const int64_t tstride = (int64_t)p.R * p.d;
   int tl[4];
   taps_layers(p.L, tl);
-  cudaError_t e = launch_embed(h->bf, h->tok_rows, h->embed, T, p.d, p.V, h->resid, h->taps, h->st);
+  cudaError_t e = launch_embed(h->bf, h->tok_rows, h->embed, T, p.d, p.V_full, h->resid, h->taps, h->st);
   h->launches++;
   if (e != cudaSuccess) return e;
   for (int g = 1; g < 4; ++g)
@@ -517,7 +600,7 @@ static cudaError_t base_forward(sf_handle* h, int T, int q_len, const int* pos0,
     if ((e = attn_layer(h, l, T, q_len, pos0, max_key))) return e;
     // o-proj + residual + RMS_ffn
     if (!gemm_resid_norm(h, &e, h->attn, p.ao, w.wo, T, p.d, p.ao, 1, h->resid, nullptr, h->resid, nullptr,
-                         w.ffn_norm)) {
+                         w.ffn_norm, true)) {
       if ((e = gemm(h, h->attn, p.ao, w.wo, T, p.d, p.ao, epi_add(h->resid, p.d, nullptr)))) return e;
       e = rmsnorm(h, h->resid, p.d, w.ffn_norm, T, h->xn, p.d);
     }
@@ -533,7 +616,7 @@ static cudaError_t base_forward(sf_handle* h, int T, int q_len, const int* pos0,
       if (tl[g] == l + 1 && first < 0) first = g;
     float* tap = first >= 0 ? h->taps + first * tstride : nullptr;
     const float* next_g = (l + 1 < p.L) ? h->lw[l + 1].attn_norm : (final_norm ? h->final_norm : nullptr);
-    if (gemm_resid_norm(h, &e, h->ffn, p.F, w.wdown, T, p.d, p.F, 1, h->resid, nullptr, h->resid, tap, next_g)) {
+    if (gemm_resid_norm(h, &e, h->ffn, p.F, w.wdown, T, p.d, p.F, 1, h->resid, nullptr, h->resid, tap, next_g, true)) {
       xn_ready = next_g != nullptr;
     } else {
       if ((e = gemm(h, h->ffn, p.F, w.wdown, T, p.d, p.F, epi_add(h->resid, p.d, tap)))) return e;
@@ -556,8 +639,10 @@ static cudaError_t ctx_forward(sf_handle* h, int T, int q_len, const int* pos0, 
     return e;
   h->launches++;
   // X = W_D I_Cat -> ctx, xn = RMS_c(X)
-  if (!gemm_resid_norm(h, &e, h->xn, 4 * p.d, h->w_d, T, p.d, 4 * p.d, 1, nullptr, nullptr, h->ctx, nullptr,
-                       h->ctx_norm)) {
+  // (tensor parallelism: this rank's W_D input columns [r 4d/tp, ..) of I_Cat)
+  const void* icat = (const char*)h->xn + (size_t)p.tp_rank * p.wd_k * p.act;
+  if (!gemm_resid_norm(h, &e, icat, 4 * p.d, h->w_d, T, p.d, p.wd_k, 1, nullptr, nullptr, h->ctx, nullptr,
+                       h->ctx_norm, true)) {
     if ((e = gemm(h, h->xn, 4 * p.d, h->w_d, T, p.d, 4 * p.d, epi_f32(h->ctx, p.d)))) return e;
     e = rmsnorm(h, h->ctx, p.d, h->ctx_norm, T, h->xn, p.d);
   }
@@ -565,7 +650,8 @@ static cudaError_t ctx_forward(sf_handle* h, int T, int q_len, const int* pos0, 
   if ((e = qkv_gemm(h, h->ctx_wqkv, p.L, T, q_len, pos0))) return e;
   if ((e = attn_layer(h, p.L, T, q_len, pos0, max_key))) return e;
   // I_D = X + MSA(...)
-  if (!gemm_resid_norm(h, &e, h->attn, p.ao, h->ctx_wo, T, p.d, p.ao, 1, h->ctx, nullptr, h->ctx, nullptr, nullptr))
+  if (!gemm_resid_norm(h, &e, h->attn, p.ao, h->ctx_wo, T, p.d, p.ao, 1, h->ctx, nullptr, h->ctx, nullptr, nullptr,
+                       true))
     e = gemm(h, h->attn, p.ao, h->ctx_wo, T, p.d, p.ao, epi_add(h->ctx, p.d, nullptr));
   return e;
 }
@@ -578,6 +664,12 @@ static cudaError_t head_argmax(sf_handle* h, const float* src, int T, float* log
   if ((e = gemm(h, h->xn, p.d, h->lm_head, T, p.V, p.d, epi_f32(logits, p.V)))) return e;
   h->launches += 2;
   ProfScope ps(h, 3, (double)T * p.V * 4.0);
+  if (p.tp > 1) {  // vocabulary-sharded head: max-reduce the shards' packed (logit, id) keys
+    if ((e = launch_argmax_key(logits, T, p.V, p.v0, h->amv, h->ami, h->tpkey, h->err, h->st))) return e;
+    if ((e = tp_max(h, h->tpkey, T))) return e;
+    h->launches++;
+    return launch_argmax_unkey(h->tpkey, T, out, h->st);
+  }
   return launch_argmax(logits, T, p.V, h->amv, h->ami, out, h->err, h->st);
 }
 
@@ -613,7 +705,7 @@ static cudaError_t do_draft(sf_handle* h) {
     return e;
   h->launches++;
   if (!gemm_resid_norm(h, &e, h->attn, p.ao, h->blk_wo, Tk, p.d, p.ao, 1, h->D, nullptr, h->D, nullptr,
-                       h->blk_ffn_norm)) {
+                       h->blk_ffn_norm, true)) {
     if ((e = gemm(h, h->attn, p.ao, h->blk_wo, Tk, p.d, p.ao, epi_add(h->D, p.d, nullptr)))) return e;
     e = rmsnorm(h, h->D, p.d, h->blk_ffn_norm, Tk, h->xn, p.d);
   }
@@ -625,7 +717,7 @@ static cudaError_t do_draft(sf_handle* h) {
   if ((e = gemm(h, h->xn, p.d, h->blk_wgu, Tk, 2 * p.F, p.d, sw))) return e;
   // E = Y + SwiGLU(...); xn = RMS_f(E) (shared frozen final norm, C8)
   bool xn_ready = gemm_resid_norm(h, &e, h->ffn, p.F, h->blk_wdown, Tk, p.d, p.F, 1, h->D, nullptr, h->D, nullptr,
-                                  h->final_norm);
+                                  h->final_norm, true);
   if (!xn_ready) e = gemm(h, h->ffn, p.F, h->blk_wdown, Tk, p.d, p.F, epi_add(h->D, p.d, nullptr));
   if (e) return e;
   // shared frozen LM head -> k draft tokens
@@ -655,6 +747,82 @@ static cudaError_t do_accept(sf_handle* h, int* acc_log, int* em_log) {
 static cudaError_t copy_out(sf_handle* h, void* dst, const void* src, size_t bytes) {
   if (!dst) return cudaSuccess;
   return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->st);
+}
+
+// ================================================================= collectives (tensor parallelism)
+#ifdef SF_WITH_NCCL
+static cudaError_t nccl_sum_f32(void* ctx, float* buf, int64_t n, cudaStream_t s) {
+  return ncclAllReduce(buf, buf, (size_t)n, ncclFloat32, ncclSum, (ncclComm_t)ctx, s) == ncclSuccess
+             ? cudaSuccess
+             : cudaErrorUnknown;
+}
+static cudaError_t nccl_max_u64(void* ctx, unsigned long long* buf, int64_t n, cudaStream_t s) {
+  return ncclAllReduce(buf, buf, (size_t)n, ncclUint64, ncclMax, (ncclComm_t)ctx, s) == ncclSuccess
+             ? cudaSuccess
+             : cudaErrorUnknown;
+}
+#endif
+
+// Several handles of one process on one device, one host thread each (tests: tensor parallelism
+// without a second GPU). Every reduction: each rank records its input, a host barrier, each rank
+// sums / maxes all inputs in rank order into its own scratch, a barrier, each copies the result
+// back, a barrier (events and inputs are reused by the next reduction). Host barriers cannot be
+// captured, so handles on a local group run their steps eagerly.
+struct sf_local_group {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t gen = 0;
+  std::vector<const void*> bufs;
+  std::vector<cudaEvent_t> ev_in, ev_mid;
+  std::vector<void*> tmp;
+  std::vector<size_t> tmp_bytes;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const int64_t g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+struct LocalCtx {
+  sf_local_group* g;
+  int rank;
+};
+static cudaError_t local_reduce(void* ctx, void* buf, int64_t n, bool mx, cudaStream_t s) {
+  LocalCtx* c = (LocalCtx*)ctx;
+  sf_local_group* g = c->g;
+  const int r = c->rank;
+  const size_t bytes = (size_t)n * (mx ? 8 : 4);
+  if (g->tmp_bytes[r] < bytes) {  // (test scratch, owned by the group)
+    cudaStreamSynchronize(s);
+    if (g->tmp[r]) cudaFree(g->tmp[r]);
+    if (cudaMalloc(&g->tmp[r], bytes) != cudaSuccess) return cudaErrorMemoryAllocation;
+    g->tmp_bytes[r] = bytes;
+  }
+  g->bufs[r] = buf;
+  cudaEventRecord(g->ev_in[r], s);
+  g->barrier();
+  for (int q = 0; q < g->n; ++q) cudaStreamWaitEvent(s, g->ev_in[q], 0);
+  cudaError_t e = launch_reduce_bufs(g->bufs.data(), g->n, n, mx, g->tmp[r], s);
+  cudaEventRecord(g->ev_mid[r], s);
+  g->barrier();
+  for (int q = 0; q < g->n; ++q) cudaStreamWaitEvent(s, g->ev_mid[q], 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(buf, g->tmp[r], bytes, cudaMemcpyDeviceToDevice, s);
+  g->barrier();
+  return e;
+}
+static cudaError_t local_sum_f32(void* ctx, float* buf, int64_t n, cudaStream_t s) {
+  return local_reduce(ctx, buf, n, false, s);
+}
+static cudaError_t local_max_u64(void* ctx, unsigned long long* buf, int64_t n, cudaStream_t s) {
+  return local_reduce(ctx, buf, n, true, s);
 }
 
 // ================================================================= C ABI
@@ -783,12 +951,11 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
   }  {
     // GEMM weight chain in launch order: draft (W_D, ctx QKV/O, W_P, block QKV/O/gate-up/down, LM
     // head), then verify (per layer QKV, O, gate-up, down; LM head), then the next step's draft
-    const int64_t d = cfg->d_model, F = cfg->d_ff, V = cfg->vocab, k = cfg->draft_len;
-    const int64_t qkv = (int64_t)(cfg->n_heads + 2 * cfg->n_kv_heads) * cfg->head_dim,
-                  ao = (int64_t)cfg->n_heads * cfg->head_dim;
+    const int64_t d = cfg->d_model, F = h->p.F, V = h->p.V, k = cfg->draft_len;
+    const int64_t qkv = h->p.qkvw, ao = h->p.ao;
     auto add = [&](const void* w, int64_t n, int64_t kk) { h->wchain.push_back({w, (size_t)(n * kk * 2)}); };
     if (k > 0) {
-      add(h->w_d, d, 4 * d);
+      add(h->w_d, d, h->p.wd_k);
       add(h->ctx_wqkv, qkv, d);
       add(h->ctx_wo, d, ao);
       add(h->w_p, k * d, d);
@@ -834,6 +1001,8 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
   h->gcnt = (int*)(w + p.o_gcnt);
   h->amv = (float*)(w + p.o_amv);
   h->ami = (int*)(w + p.o_ami);
+  h->tpbuf = p.tp > 1 ? (float*)(w + p.o_tpbuf) : nullptr;
+  h->tpkey = p.tp > 1 ? (unsigned long long*)(w + p.o_tpkey) : nullptr;
   int* ip = (int*)(w + p.o_ints);
   auto ints = [&](int n) {
     int* r = ip;
@@ -987,7 +1156,7 @@ static cudaError_t one_step(sf_handle* h, int* acc_log, int* em_log) {
     if ((e = do_draft(h))) return e;
     if (h->forced) {
       h->launches++;
-      if ((e = launch_force_drafts(h->B, h->p.k, h->p.V, h->f_cont, h->f_cont_len, h->f_corrupt,
+      if ((e = launch_force_drafts(h->B, h->p.k, h->p.V_full, h->f_cont, h->f_cont_len, h->f_corrupt,
                                    h->f_corrupt_steps, h->seq_len, h->prompt_len, h->step_counter, h->draft, h->st)))
         return e;
     }
@@ -1017,7 +1186,7 @@ sf_status specformer_decode_steps(sf_handle* h, int32_t n_steps, int32_t* emitte
     SF_TRY(one_step(h, accept_log, emitted_log));
     done = 1;
   }
-  const bool use_graph = (h->c.flags & SF_FLAG_CUDA_GRAPH) != 0;
+  const bool use_graph = (h->c.flags & SF_FLAG_CUDA_GRAPH) != 0 && (h->p.tp == 1 || h->coll.graph_safe);
   if (use_graph && h->prof_on && done < n_steps) {
     // profiling: the step graph re-captured with an event-record node around every launch (this
     // serialises the launches -- no PDL overlap across a record node), replayed one step at a time
@@ -1114,7 +1283,84 @@ void specformer_destroy(sf_handle* h) {
     cudaEventDestroy(r.b);
   }
   for (auto e : h->ev_free) cudaEventDestroy(e);
+#ifdef SF_WITH_NCCL
+  if (h->nccl_comm) ncclCommDestroy((ncclComm_t)h->nccl_comm);
+#endif
+  if (h->coll.sum_f32 == local_sum_f32) delete (LocalCtx*)h->coll.ctx;
   delete h;
+}
+
+int32_t sf_nccl_unique_id(uint8_t* out) {
+#ifdef SF_WITH_NCCL
+  if (!out) return -1;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return -1;
+  static_assert(sizeof(id.internal) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(out, id.internal, 128);
+  return 0;
+#else
+  (void)out;
+  return -1;
+#endif
+}
+
+sf_status sf_nccl_attach(sf_handle* h, const uint8_t* id, int32_t nranks, int32_t rank) {
+  if (!h || !id) return SF_ERR_ARG;
+  if (nranks != h->p.tp || rank != h->p.tp_rank) return set_err(h, SF_ERR_ARG, "nranks / rank differ from tp_size / tp_rank");
+  if (h->coll.sum_f32) return set_err(h, SF_ERR_STATE, "a collective is already attached");
+#ifdef SF_WITH_NCCL
+  ncclUniqueId uid;
+  memcpy(uid.internal, id, 128);
+  ncclComm_t comm = nullptr;
+  const ncclResult_t r = ncclCommInitRank(&comm, nranks, uid, rank);
+  if (r != ncclSuccess) return set_err(h, SF_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  h->nccl_comm = comm;
+  h->coll.sum_f32 = nccl_sum_f32;
+  h->coll.max_u64 = nccl_max_u64;
+  h->coll.ctx = comm;
+  h->coll.graph_safe = true;
+  return SF_OK;
+#else
+  return set_err(h, SF_ERR_UNSUPPORTED, "built without NCCL");
+#endif
+}
+
+sf_local_group* sf_local_group_create(int32_t n) {
+  if (n < 1 || n > 8) return nullptr;
+  sf_local_group* g = new sf_local_group();
+  g->n = n;
+  g->bufs.assign(n, nullptr);
+  g->tmp.assign(n, nullptr);
+  g->tmp_bytes.assign(n, 0);
+  g->ev_in.resize(n);
+  g->ev_mid.resize(n);
+  for (int i = 0; i < n; ++i) {
+    cudaEventCreateWithFlags(&g->ev_in[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&g->ev_mid[i], cudaEventDisableTiming);
+  }
+  return g;
+}
+
+void sf_local_group_destroy(sf_local_group* g) {
+  if (!g) return;
+  cudaDeviceSynchronize();
+  for (int i = 0; i < g->n; ++i) {
+    cudaEventDestroy(g->ev_in[i]);
+    cudaEventDestroy(g->ev_mid[i]);
+    if (g->tmp[i]) cudaFree(g->tmp[i]);
+  }
+  delete g;
+}
+
+sf_status sf_local_group_attach(sf_handle* h, sf_local_group* g, int32_t rank) {
+  if (!h || !g) return SF_ERR_ARG;
+  if (g->n != h->p.tp || rank != h->p.tp_rank) return set_err(h, SF_ERR_ARG, "group size / rank differ from tp_size / tp_rank");
+  if (h->coll.sum_f32) return set_err(h, SF_ERR_STATE, "a collective is already attached");
+  h->coll.sum_f32 = local_sum_f32;
+  h->coll.max_u64 = local_max_u64;
+  h->coll.ctx = new LocalCtx{g, rank};
+  h->coll.graph_safe = false;
+  return SF_OK;
 }
 
 int64_t specformer_kernel_launches(const sf_handle* h) { return h ? h->launches : -1; }
@@ -1149,7 +1395,7 @@ sf_status sf_debug_capture(sf_handle* h, int32_t what, void* dst, int64_t* nbyte
 sf_status sf_debug_force_drafts(sf_handle* h, const int32_t* cont_dev, int32_t cont_len, const int32_t* corrupt_dev) {
   if (!h || !cont_dev || cont_len < 1) return SF_ERR_ARG;
   if (h->state != ST_DRAFTED && h->state != ST_READY) return set_err(h, SF_ERR_STATE, "force_drafts before verify");
-  SF_TRY(launch_force_drafts(h->B, h->p.k, h->p.V, cont_dev, cont_len, corrupt_dev, 1, h->seq_len, h->prompt_len,
+  SF_TRY(launch_force_drafts(h->B, h->p.k, h->p.V_full, cont_dev, cont_len, corrupt_dev, 1, h->seq_len, h->prompt_len,
                              nullptr, h->draft, h->st));
   h->state = ST_DRAFTED;
   return SF_OK;

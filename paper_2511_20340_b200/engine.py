@@ -32,19 +32,28 @@ class EngineConfig:
     rms_eps: float = 1e-6
     kv_block: int = 16
     flags: int = 0
+    tp_size: int = 1             # tensor parallelism (include/specformer.h): ranks, this rank
+    tp_rank: int = 0
 
     @classmethod
-    def from_model(cls, m, max_batch=None, max_seq=None, draft_len=None, flags=0):
+    def from_model(cls, m, max_batch=None, max_seq=None, draft_len=None, flags=0, tp_size=1, tp_rank=0):
         """Build from any object with the model-shape attributes (e.g. synth.ModelConfig)."""
         return cls(m.n_layers, m.d_model, m.n_heads, m.n_kv_heads, m.head_dim, m.d_ff, m.vocab,
                    m.draft_len if draft_len is None else draft_len, max_batch or m.batch,
-                   max_seq or m.max_seq, m.dtype, m.rope_theta, m.rms_eps, m.kv_block, flags)
+                   max_seq or m.max_seq, m.dtype, m.rope_theta, m.rms_eps, m.kv_block, flags, tp_size, tp_rank)
 
     def to_c(self) -> N.sf_config:
         return N.sf_config(self.n_layers, self.d_model, self.n_heads, self.n_kv_heads, self.head_dim, self.d_ff,
                            self.vocab, self.draft_len, self.max_batch, self.max_seq, self.kv_block,
                            self.rope_theta, self.rms_eps, N.SF_BF16 if self.dtype == "bf16" else N.SF_FP32,
-                           1, 0, self.flags)
+                           self.tp_size, self.tp_rank, self.flags)
+
+    def vocab_shard(self):
+        """[v0, v1): this rank's LM-head rows (whole 128-row tiles; the library's split)."""
+        if self.tp_size <= 1:
+            return 0, self.vocab
+        tiles = self.vocab // 128
+        return tiles * self.tp_rank // self.tp_size * 128, tiles * (self.tp_rank + 1) // self.tp_size * 128
 
 
 def weight_table(cfg: EngineConfig):
@@ -71,20 +80,41 @@ def _pair_interleave_heads(W: torch.Tensor, hd: int) -> torch.Tensor:
     return W.view(n, hd, -1)[:, idx, :].reshape(W.shape)
 
 
-def _source_tensor(name: str, w: dict, rope_pairs: int = 0) -> torch.Tensor:
+def _rows(t: torch.Tensor, i: int, n: int) -> torch.Tensor:
+    """Block i of n equal row blocks."""
+    r = t.shape[0] // n
+    return t[i * r:(i + 1) * r]
+
+
+def _cols(t: torch.Tensor, i: int, n: int) -> torch.Tensor:
+    c = t.shape[1] // n
+    return t[:, i * c:(i + 1) * c]
+
+
+def _source_tensor(name: str, w: dict, rope_pairs: int = 0, cfg: EngineConfig | None = None) -> torch.Tensor:
     """Map a packed-table name to the caller's canonical tensors (see synth/weights.py).
-    rope_pairs = head_dim when the RoPE'd QKV projections are pair-interleaved (bf16, hd 128)."""
+    rope_pairs = head_dim when the RoPE'd QKV projections are pair-interleaved (bf16, hd 128).
+    cfg.tp_size > 1: this rank's slice (include/specformer.h, tensor parallelism): heads of the q / k /
+    v rows and O columns, FFN rows of gate / up and down columns, the vocabulary shard of the LM head,
+    the input-column block of W_D; everything else whole."""
+    tp, r = (cfg.tp_size, cfg.tp_rank) if cfg is not None and cfg.tp_size > 1 else (1, 0)
     pre, _, leaf = name.rpartition(".")
     pre = pre + "." if pre else ""
     if leaf.endswith("wqkv"):
         p = pre + leaf[:-4]
-        W = torch.cat([w[p + "wq"], w[p + "wk"], w[p + "wv"]], dim=0)
+        W = torch.cat([_rows(w[p + "wq"], r, tp), _rows(w[p + "wk"], r, tp), _rows(w[p + "wv"], r, tp)], dim=0)
         if rope_pairs and not leaf.startswith("blk_"):
             W = _pair_interleave_heads(W, rope_pairs)
         return W
     if leaf.endswith("w_gu"):
         p = pre + leaf[:-4]
-        return _interleave_gu(w[p + "w_gate"], w[p + "w_up"])
+        return _interleave_gu(_rows(w[p + "w_gate"], r, tp), _rows(w[p + "w_up"], r, tp))
+    if tp > 1:
+        if leaf in ("wo", "ctx_wo", "blk_wo", "w_down", "blk_w_down", "w_d"):
+            return _cols(w[name], r, tp)
+        if name == "lm_head":
+            v0, v1 = cfg.vocab_shard()
+            return w[name][v0:v1]
     return w[name]
 
 
@@ -98,7 +128,7 @@ def pack_weights(cfg: EngineConfig, weights: dict, device="cuda") -> torch.Tenso
     stream = torch.cuda.current_stream(device)
     rope_pairs = cfg.head_dim if (cfg.dtype == "bf16" and cfg.head_dim == 128) else 0
     for name, shape, off, dt, layout in weight_table(cfg):
-        t = _source_tensor(name, weights, rope_pairs)
+        t = _source_tensor(name, weights, rope_pairs, cfg)
         tdtype = torch.bfloat16 if dt == N.SF_BF16 else torch.float32
         if tuple(t.shape) != shape:
             raise ValueError(f"{name}: expected {shape}, got {tuple(t.shape)}")
@@ -141,6 +171,8 @@ class Engine:
             raise N.SpecFormerError(st, "specformer_init")
         self.h = h
         self.B = 0
+        v0, v1 = cfg.vocab_shard()
+        self.v0, self.v_local = v0, v1 - v0  # logits copied out are this rank's vocabulary shard
 
     # ---------------------------------------------------------------- helpers
     def _enter(self):
@@ -177,14 +209,14 @@ class Engine:
 
     def draft_step(self, want_logits=False):
         d = self._i32(self.B, self.k)
-        lg = torch.empty(self.B, self.k, self.cfg.vocab, device=self.device) if want_logits else None
+        lg = torch.empty(self.B, self.k, self.v_local, device=self.device) if want_logits else None
         self._enter()
         self._check(self.lib.specformer_draft_step(self.h, _ptr(d), _ptr(lg)), "draft_step")
         return (d, lg) if want_logits else d
 
     def verify_step(self, draft: torch.Tensor | None = None, want_logits=False):
         g = self._i32(self.B, self.k + 1)
-        lg = torch.empty(self.B, self.k + 1, self.cfg.vocab, device=self.device) if want_logits else None
+        lg = torch.empty(self.B, self.k + 1, self.v_local, device=self.device) if want_logits else None
         if draft is not None:
             draft = draft.to(torch.int32).contiguous()
         self._enter()
@@ -234,6 +266,17 @@ class Engine:
         self._check(self.lib.sf_profile_read(self.h, cls, C.byref(ms), C.byref(n), C.byref(by)), "profile_read")
         return ms.value, n.value, by.value
 
+    # ---------------------------------------------------------------- tensor parallelism
+    def attach_nccl(self, unique_id: bytes, nranks: int, rank: int):
+        """NCCL communicator over the tp ranks (unique_id from nccl_unique_id() on rank 0)."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        self._check(self.lib.sf_nccl_attach(self.h, buf, nranks, rank), "sf_nccl_attach")
+
+    def attach_local_group(self, group, rank: int):
+        """Tests: reduce with the other handles of `group` (LocalGroup) in this process."""
+        self._group = group  # keep alive
+        self._check(self.lib.sf_local_group_attach(self.h, group.g, rank), "sf_local_group_attach")
+
     def kernel_launches(self) -> int:
         return int(self.lib.specformer_kernel_launches(self.h))
 
@@ -273,3 +316,24 @@ def run_gemm(A: torch.Tensor, W: torch.Tensor, stream=None, w_tiled: bool = Fals
     if st != N.SF_OK:
         raise N.SpecFormerError(st, "sf_test_gemm")
     return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    if N.lib().sf_nccl_unique_id(buf) != 0:
+        raise N.SpecFormerError(N.SF_ERR_UNSUPPORTED, "NCCL unavailable")
+    return bytes(buf)
+
+
+class LocalGroup:
+    """n handles of one process on one device reducing through device memory (tests only)."""
+
+    def __init__(self, n: int):
+        self.g = N.lib().sf_local_group_create(n)
+        if not self.g:
+            raise N.SpecFormerError(N.SF_ERR_ARG, "sf_local_group_create")
+
+    def close(self):
+        if self.g:
+            N.lib().sf_local_group_destroy(self.g)
+            self.g = None

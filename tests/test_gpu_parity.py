@@ -12,7 +12,8 @@ import pytest
 import torch
 
 import oracle as O
-from gpu_helpers import make_engine, oracle_replay, rel_l2, run_gpu, setup
+from gpu_helpers import make_engine, max_seq_for, oracle_replay, rel_l2, run_gpu, setup
+from paper_2511_20340_b200 import Engine, EngineConfig
 from paper_2511_20340_b200 import _native as N
 from paper_2511_20340_b200 import run_gemm
 from synth import get_config, make_prompts
@@ -306,3 +307,53 @@ def test_attention_schedules_bit_exact(cfg, monkeypatch):
     for s1, s2 in zip(a["steps"], b["steps"]):
         assert np.array_equal(s1["logits"], s2["logits"])
         assert np.array_equal(s1["draft_logits"], s2["draft_logits"])
+
+
+# ------------------------------------------------------------------ tensor parallelism
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("tp", [2, 4])
+def test_tensor_parallel_matches_oracle(tp):
+    """70B-shaped GQA model split over tp ranks -- tp handles on this GPU, one host thread each,
+    reducing through a local group (the NCCL path uses the same hooks): the ranks agree on every
+    token, the concatenated vocabulary shards of their logits match the fp64 oracle within the
+    bf16 tolerance (reading C21), and the tokens match the oracle wherever its top-2 margin > 5e-2."""
+    import threading
+
+    from paper_2511_20340_b200.engine import LocalGroup
+
+    cfg = GQA2K.replace(n_kv_heads=4, batch=2, gen_len=8)
+    w, prompts = setup(cfg, seed=7, jitter=0.1)
+    group = LocalGroup(tp)
+    engines, res, errs = [], [None] * tp, []
+    for r in range(tp):
+        ec = EngineConfig.from_model(cfg, max_batch=cfg.batch, max_seq=max_seq_for(cfg, cfg.gen_len, cfg.draft_len),
+                                     tp_size=tp, tp_rank=r)
+        eng = Engine(ec, w)
+        eng.attach_local_group(group, r)
+        engines.append(eng)
+
+    def run(r):
+        try:
+            res[r] = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True, eng=engines[r])
+        except Exception as ex:  # pragma: no cover - reported below
+            errs.append(ex)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(tp)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for r in range(1, tp):
+        assert res[r]["tokens"] == res[0]["tokens"]
+    merged = {"tokens": res[0]["tokens"], "steps": []}
+    for steps in zip(*[x["steps"] for x in res]):
+        s = dict(steps[0])
+        s["logits"] = np.concatenate([x["logits"] for x in steps], axis=-1)
+        s["draft_logits"] = np.concatenate([x["draft_logits"] for x in steps], axis=-1)
+        merged["steps"].append(s)
+    assert merged["steps"][0]["logits"].shape[-1] == cfg.vocab
+    assert _check_bf16(cfg, w, prompts, merged, seqs=(0,), rel_tol=2.2e-2) > 10
+    for e in engines:
+        e.close()
+    group.close()
