@@ -158,6 +158,9 @@ def run_ours(args, cfg):
     import numpy as np
 
     from paper_2511_20340_b200 import Engine, EngineConfig, dp, roofline, timeline
+    from paper_2511_20340_b200 import tp as tpmod
+    from paper_2511_20340_b200.engine import nccl_unique_id
+    from synth.weights import weight_shapes
     from paper_2511_20340_b200 import _native as N
     from synth import make_prompts, make_weights
 
@@ -181,12 +184,27 @@ def run_ours(args, cfg):
         grow = max(grow, n_cont + GEN_CHUNK * (k + 1), (W + Kf) * (k + 1))
     max_seq = (P + grow + 32 + 15) // 16 * 16
 
-    weights = make_weights(cfg, seed=0, device="cuda")
-    ec = EngineConfig.from_model(cfg, max_batch=B, max_seq=max_seq, flags=N.SF_FLAG_CUDA_GRAPH)
+    # --tp (default for the 70B shape): the ranks split one model (tensor parallelism, strong
+    # scaling of one global batch B); otherwise each rank serves its own batch B (weak scaling)
+    tp = world if (world > 1 and (args.tp or cfg.name == "70b")) else 1
+    if cfg.name == "70b" and tp == 1:
+        raise SystemExit("the 70B shape needs tensor parallelism: torchrun --nproc-per-node >= 2 (SURVEY 8e; "
+                         "~141 GB of bf16 weights + KV do not fit one GPU)")
+    if tp > 1:
+        weights = tpmod.LazyWeights(lambda n: make_weights(cfg, seed=0, device="cuda", names={n})[n],
+                                    [n for n, _ in weight_shapes(cfg)])
+    else:
+        weights = make_weights(cfg, seed=0, device="cuda")
+    ec = EngineConfig.from_model(cfg, max_batch=B, max_seq=max_seq, flags=N.SF_FLAG_CUDA_GRAPH,
+                                 tp_size=tp, tp_rank=rank if tp > 1 else 0)
     eng = Engine(ec, weights)
     del weights
     torch.cuda.empty_cache()
-    prompts = dp.shard_rows(make_prompts(B * world, P, cfg.vocab), rank, world)  # weak scaling
+    if tp > 1:
+        eng.attach_nccl(tpmod.share_unique_id(nccl_unique_id, rank), tp, rank)
+        prompts = make_prompts(B, P, cfg.vocab)  # every rank: the same global batch
+    else:
+        prompts = dp.shard_rows(make_prompts(B * world, P, cfg.vocab), rank, world)  # weak scaling
 
     eng.prefill(prompts.cuda())
     acc_log = torch.zeros(max(K, W), B, dtype=torch.int32, device="cuda")
@@ -213,6 +231,7 @@ def run_ours(args, cfg):
     after = eng.capture(3, (B,), torch.int32).cpu()
     tokens = int((after - before).sum())
     ms_max, tokens_total = dp.reduce_timing(ms, float(tokens), device="cuda")
+    tokens_total /= tp  # tensor parallelism: every rank emits the same tokens
     value = tokens_total / (ms_max / 1e3)
     steps_per_s = K / (ms_max / 1e3)
     a_meas = tokens / (K * B)
@@ -226,6 +245,7 @@ def run_ours(args, cfg):
         sb += roofline.step_bytes(cfg, B, k, lens_t, prev_t)
         prev_t = list(lens_t)
         lens_t = [n + m + 1 for n, m in zip(lens_t, accs_t[s])]
+    sb /= tp  # tensor parallelism: each GPU streams its 1/tp of the weights and of the KV heads
     step_gbs = sb / (ms / 1e3) / 1e9
 
     def replay_lengths(lens0, prev0, accs):
@@ -365,6 +385,7 @@ def run_ours(args, cfg):
     e2e_ms = x0.elapsed_time(x1)
     e2e_tokens = B + int((em_host >= 0).sum())
     e2e_ms_max, e2e_tok = dp.reduce_timing(e2e_ms, float(e2e_tokens), device="cuda")
+    e2e_tok /= tp
 
     # ---------------- forced acceptance: drafts replaced -- after the draft step has run
     # and been paid for -- by the GPU's own greedy continuation, corrupted at slot j with
@@ -394,7 +415,9 @@ def run_ours(args, cfg):
             cont[b] = torch.tensor(toks, dtype=torch.int32)
         gen = torch.Generator().manual_seed(2)  # per (step, global sequence): identical at any GPU count
         n_cs = W + Kf + 2
-        u = torch.rand(n_cs, B * world, generator=gen)[:, rank * B:(rank + 1) * B]
+        nb = B if tp > 1 else B * world  # (tensor parallelism: one batch, the same on every rank)
+        r0 = 0 if tp > 1 else rank * B
+        u = torch.rand(n_cs, nb, generator=gen)[:, r0:r0 + B]
         cdf = torch.tensor([sum(alpha ** (i - 1) * (1 - alpha) for i in range(1, j + 1)) for j in range(1, k + 1)])
         corrupt = (torch.searchsorted(cdf, u.contiguous()) + 1).to(torch.int32)  # k + 1 = no corruption
         eng.prefill(prompts.cuda())
@@ -413,15 +436,16 @@ def run_ours(args, cfg):
         eng.sync()
         fa = eng.capture(3, (B,), torch.int32).cpu()
         f_ms, f_tok = dp.reduce_timing(f0.elapsed_time(f1), float(int((fa - fb).sum())), device="cuda")
+        f_tok /= tp
         eng.set_forced_drafts(None)
         forced = {"tokens_per_s": f_tok / (f_ms / 1e3), "verify_steps_per_s_per_gpu": Kf / (f_ms / 1e3),
-                  "ms_per_step": f_ms / Kf, "mean_accepted_length": f_tok / (Kf * B * world),
+                  "ms_per_step": f_ms / Kf, "mean_accepted_length": f_tok / (Kf * B * world // tp),
                   "a_target": a_target, "alpha": alpha, "steps": Kf,
                   "note": "drafts = GPU greedy continuation corrupted at an i.i.d. slot (seed 2); the draft "
                           "forward still runs every step"}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline and tp == 1:
         try:
             cpu = oracle_sample(cfg)
         except MemoryError as ex:  # bounded sample did not fit the host
@@ -431,17 +455,19 @@ def run_ours(args, cfg):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong" if tp > 1 else "weak",
+            "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (seeded N(0,0.02) weights, uniform-random prompts)",
             "config": {"workload": f"{cfg.name}-shaped SpecFormer decode step (draft+verify+accept), "
                                    f"batch {B}/GPU, k {k}, prompt {P}",
-                       "model": cfg.name, "batch_per_gpu": B, "global_batch": B * world, "draft_len": k,
-                       "prompt_len": P, "parallelism": f"dp{world}", "cuda_graph": True,
+                       "model": cfg.name, "batch_per_gpu": B if tp == 1 else B / tp, "global_batch": B * world // tp,
+                       "draft_len": k, "prompt_len": P, "parallelism": f"tp{tp}" if tp > 1 else f"dp{world}",
+                       "cuda_graph": True,
                        "l2": "inputs larger than L2 (14 GB weights + KV per step)"},
             "verify_steps_per_s": steps_per_s, "verify_steps_per_s_box": steps_per_s * world,
             "mean_accepted_length": a_meas,
             "forced_acceptance": forced,
-            "modeled_tokens_per_s_at_paper_a": steps_per_s * B * world * A_PAPER.get(cfg.name, 1.75),
+            "modeled_tokens_per_s_at_paper_a": steps_per_s * B * world // tp * A_PAPER.get(cfg.name, 1.75),
             "a_paper": A_PAPER.get(cfg.name),
             "roofline": {"bound": bound, "kernel": dominant, "achieved": achieved, "peak": peak_v, "unit": unit,
                          "frac": achieved / peak_v, "traffic": traffic, "peak_source": peak_src,
@@ -480,6 +506,8 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = the config's generation length - 1")
     ap.add_argument("--forced-steps", type=int, default=32)
+    ap.add_argument("--tp", action="store_true", help="N > 1: split one model over the ranks (tensor parallelism; "
+                                                      "the default for --config 70b) instead of one batch per rank")
     ap.add_argument("--timeline-steps", type=int, default=2, help="graph steps replayed with the kernel timeline on")
     ap.add_argument("--draft-len", type=int, default=None, help="override k (13B sweep: 4 / 6 / 8)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

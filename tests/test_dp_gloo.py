@@ -75,3 +75,39 @@ def test_shard_rows_validation():
     assert dp.shard_rows(x, 1, 3).tolist() == [[4, 5], [6, 7]]
     with pytest.raises(ValueError):
         dp.shard_rows(x, 0, 4)
+
+
+def _tp_worker(rank, world, port, out_q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2511_20340_b200 import tp as tpmod
+        calls = []
+        uid = tpmod.share_unique_id(lambda: (calls.append(1), bytes(range(128)))[1], rank)
+        lw = tpmod.LazyWeights(lambda n: (calls.append(n), n.upper())[1], ["a", "b"])
+        out_q.put((rank, uid, len(calls), lw["b"], sorted(lw), len(lw)))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def test_tp_unique_id_broadcast_gloo():
+    """Tensor parallelism plumbing: only rank 0 creates the NCCL unique id; every rank receives the
+    same 128 bytes; lazy weights draw a tensor per access."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_tp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, uid, ncalls, b, names, n in res:
+        assert uid == bytes(range(128))
+        assert ncalls == (1 if rank == 0 else 0)  # make_id on rank 0 only (counted before the draw)
+        assert b == "B" and names == ["a", "b"] and n == 2
