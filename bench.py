@@ -347,10 +347,10 @@ def run_ours(args, cfg):
     # DRAM bytes per launch of the dominant kernel class from the committed ncu launch list of this
     # command at this batch (profiles/ncu_traffic.json, written by tools/profile_summary.py)
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
+    traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(traffic_path):
         try:
-            traffic = json.load(open(tp)).get(f"{cfg.name}_b{B}", {}).get("traffic_bytes_per_launch", {}).get(dominant)
+            traffic = json.load(open(traffic_path)).get(f"{cfg.name}_b{B}", {}).get("traffic_bytes_per_launch", {}).get(dominant)
         except Exception:
             traffic = None
     prof_classes = {name: {"ms_total": cls[c][0], "launches": cls[c][1], "share_of_profiled_step":
