@@ -127,11 +127,12 @@ class KVCache:
             self.V[l] = self.V[l][:, :n]
 
 
-def _attn(W, prefix, x, pos, cache, layer, causal=True):
+def _attn(W, prefix, x, pos, cache, layer, causal=True, slot_causal=False):
     """Multi-head attention sub-block on normalised input x [T, d].
     With `cache`: RoPE at absolute positions, append K/V, attend causally over the
     cached prefix + the new rows (query i at position p_i sees keys at <= p_i).
-    Without cache (draft block, P204): no RoPE, all-to-all over the T rows.
+    Without cache (draft block, P204): no RoPE, all-to-all over the T rows -- or, with
+    slot_causal (the "+Att Mask" ablation, T4 P497-514), row i sees rows <= i only.
     GQA: query head h reads kv head floor(h * Hkv / Hq)."""
     c = W.cfg
     T = x.shape[0]
@@ -148,7 +149,7 @@ def _attn(W, prefix, x, pos, cache, layer, causal=True):
         mask = keypos[None, :] <= np.asarray(pos)[:, None]
     else:
         K, V = k.transpose(1, 0, 2), v.transpose(1, 0, 2)
-        mask = np.ones((T, T), dtype=bool)
+        mask = np.tril(np.ones((T, T), dtype=bool)) if slot_causal else np.ones((T, T), dtype=bool)
     out = np.empty((T, hq, hd))
     for h in range(hq):
         g = (h * hkv) // hq
@@ -203,21 +204,22 @@ def positional_ffn(W, i_d):
     return y.reshape(c.draft_len, c.d_model)
 
 
-def draft_block(W, D):
+def draft_block(W, D, slot_causal=False):
     """Draft Bi-directional Attention layer, Eq.10 (P197-204):
         E = (SwiGLU . RMS + I)((SA . RMS + I)(D)),
     SA unmasked along the l_d draft slots, no positional encoding (reading C6).
+    slot_causal: the T4 "+Att Mask" ablation (P497-514) -- slot j attends slots <= j.
     D: [k, d] -> E: [k, d]."""
     eps = W.cfg.rms_eps
-    Y = D + _attn(W, "sf.blk_", rms_norm(D, W["sf.blk_attn_norm"], eps), None, None, None)
+    Y = D + _attn(W, "sf.blk_", rms_norm(D, W["sf.blk_attn_norm"], eps), None, None, None, slot_causal=slot_causal)
     return Y + swiglu(rms_norm(Y, W["sf.blk_ffn_norm"], eps), W["sf.blk_w_gate"], W["sf.blk_w_up"],
                       W["sf.blk_w_down"])
 
 
-def draft_logits(W, i_d):
+def draft_logits(W, i_d, slot_causal=False):
     """Draft logits for one context row: positional FFN -> draft block -> frozen base
     final norm + LM head, shared (reading C8). Returns [k, V]."""
-    E = draft_block(W, positional_ffn(W, i_d))
+    E = draft_block(W, positional_ffn(W, i_d), slot_causal)
     return rms_norm(E, W["final_norm"], W.cfg.rms_eps) @ W["lm_head"].T
 
 
@@ -307,7 +309,7 @@ def sd_decode(W, prompt, n_tokens, draft_fn=None, record=False):
     return out[:n_tokens], steps
 
 
-def replay(W, prompt, gpu_steps):
+def replay(W, prompt, gpu_steps, slot_causal=False):
     """Teacher-forced oracle along a trajectory produced elsewhere (the GPU's).
     gpu_steps: list of dicts with 'draft' (k ints), 'm' (accept length) and 'last'
     (the verify block's first token). At each step the oracle verifies the SAME block,
@@ -322,7 +324,7 @@ def replay(W, prompt, gpu_steps):
     n = P
     res = []
     for st in gpu_steps:
-        dl = draft_logits(W, i_d)
+        dl = draft_logits(W, i_d, slot_causal)
         dr = [int(t) for t in st["draft"]]
         logits, taps = base_forward(W, [int(st["last"])] + dr, n, cache)
         m = int(st["m"])

@@ -1503,19 +1503,24 @@ static cudaError_t gemm_launch_chunk(bool is_bf16, const void* A, int lda, const
   return launch_sk(A, lda, W, w_tiled, T, N, K, epi, scratch, st);
 }
 
-// Rows beyond 512 (the TMEM accumulator capacity) are processed as independent column chunks;
-// per-element arithmetic is unchanged, so results do not depend on the chunking.
+// Rows beyond 512 (the TMEM accumulator capacity) are processed as independent column chunks of
+// equal size (576 rows: 2 x 288, not 512 + 64 -- each chunk streams the weights once, and two
+// half-size chunks finish sooner than a full one plus a DRAM-bound sliver); per-element
+// arithmetic is unchanged (the k segmentation depends on (N, K) only), so results do not depend
+// on the chunking.
 cudaError_t gemm_launch(bool is_bf16, const void* A, int lda, const void* W, bool w_tiled, int T, int N, int K,
                         const GemmEpi& epi, const GemmScratch& scratch, cudaStream_t st) {
   if (!is_bf16 || T <= 512) return gemm_launch_chunk(is_bf16, A, lda, W, w_tiled, T, N, K, epi, scratch, st);
-  for (int t0 = 0; t0 < T; t0 += 512) {
+  const int n_chunks = (T + 511) / 512;
+  const int chunk = std::min(512, ((T + n_chunks - 1) / n_chunks + 15) / 16 * 16);
+  for (int t0 = 0; t0 < T; t0 += chunk) {
     GemmEpi e = epi;
     const size_t out_elt = (epi.mode == EPI_STORE_ACT || epi.mode == EPI_SWIGLU_ACT) ? 2 : 4;
     if (epi.mode == EPI_QKV_ROPE) e.rope.t0 = epi.rope.t0 + t0;
     else e.out = (char*)epi.out + (size_t)t0 * epi.ldo * out_elt;
     if (epi.tap) e.tap = epi.tap + (size_t)t0 * epi.ldo;
     cudaError_t r = gemm_launch_chunk(true, (const char*)A + (size_t)t0 * lda * 2, lda, W, w_tiled,
-                                      std::min(512, T - t0), N, K, e, scratch, st);
+                                      std::min(chunk, T - t0), N, K, e, scratch, st);
     if (r != cudaSuccess) return r;
   }
   return cudaSuccess;

@@ -61,10 +61,10 @@ def run_gpu(cfg, weights, prompts, n_tokens, k=None, flags=0, want_logits=False,
     return {"tokens": [o[:n_tokens] for o in out], "steps": steps, "engine": eng}
 
 
-def oracle_replay(cfg, weights, prompt, steps, b):
+def oracle_replay(cfg, weights, prompt, steps, b, slot_causal=False):
     traj = [dict(draft=s["draft"][b].tolist(), m=int(s["m"][b]), last=int(s["last"][b])) for s in steps]
     W = O.Weights(cfg, weights)
-    return O.replay(W, list(prompt), traj)
+    return O.replay(W, list(prompt), traj, slot_causal)
 
 
 def setup(cfg, seed=0, jitter=0.0, B=None, n_layers=None):

@@ -194,10 +194,10 @@ MID = SMALL.replace(name="mid", n_layers=2, d_model=512, n_heads=4, n_kv_heads=4
 GQA = MID.replace(name="gqa", d_model=1024, n_heads=8, n_kv_heads=2, prompt_len=200, batch=3)
 
 
-def _check_bf16(cfg, w, prompts, res, seqs, rel_tol=1.5e-2):
+def _check_bf16(cfg, w, prompts, res, seqs, rel_tol=1.5e-2, slot_causal=False):
     checked = 0
     for b in seqs:
-        _, rep = oracle_replay(cfg, w, prompts[b].tolist(), res["steps"], b)
+        _, rep = oracle_replay(cfg, w, prompts[b].tolist(), res["steps"], b, slot_causal)
         for s, r in zip(res["steps"], rep):
             gl, ol = s["logits"][b].astype(np.float64), r["logits"]
             assert rel_l2(gl, ol) <= rel_tol, rel_l2(gl, ol)
@@ -357,3 +357,17 @@ def test_tensor_parallel_matches_oracle(tp):
     for e in engines:
         e.close()
     group.close()
+
+
+def test_draft_slot_causal_ablation_matches_oracle():
+    """NEXT-2 "+Att Mask" (T4, P497-514): SF_FLAG_DRAFT_CAUSAL masks the draft block's slot attention
+    causally; drafts and their logits follow the oracle's slot-causal block (and differ from the
+    bidirectional run), the verify stays exact, GPU SD == GPU AR."""
+    cfg = MID
+    w, prompts = setup(cfg, seed=5, jitter=0.1)
+    res = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True, flags=N.SF_FLAG_DRAFT_CAUSAL)
+    assert _check_bf16(cfg, w, prompts, res, seqs=(0, cfg.batch - 1), slot_causal=True) > 20
+    bi = run_gpu(cfg, w, prompts, 4, want_logits=True)
+    assert not np.allclose(bi["steps"][0]["draft_logits"], res["steps"][0]["draft_logits"])
+    ar = run_gpu(cfg, w, prompts, cfg.gen_len, k=0)
+    assert ar["tokens"] == res["tokens"]

@@ -263,6 +263,25 @@ def test_draft_block_identity_and_permutation_equivariance():
     np.testing.assert_array_equal(O.draft_block(O.Weights(cfg, w), D), D)          # S283
 
 
+def test_draft_block_slot_causal_ablation():
+    """"+Att Mask" (T4, P497-514): with the slot-causal mask, slot j ignores later slots (perturbing
+    the last slot leaves the others unchanged), slot 0 is the block applied to slot 0 alone (a k = 1
+    block, where causal and bidirectional coincide), and the last slot sees the same keys as the
+    unmasked block (so its output equals the bidirectional block's last row)."""
+    cfg = MICRO
+    W = O.Weights(cfg, make_weights(cfg, seed=8, norm_jitter=0.1))
+    D = np.random.default_rng(11).normal(size=(cfg.draft_len, cfg.d_model))
+    Ec = O.draft_block(W, D, slot_causal=True)
+    D2 = D.copy()
+    D2[-1] += 1.0
+    Ec2 = O.draft_block(W, D2, slot_causal=True)
+    np.testing.assert_array_equal(Ec2[:-1], Ec[:-1])
+    assert not np.allclose(Ec2[-1], Ec[-1])
+    np.testing.assert_allclose(Ec[:1], O.draft_block(W, D[:1]), rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(Ec[-1], O.draft_block(W, D)[-1], rtol=1e-12, atol=1e-14)
+    assert not np.allclose(Ec[0], O.draft_block(W, D)[0])
+
+
 def test_draft_logits_shape_and_constant_case():
     cfg = MICRO
     W = W_of(cfg, seed=9)
