@@ -73,6 +73,8 @@ typedef struct {
                           SF_BF16 (bf16 weights/KV, tcgen05 GEMMs, fp32 residual/accum)     */
   int32_t tp_size, tp_rank; /* tensor parallelism (see sf_nccl_attach); 1, 0 = one GPU        */
   uint64_t flags;
+  int32_t draft_blocks; /* bidirectional draft blocks (Eq.10 has one; 0 reads as 1). NEXT-2 "+Larger"
+                           (T4 P497-514): 2..4 stacked blocks, weights sf.blk<i>_* for i >= 1 */
 } sf_config;
 
 typedef struct {

@@ -209,11 +209,15 @@ def draft_block(W, D, slot_causal=False):
         E = (SwiGLU . RMS + I)((SA . RMS + I)(D)),
     SA unmasked along the l_d draft slots, no positional encoding (reading C6).
     slot_causal: the T4 "+Att Mask" ablation (P497-514) -- slot j attends slots <= j.
-    D: [k, d] -> E: [k, d]."""
+    cfg.draft_blocks > 1: the T4 "+Larger" ablation read as that many such layers applied in turn
+    (weights sf.blk_* then sf.blk<i>_*). D: [k, d] -> E: [k, d]."""
     eps = W.cfg.rms_eps
-    Y = D + _attn(W, "sf.blk_", rms_norm(D, W["sf.blk_attn_norm"], eps), None, None, None, slot_causal=slot_causal)
-    return Y + swiglu(rms_norm(Y, W["sf.blk_ffn_norm"], eps), W["sf.blk_w_gate"], W["sf.blk_w_up"],
-                      W["sf.blk_w_down"])
+    E = D
+    for i in range(max(1, getattr(W.cfg, "draft_blocks", 1))):
+        b = "sf.blk_" if i == 0 else f"sf.blk{i}_"
+        Y = E + _attn(W, b, rms_norm(E, W[b + "attn_norm"], eps), None, None, None, slot_causal=slot_causal)
+        E = Y + swiglu(rms_norm(Y, W[b + "ffn_norm"], eps), W[b + "w_gate"], W[b + "w_up"], W[b + "w_down"])
+    return E
 
 
 def draft_logits(W, i_d, slot_causal=False):

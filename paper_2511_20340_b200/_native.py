@@ -25,7 +25,8 @@ class sf_config(C.Structure):
                 ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("d_ff", C.c_int32), ("vocab", C.c_int32),
                 ("draft_len", C.c_int32), ("max_batch", C.c_int32), ("max_seq", C.c_int32),
                 ("kv_block", C.c_int32), ("rope_theta", C.c_float), ("rms_eps", C.c_float),
-                ("dtype", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32), ("flags", C.c_uint64)]
+                ("dtype", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32), ("flags", C.c_uint64),
+                ("draft_blocks", C.c_int32)]
 
 
 class sf_tensor_desc(C.Structure):

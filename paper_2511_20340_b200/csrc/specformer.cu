@@ -51,6 +51,7 @@ bool valid_config(const sf_config* c, std::string* why) {
   if (c->n_heads % c->n_kv_heads) return fail("n_heads % n_kv_heads != 0");
   if (c->head_dim != 16 && c->head_dim != 64 && c->head_dim != 128) return fail("head_dim must be 16, 64 or 128");
   if (c->draft_len < 0 || c->draft_len > 16) return fail("draft_len must be in [0, 16]");
+  if (c->draft_blocks < 0 || c->draft_blocks > 4) return fail("draft_blocks must be in [0, 4]");
   if (c->max_batch < 1 || c->max_batch > 1024) return fail("max_batch must be in [1, 1024]");
   if (c->kv_block != 16) return fail("kv_block must be 16");
   if (c->max_seq < 16 || c->max_seq % 16) return fail("max_seq must be a positive multiple of 16");
@@ -91,6 +92,9 @@ static void vocab_shard(const sf_config* c, int* v0, int* v1) {
   *v1 = (int)((int64_t)tiles * (r + 1) / tp) * 128;
 }
 
+// draft bidirectional blocks (Eq.10 has one; NEXT-2 "+Larger" stacks more): 0 reads as 1
+static int draft_blocks(const sf_config* c) { return c->draft_blocks > 1 ? c->draft_blocks : 1; }
+
 std::vector<TensorSpec> tensor_specs(const sf_config* c) {
   const int tp = tp_of(c);
   int v0, v1;
@@ -120,12 +124,15 @@ std::vector<TensorSpec> tensor_specs(const sf_config* c) {
     t.push_back({"sf.pos_norm", {d}, false});
     t.push_back({"sf.w_p", {k * d, d}, true});
     t.push_back({"sf.b_p", {k * d}, false});
-    t.push_back({"sf.blk_attn_norm", {d}, false});
-    t.push_back({"sf.blk_wqkv", {qkv, d}, true});
-    t.push_back({"sf.blk_wo", {d, ao}, true});
-    t.push_back({"sf.blk_ffn_norm", {d}, false});
-    t.push_back({"sf.blk_w_gu", {2 * F, d}, true});
-    t.push_back({"sf.blk_w_down", {d, F}, true});
+    for (int i = 0; i < draft_blocks(c); ++i) {  // block 0: "sf.blk_*", block i > 0: "sf.blk<i>_*"
+      const std::string b = i == 0 ? "sf.blk_" : "sf.blk" + std::to_string(i) + "_";
+      t.push_back({b + "attn_norm", {d}, false});
+      t.push_back({b + "wqkv", {qkv, d}, true});
+      t.push_back({b + "wo", {d, ao}, true});
+      t.push_back({b + "ffn_norm", {d}, false});
+      t.push_back({b + "w_gu", {2 * F, d}, true});
+      t.push_back({b + "w_down", {d, F}, true});
+    }
   }
   return t;
 }
@@ -250,6 +257,11 @@ struct sf_handle {
               *blk_attn_norm = nullptr, *blk_ffn_norm = nullptr;
   const void *w_d = nullptr, *ctx_wqkv = nullptr, *ctx_wo = nullptr, *w_p = nullptr, *blk_wqkv = nullptr,
              *blk_wo = nullptr, *blk_wgu = nullptr, *blk_wdown = nullptr;
+  struct Blk {
+    const float *attn_norm, *ffn_norm;
+    const void *wqkv, *wo, *wgu, *wdown;
+  };
+  std::vector<Blk> blks;  // the draft blocks in order (blks[0] = the blk_* pointers above)
   // workspace views
   char *kpool = nullptr, *vpool = nullptr;
   int* bt = nullptr;
@@ -698,28 +710,38 @@ static cudaError_t do_draft(sf_handle* h) {
     e = rmsnorm(h, h->D, p.d, h->blk_attn_norm, Tk, h->xn, p.d);
   }
   if (e) return e;
-  // draft bidirectional layer (Eq.10)
-  if ((e = gemm(h, h->xn, p.d, h->blk_wqkv, Tk, p.qkvw, p.d, epi_act(h->qkv, p.qkvw)))) return e;
-  if ((e = launch_bidir_attention(h->bf, h->qkv, B, k, p.Hq, p.Hkv, p.hd, (h->c.flags & SF_FLAG_DRAFT_CAUSAL) != 0,
-                                  h->attn, h->st)))
-    return e;
-  h->launches++;
-  if (!gemm_resid_norm(h, &e, h->attn, p.ao, h->blk_wo, Tk, p.d, p.ao, 1, h->D, nullptr, h->D, nullptr,
-                       h->blk_ffn_norm, true)) {
-    if ((e = gemm(h, h->attn, p.ao, h->blk_wo, Tk, p.d, p.ao, epi_add(h->D, p.d, nullptr)))) return e;
-    e = rmsnorm(h, h->D, p.d, h->blk_ffn_norm, Tk, h->xn, p.d);
+  // draft bidirectional layer(s) (Eq.10; more than one: NEXT-2 "+Larger")
+  bool xn_ready = false;
+  for (size_t bi = 0; bi < h->blks.size(); ++bi) {
+    const auto& bw = h->blks[bi];
+    if ((e = gemm(h, h->xn, p.d, bw.wqkv, Tk, p.qkvw, p.d, epi_act(h->qkv, p.qkvw)))) return e;
+    if ((e = launch_bidir_attention(h->bf, h->qkv, B, k, p.Hq, p.Hkv, p.hd, (h->c.flags & SF_FLAG_DRAFT_CAUSAL) != 0,
+                                    h->attn, h->st)))
+      return e;
+    h->launches++;
+    if (!gemm_resid_norm(h, &e, h->attn, p.ao, bw.wo, Tk, p.d, p.ao, 1, h->D, nullptr, h->D, nullptr, bw.ffn_norm,
+                         true)) {
+      if ((e = gemm(h, h->attn, p.ao, bw.wo, Tk, p.d, p.ao, epi_add(h->D, p.d, nullptr)))) return e;
+      e = rmsnorm(h, h->D, p.d, bw.ffn_norm, Tk, h->xn, p.d);
+    }
+    if (e) return e;
+    GemmEpi sw;
+    sw.mode = EPI_SWIGLU_ACT;
+    sw.out = h->ffn;
+    sw.ldo = p.F;
+    if ((e = gemm(h, h->xn, p.d, bw.wgu, Tk, 2 * p.F, p.d, sw))) return e;
+    // E = Y + SwiGLU(...); xn = the next block's RMS_1(E), after the last RMS_f(E) (shared frozen
+    // final norm, C8)
+    const bool last = bi + 1 == h->blks.size();
+    const float* next_g = last ? h->final_norm : h->blks[bi + 1].attn_norm;
+    xn_ready = gemm_resid_norm(h, &e, h->ffn, p.F, bw.wdown, Tk, p.d, p.F, 1, h->D, nullptr, h->D, nullptr, next_g,
+                               true);
+    if (!xn_ready) {
+      if ((e = gemm(h, h->ffn, p.F, bw.wdown, Tk, p.d, p.F, epi_add(h->D, p.d, nullptr)))) return e;
+      if (!last && (e = rmsnorm(h, h->D, p.d, next_g, Tk, h->xn, p.d))) return e;
+    }
+    if (e) return e;
   }
-  if (e) return e;
-  GemmEpi sw;
-  sw.mode = EPI_SWIGLU_ACT;
-  sw.out = h->ffn;
-  sw.ldo = p.F;
-  if ((e = gemm(h, h->xn, p.d, h->blk_wgu, Tk, 2 * p.F, p.d, sw))) return e;
-  // E = Y + SwiGLU(...); xn = RMS_f(E) (shared frozen final norm, C8)
-  bool xn_ready = gemm_resid_norm(h, &e, h->ffn, p.F, h->blk_wdown, Tk, p.d, p.F, 1, h->D, nullptr, h->D, nullptr,
-                                  h->final_norm, true);
-  if (!xn_ready) e = gemm(h, h->ffn, p.F, h->blk_wdown, Tk, p.d, p.F, epi_add(h->D, p.d, nullptr));
-  if (e) return e;
   // shared frozen LM head -> k draft tokens
   return head_argmax(h, h->D, Tk, h->dlogits, h->draft, xn_ready);
 }
@@ -948,6 +970,11 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
     h->blk_ffn_norm = (const float*)get("sf.blk_ffn_norm");
     h->blk_wgu = get("sf.blk_w_gu");
     h->blk_wdown = get("sf.blk_w_down");
+    for (int i = 0; i < draft_blocks(cfg); ++i) {
+      const std::string b = i == 0 ? "sf.blk_" : "sf.blk" + std::to_string(i) + "_";
+      h->blks.push_back({(const float*)get(b + "attn_norm"), (const float*)get(b + "ffn_norm"), get(b + "wqkv"),
+                         get(b + "wo"), get(b + "w_gu"), get(b + "w_down")});
+    }
   }  {
     // GEMM weight chain in launch order: draft (W_D, ctx QKV/O, W_P, block QKV/O/gate-up/down, LM
     // head), then verify (per layer QKV, O, gate-up, down; LM head), then the next step's draft
@@ -959,10 +986,12 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
       add(h->ctx_wqkv, qkv, d);
       add(h->ctx_wo, d, ao);
       add(h->w_p, k * d, d);
-      add(h->blk_wqkv, qkv, d);
-      add(h->blk_wo, d, ao);
-      add(h->blk_wgu, 2 * F, d);
-      add(h->blk_wdown, d, F);
+      for (const auto& b : h->blks) {
+        add(b.wqkv, qkv, d);
+        add(b.wo, d, ao);
+        add(b.wgu, 2 * F, d);
+        add(b.wdown, d, F);
+      }
       add(h->lm_head, V, d);
     }
     for (int l = 0; l < cfg->n_layers; ++l) {

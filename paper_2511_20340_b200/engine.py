@@ -34,19 +34,21 @@ class EngineConfig:
     flags: int = 0
     tp_size: int = 1             # tensor parallelism (include/specformer.h): ranks, this rank
     tp_rank: int = 0
+    draft_blocks: int = 1        # NEXT-2 "+Larger": stacked draft blocks
 
     @classmethod
     def from_model(cls, m, max_batch=None, max_seq=None, draft_len=None, flags=0, tp_size=1, tp_rank=0):
         """Build from any object with the model-shape attributes (e.g. synth.ModelConfig)."""
         return cls(m.n_layers, m.d_model, m.n_heads, m.n_kv_heads, m.head_dim, m.d_ff, m.vocab,
                    m.draft_len if draft_len is None else draft_len, max_batch or m.batch,
-                   max_seq or m.max_seq, m.dtype, m.rope_theta, m.rms_eps, m.kv_block, flags, tp_size, tp_rank)
+                   max_seq or m.max_seq, m.dtype, m.rope_theta, m.rms_eps, m.kv_block, flags, tp_size, tp_rank,
+                   getattr(m, "draft_blocks", 1))
 
     def to_c(self) -> N.sf_config:
         return N.sf_config(self.n_layers, self.d_model, self.n_heads, self.n_kv_heads, self.head_dim, self.d_ff,
                            self.vocab, self.draft_len, self.max_batch, self.max_seq, self.kv_block,
                            self.rope_theta, self.rms_eps, N.SF_BF16 if self.dtype == "bf16" else N.SF_FP32,
-                           self.tp_size, self.tp_rank, self.flags)
+                           self.tp_size, self.tp_rank, self.flags, self.draft_blocks)
 
     def vocab_shard(self):
         """[v0, v1): this rank's LM-head rows (whole 128-row tiles; the library's split)."""
@@ -103,14 +105,14 @@ def _source_tensor(name: str, w: dict, rope_pairs: int = 0, cfg: EngineConfig | 
     if leaf.endswith("wqkv"):
         p = pre + leaf[:-4]
         W = torch.cat([_rows(w[p + "wq"], r, tp), _rows(w[p + "wk"], r, tp), _rows(w[p + "wv"], r, tp)], dim=0)
-        if rope_pairs and not leaf.startswith("blk_"):
+        if rope_pairs and not leaf.startswith("blk"):  # (draft blocks: no RoPE, natural rows)
             W = _pair_interleave_heads(W, rope_pairs)
         return W
     if leaf.endswith("w_gu"):
         p = pre + leaf[:-4]
         return _interleave_gu(_rows(w[p + "w_gate"], r, tp), _rows(w[p + "w_up"], r, tp))
     if tp > 1:
-        if leaf in ("wo", "ctx_wo", "blk_wo", "w_down", "blk_w_down", "w_d"):
+        if leaf.endswith("wo") or leaf.endswith("w_down") or leaf == "w_d":  # row-parallel
             return _cols(w[name], r, tp)
         if name == "lm_head":
             v0, v1 = cfg.vocab_shard()

@@ -25,6 +25,7 @@ class ModelConfig:
     prompt_len: int
     gen_len: int
     kv_block: int = 16
+    draft_blocks: int = 1   # NEXT-2 "+Larger" (T4): stacked draft blocks, weights sf.blk<i>_* for i >= 1
     rope_theta: float = 10000.0
     rms_eps: float = 1e-6
 

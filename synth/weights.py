@@ -51,11 +51,17 @@ def weight_shapes(c: ModelConfig, n_layers: int | None = None):
     out += _attn_shapes("sf.blk_", c)
     out += [("sf.blk_ffn_norm", (d,)), ("sf.blk_w_gate", (F, d)), ("sf.blk_w_up", (F, d)),
             ("sf.blk_w_down", (d, F))]
+    for i in range(1, getattr(c, "draft_blocks", 1)):  # NEXT-2 "+Larger": appended, earlier seeds unchanged
+        b = f"sf.blk{i}_"
+        out.append((b + "attn_norm", (d,)))
+        out += _attn_shapes(b, c)
+        out += [(b + "ffn_norm", (d,)), (b + "w_gate", (F, d)), (b + "w_up", (F, d)), (b + "w_down", (d, F))]
     return out
 
 
 def _is_norm(name: str) -> bool:
-    return name.rsplit(".", 1)[-1] in _NORMS
+    leaf = name.rsplit(".", 1)[-1]
+    return leaf in _NORMS or (leaf.startswith("blk") and leaf.split("_", 1)[-1] in _NORMS)
 
 
 def make_weights(c: ModelConfig, seed: int = 0, device="cpu", norm_jitter: float = 0.0,

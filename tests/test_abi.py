@@ -97,3 +97,17 @@ def test_null_handle_calls(lib):
     assert lib.specformer_sync(None) == N.SF_ERR_ARG
     assert lib.specformer_kernel_launches(None) == -1
     lib.specformer_destroy(None)
+
+
+def test_draft_blocks_table(lib):
+    """NEXT-2 "+Larger": extra draft blocks appear as sf.blk<i>_* with the block's shapes."""
+    m = get_config("small").replace(draft_blocks=3)
+    tab = {n: s for n, s, *_ in weight_table(EngineConfig.from_model(m))}
+    for i in (1, 2):
+        b = f"sf.blk{i}_"
+        assert tab[b + "wqkv"] == tab["sf.blk_wqkv"] and tab[b + "w_down"] == tab["sf.blk_w_down"]
+        assert tab[b + "attn_norm"] == (m.d_model,)
+    assert not any(n.startswith("sf.blk3_") for n in tab)
+    c = EngineConfig.from_model(m).to_c()
+    c.draft_blocks = 5
+    assert lib.sf_weights_bytes(C.byref(c)) == -1

@@ -371,3 +371,14 @@ def test_draft_slot_causal_ablation_matches_oracle():
     assert not np.allclose(bi["steps"][0]["draft_logits"], res["steps"][0]["draft_logits"])
     ar = run_gpu(cfg, w, prompts, cfg.gen_len, k=0)
     assert ar["tokens"] == res["tokens"]
+
+
+def test_draft_blocks_larger_matches_oracle():
+    """NEXT-2 "+Larger" (T4, P497-514) as two stacked draft blocks: drafts and their logits follow
+    the oracle's two-block head, the verify stays exact, GPU SD == GPU AR."""
+    cfg = MID.replace(draft_blocks=2)
+    w, prompts = setup(cfg, seed=5, jitter=0.1)
+    res = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True)
+    assert _check_bf16(cfg, w, prompts, res, seqs=(0, cfg.batch - 1)) > 20
+    ar = run_gpu(cfg, w, prompts, cfg.gen_len, k=0)
+    assert ar["tokens"] == res["tokens"]

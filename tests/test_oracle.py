@@ -282,6 +282,23 @@ def test_draft_block_slot_causal_ablation():
     assert not np.allclose(Ec[0], O.draft_block(W, D)[0])
 
 
+def test_draft_blocks_larger_ablation():
+    """"+Larger" (T4, P497-514) read as stacked draft blocks: a second block whose output projections
+    are zero is the identity (so two blocks reduce to one), and a second block equals applying the
+    one-block function with that block's weights to the first block's output."""
+    cfg2 = MICRO.replace(draft_blocks=2)
+    w = make_weights(cfg2, seed=8, norm_jitter=0.1)
+    D = np.random.default_rng(12).normal(size=(cfg2.draft_len, cfg2.d_model))
+    E1 = O.draft_block(O.Weights(MICRO, w), D)
+    E2 = O.draft_block(O.Weights(cfg2, w), D)
+    assert not np.allclose(E1, E2)
+    moved = {k.replace("sf.blk1_", "sf.blk_"): v for k, v in w.items() if k.startswith("sf.blk1_")}
+    np.testing.assert_allclose(E2, O.draft_block(O.Weights(MICRO, {**w, **moved}), E1), rtol=1e-12, atol=1e-14)
+    w["sf.blk1_wo"].zero_()
+    w["sf.blk1_w_down"].zero_()
+    np.testing.assert_array_equal(O.draft_block(O.Weights(cfg2, w), D), E1)
+
+
 def test_draft_logits_shape_and_constant_case():
     cfg = MICRO
     W = W_of(cfg, seed=9)
