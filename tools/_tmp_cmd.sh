@@ -1,4 +1,6 @@
-mkdir -p gpurun_out/r02p
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r02p/build.log 2>&1
-for B in 1 16 64; do timeout 600 python bench.py --batch $B --no-cpu-baseline --forced-steps 0 > gpurun_out/r02p/b$B.json 2> gpurun_out/r02p/b$B.err; echo "b$B rc=$?"; done
-python tools/show_bench.py gpurun_out/r02p/*.json | grep -v "event\|timeline"
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+B=64 FULL=1 bash tools/profile_round.sh r02q
+B=16 bash tools/profile_round.sh r02q
+B=1 bash tools/profile_round.sh r02q
+for B in 64 1; do CFG=7b B=$B STEPS=2 timeout 300 python tools/ktrace.py > gpurun_out/r02q/ktrace_7b_b$B.txt 2>&1; done
+NO_NCU=1 bash tools/gpu_check.sh r02q_check
