@@ -1,6 +1,4 @@
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-B=64 FULL=1 bash tools/profile_round.sh r02q
-B=16 bash tools/profile_round.sh r02q
-B=1 bash tools/profile_round.sh r02q
-for B in 64 1; do CFG=7b B=$B STEPS=2 timeout 300 python tools/ktrace.py > gpurun_out/r02q/ktrace_7b_b$B.txt 2>&1; done
-NO_NCU=1 bash tools/gpu_check.sh r02q_check
+mkdir -p gpurun_out/r02r
+CMD="python bench.py --batch 64 --steps 2 --warmup 3 --no-cpu-baseline --forced-steps 0 --e2e-steps 2"
+$CMD > gpurun_out/r02r/plain.log 2>&1 && ncu --profile-from-start off --set full --clock-control none --import-source on -k "regex:attn_fd_kernel|resid_norm" -s 4 -c 3 -o gpurun_out/r02r/attn_b64 -f $CMD > gpurun_out/r02r/ncu.log 2>&1; echo rc=$?
