@@ -3,9 +3,13 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
 
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
 #include <utility>
 
 #define SF_DEV __device__ __forceinline__
@@ -93,6 +97,52 @@ inline bool pdl_enabled() {
   static const bool on = !(getenv("SF_NO_PDL") && atoi(getenv("SF_NO_PDL")) > 0);
   return on;
 }
+// Host: cuTensorMapEncodeTiled results cached by their arguments (the same weights, KV pools and
+// activation buffers are described again at every eager launch -- prefill runs thousands of them).
+struct TmapKey {
+  uint64_t w[18];
+  bool operator==(const TmapKey& o) const { return memcmp(w, o.w, sizeof(w)) == 0; }
+};
+struct TmapHash {
+  size_t operator()(const TmapKey& k) const {
+    uint64_t h = 1469598103934665603ull;
+    for (uint64_t v : k.w) h = (h ^ v) * 1099511628211ull;
+    return (size_t)h;
+  }
+};
+inline CUresult encode_tmap_cached(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, CUtensorMapDataType dt,
+                                   cuuint32_t rank, void* ptr, const cuuint64_t* dims, const cuuint64_t* strides,
+                                   const cuuint32_t* box, CUtensorMapSwizzle swz) {
+  TmapKey k;
+  memset(&k, 0, sizeof(k));
+  k.w[0] = (uint64_t)ptr;
+  k.w[1] = ((uint64_t)dt << 32) | ((uint64_t)swz << 8) | rank;
+  for (cuuint32_t i = 0; i < rank && i < 5; ++i) {
+    k.w[2 + i] = dims[i];
+    k.w[7 + i] = box[i];
+    if (i + 1 < rank) k.w[12 + i] = strides[i];
+  }
+  static std::mutex mu;
+  static std::unordered_map<TmapKey, CUtensorMap, TmapHash> cache;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(k);
+    if (it != cache.end()) {
+      *m = it->second;
+      return CUDA_SUCCESS;
+    }
+  }
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  const CUresult r = enc(m, dt, rank, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r == CUDA_SUCCESS) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() > 4096) cache.clear();  // (buffers of destroyed handles)
+    cache.emplace(k, *m);
+  }
+  return r;
+}
+
 // <<<grid, block, smem, stream>>> with the PDL attribute (and an optional cluster shape).
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -935,11 +935,8 @@ static bool make_map(CUtensorMap* m, const void* ptr, int rows, int K, int ld_el
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld_elems * 2};
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  return encode_tmap_cached(g_encode, m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                            box, CU_TENSOR_MAP_SWIZZLE_128B) == CUDA_SUCCESS;
 }
 
 // MMA N tiling of T token columns (granularity g: 16, or 32 for the multicast pairs whose quarter
@@ -1030,11 +1027,8 @@ static bool make_map_tiled(CUtensorMap* m, const void* ptr, long long rows) {
   cuuint64_t dims[2] = {(cuuint64_t)BK, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)BK * 2};
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)BM};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  return encode_tmap_cached(g_encode, m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                            box, CU_TENSOR_MAP_SWIZZLE_NONE) == CUDA_SUCCESS;
 }
 
 // CTA-pair (cta_group::2) mode for a weight shape: a function of (N, K) only (batch invariance)

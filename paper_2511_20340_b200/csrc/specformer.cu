@@ -183,7 +183,10 @@ Plan make_plan(const sf_config* c) {
   p.nchunk = (c->max_seq + kAttnChunk - 1) / kAttnChunk;
   p.rows_v = p.B * (p.k + 1);
   p.rows_d = std::max(1, p.B * p.k);
-  p.C_pf = std::max(p.k + 1, std::min(64, std::max(1, 512 / p.B)));
+  // prefill chunk: rows per sequence such that a chunk is one 512-row GEMM pass (the weights are
+  // streamed once per chunk; 512 = the TMEM accumulator width)
+  static const int pf_cap = getenv("SF_PF_CAP") ? atoi(getenv("SF_PF_CAP")) : 512;
+  p.C_pf = std::max(p.k + 1, std::min(pf_cap, std::max(1, 512 / p.B)));
   p.rows_pf = p.B * p.C_pf;
   p.R = std::max(p.rows_v, p.rows_pf);
   p.kv_layer_bytes = (int64_t)p.n_pages * p.Hkv * 16 * p.hd * p.act;
@@ -366,9 +369,12 @@ struct ProfScope {
 };
 
 // SF_DEBUG_SYNC=1 (debugging only): synchronise after every launch group and name the first failure
-static cudaError_t dbg_sync(sf_handle* h, const char* what, cudaError_t e) {
+static bool dbg_on() {
   static const bool on = getenv("SF_DEBUG_SYNC") && atoi(getenv("SF_DEBUG_SYNC")) > 0;
-  if (!on || e != cudaSuccess) return e;
+  return on;
+}
+static cudaError_t dbg_sync(sf_handle* h, const char* what, cudaError_t e) {
+  if (!dbg_on() || e != cudaSuccess) return e;
   cudaError_t r = cudaStreamSynchronize(h->st);
   if (r != cudaSuccess) fprintf(stderr, "SF_DEBUG_SYNC: %s failed: %s\n", what, cudaGetErrorString(r));
   return r;
@@ -402,9 +408,11 @@ static cudaError_t gemm(sf_handle* h, const void* A, int lda, const void* W, int
   sc.counters = h->gcnt;
   sc.n_counters = 4096;
   h->launches += (T + 511) / 512;
+  const cudaError_t e = gemm_launch(h->bf, A, lda, W, h->bf, T, N, K, epi, sc, h->st);
+  if (!dbg_on()) return e;
   char nm[96];
   snprintf(nm, sizeof nm, "gemm T=%d N=%d K=%d mode=%d", T, N, K, epi.mode);
-  return dbg_sync(h, nm, gemm_launch(h->bf, A, lda, W, h->bf, T, N, K, epi, sc, h->st));
+  return dbg_sync(h, nm, e);
 }
 static GemmEpi epi_act(void* out, int ldo) {
   GemmEpi e;
