@@ -111,8 +111,11 @@ SF_DEV unsigned long long gtimer() {
   return t;
 }
 // trace slots: 0 start, 1 setup done, 2 producer first issue, 3 MMA first full, 4 MMA last issue,
-// 5 epilogue done, 8 + 4 s + {0 MMA seg start, 1 MMA seg issued, 2 epi seg ready, 3 epi seg done}
-// (s < 4), 24 + i: MMA full-barrier pass of unit i (i < 40)
+// 5 epilogue done, 6 parked tile done, 8 + 4 s + {0 MMA seg start, 1 MMA seg issued, 2 epi seg ready,
+// 3 epi seg done} (s < 4), 24 + i: MMA full-barrier pass of unit i (i < 40), 64 + i: producer issue of
+// unit i, final phase 104 flags / 105 fixup loaded / 106 + 2c, 107 + 2c chunk c added / stored,
+// 114 + 4c TMEM loaded, 116 + 4c staged (c < 2), small-T head 122 flags / 123 fixed up / 124 stored,
+// setup 125 barriers initialised / 126 TMEM allocated / 127 CTA barrier (tools/gemm_trace_step.py)
 #define SF_TR(i) \
   do {           \
     if (p.trace) p.trace[(size_t)blockIdx.x * 128 + (i)] = gtimer(); \
