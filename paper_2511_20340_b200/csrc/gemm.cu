@@ -97,6 +97,12 @@ struct SkParams {
   int cgrp;  // ring slots released per tcgen05.commit
   int drain; // tile-entry cost of the stream-K partition (sk_begin)
   int park;  // park mid-range full tiles (T >= 64) for the final phase
+  // chain (gate/up -> down in one launch, CHAIN instantiation): phase B's k-blocks, tiles, drain,
+  // its partial slots, per-k-block readiness flags of phase A's output and the launch's done counter
+  int kbB, n_tilesB, drainB;
+  float* partialB;
+  int* readyB;
+  int* doneB;
   uint32_t tmem_cols;
   const __nv_bfloat16* w_tiles;  // tile-contiguous weights (w_tiled, CG == 1 bulk path)
   GemmEpi epi;
@@ -182,9 +188,10 @@ SF_DEV void tma_load_2d_2sm_mc(void* smem_dst, const CUtensorMap* map, uint64_t*
 // MODE = the epilogue (EpiMode), a template parameter so each instantiation carries only its own
 // store path: the kernel's code is executed cold once per CTA in the final phase, and every
 // instruction-cache line it does not need is a fetch that competes with the weight stream.
-template <int CG, int MODE>
+template <int CG, int MODE, bool CHAIN = false>
 __global__ void __launch_bounds__(384, 1)
-gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA, const SkParams p) {
+gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
+               const __grid_constant__ CUtensorMap tmWB, const __grid_constant__ CUtensorMap tmAB, const SkParams p) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
@@ -214,6 +221,14 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   const int nseg = u1 > u0 ? (int)((u1 - 1) / kb) - t_first + 1 : 0;
   auto seg_lo = [=](int i) -> long long { return max(u0, (long long)(t_first + i) * kb); };
   auto seg_hi = [=](int i) -> long long { return min(u1, (long long)(t_first + i + 1) * kb); };
+  // CHAIN: phase B (the down projection) -- this group's range of its own (tile, k-block) units
+  const int kbB = CHAIN ? p.kbB : 1;
+  const long long u0B = CHAIN ? sk_begin(c, p.G, p.n_tilesB, kbB, p.drainB) : 0;
+  const long long u1B = CHAIN ? sk_begin(c + 1, p.G, p.n_tilesB, kbB, p.drainB) : 0;
+  const int tB_first = (int)(u0B / kbB);
+  const int nsegB = u1B > u0B ? (int)((u1B - 1) / kbB) - tB_first + 1 : 0;
+  auto segB_lo = [=](int i) -> long long { return max(u0B, (long long)(tB_first + i) * kbB); };
+  auto segB_hi = [=](int i) -> long long { return min(u1B, (long long)(tB_first + i + 1) * kbB); };
   if (threadIdx.x == 0) SF_TR(0);
   KtScope kt_(KT_GEMM, (uint32_t)p.N | ((uint32_t)min(kb, 511) << 15), 128);  // param: N | (K / 64) << 15
 
@@ -336,6 +351,34 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       if (s > grp_last) grp_last += p.cgrp;
       if (s == 0) grp_last = p.cgrp - 1;
     }
+    if constexpr (CHAIN) {
+      // phase B: its weights stream into the ring as phase A's last stages free up; activation
+      // k-block k = features [64 k, 64 k + 64) of phase A's output, loaded once the CTA that writes
+      // them has published it
+      for (int si = 0; si < nsegB; ++si)
+      for (int t = tB_first + si, k = (int)(segB_lo(si) - (long long)t * kbB), ke = (int)(segB_hi(si) - (long long)t * kbB);
+           k < ke; ++k, ++j) {
+        mbar_wait(&empty[grp_last], ph ^ 1u);
+        if (elect_one()) {
+          uint8_t* st = smem + (size_t)s * stage_bytes;
+          if (prank == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * stage_bytes));
+          tma_load_2d_2sm(st, &tmWB, &full[s], 0, ((t * CG + (int)rank) * kbB + k) * BM, kEvictFirst);
+          while (ld_acquire(&p.readyB[k]) == 0) {
+          }
+          fence_proxy_async_global();  // phase A's generic stores -> this TMA read
+          for (int jj = 0; jj < p.n_sub; ++jj)
+            tma_load_2d_2sm(st + BM * BK * 2 + jj * a_rows * BK * 2, &tmAB, &full[s], k * BK,
+                            jj * p.NT + (int)rank * a_rows, kEvictLast);
+        }
+        __syncwarp();
+        if (++s == p.stages) {
+          s = 0;
+          ph ^= 1u;
+        }
+        if (s > grp_last) grp_last += p.cgrp;
+        if (s == 0) grp_last = p.cgrp - 1;
+      }
+    }
     if (p.epi.pf && p.epi.pf_bytes >= 16 * gridDim.x && elect_one()) {
       // this CTA's slice of the next GEMM's weights -> L2, while the last stages drain and the
       // epilogue runs (the DRAM would otherwise idle through the tail)
@@ -353,8 +396,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     int s = 0, gcnt = 0;
     uint32_t ph = 0;
     long long j = 0;  // units consumed
-    for (int seg = 0; seg < nseg; ++seg) {
-      const long long u = seg_lo(seg), se = seg_hi(seg);
+    for (int seg = 0; seg < nseg + nsegB; ++seg) {  // (phase B segments follow, CHAIN)
+      const long long u = seg < nseg ? seg_lo(seg) : segB_lo(seg - nseg);
+      const long long se = seg < nseg ? seg_hi(seg) : segB_hi(seg - nseg);
       const int b = seg % p.nbuf;
       mbar_wait(&acce[b], ((uint32_t)(seg / p.nbuf) & 1u) ^ 1u);
       tc_fence_after();
@@ -400,7 +444,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       __syncwarp();
       if (lane == 0) {
         if (seg < 4) SF_TR(8 + 4 * seg + 1);
-        if (seg == nseg - 1) SF_TR(4);
+        if (seg == nseg + nsegB - 1) SF_TR(4);
       }
     }
   }
@@ -639,20 +683,24 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     // Epilogue of segment [u, se) of tile t from TMEM buffer b by ng groups (this thread: group
     // gid, barrier over nthr threads). final: every MMA of the CTA has completed (ring idle).
     auto segment_epilogue = [&](long long u, int t, long long se, int b, int gid, int ng, int nthr, bool final,
-                                int& defer_vt) {
-      const long long ts = (long long)t * kb, te = ts + kb;
+                                int& defer_vt, bool phase_b) {
+      const int kbs = phase_b ? kbB : kb;
+      const long long ts = (long long)t * kbs, te = ts + kbs;
       const uint32_t t_row = tmem + (uint32_t)(b * cols) + ((uint32_t)(quad * 32) << 16);
       const int vt = t * CG + (int)rank;  // 128-row tile index of this CTA's rows
       const bool is_full = (u == ts) && (se == te);
       const bool is_head = (u == ts) && !is_full;
       const int cstep = 32 * ng;
-      if (mode == EPI_PARTIAL || (!is_full && !is_head) || (is_full && !final && can_stage && p.park && p.T >= 64)) {
+      if (phase_b || mode == EPI_PARTIAL || (!is_full && !is_head) ||
+          (is_full && !final && can_stage && p.park && p.T >= 64)) {
         // fp32 accumulator -> [T][128] slot (each warp store is one 128-byte line):
         //  EPI_PARTIAL: slot 2 group + (first segment of the range ? 0 : 1), reduced in k order by
         //    the consumer; tail of a tile owned by another group: this CTA's slot, then its flag;
         //  full tile in mid-range: parked, finished in the final phase instead of stalling the MMA
-        const bool tail = mode != EPI_PARTIAL && !is_full && !is_head;
-        float* dst = mode == EPI_PARTIAL
+        //  phase B of a chain: as EPI_PARTIAL, into its own partial slots
+        const bool tail = !phase_b && mode != EPI_PARTIAL && !is_full && !is_head;
+        float* dst = phase_b ? p.partialB + ((size_t)(2 * c + (u == u0B ? 0 : 1)) * CG + (int)rank) * p.T * BM
+                     : mode == EPI_PARTIAL
                          ? p.partial + ((size_t)(2 * c + (u == u0 ? 0 : 1)) * CG + (int)rank) * p.T * BM
                          : (tail ? slot_base : defer_base);
         for (int c0 = gid * 32; c0 < p.T; c0 += cstep) {
@@ -668,7 +716,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           named_sync(final ? 5 : 1, nthr);
           if (lead) st_release(&p.flags[slot], 1);
         }
-        if (mode != EPI_PARTIAL && is_full) defer_vt = vt;
+        if (!phase_b && mode != EPI_PARTIAL && is_full) defer_vt = vt;
         return;
       }
       // head or full tile: add the other groups' k segments of this tile (they publish them first
@@ -756,16 +804,23 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         if (lead)
           for (int cc = c_lo; cc <= c_hi; ++cc) p.flags[cc * CG + (int)rank] = 0;  // re-arm for the next launch
       }
+      if constexpr (CHAIN) {  // this CTA's output features of tile t are in memory: phase B may load them
+        __threadfence();
+        named_sync(final ? 5 : 1, nthr);
+        if (lead) st_release(&p.readyB[vt], 1);
+      }
     };
 
     // segments of [u0, u1): all but the last by the 8 epilogue warps while the MMA streams on; the
     // last one (and a parked full tile) by all 12 warps -- one inlined copy of the epilogue
-    const int nseg_total = nseg;
+    const int nseg_total = nseg + nsegB;
     int defer_vt = -1;
     int gid = 0;
     for (int seg = 0; seg < nseg_total; ++seg) {
-      const long long u = seg_lo(seg), se = seg_hi(seg);
-      const int t = (int)(u / kb);
+      const bool phase_b = seg >= nseg;  // (CHAIN)
+      const long long u = phase_b ? segB_lo(seg - nseg) : seg_lo(seg);
+      const long long se = phase_b ? segB_hi(seg - nseg) : seg_hi(seg);
+      const int t = (int)(u / (phase_b ? kbB : kb));
       // the 12-warp final phase pays off for large T only (small T: a few rows per chunk, the
       // extra barriers would dominate)
       const bool final = seg == nseg_total - 1 && p.T >= 64;
@@ -790,7 +845,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         // small T, a head piece with one or two partner segments: wait for the partners' flags and
         // load their partials of this thread's chunk now, off the critical path after the last MMA
         pre_fix = false;
-        if (mode != EPI_PARTIAL && !final && p.T <= kPreT && u == (long long)t * kb && se < (long long)(t + 1) * kb) {
+        if (!phase_b && mode != EPI_PARTIAL && !final && p.T <= kPreT && u == (long long)t * kb &&
+            se < (long long)(t + 1) * kb) {
           const int c_hi = sk_group_of(t * kb + kb - 1, p.G, p.n_tiles, kb, p.drain);
           const int n_o = c_hi - c;
           if (n_o >= 1 && n_o <= 2) {
@@ -813,7 +869,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         mbar_wait_sleep(&accf[b], (uint32_t)(seg / p.nbuf) & 1u);
         if (lead && seg < 4) SF_TR(8 + 4 * seg + 2);
         tc_fence_after();
-        segment_epilogue(u, t, se, b, gid, ng, nthr, final, defer_vt);
+        segment_epilogue(u, t, se, b, gid, ng, nthr, final, defer_vt, phase_b);
         if (!final) {
           tc_fence_before();
           named_sync(1, 256);
@@ -853,6 +909,17 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CHAIN) {
+    // the last CTA out re-arms the readiness flags for the next launch (every producer is done with them)
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(p.doneB, 1) == (int)gridDim.x - 1) {
+        for (int k = 0; k < p.kbB; ++k) p.readyB[k] = 0;
+        *p.doneB = 0;
+        __threadfence();
+      }
+    }
+  }
   if constexpr (kPair) cluster_sync();
   tc_fence_after();
   if (warp == 2) {
@@ -1076,7 +1143,7 @@ static int gemm_cg(int N, int K) {
   return 1;
 }
 
-using SkKernel = void (*)(const CUtensorMap, const CUtensorMap, const SkParams);
+using SkKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const SkParams);
 static SkKernel sk_kernel_for(int cg, int mode) {
 #define SF_SK(CGV)                                              \
   switch (mode) {                                               \
@@ -1094,13 +1161,26 @@ static SkKernel sk_kernel_for(int cg, int mode) {
 #undef SF_SK
 }
 
+// phase B of a chain launch (gate/up -> down): the down projection over the SwiGLU output
+struct ChainB {
+  const void* W;   // tiled weights [N, K]
+  int N, K;
+  const void* act;  // [T, K] bf16, row stride K (phase A's output)
+  float* partial;   // its EPI_PARTIAL slots
+  int* ready;       // [K / 64] readiness flags (zero)
+  int* done;        // launch counter (zero)
+};
+
 static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled, int T, int N, int K,
-                             const GemmEpi& epi, const GemmScratch& scratch, cudaStream_t st) {
+                             const GemmEpi& epi, const GemmScratch& scratch, cudaStream_t st,
+                             const ChainB* chain = nullptr) {
   static bool attr = false;
   if (!attr) {
     for (int cg = 1; cg <= 4; cg *= 2)
       for (int md = 0; md <= EPI_QKV_ROPE; ++md)
         cudaFuncSetAttribute(sk_kernel_for(cg, md), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(gemm_sk_kernel<2, EPI_SWIGLU_ACT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
     attr = true;
   }
   const int CG = (w_tiled && T >= 1) ? gemm_cg(N, K) : 1;
@@ -1165,8 +1245,26 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
     return cudaErrorInvalidValue;
   }
   if (!make_map(&ma, A, T, K, lda, p.NT / CG)) return cudaErrorInvalidValue;
+  CUtensorMap mwB = mw, maB = ma;
+  if (chain) {
+    if (CG != 2 || epi.mode != EPI_SWIGLU_ACT || gemm_cg(chain->N, chain->K) != 2 || chain->K * 2 != N)
+      return cudaErrorInvalidValue;
+    p.kbB = chain->K / BK;
+    p.n_tilesB = chain->N / (BM * CG);
+    if (std::min<long long>(max_groups(CG), (long long)p.n_tilesB * p.kbB) != p.G || p.n_tilesB > p.G)
+      return cudaErrorInvalidValue;  // both phases on the same groups; phase B published as EPI_PARTIAL
+    p.drainB = sk_drain(EPI_PARTIAL);
+    if (!sk_fits(p.G, p.n_tilesB, p.kbB, p.drainB)) return cudaErrorInvalidValue;
+    p.partialB = chain->partial;
+    p.readyB = chain->ready;
+    p.doneB = chain->done;
+    p.park = 0;  // (a parked tile's output would be written after phase B needs it)
+    if (!make_map_tiled(&mwB, chain->W, (long long)chain->N * p.kbB) ||
+        !make_map(&maB, chain->act, T, chain->K, chain->K, p.NT / CG))
+      return cudaErrorInvalidValue;
+  }
   if (CG == 1) {
-    launch_k(sk_kernel_for(1, epi.mode), dim3(p.G), dim3(384), smem, st, mw, ma, p);
+    launch_k(sk_kernel_for(1, epi.mode), dim3(p.G), dim3(384), smem, st, mw, ma, mw, ma, p);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg{};
@@ -1183,7 +1281,40 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   attrs[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, sk_kernel_for(2, epi.mode), mw, ma, p);
+  if (chain) return cudaLaunchKernelEx(&cfg, gemm_sk_kernel<2, EPI_SWIGLU_ACT, true>, mw, ma, mwB, maB, p);
+  return cudaLaunchKernelEx(&cfg, sk_kernel_for(2, epi.mode), mw, ma, mw, ma, p);
+}
+
+// Gate/up (SwiGLU) -> down in one launch (see gemm_sk_kernel CHAIN). Phase B's partial slots start
+// at scratch.partial + gemm_chain_partial_offset(T) floats; its k segmentation is the standalone
+// down GEMM's (same groups, same drain), so gemm_partial_geom / launch_resid_norm read it unchanged.
+static constexpr int kChainReady = 1024, kChainDone = 4000;  // GemmScratch::counters layout
+int64_t gemm_chain_partial_offset(int T) {
+  return (int64_t)2 * max_groups(2) * 2 * ((T + 31) / 32 * 32) * BM;
+}
+int64_t gemm_chain_partial_elems(int T) { return 2 * gemm_chain_partial_offset(T); }
+bool gemm_chain_supported(int T, int NA, int KA, int NB) {
+  const int KB = NA / 2;
+  if (T < 1 || T > 512 || NA % (2 * BM) || KA % BK || NB % (2 * BM) || KB % BK || KB / BK > kChainDone - kChainReady)
+    return false;
+  if (gemm_cg(NA, KA) != 2 || gemm_cg(NB, KB) != 2) return false;
+  const long long UA = (long long)(NA / (2 * BM)) * (KA / BK), UB = (long long)(NB / (2 * BM)) * (KB / BK);
+  const int G = max_groups(2);
+  PartialGeom g;
+  return UA >= G && UB >= G && NB / (2 * BM) <= G && gemm_partial_geom(T, NB, KB, &g);
+}
+cudaError_t gemm_chain_launch(const void* A, int lda, const void* WA, int NA, int KA, void* act, const void* WB,
+                              int NB, int T, const GemmScratch& scratch, cudaStream_t st) {
+  if (!gemm_chain_supported(T, NA, KA, NB) || !ensure_encode()) return cudaErrorInvalidValue;
+  if (scratch.n_counters <= kChainDone || scratch.partial_elems < gemm_chain_partial_elems(T))
+    return cudaErrorInvalidValue;
+  GemmEpi e;
+  e.mode = EPI_SWIGLU_ACT;
+  e.out = act;
+  e.ldo = NA / 2;
+  ChainB cb{WB, NB, NA / 2, act, scratch.partial + gemm_chain_partial_offset(T), scratch.counters + kChainReady,
+            scratch.counters + kChainDone};
+  return launch_sk(A, lda, WA, true, T, NA, KA, e, scratch, st, &cb);
 }
 
 bool gemm_partial_geom(int T, int N, int K, PartialGeom* g, int drain) {

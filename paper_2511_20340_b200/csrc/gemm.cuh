@@ -94,6 +94,17 @@ cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T,
                               const float* add, const float* bias, float* out, float* tap, const float* gamma,
                               float eps, __nv_bfloat16* xn, cudaStream_t s);
 
+// Gate/up (SwiGLU, rows interleaved) -> down in ONE launch: phase A computes act = SwiGLU(A . WA^T)
+// [T, NA/2] and publishes each finished 128-row tile; phase B (down, NB rows, K = NA/2) streams its
+// weights into the ring while phase A drains and loads an activation k-block once published. Phase B
+// is written as EPI_PARTIAL slots at scratch.partial + gemm_chain_partial_offset(T) with the
+// standalone down GEMM's k segmentation (bit-identical results; launch_resid_norm consumes them).
+bool gemm_chain_supported(int T, int NA, int KA, int NB);
+int64_t gemm_chain_partial_offset(int T);
+int64_t gemm_chain_partial_elems(int T);  // scratch floats the chain needs
+cudaError_t gemm_chain_launch(const void* A, int lda, const void* WA, int NA, int KA, void* act, const void* WB,
+                              int NB, int T, const GemmScratch& scratch, cudaStream_t s);
+
 // Consumer of an EPI_PARTIAL QKV projection (bf16, head_dim 128, one 128-row tile per head, rows
 // pair-interleaved per head as for EPI_QKV_ROPE): for every (row t, head h) the head's k-segment
 // partials are summed in k order (the first segment, then the others: the same additions as the

@@ -196,6 +196,7 @@ Plan make_plan(const sf_config* c) {
                            {p.d, p.wd_k}, {std::max(1, p.k) * p.d, p.d}};
   p.gpart_elems = 0;
   for (auto& s : shapes) p.gpart_elems = std::max<int64_t>(p.gpart_elems, gemm_partial_elems(bf, std::min(p.R, 512), s[0], s[1]));
+  if (bf) p.gpart_elems = std::max<int64_t>(p.gpart_elems, gemm_chain_partial_elems(std::min(p.R, 512)));
   p.n_amrows = std::max(p.rows_v, std::max(p.rows_d, p.B));
   int64_t o = 0;
   auto take = [&](int64_t bytes) {
@@ -495,6 +496,41 @@ static bool gemm_resid_norm(sf_handle* h, cudaError_t* err, const void* A, int l
   return true;
 }
 
+// Gate/up -> down + residual (+ tap) + next norm with the two GEMMs chained in one launch
+// (gemm_chain_launch; bit-identical to the unchained pair). Opt-in, SF_GEMM_CHAIN=1 (read per call):
+// measured no faster than the two launches -- every gate/up tile is finished by its
+// head group near the end of the gate/up pass, so the down pass still waits for it. Returns false
+// (nothing launched) when off or when the shapes do not allow it.
+static bool chain_ffn(sf_handle* h, cudaError_t* err, const void* wgu, const void* wdown, int T, float* resid,
+                      float* tap, const float* gamma) {
+  const char* env = getenv("SF_GEMM_CHAIN");
+  if (!env || atoi(env) == 0) return false;
+  const Plan& p = h->p;
+  if (!h->bf || p.tp > 1 || T > 512 || !gemm_chain_supported(T, 2 * p.F, p.d, p.d) ||
+      !resid_norm_supported(p.d, T, p.d, p.F))
+    return false;
+  PartialGeom g;
+  if (!gemm_partial_geom(T, p.d, p.F, &g)) return false;
+  GemmScratch sc;
+  sc.partial = h->gpart;
+  sc.partial_elems = p.gpart_elems;
+  sc.counters = h->gcnt;
+  sc.n_counters = 4096;
+  {
+    ProfScope ps(h, 0, (double)2 * p.F * p.d * 2 + (double)p.d * p.F * 2);
+    h->launches++;
+    if ((*err = dbg_sync(h, "gemm chain", gemm_chain_launch(h->xn, p.d, wgu, 2 * p.F, p.d, h->ffn, wdown, p.d, T, sc,
+                                                            h->st))) != cudaSuccess)
+      return true;
+  }
+  ProfScope ps(h, 2, (double)T * p.d * 4.0 * 3);
+  h->launches++;
+  *err = dbg_sync(h, "resid_norm", launch_resid_norm(h->gpart + gemm_chain_partial_offset(T), &g, T, 1, p.d, resid,
+                                                     nullptr, nullptr, resid, tap, gamma, h->c.rms_eps,
+                                                     gamma ? (__nv_bfloat16*)h->xn : nullptr, h->st));
+  return true;
+}
+
 static const int* taps_layers(int L, int* out4) {
   out4[0] = 0;
   out4[1] = L / 2;
@@ -625,22 +661,27 @@ static cudaError_t base_forward(sf_handle* h, int T, int q_len, const int* pos0,
       e = rmsnorm(h, h->resid, p.d, w.ffn_norm, T, h->xn, p.d);
     }
     if (e) return e;
-    GemmEpi sw;
-    sw.mode = EPI_SWIGLU_ACT;
-    sw.out = h->ffn;
-    sw.ldo = p.F;
-    if ((e = gemm(h, h->xn, p.d, w.wgu, T, 2 * p.F, p.d, sw))) return e;
     // down-proj + residual (+ hook tap HS[l+1]) + the next RMSNorm
     int first = -1;
     for (int g = 0; g < 4; ++g)
       if (tl[g] == l + 1 && first < 0) first = g;
     float* tap = first >= 0 ? h->taps + first * tstride : nullptr;
     const float* next_g = (l + 1 < p.L) ? h->lw[l + 1].attn_norm : (final_norm ? h->final_norm : nullptr);
-    if (gemm_resid_norm(h, &e, h->ffn, p.F, w.wdown, T, p.d, p.F, 1, h->resid, nullptr, h->resid, tap, next_g, true)) {
+    if (chain_ffn(h, &e, w.wgu, w.wdown, T, h->resid, tap, next_g)) {
       xn_ready = next_g != nullptr;
     } else {
-      if ((e = gemm(h, h->ffn, p.F, w.wdown, T, p.d, p.F, epi_add(h->resid, p.d, tap)))) return e;
-      xn_ready = false;
+      GemmEpi sw;
+      sw.mode = EPI_SWIGLU_ACT;
+      sw.out = h->ffn;
+      sw.ldo = p.F;
+      if ((e = gemm(h, h->xn, p.d, w.wgu, T, 2 * p.F, p.d, sw))) return e;
+      if (gemm_resid_norm(h, &e, h->ffn, p.F, w.wdown, T, p.d, p.F, 1, h->resid, nullptr, h->resid, tap, next_g,
+                          true)) {
+        xn_ready = next_g != nullptr;
+      } else {
+        if ((e = gemm(h, h->ffn, p.F, w.wdown, T, p.d, p.F, epi_add(h->resid, p.d, tap)))) return e;
+        xn_ready = false;
+      }
     }
     if (e) return e;
     for (int g = first + 1; first >= 0 && g < 4; ++g)

@@ -382,3 +382,19 @@ def test_draft_blocks_larger_matches_oracle():
     assert _check_bf16(cfg, w, prompts, res, seqs=(0, cfg.batch - 1)) > 20
     ar = run_gpu(cfg, w, prompts, cfg.gen_len, k=0)
     assert ar["tokens"] == res["tokens"]
+
+
+@pytest.mark.parametrize("cfg", [W7D2, GQA2K], ids=["7b_width_depth2", "gqa_d2048"])
+def test_chained_ffn_bit_exact(cfg, monkeypatch):
+    """The gate/up -> down chain (one launch: the down projection's weights stream while the gate/up
+    tiles finish; its activation k-blocks load as they are published) keeps both GEMMs' k
+    segmentation: bit-identical logits, drafts and tokens with the chain on and off."""
+    w, prompts = setup(cfg, seed=9, jitter=0.1)
+    monkeypatch.setenv("SF_GEMM_CHAIN", "1")
+    on = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True)
+    monkeypatch.setenv("SF_GEMM_CHAIN", "0")
+    off = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True)
+    assert on["tokens"] == off["tokens"]
+    for s1, s2 in zip(on["steps"], off["steps"]):
+        assert np.array_equal(s1["logits"], s2["logits"])
+        assert np.array_equal(s1["draft_logits"], s2["draft_logits"])
