@@ -398,3 +398,32 @@ def test_chained_ffn_bit_exact(cfg, monkeypatch):
     for s1, s2 in zip(on["steps"], off["steps"]):
         assert np.array_equal(s1["logits"], s2["logits"])
         assert np.array_equal(s1["draft_logits"], s2["draft_logits"])
+
+
+# ------------------------------------------------------------------ 7B shape at full depth (bf16)
+def test_full_depth_7b_bf16():
+    """Reading C21 (iii)/(iv) at full depth (32 layers, d = 4096): logits and draft logits rel-L2 within
+    2x the ideal bf16 pipeline's (<= 9e-2; an ideal pipeline already gives ~4e-2 and flips ~4% of the
+    margin > 5e-2 positions), so tokens are checked as epsilon-argmax (the GPU's token is
+    within 4 sigma_diff of the oracle's best logit) and the strict flip rate is reported; accept
+    lengths exact; GPU SD == GPU AR bit-exact (the hard losslessness assertion at depth)."""
+    cfg = get_config("7b").replace(batch=1, prompt_len=48, gen_len=8)
+    w, prompts = setup(cfg, seed=11, jitter=0.1)
+    res = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True)
+    _, rep = oracle_replay(cfg, w, prompts[0].tolist(), res["steps"], 0)
+    flips = checked = 0
+    for s, r in zip(res["steps"], rep):
+        gl, ol = s["logits"][0].astype(np.float64), r["logits"]
+        assert rel_l2(gl, ol) <= 9e-2, rel_l2(gl, ol)
+        dl, odl = s["draft_logits"][0].astype(np.float64), r["draft_logits"]
+        assert rel_l2(dl, odl) <= 9e-2, rel_l2(dl, odl)
+        sig = float(np.std(gl - ol))
+        for i in range(cfg.draft_len + 1):
+            assert ol[i][s["greedy"][0][i]] >= ol[i].max() - 4 * sig  # epsilon-argmax
+            if O.top2_margin(ol[i]) > 5e-2:
+                checked += 1
+                flips += int(s["greedy"][0][i] != r["greedy"][i])
+        assert O.accept(s["draft"][0], s["greedy"][0])[0] == s["m"][0]
+    print(f"full-depth 7B bf16: {flips}/{checked} argmax flips where the oracle margin > 5e-2 (reported)")
+    ar = run_gpu(cfg, w, prompts, cfg.gen_len, k=0)
+    assert ar["tokens"] == res["tokens"]
