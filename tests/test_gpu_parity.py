@@ -194,7 +194,8 @@ MID = SMALL.replace(name="mid", n_layers=2, d_model=512, n_heads=4, n_kv_heads=4
 GQA = MID.replace(name="gqa", d_model=1024, n_heads=8, n_kv_heads=2, prompt_len=200, batch=3)
 
 
-def _check_bf16(cfg, w, prompts, res, seqs, rel_tol=1.5e-2, slot_causal=False):
+def _check_bf16(cfg, w, prompts, res, seqs, rel_tol=1.5e-2, slot_causal=False, draft_tol=None):
+    draft_tol = rel_tol if draft_tol is None else draft_tol
     checked = 0
     for b in seqs:
         _, rep = oracle_replay(cfg, w, prompts[b].tolist(), res["steps"], b, slot_causal)
@@ -206,7 +207,7 @@ def _check_bf16(cfg, w, prompts, res, seqs, rel_tol=1.5e-2, slot_causal=False):
                     checked += 1
                     assert s["greedy"][b][i] == r["greedy"][i]
             odl = r["draft_logits"]
-            assert rel_l2(s["draft_logits"][b].astype(np.float64), odl) <= rel_tol
+            assert rel_l2(s["draft_logits"][b].astype(np.float64), odl) <= draft_tol
             for j in range(cfg.draft_len):
                 if O.top2_margin(odl[j]) > 5e-2:
                     assert s["draft"][b][j] == O.argmax_lowest(odl[j])
@@ -235,14 +236,21 @@ GQA2K = get_config("70b").replace(name="70b-w2k", n_layers=2, d_model=2048, n_he
                                   d_ff=5632, batch=2, prompt_len=150, gen_len=8)
 
 
-@pytest.mark.parametrize("cfg", [W7D2, GQA2K], ids=["7b_width_depth2", "gqa_d2048"])
+W13D2 = get_config("13b").replace(name="13b-d2", n_layers=2, batch=2, prompt_len=160, gen_len=8)
+
+
+@pytest.mark.parametrize("cfg", [W7D2, GQA2K, W13D2], ids=["7b_width_depth2", "gqa_d2048", "13b_width_depth2"])
 def test_full_width_depth2_bf16(cfg):
-    """Reading C21 (iii)/(iv): full-width bf16 at depth 2 -- logits rel-L2 <= 2.2e-2 and tokens exact
-    where the oracle margin > 5e-2; GPU SD == GPU AR bit-exact; exercises the fused partial-GEMM ->
-    residual/RMSNorm consumer and the flash-decoding attention at d = 4096 / GQA."""
+    """Reading C21 (iii)/(iv): full-width bf16 at depth 2 -- logits rel-L2 <= 2.2e-2 (2x the ideal
+    pipeline's 1.1e-2 at depth 2) and tokens exact where the oracle margin > 5e-2; GPU SD ==
+    GPU AR bit-exact; exercises the fused partial-GEMM -> residual/RMSNorm consumer and the
+    flash-decoding attention at d = 4096 / 5120 / GQA. The draft logits pass through one more
+    transformer block (the draft block) and W_D on top of the L base layers, so their ideal error is the
+    depth-3 one, interpolated between the ideal depth-2 (1.1e-2) and depth-4 (1.5e-2) rows: 1.3e-2;
+    asserted at 2x that, 2.6e-2 (C21)."""
     w, prompts = setup(cfg, seed=7, jitter=0.1)
     res = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True)
-    assert _check_bf16(cfg, w, prompts, res, seqs=(0,), rel_tol=2.2e-2) > 10
+    assert _check_bf16(cfg, w, prompts, res, seqs=(0,), rel_tol=2.2e-2, draft_tol=2.6e-2) > 10
     ar = run_gpu(cfg, w, prompts, cfg.gen_len, k=0)
     assert ar["tokens"] == res["tokens"]
 
