@@ -318,12 +318,15 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
       }
       l_lo = l_lo * a_lo + ps_lo;
       l_hi = l_hi * a_hi + ps_hi;
+      // (no row of the warp raised its max: every factor is exactly 1 and the rescale is the identity)
+      if (!__all_sync(0xffffffffu, a_lo == 1.f && a_hi == 1.f)) {
 #pragma unroll
-      for (int nt = 0; nt < 16; ++nt) {
-        o[nt][0] *= a_lo;
-        o[nt][1] *= a_lo;
-        o[nt][2] *= a_hi;
-        o[nt][3] *= a_hi;
+        for (int nt = 0; nt < 16; ++nt) {
+          o[nt][0] *= a_lo;
+          o[nt][1] *= a_lo;
+          o[nt][2] *= a_hi;
+          o[nt][3] *= a_hi;
+        }
       }
       // O += P V_w: 2 k-steps (this warp's 32 keys) x 16 n-tiles (128 dims)
 #pragma unroll
