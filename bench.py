@@ -195,7 +195,10 @@ def run_ours(args, cfg):
                                     [n for n, _ in weight_shapes(cfg)])
     else:
         weights = make_weights(cfg, seed=0, device="cuda")
-    ec = EngineConfig.from_model(cfg, max_batch=B, max_seq=max_seq, flags=N.SF_FLAG_CUDA_GRAPH,
+    # the step consumes only the argmax of the logits: the bf16 LM heads fuse it and do not store them
+    no_logits = cfg.dtype == "bf16" and not args.keep_logits
+    ec = EngineConfig.from_model(cfg, max_batch=B, max_seq=max_seq,
+                                 flags=N.SF_FLAG_CUDA_GRAPH | (N.SF_FLAG_NO_LOGITS if no_logits else 0),
                                  tp_size=tp, tp_rank=rank if tp > 1 else 0)
     eng = Engine(ec, weights)
     del weights
@@ -242,7 +245,7 @@ def run_ours(args, cfg):
     sb = 0.0
     prev_t = prev_before.tolist()
     for s in range(K):
-        sb += roofline.step_bytes(cfg, B, k, lens_t, prev_t)
+        sb += roofline.step_bytes(cfg, B, k, lens_t, prev_t, logits=not no_logits)
         prev_t = list(lens_t)
         lens_t = [n + m + 1 for n, m in zip(lens_t, accs_t[s])]
     sb /= tp  # tensor parallelism: each GPU streams its 1/tp of the weights and of the KV heads
@@ -253,7 +256,7 @@ def run_ours(args, cfg):
         lens, prevs, kv, by, fl = list(lens0), list(prev0), 0.0, 0.0, 0.0
         for a in accs:
             kv += roofline.attention_kv_bytes(cfg, lens, prevs, k)
-            by += roofline.step_bytes(cfg, B, k, lens, prevs)
+            by += roofline.step_bytes(cfg, B, k, lens, prevs, logits=not no_logits)
             fl += roofline.step_flops(cfg, B, k, lens)
             prevs = list(lens)
             lens = [n + m + 1 for n, m in zip(lens, a)]
@@ -470,7 +473,7 @@ def run_ours(args, cfg):
                                    f"batch {B}/GPU, k {k}, prompt {P}",
                        "model": cfg.name, "batch_per_gpu": B if tp == 1 else B / tp, "global_batch": B * world // tp,
                        "draft_len": k, "prompt_len": P, "parallelism": f"tp{tp}" if tp > 1 else f"dp{world}",
-                       "cuda_graph": True,
+                       "cuda_graph": True, "logits": "not stored (fused LM-head argmax)" if no_logits else "stored",
                        "l2": "inputs larger than L2 (14 GB weights + KV per step)"},
             "verify_steps_per_s": steps_per_s, "verify_steps_per_s_box": steps_per_s * world,
             "mean_accepted_length": a_meas,
@@ -520,6 +523,8 @@ def main():
     ap.add_argument("--timeline-steps", type=int, default=2, help="graph steps replayed with the kernel timeline on")
     ap.add_argument("--draft-len", type=int, default=None, help="override k (13B sweep: 4 / 6 / 8)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--keep-logits", action="store_true", help="store the fp32 logits every step (the API's "
+                    "logits read-out; default: not stored, the LM heads' fused argmax gives the tokens)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

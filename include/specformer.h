@@ -58,6 +58,10 @@ typedef enum { SF_FP32 = 0, SF_BF16 = 1 } sf_dtype;
 /* flags */
 #define SF_FLAG_CUDA_GRAPH  (1ull << 0) /* capture draft+verify+accept as one CUDA graph for decode_steps */
 #define SF_FLAG_DRAFT_CAUSAL (1ull << 1) /* NEXT-2 ablation "+Att Mask": causal draft-slot mask (not default) */
+/* NEXT-4, bf16 only: the LM-head GEMMs do not store the fp32 logits (the greedy / draft tokens come
+ * from the argmax fused into their epilogue either way); specformer_read_logits then
+ * returns SF_ERR_STATE. */
+#define SF_FLAG_NO_LOGITS   (1ull << 2)
 
 typedef struct {
   int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab;

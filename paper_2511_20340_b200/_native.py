@@ -18,6 +18,7 @@ STATUS_NAMES = ["SF_OK", "SF_ERR_ARG", "SF_ERR_SHAPE", "SF_ERR_CAPACITY", "SF_ER
 SF_FP32, SF_BF16 = 0, 1
 SF_FLAG_CUDA_GRAPH = 1 << 0
 SF_FLAG_DRAFT_CAUSAL = 1 << 1
+SF_FLAG_NO_LOGITS = 1 << 2
 
 
 class sf_config(C.Structure):

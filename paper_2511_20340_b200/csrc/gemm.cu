@@ -544,7 +544,40 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     // one 32-token chunk of this thread's row m: stage [32 tokens][tile columns] in smem, then
     // write whole rows with 16-byte vectors (per-thread column stores would be 32-byte sectors
     // 10-100 KB apart)
+    // (EPI_STORE_F32 + amax) the best (logit, id) key of each of the 32 tokens over this warp's 32
+    // rows: a butterfly reduce-scatter (31 exchanges) leaves token c0 + lane's key in lane `lane`
+    auto amax_keys = [&](const float (&v)[32], int c0, int nq, int vt_) {
+      const unsigned id = p.epi.amax_v0 + (unsigned)(vt_ * BM + m);
+      unsigned long long k[32];
+      bool bad = false;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const float x = v[q] == 0.f ? 0.f : v[q];  // -0 -> +0
+        bad |= (q < nq) && !isfinite(x);
+        unsigned u = __float_as_uint(x);
+        u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+        k[q] = (q < nq) ? (((unsigned long long)u << 32) | (0xFFFFFFFFu - id)) : 0ull;
+      }
+#pragma unroll
+      for (int s = 16; s >= 1; s >>= 1) {
+        const bool up = (lane & s) != 0;
+#pragma unroll
+        for (int j = 0; j < s; ++j) {
+          const unsigned long long keep = up ? k[j + s] : k[j];
+          const unsigned long long r = __shfl_xor_sync(0xffffffffu, up ? k[j] : k[j + s], s);
+          k[j] = keep > r ? keep : r;
+        }
+      }
+      if (lane < nq) atomicMax(p.epi.amax + c0 + lane, k[0]);
+      if (bad && p.epi.amax_err) atomicOr(p.epi.amax_err, 1);
+    };
     auto staged_store = [&](float (&v)[32], int c0, int nq, int vt_, int gid) {
+      if constexpr (MODE == EPI_STORE_F32) {
+        if (p.epi.amax) {
+          amax_keys(v, c0, nq, vt_);
+          if (!p.epi.out) return;  // (uniform over the CTA)
+        }
+      }
       uint8_t* sb = stg + (size_t)gid * kStageBytes;
       const int rowb = mode == EPI_SWIGLU_ACT ? 128 : ((mode == EPI_STORE_ACT || mode == EPI_QKV_ROPE) ? 256 : 512);
       if constexpr (MODE == EPI_QKV_ROPE) {
@@ -606,6 +639,12 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       if constexpr (MODE == EPI_QKV_ROPE) {
         rope_rows(v, c0, nq, vt_, [&](int q, int dim, float y, __nv_bfloat16* row) { row[dim] = __float2bfloat16_rn(y); });
         return;
+      }
+      if constexpr (MODE == EPI_STORE_F32) {
+        if (p.epi.amax) {
+          amax_keys(v, c0, nq, vt_);
+          if (!p.epi.out) return;
+        }
       }
       const int n = vt_ * BM + m;
       if (mode == EPI_STORE_ACT) {
@@ -1647,6 +1686,8 @@ cudaError_t gemm_launch(bool is_bf16, const void* A, int lda, const void* W, boo
     if (epi.mode == EPI_QKV_ROPE) e.rope.t0 = epi.rope.t0 + t0;
     else e.out = (char*)epi.out + (size_t)t0 * epi.ldo * out_elt;
     if (epi.tap) e.tap = epi.tap + (size_t)t0 * epi.ldo;
+    if (epi.amax) e.amax = epi.amax + t0;
+    if (!epi.out) e.out = nullptr;
     cudaError_t r = gemm_launch_chunk(true, (const char*)A + (size_t)t0 * lda * 2, lda, W, w_tiled,
                                       std::min(chunk, T - t0), N, K, e, scratch, st);
     if (r != cudaSuccess) return r;

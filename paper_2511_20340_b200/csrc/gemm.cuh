@@ -47,6 +47,14 @@ struct GemmEpi {
   // whose results must agree bit for bit across modes (the QKV projection: EPI_QKV_ROPE for short
   // blocks, EPI_PARTIAL + launch_rope_partial for long ones) pass the same value.
   int drain = -1;
+  // EPI_STORE_F32 on the tcgen05 path (the LM head, NEXT-4): argmax fused into the epilogue. For
+  // each row t the CTA reduces its tile's packed keys orderable(acc) << 32 | (0xFFFFFFFF - (amax_v0 +
+  // n)) over n with warp shuffles and atomicMax-es them into amax[t] (largest logit, lowest id on
+  // ties; +0 and -0 compare equal), which must hold 0 (or a smaller key) beforehand; a non-finite
+  // value sets *amax_err. out == nullptr: the fp32 values are not stored at all.
+  unsigned long long* amax = nullptr;
+  unsigned amax_v0 = 0;
+  int* amax_err = nullptr;
 };
 
 struct GemmScratch {

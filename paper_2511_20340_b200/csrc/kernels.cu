@@ -673,7 +673,7 @@ __global__ void argmax_final_kernel(const float* pval, const int* pidx, int R, i
 // logit, lowest id on ties -- the same rule as above over the whole vocabulary), and the winner's id
 // is unpacked.
 SF_DEV unsigned long long argmax_key(float v, unsigned id) {
-  unsigned u = __float_as_uint(v);
+  unsigned u = __float_as_uint(v == 0.f ? 0.f : v);  // (-0 == +0, as in better())
   u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // order-preserving map of the finite floats
   return ((unsigned long long)u << 32) | (0xFFFFFFFFu - id);
 }
@@ -690,7 +690,7 @@ __global__ void argmax_key_kernel(const float* pval, const int* pidx, int R, int
   for (int s = 0; s < nsplit; ++s) better(bv, bi, pval[row * nsplit + s], pidx[row * nsplit + s]);
   keys[row] = (bi == INT_MAX) ? 0ull : argmax_key(bv, (unsigned)(v0 + bi));
 }
-__global__ void argmax_unkey_kernel(const unsigned long long* keys, int R, int* out) {
+__global__ void argmax_unkey_kernel(unsigned long long* keys, int R, int* out, int reset) {
   KtScope kt_(KT_ARGMAX_F, 0u);
   pdl_wait();
   kt_.mark();
@@ -699,6 +699,7 @@ __global__ void argmax_unkey_kernel(const unsigned long long* keys, int R, int* 
   if (row >= R) return;
   const unsigned long long k = keys[row];
   out[row] = k ? (int)(0xFFFFFFFFu - (unsigned)(k & 0xFFFFFFFFull)) : 0;
+  if (reset) keys[row] = 0ull;  // ready for the next fused-argmax launch
 }
 
 // ------------------------------------------------------------------------ accept + commit
@@ -954,8 +955,8 @@ cudaError_t launch_argmax_key(const float* logits, int R, int V, int v0, float* 
   launch_k(argmax_partial_kernel, dim3(grid), dim3(256), 0, s, logits, V, ns, pval, pidx, err);
   return launch_k(argmax_key_kernel, dim3(SF_GRID(R, 128)), dim3(128), 0, s, pval, pidx, R, ns, v0, keys);
 }
-cudaError_t launch_argmax_unkey(const unsigned long long* keys, int R, int* out, cudaStream_t s) {
-  return launch_k(argmax_unkey_kernel, dim3(SF_GRID(R, 128)), dim3(128), 0, s, keys, R, out);
+cudaError_t launch_argmax_unkey(unsigned long long* keys, int R, int* out, cudaStream_t s, bool reset) {
+  return launch_k(argmax_unkey_kernel, dim3(SF_GRID(R, 128)), dim3(128), 0, s, keys, R, out, reset ? 1 : 0);
 }
 
 cudaError_t launch_argmax(const float* logits, int R, int V, float* pval, int* pidx, int* out, int* err,

@@ -53,7 +53,8 @@ cudaError_t launch_argmax(const float* logits, int R, int V, float* pval, int* p
 // tensor parallelism: per-row packed (logit, v0 + id) keys of this vocabulary shard / their unpacking
 cudaError_t launch_argmax_key(const float* logits, int R, int V, int v0, float* pval, int* pidx,
                               unsigned long long* keys, int* err, cudaStream_t s);
-cudaError_t launch_argmax_unkey(const unsigned long long* keys, int R, int* out, cudaStream_t s);
+// (reset: zero the keys after reading them, for the next fused-argmax LM head)
+cudaError_t launch_argmax_unkey(unsigned long long* keys, int R, int* out, cudaStream_t s, bool reset = false);
 // tensor parallelism, tests (one process, several handles): out[i] = sum / max over the n buffers in
 // buffer order
 cudaError_t launch_reduce_bufs(const void* const* bufs, int n, int64_t count, bool max_u64, void* out,

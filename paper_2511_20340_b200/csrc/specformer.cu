@@ -233,7 +233,7 @@ Plan make_plan(const sf_config* c) {
   p.o_ints = take((int64_t)(16 * p.B + 2 * p.R + 8 + p.rows_v * 2 + p.rows_d) * 4);
   p.o_prompt = take((int64_t)p.B * c->max_seq * 4);
   p.o_tpbuf = p.tp > 1 ? take((int64_t)p.R * p.d * 4) : 0;   // row-parallel GEMM output, all-reduced
-  p.o_tpkey = p.tp > 1 ? take(p.n_amrows * 8) : 0;           // packed (logit, id) argmax keys, max-reduced
+  p.o_tpkey = bf ? take(p.n_amrows * 8) : 0;  // packed (logit, id) argmax keys (fused LM-head argmax; TP max-reduces them)
   p.total = o;
   return p;
 }
@@ -384,7 +384,7 @@ static cudaError_t dbg_sync(sf_handle* h, const char* what, cudaError_t e) {
 static cudaError_t gemm(sf_handle* h, const void* A, int lda, const void* W, int T, int N, int K, GemmEpi epi) {
   const double wb = h->bf ? 2.0 : 4.0;
   const double ob = (epi.mode == EPI_STORE_ACT || epi.mode == EPI_SWIGLU_ACT) ? wb : 4.0;
-  const double outc = epi.mode == EPI_SWIGLU_ACT ? N / 2 : N;
+  const double outc = epi.amax && !epi.out ? 2 : epi.mode == EPI_SWIGLU_ACT ? N / 2 : N;  // (fused argmax: a key)
   // algorithmic bytes: weight once + activation once + output once (+ residual read for ADD)
   ProfScope ps(h, 0, (double)N * K * wb + (double)T * K * wb + (double)T * outc * ob * (epi.mode == EPI_ADD_F32 ? 2 : 1));
   static const size_t cap = (size_t)(getenv("SF_GEMM_PF_MB") ? atof(getenv("SF_GEMM_PF_MB")) : 0.0) * (1 << 20);
@@ -722,15 +722,22 @@ static cudaError_t head_argmax(sf_handle* h, const float* src, int T, float* log
   const Plan& p = h->p;
   cudaError_t e;
   if (!xn_ready && (e = rmsnorm(h, src, p.d, h->final_norm, T, h->xn, p.d))) return e;
+  if (h->bf) {
+    // LM head with the argmax fused into its epilogue (packed (logit, id) keys, NEXT-4); a
+    // vocabulary-sharded head max-reduces the shards' keys (TP), then the winner's id is unpacked
+    GemmEpi ea = epi_f32((h->c.flags & SF_FLAG_NO_LOGITS) ? nullptr : logits, p.V);
+    ea.amax = h->tpkey;
+    ea.amax_v0 = (unsigned)p.v0;
+    ea.amax_err = h->err;
+    if ((e = gemm(h, h->xn, p.d, h->lm_head, T, p.V, p.d, ea))) return e;
+    h->launches++;
+    ProfScope ps(h, 3, (double)T * 8.0);
+    if (p.tp > 1 && (e = tp_max(h, h->tpkey, T))) return e;
+    return launch_argmax_unkey(h->tpkey, T, out, h->st, true);
+  }
   if ((e = gemm(h, h->xn, p.d, h->lm_head, T, p.V, p.d, epi_f32(logits, p.V)))) return e;
   h->launches += 2;
   ProfScope ps(h, 3, (double)T * p.V * 4.0);
-  if (p.tp > 1) {  // vocabulary-sharded head: max-reduce the shards' packed (logit, id) keys
-    if ((e = launch_argmax_key(logits, T, p.V, p.v0, h->amv, h->ami, h->tpkey, h->err, h->st))) return e;
-    if ((e = tp_max(h, h->tpkey, T))) return e;
-    h->launches++;
-    return launch_argmax_unkey(h->tpkey, T, out, h->st);
-  }
   return launch_argmax(logits, T, p.V, h->amv, h->ami, out, h->err, h->st);
 }
 
@@ -1080,7 +1087,7 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
   h->amv = (float*)(w + p.o_amv);
   h->ami = (int*)(w + p.o_ami);
   h->tpbuf = p.tp > 1 ? (float*)(w + p.o_tpbuf) : nullptr;
-  h->tpkey = p.tp > 1 ? (unsigned long long*)(w + p.o_tpkey) : nullptr;
+  h->tpkey = h->bf ? (unsigned long long*)(w + p.o_tpkey) : nullptr;
   int* ip = (int*)(w + p.o_ints);
   auto ints = [&](int n) {
     int* r = ip;
@@ -1150,6 +1157,7 @@ sf_status specformer_prefill(sf_handle* h, const int32_t* tokens, int32_t B, int
   const Plan& p = h->p;
   SF_TRY(cudaMemcpyAsync(h->prompt, tokens, (size_t)B * P * 4, cudaMemcpyDefault, h->st));
   SF_TRY(cudaMemsetAsync(h->err, 0, 4, h->st));
+  if (h->tpkey) SF_TRY(cudaMemsetAsync(h->tpkey, 0, (size_t)p.n_amrows * 8, h->st));
   const int C = p.C_pf;
   int Cc = 0;
   for (int c0 = 0; c0 < P; c0 += C) {
@@ -1175,6 +1183,8 @@ sf_status specformer_draft_step(sf_handle* h, int32_t* draft, float* draft_logit
   if (!h) return SF_ERR_ARG;
   if (h->p.k == 0) return set_err(h, SF_ERR_UNSUPPORTED, "draft_len == 0 (AR mode) has no draft head");
   if (h->state != ST_READY) return set_err(h, SF_ERR_STATE, "draft_step needs prefill or accept_commit first");
+  if (draft_logits && (h->c.flags & SF_FLAG_NO_LOGITS))
+    return set_err(h, SF_ERR_STATE, "logits not kept (SF_FLAG_NO_LOGITS)");
   h->launches = 0;
   SF_TRY(do_draft(h));
   SF_TRY(copy_out(h, draft, h->draft, (size_t)h->B * h->p.k * 4));
@@ -1186,6 +1196,7 @@ sf_status specformer_draft_step(sf_handle* h, int32_t* draft, float* draft_logit
 sf_status specformer_verify_step(sf_handle* h, const int32_t* draft_in, int32_t* greedy, float* logits) {
   if (!h) return SF_ERR_ARG;
   const int k = h->p.k;
+  if (logits && (h->c.flags & SF_FLAG_NO_LOGITS)) return set_err(h, SF_ERR_STATE, "logits not kept (SF_FLAG_NO_LOGITS)");
   const bool ok_state = h->state == ST_DRAFTED || (h->state == ST_READY && (k == 0 || draft_in));
   if (!ok_state) return set_err(h, SF_ERR_STATE, "verify_step needs a draft (draft_step or draft_in)");
   if (h->host_len_hi + k + 1 > h->c.max_seq) {

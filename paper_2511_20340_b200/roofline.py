@@ -2,8 +2,9 @@
 
 Counted once per pass: every weight byte of the base model (verify) and of the SpecFormer head +
 shared LM head (draft), every KV byte once per (sequence, layer) -- the k+1 query rows share one
-KV stream -- and the fp32 logits once written and once read. Not counted: re-reads, padded MMA
-rows, split-K / split-KV partials, L2 hits.
+KV stream -- and the fp32 logits once written and once read (with SF_FLAG_NO_LOGITS: the fused
+argmax's 8-byte keys per row instead). Not counted: re-reads, padded MMA rows, split-K / split-KV
+partials, L2 hits.
 """
 from __future__ import annotations
 
@@ -33,13 +34,14 @@ def attention_kv_bytes(c, lens_verify, lens_ctx, k, elt=2):
     return per * (c.n_layers * sum(n + k + 1 for n in lens_verify) + sum(n + k + 1 for n in lens_ctx))
 
 
-def step_bytes(c, B, k, lens_verify, lens_ctx, elt=2):
+def step_bytes(c, B, k, lens_verify, lens_ctx, elt=2, logits=True):
     V, d = c.vocab, c.d_model
     w = (base_linear_params(c) + V * d) * elt          # verify: base + LM head
     w += (head_params(c, k) + V * d) * elt             # draft: head + LM head again
     kv = attention_kv_bytes(c, lens_verify, lens_ctx, k, elt)
-    logits = (B * (k + 1) + B * k) * V * 4 * 2
-    return w + kv + logits
+    rows = B * (k + 1) + B * k
+    out = rows * V * 4 * 2 if logits else rows * 8 * 2
+    return w + kv + out
 
 
 def step_flops(c, B, k, lens_verify):

@@ -317,6 +317,44 @@ def test_attention_schedules_bit_exact(cfg, monkeypatch):
         assert np.array_equal(s1["draft_logits"], s2["draft_logits"])
 
 
+# ------------------------------------------------------------------ fused LM-head argmax (NEXT-4)
+@pytest.mark.parametrize("cfg", [MID, GQA], ids=["mha128", "gqa4"])
+def test_fused_argmax_ties_and_no_logits(cfg):
+    """The bf16 LM head reduces packed (logit, id) keys in its epilogue (lane butterfly, warps and CTAs
+    via atomicMax) instead of a separate argmax pass. Greedy rule (P25; reading: lowest id on ties):
+    every greedy / draft token equals the lowest-id argmax of the GPU's own fp32 logits. Ties are
+    forced with duplicated LM-head rows (+u at ids 130 and 200, -u at 131 and 255: one 128-row tile,
+    different lanes and warps, so the two logits are bit-identical) of a norm that makes one pair the
+    maximum at most positions: the lower id must win every time. SF_FLAG_NO_LOGITS (logits not
+    stored) gives the same tokens, drafts and accept lengths, and refuses to return logits."""
+    w, prompts = setup(cfg, seed=9, jitter=0.1)
+    g = torch.Generator().manual_seed(11)
+    u = (0.5 * torch.randn(cfg.d_model, generator=g)).to(w["lm_head"].dtype)
+    lm = w["lm_head"].clone()
+    lm[130], lm[200], lm[131], lm[255] = u, u, -u, -u
+    w["lm_head"] = lm
+    res = run_gpu(cfg, w, prompts, 16, want_logits=True)
+    hot = 0
+    for s in res["steps"]:
+        for key_l, key_t in (("logits", "greedy"), ("draft_logits", "draft")):
+            L, tok = s[key_l], s[key_t]
+            assert np.array_equal(L[..., 130], L[..., 200]) and np.array_equal(L[..., 131], L[..., 255])
+            for b in range(L.shape[0]):
+                for i in range(L.shape[1]):
+                    assert tok[b][i] == O.argmax_lowest(L[b, i])
+                    assert tok[b][i] not in (200, 255)
+                    hot += tok[b][i] in (130, 131)
+    assert hot > 50
+    nl = run_gpu(cfg, w, prompts, 16, flags=N.SF_FLAG_NO_LOGITS)
+    assert nl["tokens"] == res["tokens"]
+    for s1, s2 in zip(res["steps"], nl["steps"]):
+        for key in ("draft", "greedy", "m"):
+            assert np.array_equal(s1[key], s2[key])
+    eng = nl["engine"]
+    with pytest.raises(N.SpecFormerError):
+        eng.draft_step(want_logits=True)
+
+
 # ------------------------------------------------------------------ tensor parallelism (SURVEY 8e)
 @pytest.mark.timeout(600)
 @pytest.mark.parametrize("tp", [2, 4])
