@@ -38,3 +38,13 @@ def test_step_flops_dominated_by_2TNK():
     lin = 2 * B * (k + 1) * (R.base_linear_params(c) + c.vocab * c.d_model)
     assert lin < f < 1.2 * lin  # 4.61 TF at 7B, B = 64
     assert f == pytest.approx(4.61e12, rel=3e-2)
+
+
+def test_step_bytes_without_logits():
+    """SF_FLAG_NO_LOGITS (fused LM-head argmax): the verify + draft rows' fp32 logits round trip is
+    replaced by one 8-byte key per row, written and read."""
+    c = get_config("7b")
+    B, k, lens = 16, 4, [700] * 16
+    rows = B * (k + 1) + B * k
+    full, fused = R.step_bytes(c, B, k, lens, lens), R.step_bytes(c, B, k, lens, lens, logits=False)
+    assert full - fused == rows * c.vocab * 4 * 2 - rows * 8 * 2
