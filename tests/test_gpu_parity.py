@@ -355,6 +355,55 @@ def test_fused_argmax_ties_and_no_logits(cfg):
         eng.draft_step(want_logits=True)
 
 
+def test_fused_argmax_nonfinite_flag():
+    """A NaN reaching the bf16 LM head's fused argmax raises the sticky SF_ERR_NONFINITE (SPEC S26),
+    as the separate argmax pass does in fp32 mode (test_state_machine_and_nonfinite)."""
+    w, prompts = setup(MID, seed=3)
+    w["lm_head"] = w["lm_head"].clone()
+    w["lm_head"][77, 5] = float("nan")
+    eng = make_engine(MID, w, MID.batch, 8)
+    eng.prefill(prompts.cuda())
+    with pytest.raises(N.SpecFormerError) as e:
+        eng.sync()
+    assert e.value.status == N.SF_ERR_NONFINITE
+
+
+@pytest.mark.timeout(900)
+def test_bench_configuration_matches_eager_path():
+    """bench.py's launch configuration -- 7B shape at full depth, B = 64, each decode step one CUDA
+    graph replay (specformer_decode_steps), SF_FLAG_NO_LOGITS -- emits the same tokens and accept
+    lengths, step by step, as the eager draft / verify / accept calls with the logits kept: the path
+    the oracle tests check (at full depth: test_full_depth_7b_*; across batch sizes: batch invariance)."""
+    from synth import make_weights
+    cfg = get_config("7b").replace(prompt_len=128)
+    B, n_steps, k = 64, 6, cfg.draft_len
+    w = make_weights(cfg, seed=0, device="cuda")
+    prompts = make_prompts(B, cfg.prompt_len, cfg.vocab, seed=2).cuda()
+    ms = max_seq_for(cfg, n_steps * (k + 1), k)
+    eager = Engine(EngineConfig.from_model(cfg, max_batch=B, max_seq=ms), w)
+    eager.prefill(prompts)
+    ems, accs = [], []
+    for _ in range(n_steps):
+        eager.draft_step(want_logits=True)
+        eager.verify_step(want_logits=True)
+        m, em, _ = eager.accept_commit()
+        eager.sync()
+        accs.append(m.cpu())
+        ems.append(em.cpu())
+    eager.close()
+    del eager
+    graph = Engine(EngineConfig.from_model(cfg, max_batch=B, max_seq=ms,
+                                           flags=N.SF_FLAG_CUDA_GRAPH | N.SF_FLAG_NO_LOGITS), w)
+    graph.prefill(prompts)
+    em_log = torch.zeros(n_steps, B, k + 1, dtype=torch.int32, device="cuda")
+    acc_log = torch.zeros(n_steps, B, dtype=torch.int32, device="cuda")
+    graph.decode_steps(n_steps, em_log, acc_log)
+    graph.sync()
+    assert torch.equal(acc_log.cpu(), torch.stack(accs).to(torch.int32))
+    assert torch.equal(em_log.cpu(), torch.stack(ems).to(torch.int32))
+    graph.close()
+
+
 # ------------------------------------------------------------------ tensor parallelism (SURVEY 8e)
 @pytest.mark.timeout(600)
 @pytest.mark.parametrize("tp", [2, 4])
