@@ -15,7 +15,7 @@ per-piece pins (residual identities, W_P = 0 => D = b_P, permutation equivarianc
 """
 from .model import (  # noqa: F401
     Weights, rms_norm, group_rms_norm, rope, attention_dense_masked, swiglu, argmax_lowest,
-    taps_index, KVCache, base_forward, context_layer, positional_ffn, draft_block, top2_margin,
+    taps_index, KVCache, decoder_layer, base_forward, context_layer, positional_ffn, draft_block, top2_margin,
     draft_logits, draft_tokens, accept, decode_greedy, sd_decode, replay, prefill,
 )
 from . import analytics  # noqa: F401

@@ -158,6 +158,15 @@ def _attn(W, prefix, x, pos, cache, layer, causal=True, slot_causal=False):
 
 
 # --------------------------------------------------------------------------- base model
+def decoder_layer(W, l, h, pos, cache):
+    """Base decoder layer l (0-based) on the residual stream h [T, d] at positions pos: the
+    pre-norm block of Eq.7 (P160-165), h += Attn(RMS(h)); h += SwiGLU(RMS(h)). Returns HS[l+1]."""
+    eps = W.cfg.rms_eps
+    p = f"layers.{l}."
+    h = h + _attn(W, p, rms_norm(h, W[p + "attn_norm"], eps), pos, cache, l)
+    return h + swiglu(rms_norm(h, W[p + "ffn_norm"], eps), W[p + "w_gate"], W[p + "w_up"], W[p + "w_down"])
+
+
 def base_forward(W, tokens, pos0, cache):
     """Base decoder forward over `tokens` at positions pos0.. (pre-norm blocks, Eq.7
     P160-165: h += Attn(RMS(h)); h += SwiGLU(RMS(h))). Returns (logits [T, V],
@@ -171,9 +180,7 @@ def base_forward(W, tokens, pos0, cache):
     h = W["embed"][tokens].copy()
     hs = [h.copy()]
     for l in range(L):
-        p = f"layers.{l}."
-        h = h + _attn(W, p, rms_norm(h, W[p + "attn_norm"], eps), pos, cache, l)
-        h = h + swiglu(rms_norm(h, W[p + "ffn_norm"], eps), W[p + "w_gate"], W[p + "w_up"], W[p + "w_down"])
+        h = decoder_layer(W, l, h, pos, cache)
         hs.append(h.copy())
     logits = rms_norm(h, W["final_norm"], eps) @ W["lm_head"].T
     taps = np.stack([hs[i] for i in taps_index(L)])
@@ -304,7 +311,7 @@ def sd_decode(W, prompt, n_tokens, draft_fn=None, record=False):
         cache.truncate(range(L), n + m + 1)
         i_d = context_layer(W, taps[:, : m + 1], n, cache)[m]
         if record:
-            steps.append(dict(n=n, draft=dr, greedy=greedy, m=m, logits=logits, draft_logits=dl))
+            steps.append(dict(n=n, draft=dr, greedy=greedy, m=m, logits=logits, draft_logits=dl, i_d=i_d))
         else:
             steps.append(dict(m=m))
         out += emitted
