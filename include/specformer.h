@@ -158,7 +158,11 @@ const char* specformer_build_info(void);
 sf_status sf_debug_set_block_table(sf_handle* h, const int32_t* table_host, int32_t B, int32_t n_pages_per_seq);
 /* Copy an internal buffer to dst (dev or host). what: 0 taps [4, B(k+1), d] f32 of the last
  * verify; 1 I_D rows used by the last draft [B, d] f32; 2 E (draft block output) [B, k, d] f32;
- * 3 seq_len [B] i32; 4 last_token [B] i32; 5 n_prev [B] i32 (length before the last commit). Returns bytes copied via *nbytes. */
+ * 3 seq_len [B] i32; 4 last_token [B] i32; 5 n_prev [B] i32 (length before the last commit);
+ * 6 hook taps of EVERY row of the last base forward (prefill: its last chunk, rows b-major) [4, rows, d]
+ * f32; 7 context-layer output I_D of every row of the last context pass [rows, d] f32; 8 prompt_len
+ * [B] i32. Returns bytes copied via *nbytes (6 / 7: query the size with a first call into a buffer of
+ * sf_workspace-sized capacity, or compute rows from the call sequence). */
 sf_status sf_debug_capture(sf_handle* h, int32_t what, void* dst, int64_t* nbytes);
 /* Forced-acceptance drafts: overwrite the internal draft with
  * cont[b, g + j] (j = 1..k, g = seq_len - prompt_len, cont = AR continuation with cont[b,0] = g0)

@@ -63,7 +63,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose and out:
             print(out)
     tmp = LIB + ".tmp"
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
+    # shared CUDA runtime: the library binds to the process's libcudart.so.12 (torch's, when torch is
+    # loaded first) instead of carrying a static copy of the whole runtime
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "shared", "-o", tmp, *objs,
+           "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     if NCCL:
         lib = os.path.join(NCCL, "lib")
         cmd += ["-L" + lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]

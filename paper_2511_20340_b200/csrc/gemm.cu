@@ -174,17 +174,6 @@ SF_DEV void umma_commit_2sm(uint64_t* bar, uint16_t mask) {
       "h"(mask)
       : "memory");
 }
-// 2-SM TMA multicast: the box lands at the same offset in every CTA of `mask`; each destination's
-// transaction bytes are credited to the barrier of ITS pair leader (peer bit cleared)
-SF_DEV void tma_load_2d_2sm_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint16_t mask,
-                               uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      ".L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "h"(mask), "r"(c0), "r"(c1), "l"(policy)
-      : "memory");
-}
-
 // MODE = the epilogue (EpiMode), a template parameter so each instantiation carries only its own
 // store path: the kernel's code is executed cold once per CTA in the final phase, and every
 // instruction-cache line it does not need is a fetch that competes with the weight stream.
@@ -195,9 +184,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
-  // CG = CTAs per cluster: 1; 2 = one CTA pair (cta_group::2 MMA, M = 256); 4 = two CTA pairs that
-  // share the activation tile through TMA multicast (each CTA loads a quarter of it)
-  constexpr bool kPair = CG >= 2;
+  // CG = CTAs per cluster: 1, or 2 = one CTA pair (cta_group::2 MMA, M = 256)
+  static_assert(CG == 1 || CG == 2, "CTA groups of 1 or 2");
+  constexpr bool kPair = CG == 2;
   const int a_rows = kPair ? p.NT / 2 : p.NT;  // activation rows of each sub-tile in this CTA's smem
   const int a_bytes = p.n_sub * a_rows * BK * 2;
   const int stage_bytes = BM * BK * 2 + a_bytes;
@@ -237,7 +226,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     prefetch_tmap(&tmA);
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);  // pair leader: one arrive_expect_tx covering both CTAs' bytes
-      mbar_init(&empty[s], CG == 4 ? 2 : 1);  // CG 4: a slot is refilled (multicast) once BOTH pairs consumed it
+      mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
@@ -326,19 +315,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
             // tiled weights viewed as a [blocks*128, 64] tensor: this CTA's 128-row tile of unit tile t
             tma_load_2d_2sm(st, &tmW, &full[s], 0, ((t * CG + (int)rank) * kb + k) * BM, kEvictFirst);
           }
-          if constexpr (CG == 4) {
-            // this CTA's pair-half of the activation (rows prank * a_rows ..) is also needed by the
-            // CTA at the same position in the other pair: each loads one half of it, multicast to both
-            const int hr = a_rows / 2, pr = (int)(rank >> 1);
-            const uint16_t mask = (uint16_t)((1u << prank) | (1u << (prank + 2)));
-            for (int j = 0; j < p.n_sub; ++j)
-              tma_load_2d_2sm_mc(st + BM * BK * 2 + j * a_rows * BK * 2 + pr * hr * BK * 2, &tmA, &full[s], k * BK,
-                                 j * p.NT + (int)prank * a_rows + pr * hr, mask, kEvictLast);
-          } else {
-            for (int j = 0; j < p.n_sub; ++j)
-              tma_load_2d_2sm(st + BM * BK * 2 + j * a_rows * BK * 2, &tmA, &full[s], k * BK,
-                              j * p.NT + (int)rank * a_rows, kEvictLast);
-          }
+          for (int j = 0; j < p.n_sub; ++j)
+            tma_load_2d_2sm(st + BM * BK * 2 + j * a_rows * BK * 2, &tmA, &full[s], k * BK,
+                            j * p.NT + (int)rank * a_rows, kEvictLast);
           // no arrival from the peer: its bytes complete_tx on the leader's barrier, which the leader
           // armed for both CTAs; they cannot land before that phase (the slot was released first)
         }
@@ -427,7 +406,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
             }
           if (++gcnt == p.cgrp) {  // frees slots s-cgrp+1..s (in both CTAs of a pair)
             if constexpr (CG == 1) umma_commit(&empty[s]);
-            else umma_commit_2sm(&empty[s], CG == 4 ? (uint16_t)0xF : (uint16_t)(3u << pbase));
+            else umma_commit_2sm(&empty[s], (uint16_t)(3u << pbase));
           }
         }
         __syncwarp();
@@ -970,8 +949,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------------ SIMT fp32 kernel
-// grid (ceil(Nout/32), ceil(T/32)), block (32, 8). Each output element reduces k = 0..K-1 in
-// order (batch-invariant). DUAL: SwiGLU over the 64-row interleaved gate/up layout.
+// grid (ceil(Nout/32), ceil(T/32)), block (32, 8). Each output element sums k in 32-wide blocks,
+// each block in k order, the block sums in k order (fixed for every T: batch-invariant). DUAL:
+// SwiGLU over the 64-row interleaved gate/up layout.
 template <bool DUAL>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict__ A, int lda,
                                                          const float* __restrict__ W, int T, int N, int K,
@@ -997,6 +977,9 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
       if (DUAL) Us[i][tx] = (o < Nout && kk < K) ? W[(size_t)(wrow(o) + 1) * K + kk] : 0.f;
     }
     __syncthreads();
+    // blocked k order: each 32-wide k block is summed on its own, then added to the running total
+    // (rounding error grows with 32 + K/32 terms instead of K; the order depends on K only)
+    float blk[4] = {0, 0, 0, 0}, blku[4] = {0, 0, 0, 0};
 #pragma unroll 8
     for (int c = 0; c < 32; ++c) {
       const float w = Ws[tx][c];
@@ -1004,9 +987,14 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float a = As[ty + 8 * i][c];
-        acc[i] = fmaf(a, w, acc[i]);
-        if (DUAL) accu[i] = fmaf(a, u, accu[i]);
+        blk[i] = fmaf(a, w, blk[i]);
+        if (DUAL) blku[i] = fmaf(a, u, blku[i]);
       }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      acc[i] += blk[i];
+      if (DUAL) accu[i] += blku[i];
     }
     __syncthreads();
   }
@@ -1048,8 +1036,7 @@ static bool make_map(CUtensorMap* m, const void* ptr, int rows, int K, int ld_el
                             box, CU_TENSOR_MAP_SWIZZLE_128B) == CUDA_SUCCESS;
 }
 
-// MMA N tiling of T token columns (granularity g: 16, or 32 for the multicast pairs whose quarter
-// activation boxes must start on 8-row swizzle atoms)
+// MMA N tiling of T token columns (granularity g = 16)
 static void tc_shape(int T, int* NT, int* n_sub, int g = 16) {
   const int Tp = std::max(g, (T + g - 1) / g * g);
   if (Tp <= 256) {
@@ -1171,13 +1158,11 @@ static int max_groups(int cg) {
 
 // CTA-pair mode halves each SM's share of the activation tile (the MMA reads the B operand from
 // both CTAs' shared memory), the L2->SM traffic that bounds the skinny GEMM at large T.
-// CG 4 (two pairs sharing the activation tile by 2-SM TMA multicast) would quarter it again, but
-// it deadlocks on the first launch in this build (not yet understood) and a B200 co-schedules only
-// 33 4-CTA clusters (132 SMs): experimental, SF_GEMM_CG=4 only.
+// (A 4-CTA variant multicasting the activation between two pairs deadlocked in round 1 and was
+// removed.) SF_GEMM_CG=1 forces single-CTA groups (tests / experiments).
 static int gemm_cg(int N, int K) {
   (void)K;
   static const int env = getenv("SF_GEMM_CG") ? atoi(getenv("SF_GEMM_CG")) : 2;
-  if (env >= 4 && N % (4 * BM) == 0) return 4;
   if (env >= 2 && N % (2 * BM) == 0) return 2;
   return 1;
 }
@@ -1194,7 +1179,6 @@ static SkKernel sk_kernel_for(int cg, int mode) {
     case EPI_QKV_ROPE: return gemm_sk_kernel<CGV, EPI_QKV_ROPE>;     \
     default: return gemm_sk_kernel<CGV, EPI_PARTIAL>;           \
   }
-  if (cg == 4) SF_SK(4);
   if (cg == 2) SF_SK(2);
   SF_SK(1);
 #undef SF_SK
@@ -1215,7 +1199,7 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
                              const ChainB* chain = nullptr) {
   static bool attr = false;
   if (!attr) {
-    for (int cg = 1; cg <= 4; cg *= 2)
+    for (int cg = 1; cg <= 2; cg *= 2)
       for (int md = 0; md <= EPI_QKV_ROPE; ++md)
         cudaFuncSetAttribute(sk_kernel_for(cg, md), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(gemm_sk_kernel<2, EPI_SWIGLU_ACT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1228,7 +1212,7 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   p.N = N;
   p.K = K;
   p.Tp = (T + 31) / 32 * 32;
-  tc_shape(T, &p.NT, &p.n_sub, CG == 4 ? 32 : 16);
+  tc_shape(T, &p.NT, &p.n_sub);
   p.kb_total = K / BK;
   p.n_tiles = N / (BM * CG);
   const long long U = (long long)p.n_tiles * p.kb_total;

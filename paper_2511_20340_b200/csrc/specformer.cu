@@ -290,11 +290,13 @@ struct sf_handle {
   int state = ST_INIT;
   bool ctx_pending = false;
   bool final_xn_ready = false;
+  int fwd_rows = 0, ctx_rows = 0;  // rows of the last base forward / context-layer pass (debug capture)
   int64_t launches = 0;
   int64_t host_len_hi = 0;  // host upper bound of max(seq_len)
   std::string err_msg;
   // graph
   cudaGraphExec_t gexec = nullptr;
+  int g_B = 0;  // batch size the cached step graph was captured at (its grids, T = B(k+1), accept B)
   int64_t graph_launches = 0;
   int *g_acc_log = nullptr, *g_em_log = nullptr;
   // per-kernel-class profiling (eager launches only; bench roofline)
@@ -482,17 +484,33 @@ static bool gemm_resid_norm(sf_handle* h, cudaError_t* err, const void* A, int l
                                                           gamma ? (__nv_bfloat16*)h->xn : nullptr, h->st));
     return true;
   }
-  if (!h->bf || T > 512) return false;
-  if (!resid_norm_supported(h->p.d, T, N, K)) return false;
+  if (!h->bf) return false;
+  // blocks of more than 512 rows (13B k = 8 at B = 64; prefill chunks) run as balanced row chunks of
+  // <= 512 (the TMEM accumulator width), each GEMM publishing its partials for its own consumer: every
+  // row gets the same additions in the same order at every T (batch invariance, reading C23)
+  const int n_chunks = (T + 511) / 512;
+  const int chunk = n_chunks == 1 ? T : std::min(512, ((T + n_chunks - 1) / n_chunks + 15) / 16 * 16);
+  if (!resid_norm_supported(h->p.d, chunk, N, K)) return false;
   PartialGeom g;
-  if (!gemm_partial_geom(T, N, K, &g)) return false;
-  GemmEpi e;
-  e.mode = EPI_PARTIAL;
-  if ((*err = gemm(h, A, lda, W, T, N, K, e)) != cudaSuccess) return true;
-  ProfScope ps(h, 2, (double)T * N * 4.0 * 3);
-  h->launches++;
-  *err = dbg_sync(h, "resid_norm", launch_resid_norm(h->gpart, &g, T, rep, h->p.d, resid, nullptr, bias, out, tap,
-                                                     gamma, h->c.rms_eps, gamma ? (__nv_bfloat16*)h->xn : nullptr, h->st));
+  if (!gemm_partial_geom(chunk, N, K, &g)) return false;
+  const int64_t rd = (int64_t)rep * h->p.d;  // elements of one GEMM row in the [T rep, d] views
+  for (int t0 = 0; t0 < T; t0 += chunk) {
+    const int Tc = std::min(chunk, T - t0);
+    if (!gemm_partial_geom(Tc, N, K, &g)) {
+      *err = cudaErrorInvalidValue;
+      return true;
+    }
+    GemmEpi e;
+    e.mode = EPI_PARTIAL;
+    if ((*err = gemm(h, (const char*)A + (size_t)t0 * lda * h->p.act, lda, W, Tc, N, K, e)) != cudaSuccess) return true;
+    ProfScope ps(h, 2, (double)Tc * N * 4.0 * 3);
+    h->launches++;
+    *err = dbg_sync(h, "resid_norm",
+                    launch_resid_norm(h->gpart, &g, Tc, rep, h->p.d, resid ? resid + t0 * rd : nullptr, nullptr, bias,
+                                      out + t0 * rd, tap ? tap + t0 * rd : nullptr, gamma, h->c.rms_eps,
+                                      gamma ? (__nv_bfloat16*)h->xn + t0 * rd : nullptr, h->st));
+    if (*err != cudaSuccess) return true;
+  }
   return true;
 }
 
@@ -645,6 +663,7 @@ static cudaError_t base_forward(sf_handle* h, int T, int q_len, const int* pos0,
   taps_layers(p.L, tl);
   cudaError_t e = launch_embed(h->bf, h->tok_rows, h->embed, T, p.d, p.V_full, h->resid, h->taps, h->st);
   h->launches++;
+  h->fwd_rows = T;
   if (e != cudaSuccess) return e;
   for (int g = 1; g < 4; ++g)
     if (tl[g] == 0) cudaMemcpyAsync(h->taps + g * tstride, h->taps, (size_t)T * p.d * 4, cudaMemcpyDeviceToDevice, h->st);
@@ -696,6 +715,7 @@ static cudaError_t base_forward(sf_handle* h, int T, int q_len, const int* pos0,
 static cudaError_t ctx_forward(sf_handle* h, int T, int q_len, const int* pos0, int max_key) {
   const Plan& p = h->p;
   cudaError_t e;
+  h->ctx_rows = T;
   if ((e = launch_group_rms(h->bf, h->taps, (int64_t)p.R * p.d, h->group_scale, h->c.rms_eps, T, p.d, h->xn, h->st)))
     return e;
   h->launches++;
@@ -1153,6 +1173,11 @@ sf_status specformer_prefill(sf_handle* h, const int32_t* tokens, int32_t B, int
   if (P < 1) return set_err(h, SF_ERR_SHAPE, "empty prompt");
   if (P + h->p.k + 1 > h->c.max_seq) return set_err(h, SF_ERR_CAPACITY, "prompt exceeds max_seq");
   h->launches = 0;
+  if (h->gexec && h->g_B != B) {  // the cached step graph was captured for another batch size
+    SF_TRY(cudaStreamSynchronize(h->st));
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
   h->B = B;
   const Plan& p = h->p;
   SF_TRY(cudaMemcpyAsync(h->prompt, tokens, (size_t)B * P * 4, cudaMemcpyDefault, h->st));
@@ -1319,7 +1344,7 @@ sf_status specformer_decode_steps(sf_handle* h, int32_t n_steps, int32_t* emitte
     h->ctx_pending = k > 0;
   } else if (use_graph && done < n_steps) {
     // the graph depends on the log pointers only (the log capacity is read on the device)
-    if (h->gexec && (h->g_acc_log != accept_log || h->g_em_log != emitted_log)) {
+    if (h->gexec && (h->g_acc_log != accept_log || h->g_em_log != emitted_log || h->g_B != h->B)) {
       cudaGraphExecDestroy(h->gexec);
       h->gexec = nullptr;
     }
@@ -1339,6 +1364,7 @@ sf_status specformer_decode_steps(sf_handle* h, int32_t n_steps, int32_t* emitte
       h->launches = before;
       h->g_acc_log = accept_log;
       h->g_em_log = emitted_log;
+      h->g_B = h->B;
     }
     for (int s = done; s < n_steps; ++s) {
       SF_TRY(cudaGraphLaunch(h->gexec, h->st));
@@ -1359,6 +1385,14 @@ sf_status specformer_sync(sf_handle* h) {
   int err = 0;
   SF_TRY(cudaMemcpy(&err, h->err, 4, cudaMemcpyDeviceToHost));
   if (err & 1) return set_err(h, SF_ERR_NONFINITE, "non-finite logits");
+#ifdef SF_WITH_NCCL
+  if (h->nccl_comm) {  // asynchronous communicator errors (a peer failed, a network / NVLink error)
+    ncclResult_t ar = ncclSuccess;
+    const ncclResult_t r = ncclCommGetAsyncError((ncclComm_t)h->nccl_comm, &ar);
+    if (r != ncclSuccess || ar != ncclSuccess)
+      return set_err(h, SF_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(r != ncclSuccess ? r : ar));
+  }
+#endif
   return SF_OK;
 }
 
@@ -1473,6 +1507,16 @@ sf_status sf_debug_capture(sf_handle* h, int32_t what, void* dst, int64_t* nbyte
     case 3: src = h->seq_len; bytes = (size_t)B * 4; break;
     case 4: src = h->last_token; bytes = (size_t)B * 4; break;
     case 5: src = h->n_prev; bytes = (size_t)B * 4; break;
+    case 6: {  // taps of every row of the last base forward [4, fwd_rows, d]
+      const int R = h->fwd_rows;
+      for (int g = 0; g < 4; ++g)
+        SF_TRY(cudaMemcpyAsync((char*)dst + (size_t)g * R * p.d * 4, h->taps + (size_t)g * p.R * p.d,
+                               (size_t)R * p.d * 4, cudaMemcpyDefault, h->st));
+      bytes = (size_t)4 * R * p.d * 4;
+      break;
+    }
+    case 7: src = h->ctx; bytes = (size_t)h->ctx_rows * p.d * 4; break;
+    case 8: src = h->prompt_len; bytes = (size_t)B * 4; break;
     default: return set_err(h, SF_ERR_ARG, "unknown capture id");
   }
   if (src) SF_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->st));

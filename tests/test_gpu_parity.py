@@ -525,12 +525,11 @@ def test_full_depth_7b_bf16():
 
 
 def test_full_depth_7b_fp32():
-    """Reading C21 (iii)/(iv), fp32 mode at full depth (7B shape, 32 layers; SIMT GEMMs, split-KV
-    attention): logits and draft logits elementwise within 3e-4 abs + 1e-5 rel of the fp64 oracle
-    (measured 1.45e-4 max abs, rel-L2 2.5e-5: the batch-invariant SIMT GEMM accumulates each dot product
-    sequentially in k, K up to 11008, where SURVEY 8c's 5.5e-5 came from a blocked fp32 reference; the
-    bound is 2x the measurement), greedy and draft tokens bit-exact wherever the oracle margin exceeds
-    1e-4 (fp32-noise ties below that are reported), accept lengths exact."""
+    """Reading C21 (iii)/(iv), fp32 mode at full depth (7B shape, 32 layers; SIMT GEMMs with a fixed
+    blocked k order, split-KV attention): logits and draft logits elementwise within 1e-4 abs + 1e-5 rel
+    of the fp64 oracle (SURVEY 8c C21 iii: an ideal blocked fp32 pipeline gives 5.5e-5 max abs), greedy
+    and draft tokens bit-exact wherever the oracle margin exceeds 1e-4 (fp32-noise ties below that are
+    reported), accept lengths exact."""
     cfg = get_config("7b").replace(dtype="fp32", batch=1, prompt_len=32, gen_len=6)
     w, prompts = setup(cfg, seed=12)  # unit norm scales, as in the SURVEY 8c ideal-pipeline figure
     res = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True)
@@ -539,7 +538,7 @@ def test_full_depth_7b_fp32():
     for s, r in zip(res["steps"], rep):
         for gl, ol in ((s["logits"][0], r["logits"]), (s["draft_logits"][0], r["draft_logits"])):
             err = np.abs(gl.astype(np.float64) - ol)
-            assert np.all(err <= 3e-4 + 1e-5 * np.abs(ol)), f"{float(err.max()):.3e}"
+            assert np.all(err <= 1e-4 + 1e-5 * np.abs(ol)), f"{float(err.max()):.3e}"
         for i in range(cfg.draft_len + 1):
             if s["greedy"][0][i] != r["greedy"][i]:
                 assert O.top2_margin(r["logits"][i]) < 1e-4
