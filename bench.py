@@ -54,9 +54,19 @@ class ClockSampler:
         except Exception:
             self.max_mhz = None
         self._stop = threading.Event()
+        self.active = True  # start() / stop() restrict the samples to the timed windows
+
+    def start(self):
+        self.active = True
+
+    def stop(self):
+        self.active = False
 
     def _run(self):
         while not self._stop.is_set():
+            if not self.active:
+                time.sleep(0.002)
+                continue
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
@@ -68,6 +78,7 @@ class ClockSampler:
             time.sleep(0.01)
 
     def __enter__(self):
+        self.active = False
         if self.ok:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
@@ -86,63 +97,90 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- oracle leg
-def oracle_sample(cfg, n_steps=2, prompt_len=32):
-    """Time the fp64 oracle (as it stands) on a bounded sample of the workload: ONE sequence at the
-    config's full width with the base truncated to L = 1 and L = 2 layers (same SpecFormer head),
-    prompt `prompt_len`. For each depth, oracle.sd_decode runs twice -- 1 + s1 and 1 + s1 + s2
-    tokens -- and the difference of the two wall times divided by the difference of their step
-    counts is the per-step time (the prefill cancels). Full depth is extrapolated linearly in L:
-    t(L) = t(1) + (L - 1) (t(2) - t(1)). The oracle computes sequences one by one, so the box-level
-    tokens/s = tokens per step per sequence / t(L_full)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_sample(cfg, n_steps=2, prompt_len=None, threads=None):
+    """Time the fp64 oracle (as it stands, never tuned) on a bounded sample of the workload: ONE
+    sequence at the config's full width and prompt length (512 for the 7B shape) with the base
+    truncated to L = 1 and L = 2 layers (the SpecFormer head unchanged). For each depth,
+    oracle.sd_decode runs the prefill and n_steps decode steps; the mean wall time of those steps
+    (oracle step_times hook) is the measured per-step time at that depth. Full depth is an
+    EXTRAPOLATION, linear in L: t(L) = t(1) + (L - 1) (t(2) - t(1)). The
+    oracle computes sequences one at a time, so box tokens/s = tokens per step / t(L_full).
+    `threads`: BLAS threads (None = every core of the affinity mask; 1 = the single-thread figure)."""
     import oracle as O
     from synth import make_prompts, make_weights
 
+    P = cfg.prompt_len if prompt_len is None else prompt_len
     c2 = cfg.replace(n_layers=2)
     w = make_weights(c2, seed=0, device="cpu")
-    prompt = make_prompts(1, prompt_len, cfg.vocab)[0].tolist()
-    times, toks = {}, {}
-    s1, s2 = 1, n_steps
-    for L in (1, 2):
-        W = O.Weights(cfg.replace(n_layers=L), w)
-        O.sd_decode(W, prompt, 2)  # warm the fp64 weight cache (upcast) outside the timing
-        t0 = time.perf_counter()
-        _, st_a = O.sd_decode(W, prompt, 1 + s1)
-        t1 = time.perf_counter()
-        _, st_b = O.sd_decode(W, prompt, 1 + s1 + s2)
-        t2 = time.perf_counter()
-        dsteps = max(1, len(st_b) - len(st_a))
-        times[L] = max(1e-6, ((t2 - t1) - (t1 - t0)) / dsteps)
-        toks[L] = sum(s["m"] + 1 for s in st_b) / max(1, len(st_b))
-    t_full = times[1] + (cfg.n_layers - 1) * max(0.0, times[2] - times[1])
+    prompt = make_prompts(1, P, cfg.vocab)[0].tolist()
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    nthr = cores if threads is None else threads
+    try:
+        from threadpoolctl import threadpool_limits
+        limit = threadpool_limits(limits=nthr)
+    except Exception:  # pragma: no cover - threadpoolctl is in the image
+        limit = None
+    times, toks, steps_run, secs_run = {}, {}, 0, 0.0
+    try:
+        for L in (1, 2):
+            W = O.Weights(cfg.replace(n_layers=L), w)
+            O.sd_decode(W, prompt[:8], 2)  # warm the fp64 weight cache (upcast) outside the timing
+            st_times = []
+            _, st = O.sd_decode(W, prompt, 1 + n_steps, step_times=st_times)  # prefill, then n_steps steps
+            times[L] = sum(st_times) / len(st_times)
+            toks[L] = sum(s_["m"] + 1 for s_ in st) / max(1, len(st))
+            steps_run += len(st_times)
+            secs_run += sum(st_times)
+    finally:
+        if limit is not None and hasattr(limit, "unregister"):
+            limit.unregister()
+    t_full = times[1] + (cfg.n_layers - 1) * max(0.0, times[2] - times[1])
     a = toks[2]
-    return {"value": a / t_full, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-            "sample": f"1 sequence, width {cfg.d_model}, base depth 1 and 2 of {cfg.n_layers} layers "
-                      f"(linear extrapolation in L), prompt {prompt_len}, per-step time from the difference "
-                      f"of {1 + s1} vs {1 + s1 + s2} generated tokens; t_step(L=1)={times[1]:.3f}s "
-                      f"t_step(L=2)={times[2]:.3f}s -> t_step(L={cfg.n_layers})={t_full:.2f}s per sequence; "
-                      f"sequences are processed one at a time (numpy fp64, BLAS threads = {cores})",
-            "seconds_per_step_per_sequence": t_full}
+    return {"value": a / t_full, "unit": "tokens/s", "cores": nthr, "kind": "oracle", "cpu_model": cpu_model(),
+            "extrapolated": True,
+            "sample": f"1 sequence, width {cfg.d_model}, prompt {P}, base depth 1 and 2 of {cfg.n_layers} layers; "
+                      f"measured per-step time t_step(L=1)={times[1]:.3f}s t_step(L=2)={times[2]:.3f}s "
+                      f"(mean of {n_steps} decode steps after the untimed prefill), full depth EXTRAPOLATED "
+                      f"linearly in L: t_step(L={cfg.n_layers})={t_full:.2f}s per sequence; sequences one at a "
+                      f"time (numpy fp64, BLAS threads = {nthr}, {cpu_model()})",
+            "seconds_per_step_per_sequence": t_full, "measured_steps": steps_run,
+            "measured_ms_per_step": 1e3 * secs_run / max(1, steps_run),
+            "measured_s_per_step_depth": {"1": times[1], "2": times[2]}}
 
 
 def run_reference(args, cfg):
+    """--impl reference: the fp64 oracle as it stands on the host cores, rank 0 only.
+    ms_per_step is the time of the oracle steps that actually ran (depth-1 and depth-2 samples of one
+    sequence); value is the labelled full-depth extrapolation in tokens/s."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    for _ in range(args.warmup):
-        pass  # the oracle has no warm-up state; warm-up steps are part of each sample below
     t0 = time.perf_counter()
-    cb = oracle_sample(cfg, n_steps=max(2, min(args.steps, 4)))
+    cb = oracle_sample(cfg, n_steps=max(2, min(args.steps, 3)))
+    cb1 = oracle_sample(cfg, n_steps=2, threads=1)  # the single-thread figure
     wall = time.perf_counter() - t0
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * cb["seconds_per_step_per_sequence"] * args.batch,
+            "n_gpus": args.gpus, "steps": cb["measured_steps"], "warmup": args.warmup,
+            "ms_per_step": cb["measured_ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded N(0,0.02) weights, uniform-random prompts)",
             "config": {"workload": f"{cfg.name}-shaped SpecFormer decode step, batch {args.batch}/GPU, k {cfg.draft_len}",
                        "model": cfg.name, "batch_per_gpu": args.batch, "draft_len": cfg.draft_len,
                        "prompt_len": cfg.prompt_len, "l2": "inputs larger than L2"},
+            "note": "steps / ms_per_step: the oracle steps actually run (one sequence, base depth 1 and 2); value: "
+                    "full-depth tokens/s extrapolated linearly in depth (cpu_baseline.sample)",
             "cpu_baseline": cb,
+            "cpu_baseline_1thread": cb1,
             "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": wall}
     print(json.dumps(line), flush=True)
@@ -209,29 +247,61 @@ def run_ours(args, cfg):
     else:
         prompts = dp.shard_rows(make_prompts(B * world, P, cfg.vocab), rank, world)  # weak scaling
 
-    eng.prefill(prompts.cuda())
-    acc_log = torch.zeros(max(K, W), B, dtype=torch.int32, device="cuda")
-    eng.decode_steps(W, None, acc_log)  # warm-up; also captures the step graph the timed window replays
-    eng.sync()
-    before = eng.capture(3, (B,), torch.int32).cpu()
-    prev_before = eng.capture(5, (B,), torch.int32).cpu()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    n_win = max(1, args.windows)
+
+    def timed_windows(Bs, prompts_s, clk=None):
+        """n_win windows, each: prefill (untimed) + W warm-up steps + K timed steps of the captured step
+        graph between CUDA events on the engine stream (barrier + sync on both sides); returns the window
+        with the median time and every window's time."""
+        wins = []
+        acc = torch.zeros(max(K, W), Bs, dtype=torch.int32, device="cuda")
+        for _ in range(n_win):
+            eng.prefill(prompts_s.cuda())
+            eng.decode_steps(W, None, acc)  # warm-up; (re)captures the step graph the window replays
+            eng.sync()
+            b0 = eng.capture(3, (Bs,), torch.int32).cpu()
+            p0 = eng.capture(5, (Bs,), torch.int32).cpu()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            if clk is not None:
+                clk.start()
+            torch.cuda.cudart().cudaProfilerStart()  # ncu --profile-from-start off: the timed windows only
+            e0.record(eng.stream)
+            eng.decode_steps(K, None, acc)
+            e1.record(eng.stream)
+            torch.cuda.synchronize()
+            torch.cuda.cudart().cudaProfilerStop()
+            if clk is not None:
+                clk.stop()
+            if world > 1:
+                dist.barrier()
+            eng.sync()
+            wms = e0.elapsed_time(e1)
+            a1 = eng.capture(3, (Bs,), torch.int32).cpu()
+            wins.append({"ms": wms, "before": b0, "prev_before": p0, "after": a1, "acc": acc.cpu().clone(),
+                         "launches": eng.kernel_launches()})
+        order = sorted(range(n_win), key=lambda i: wins[i]["ms"])
+        med = dict(wins[order[n_win // 2]])
+        med["all_ms"] = [w_["ms"] for w_ in wins]
+        return med
+
+    def window_roofline(win, Bs):
+        lens_t, prev_t, accs_t = win["before"].tolist(), win["prev_before"].tolist(), win["acc"].tolist()
+        sb_ = 0.0
+        for s_ in range(K):
+            sb_ += roofline.step_bytes(cfg, Bs, k, lens_t, prev_t, logits=not no_logits)
+            prev_t = list(lens_t)
+            lens_t = [n + m + 1 for n, m in zip(lens_t, accs_t[s_])]
+        return sb_ / tp
+
     with ClockSampler(local) as clk:
-        torch.cuda.cudart().cudaProfilerStart()  # ncu --profile-from-start off: the timed window only
-        e0.record(eng.stream)
-        eng.decode_steps(K, None, acc_log)
-        e1.record(eng.stream)
-        torch.cuda.synchronize()
-        torch.cuda.cudart().cudaProfilerStop()
-    if world > 1:
-        dist.barrier()
-    eng.sync()
-    ms = e0.elapsed_time(e1)
-    launches = eng.kernel_launches()
-    after = eng.capture(3, (B,), torch.int32).cpu()
+        main = timed_windows(B, prompts, clk)
+    ms = main["ms"]
+    launches = main["launches"]
+    before, prev_before, after = main["before"], main["prev_before"], main["after"]
+    acc_log = main["acc"].cuda()
     tokens = int((after - before).sum())
     ms_max, tokens_total = dp.reduce_timing(ms, float(tokens), device="cuda")
     tokens_total /= tp  # tensor parallelism: every rank emits the same tokens
@@ -240,31 +310,127 @@ def run_ours(args, cfg):
     a_meas = tokens / (K * B)
 
     # ---------------- whole-step roofline over the timed (graph) region, lengths from the accept log
-    lens_t = before.tolist()
-    accs_t = acc_log.cpu().tolist()
-    sb = 0.0
-    prev_t = prev_before.tolist()
-    for s in range(K):
-        sb += roofline.step_bytes(cfg, B, k, lens_t, prev_t, logits=not no_logits)
-        prev_t = list(lens_t)
-        lens_t = [n + m + 1 for n, m in zip(lens_t, accs_t[s])]
-    sb /= tp  # tensor parallelism: each GPU streams its 1/tp of the weights and of the KV heads
+    sb = window_roofline(main, B)  # (tensor parallelism: each GPU streams 1/tp of the weights / KV heads)
     step_gbs = sb / (ms / 1e3) / 1e9
 
-    def replay_lengths(lens0, prev0, accs):
+    def replay_lengths(lens0, prev0, accs, Bs):
         """algorithmic KV bytes / step bytes / step flops of the steps whose accept rows are accs"""
         lens, prevs, kv, by, fl = list(lens0), list(prev0), 0.0, 0.0, 0.0
         for a in accs:
             kv += roofline.attention_kv_bytes(cfg, lens, prevs, k)
-            by += roofline.step_bytes(cfg, B, k, lens, prevs, logits=not no_logits)
-            fl += roofline.step_flops(cfg, B, k, lens)
+            by += roofline.step_bytes(cfg, Bs, k, lens, prevs, logits=not no_logits)
+            fl += roofline.step_flops(cfg, Bs, k, lens)
             prevs = list(lens)
             lens = [n + m + 1 for n, m in zip(lens, a)]
         return kv, by, fl
 
-    # ---------------- kernel timeline: Kt replays of the timed step graph with the per-CTA
-    # %globaltimer probes switched on; the step's critical path is attributed to kernel classes
-    hbm, tf_burst, tf_sust, peak_src = peaks()
+    hbm, tf_burst, tf_sust, peak_src0 = peaks()
+    d_, F_, V_ = cfg.d_model, cfg.d_ff, cfg.vocab
+    qkv_ = (cfg.n_heads + 2 * cfg.n_kv_heads) * cfg.head_dim
+    ao_ = cfg.n_heads * cfg.head_dim
+
+    def gemm_flops(Bs):
+        """GEMM FLOPs of one step (2 T N K summed over the step's contractions)"""
+        Tv, Td = Bs * (k + 1), Bs * k
+        per_layer = qkv_ * d_ + d_ * ao_ + 2 * F_ * d_ + d_ * F_
+        return 2.0 * (Tv * (cfg.n_layers * per_layer + V_ * d_) + Tv * (4 * d_ * d_ + qkv_ * d_ + d_ * ao_)
+                      + Bs * k * d_ * d_ + Td * (qkv_ * d_ + d_ * ao_ + 3 * F_ * d_ + V_ * d_)) / tp
+
+    def event_profile(Bs):
+        """Kp steps of the step graph re-captured with a CUDA event-record node around every launch (on
+        the engine stream: the launches' own stream), replayed one step at a time; per kernel class:
+        time, launches, algorithmic bytes (GEMM: host-known weights + activations + outputs; attention:
+        KV bytes from the accept log). The record nodes serialise the launches (no PDL overlap), so these
+        per-launch times are conservative. Also picks the dominant class and its roofline."""
+        lens0 = eng.capture(3, (Bs,), torch.int32).cpu().tolist()
+        prev0 = eng.capture(5, (Bs,), torch.int32).cpu().tolist()  # context layer runs at n_prev
+        acc_p = torch.zeros(Kp, Bs, dtype=torch.int32, device="cuda")
+        eng.profile(True)
+        ep0, ep1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ep0.record(eng.stream)
+        eng.decode_steps(Kp, None, acc_p)
+        ep1.record(eng.stream)
+        eng.sync()
+        tot = ep0.elapsed_time(ep1)
+        cls = {c: eng.profile_read(c) for c in range(4)}
+        eng.profile(False)
+        attn_bytes, _, step_flops_tot = replay_lengths(lens0, prev0, acc_p.cpu().tolist(), Bs)
+        attn_bytes /= tp
+        gemm_ms, gemm_n, gemm_bytes = cls[0]
+        attn_ms, attn_n, _ = cls[1]
+        gf = gemm_flops(Bs)
+        classes = {name: {"ms_total": cls[c][0], "launches": cls[c][1], "share_of_profiled_step":
+                          cls[c][0] / max(1e-9, tot)}
+                   for c, name in enumerate(["gemm", "attention", "norm", "argmax"])}
+        g_gbs = gemm_bytes / max(1e-12, gemm_ms / 1e3) / 1e9
+        g_tfs = gf * Kp / max(1e-12, gemm_ms / 1e3) / 1e12
+        a_gbs = attn_bytes / max(1e-12, attn_ms / 1e3) / 1e9
+        g_bound_tc = gf / (tf_sust * 1e12) > (gemm_bytes / Kp) / (hbm * 1e9)
+        classes["gemm"].update(achieved_gbs=g_gbs, achieved_tflops=g_tfs, bound="tensor" if g_bound_tc else "hbm",
+                               frac=(g_tfs / tf_sust) if g_bound_tc else (g_gbs / hbm),
+                               bytes_per_step=gemm_bytes / Kp, flops_per_step=gf)
+        classes["attention"].update(achieved_gbs=a_gbs, frac=a_gbs / hbm, bytes_per_step=attn_bytes / Kp)
+        dominant = "gemm" if gemm_ms >= attn_ms else "attention"
+        n_dom = (gemm_n if dominant == "gemm" else attn_n) / max(1, Kp)
+        dom_ms = (gemm_ms if dominant == "gemm" else attn_ms) / max(1, Kp) / max(1e-9, n_dom)
+        if dominant == "gemm" and g_bound_tc:
+            bound, unit, peak_v, units = "tensor", "TFLOP/s", tf_sust, gf / max(1e-9, n_dom)
+            psrc = peak_src0 + " (bf16_tflops_sustained: kernel timed inside the step)"
+            achieved = units / (dom_ms / 1e3) / 1e12
+        else:
+            bound, unit, peak_v, psrc = "hbm", "GB/s", hbm, peak_src0 + " (hbm_gbs)"
+            units = (gemm_bytes if dominant == "gemm" else attn_bytes) / max(1, Kp) / max(1e-9, n_dom)
+            achieved = units / (dom_ms / 1e3) / 1e9
+        return {"classes": classes, "profiled_steps": Kp, "profiled_ms_total": tot, "dominant": dominant,
+                "bound": bound, "unit": unit, "peak": peak_v, "peak_source": psrc, "achieved": achieved,
+                "frac": achieved / peak_v, "units_per_launch": units, "ms_per_launch": dom_ms,
+                "launches_per_step": n_dom, "step_flops": step_flops_tot / max(1, Kp)}
+
+    def e2e_run(Bs, prompts_s, n_steps):
+        """One generation through the public C ABI: prompt H2D from pinned host memory, prefill, then per
+        step one specformer_decode_steps(1) call (the captured step graph) followed by the D2H read of that
+        step's accept lengths and emitted tokens into pinned host buffers; all inside the events."""
+        lib = eng.lib
+        host_prompts = prompts_s.clone().pin_memory()
+        g_host = torch.empty(Bs, dtype=torch.int32).pin_memory()
+        m_host = torch.empty(n_steps, Bs, dtype=torch.int32).pin_memory()
+        em_host = torch.empty(n_steps, Bs, k + 1, dtype=torch.int32).pin_memory()
+        em_dev = torch.empty(1, Bs, k + 1, dtype=torch.int32, device="cuda")
+        m_dev = torch.empty(1, Bs, dtype=torch.int32, device="cuda")
+        p = lambda t: C.c_void_p(t.data_ptr())
+        st = lib.specformer_prefill(eng.h, p(host_prompts), Bs, P, p(g_host))  # warm-up: captures the step graph
+        for _ in range(2):
+            st |= lib.specformer_decode_steps(eng.h, 1, p(em_dev), p(m_dev))
+        eng.sync()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(eng.stream)
+        st |= lib.specformer_prefill(eng.h, p(host_prompts), Bs, P, p(g_host))
+        with torch.cuda.stream(eng.stream):  # the D2H copies run on the engine stream, after each step
+            for s_ in range(n_steps):
+                st |= lib.specformer_decode_steps(eng.h, 1, p(em_dev), p(m_dev))
+                em_host[s_].copy_(em_dev[0], non_blocking=True)
+                m_host[s_].copy_(m_dev[0], non_blocking=True)
+        x1.record(eng.stream)
+        eng.sync()
+        if st != 0:
+            raise RuntimeError("e2e C-ABI call failed")
+        e_ms = x0.elapsed_time(x1)
+        e_tok = Bs + int((em_host >= 0).sum())
+        e_ms_max, e_tok = dp.reduce_timing(e_ms, float(e_tok), device="cuda")
+        e_tok /= tp
+        return {"value": e_tok / (e_ms_max / 1e3), "unit": "tokens/s",
+                "h2d_bytes_per_step": Bs * P * 4 / n_steps, "d2h_bytes_per_step": Bs * (k + 2) * 4,
+                "steps": n_steps, "includes_prefill": True,
+                "note": "one generation through the public C ABI with pinned host buffers: prompt H2D + prefill + "
+                        "per-step specformer_decode_steps(1) calls (draft + verify + accept, replayed from the "
+                        "step's CUDA graph), each step's accept lengths / emitted tokens copied to the host; "
+                        "prompt bytes amortised over the steps"}
+
+    # ---------------- kernel timeline (secondary): Kt replays of the timed step graph with the per-CTA
+    # %globaltimer probes on; the step's critical path attributed to kernel classes (credits PDL overlap)
     Kt = args.timeline_steps
     tl = None
     if Kt > 0 and N.lib().sf_debug_ktrace_enable(1) == 0:
@@ -279,7 +445,7 @@ def run_ours(args, cfg):
         n_rec = N.lib().sf_debug_ktrace(C.c_void_p(buf.ctypes.data), buf.size)
         N.lib().sf_debug_ktrace_enable(0)
         cp = timeline.critical_path(buf[:n_rec], key=timeline.kclass)
-        kv_t, _, _ = replay_lengths(lt0, pt0, acc_log[:Kt].cpu().tolist())
+        kv_t, _, _ = replay_lengths(lt0, pt0, acc_log[:Kt].cpu().tolist(), B)
         tl = {"steps": Kt, "cta_records": int(n_rec), "events_ms_per_step": t0e.elapsed_time(t1e) / Kt,
               "span_ms_per_step": cp["span_us"] / 1e3 / Kt, "idle_gap_ms_per_step": cp["gap_us"] / 1e3 / Kt,
               "classes": {c: {"exposed_ms_per_step": cp["exposed"][c] / 1e3 / Kt,
@@ -287,66 +453,13 @@ def run_ours(args, cfg):
                               "share_of_step": cp["exposed"][c] / max(1e-9, cp["span_us"])}
                           for c in cp["exposed"]},
               "attention_kv_bytes": kv_t}
+        g_tl = tl["classes"].get("gemm")
+        if g_tl:
+            g_ms = g_tl["exposed_ms_per_step"] / max(1e-9, g_tl["launches_per_step"])
+            tl["gemm_tflops_exposed"] = gemm_flops(B) / max(1e-9, g_tl["launches_per_step"]) / (g_ms / 1e3) / 1e12
 
-    # ---------------- per-class CUDA-event times: the step graph re-captured with an event-record
-    # node around every launch (Kp replays); also gives the host-known GEMM bytes per launch
-    lens0 = eng.capture(3, (B,), torch.int32).cpu().tolist()
-    prev0 = eng.capture(5, (B,), torch.int32).cpu().tolist()  # context layer runs at n_prev
-    acc_p = torch.zeros(Kp, B, dtype=torch.int32, device="cuda")
-    eng.profile(True)
-    ep0, ep1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ep0.record(eng.stream)
-    eng.decode_steps(Kp, None, acc_p)
-    ep1.record(eng.stream)
-    eng.sync()
-    prof_ms_total = ep0.elapsed_time(ep1)
-    cls = {c: eng.profile_read(c) for c in range(4)}
-    eng.profile(False)
-    attn_bytes, step_bytes_tot, step_flops_tot = replay_lengths(lens0, prev0, acc_p.cpu().tolist())
-    gemm_ms, gemm_n, gemm_bytes = cls[0]
-    attn_ms, attn_n, _ = cls[1]
-    # GEMM FLOPs of one step (2 T N K summed over the step's contractions)
-    d_, F_, V_ = cfg.d_model, cfg.d_ff, cfg.vocab
-    qkv_ = (cfg.n_heads + 2 * cfg.n_kv_heads) * cfg.head_dim
-    ao_ = cfg.n_heads * cfg.head_dim
-    Tv, Td = B * (k + 1), B * k
-    per_layer = qkv_ * d_ + d_ * ao_ + 2 * F_ * d_ + d_ * F_
-    gemm_flops_step = 2.0 * (Tv * (cfg.n_layers * per_layer + V_ * d_)
-                             + Tv * (4 * d_ * d_ + qkv_ * d_ + d_ * ao_)
-                             + B * k * d_ * d_ + Td * (qkv_ * d_ + d_ * ao_ + 3 * F_ * d_ + V_ * d_))
-    gemm_bytes_step = gemm_bytes / max(1, Kp)
-    gemm_n_step = gemm_n / max(1, Kp)
-    # the dominant class and its per-launch duration: from the timeline (graph replay, PDL overlap
-    # intact, exposed critical-path time per launch) when it ran, else from the event-node graph
-    if tl is not None:
-        ex = {c: tl["classes"].get(c, {}).get("exposed_ms_per_step", 0.0) for c in ("gemm", "attention")}
-        dominant = "gemm" if ex["gemm"] >= ex["attention"] else "attention"
-        n_dom = tl["classes"][dominant]["launches_per_step"]
-        dom_ms = ex[dominant] / max(1e-9, n_dom)
-        dur_source = "kernel timeline: exposed critical-path time per launch over graph replays"
-        attn_bytes_step = tl["attention_kv_bytes"] / Kt
-    else:
-        dominant = "gemm" if gemm_ms >= attn_ms else "attention"
-        n_dom = (gemm_n if dominant == "gemm" else attn_n) / max(1, Kp)
-        dom_ms = (gemm_ms if dominant == "gemm" else attn_ms) / max(1, Kp) / max(1e-9, n_dom)
-        dur_source = "CUDA event-record nodes around each launch (no PDL overlap)"
-        attn_bytes_step = attn_bytes / max(1, Kp)
-    if dominant == "gemm":
-        t_hbm = gemm_bytes_step / (hbm * 1e9)
-        t_tc = gemm_flops_step / (tf_sust * 1e12)
-        if t_tc > t_hbm:  # compute-bound at this batch: judge against the sustained bf16 peak
-            bound, unit, peak_v = "tensor", "TFLOP/s", tf_sust
-            peak_src = peak_src + " (bf16_tflops_sustained: kernel timed inside the step)"
-            dom_units = gemm_flops_step / max(1e-9, n_dom)
-            achieved = dom_units / (dom_ms / 1e3) / 1e12
-        else:
-            bound, unit, peak_v = "hbm", "GB/s", hbm
-            dom_units = gemm_bytes_step / max(1e-9, n_dom)
-            achieved = dom_units / (dom_ms / 1e3) / 1e9
-    else:
-        bound, unit, peak_v = "hbm", "GB/s", hbm
-        dom_units = attn_bytes_step / max(1e-9, n_dom)
-        achieved = dom_units / (dom_ms / 1e3) / 1e9
+    ev = event_profile(B)
+    dominant = ev["dominant"]
     # DRAM bytes per launch of the dominant kernel class from the committed ncu launch list of this
     # command at this batch (profiles/ncu_traffic.json, written by tools/profile_summary.py)
     traffic = None
@@ -356,47 +469,31 @@ def run_ours(args, cfg):
             traffic = json.load(open(traffic_path)).get(f"{cfg.name}_b{B}", {}).get("traffic_bytes_per_launch", {}).get(dominant)
         except Exception:
             traffic = None
-    prof_classes = {name: {"ms_total": cls[c][0], "launches": cls[c][1], "share_of_profiled_step":
-                           cls[c][0] / max(1e-9, prof_ms_total)}
-                    for c, name in enumerate(["gemm", "attention", "norm", "argmax"])}
-    prof_classes["gemm"]["achieved_gbs"] = gemm_bytes / max(1e-12, gemm_ms / 1e3) / 1e9
-    prof_classes["gemm"]["achieved_tflops"] = gemm_flops_step * Kp / max(1e-12, gemm_ms / 1e3) / 1e12
-    prof_classes["attention"]["achieved_gbs"] = attn_bytes / max(1e-12, attn_ms / 1e3) / 1e9
+    e2e = e2e_run(B, prompts, Ke)
 
-    # ---------------- e2e: one generation through the public C ABI -- prompt H2D from pinned host
-    # memory, prefill, then per step one specformer_decode_steps(1) call (the captured step graph)
-    # and a D2H read of that step's accept lengths and emitted tokens into pinned host buffers
-    lib = eng.lib
-    host_prompts = prompts.clone().pin_memory()
-    g_host = torch.empty(B, dtype=torch.int32).pin_memory()
-    m_host = torch.empty(Ke, B, dtype=torch.int32).pin_memory()
-    em_host = torch.empty(Ke, B, k + 1, dtype=torch.int32).pin_memory()
-    em_dev = torch.empty(1, B, k + 1, dtype=torch.int32, device="cuda")
-    m_dev = torch.empty(1, B, dtype=torch.int32, device="cuda")
-    p = lambda t: C.c_void_p(t.data_ptr())
-    st = lib.specformer_prefill(eng.h, p(host_prompts), B, P, p(g_host))  # warm-up: captures the step graph
-    for _ in range(2):
-        st |= lib.specformer_decode_steps(eng.h, 1, p(em_dev), p(m_dev))
-    eng.sync()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    x0.record(eng.stream)
-    st |= lib.specformer_prefill(eng.h, p(host_prompts), B, P, p(g_host))
-    with torch.cuda.stream(eng.stream):  # the D2H copies run on the engine stream, after each step
-        for s in range(Ke):
-            st |= lib.specformer_decode_steps(eng.h, 1, p(em_dev), p(m_dev))
-            em_host[s].copy_(em_dev[0], non_blocking=True)
-            m_host[s].copy_(m_dev[0], non_blocking=True)
-    x1.record(eng.stream)
-    eng.sync()
-    if st != 0:
-        raise RuntimeError("e2e C-ABI call failed")
-    e2e_ms = x0.elapsed_time(x1)
-    e2e_tokens = B + int((em_host >= 0).sum())
-    e2e_ms_max, e2e_tok = dp.reduce_timing(e2e_ms, float(e2e_tokens), device="cuda")
-    e2e_tok /= tp
+    # ---------------- batch sweep (BASELINE metric: verify-steps/s vs batch 1-64): the same engine
+    # re-prefilled at each smaller batch; per batch the median of the timed windows, the step
+    # roofline, event-timed GEMM / attention fractions and one end-to-end generation
+    sweep = []
+    for Bs in args.sweep_list:
+        if Bs >= B or tp > 1:
+            continue
+        pr_s = prompts[:Bs].contiguous()
+        win = timed_windows(Bs, pr_s)
+        sb_s = window_roofline(win, Bs)
+        w_ms, w_tok = dp.reduce_timing(win["ms"], float(int((win["after"] - win["before"]).sum())), device="cuda")
+        ev_s = event_profile(Bs)
+        sweep.append({"batch_per_gpu": Bs, "value": w_tok / (w_ms / 1e3), "unit": "tokens/s",
+                      "ms_per_step": w_ms / K, "window_ms": win["all_ms"],
+                      "verify_steps_per_s": K / (w_ms / 1e3), "mean_accepted_length": w_tok / (K * Bs * world),
+                      "step_roofline": {"bound": "hbm", "achieved": sb_s / (win["ms"] / 1e3) / 1e9, "peak": hbm,
+                                        "unit": "GB/s", "frac": sb_s / (win["ms"] / 1e3) / 1e9 / hbm,
+                                        "bytes_per_step": sb_s / K, "t_roof_ms": (sb_s / K) / (hbm * 1e9) * 1e3},
+                      "roofline": {k_: ev_s[k_] for k_ in ("bound", "achieved", "peak", "unit", "frac", "peak_source",
+                                                           "ms_per_launch", "launches_per_step")} | {"kernel": ev_s["dominant"]},
+                      "event_classes": ev_s["classes"],
+                      "e2e": e2e_run(Bs, pr_s, min(Ke, args.sweep_e2e_steps)),
+                      "gpu_launches": win["launches"]})
 
     # ---------------- forced acceptance: drafts replaced -- after the draft step has run
     # and been paid for -- by the GPU's own greedy continuation, corrupted at slot j with
@@ -474,28 +571,29 @@ def run_ours(args, cfg):
                        "model": cfg.name, "batch_per_gpu": B if tp == 1 else B / tp, "global_batch": B * world // tp,
                        "draft_len": k, "prompt_len": P, "parallelism": f"tp{tp}" if tp > 1 else f"dp{world}",
                        "cuda_graph": True, "logits": "not stored (fused LM-head argmax)" if no_logits else "stored",
-                       "l2": "inputs larger than L2 (14 GB weights + KV per step)"},
+                       "l2": "inputs larger than L2 (14 GB weights + KV per step)",
+                       "timing": f"median of {n_win} windows of {K} steps, each after a fresh prefill + {W} warm-up steps"},
             "verify_steps_per_s": steps_per_s, "verify_steps_per_s_box": steps_per_s * world,
             "mean_accepted_length": a_meas,
             "forced_acceptance": forced,
             "modeled_tokens_per_s_at_paper_a": steps_per_s * B * world // tp * A_PAPER.get(cfg.name, 1.75),
             "a_paper": A_PAPER.get(cfg.name),
-            "roofline": {"bound": bound, "kernel": dominant, "achieved": achieved, "peak": peak_v, "unit": unit,
-                         "frac": achieved / peak_v, "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_units_per_launch": dom_units, "ms_per_launch": dom_ms,
-                         "launches_per_step": n_dom, "duration_source": dur_source,
-                         "timeline": tl, "event_classes": prof_classes, "event_profiled_steps": Kp},
+            "roofline": {"bound": ev["bound"], "kernel": dominant, "achieved": ev["achieved"], "peak": ev["peak"],
+                         "unit": ev["unit"], "frac": ev["frac"], "traffic": traffic, "peak_source": ev["peak_source"],
+                         "algorithmic_units_per_launch": ev["units_per_launch"], "ms_per_launch": ev["ms_per_launch"],
+                         "launches_per_step": ev["launches_per_step"],
+                         "duration_source": "CUDA event-record nodes around every launch on the engine stream (the "
+                                            "step graph re-captured with them; serialises the launches, no PDL "
+                                            "overlap), averaged over the profiled steps",
+                         "event_classes": ev["classes"], "event_profiled_steps": Kp,
+                         "timeline": tl},
             "step_roofline": {"bound": "hbm", "achieved": step_gbs, "peak": hbm, "unit": "GB/s",
                               "frac": step_gbs / hbm, "bytes_per_step": sb / K,
-                              "flops_per_step": step_flops_tot / max(1, Kp),
+                              "flops_per_step": ev["step_flops"],
                               "t_roof_ms": (sb / K) / (hbm * 1e9) * 1e3},
-            "e2e": {"value": e2e_tok / (e2e_ms_max / 1e3), "unit": "tokens/s",
-                    "h2d_bytes_per_step": B * P * 4 / Ke, "d2h_bytes_per_step": B * (k + 2) * 4,
-                    "steps": Ke, "includes_prefill": True,
-                    "note": "one generation through the public C ABI with pinned host buffers: prompt H2D + "
-                            "prefill + Ke specformer_decode_steps(1) calls (draft + verify + accept, replayed "
-                            "from the step's CUDA graph), each step's accept lengths / emitted tokens copied "
-                            "to the host; prompt bytes amortised over the steps"},
+            "windows": {"n": n_win, "ms": main["all_ms"], "reported": "median"},
+            "batch_sweep": sweep,
+            "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
@@ -523,11 +621,15 @@ def main():
     ap.add_argument("--timeline-steps", type=int, default=2, help="graph steps replayed with the kernel timeline on")
     ap.add_argument("--draft-len", type=int, default=None, help="override k (13B sweep: 4 / 6 / 8)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--windows", type=int, default=3, help="timed windows (median reported)")
+    ap.add_argument("--sweep", default="1,16", help="smaller batches measured in the same run (BASELINE: 1-64)")
+    ap.add_argument("--sweep-e2e-steps", type=int, default=64)
     ap.add_argument("--keep-logits", action="store_true", help="store the fp32 logits every step (the API's "
                     "logits read-out; default: not stored, the LM heads' fused argmax gives the tokens)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    args.sweep_list = [int(x) for x in args.sweep.split(",") if x.strip()] if args.sweep else []
     from synth import get_config
     cfg = get_config(args.config)
     if args.draft_len is not None:

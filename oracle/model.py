@@ -11,6 +11,8 @@ attention is materialised as the full masked score matrix per head.
 """
 from __future__ import annotations
 
+import time
+
 import numpy as np
 
 
@@ -280,7 +282,7 @@ def decode_greedy(W, prompt, n_tokens):
     return out
 
 
-def sd_decode(W, prompt, n_tokens, draft_fn=None, record=False):
+def sd_decode(W, prompt, n_tokens, draft_fn=None, record=False, step_times=None):
     """SpecFormer speculative decoding, the three-step protocol of P20-23:
       1. draft k tokens from the context layer's row for the newest committed position
          (draft_fn(step, n, out) may override, e.g. perfect or adversarial drafts);
@@ -290,7 +292,8 @@ def sd_decode(W, prompt, n_tokens, draft_fn=None, record=False):
          run the context layer over the m+1 committed verify rows (C14), next draft row
          = I_D[m].
     Stops once >= n_tokens are emitted and trims the overshoot (reading C15; S400).
-    Returns (tokens, steps) where steps lists per-step dicts when record=True."""
+    Returns (tokens, steps) where steps lists per-step dicts when record=True. step_times (a list,
+    optional; bench.py's CPU baseline) receives each step's wall time -- timing only, no arithmetic."""
     c = W.cfg
     L = c.n_layers
     cache = _new_cache(c)
@@ -299,6 +302,7 @@ def sd_decode(W, prompt, n_tokens, draft_fn=None, record=False):
     out, n, last = [g0], P, g0
     steps = []
     while len(out) < n_tokens:
+        t_step = time.perf_counter() if step_times is not None else 0.0
         dl = None
         if draft_fn is None:
             dl = draft_logits(W, i_d)
@@ -317,6 +321,8 @@ def sd_decode(W, prompt, n_tokens, draft_fn=None, record=False):
         out += emitted
         last = greedy[m]
         n += m + 1
+        if step_times is not None:
+            step_times.append(time.perf_counter() - t_step)
     return out[:n_tokens], steps
 
 
