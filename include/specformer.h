@@ -195,6 +195,11 @@ sf_status sf_pack_matrix(int32_t dtype, const void* src_dev, void* dst_dev, int6
  * 2 (A bf16, W already in layout 1). out dev fp32. Uses the same kernels as the hot path. */
 sf_status sf_test_gemm(int32_t dtype, const void* A, const void* W, float* out, int32_t T, int32_t N, int32_t K,
                        void* stream);
+/* Tools only: average device time (ms, CUDA events over `reps` back-to-back launches after 2 warm-up
+ * launches) of one bf16 EPI_PARTIAL GEMM out[T, N] = A[T, K] W[N, K]^T on zeroed inputs the call
+ * allocates and frees: impl 0 the standalone stream-K launch, 1 the same GEMM as a one-phase
+ * layer-sequence launch. */
+sf_status sf_bench_gemm(int32_t impl, int32_t T, int32_t N, int32_t K, int32_t reps, float* ms_out);
 /* Tools only: when the process ran with SF_GEMM_TRACE=1, copy (and clear) the per-CTA %globaltimer
  * timeline (ns; [CTA][64] uint64, slot map in csrc/gemm.cu) of the last tcgen05 GEMM launches into
  * host memory dst_host (cap entries). Returns the number of entries copied, 0 if tracing is off. */

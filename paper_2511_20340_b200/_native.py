@@ -62,6 +62,7 @@ SIGNATURES = [
                                   C.POINTER(C.c_double)]),
     ("sf_pack_matrix", C.c_int, [C.c_int32, _P, _P, C.c_int64, C.c_int64, _P]),
     ("sf_test_gemm", C.c_int, [C.c_int32, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, _P]),
+    ("sf_bench_gemm", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
     ("sf_debug_gemm_trace", C.c_int32, [_P, C.c_int32]),
     ("sf_debug_ktrace", C.c_int32, [_P, C.c_int32]),
     ("sf_debug_ktrace_enable", C.c_int32, [C.c_int32]),

@@ -166,7 +166,7 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
 // timeline of a CUDA-graph step). Off by default: one predicated load per CTA.
 enum KtKind : uint32_t {
   KT_GEMM = 1, KT_RESID_NORM, KT_ROPE, KT_ATTN, KT_RMSNORM, KT_GROUP_RMS, KT_EMBED, KT_ARGMAX_P, KT_ARGMAX_F,
-  KT_ACCEPT, KT_BIDIR, KT_GATHER, KT_ROWS, KT_GEMM_SIMT, KT_ATTN_PART, KT_ATTN_COMB, KT_MISC, KT_ITEM
+  KT_ACCEPT, KT_BIDIR, KT_GATHER, KT_ROWS, KT_GEMM_SIMT, KT_ATTN_PART, KT_ATTN_COMB, KT_MISC, KT_ITEM, KT_GEMM_SEQ
 };
 
 struct KtRec {

@@ -124,4 +124,33 @@ cudaError_t launch_rope_partial(const float* partial, const PartialGeom* g, int 
                                 const float2* rope, int Hq, int Hkv, const int* bt, int pps, void* Kp, void* Vp,
                                 void* q_out, cudaStream_t s);
 
+// Layer-sequence kernel (csrc/gemm_seq.cuh): several GEMM phases (bf16, CTA pairs, modes EPI_PARTIAL /
+// EPI_SWIGLU_ACT / EPI_QKV_ROPE) and consumers of the preceding EPI_PARTIAL phase (residual + RMSNorm,
+// RoPE / KV append) in ONE persistent launch, each with the standalone launches' partition and
+// arithmetic (bit-identical results); the weight stream runs ahead across phase boundaries.
+enum SeqKind : int { SEQ_GEMM = 0, SEQ_RESID_NORM = 1, SEQ_ROPE = 2 };
+constexpr int kSeqMaxPhases = 8;
+constexpr int kSeqMaxGemm = 4;
+struct SeqStep {
+  int kind = SEQ_GEMM;
+  // SEQ_GEMM: out = A[T, K] . W[N, K]^T (W tile-contiguous), epilogue epi (PARTIAL / SWIGLU / QKV_ROPE)
+  const void* A = nullptr;
+  int lda = 0;
+  const void* W = nullptr;
+  int N = 0, K = 0;
+  GemmEpi epi;  // (SEQ_ROPE: epi.rope)
+  // SEQ_RESID_NORM (as launch_resid_norm with rep = 1, add = bias = null, d = the GEMM's N)
+  const float* resid = nullptr;
+  float* out = nullptr;
+  float* tap = nullptr;
+  const float* gamma = nullptr;
+  __nv_bfloat16* xn = nullptr;
+  int d = 0;
+  float eps = 0.f;
+};
+bool gemm_seq_supported(int T, const SeqStep* steps, int n);
+// done: >= n zeroed ints, exit_cnt: one zeroed int (re-armed by the kernel); scratch as gemm_launch's
+cudaError_t gemm_seq_launch(int T, const SeqStep* steps, int n, const GemmScratch& scratch, int* done, int* exit_cnt,
+                            cudaStream_t s);
+
 }  // namespace sf

@@ -614,11 +614,14 @@ static cudaError_t qkv_gemm(sf_handle* h, const void* W, int layer, int T, int q
   return gemm(h, h->xn, p.d, W, T, p.qkvw, p.d, e);
 }
 
-static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const int* pos0, int max_key) {
+static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const int* pos0, int max_key,
+                              bool rope_done = false) {
   const Plan& p = h->p;
   ProfScope ps(h, 1, 0.0);  // KV bytes depend on device-resident lengths: the bench computes them
   cudaError_t e = cudaSuccess;
-  if (qkv_partial(h, T)) {
+  if (rope_done) {
+    // q rotated and K / V appended already (the layer-sequence kernel's QKV phase)
+  } else if (qkv_partial(h, T)) {
     PartialGeom g;
     e = gemm_partial_geom(T, p.qkvw, p.d, &g, kQkvDrain)
             ? launch_rope_partial(h->gpart, &g, T, q_len, pos0, (const float2*)h->rope, p.Hq, p.Hkv, h->bt, p.pps,
@@ -653,6 +656,74 @@ static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const i
   return dbg_sync(h, "attention", launch_attention(h->bf, ap, h->st));
 }
 
+// Small verify blocks (T <= SF_SEQ_T, default 80: batch <= 16 at k = 4): the part of base layer l
+// between two attentions -- O-proj + residual + RMS_ffn, gate/up SwiGLU, down + residual (+ tap) +
+// the next norm, and layer l+1's QKV with RoPE / KV append -- as ONE persistent launch
+// (gemm_seq_launch, csrc/gemm_seq.cuh) with the standalone launches' partition and arithmetic
+// (bit-identical; SF_SEQ_T=0 turns it off). Returns false (nothing launched) when the shapes or
+// switches call for the standalone path.
+static int seq_T() {
+  const char* e = getenv("SF_SEQ_T");  // (read per call: tests compare both paths)
+  return e ? atoi(e) : 0;  // (off by default until it measures faster than the standalone launches)
+}
+static bool layer_seq(sf_handle* h, cudaError_t* err, int l, int T, int q_len, const int* pos0, float* tap,
+                      const float* next_g) {
+  const Plan& p = h->p;
+  const char* chain = getenv("SF_GEMM_CHAIN");
+  if (!h->bf || p.hd != 128 || p.tp > 1 || T > seq_T() || T > 128 || (chain && atoi(chain) != 0)) return false;
+  if (!resid_norm_supported(p.d, T, p.d, p.ao) || !resid_norm_supported(p.d, T, p.d, p.F)) return false;
+  const auto& w = h->lw[l];
+  SeqStep st[kSeqMaxPhases];
+  int n = 0;
+  SeqStep& o = st[n++];  // O-proj -> k-segment partials
+  o.A = h->attn, o.lda = p.ao, o.W = w.wo, o.N = p.d, o.K = p.ao;
+  o.epi.mode = EPI_PARTIAL;
+  SeqStep& r1 = st[n++];  // residual + RMS_ffn
+  r1.kind = SEQ_RESID_NORM;
+  r1.resid = h->resid, r1.out = h->resid, r1.gamma = w.ffn_norm, r1.xn = (__nv_bfloat16*)h->xn, r1.d = p.d;
+  r1.eps = h->c.rms_eps;
+  SeqStep& gu = st[n++];  // gate/up SwiGLU
+  gu.A = h->xn, gu.lda = p.d, gu.W = w.wgu, gu.N = 2 * p.F, gu.K = p.d;
+  gu.epi.mode = EPI_SWIGLU_ACT, gu.epi.out = h->ffn, gu.epi.ldo = p.F;
+  SeqStep& dn = st[n++];  // down -> partials
+  dn.A = h->ffn, dn.lda = p.F, dn.W = w.wdown, dn.N = p.d, dn.K = p.F;
+  dn.epi.mode = EPI_PARTIAL;
+  SeqStep& r2 = st[n++];  // residual (+ tap) + the next norm
+  r2.kind = SEQ_RESID_NORM;
+  r2.resid = h->resid, r2.out = h->resid, r2.tap = tap, r2.gamma = next_g;
+  r2.xn = next_g ? (__nv_bfloat16*)h->xn : nullptr, r2.d = p.d, r2.eps = h->c.rms_eps;
+  if (l + 1 < p.L) {  // layer l+1's QKV projection, as qkv_gemm would run it at this T
+    RopeEpi R;
+    R.pos0 = pos0, R.q_len = q_len, R.table = h->rope, R.Hq = p.Hq, R.Hkv = p.Hkv, R.bt = h->bt, R.pps = p.pps;
+    R.Kp = h->kp(l + 1), R.Vp = h->vp(l + 1), R.q_out = h->qrot;
+    SeqStep& q = st[n++];
+    q.A = h->xn, q.lda = p.d, q.W = h->lw[l + 1].wqkv, q.N = p.qkvw, q.K = p.d;
+    q.epi.drain = kQkvDrain;
+    if (fused_rope(h, T)) {
+      q.epi.mode = EPI_QKV_ROPE, q.epi.ldo = 128, q.epi.rope = R;
+    } else if (qkv_partial(h, T)) {
+      q.epi.mode = EPI_PARTIAL;
+      SeqStep& rp = st[n++];
+      rp.kind = SEQ_ROPE;
+      rp.epi.rope = R;
+    } else {
+      return false;
+    }
+  }
+  if (!gemm_seq_supported(T, st, n)) return false;
+  double wbytes = 2.0 * ((double)p.d * p.ao + 3.0 * p.d * p.F + (l + 1 < p.L ? (double)p.qkvw * p.d : 0.0));
+  ProfScope ps(h, 0, wbytes);
+  GemmScratch sc;
+  sc.partial = h->gpart;
+  sc.partial_elems = p.gpart_elems;
+  sc.counters = h->gcnt;
+  sc.n_counters = 2048;  // (2048.. : the layer-sequence completion counters)
+  int* done = h->gcnt + 2048 + (l % 96) * 16;
+  h->launches++;
+  *err = dbg_sync(h, "layer_seq", gemm_seq_launch(T, st, n, sc, done, done + 15, h->st));
+  return true;
+}
+
 // Base decoder forward over T rows (q_len per sequence, positions pos0[b] + i); writes resid and
 // the 4 hook taps (P175) into h->taps.
 static cudaError_t base_forward(sf_handle* h, int T, int q_len, const int* pos0, int max_key,
@@ -668,11 +739,33 @@ static cudaError_t base_forward(sf_handle* h, int T, int q_len, const int* pos0,
   for (int g = 1; g < 4; ++g)
     if (tl[g] == 0) cudaMemcpyAsync(h->taps + g * tstride, h->taps, (size_t)T * p.d * 4, cudaMemcpyDeviceToDevice, h->st);
   bool xn_ready = false;  // xn already holds RMS_attn(resid) of this layer (fused into the last consumer)
+  bool qkv_done = false;  // layer l's QKV projection, RoPE and KV append ran in the previous layer_seq launch
   for (int l = 0; l < p.L; ++l) {
     const auto& w = h->lw[l];
-    if (!xn_ready && (e = rmsnorm(h, h->resid, p.d, w.attn_norm, T, h->xn, p.d))) return e;
-    if ((e = qkv_gemm(h, w.wqkv, l, T, q_len, pos0))) return e;
-    if ((e = attn_layer(h, l, T, q_len, pos0, max_key))) return e;
+    if (qkv_done) {
+      if ((e = attn_layer(h, l, T, q_len, pos0, max_key, true))) return e;
+    } else {
+      if (!xn_ready && (e = rmsnorm(h, h->resid, p.d, w.attn_norm, T, h->xn, p.d))) return e;
+      if ((e = qkv_gemm(h, w.wqkv, l, T, q_len, pos0))) return e;
+      if ((e = attn_layer(h, l, T, q_len, pos0, max_key))) return e;
+    }
+    qkv_done = false;
+    {
+      int first = -1;
+      for (int g = 0; g < 4; ++g)
+        if (tl[g] == l + 1 && first < 0) first = g;
+      float* tap = first >= 0 ? h->taps + first * tstride : nullptr;
+      const float* next_g = (l + 1 < p.L) ? h->lw[l + 1].attn_norm : (final_norm ? h->final_norm : nullptr);
+      if (layer_seq(h, &e, l, T, q_len, pos0, tap, next_g)) {
+        if (e) return e;
+        for (int g = first + 1; first >= 0 && g < 4; ++g)
+          if (tl[g] == l + 1)
+            cudaMemcpyAsync(h->taps + g * tstride, tap, (size_t)T * p.d * 4, cudaMemcpyDeviceToDevice, h->st);
+        xn_ready = next_g != nullptr;
+        qkv_done = l + 1 < p.L;
+        continue;
+      }
+    }
     // o-proj + residual + RMS_ffn
     if (!gemm_resid_norm(h, &e, h->attn, p.ao, w.wo, T, p.d, p.ao, 1, h->resid, nullptr, h->resid, nullptr,
                          w.ffn_norm, true)) {
@@ -1643,6 +1736,57 @@ sf_status sf_test_gemm(int32_t dtype, const void* A, const void* W, float* out, 
   e.out = out;
   e.ldo = N;
   return gemm_launch(bf, A, K, Wuse, bf, T, N, K, e, sc, st) == cudaSuccess ? SF_OK : SF_ERR_CUDA;
+}
+
+sf_status sf_bench_gemm(int32_t impl, int32_t T, int32_t N, int32_t K, int32_t reps, float* ms_out) {
+  // tools only: the GEMM main loop in isolation -- impl 0 the standalone EPI_PARTIAL launch, 1 the
+  // same GEMM as a one-phase layer-sequence launch; random bf16 weights / activations
+  if (T < 1 || N < 256 || K < 64 || reps < 1 || !ms_out) return SF_ERR_ARG;
+  void *A = nullptr, *W = nullptr;
+  float* part = nullptr;
+  int* cnt = nullptr;
+  const int64_t pe = gemm_partial_elems(true, std::min(T, 512), N, K);
+  if (cudaMalloc(&A, (size_t)T * K * 2) || cudaMalloc(&W, (size_t)N * K * 2) || cudaMalloc((void**)&part, pe * 4) ||
+      cudaMalloc((void**)&cnt, 4096 * 4))
+    return SF_ERR_CUDA;
+  cudaMemset(A, 0, (size_t)T * K * 2);
+  cudaMemset(W, 0, (size_t)N * K * 2);
+  cudaMemset(cnt, 0, 4096 * 4);
+  GemmScratch sc;
+  sc.partial = part;
+  sc.partial_elems = pe;
+  sc.counters = cnt;
+  sc.n_counters = 2048;
+  cudaStream_t st;
+  cudaStreamCreate(&st);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  SeqStep step;
+  step.A = A, step.lda = K, step.W = W, step.N = N, step.K = K;
+  step.epi.mode = EPI_PARTIAL;
+  GemmEpi e;
+  e.mode = EPI_PARTIAL;
+  cudaError_t err = cudaSuccess;
+  for (int r = -2; r < reps; ++r) {
+    if (r == 0) cudaEventRecord(e0, st);
+    err = impl == 0 ? gemm_launch(true, A, K, W, true, T, N, K, e, sc, st)
+                    : gemm_seq_launch(T, &step, 1, sc, cnt + 2048, cnt + 2048 + 15, st);
+    if (err != cudaSuccess) break;
+  }
+  cudaEventRecord(e1, st);
+  cudaStreamSynchronize(st);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *ms_out = ms / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(st);
+  cudaFree(A);
+  cudaFree(W);
+  cudaFree(part);
+  cudaFree(cnt);
+  return err == cudaSuccess ? SF_OK : SF_ERR_CUDA;
 }
 
 sf_status sf_pack_matrix(int32_t dtype, const void* src_dev, void* dst_dev, int64_t N, int64_t K, void* stream) {

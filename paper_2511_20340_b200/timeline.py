@@ -15,11 +15,11 @@ import numpy as np
 
 KIND = {1: "gemm", 2: "resid_norm", 3: "rope", 4: "attn", 5: "rmsnorm", 6: "group_rms", 7: "embed", 8: "argmax_p",
         9: "argmax_f", 10: "accept", 11: "bidir", 12: "gather", 13: "rows", 14: "gemm_simt", 15: "attn_part",
-        16: "attn_comb", 17: "misc", 18: "item"}
+        16: "attn_comb", 17: "misc", 18: "item", 19: "gemm_seq"}
 KT_ITEM = 18
 REC = np.dtype([("kid", "<u4"), ("sm", "<u4"), ("t0", "<u8"), ("tw", "<u8"), ("t1", "<u8"), ("pad", "<u8")])
 # kernel classes of the bench roofline (same split as sf_profile_read)
-CLASS = {"gemm": "gemm", "gemm_simt": "gemm", "attn": "attention", "rope": "attention", "attn_part": "attention",
+CLASS = {"gemm": "gemm", "gemm_simt": "gemm", "gemm_seq": "gemm", "attn": "attention", "rope": "attention", "attn_part": "attention",
          "attn_comb": "attention", "resid_norm": "norm", "rmsnorm": "norm", "group_rms": "norm", "embed": "norm",
          "gather": "norm", "rows": "norm"}
 

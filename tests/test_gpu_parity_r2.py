@@ -344,3 +344,30 @@ def test_teacher_forced_layers(cfg, kind):
         assert r12 <= 1e-2 * np.sqrt(2), r12
         msg += f", layers 1-2 from HS[0] {r12:.2e}"
     print(msg)
+
+
+# ------------------------------------------------------------------ layer-sequence kernel (small T)
+SEQ_CFGS = [MID, GQA, W7D2.replace(name="7b-d3-b16", n_layers=3, batch=16, prompt_len=64),
+            W7D2.replace(name="7b-d3-b12", n_layers=3, batch=12, prompt_len=64)]
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("cfg", SEQ_CFGS, ids=["mha128_T20", "gqa4_T15", "7b_width_T80", "7b_width_T60"])
+def test_layer_seq_bit_exact(cfg, monkeypatch):
+    """The persistent layer-sequence launch (T <= 80: O-proj -> residual/RMSNorm -> gate/up -> down ->
+    residual/RMSNorm -> next QKV with RoPE / KV append in one kernel; csrc/gemm_seq.cuh) keeps the
+    standalone launches' partition and arithmetic: logits, draft logits, tokens and accept lengths are
+    bit-identical with it off (SF_SEQ_T=0), across the fused-RoPE (T < 64) and RoPE-consumer (T >= 64)
+    forms of the QKV phase, with ragged forced acceptance."""
+    w, prompts = setup(cfg, seed=28, jitter=0.1)
+    k, n_steps = cfg.draft_len, 5
+    ar = run_gpu(cfg, w, prompts, n_steps * (k + 1) + k + 2, k=0)["tokens"]
+    slots = corrupt_slots(n_steps, cfg.batch, k, seed=8)
+    monkeypatch.setenv("SF_SEQ_T", "0")
+    off = forced_run(cfg, w, prompts, n_steps, slots, ar)
+    monkeypatch.setenv("SF_SEQ_T", "80")
+    on = forced_run(cfg, w, prompts, n_steps, slots, ar)
+    for s1, s2 in zip(off["steps"], on["steps"]):
+        for key in ("logits", "draft_logits", "greedy", "m", "emitted", "seq_len", "last_token"):
+            assert np.array_equal(s1[key], s2[key]), key
+    check_commit_integers(cfg, prompts, on)
