@@ -149,8 +149,9 @@ struct SeqStep {
   float eps = 0.f;
 };
 bool gemm_seq_supported(int T, const SeqStep* steps, int n);
-// done: >= n zeroed ints, exit_cnt: one zeroed int (re-armed by the kernel); scratch as gemm_launch's
-cudaError_t gemm_seq_launch(int T, const SeqStep* steps, int n, const GemmScratch& scratch, int* done, int* exit_cnt,
-                            cudaStream_t s);
+// sync: kSeqSyncInts device ints, zeroed once, private to one call site (the kernel keeps them
+// consistent across launches with a launch epoch); scratch as gemm_launch's
+constexpr int kSeqSyncInts = 64 + 8 * 128 * 33;
+cudaError_t gemm_seq_launch(int T, const SeqStep* steps, int n, const GemmScratch& scratch, int* sync, cudaStream_t s);
 
 }  // namespace sf

@@ -46,8 +46,9 @@ struct SeqParams {
   uint32_t tmem_cols;
   float* partial;  // split-K partial slots (the standalone GEMMs' scratch)
   int* flags;      // per-CTA tail-piece flags (standalone layout)
-  int* done;       // [n_phases] CTA completion counters (zero; re-armed by the last CTA out)
-  int* exit_cnt;
+  int* sync;       // kSeqSyncInts ints (zeroed once): launch epoch, exit counter, per-phase completion
+                   // counters, per-(phase, CTA) and per-(phase, 128-row tile) flags -- all monotonic
+                   // in the epoch, so nothing is re-armed between launches
   SeqPhase ph[kSeqMaxPhases];
 };
 struct SeqMaps {
@@ -55,6 +56,14 @@ struct SeqMaps {
   CUtensorMap a[kSeqMaxGemm];  // activations [T, K], box NT / 2 rows
 };
 static_assert(sizeof(SeqParams) + sizeof(SeqMaps) <= 4000, "kernel parameter space");
+// sync block layout
+constexpr int kSeqRows = 128;  // T limit
+SF_DEV int* seq_done(int* sy, int ph) { return sy + 8 + ph; }
+SF_DEV int* seq_rowcnt(int* sy, int ph, int row) { return sy + 64 + ph * kSeqRows + row; }
+SF_DEV float* seq_ss(int* sy, int ph, int row) {  // [32] per-virtual-warp sums of squares of a row
+  return reinterpret_cast<float*>(sy + 64 + kSeqMaxPhases * kSeqRows) + ((size_t)ph * kSeqRows + row) * 32;
+}
+static_assert(64 + kSeqMaxPhases * kSeqRows * 33 <= kSeqSyncInts, "sync block");
 
 SF_DEV int rn_ng_dev(int d) {  // float4 groups per virtual thread (rn_ng, device copy)
   for (int ng = 1; ng <= 4; ++ng)
@@ -183,23 +192,28 @@ gemm_seq_kernel(const __grid_constant__ SeqMaps maps, const __grid_constant__ Se
     for (int i = 0; i < p.npre && wph < n_ph; ++i) SF_SEQ_ISSUE_W();
     pdl_wait();
     pdl_trigger();
-    int ready = 0;  // phases <= ready have their inputs
+    int E1 = 0;  // this launch's epoch mark
+    if (lane == 0) E1 = ld_acquire(p.sync) + 1;
+    E1 = __shfl_sync(0xffffffffu, E1, 0);
+    int ready = 0;  // phases <= ready have all their inputs
     while (aph < n_ph) {
       if (pending > 0) {
-        if (aph > ready) {
+        bool go = aph <= ready;
+        if (!go) {
           int v = 0;
-          if (lane == 0) v = ld_acquire(&p.done[aph - 1]);
+          if (lane == 0) v = ld_acquire(seq_done(p.sync, aph - 1));
           v = __shfl_sync(0xffffffffu, v, 0);
-          if (v >= (int)gridDim.x) {
+          if (v >= E1 * (int)gridDim.x) {
             ready = aph;
-            fence_proxy_async_global();  // the consumers' generic stores -> this TMA read
+            go = true;
+            fence_proxy_async_global();  // the producers' generic stores -> this TMA read
             if (lane == 0) {
               const unsigned long long tn = kt_now();
               kt_item(0x400000u | ((uint32_t)aph << 8) | (uint32_t)(blockIdx.x & 0xFF), tn, tn, tn);
             }
           }
         }
-        if (aph <= ready) {
+        if (go) {
           if (elect_one())
             tma_load_2d_2sm(smem + (size_t)as * stage_bytes + BM * BK * 2, &maps.a[amap], &full[as], ak * BK,
                             (int)rank * a_rows, kEvictLast);
@@ -302,6 +316,7 @@ gemm_seq_kernel(const __grid_constant__ SeqMaps maps, const __grid_constant__ Se
     kt_.mark();
     const int quad = warp & 3, m = quad * 32 + lane, gid = (warp - 4) >> 2, ew = warp - 4;
     const bool lead = threadIdx.x == 128;
+    const int E1 = *reinterpret_cast<volatile int*>(p.sync) + 1;  // this launch's epoch mark
     const int T = p.T;
     int total_segs = 0;
     for (int pi = 0; pi < p.n_phases; ++pi) {
@@ -394,7 +409,7 @@ gemm_seq_kernel(const __grid_constant__ SeqMaps maps, const __grid_constant__ Se
     float pf1[kPreT], pf2[kPreT];
     bool pre_fix = false;
 
-    auto segment_epilogue = [&](const SeqPhase& P, long long u, int t, long long se, int b, long long u0) {
+    auto segment_epilogue = [&](const SeqPhase& P, int pi_cur, long long u, int t, long long se, int b, long long u0) {
       const int kb = P.kb;
       const long long ts = (long long)t * kb, te = ts + kb;
       const uint32_t t_row = tmem + (uint32_t)(b * p.NT) + ((uint32_t)(quad * 32) << 16);
@@ -475,18 +490,22 @@ gemm_seq_kernel(const __grid_constant__ SeqMaps maps, const __grid_constant__ Se
       }
     };
 
-    // residual + partial sum + RMSNorm of row r: resid_norm_kernel's arithmetic, its reduction tree
-    // replayed (virtual thread vt = 32 vw + lane, virtual warp vw on real warp vw % 8)
-    auto resid_norm_row = [&](const SeqPhase& P, int r) {
-      const int d = P.d, NG = rn_ng_dev(d), nthr = d / (4 * NG), nvw = nthr >> 5;
-      for (int vw0 = 0; vw0 < nvw; vw0 += 8) {
-        const int vw = vw0 + ew;
-        if (vw >= nvw) continue;  // (warp-uniform)
+    // residual + partial sum + RMSNorm of row r: resid_norm_kernel's arithmetic and reduction tree. The
+    // row kernel's virtual thread vt (d / 4 NG of them, 32-lane virtual warps vw) is lane vt % 32 of warp
+    // vw % 8 of the quarter task vw / 8; the quarter tasks of a row run on different CTAs (one load
+    // round trip each), publish their virtual warps' sums, and each replays the row kernel's final
+    // 32-value warp reduction on the published sums (the same values in the same order -> same bits)
+    auto rn_task = [&](const SeqPhase& P, int pi_rn, int r, int qq) {
+      const int d = P.d, NG = rn_ng_dev(d), nthr = d / (4 * NG), nvw = nthr >> 5, nq = (nvw + 7) / 8;
+      const int vw = qq * 8 + ew;
+      const bool act = vw < nvw;  // (warp-uniform)
+      float4 x[2];
+      if (act) {
         const int vt = vw * 32 + lane;
         float ss = 0.f;
         for (int j = 0; j < NG; ++j) {
           const int i = 4 * vt + 4 * nthr * j;
-          float4 x = *reinterpret_cast<const float4*>(P.resid + (size_t)r * d + i);
+          float4 xx = *reinterpret_cast<const float4*>(P.resid + (size_t)r * d + i);
           const int tile = i / BM, mm = i % BM;
           const int ns = seg_n[tile];
           const int* so = seg_off + tile * kRnMaxSeg;
@@ -499,48 +518,51 @@ gemm_seq_kernel(const __grid_constant__ SeqMaps maps, const __grid_constant__ Se
 #pragma unroll
             for (int q = 0; q < 8; ++q)
               if (q0 + q < ns) {
-                x.x += pv[q].x;
-                x.y += pv[q].y;
-                x.z += pv[q].z;
-                x.w += pv[q].w;
+                xx.x += pv[q].x;
+                xx.y += pv[q].y;
+                xx.z += pv[q].z;
+                xx.w += pv[q].w;
               }
           }
-          *reinterpret_cast<float4*>(P.out + (size_t)r * d + i) = x;
-          if (P.tap) *reinterpret_cast<float4*>(P.tap + (size_t)r * d + i) = x;
-          ss = fmaf(x.x, x.x, ss);
-          ss = fmaf(x.y, x.y, ss);
-          ss = fmaf(x.z, x.z, ss);
-          ss = fmaf(x.w, x.w, ss);
+          *reinterpret_cast<float4*>(P.out + (size_t)r * d + i) = xx;
+          if (P.tap) *reinterpret_cast<float4*>(P.tap + (size_t)r * d + i) = xx;
+          ss = fmaf(xx.x, xx.x, ss);
+          ss = fmaf(xx.y, xx.y, ss);
+          ss = fmaf(xx.z, xx.z, ss);
+          ss = fmaf(xx.w, xx.w, ss);
+          x[j & 1] = xx;
         }
         ss = warp_sum(ss);
-        if (lane == 0) red[vw] = ss;
+        if (lane == 0) seq_ss(p.sync, pi_rn, r)[vw] = ss;
       }
+      named_sync(1, 256);
+      if (lead) red_release_add(seq_rowcnt(p.sync, pi_rn, r), 1);
       if (!P.gamma) return;
+      if (lead)
+        while (ld_acquire(seq_rowcnt(p.sync, pi_rn, r)) < E1 * nq) __nanosleep(32);
       named_sync(1, 256);
       if (ew == 0) {
-        float v = (lane < nvw) ? red[lane] : 0.f;
+        float v = (lane < nvw) ? __ldcg(seq_ss(p.sync, pi_rn, r) + lane) : 0.f;
         v = warp_sum(v);
         if (lane == 0) red[32] = v;
       }
       named_sync(1, 256);
       const float rs = 1.0f / sqrtf(red[32] / (float)d + P.eps);
-      for (int vw0 = 0; vw0 < nvw; vw0 += 8) {
-        const int vw = vw0 + ew;
-        if (vw >= nvw) continue;
+      if (act) {
         const int vt = vw * 32 + lane;
         for (int j = 0; j < NG; ++j) {
           const int i = 4 * vt + 4 * nthr * j;
-          const float4 x = *reinterpret_cast<const float4*>(P.out + (size_t)r * d + i);  // (this thread's store)
+          const float4 xx = x[j & 1];
           const float4 gg = *reinterpret_cast<const float4*>(P.gamma + i);
-          __nv_bfloat162 lo = __floats2bfloat162_rn(x.x * rs * gg.x, x.y * rs * gg.y);
-          __nv_bfloat162 hi = __floats2bfloat162_rn(x.z * rs * gg.z, x.w * rs * gg.w);
+          __nv_bfloat162 lo = __floats2bfloat162_rn(xx.x * rs * gg.x, xx.y * rs * gg.y);
+          __nv_bfloat162 hi = __floats2bfloat162_rn(xx.z * rs * gg.z, xx.w * rs * gg.w);
           uint2 pk;
           pk.x = *reinterpret_cast<uint32_t*>(&lo);
           pk.y = *reinterpret_cast<uint32_t*>(&hi);
           *reinterpret_cast<uint2*>(P.xn + (size_t)r * d + i) = pk;
         }
       }
-      named_sync(1, 256);  // red is reused by the next row
+      named_sync(1, 256);  // red is reused by the next task
     };
 
     int gseg = 0;
@@ -588,7 +610,7 @@ gemm_seq_kernel(const __grid_constant__ SeqMaps maps, const __grid_constant__ Se
             mbar_wait_sleep(&accf[b], (uint32_t)(gseg / p.nbuf) & 1u);
             tc_fence_after();
             const unsigned long long ks1 = lead ? kt_now() : 0ull;
-            segment_epilogue(P, lo, t, hi, b, u0);
+            segment_epilogue(P, pi, lo, t, hi, b, u0);
             if (lead)
               kt_item(0x100000u | ((uint32_t)pi << 8) | (uint32_t)((lo == (long long)t * kb ? 1 : 0) | (hi == (long long)(t + 1) * kb ? 2 : 0)),
                       ks0, ks1, kt_now());
@@ -604,7 +626,7 @@ gemm_seq_kernel(const __grid_constant__ SeqMaps maps, const __grid_constant__ Se
       } else {
         // consumer phase: once every CTA has published the producing GEMM's partials
         if (lead)
-          while (ld_acquire(&p.done[pi - 1]) < (int)gridDim.x) __nanosleep(64);
+          while (ld_acquire(seq_done(p.sync, pi - 1)) < E1 * (int)gridDim.x) __nanosleep(64);
         // the producing GEMM's k-segment table per 128-column tile (launch_resid_norm's)
         {
           const int n128 = P.pntiles * 2;
@@ -618,7 +640,8 @@ gemm_seq_kernel(const __grid_constant__ SeqMaps maps, const __grid_constant__ Se
         named_sync(1, 256);
         if (lead) ktw = kt_now();
         if (P.kind == SEQ_RESID_NORM) {
-          for (int r = blockIdx.x; r < T; r += gridDim.x) resid_norm_row(P, r);
+          const int d = P.d, nq = (d / (4 * rn_ng_dev(d)) / 32 + 7) / 8;
+          for (int tau = blockIdx.x; tau < T * nq; tau += gridDim.x) rn_task(P, pi, tau / nq, tau % nq);
         } else {
           const RopeEpi& R = P.epi.rope;
           const int H = R.Hq + 2 * R.Hkv;
@@ -635,20 +658,18 @@ gemm_seq_kernel(const __grid_constant__ SeqMaps maps, const __grid_constant__ Se
       // this CTA's part of phase pi is in memory (barrier, then the lead's cumulative release)
       named_sync(1, 256);
       if (lead) {
-        red_release_add(&p.done[pi], 1);
+        red_release_add(seq_done(p.sync, pi), 1);
         kt_item(0x800000u | ((uint32_t)pi << 8) | (uint32_t)(blockIdx.x & 0xFF), kt0, ktw, kt_now());
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) {  // the last CTA out re-arms the completion counters for the next launch
+  if (threadIdx.x == 0) {  // the last CTA out advances the epoch (every CTA has read it by now)
+    const int E1x = *reinterpret_cast<volatile int*>(p.sync) + 1;
     int prev;
-    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(p.exit_cnt) : "memory");
-    if (prev == (int)gridDim.x - 1) {  // (visible to the next launch: kernel completion flushes)
-      for (int i = 0; i < p.n_phases; ++i) p.done[i] = 0;
-      *p.exit_cnt = 0;
-    }
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(p.sync + 1) : "memory");
+    if (prev == E1x * (int)gridDim.x - 1) st_release(p.sync, E1x);
   }
   cluster_sync();
   tc_fence_after();
@@ -679,7 +700,7 @@ bool gemm_seq_supported(int T, const SeqStep* st, int n) {
         const int n_tiles = prevN / (2 * BM), G = (int)std::min<long long>(max_groups(2), (long long)n_tiles * (st[i - 1].K / BK));
         if ((G + n_tiles - 1) / n_tiles + 1 > kRnMaxSeg || 2 * n_tiles > kRnMaxTiles) return false;
       }
-      if (s.kind == SEQ_RESID_NORM && (s.d != prevN || !rn_ng(s.d))) return false;
+      if (s.kind == SEQ_RESID_NORM && (s.d != prevN || !rn_ng(s.d) || rn_ng(s.d) > 2)) return false;
       if (s.kind == SEQ_ROPE && prevN != (s.epi.rope.Hq + 2 * s.epi.rope.Hkv) * BM) return false;
       if (s.kind != SEQ_RESID_NORM && s.kind != SEQ_ROPE) return false;
       prev_mode = -1;
@@ -688,9 +709,8 @@ bool gemm_seq_supported(int T, const SeqStep* st, int n) {
   return true;
 }
 
-cudaError_t gemm_seq_launch(int T, const SeqStep* st, int n, const GemmScratch& scratch, int* done, int* exit_cnt,
-                            cudaStream_t stream) {
-  if (!gemm_seq_supported(T, st, n) || !ensure_encode() || !done || !exit_cnt) return cudaErrorInvalidValue;
+cudaError_t gemm_seq_launch(int T, const SeqStep* st, int n, const GemmScratch& scratch, int* sync, cudaStream_t stream) {
+  if (!gemm_seq_supported(T, st, n) || !ensure_encode() || !sync) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -720,8 +740,7 @@ cudaError_t gemm_seq_launch(int T, const SeqStep* st, int n, const GemmScratch& 
   p.npre = std::max(1, std::min(env_npre, p.stages));
   p.partial = scratch.partial;
   p.flags = scratch.counters;
-  p.done = done;
-  p.exit_cnt = exit_cnt;
+  p.sync = sync;
   p.n_phases = n;
   const int Gmax = max_groups(2);
   if (!scratch.partial || scratch.partial_elems < (int64_t)2 * Gmax * 2 * p.Tp * BM || scratch.n_counters < Gmax * 2)

@@ -152,7 +152,7 @@ struct Plan {
   // offsets
   int64_t o_k, o_v, o_bt, o_rope, o_resid, o_xn, o_qkv, o_qrot, o_attn, o_ffn, o_taps, o_ctx, o_idrow, o_D,
       o_hlast, o_logits, o_dlogits, o_apo, o_apml, o_gpart, o_gcnt, o_amv, o_ami, o_ints, o_prompt, o_acnt,
-      o_tpbuf, o_tpkey;
+      o_tpbuf, o_tpkey, o_seqsync;
   int64_t n_acnt;
   int64_t gpart_elems, n_amrows;
   int64_t total;
@@ -234,6 +234,7 @@ Plan make_plan(const sf_config* c) {
   p.o_prompt = take((int64_t)p.B * c->max_seq * 4);
   p.o_tpbuf = p.tp > 1 ? take((int64_t)p.R * p.d * 4) : 0;   // row-parallel GEMM output, all-reduced
   p.o_tpkey = bf ? take(p.n_amrows * 8) : 0;  // packed (logit, id) argmax keys (fused LM-head argmax; TP max-reduces them)
+  p.o_seqsync = bf ? take((int64_t)p.L * kSeqSyncInts * 4) : 0;  // layer-sequence launches' sync blocks (zeroed)
   p.total = o;
   return p;
 }
@@ -273,6 +274,7 @@ struct sf_handle {
   float *resid, *qrot, *taps, *ctx, *idrow, *D, *hlast, *logits, *dlogits, *apo, *apml, *gpart, *amv;
   void *xn, *qkv, *attn, *ffn;
   int *gcnt, *ami, *acnt;
+  int* seqsync = nullptr;  // [L][kSeqSyncInts] (layer_seq)
   // tensor parallelism: row-parallel GEMM output / argmax keys, and the collective that reduces them
   float* tpbuf = nullptr;
   unsigned long long* tpkey = nullptr;
@@ -664,7 +666,7 @@ static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const i
 // switches call for the standalone path.
 static int seq_T() {
   const char* e = getenv("SF_SEQ_T");  // (read per call: tests compare both paths)
-  return e ? atoi(e) : 0;  // (off by default until it measures faster than the standalone launches)
+  return e ? atoi(e) : 32;  // measured: faster up to T = 20 (B = 4 at k = 4), slower from T = 40
 }
 static bool layer_seq(sf_handle* h, cudaError_t* err, int l, int T, int q_len, const int* pos0, float* tap,
                       const float* next_g) {
@@ -717,10 +719,9 @@ static bool layer_seq(sf_handle* h, cudaError_t* err, int l, int T, int q_len, c
   sc.partial = h->gpart;
   sc.partial_elems = p.gpart_elems;
   sc.counters = h->gcnt;
-  sc.n_counters = 2048;  // (2048.. : the layer-sequence completion counters)
-  int* done = h->gcnt + 2048 + (l % 96) * 16;
+  sc.n_counters = 4096;
   h->launches++;
-  *err = dbg_sync(h, "layer_seq", gemm_seq_launch(T, st, n, sc, done, done + 15, h->st));
+  *err = dbg_sync(h, "layer_seq", gemm_seq_launch(T, st, n, sc, h->seqsync + (size_t)l * kSeqSyncInts, h->st));
   return true;
 }
 
@@ -1201,6 +1202,7 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
   h->ami = (int*)(w + p.o_ami);
   h->tpbuf = p.tp > 1 ? (float*)(w + p.o_tpbuf) : nullptr;
   h->tpkey = h->bf ? (unsigned long long*)(w + p.o_tpkey) : nullptr;
+  h->seqsync = h->bf ? (int*)(w + p.o_seqsync) : nullptr;
   int* ip = (int*)(w + p.o_ints);
   auto ints = [&](int n) {
     int* r = ip;
@@ -1230,6 +1232,7 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
   e = cudaMemcpyAsync(h->bt, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice, h->st);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->gcnt, 0, 4096 * 4, h->st);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->acnt, 0, (size_t)p.n_acnt * 4, h->st);
+  if (e == cudaSuccess && h->seqsync) e = cudaMemsetAsync(h->seqsync, 0, (size_t)p.L * kSeqSyncInts * 4, h->st);
   // whole 16-key pages are staged by TMA: never-written slots must hold finite values (masked keys
   // get probability exactly 0, and 0 * finite = 0)
   if (e == cudaSuccess) e = cudaMemsetAsync(h->kpool, 0, (size_t)p.kv_layer_bytes * (p.L + 1), h->st);
@@ -1744,11 +1747,12 @@ sf_status sf_bench_gemm(int32_t impl, int32_t T, int32_t N, int32_t K, int32_t r
   if (T < 1 || N < 256 || K < 64 || reps < 1 || !ms_out) return SF_ERR_ARG;
   void *A = nullptr, *W = nullptr;
   float* part = nullptr;
-  int* cnt = nullptr;
+  int *cnt = nullptr, *sync = nullptr;
   const int64_t pe = gemm_partial_elems(true, std::min(T, 512), N, K);
   if (cudaMalloc(&A, (size_t)T * K * 2) || cudaMalloc(&W, (size_t)N * K * 2) || cudaMalloc((void**)&part, pe * 4) ||
-      cudaMalloc((void**)&cnt, 4096 * 4))
+      cudaMalloc((void**)&cnt, 4096 * 4) || cudaMalloc((void**)&sync, kSeqSyncInts * 4))
     return SF_ERR_CUDA;
+  cudaMemset(sync, 0, kSeqSyncInts * 4);
   cudaMemset(A, 0, (size_t)T * K * 2);
   cudaMemset(W, 0, (size_t)N * K * 2);
   cudaMemset(cnt, 0, 4096 * 4);
@@ -1770,8 +1774,7 @@ sf_status sf_bench_gemm(int32_t impl, int32_t T, int32_t N, int32_t K, int32_t r
   cudaError_t err = cudaSuccess;
   for (int r = -2; r < reps; ++r) {
     if (r == 0) cudaEventRecord(e0, st);
-    err = impl == 0 ? gemm_launch(true, A, K, W, true, T, N, K, e, sc, st)
-                    : gemm_seq_launch(T, &step, 1, sc, cnt + 2048, cnt + 2048 + 15, st);
+    err = impl == 0 ? gemm_launch(true, A, K, W, true, T, N, K, e, sc, st) : gemm_seq_launch(T, &step, 1, sc, sync, st);
     if (err != cudaSuccess) break;
   }
   cudaEventRecord(e1, st);
@@ -1786,6 +1789,7 @@ sf_status sf_bench_gemm(int32_t impl, int32_t T, int32_t N, int32_t K, int32_t r
   cudaFree(W);
   cudaFree(part);
   cudaFree(cnt);
+  cudaFree(sync);
   return err == cudaSuccess ? SF_OK : SF_ERR_CUDA;
 }
 
