@@ -129,12 +129,15 @@ class KVCache:
             self.V[l] = self.V[l][:, :n]
 
 
-def _attn(W, prefix, x, pos, cache, layer, causal=True, slot_causal=False):
+def _attn(W, prefix, x, pos, cache, layer, causal=True, slot_causal=False, ctx_prefix=None):
     """Multi-head attention sub-block on normalised input x [T, d].
     With `cache`: RoPE at absolute positions, append K/V, attend causally over the
     cached prefix + the new rows (query i at position p_i sees keys at <= p_i).
     Without cache (draft block, P204): no RoPE, all-to-all over the T rows -- or, with
     slot_causal (the "+Att Mask" ablation, T4 P497-514), row i sees rows <= i only.
+    ctx_prefix = (K, V, n) (the BIDIR_PREFIX draft variant): the T draft slots sit
+    at positions n..n+T-1 (queries and keys rotated there) and every slot sees the n cached
+    context-layer keys [Hkv, n, hd] (positions 0..n-1) and all T slots.
     GQA: query head h reads kv head floor(h * Hkv / Hq)."""
     c = W.cfg
     T = x.shape[0]
@@ -142,7 +145,15 @@ def _attn(W, prefix, x, pos, cache, layer, causal=True, slot_causal=False):
     q = (x @ W[prefix + "wq"].T).reshape(T, hq, hd)
     k = (x @ W[prefix + "wk"].T).reshape(T, hkv, hd)
     v = (x @ W[prefix + "wv"].T).reshape(T, hkv, hd)
-    if cache is not None:
+    if ctx_prefix is not None:
+        PK, PV, n = ctx_prefix
+        spos = n + np.arange(T)
+        q = rope(q, spos, c.rope_theta)
+        k = rope(k, spos, c.rope_theta)
+        K = np.concatenate([PK[:, :n], k.transpose(1, 0, 2)], axis=1)
+        V = np.concatenate([PV[:, :n], v.transpose(1, 0, 2)], axis=1)
+        mask = np.ones((T, n + T), dtype=bool)
+    elif cache is not None:
         q = rope(q, pos, c.rope_theta)
         k = rope(k, pos, c.rope_theta)
         cache.append(layer, k, v, int(pos[0]))
@@ -207,32 +218,40 @@ def context_layer(W, taps, pos0, cache):
 
 def positional_ffn(W, i_d):
     """Positional FFN, Eq.9 (P189-193): D = W_P RMS(I_D) + b_P, W_P: d -> l_d*d,
-    reshaped so slot j takes output rows [j*d, (j+1)*d). i_d: [d] -> D: [k, d]."""
+    reshaped so slot j takes output rows [j*d, (j+1)*d). i_d: [d] -> D: [k, d].
+    cfg.no_pos_ffn (the T4 "-Pos" ablation, P499 / P189 -- DESIGN.md §3 reading): W_P removed, each
+    slot gets the same normalised row plus its own position vector, D_j = RMS(I_D) + b_P[j]
+    ("assigning a basic mask per position")."""
     c = W.cfg
-    y = W["sf.w_p"] @ rms_norm(i_d, W["sf.pos_norm"], c.rms_eps) + W["sf.b_p"]
+    r = rms_norm(i_d, W["sf.pos_norm"], c.rms_eps)
+    if getattr(c, "no_pos_ffn", False):
+        return np.tile(r, c.draft_len).reshape(c.draft_len, c.d_model) + W["sf.b_p"].reshape(c.draft_len, c.d_model)
+    y = W["sf.w_p"] @ r + W["sf.b_p"]
     return y.reshape(c.draft_len, c.d_model)
 
 
-def draft_block(W, D, slot_causal=False):
+def draft_block(W, D, slot_causal=False, ctx_prefix=None):
     """Draft Bi-directional Attention layer, Eq.10 (P197-204):
         E = (SwiGLU . RMS + I)((SA . RMS + I)(D)),
     SA unmasked along the l_d draft slots, no positional encoding (reading C6).
     slot_causal: the T4 "+Att Mask" ablation (P497-514) -- slot j attends slots <= j.
     cfg.draft_blocks > 1: the T4 "+Larger" ablation read as that many such layers applied in turn
-    (weights sf.blk_* then sf.blk<i>_*). D: [k, d] -> E: [k, d]."""
+    (weights sf.blk_* then sf.blk<i>_*). ctx_prefix: the BIDIR_PREFIX variant (see _attn).
+    D: [k, d] -> E: [k, d]."""
     eps = W.cfg.rms_eps
     E = D
     for i in range(max(1, getattr(W.cfg, "draft_blocks", 1))):
         b = "sf.blk_" if i == 0 else f"sf.blk{i}_"
-        Y = E + _attn(W, b, rms_norm(E, W[b + "attn_norm"], eps), None, None, None, slot_causal=slot_causal)
+        Y = E + _attn(W, b, rms_norm(E, W[b + "attn_norm"], eps), None, None, None, slot_causal=slot_causal,
+                      ctx_prefix=ctx_prefix)
         E = Y + swiglu(rms_norm(Y, W[b + "ffn_norm"], eps), W[b + "w_gate"], W[b + "w_up"], W[b + "w_down"])
     return E
 
 
-def draft_logits(W, i_d, slot_causal=False):
+def draft_logits(W, i_d, slot_causal=False, ctx_prefix=None):
     """Draft logits for one context row: positional FFN -> draft block -> frozen base
     final norm + LM head, shared (reading C8). Returns [k, V]."""
-    E = draft_block(W, positional_ffn(W, i_d), slot_causal)
+    E = draft_block(W, positional_ffn(W, i_d), slot_causal, ctx_prefix)
     return rms_norm(E, W["final_norm"], W.cfg.rms_eps) @ W["lm_head"].T
 
 
@@ -256,6 +275,15 @@ def accept(draft, greedy):
 # --------------------------------------------------------------------------- loops
 def _new_cache(c):
     return KVCache(c.n_layers + 1, c.n_kv_heads, c.head_dim)
+
+
+def _ctx_prefix(W, cache, n):
+    """The BIDIR_PREFIX draft variant's prefix: the context layer's (layer L) cached K / V of the n
+    committed positions; None for the paper's draft block."""
+    if not getattr(W.cfg, "draft_prefix", False):
+        return None
+    L = W.cfg.n_layers
+    return cache.K[L][:, :n], cache.V[L][:, :n], n
 
 
 def prefill(W, prompt, cache):
@@ -305,7 +333,7 @@ def sd_decode(W, prompt, n_tokens, draft_fn=None, record=False, step_times=None)
         t_step = time.perf_counter() if step_times is not None else 0.0
         dl = None
         if draft_fn is None:
-            dl = draft_logits(W, i_d)
+            dl = draft_logits(W, i_d, ctx_prefix=_ctx_prefix(W, cache, n))
             dr = [argmax_lowest(r) for r in dl]
         else:
             dr = [int(t) for t in draft_fn(len(steps), n, list(out))]
@@ -341,7 +369,7 @@ def replay(W, prompt, gpu_steps, slot_causal=False):
     n = P
     res = []
     for st in gpu_steps:
-        dl = draft_logits(W, i_d, slot_causal)
+        dl = draft_logits(W, i_d, slot_causal, _ctx_prefix(W, cache, n))
         dr = [int(t) for t in st["draft"]]
         logits, taps = base_forward(W, [int(st["last"])] + dr, n, cache)
         m = int(st["m"])

@@ -26,6 +26,8 @@ class ModelConfig:
     gen_len: int
     kv_block: int = 16
     draft_blocks: int = 1   # NEXT-2 "+Larger" (T4): stacked draft blocks, weights sf.blk<i>_* for i >= 1
+    no_pos_ffn: bool = False   # NEXT-2 "-Pos" (T4): no W_P, D_j = RMS(I_D) + b_P[j]
+    draft_prefix: bool = False  # NEXT-2 BIDIR_PREFIX: draft slots also attend the context layer's cache
     rope_theta: float = 10000.0
     rms_eps: float = 1e-6
 

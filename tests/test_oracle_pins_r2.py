@@ -123,3 +123,81 @@ def test_next_draft_row_is_fresh_prefill_last_row(corrupt):
         g0, i_d_fresh, _ = O.prefill(W, committed, cache)
         np.testing.assert_allclose(s["i_d"], i_d_fresh, rtol=1e-10, atol=1e-12)
         assert g0 == ([ar[0]] + out)[-1]  # and its greedy token is the committed last token
+
+
+# ------------------------------------------------------------------ NEXT-2 variants: "-Pos", BIDIR_PREFIX
+VAR = get_config("tiny").replace(name="var", n_layers=2, d_model=16, n_heads=4, n_kv_heads=2, head_dim=4,
+                                 d_ff=20, vocab=41, draft_len=3, prompt_len=6, gen_len=12)
+
+
+def _w64(cfg, seed, **kw):
+    return {k: v.double().numpy() for k, v in make_weights(cfg, seed=seed, norm_jitter=0.1, **kw).items()}
+
+
+def test_no_pos_ffn_is_identity_stack_plus_bias():
+    """"-Pos" (T4 P499; reading: W_P removed, D_j = RMS(I_D) + b_P[j]) equals Eq.9 with W_P replaced by k
+    stacked identities -- and with b_P = 0 every slot is the same row, so the (permutation-equivariant)
+    bidirectional block gives k identical draft-logit rows."""
+    cfg = VAR.replace(no_pos_ffn=True)
+    w = _w64(cfg, 5)
+    i_d = np.random.default_rng(6).normal(size=cfg.d_model)
+    D = O.positional_ffn(O.Weights(cfg, w), i_d)
+    w_id = dict(w)
+    w_id["sf.w_p"] = np.tile(np.eye(cfg.d_model), (cfg.draft_len, 1))
+    np.testing.assert_allclose(D, O.positional_ffn(O.Weights(VAR, w_id), i_d), rtol=1e-13, atol=1e-15)
+    w0 = dict(w)
+    w0["sf.b_p"] = np.zeros_like(w["sf.b_p"])
+    dl = O.draft_logits(O.Weights(cfg, w0), i_d)
+    for j in range(1, cfg.draft_len):
+        np.testing.assert_allclose(dl[j], dl[0], rtol=1e-12, atol=1e-13)
+    assert not np.allclose(O.draft_logits(O.Weights(cfg, w), i_d)[1], O.draft_logits(O.Weights(cfg, w), i_d)[0])
+
+
+def test_draft_prefix_attention_brute_force_and_zero_prefix_closed_form():
+    """BIDIR_PREFIX (reading: the draft slots sit at positions n..n+k-1, rotated there, and
+    every slot sees the context layer's n cached keys and all k slots): one head against scalar loops;
+    with a zero prefix (K = V = 0) the output is the closed form sum_j e^s_j v_j / (n + sum_j e^s_j)."""
+    cfg = VAR.replace(draft_prefix=True)
+    W = O.Weights(cfg, _w64(cfg, 7))
+    rng = np.random.default_rng(8)
+    k, n, hd = cfg.draft_len, 5, cfg.head_dim
+    x = rng.normal(size=(k, cfg.d_model))
+    PK, PV = rng.normal(size=(2, n, hd)), rng.normal(size=(2, n, hd))  # [Hkv, n, hd] each
+    out = OM._attn(W, "sf.blk_", x, None, None, None, ctx_prefix=(PK, PV, n)) @ np.linalg.pinv(W["sf.blk_wo"].T)
+    q = O.rope((x @ W["sf.blk_wq"].T).reshape(k, 4, hd), n + np.arange(k), cfg.rope_theta)
+    kk = O.rope((x @ W["sf.blk_wk"].T).reshape(k, 2, hd), n + np.arange(k), cfg.rope_theta)
+    v = (x @ W["sf.blk_wv"].T).reshape(k, 2, hd)
+    for h in range(4):
+        g = h // 2
+        keys = [PK[g, j] for j in range(n)] + [kk[j, g] for j in range(k)]
+        vals = [PV[g, j] for j in range(n)] + [v[j, g] for j in range(k)]
+        for i in range(k):
+            sc = [sum(q[i, h, c] * kv[c] for c in range(hd)) / math.sqrt(hd) for kv in keys]
+            mx = max(sc)
+            e = [math.exp(t - mx) for t in sc]
+            exp = [sum(e[j] * vals[j][c] for j in range(n + k)) / sum(e) for c in range(hd)]
+            np.testing.assert_allclose(out[i, h * hd:(h + 1) * hd], exp, rtol=1e-9, atol=1e-11)
+    Z = np.zeros((2, n, hd))
+    out0 = OM._attn(W, "sf.blk_", x, None, None, None, ctx_prefix=(Z, Z, n)) @ np.linalg.pinv(W["sf.blk_wo"].T)
+    for h in range(4):
+        g = h // 2
+        for i in range(k):
+            sc = [float(q[i, h] @ kk[j, g]) / math.sqrt(hd) for j in range(k)]
+            num = sum(math.exp(s) * v[j, g] for j, s in enumerate(sc))
+            np.testing.assert_allclose(out0[i, h * hd:(h + 1) * hd], num / (n + sum(math.exp(s) for s in sc)),
+                                       rtol=1e-9, atol=1e-11)
+
+
+@pytest.mark.parametrize("variant", [dict(no_pos_ffn=True), dict(draft_prefix=True),
+                                     dict(no_pos_ffn=True, draft_prefix=True)], ids=["nopos", "prefix", "both"])
+def test_variants_stay_lossless(variant):
+    """The variants change the drafts only: SD output == AR output exactly (P25), and with the prefix
+    variant the draft depends on the committed context (different drafts than the paper's block)."""
+    cfg = VAR.replace(**variant)
+    w = _w64(cfg, 9)
+    prompt = make_prompts(1, cfg.prompt_len, cfg.vocab, seed=10)[0].tolist()
+    W = O.Weights(cfg, w)
+    toks, steps = O.sd_decode(W, prompt, cfg.gen_len, record=True)
+    assert toks == O.decode_greedy(W, prompt, cfg.gen_len)
+    base = O.sd_decode(O.Weights(VAR, w), prompt, cfg.gen_len, record=True)[1]
+    assert not np.allclose(steps[0]["draft_logits"], base[0]["draft_logits"])
