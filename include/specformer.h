@@ -62,6 +62,15 @@ typedef enum { SF_FP32 = 0, SF_BF16 = 1 } sf_dtype;
  * from the argmax fused into their epilogue either way); specformer_read_logits then
  * returns SF_ERR_STATE. */
 #define SF_FLAG_NO_LOGITS   (1ull << 2)
+/* NEXT-2 ablation "-Pos" (T4, PAPER P497-514; reading in DESIGN.md §3): no positional FFN matrix -- each
+ * draft slot is D_j = RMS_p(I_D) + b_P[j] (the weight table has no sf.w_p). Not the default. */
+#define SF_FLAG_NO_POS_FFN  (1ull << 3)
+/* NEXT-2 variant BIDIR_PREFIX (the north_star's wording: "draft slots attend causally over the prefix KV
+ * cache and bidirectionally among themselves"; reading in DESIGN.md §3): the draft block's slots sit at
+ * positions seq_len .. seq_len + k - 1 (RoPE'd there; their K / V written to the context layer's pages
+ * beyond the committed length) and every slot sees the context layer's committed keys and all k slots.
+ * Not the default; bf16 / fp32, no tensor parallelism. */
+#define SF_FLAG_DRAFT_PREFIX (1ull << 4)
 
 typedef struct {
   int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab;

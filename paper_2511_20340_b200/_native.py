@@ -19,6 +19,8 @@ SF_FP32, SF_BF16 = 0, 1
 SF_FLAG_CUDA_GRAPH = 1 << 0
 SF_FLAG_DRAFT_CAUSAL = 1 << 1
 SF_FLAG_NO_LOGITS = 1 << 2
+SF_FLAG_NO_POS_FFN = 1 << 3
+SF_FLAG_DRAFT_PREFIX = 1 << 4
 
 
 class sf_config(C.Structure):

@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
     it.b = r / p.Hkv;
     const int r0 = it.qt * 16;
     const int nr = min(16, R - r0);
-    const int kmax = min(p.pos0[it.b] + min(p.q_len - 1, (r0 + nr - 1) / G), p.max_key - 1);
+    const int kmax = min(p.pos0[it.b] + attn_row_last(p, min(p.q_len - 1, (r0 + nr - 1) / G)), p.max_key - 1);
     const int nch = kmax / CH + 1;
     it.nseg = (nch + seg_ch - 1) / seg_ch;
     it.c0 = split ? it.seg * seg_ch : 0;
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
         qa[kk][2 + hr] = ok ? qrow[(d0 + 8) / 2] : 0u;
       }
     }
-    const int pos_lo = base + (r0 + g) / G, pos_hi = base + (r0 + g + 8) / G;
+    const int pos_lo = base + attn_row_last(p, (r0 + g) / G), pos_hi = base + attn_row_last(p, (r0 + g + 8) / G);
     const bool row_lo = g < nr, row_hi = g + 8 < nr;
     float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;  // log2-domain running max
     float o[16][4];

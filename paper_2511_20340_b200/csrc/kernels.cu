@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(128) attn_partial_kernel(AttnParams p) {
   const int nr = min(QT, R - r0);
   const int base = p.pos0[b];
   const int kstart = c * kAttnChunk;
-  const int kmax = base + min(p.q_len - 1, (r0 + nr - 1) / G);  // largest position among this tile's rows
+  const int kmax = base + attn_row_last(p, min(p.q_len - 1, (r0 + nr - 1) / G));  // largest visible key of the tile
   if (kstart > kmax) return;
   const int nk = min(kAttnChunk, kmax + 1 - kstart);
   const int tid = threadIdx.x;
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(128) attn_partial_kernel(AttnParams p) {
 #pragma unroll
     for (int r = 0; r < QT; ++r) {
       if (r < nr) {
-        const int pos = base + (r0 + r) / G;
+        const int pos = base + attn_row_last(p, (r0 + r) / G);
         const bool vis = (j < nk) && (kstart + j <= pos);
         S[r * kAttnChunk + j] = vis ? acc[r] * scale : -INFINITY;
       }
@@ -516,7 +516,7 @@ __global__ void attn_combine_kernel(AttnParams p) {
   pdl_trigger();
   const int t = blockIdx.x, h = blockIdx.y;
   const int b = t / p.q_len, qi = t % p.q_len;
-  const int pos = p.pos0[b] + qi;
+  const int pos = p.pos0[b] + attn_row_last(p, qi);
   const int nc = pos / kAttnChunk + 1;
   const size_t o0 = ((size_t)t * p.Hq + h) * p.nchunk_max;
   float M = -INFINITY;
@@ -591,6 +591,31 @@ __global__ void __launch_bounds__(128) bidir_attn_kernel(const TA* qkv, int k, i
 }
 
 // ------------------------------------------------------------------------ gather
+// "-Pos" (T4 ablation, DESIGN.md §3 reading): every draft slot gets the normalised context row plus its
+// own position vector. One CTA per sequence; fixed reduction tree (blockDim 256).
+__global__ void __launch_bounds__(256) pos_broadcast_kernel(const float* src, const float* gamma, const float* bias,
+                                                            int k, int d, float eps, float* D) {
+  KtScope kt_(KT_GATHER, (uint32_t)(d));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
+  __shared__ float red[32];
+  const int b = blockIdx.x;
+  const float* x = src + (size_t)b * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss = fmaf(x[i], x[i], ss);
+  ss = block_sum_dyn(ss, red);
+  const float r = 1.0f / sqrtf(ss / (float)d + eps);
+  for (int j = 0; j < k; ++j)
+    for (int i = threadIdx.x; i < d; i += blockDim.x)
+      D[((size_t)b * k + j) * d + i] = x[i] * r * gamma[i] + bias[(size_t)j * d + i];
+}
+cudaError_t launch_pos_broadcast(const float* src, const float* gamma, const float* bias, int B, int k, int d, float eps,
+                                 float* D, cudaStream_t s) {
+  launch_k(pos_broadcast_kernel, dim3(B), dim3(256), 0, s, src, gamma, bias, k, d, eps, D);
+  return cudaGetLastError();
+}
+
 __global__ void gather_rows_kernel(const float* src, int q_len, const int* idx, int const_idx, int d, float* dst) {
   KtScope kt_(KT_GATHER, (uint32_t)(d));
   pdl_wait();
@@ -842,8 +867,8 @@ cudaError_t launch_group_rms(bool bf, const float* taps, int64_t tap_stride, con
 }
 cudaError_t launch_rope_append(bool bf, const void* qkv, int T, int q_len, const int* pos0, const float2* rope,
                                int Hq, int Hkv, int hd, const int* bt, int pps, void* Kp, void* Vp, void* q_out,
-                               bool q_bf16, cudaStream_t s) {
-  if (bf && q_bf16 && hd == 128) {
+                               bool q_bf16, cudaStream_t s, bool pair_rows) {
+  if (bf && q_bf16 && hd == 128 && pair_rows) {
     const int items = T * (Hq + 2 * Hkv);
     const int grid = std::max(1, std::min((items + 15) / 16, 148 * 4));
     return launch_k(rope_append128_kernel, dim3(grid), dim3(256), 0, s, (const __nv_bfloat16*)qkv, T, q_len, pos0, rope,

@@ -21,7 +21,13 @@ struct AttnParams {
   int max_key;               // upper bound of pos0[b] + q_len (grid sizing), <= max_seq
   int n_pages;               // pages in the pool (TMA tensor-map extent)
   int* seg_cnt;              // [B * Hkv * query tiles] zeroed arrival counters (bf16 hd=128 kernel)
+  // 0: CAUSAL_PREFIX (row i of sequence b sees keys <= pos0[b] + i); 1: BIDIR_PREFIX (every row of
+  // sequence b sees keys <= pos0[b] + q_len - 1: the whole prefix and all of the block's rows; the
+  // NEXT-2 draft mask variant)
+  int bidir_tail;
 };
+// last key position row qi of a sequence may see, relative to pos0
+__host__ __device__ inline int attn_row_last(const AttnParams& p, int qi) { return p.bidir_tail ? p.q_len - 1 : qi; }
 
 constexpr int kAttnChunk = 128;  // fixed absolute key-chunk size (split-KV boundaries, C23)
 constexpr int kAttnSeg = 2048;   // flash-decoding key segment (fixed absolute bounds; defines the arithmetic)
@@ -41,11 +47,14 @@ cudaError_t launch_group_rms(bool is_bf16, const float* taps, int64_t tap_stride
 // q_bf16: rotated queries written as bf16 (the flash-decoding attention's operand precision)
 cudaError_t launch_rope_append(bool is_bf16, const void* qkv, int T, int q_len, const int* pos0,
                                const float2* rope, int Hq, int Hkv, int hd, const int* block_table,
-                               int pages_per_seq, void* Kp, void* Vp, void* q_out, bool q_bf16, cudaStream_t s);
+                               int pages_per_seq, void* Kp, void* Vp, void* q_out, bool q_bf16, cudaStream_t s, bool pair_rows = true);
 cudaError_t launch_attention(bool is_bf16, const AttnParams& p, cudaStream_t s);
 cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s);   // bf16, hd 128 (flash-decoding)
 cudaError_t launch_bidir_attention(bool is_bf16, const void* qkv, int B, int k, int Hq, int Hkv, int hd,
                                    bool causal, void* out, cudaStream_t s);
+// "-Pos" draft variant (NEXT-2): D[b k + j] = RMS(src[b]) * gamma + bias[j d .. (j+1) d) (fp32 rows)
+cudaError_t launch_pos_broadcast(const float* src, const float* gamma, const float* bias, int B, int k, int d, float eps,
+                                 float* D, cudaStream_t s);
 cudaError_t launch_gather_rows(const float* src, int q_len, const int* idx, int const_idx, int B, int d,
                                float* dst, cudaStream_t s);
 cudaError_t launch_argmax(const float* logits, int R, int V, float* pval, int* pidx, int* out, int* err,

@@ -68,6 +68,8 @@ bool valid_config(const sf_config* c, std::string* why) {
     if (c->vocab % 128 || c->vocab / 128 < tp) return fail("vocab must be a multiple of 128 with >= tp_size tiles");
   }
   if (c->d_ff % 64) return fail("d_ff must be a multiple of 64 (interleaved gate/up groups)");
+  if (c->tp_size > 1 && (c->flags & (SF_FLAG_NO_POS_FFN | SF_FLAG_DRAFT_PREFIX)))
+    return fail("the -Pos / BIDIR_PREFIX draft variants are single-GPU");
   if (c->dtype == SF_BF16) {
     const int qkv = (c->n_heads + 2 * c->n_kv_heads) * c->head_dim;
     if (c->d_model % 128 || qkv % 128 || (2 * c->d_ff) % 128 || c->vocab % 128 ||
@@ -122,7 +124,7 @@ std::vector<TensorSpec> tensor_specs(const sf_config* c) {
     t.push_back({"sf.ctx_wqkv", {qkv, d}, true});
     t.push_back({"sf.ctx_wo", {d, ao}, true});
     t.push_back({"sf.pos_norm", {d}, false});
-    t.push_back({"sf.w_p", {k * d, d}, true});
+    if (!(c->flags & SF_FLAG_NO_POS_FFN)) t.push_back({"sf.w_p", {k * d, d}, true});
     t.push_back({"sf.b_p", {k * d}, false});
     for (int i = 0; i < draft_blocks(c); ++i) {  // block 0: "sf.blk_*", block i > 0: "sf.blk<i>_*"
       const std::string b = i == 0 ? "sf.blk_" : "sf.blk" + std::to_string(i) + "_";
@@ -866,11 +868,19 @@ static cudaError_t do_draft(sf_handle* h) {
     h->ctx_pending = false;
   }
   // positional FFN (Eq.9): D = W_P RMS(I_D) + b_P  -> [B, k*d] == [B*k, d]
-  if ((e = rmsnorm(h, h->idrow, p.d, h->pos_norm, B, h->xn, p.d))) return e;
   const int Tk = B * k;
+  if (h->c.flags & SF_FLAG_NO_POS_FFN) {
+    // "-Pos" (NEXT-2): D_j = RMS_p(I_D) + b_P[j]; xn = RMS_1(D)
+    h->launches += 2;
+    if ((e = launch_pos_broadcast(h->idrow, h->pos_norm, h->b_p, B, k, p.d, h->c.rms_eps, h->D, h->st))) return e;
+    if ((e = rmsnorm(h, h->D, p.d, h->blk_attn_norm, Tk, h->xn, p.d))) return e;
+  } else if ((e = rmsnorm(h, h->idrow, p.d, h->pos_norm, B, h->xn, p.d))) {
+    return e;
+  }
   // D = W_P RMS_p(I_D) + b_P viewed as [B*k, d]; xn = RMS_1(D)
-  if (!gemm_resid_norm(h, &e, h->xn, p.d, h->w_p, B, k * p.d, p.d, k, nullptr, h->b_p, h->D, nullptr,
-                       h->blk_attn_norm)) {
+  if ((h->c.flags & SF_FLAG_NO_POS_FFN)) {
+  } else if (!gemm_resid_norm(h, &e, h->xn, p.d, h->w_p, B, k * p.d, p.d, k, nullptr, h->b_p, h->D, nullptr,
+                              h->blk_attn_norm)) {
     GemmEpi eb;
     eb.mode = EPI_BIAS_F32;
     eb.out = h->D;
@@ -885,10 +895,41 @@ static cudaError_t do_draft(sf_handle* h) {
   for (size_t bi = 0; bi < h->blks.size(); ++bi) {
     const auto& bw = h->blks[bi];
     if ((e = gemm(h, h->xn, p.d, bw.wqkv, Tk, p.qkvw, p.d, epi_act(h->qkv, p.qkvw)))) return e;
-    if ((e = launch_bidir_attention(h->bf, h->qkv, B, k, p.Hq, p.Hkv, p.hd, (h->c.flags & SF_FLAG_DRAFT_CAUSAL) != 0,
-                                    h->attn, h->st)))
-      return e;
-    h->launches++;
+    if (h->c.flags & SF_FLAG_DRAFT_PREFIX) {
+      // BIDIR_PREFIX (NEXT-2): slots at positions seq_len..seq_len+k-1 of the context layer's pages (beyond
+      // the committed length: the next context pass overwrites them), every slot sees the committed keys
+      // and all k slots. The draft block's q|k|v rows are in natural order (no RoPE pairing).
+      if ((e = launch_rope_append(h->bf, h->qkv, Tk, k, h->seq_len, h->rope, p.Hq, p.Hkv, p.hd, h->bt, p.pps,
+                                  h->kp(p.L), h->vp(p.L), h->qrot, h->bf && p.hd == 128, h->st, false)))
+        return e;
+      AttnParams ap{};
+      ap.q = h->qrot;
+      ap.Kp = h->kp(p.L);
+      ap.Vp = h->vp(p.L);
+      ap.block_table = h->bt;
+      ap.pages_per_seq = p.pps;
+      ap.pos0 = h->seq_len;
+      ap.q_len = k;
+      ap.B = B;
+      ap.Hq = p.Hq;
+      ap.Hkv = p.Hkv;
+      ap.hd = p.hd;
+      ap.nchunk_max = p.nchunk;
+      ap.part_o = h->apo;
+      ap.part_ml = h->apml;
+      ap.seg_cnt = h->acnt;
+      ap.out = h->attn;
+      ap.max_key = h->c.max_seq;
+      ap.n_pages = p.n_pages;
+      ap.bidir_tail = 1;
+      h->launches += 2;
+      if ((e = launch_attention(h->bf, ap, h->st))) return e;
+    } else {
+      if ((e = launch_bidir_attention(h->bf, h->qkv, B, k, p.Hq, p.Hkv, p.hd, (h->c.flags & SF_FLAG_DRAFT_CAUSAL) != 0,
+                                      h->attn, h->st)))
+        return e;
+      h->launches++;
+    }
     if (!gemm_resid_norm(h, &e, h->attn, p.ao, bw.wo, Tk, p.d, p.ao, 1, h->D, nullptr, h->D, nullptr, bw.ffn_norm,
                          true)) {
       if ((e = gemm(h, h->attn, p.ao, bw.wo, Tk, p.d, p.ao, epi_add(h->D, p.d, nullptr)))) return e;
@@ -1306,6 +1347,14 @@ sf_status specformer_draft_step(sf_handle* h, int32_t* draft, float* draft_logit
   if (h->state != ST_READY) return set_err(h, SF_ERR_STATE, "draft_step needs prefill or accept_commit first");
   if (draft_logits && (h->c.flags & SF_FLAG_NO_LOGITS))
     return set_err(h, SF_ERR_STATE, "logits not kept (SF_FLAG_NO_LOGITS)");
+  if ((h->c.flags & SF_FLAG_DRAFT_PREFIX) && h->host_len_hi + h->p.k > h->c.max_seq) {
+    // the BIDIR_PREFIX slots occupy positions seq_len .. seq_len + k - 1 of the context layer's pages
+    std::vector<int> sl(h->B);
+    SF_TRY(cudaMemcpyAsync(sl.data(), h->seq_len, (size_t)h->B * 4, cudaMemcpyDeviceToHost, h->st));
+    SF_TRY(cudaStreamSynchronize(h->st));
+    h->host_len_hi = *std::max_element(sl.begin(), sl.end());
+    if (h->host_len_hi + h->p.k > h->c.max_seq) return set_err(h, SF_ERR_CAPACITY, "seq_len + k > max_seq");
+  }
   h->launches = 0;
   SF_TRY(do_draft(h));
   SF_TRY(copy_out(h, draft, h->draft, (size_t)h->B * h->p.k * 4));

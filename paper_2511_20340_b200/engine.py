@@ -39,6 +39,9 @@ class EngineConfig:
     @classmethod
     def from_model(cls, m, max_batch=None, max_seq=None, draft_len=None, flags=0, tp_size=1, tp_rank=0):
         """Build from any object with the model-shape attributes (e.g. synth.ModelConfig)."""
+        # the NEXT-2 draft variants of the model config map to their flags
+        flags |= (N.SF_FLAG_NO_POS_FFN if getattr(m, "no_pos_ffn", False) else 0) | \
+            (N.SF_FLAG_DRAFT_PREFIX if getattr(m, "draft_prefix", False) else 0)
         return cls(m.n_layers, m.d_model, m.n_heads, m.n_kv_heads, m.head_dim, m.d_ff, m.vocab,
                    m.draft_len if draft_len is None else draft_len, max_batch or m.batch,
                    max_seq or m.max_seq, m.dtype, m.rope_theta, m.rms_eps, m.kv_block, flags, tp_size, tp_rank,

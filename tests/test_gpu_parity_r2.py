@@ -371,3 +371,31 @@ def test_layer_seq_bit_exact(cfg, monkeypatch):
         for key in ("logits", "draft_logits", "greedy", "m", "emitted", "seq_len", "last_token"):
             assert np.array_equal(s1[key], s2[key]), key
     check_commit_integers(cfg, prompts, on)
+
+
+# ------------------------------------------------------------------ NEXT-2 draft variants
+VARIANTS = [dict(no_pos_ffn=True), dict(draft_prefix=True), dict(no_pos_ffn=True, draft_prefix=True)]
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("base,fp32,seqs", [(TINY.replace(batch=2), True, (0, 1)), (MID, False, (0, 3)),
+                                            (GQA, False, (0, 2))], ids=["tiny_fp32", "mha128", "gqa4"])
+@pytest.mark.parametrize("variant", VARIANTS, ids=["nopos", "prefix", "both"])
+def test_draft_variants_match_oracle(base, fp32, seqs, variant):
+    """NEXT-2 "-Pos" (SF_FLAG_NO_POS_FFN) and BIDIR_PREFIX (SF_FLAG_DRAFT_PREFIX; the slots also attend the
+    context layer's committed keys, at a different n every step under ragged forced acceptance) against
+    the oracle's variant head (DESIGN.md §3 readings), step by step; the verify and accept are unchanged
+    (tokens == the GPU's AR continuation)."""
+    cfg = base.replace(**variant)
+    w, prompts = setup(cfg, seed=29, jitter=0.0 if fp32 else 0.1)
+    k, n_steps = cfg.draft_len, 6
+    ar = run_gpu(cfg, w, prompts, n_steps * (k + 1) + k + 2, k=0)["tokens"]
+    slots = corrupt_slots(n_steps, cfg.batch, k, seed=9)
+    res = forced_run(cfg, w, prompts, n_steps, slots, ar)
+    check_commit_integers(cfg, prompts, res)
+    for b in range(cfg.batch):
+        assert res["tokens"][b] == ar[b][:len(res["tokens"][b])]
+    assert check_against_oracle(cfg, w, prompts, res, seqs, fp32) > 10
+    # free-running SD with the variant's own drafts is still lossless on the device
+    sd = run_gpu(cfg, w, prompts, 16)
+    assert sd["tokens"] == [a[:16] for a in ar]
