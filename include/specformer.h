@@ -71,6 +71,13 @@ typedef enum { SF_FP32 = 0, SF_BF16 = 1 } sf_dtype;
  * beyond the committed length) and every slot sees the context layer's committed keys and all k slots.
  * Not the default; bf16 / fp32, no tensor parallelism. */
 #define SF_FLAG_DRAFT_PREFIX (1ull << 4)
+/* NEXT-4: KV pages come from a device-side pool of sf_config.pool_pages pages (0: max_batch x
+ * max_seq / 16) instead of fixed per-sequence ranges: a sequence takes pages just before it writes them
+ * (prefill: P + k + 1 positions; each accept_commit: up to seq_len + k + 1, fused into the accept kernel)
+ * and returns them with specformer_release; specformer_prefill_slot admits a new sequence into a released
+ * slot while the others keep decoding (continuous batching, PAPER P18). An exhausted pool is a sticky
+ * SF_ERR_CAPACITY at specformer_sync. */
+#define SF_FLAG_PAGE_POOL   (1ull << 5)
 
 typedef struct {
   int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab;
@@ -88,6 +95,8 @@ typedef struct {
   uint64_t flags;
   int32_t draft_blocks; /* bidirectional draft blocks (Eq.10 has one; 0 reads as 1). NEXT-2 "+Larger"
                            (T4 P497-514): 2..4 stacked blocks, weights sf.blk<i>_* for i >= 1 */
+  int32_t pool_pages;   /* SF_FLAG_PAGE_POOL: KV pages in the pool (0: max_batch x max_seq / 16); the
+                           per-layer KV pools are sized to it */
 } sf_config;
 
 typedef struct {
@@ -150,6 +159,16 @@ sf_status specformer_accept_commit(sf_handle* h, int32_t* accept_len, int32_t* e
  * when SF_FLAG_CUDA_GRAPH). emitted_log (dev, [n_steps, B, k+1]) and accept_log (dev,
  * [n_steps, B]) may be NULL. Fails with SF_ERR_CAPACITY if a step could overflow max_seq. */
 sf_status specformer_decode_steps(sf_handle* h, int32_t n_steps, int32_t* emitted_log, int32_t* accept_log);
+
+/* SF_FLAG_PAGE_POOL only (NEXT-4, continuous batching). specformer_release returns sequence slot's KV
+ * pages to the pool; the slot must then be re-filled with specformer_prefill_slot before the next
+ * draft / verify / decode call (SF_ERR_STATE otherwise). specformer_prefill_slot runs the prefill of one
+ * new sequence (tokens dev or host [P]) into slot (< the batch of the last specformer_prefill) while the
+ * other slots keep their state: seq_len[slot] = P, first_token (dev or host [1], may be NULL) = g0.
+ * Errors: SF_ERR_UNSUPPORTED without the flag, SF_ERR_STATE before the first batch prefill or between
+ * verify and accept, SF_ERR_SHAPE for a bad slot / P, SF_ERR_CAPACITY if P + k + 1 > max_seq. */
+sf_status specformer_release(sf_handle* h, int32_t slot);
+sf_status specformer_prefill_slot(sf_handle* h, int32_t slot, const int32_t* tokens, int32_t P, int32_t* first_token);
 
 /* Stream sync + sticky device error flags -> status. */
 sf_status specformer_sync(sf_handle* h);

@@ -21,6 +21,7 @@ SF_FLAG_DRAFT_CAUSAL = 1 << 1
 SF_FLAG_NO_LOGITS = 1 << 2
 SF_FLAG_NO_POS_FFN = 1 << 3
 SF_FLAG_DRAFT_PREFIX = 1 << 4
+SF_FLAG_PAGE_POOL = 1 << 5
 
 
 class sf_config(C.Structure):
@@ -29,7 +30,7 @@ class sf_config(C.Structure):
                 ("draft_len", C.c_int32), ("max_batch", C.c_int32), ("max_seq", C.c_int32),
                 ("kv_block", C.c_int32), ("rope_theta", C.c_float), ("rms_eps", C.c_float),
                 ("dtype", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32), ("flags", C.c_uint64),
-                ("draft_blocks", C.c_int32)]
+                ("draft_blocks", C.c_int32), ("pool_pages", C.c_int32)]
 
 
 class sf_tensor_desc(C.Structure):
@@ -49,6 +50,8 @@ SIGNATURES = [
     ("specformer_draft_step", C.c_int, [_P, _P, _P]),
     ("specformer_verify_step", C.c_int, [_P, _P, _P, _P]),
     ("specformer_accept_commit", C.c_int, [_P, _P, _P, _P]),
+    ("specformer_release", C.c_int, [_P, C.c_int32]),
+    ("specformer_prefill_slot", C.c_int, [_P, C.c_int32, _P, C.c_int32, _P]),
     ("specformer_decode_steps", C.c_int, [_P, C.c_int32, _P, _P]),
     ("specformer_sync", C.c_int, [_P]),
     ("specformer_last_error", C.c_char_p, [_P]),

@@ -729,9 +729,72 @@ __global__ void argmax_unkey_kernel(unsigned long long* keys, int R, int* out, i
 
 // ------------------------------------------------------------------------ accept + commit
 // P25: accept only drafts equal to the base model's greedy outputs. Single CTA (B <= 1024).
+// ------------------------------------------------------------------------ KV page pool (NEXT-4)
+// A stack of free page ids (pool[0..*top)) shared by the handle's sequences; sequence b's logical page i
+// is bt[b pps + i] for i < alloc_cnt[b]. Pages are taken just before positions are written: up to
+// position need_pos - 1 (prefill: P + k + 1; after each commit: seq_len + k + 1, the next verify's
+// block). An empty pool sets the sticky capacity bit (err |= 2) and leaves the sequence short.
+SF_DEV void page_take(int b, int need_pos, const PagePool& pp) {
+  const int need = min(pp.pps, (need_pos + 15) / 16);
+  int have = pp.alloc_cnt[b];
+  while (have < need) {
+    const int t = atomicSub(pp.top, 1) - 1;
+    if (t < 0) {
+      atomicAdd(pp.top, 1);
+      atomicOr(pp.err, 2);
+      break;
+    }
+    pp.bt[b * pp.pps + have] = pp.pool[t];
+    ++have;
+  }
+  pp.alloc_cnt[b] = have;
+}
+__global__ void page_take_kernel(int b0, int nb, const int* seq_len, int extra, PagePool pp) {
+  KtScope kt_(KT_MISC, (uint32_t)(6));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nb) page_take(b0 + i, (seq_len ? seq_len[b0 + i] : 0) + extra, pp);
+}
+__global__ void page_release_kernel(int b0, int nb, PagePool pp) {
+  KtScope kt_(KT_MISC, (uint32_t)(7));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nb) return;
+  const int b = b0 + i, cnt = pp.alloc_cnt[b];
+  const int t = atomicAdd(pp.top, cnt);
+  for (int j = 0; j < cnt; ++j) pp.pool[t + j] = pp.bt[b * pp.pps + j];
+  pp.alloc_cnt[b] = 0;
+}
+__global__ void page_reset_kernel(int n_pages, int B, PagePool pp) {
+  KtScope kt_(KT_MISC, (uint32_t)(8));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_pages) pp.pool[i] = n_pages - 1 - i;  // (the stack hands out pages 0, 1, 2, ... first)
+  if (i < B) pp.alloc_cnt[i] = 0;
+  if (i == 0) *pp.top = n_pages;
+}
+cudaError_t launch_page_take(int b0, int nb, const int* seq_len, int extra, const PagePool& pp, cudaStream_t s) {
+  launch_k(page_take_kernel, dim3((nb + 127) / 128), dim3(128), 0, s, b0, nb, seq_len, extra, pp);
+  return cudaGetLastError();
+}
+cudaError_t launch_page_release(int b0, int nb, const PagePool& pp, cudaStream_t s) {
+  launch_k(page_release_kernel, dim3((nb + 127) / 128), dim3(128), 0, s, b0, nb, pp);
+  return cudaGetLastError();
+}
+cudaError_t launch_page_reset(int n_pages, int B, const PagePool& pp, cudaStream_t s) {
+  launch_k(page_reset_kernel, dim3((std::max(n_pages, B) + 255) / 256), dim3(256), 0, s, n_pages, B, pp);
+  return cudaGetLastError();
+}
+
 __global__ void accept_kernel(int B, int k, const int* draft, const int* greedy, int* seq_len, int* n_prev,
                               int* last_token, int* r_b, int* accept_len, int* emitted, int* step_counter,
-                              int* accept_log, int* emitted_log, const int* log_cap_dev) {
+                              int* accept_log, int* emitted_log, const int* log_cap_dev, PagePool pp) {
   KtScope kt_(KT_ACCEPT, (uint32_t)(k));
   pdl_wait();
   kt_.mark();
@@ -754,6 +817,7 @@ __global__ void accept_kernel(int B, int k, const int* draft, const int* greedy,
     seq_len[b] += m + 1;
     last_token[b] = g[m];
     r_b[b] = m;
+    if (pp.pool) page_take(b, seq_len[b] + k + 1, pp);  // pages for the next verify block
   }
   __syncthreads();
   if (threadIdx.x == 0 && step_counter) *step_counter = step + 1;
@@ -994,10 +1058,10 @@ cudaError_t launch_argmax(const float* logits, int R, int V, float* pval, int* p
 }
 cudaError_t launch_accept(int B, int k, const int* draft, const int* greedy, int* seq_len, int* n_prev,
                           int* last_token, int* r_b, int* accept_len, int* emitted, int* step_counter,
-                          int* accept_log, int* emitted_log, const int* log_cap, cudaStream_t s) {
+                          int* accept_log, int* emitted_log, const int* log_cap, const PagePool& pp, cudaStream_t s) {
   const int th = ((B + 31) / 32) * 32;
   launch_k(accept_kernel, dim3(1), dim3(th), 0, s, B, k, draft, greedy, seq_len, n_prev, last_token, r_b, accept_len, emitted,
-                                 step_counter, accept_log, emitted_log, log_cap);
+                                 step_counter, accept_log, emitted_log, log_cap, pp);
   return cudaGetLastError();
 }
 cudaError_t launch_force_drafts(int B, int k, int V, const int* cont, int cont_len, const int* corrupt,

@@ -68,9 +68,21 @@ cudaError_t launch_argmax_unkey(unsigned long long* keys, int R, int* out, cudaS
 // buffer order
 cudaError_t launch_reduce_bufs(const void* const* bufs, int n, int64_t count, bool max_u64, void* out,
                                cudaStream_t s);
+// KV page pool (NEXT-4; csrc/kernels.cu): all pointers null = static per-sequence page ranges
+struct PagePool {
+  int* pool = nullptr;       // [n_pages] free page ids, a stack
+  int* top = nullptr;        // [1] stack height
+  int* alloc_cnt = nullptr;  // [B] pages held by each sequence (bt[b pps + i], i < alloc_cnt[b])
+  int* bt = nullptr;         // [B, pps] page table
+  int* err = nullptr;        // sticky error flags (bit 1: pool exhausted)
+  int pps = 0;
+};
+cudaError_t launch_page_take(int b0, int nb, const int* seq_len, int extra, const PagePool& pp, cudaStream_t s);
+cudaError_t launch_page_release(int b0, int nb, const PagePool& pp, cudaStream_t s);
+cudaError_t launch_page_reset(int n_pages, int B, const PagePool& pp, cudaStream_t s);
 cudaError_t launch_accept(int B, int k, const int* draft, const int* greedy, int* seq_len, int* n_prev,
                           int* last_token, int* r_b, int* accept_len, int* emitted, int* step_counter,
-                          int* accept_log, int* emitted_log, const int* log_cap /* device */, cudaStream_t s);
+                          int* accept_log, int* emitted_log, const int* log_cap /* device */, const PagePool& pp, cudaStream_t s);
 cudaError_t launch_force_drafts(int B, int k, int V, const int* cont, int cont_len, const int* corrupt,
                                 int corrupt_steps, const int* seq_len, const int* prompt_len,
                                 const int* step_counter, int* draft, cudaStream_t s);

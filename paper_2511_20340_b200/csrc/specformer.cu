@@ -68,6 +68,7 @@ bool valid_config(const sf_config* c, std::string* why) {
     if (c->vocab % 128 || c->vocab / 128 < tp) return fail("vocab must be a multiple of 128 with >= tp_size tiles");
   }
   if (c->d_ff % 64) return fail("d_ff must be a multiple of 64 (interleaved gate/up groups)");
+  if (c->pool_pages < 0) return fail("pool_pages must be >= 0");
   if (c->tp_size > 1 && (c->flags & (SF_FLAG_NO_POS_FFN | SF_FLAG_DRAFT_PREFIX)))
     return fail("the -Pos / BIDIR_PREFIX draft variants are single-GPU");
   if (c->dtype == SF_BF16) {
@@ -150,11 +151,12 @@ struct Plan {
   int B, k, d, Hq, Hkv, hd, F, V, L, qkvw, ao;  // Hq, Hkv, F, V: this rank's share (tensor parallelism)
   int tp, tp_rank, V_full, v0, wd_k;            // ranks, full vocabulary, vocab shard offset, W_D input width
   int pps, n_pages, nchunk, rows_v, rows_d, C_pf, rows_pf, R;
+  bool pool;  // SF_FLAG_PAGE_POOL: pages from a device-side free-page stack
   int64_t act, kv_layer_bytes;
   // offsets
   int64_t o_k, o_v, o_bt, o_rope, o_resid, o_xn, o_qkv, o_qrot, o_attn, o_ffn, o_taps, o_ctx, o_idrow, o_D,
       o_hlast, o_logits, o_dlogits, o_apo, o_apml, o_gpart, o_gcnt, o_amv, o_ami, o_ints, o_prompt, o_acnt,
-      o_tpbuf, o_tpkey, o_seqsync;
+      o_tpbuf, o_tpkey, o_seqsync, o_pool;
   int64_t n_acnt;
   int64_t gpart_elems, n_amrows;
   int64_t total;
@@ -181,7 +183,8 @@ Plan make_plan(const sf_config* c) {
   p.ao = p.Hq * p.hd;
   p.act = c->dtype == SF_BF16 ? 2 : 4;
   p.pps = c->max_seq / 16;
-  p.n_pages = p.B * p.pps;
+  p.pool = (c->flags & SF_FLAG_PAGE_POOL) != 0;
+  p.n_pages = (p.pool && c->pool_pages > 0) ? c->pool_pages : p.B * p.pps;
   p.nchunk = (c->max_seq + kAttnChunk - 1) / kAttnChunk;
   p.rows_v = p.B * (p.k + 1);
   p.rows_d = std::max(1, p.B * p.k);
@@ -208,7 +211,8 @@ Plan make_plan(const sf_config* c) {
   };
   p.o_k = take(p.kv_layer_bytes * (p.L + 1));
   p.o_v = take(p.kv_layer_bytes * (p.L + 1));
-  p.o_bt = take((int64_t)p.n_pages * 4);
+  p.o_bt = take((int64_t)p.B * p.pps * 4);
+  p.o_pool = take((int64_t)(p.n_pages + p.B + 8) * 4);  // free-page stack, per-sequence page counts, stack top
   p.o_rope = take((int64_t)c->max_seq * (p.hd / 2) * 8);
   p.o_resid = take((int64_t)p.R * p.d * 4);
   p.o_xn = take((int64_t)p.R * 4 * p.d * p.act);
@@ -277,6 +281,8 @@ struct sf_handle {
   void *xn, *qkv, *attn, *ffn;
   int *gcnt, *ami, *acnt;
   int* seqsync = nullptr;  // [L][kSeqSyncInts] (layer_seq)
+  PagePool pp;                 // NEXT-4 page pool (null pointers: static per-sequence page ranges)
+  std::vector<char> released;  // slots released and not yet re-filled (page pool)
   // tensor parallelism: row-parallel GEMM output / argmax keys, and the collective that reduces them
   float* tpbuf = nullptr;
   unsigned long long* tpkey = nullptr;
@@ -972,9 +978,15 @@ static cudaError_t do_accept(sf_handle* h, int* acc_log, int* em_log) {
   const Plan& p = h->p;
   h->launches++;
   cudaError_t e = launch_accept(h->B, p.k, h->draft, h->greedy, h->seq_len, h->n_prev, h->last_token, h->r_b,
-                                h->accept_len, h->emitted, h->step_counter, acc_log, em_log, h->d_logcap, h->st);
+                                h->accept_len, h->emitted, h->step_counter, acc_log, em_log, h->d_logcap, h->pp, h->st);
   if (p.k > 0) h->ctx_pending = true;
   return e;
+}
+
+static bool any_released(const sf_handle* h) {
+  for (char r : h->released)
+    if (r) return true;
+  return false;
 }
 
 static cudaError_t copy_out(sf_handle* h, void* dst, const void* src, size_t bytes) {
@@ -1267,10 +1279,22 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
   h->g_pf = ints(p.B);
   h->prompt = (int*)(w + p.o_prompt);
   cudaError_t e = cudaSuccess;
-  // page table: identity (sequence b owns pages [b*pps, (b+1)*pps)); tests may permute it
-  std::vector<int> bt(p.n_pages);
-  for (int i = 0; i < p.n_pages; ++i) bt[i] = i;
+  // page table: identity (sequence b owns pages [b*pps, (b+1)*pps)); tests may permute it. With the page
+  // pool, entries are filled as pages are taken.
+  std::vector<int> bt((size_t)p.B * p.pps);
+  for (size_t i = 0; i < bt.size(); ++i) bt[i] = p.pool ? 0 : (int)i;
   e = cudaMemcpyAsync(h->bt, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice, h->st);
+  if (p.pool) {
+    int* pw = (int*)(w + p.o_pool);
+    h->pp.pool = pw;
+    h->pp.alloc_cnt = pw + p.n_pages;
+    h->pp.top = pw + p.n_pages + p.B;
+    h->pp.bt = h->bt;
+    h->pp.err = h->err;
+    h->pp.pps = p.pps;
+    h->released.assign(p.B, 0);
+    if (e == cudaSuccess) e = launch_page_reset(p.n_pages, p.B, h->pp, h->st);
+  }
   if (e == cudaSuccess) e = cudaMemsetAsync(h->gcnt, 0, 4096 * 4, h->st);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->acnt, 0, (size_t)p.n_acnt * 4, h->st);
   if (e == cudaSuccess && h->seqsync) e = cudaMemsetAsync(h->seqsync, 0, (size_t)p.L * kSeqSyncInts * 4, h->st);
@@ -1292,6 +1316,7 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
 sf_status sf_debug_set_block_table(sf_handle* h, const int32_t* table_host, int32_t B, int32_t n_pages_per_seq) {
   if (!h || !table_host) return SF_ERR_ARG;
   if (h->state != ST_INIT) return set_err(h, SF_ERR_STATE, "block table can only be set before prefill");
+  if (h->p.pool) return set_err(h, SF_ERR_UNSUPPORTED, "the page pool owns the block table");
   if (B != h->p.B || n_pages_per_seq != h->p.pps) return set_err(h, SF_ERR_SHAPE, "block table shape");
   std::vector<char> seen(h->p.n_pages, 0);
   for (int i = 0; i < B * n_pages_per_seq; ++i) {
@@ -1319,6 +1344,11 @@ sf_status specformer_prefill(sf_handle* h, const int32_t* tokens, int32_t B, int
   const Plan& p = h->p;
   SF_TRY(cudaMemcpyAsync(h->prompt, tokens, (size_t)B * P * 4, cudaMemcpyDefault, h->st));
   SF_TRY(cudaMemsetAsync(h->err, 0, 4, h->st));
+  if (p.pool) {  // a new batch: every page back to the pool, then the prompts' pages (+ the first verify block)
+    SF_TRY(launch_page_reset(p.n_pages, p.B, h->pp, h->st));
+    SF_TRY(launch_page_take(0, B, nullptr, P + p.k + 1, h->pp, h->st));
+    std::fill(h->released.begin(), h->released.end(), 0);
+  }
   if (h->tpkey) SF_TRY(cudaMemsetAsync(h->tpkey, 0, (size_t)p.n_amrows * 8, h->st));
   const int C = p.C_pf;
   int Cc = 0;
@@ -1345,6 +1375,7 @@ sf_status specformer_draft_step(sf_handle* h, int32_t* draft, float* draft_logit
   if (!h) return SF_ERR_ARG;
   if (h->p.k == 0) return set_err(h, SF_ERR_UNSUPPORTED, "draft_len == 0 (AR mode) has no draft head");
   if (h->state != ST_READY) return set_err(h, SF_ERR_STATE, "draft_step needs prefill or accept_commit first");
+  if (any_released(h)) return set_err(h, SF_ERR_STATE, "a released slot must be re-filled (specformer_prefill_slot)");
   if (draft_logits && (h->c.flags & SF_FLAG_NO_LOGITS))
     return set_err(h, SF_ERR_STATE, "logits not kept (SF_FLAG_NO_LOGITS)");
   if ((h->c.flags & SF_FLAG_DRAFT_PREFIX) && h->host_len_hi + h->p.k > h->c.max_seq) {
@@ -1369,6 +1400,7 @@ sf_status specformer_verify_step(sf_handle* h, const int32_t* draft_in, int32_t*
   if (logits && (h->c.flags & SF_FLAG_NO_LOGITS)) return set_err(h, SF_ERR_STATE, "logits not kept (SF_FLAG_NO_LOGITS)");
   const bool ok_state = h->state == ST_DRAFTED || (h->state == ST_READY && (k == 0 || draft_in));
   if (!ok_state) return set_err(h, SF_ERR_STATE, "verify_step needs a draft (draft_step or draft_in)");
+  if (any_released(h)) return set_err(h, SF_ERR_STATE, "a released slot must be re-filled (specformer_prefill_slot)");
   if (h->host_len_hi + k + 1 > h->c.max_seq) {
     // refresh the host bound from the device lengths before failing
     std::vector<int> sl(h->B);
@@ -1409,6 +1441,61 @@ sf_status specformer_accept_commit(sf_handle* h, int32_t* accept_len, int32_t* e
   return SF_OK;
 }
 
+sf_status specformer_release(sf_handle* h, int32_t slot) {
+  if (!h) return SF_ERR_ARG;
+  if (!h->p.pool) return set_err(h, SF_ERR_UNSUPPORTED, "specformer_release needs SF_FLAG_PAGE_POOL");
+  if (h->state != ST_READY) return set_err(h, SF_ERR_STATE, "release needs prefill or accept_commit first");
+  if (slot < 0 || slot >= h->B) return set_err(h, SF_ERR_SHAPE, "slot out of range");
+  if (h->released[slot]) return SF_OK;
+  SF_TRY(launch_page_release(slot, 1, h->pp, h->st));
+  h->released[slot] = 1;
+  return SF_OK;
+}
+
+sf_status specformer_prefill_slot(sf_handle* h, int32_t slot, const int32_t* tokens, int32_t P, int32_t* first_token) {
+  if (!h || !tokens) return SF_ERR_ARG;
+  const Plan& p = h->p;
+  if (!p.pool) return set_err(h, SF_ERR_UNSUPPORTED, "specformer_prefill_slot needs SF_FLAG_PAGE_POOL");
+  if (h->state != ST_READY || h->B == 0) return set_err(h, SF_ERR_STATE, "prefill_slot needs a batch prefill first");
+  if (slot < 0 || slot >= h->B) return set_err(h, SF_ERR_SHAPE, "slot out of range");
+  if (P < 1) return set_err(h, SF_ERR_SHAPE, "empty prompt");
+  if (P + p.k + 1 > h->c.max_seq) return set_err(h, SF_ERR_CAPACITY, "prompt exceeds max_seq");
+  h->launches = 0;
+  if (!h->released[slot]) SF_TRY(launch_page_release(slot, 1, h->pp, h->st));
+  if (p.k > 0 && h->ctx_pending) {
+    // the other sequences' pending context pass (over the last verify's rows) runs first: the slot's
+    // prefill reuses the activation buffers
+    SF_TRY(ctx_forward(h, h->B * (p.k + 1), p.k + 1, h->n_prev, h->c.max_seq));
+    SF_TRY(launch_gather_rows(h->ctx, p.k + 1, h->r_b, 0, h->B, p.d, h->idrow, h->st));
+    h->ctx_pending = false;
+  }
+  SF_TRY(cudaMemcpyAsync(h->prompt, tokens, (size_t)P * 4, cudaMemcpyDefault, h->st));
+  SF_TRY(launch_page_take(slot, 1, nullptr, P + p.k + 1, h->pp, h->st));
+  // the one-sequence prefill sees the slot's page-table row as row 0 (chunks of up to R rows)
+  int* bt_all = h->bt;
+  h->bt = bt_all + (size_t)slot * p.pps;
+  const int C = std::min(p.R, std::max(p.C_pf, 1) * std::max(1, p.B));
+  int Cc = 0;
+  cudaError_t e = cudaSuccess;
+  for (int c0 = 0; c0 < P && e == cudaSuccess; c0 += C) {
+    Cc = std::min(C, P - c0);
+    e = launch_build_prefill_rows(1, P, c0, Cc, h->prompt, h->tok_rows, h->pos0_pf, h->st);
+    if (e == cudaSuccess) e = base_forward(h, Cc, Cc, h->pos0_pf, c0 + Cc, /*final_norm=*/false);
+    if (e == cudaSuccess && p.k > 0) e = ctx_forward(h, Cc, Cc, h->pos0_pf, c0 + Cc);
+  }
+  h->bt = bt_all;
+  SF_TRY(e);
+  if (p.k > 0) SF_TRY(launch_gather_rows(h->ctx, Cc, nullptr, Cc - 1, 1, p.d, h->idrow + (size_t)slot * p.d, h->st));
+  SF_TRY(launch_gather_rows(h->resid, Cc, nullptr, Cc - 1, 1, p.d, h->hlast, h->st));
+  SF_TRY(head_argmax(h, h->hlast, 1, h->logits, h->g_pf + slot));
+  SF_TRY(launch_prefill_finish(1, P, h->g_pf + slot, h->seq_len + slot, h->n_prev + slot, h->last_token + slot,
+                               h->r_b + slot, h->prompt_len + slot, nullptr, h->st));
+  SF_TRY(copy_out(h, first_token, h->g_pf + slot, 4));
+  h->released[slot] = 0;
+  h->host_len_hi = std::max<int64_t>(h->host_len_hi, P);
+  return SF_OK;
+}
+
 static cudaError_t one_step(sf_handle* h, int* acc_log, int* em_log) {
   cudaError_t e;
   if (h->p.k > 0) {
@@ -1428,6 +1515,7 @@ sf_status specformer_decode_steps(sf_handle* h, int32_t n_steps, int32_t* emitte
   if (!h) return SF_ERR_ARG;
   if (n_steps < 0) return SF_ERR_ARG;
   if (h->state != ST_READY) return set_err(h, SF_ERR_STATE, "decode_steps needs prefill or accept_commit first");
+  if (any_released(h)) return set_err(h, SF_ERR_STATE, "a released slot must be re-filled (specformer_prefill_slot)");
   const int k = h->p.k;
   if (h->host_len_hi + (int64_t)n_steps * (k + 1) > h->c.max_seq) {
     std::vector<int> sl(h->B);
@@ -1530,6 +1618,7 @@ sf_status specformer_sync(sf_handle* h) {
   int err = 0;
   SF_TRY(cudaMemcpy(&err, h->err, 4, cudaMemcpyDeviceToHost));
   if (err & 1) return set_err(h, SF_ERR_NONFINITE, "non-finite logits");
+  if (err & 2) return set_err(h, SF_ERR_CAPACITY, "KV page pool exhausted");
 #ifdef SF_WITH_NCCL
   if (h->nccl_comm) {  // asynchronous communicator errors (a peer failed, a network / NVLink error)
     ncclResult_t ar = ncclSuccess;

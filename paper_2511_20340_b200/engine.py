@@ -35,6 +35,7 @@ class EngineConfig:
     tp_size: int = 1             # tensor parallelism (include/specformer.h): ranks, this rank
     tp_rank: int = 0
     draft_blocks: int = 1        # NEXT-2 "+Larger": stacked draft blocks
+    pool_pages: int = 0          # NEXT-4 (SF_FLAG_PAGE_POOL): KV pages in the pool (0: max_batch x max_seq / 16)
 
     @classmethod
     def from_model(cls, m, max_batch=None, max_seq=None, draft_len=None, flags=0, tp_size=1, tp_rank=0):
@@ -51,7 +52,7 @@ class EngineConfig:
         return N.sf_config(self.n_layers, self.d_model, self.n_heads, self.n_kv_heads, self.head_dim, self.d_ff,
                            self.vocab, self.draft_len, self.max_batch, self.max_seq, self.kv_block,
                            self.rope_theta, self.rms_eps, N.SF_BF16 if self.dtype == "bf16" else N.SF_FP32,
-                           self.tp_size, self.tp_rank, self.flags, self.draft_blocks)
+                           self.tp_size, self.tp_rank, self.flags, self.draft_blocks, self.pool_pages)
 
     def vocab_shard(self):
         """[v0, v1): this rank's LM-head rows (whole 128-row tiles; the library's split)."""
@@ -241,6 +242,19 @@ class Engine:
 
     def sync(self):
         self._check(self.lib.specformer_sync(self.h), "sync")
+
+    def release(self, slot: int):
+        """SF_FLAG_PAGE_POOL: return sequence `slot`'s KV pages to the pool (re-fill it with prefill_slot)."""
+        self._check(self.lib.specformer_release(self.h, slot), "release")
+
+    def prefill_slot(self, slot: int, tokens: torch.Tensor):
+        """SF_FLAG_PAGE_POOL: prefill one new sequence (int32 [P]) into `slot`; returns g0 [1] (device)."""
+        tokens = tokens.to(torch.int32).contiguous()
+        first = self._i32(1)
+        self._enter()
+        self._check(self.lib.specformer_prefill_slot(self.h, slot, _ptr(tokens), tokens.numel(), _ptr(first)),
+                    "prefill_slot")
+        return first
 
     def set_block_table(self, table: torch.Tensor):
         t = table.to(torch.int32).contiguous().cpu()

@@ -399,3 +399,80 @@ def test_draft_variants_match_oracle(base, fp32, seqs, variant):
     # free-running SD with the variant's own drafts is still lossless on the device
     sd = run_gpu(cfg, w, prompts, 16)
     assert sd["tokens"] == [a[:16] for a in ar]
+
+
+# ------------------------------------------------------------------ NEXT-4: device-side KV page pool
+def _steps(eng, n, B):
+    """n eager draft -> verify -> accept steps; per step (emitted [B, k+1], logits [B, k+1, V])."""
+    out = []
+    for _ in range(n):
+        eng.draft_step()
+        g, lg = eng.verify_step(want_logits=True)
+        _, em, _ = eng.accept_commit()
+        eng.sync()
+        out.append((em.cpu().numpy(), lg.cpu().numpy()))
+    return out
+
+
+def test_page_pool_matches_static_pages_and_reports_exhaustion():
+    """SF_FLAG_PAGE_POOL (NEXT-4): pages taken from the device-side pool as sequences grow (prefill, then
+    fused into the accept kernel) give bit-identical logits / tokens to the static per-sequence ranges,
+    with the pool sized to what the run needs (oversubscribed vs max_batch x max_seq); a pool too small
+    for the run is a sticky SF_ERR_CAPACITY."""
+    cfg = MID
+    w, prompts = setup(cfg, seed=30, jitter=0.1)
+    B, k, n = cfg.batch, cfg.draft_len, 6
+    ms = max_seq_for(cfg, n * (k + 1), k)
+    stat = Engine(EngineConfig.from_model(cfg, max_batch=B, max_seq=ms), w)
+    stat.prefill(prompts.cuda())
+    ref = _steps(stat, n, B)
+    need = B * ((cfg.prompt_len + n + k + 1 + 15) // 16)  # a = 1 with random weights: one token per step
+    assert need < B * (ms // 16)
+    ec = EngineConfig.from_model(cfg, max_batch=B, max_seq=ms, flags=N.SF_FLAG_PAGE_POOL)
+    ec.pool_pages = need
+    pool = Engine(ec, w)
+    pool.prefill(prompts.cuda())
+    got = _steps(pool, n, B)
+    for (e1, l1), (e2, l2) in zip(ref, got):
+        assert np.array_equal(e1, e2) and np.array_equal(l1, l2)
+    ec_small = EngineConfig.from_model(cfg, max_batch=B, max_seq=ms, flags=N.SF_FLAG_PAGE_POOL)
+    ec_small.pool_pages = B * (cfg.prompt_len // 16)
+    small = Engine(ec_small, w)
+    small.prefill(prompts.cuda())
+    with pytest.raises(N.SpecFormerError) as e:
+        small.sync()
+    assert e.value.status == N.SF_ERR_CAPACITY
+
+
+def test_continuous_batching_prefill_slot():
+    """Continuous batching (PAPER P18; NEXT-4): after 3 steps, slot 1's sequence is released and a new
+    prompt is prefilled into it while slots 0 and 2 keep decoding. Slots 0 / 2 emit exactly the tokens
+    of an uninterrupted run; the new sequence emits the tokens and logits of a fresh one-sequence run
+    (bit-exact: batch-invariant kernels)."""
+    cfg = MID.replace(batch=3)
+    w, prompts = setup(cfg, seed=31, jitter=0.1)
+    newp = make_prompts(1, cfg.prompt_len - 37, cfg.vocab, seed=77)
+    B, k = 3, cfg.draft_len
+    ms = max_seq_for(cfg, 12 * (k + 1), k)
+    mk = lambda Bm: Engine(EngineConfig.from_model(cfg, max_batch=Bm, max_seq=ms, flags=N.SF_FLAG_PAGE_POOL), w)
+    full = mk(B)
+    full.prefill(prompts.cuda())
+    ref = _steps(full, 7, B)
+    eng = mk(B)
+    eng.prefill(prompts.cuda())
+    first = _steps(eng, 3, B)
+    eng.release(1)
+    with pytest.raises(N.SpecFormerError) as e:
+        eng.draft_step()
+    assert e.value.status == N.SF_ERR_STATE
+    g0 = eng.prefill_slot(1, newp[0].cuda())
+    after = _steps(eng, 4, B)
+    for s, (em, lg) in enumerate(first + after):
+        for b in (0, 2):
+            assert np.array_equal(em[b], ref[s][0][b]) and np.array_equal(lg[b], ref[s][1][b]), (s, b)
+    solo = mk(1)
+    sg0 = solo.prefill(newp.cuda())
+    sref = _steps(solo, 4, 1)
+    assert int(g0.cpu()[0]) == int(sg0.cpu()[0])
+    for (em, lg), (se, sl) in zip(after, sref):
+        assert np.array_equal(em[1], se[0]) and np.array_equal(lg[1], sl[0])
