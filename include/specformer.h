@@ -78,6 +78,10 @@ typedef enum { SF_FP32 = 0, SF_BF16 = 1 } sf_dtype;
  * slot while the others keep decoding (continuous batching, PAPER P18). An exhausted pool is a sticky
  * SF_ERR_CAPACITY at specformer_sync. */
 #define SF_FLAG_PAGE_POOL   (1ull << 5)
+/* Tensor parallelism: the row-parallel partial outputs are all-reduced in bf16 by default (rounded RNE
+ * from the fp32 GEMM output, summed by the collective, widened back: SURVEY 8e's volume, half the bytes
+ * of fp32); this flag all-reduces them in fp32 instead. Parity of both measured in DESIGN.md §8. */
+#define SF_FLAG_TP_F32_REDUCE (1ull << 6)
 
 typedef struct {
   int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab;

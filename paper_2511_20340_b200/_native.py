@@ -22,6 +22,7 @@ SF_FLAG_NO_LOGITS = 1 << 2
 SF_FLAG_NO_POS_FFN = 1 << 3
 SF_FLAG_DRAFT_PREFIX = 1 << 4
 SF_FLAG_PAGE_POOL = 1 << 5
+SF_FLAG_TP_F32_REDUCE = 1 << 6
 
 
 class sf_config(C.Structure):

@@ -1016,10 +1016,14 @@ struct BufList {
 };
 __global__ void reduce_bufs_kernel(BufList bl, int n, int64_t count, int max_u64, void* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
-    if (max_u64) {
+    if (max_u64 == 1) {
       unsigned long long m = 0;
       for (int q = 0; q < n; ++q) m = max(m, reinterpret_cast<const unsigned long long*>(bl.p[q])[i]);
       reinterpret_cast<unsigned long long*>(out)[i] = m;
+    } else if (max_u64 == 2) {  // bf16 sum, fp32 accumulation in rank order, one rounding
+      float a = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(bl.p[0])[i]);
+      for (int q = 1; q < n; ++q) a += __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(bl.p[q])[i]);
+      reinterpret_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(a);
     } else {
       float a = reinterpret_cast<const float*>(bl.p[0])[i];
       for (int q = 1; q < n; ++q) a += reinterpret_cast<const float*>(bl.p[q])[i];  // buffer (rank) order
@@ -1027,14 +1031,29 @@ __global__ void reduce_bufs_kernel(BufList bl, int n, int64_t count, int max_u64
     }
   }
 }
-cudaError_t launch_reduce_bufs(const void* const* bufs, int n, int64_t count, bool max_u64, void* out,
-                               cudaStream_t s) {
+cudaError_t launch_reduce_bufs(const void* const* bufs, int n, int64_t count, int mode, void* out, cudaStream_t s) {
   if (n < 1 || n > 8) return cudaErrorInvalidValue;
   BufList bl{};
   for (int q = 0; q < n; ++q) bl.p[q] = bufs[q];
   const int grid = (int)std::min<int64_t>(1184, (count + 255) / 256);
-  reduce_bufs_kernel<<<std::max(grid, 1), 256, 0, s>>>(bl, n, count, max_u64 ? 1 : 0, out);
+  reduce_bufs_kernel<<<std::max(grid, 1), 256, 0, s>>>(bl, n, count, mode, out);
   return cudaGetLastError();
+}
+// tensor parallelism, bf16 all-reduce (SF_FLAG_TP_BF16_REDUCE): the rank's fp32 row-parallel output
+// rounded to bf16 (RNE) for the collective, and the reduced bf16 sum widened back
+__global__ void cvt_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int64_t n, int to_bf) {
+  KtScope kt_(KT_MISC, (uint32_t)(9));
+  pdl_wait();
+  kt_.mark();
+  pdl_trigger();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (to_bf) out[i] = __float2bfloat16_rn(in[i]);
+    else const_cast<float*>(in)[i] = __bfloat162float(out[i]);
+  }
+}
+cudaError_t launch_cvt_f32_bf16(float* f32, __nv_bfloat16* bf, int64_t n, bool to_bf, cudaStream_t s) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(1184, (n + 255) / 256));
+  return launch_k(cvt_f32_bf16_kernel, dim3(grid), dim3(256), 0, s, (const float*)f32, bf, n, to_bf ? 1 : 0);
 }
 
 cudaError_t launch_argmax_key(const float* logits, int R, int V, int v0, float* pval, int* pidx,

@@ -66,8 +66,9 @@ cudaError_t launch_argmax_key(const float* logits, int R, int V, int v0, float* 
 cudaError_t launch_argmax_unkey(unsigned long long* keys, int R, int* out, cudaStream_t s, bool reset = false);
 // tensor parallelism, tests (one process, several handles): out[i] = sum / max over the n buffers in
 // buffer order
-cudaError_t launch_reduce_bufs(const void* const* bufs, int n, int64_t count, bool max_u64, void* out,
-                               cudaStream_t s);
+// tensor-parallel test group: out = reduction of n equal buffers (mode 0: fp32 sum, 1: u64 max, 2: bf16 sum)
+cudaError_t launch_cvt_f32_bf16(float* f32, __nv_bfloat16* bf, int64_t n, bool to_bf, cudaStream_t s);
+cudaError_t launch_reduce_bufs(const void* const* bufs, int n, int64_t count, int mode, void* out, cudaStream_t s);
 // KV page pool (NEXT-4; csrc/kernels.cu): all pointers null = static per-sequence page ranges
 struct PagePool {
   int* pool = nullptr;       // [n_pages] free page ids, a stack

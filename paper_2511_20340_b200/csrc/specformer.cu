@@ -156,7 +156,7 @@ struct Plan {
   // offsets
   int64_t o_k, o_v, o_bt, o_rope, o_resid, o_xn, o_qkv, o_qrot, o_attn, o_ffn, o_taps, o_ctx, o_idrow, o_D,
       o_hlast, o_logits, o_dlogits, o_apo, o_apml, o_gpart, o_gcnt, o_amv, o_ami, o_ints, o_prompt, o_acnt,
-      o_tpbuf, o_tpkey, o_seqsync, o_pool;
+      o_tpbuf, o_tpbf, o_tpkey, o_seqsync, o_pool;
   int64_t n_acnt;
   int64_t gpart_elems, n_amrows;
   int64_t total;
@@ -239,6 +239,7 @@ Plan make_plan(const sf_config* c) {
   p.o_ints = take((int64_t)(16 * p.B + 2 * p.R + 8 + p.rows_v * 2 + p.rows_d) * 4);
   p.o_prompt = take((int64_t)p.B * c->max_seq * 4);
   p.o_tpbuf = p.tp > 1 ? take((int64_t)p.R * p.d * 4) : 0;   // row-parallel GEMM output, all-reduced
+  p.o_tpbf = p.tp > 1 ? take((int64_t)p.R * p.d * 2) : 0;     // its bf16 form (the default all-reduce)
   p.o_tpkey = bf ? take(p.n_amrows * 8) : 0;  // packed (logit, id) argmax keys (fused LM-head argmax; TP max-reduces them)
   p.o_seqsync = bf ? take((int64_t)p.L * kSeqSyncInts * 4) : 0;  // layer-sequence launches' sync blocks (zeroed)
   p.total = o;
@@ -285,9 +286,11 @@ struct sf_handle {
   std::vector<char> released;  // slots released and not yet re-filled (page pool)
   // tensor parallelism: row-parallel GEMM output / argmax keys, and the collective that reduces them
   float* tpbuf = nullptr;
+  __nv_bfloat16* tpbf = nullptr;  // the bf16 copy that is all-reduced (unless SF_FLAG_TP_F32_REDUCE)
   unsigned long long* tpkey = nullptr;
   struct Coll {
     cudaError_t (*sum_f32)(void* ctx, float* buf, int64_t n, cudaStream_t s) = nullptr;
+    cudaError_t (*sum_bf16)(void* ctx, __nv_bfloat16* buf, int64_t n, cudaStream_t s) = nullptr;
     cudaError_t (*max_u64)(void* ctx, unsigned long long* buf, int64_t n, cudaStream_t s) = nullptr;
     void* ctx = nullptr;
     bool graph_safe = false;  // only device work is enqueued (NCCL): decode_steps may capture it
@@ -470,6 +473,14 @@ static cudaError_t tp_sum(sf_handle* h, float* buf, int64_t n) {
     return cudaErrorNotReady;
   }
   h->launches++;
+  if (!(h->c.flags & SF_FLAG_TP_F32_REDUCE)) {
+    // the row-parallel partial sums travel as bf16 (half the bytes of fp32)
+    cudaError_t e = launch_cvt_f32_bf16(buf, h->tpbf, n, true, h->st);
+    if (e == cudaSuccess) e = h->coll.sum_bf16(h->coll.ctx, h->tpbf, n, h->st);
+    if (e == cudaSuccess) e = launch_cvt_f32_bf16(buf, h->tpbf, n, false, h->st);
+    h->launches += 2;
+    return e;
+  }
   return h->coll.sum_f32(h->coll.ctx, buf, n, h->st);
 }
 static cudaError_t tp_max(sf_handle* h, unsigned long long* buf, int64_t n) {
@@ -1001,6 +1012,11 @@ static cudaError_t nccl_sum_f32(void* ctx, float* buf, int64_t n, cudaStream_t s
              ? cudaSuccess
              : cudaErrorUnknown;
 }
+static cudaError_t nccl_sum_bf16(void* ctx, __nv_bfloat16* buf, int64_t n, cudaStream_t s) {
+  return ncclAllReduce(buf, buf, (size_t)n, ncclBfloat16, ncclSum, (ncclComm_t)ctx, s) == ncclSuccess
+             ? cudaSuccess
+             : cudaErrorUnknown;
+}
 static cudaError_t nccl_max_u64(void* ctx, unsigned long long* buf, int64_t n, cudaStream_t s) {
   return ncclAllReduce(buf, buf, (size_t)n, ncclUint64, ncclMax, (ncclComm_t)ctx, s) == ncclSuccess
              ? cudaSuccess
@@ -1040,11 +1056,11 @@ struct LocalCtx {
   sf_local_group* g;
   int rank;
 };
-static cudaError_t local_reduce(void* ctx, void* buf, int64_t n, bool mx, cudaStream_t s) {
+static cudaError_t local_reduce(void* ctx, void* buf, int64_t n, int mode, cudaStream_t s) {
   LocalCtx* c = (LocalCtx*)ctx;
   sf_local_group* g = c->g;
   const int r = c->rank;
-  const size_t bytes = (size_t)n * (mx ? 8 : 4);
+  const size_t bytes = (size_t)n * (mode == 1 ? 8 : mode == 2 ? 2 : 4);
   if (g->tmp_bytes[r] < bytes) {  // (test scratch, owned by the group)
     cudaStreamSynchronize(s);
     if (g->tmp[r]) cudaFree(g->tmp[r]);
@@ -1055,7 +1071,7 @@ static cudaError_t local_reduce(void* ctx, void* buf, int64_t n, bool mx, cudaSt
   cudaEventRecord(g->ev_in[r], s);
   g->barrier();
   for (int q = 0; q < g->n; ++q) cudaStreamWaitEvent(s, g->ev_in[q], 0);
-  cudaError_t e = launch_reduce_bufs(g->bufs.data(), g->n, n, mx, g->tmp[r], s);
+  cudaError_t e = launch_reduce_bufs(g->bufs.data(), g->n, n, mode, g->tmp[r], s);
   cudaEventRecord(g->ev_mid[r], s);
   g->barrier();
   for (int q = 0; q < g->n; ++q) cudaStreamWaitEvent(s, g->ev_mid[q], 0);
@@ -1064,10 +1080,13 @@ static cudaError_t local_reduce(void* ctx, void* buf, int64_t n, bool mx, cudaSt
   return e;
 }
 static cudaError_t local_sum_f32(void* ctx, float* buf, int64_t n, cudaStream_t s) {
-  return local_reduce(ctx, buf, n, false, s);
+  return local_reduce(ctx, buf, n, 0, s);
+}
+static cudaError_t local_sum_bf16(void* ctx, __nv_bfloat16* buf, int64_t n, cudaStream_t s) {
+  return local_reduce(ctx, buf, n, 2, s);
 }
 static cudaError_t local_max_u64(void* ctx, unsigned long long* buf, int64_t n, cudaStream_t s) {
-  return local_reduce(ctx, buf, n, true, s);
+  return local_reduce(ctx, buf, n, 1, s);
 }
 
 // ================================================================= C ABI
@@ -1254,6 +1273,7 @@ sf_status specformer_init(const sf_config* cfg, void* weights_dev, void* workspa
   h->amv = (float*)(w + p.o_amv);
   h->ami = (int*)(w + p.o_ami);
   h->tpbuf = p.tp > 1 ? (float*)(w + p.o_tpbuf) : nullptr;
+  h->tpbf = p.tp > 1 ? (__nv_bfloat16*)(w + p.o_tpbf) : nullptr;
   h->tpkey = h->bf ? (unsigned long long*)(w + p.o_tpkey) : nullptr;
   h->seqsync = h->bf ? (int*)(w + p.o_seqsync) : nullptr;
   int* ip = (int*)(w + p.o_ints);
@@ -1673,6 +1693,7 @@ sf_status sf_nccl_attach(sf_handle* h, const uint8_t* id, int32_t nranks, int32_
   if (r != ncclSuccess) return set_err(h, SF_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
   h->nccl_comm = comm;
   h->coll.sum_f32 = nccl_sum_f32;
+  h->coll.sum_bf16 = nccl_sum_bf16;
   h->coll.max_u64 = nccl_max_u64;
   h->coll.ctx = comm;
   h->coll.graph_safe = true;
@@ -1714,6 +1735,7 @@ sf_status sf_local_group_attach(sf_handle* h, sf_local_group* g, int32_t rank) {
   if (g->n != h->p.tp || rank != h->p.tp_rank) return set_err(h, SF_ERR_ARG, "group size / rank differ from tp_size / tp_rank");
   if (h->coll.sum_f32) return set_err(h, SF_ERR_STATE, "a collective is already attached");
   h->coll.sum_f32 = local_sum_f32;
+  h->coll.sum_bf16 = local_sum_bf16;
   h->coll.max_u64 = local_max_u64;
   h->coll.ctx = new LocalCtx{g, rank};
   h->coll.graph_safe = false;

@@ -476,3 +476,68 @@ def test_continuous_batching_prefill_slot():
     assert int(g0.cpu()[0]) == int(sg0.cpu()[0])
     for (em, lg), (se, sl) in zip(after, sref):
         assert np.array_equal(em[1], se[0]) and np.array_equal(lg[1], sl[0])
+
+
+# ------------------------------------------------------------------ tensor parallelism: all-reduce precision
+GQA2K = get_config("70b").replace(name="70b-w2k", n_layers=2, d_model=2048, n_heads=16, n_kv_heads=4, d_ff=5632,
+                                  batch=2, prompt_len=150, gen_len=8)
+
+
+def _tp_run(cfg, w, prompts, tp, flags):
+    import threading
+
+    from paper_2511_20340_b200.engine import LocalGroup
+    group = LocalGroup(tp)
+    engines, res, errs = [], [None] * tp, []
+    for r in range(tp):
+        ec = EngineConfig.from_model(cfg, max_batch=cfg.batch, max_seq=max_seq_for(cfg, cfg.gen_len, cfg.draft_len),
+                                     tp_size=tp, tp_rank=r, flags=flags)
+        eng = Engine(ec, w)
+        eng.attach_local_group(group, r)
+        engines.append(eng)
+
+    def run(r):
+        try:
+            res[r] = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True, eng=engines[r])
+        except Exception as ex:  # pragma: no cover - reported below
+            errs.append(ex)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(tp)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    merged = {"tokens": res[0]["tokens"], "steps": []}
+    for steps in zip(*[x["steps"] for x in res]):
+        s = dict(steps[0])
+        s["logits"] = np.concatenate([x["logits"] for x in steps], axis=-1)
+        s["draft_logits"] = np.concatenate([x["draft_logits"] for x in steps], axis=-1)
+        merged["steps"].append(s)
+    for e in engines:
+        e.close()
+    group.close()
+    return merged
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("tp", [2, 4])
+def test_tp_bf16_reduce_parity(tp):
+    """SURVEY 8e specifies the row-parallel all-reduce in bf16, the default (fp32 GEMM output rounded RNE,
+    summed, widened back); SF_FLAG_TP_F32_REDUCE keeps fp32. Both stay within the bf16
+    tolerance of the fp64 oracle (reading C21, depth 2: rel-L2 <= 2.2e-2, tokens exact where the oracle
+    margin > 5e-2); the measured rel-L2 of each is printed for DESIGN.md §8 (the local group rounds the
+    bf16 sum once; a ring all-reduce rounds at every hop)."""
+    cfg = GQA2K
+    w, prompts = setup(cfg, seed=32, jitter=0.1)
+    errs = {}
+    for name, flags in (("fp32", N.SF_FLAG_TP_F32_REDUCE), ("bf16", 0)):
+        merged = _tp_run(cfg, w, prompts, tp, flags)
+        _, rep = oracle_replay(cfg, w, prompts[0].tolist(), merged["steps"], 0)
+        errs[name] = max(rel_l2(s["logits"][0].astype(np.float64), r["logits"]) for s, r in zip(merged["steps"], rep))
+        assert errs[name] <= 2.2e-2, (name, errs[name])
+        for s, r in zip(merged["steps"], rep):
+            for i in range(cfg.draft_len + 1):
+                if O.top2_margin(r["logits"][i]) > 5e-2:
+                    assert s["greedy"][0][i] == r["greedy"][i]
+    print(f"TP={tp}: logits rel-L2 vs oracle, fp32 all-reduce {errs['fp32']:.3e}, bf16 all-reduce {errs['bf16']:.3e}")
