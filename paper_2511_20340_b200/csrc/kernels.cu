@@ -1039,7 +1039,7 @@ cudaError_t launch_reduce_bufs(const void* const* bufs, int n, int64_t count, in
   reduce_bufs_kernel<<<std::max(grid, 1), 256, 0, s>>>(bl, n, count, mode, out);
   return cudaGetLastError();
 }
-// tensor parallelism, bf16 all-reduce (SF_FLAG_TP_BF16_REDUCE): the rank's fp32 row-parallel output
+// tensor parallelism, bf16 all-reduce (the default; SF_FLAG_TP_F32_REDUCE: fp32): the rank's fp32 row-parallel output
 // rounded to bf16 (RNE) for the collective, and the reduced bf16 sum widened back
 __global__ void cvt_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int64_t n, int to_bf) {
   KtScope kt_(KT_MISC, (uint32_t)(9));
