@@ -187,6 +187,10 @@ def run_reference(args, cfg):
 
 
 # --------------------------------------------------------------------------- GPU leg
+def _log(msg):
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def run_ours(args, cfg):
     import ctypes as C
 
@@ -255,8 +259,11 @@ def run_ours(args, cfg):
         with the median time and every window's time."""
         wins = []
         acc = torch.zeros(max(K, W), Bs, dtype=torch.int32, device="cuda")
-        for _ in range(n_win):
+        for wi in range(n_win):
+            _log(f"  window {wi}: prefill B={Bs}")
             eng.prefill(prompts_s.cuda())
+            eng.sync()
+            _log(f"  window {wi}: warm-up")
             eng.decode_steps(W, None, acc)  # warm-up; (re)captures the step graph the window replays
             eng.sync()
             b0 = eng.capture(3, (Bs,), torch.int32).cpu()
@@ -296,6 +303,7 @@ def run_ours(args, cfg):
             lens_t = [n + m + 1 for n, m in zip(lens_t, accs_t[s_])]
         return sb_ / tp
 
+    _log(f"timed windows B={B}")
     with ClockSampler(local) as clk:
         main = timed_windows(B, prompts, clk)
     ms = main["ms"]
@@ -434,6 +442,7 @@ def run_ours(args, cfg):
     Kt = args.timeline_steps
     tl = None
     if Kt > 0 and N.lib().sf_debug_ktrace_enable(1) == 0:
+        _log("timeline")
         lt0 = eng.capture(3, (B,), torch.int32).cpu().tolist()
         pt0 = eng.capture(5, (B,), torch.int32).cpu().tolist()
         t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -458,6 +467,7 @@ def run_ours(args, cfg):
             g_ms = g_tl["exposed_ms_per_step"] / max(1e-9, g_tl["launches_per_step"])
             tl["gemm_tflops_exposed"] = gemm_flops(B) / max(1e-9, g_tl["launches_per_step"]) / (g_ms / 1e3) / 1e12
 
+    _log("event profile")
     ev = event_profile(B)
     dominant = ev["dominant"]
     # DRAM bytes per launch of the dominant kernel class from the committed ncu launch list of this
@@ -469,7 +479,32 @@ def run_ours(args, cfg):
             traffic = json.load(open(traffic_path)).get(f"{cfg.name}_b{B}", {}).get("traffic_bytes_per_launch", {}).get(dominant)
         except Exception:
             traffic = None
+    _log("e2e")
     e2e = e2e_run(B, prompts, Ke)
+    _log("prefill")
+
+    # ---------------- prefill (untimed in the decode metric; NEXT-4): chunked base forward +
+    # context layer over the B x P prompt rows, timed with CUDA events on the engine stream
+    pf_ms = []
+    for _ in range(2):
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        q0.record(eng.stream)
+        eng.prefill(prompts.cuda())
+        q1.record(eng.stream)
+        eng.sync()
+        pf_ms.append(q0.elapsed_time(q1))
+    c_pf = max(k + 1, min(512, max(1, 512 // B)))
+    n_chunks = -(-P // c_pf)
+    pf_flops = roofline.prefill_flops(cfg, B, P, k) / tp
+    pf_bytes = roofline.prefill_bytes(cfg, B, P, k, n_chunks) / tp
+    pms = min(pf_ms)
+    pf_tc = pf_flops / (pms / 1e3) / 1e12
+    prefill = {"ms": pms, "tokens_per_s": B * P / (pms / 1e3), "chunks": n_chunks, "rows_per_chunk": B * c_pf,
+               "flops": pf_flops, "bytes": pf_bytes, "achieved_tflops": pf_tc, "frac_tensor_sustained": pf_tc / tf_sust,
+               "achieved_gbs": pf_bytes / (pms / 1e3) / 1e9,
+               "t_roof_ms": 1e3 * max(pf_flops / (tf_sust * 1e12), pf_bytes / (hbm * 1e9)),
+               "frac_roofline": 1e3 * max(pf_flops / (tf_sust * 1e12), pf_bytes / (hbm * 1e9)) / pms}
 
     # ---------------- batch sweep (BASELINE metric: verify-steps/s vs batch 1-64): the same engine
     # re-prefilled at each smaller batch; per batch the median of the timed windows, the step
@@ -478,11 +513,14 @@ def run_ours(args, cfg):
     for Bs in args.sweep_list:
         if Bs >= B or tp > 1:
             continue
+        _log(f"sweep B={Bs}")
         pr_s = prompts[:Bs].contiguous()
         win = timed_windows(Bs, pr_s)
         sb_s = window_roofline(win, Bs)
         w_ms, w_tok = dp.reduce_timing(win["ms"], float(int((win["after"] - win["before"]).sum())), device="cuda")
+        _log("  event profile")
         ev_s = event_profile(Bs)
+        _log("  e2e")
         sweep.append({"batch_per_gpu": Bs, "value": w_tok / (w_ms / 1e3), "unit": "tokens/s",
                       "ms_per_step": w_ms / K, "window_ms": win["all_ms"],
                       "verify_steps_per_s": K / (w_ms / 1e3), "mean_accepted_length": w_tok / (K * Bs * world),
@@ -500,6 +538,7 @@ def run_ours(args, cfg):
     # P(j) = alpha^(j-1) (1 - alpha) (none with alpha^k), alpha set so E[tokens/step] = a_paper
     forced = None
     if Kf:
+        _log("forced acceptance")
         a_target = A_PAPER.get(cfg.name, 1.75)
         lo, hi = 0.0, 0.999
         for _ in range(60):
@@ -554,6 +593,7 @@ def run_ours(args, cfg):
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and tp == 1:
+        _log("cpu baseline")
         try:
             cpu = oracle_sample(cfg)
         except MemoryError as ex:  # bounded sample did not fit the host
@@ -592,6 +632,7 @@ def run_ours(args, cfg):
                               "flops_per_step": ev["step_flops"],
                               "t_roof_ms": (sb / K) / (hbm * 1e9) * 1e3},
             "windows": {"n": n_win, "ms": main["all_ms"], "reported": "median"},
+            "prefill": prefill,
             "batch_sweep": sweep,
             "e2e": e2e,
             "gpu_launches": launches,

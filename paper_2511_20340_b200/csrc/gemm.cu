@@ -1590,7 +1590,8 @@ SF_DEV void rope_partial_item(const float* __restrict__ partial, int t, int h, i
   *reinterpret_cast<__nv_bfloat162*>(dst + 64 + 2 * lane) = __floats2bfloat162_rn(y20, y21);
 }
 
-// One warp per (row, head) item (persistent grid).
+// One warp per (row, head) item (persistent grid, two items in flight per warp): the arithmetic of
+// rope_partial_item (the layer-sequence kernel's consumer), with both items' loads issued first.
 __global__ void __launch_bounds__(256) rope_partial_kernel(const float* __restrict__ partial, int G, int kb, int drain,
                                                            int CG, int H, int Tslot, int T, int q_len,
                                                            const int* __restrict__ pos0, const float2* __restrict__ rope,
@@ -1598,8 +1599,8 @@ __global__ void __launch_bounds__(256) rope_partial_kernel(const float* __restri
                                                            __nv_bfloat16* Kp, __nv_bfloat16* Vp, __nv_bfloat16* q_out) {
   __shared__ int seg_n[kRnMaxTiles];
   __shared__ int seg_off[kRnMaxTiles][kRnMaxSeg];  // slot * Tslot * 128, k order
-  const int groups = G / CG, n_tiles_grp = H / CG;
   {  // geometry only (no dependency on the previous kernel)
+    const int groups = G / CG, n_tiles_grp = H / CG;
     for (int vt = threadIdx.x; vt < H; vt += blockDim.x) {
       seg_n[vt] = pseg_count(vt, groups, n_tiles_grp, kb, drain, CG);
       for (int q = 0; q < kRnMaxSeg && q < seg_n[vt]; ++q)
@@ -1611,13 +1612,68 @@ __global__ void __launch_bounds__(256) rope_partial_kernel(const float* __restri
   pdl_wait();
   kt_.mark();
   pdl_trigger();
+  const int lane = threadIdx.x & 31;
   const int nw = gridDim.x * (blockDim.x >> 5);
   const int items = T * H;
-  for (int it = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < items; it += nw) {
-    const int t = it / H, h = it % H;
-    const int* so = seg_off[h];
-    rope_partial_item(partial, t, h, seg_n[h], [&](int q) { return (size_t)so[q]; }, q_len, pos0, rope, Hq, Hkv, bt,
-                      pps, Kp, Vp, q_out);
+  for (int i0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i0 < items; i0 += 2 * nw) {
+    uint32_t a[2], bb[2];
+    float4 cs[2];
+    int t[2], h[2], pos[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int it = min(i0 + u * nw, items - 1);
+      t[u] = it / H;
+      h[u] = it % H;
+      pos[u] = pos0[t[u] / q_len] + t[u] % q_len;
+      const float* base = partial + (size_t)t[u] * BM + 4 * lane;
+      const int ns = seg_n[h[u]];
+      float4 x = __ldcg(reinterpret_cast<const float4*>(base + seg_off[h[u]][0]));
+      for (int q0 = 1; q0 < ns; q0 += 4) {  // k order; up to four loads in flight
+        float4 pv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q0 + q < ns) pv[q] = __ldcg(reinterpret_cast<const float4*>(base + seg_off[h[u]][q0 + q]));
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q0 + q < ns) {
+            x.x += pv[q].x;
+            x.y += pv[q].y;
+            x.z += pv[q].z;
+            x.w += pv[q].w;
+          }
+      }
+      // positions (4l, 4l+1, 4l+2, 4l+3) = dims (2l, 2l+64, 2l+1, 2l+65), rounded as the GEMM would
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.z);  // dims 2l, 2l+1
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(x.y, x.w);  // dims 2l+64, 2l+65
+      a[u] = *reinterpret_cast<const uint32_t*>(&lo);
+      bb[u] = *reinterpret_cast<const uint32_t*>(&hi);
+      cs[u] = *reinterpret_cast<const float4*>(rope + (size_t)pos[u] * 64 + 2 * lane);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (i0 + u * nw >= items) break;
+      const int b = t[u] / q_len;
+      if (h[u] >= Hq + Hkv) {  // value head: plain copy into the page
+        const int blk = bt[b * pps + pos[u] / 16], slot = pos[u] % 16;
+        __nv_bfloat16* dst = Vp + (((size_t)blk * Hkv + (h[u] - Hq - Hkv)) * 16 + slot) * 128;
+        *reinterpret_cast<uint32_t*>(dst + 2 * lane) = a[u];
+        *reinterpret_cast<uint32_t*>(dst + 64 + 2 * lane) = bb[u];
+        continue;
+      }
+      const float2 x1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a[u]));
+      const float2 x2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bb[u]));
+      const float y10 = rope_y1(x1.x, x2.x, cs[u].x, cs[u].y), y20 = rope_y2(x1.x, x2.x, cs[u].x, cs[u].y);
+      const float y11 = rope_y1(x1.y, x2.y, cs[u].z, cs[u].w), y21 = rope_y2(x1.y, x2.y, cs[u].z, cs[u].w);
+      __nv_bfloat16* dst;
+      if (h[u] < Hq) {
+        dst = q_out + ((size_t)t[u] * Hq + h[u]) * 128;
+      } else {
+        const int blk = bt[b * pps + pos[u] / 16], slot = pos[u] % 16;
+        dst = Kp + (((size_t)blk * Hkv + (h[u] - Hq)) * 16 + slot) * 128;
+      }
+      *reinterpret_cast<__nv_bfloat162*>(dst + 2 * lane) = __floats2bfloat162_rn(y10, y11);
+      *reinterpret_cast<__nv_bfloat162*>(dst + 64 + 2 * lane) = __floats2bfloat162_rn(y20, y21);
+    }
   }
 }
 
@@ -1639,7 +1695,7 @@ cudaError_t launch_rope_partial(const float* partial, const PartialGeom* g, int 
   if ((groups + H / CG - 1) / (H / CG) + 1 > kRnMaxSeg) return cudaErrorInvalidValue;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int grid = std::max(1, std::min(32 * sms, (T * H + 7) / 8));  // one item per warp
+  const int grid = std::max(1, std::min(6 * sms, (T * H + 15) / 16));
   return launch_k(rope_partial_kernel, dim3(grid), dim3(256), 0, st, partial, g->G, g->kb, g->drain, CG, H, g->T, T,
                   q_len, pos0, rope, Hq, Hkv, bt, pps, (__nv_bfloat16*)Kp, (__nv_bfloat16*)Vp, (__nv_bfloat16*)q_out);
 }

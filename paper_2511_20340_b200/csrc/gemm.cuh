@@ -151,7 +151,7 @@ struct SeqStep {
 bool gemm_seq_supported(int T, const SeqStep* steps, int n);
 // sync: kSeqSyncInts device ints, zeroed once, private to one call site (the kernel keeps them
 // consistent across launches with a launch epoch); scratch as gemm_launch's
-constexpr int kSeqSyncInts = 64 + 8 * 128 * 33;
+constexpr int kSeqSyncInts = 64 + 8 * 128 * 36;
 cudaError_t gemm_seq_launch(int T, const SeqStep* steps, int n, const GemmScratch& scratch, int* sync, cudaStream_t s);
 
 }  // namespace sf

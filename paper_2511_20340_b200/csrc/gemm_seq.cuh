@@ -59,11 +59,13 @@ static_assert(sizeof(SeqParams) + sizeof(SeqMaps) <= 4000, "kernel parameter spa
 // sync block layout
 constexpr int kSeqRows = 128;  // T limit
 SF_DEV int* seq_done(int* sy, int ph) { return sy + 8 + ph; }
-SF_DEV int* seq_rowcnt(int* sy, int ph, int row) { return sy + 64 + ph * kSeqRows + row; }
+// quarter task qq of row `row` has published its sums in this launch: flag == the launch's epoch mark
+// (epoch-stamped, so rows a launch does not touch -- a shorter block -- need no re-arming)
+SF_DEV int* seq_rowflag(int* sy, int ph, int row, int qq) { return sy + 64 + (ph * kSeqRows + row) * 4 + qq; }
 SF_DEV float* seq_ss(int* sy, int ph, int row) {  // [32] per-virtual-warp sums of squares of a row
-  return reinterpret_cast<float*>(sy + 64 + kSeqMaxPhases * kSeqRows) + ((size_t)ph * kSeqRows + row) * 32;
+  return reinterpret_cast<float*>(sy + 64 + kSeqMaxPhases * kSeqRows * 4) + ((size_t)ph * kSeqRows + row) * 32;
 }
-static_assert(64 + kSeqMaxPhases * kSeqRows * 33 <= kSeqSyncInts, "sync block");
+static_assert(64 + kSeqMaxPhases * kSeqRows * (4 + 32) <= kSeqSyncInts, "sync block");
 
 SF_DEV int rn_ng_dev(int d) {  // float4 groups per virtual thread (rn_ng, device copy)
   for (int ng = 1; ng <= 4; ++ng)
@@ -536,10 +538,11 @@ gemm_seq_kernel(const __grid_constant__ SeqMaps maps, const __grid_constant__ Se
         if (lane == 0) seq_ss(p.sync, pi_rn, r)[vw] = ss;
       }
       named_sync(1, 256);
-      if (lead) red_release_add(seq_rowcnt(p.sync, pi_rn, r), 1);
+      if (lead) st_release(seq_rowflag(p.sync, pi_rn, r, qq), E1);
       if (!P.gamma) return;
       if (lead)
-        while (ld_acquire(seq_rowcnt(p.sync, pi_rn, r)) < E1 * nq) __nanosleep(32);
+        for (int q2 = 0; q2 < nq; ++q2)
+          while (ld_acquire(seq_rowflag(p.sync, pi_rn, r, q2)) < E1) __nanosleep(32);
       named_sync(1, 256);
       if (ew == 0) {
         float v = (lane < nvw) ? __ldcg(seq_ss(p.sync, pi_rn, r) + lane) : 0.f;

@@ -1773,6 +1773,7 @@ sf_status sf_debug_capture(sf_handle* h, int32_t what, void* dst, int64_t* nbyte
     }
     case 7: src = h->ctx; bytes = (size_t)h->ctx_rows * p.d * 4; break;
     case 8: src = h->prompt_len; bytes = (size_t)B * 4; break;
+    case 9: src = h->seqsync; bytes = h->seqsync ? (size_t)p.L * kSeqSyncInts * 4 : 0; break;  // layer_seq sync blocks
     default: return set_err(h, SF_ERR_ARG, "unknown capture id");
   }
   if (src) SF_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->st));

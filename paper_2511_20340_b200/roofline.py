@@ -54,3 +54,23 @@ def step_flops(c, B, k, lens_verify):
     ctx = sum(lens_verify) / max(1, len(lens_verify)) + k + 1
     f += 4 * T * ctx * c.n_heads * c.head_dim * (c.n_layers + 1)
     return f
+
+
+def prefill_flops(c, B, P, k):
+    """FLOPs of the prefill: base layers + the context layer L+1 (W_D, its QKV / O) over
+    all B P prompt rows, causal attention over the prompt in every layer (P (P+1) / 2 query-key pairs per
+    head, score + value products: 4 hd each) and the LM head on the last row of each sequence."""
+    d = c.d_model
+    rows = B * P
+    f = 2 * rows * (base_linear_params(c) + 4 * d * d + _attn_params(c))
+    f += 4 * B * (P * (P + 1) // 2) * c.n_heads * c.head_dim * (c.n_layers + 1)
+    f += 2 * B * c.vocab * d
+    return f
+
+
+def prefill_bytes(c, B, P, k, chunks, elt=2):
+    """Algorithmic bytes of the chunked prefill: every weight once per chunk pass, the KV of all L+1
+    layers written once and re-read by the later chunks' attention (lower bound: written once)."""
+    w = (base_linear_params(c) + 4 * c.d_model * c.d_model + _attn_params(c)) * elt * chunks
+    kv = B * P * (c.n_layers + 1) * kv_bytes_per_token_layer(c, elt)
+    return w + kv + c.vocab * c.d_model * elt

@@ -541,3 +541,26 @@ def test_tp_bf16_reduce_parity(tp):
                 if O.top2_margin(r["logits"][i]) > 5e-2:
                     assert s["greedy"][0][i] == r["greedy"][i]
     print(f"TP={tp}: logits rel-L2 vs oracle, fp32 all-reduce {errs['fp32']:.3e}, bf16 all-reduce {errs['bf16']:.3e}")
+
+
+@pytest.mark.timeout(300)
+def test_layer_seq_block_sizes_change_on_one_handle():
+    """One handle (max_batch 64 -> 8-row prefill chunks) alternating layer-sequence launches of different
+    block sizes -- prefill chunks of 8 rows, decode blocks of 5, the profiling step graph, a second
+    prefill -- stays live (per-launch epoch stamps, no stale counters for rows a shorter block did not
+    touch) and emits the same tokens as a fresh handle each time."""
+    cfg = MID
+    w, prompts = setup(cfg, seed=34, jitter=0.1)
+    ms = max_seq_for(cfg, 40, cfg.draft_len)
+    big = Engine(EngineConfig.from_model(cfg, max_batch=64, max_seq=ms, flags=N.SF_FLAG_CUDA_GRAPH), w)
+    ref = run_gpu(cfg.replace(batch=1), w, prompts[:1], 12)["tokens"]
+    for it in range(2):
+        big.prefill(prompts[:1].cuda())
+        em = torch.zeros(11, 1, cfg.draft_len + 1, dtype=torch.int32, device="cuda")
+        if it == 1:
+            big.profile(True)
+        big.decode_steps(11, em, None)
+        big.sync()
+        big.profile(False)
+        toks = [t for t in em.cpu().numpy().reshape(-1) if t >= 0]
+        assert toks[:11] == ref[0][1:12], it
