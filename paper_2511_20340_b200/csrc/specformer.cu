@@ -230,7 +230,8 @@ Plan make_plan(const sf_config* c) {
   p.o_apo = take((int64_t)p.R * p.Hq * p.nchunk * 4 * p.hd * 4);
   p.o_apml = take((int64_t)p.R * p.Hq * p.nchunk * 4 * 2 * 4);
   // split-KV arrival counters: one per (sequence, kv head, 16-row query tile) at the longest block
-  p.n_acnt = (int64_t)p.B * p.Hkv * ((std::max(p.k + 1, p.C_pf) * (p.Hq / p.Hkv) + 15) / 16);
+  p.n_acnt = std::max<int64_t>((int64_t)p.B * p.Hkv * ((std::max(p.k + 1, p.C_pf) * (p.Hq / p.Hkv) + 15) / 16),
+                               (int64_t)p.Hkv * ((p.R * (p.Hq / p.Hkv) + 15) / 16 + 1));  // (one long sequence)
   p.o_acnt = take(p.n_acnt * 4);
   p.o_gpart = take(p.gpart_elems * 4);
   p.o_gcnt = take(4096 * 4);
@@ -1370,7 +1371,10 @@ sf_status specformer_prefill(sf_handle* h, const int32_t* tokens, int32_t B, int
     std::fill(h->released.begin(), h->released.end(), 0);
   }
   if (h->tpkey) SF_TRY(cudaMemsetAsync(h->tpkey, 0, (size_t)p.n_amrows * 8, h->st));
-  const int C = p.C_pf;
+  // chunk rows per sequence for THIS batch (one 512-row GEMM pass per chunk; a handle sized for a large
+  // batch prefills a small one in few chunks), within the plan's row capacity
+  static const int pf_cap = getenv("SF_PF_CAP") ? atoi(getenv("SF_PF_CAP")) : 512;
+  const int C = std::max(p.k + 1, std::min(std::min(pf_cap, std::max(1, 512 / B)), p.R / B));
   int Cc = 0;
   for (int c0 = 0; c0 < P; c0 += C) {
     Cc = std::min(C, P - c0);
