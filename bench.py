@@ -670,7 +670,7 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    args.sweep_list = [int(x) for x in args.sweep.split(",") if x.strip()] if args.sweep else []
+    args.sweep_list = [int(x) for x in args.sweep.split(",") if x.strip()] if args.sweep not in ("", "none") else []
     from synth import get_config
     cfg = get_config(args.config)
     if args.draft_len is not None:

@@ -38,7 +38,7 @@ def main(path, steps, out_txt, out_json=None):
     if out_json:
         traffic, tot = {}, collections.defaultdict(lambda: [0, 0.0])
         for k, (n, t, b) in agg.items():
-            cls = "gemm" if k.startswith("gemm_sk_kernel") else ("attention" if k.startswith("attn_fd_kernel") else None)
+            cls = "gemm" if k.startswith(("gemm_sk_kernel", "gemm_seq_kernel")) else ("attention" if k.startswith("attn_fd_kernel") else None)
             if cls:
                 tot[cls][0] += n
                 tot[cls][1] += b
