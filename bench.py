@@ -515,7 +515,8 @@ def run_ours(args, cfg):
             continue
         _log(f"sweep B={Bs}")
         pr_s = prompts[:Bs].contiguous()
-        win = timed_windows(Bs, pr_s)
+        with ClockSampler(local) as clk_s:
+            win = timed_windows(Bs, pr_s, clk_s)
         sb_s = window_roofline(win, Bs)
         w_ms, w_tok = dp.reduce_timing(win["ms"], float(int((win["after"] - win["before"]).sum())), device="cuda")
         _log("  event profile")
@@ -531,6 +532,7 @@ def run_ours(args, cfg):
                                                            "ms_per_launch", "launches_per_step")} | {"kernel": ev_s["dominant"]},
                       "event_classes": ev_s["classes"],
                       "e2e": e2e_run(Bs, pr_s, min(Ke, args.sweep_e2e_steps)),
+                      "clocks": clk_s.summary(),
                       "gpu_launches": win["launches"]})
 
     # ---------------- forced acceptance: drafts replaced -- after the draft step has run
