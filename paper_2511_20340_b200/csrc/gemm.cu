@@ -95,6 +95,7 @@ struct SkParams {
   int Tp;  // T rounded up to 32 (row stride of the fixup partial slots)
   int NT, n_sub, stages, kb_total, n_tiles, G, nbuf, w_tiled, w_tma, stage_ok, bulk_ok, npre;
   int cgrp;  // ring slots released per tcgen05.commit
+  int probe;  // measurement only (SF_GEMM_PROBE=1): the producer loads nothing
   int drain; // tile-entry cost of the stream-K partition (sk_begin)
   int park;  // park mid-range full tiles (T >= 64) for the final phase
   // chain (gate/up -> down in one launch, CHAIN instantiation): phase B's k-blocks, tiles, drain,
@@ -259,7 +260,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     // ---- TMA producer warp (converged; one elected lane issues)
     // The weights do not depend on the previous kernel: the first ring's worth of weight tiles is
     // requested before the grid dependency resolves (PDL), the activation tiles after it.
-    const long long npre = p.w_tiled ? min((long long)p.npre, u1 - u0) : 0;
+    const long long npre = (p.w_tiled && !p.probe) ? min((long long)p.npre, u1 - u0) : 0;
     if (npre > 0 && elect_one()) {
       int si = 0;
       long long up = seg_lo(0);
@@ -295,7 +296,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       if (!pre) mbar_wait(&empty[grp_last], ph ^ 1u);  // slot group released
       if (j == 0 && lane == 0) SF_TR(2);
       if (lane == 0 && j < 40) SF_TR(64 + (int)j);
-      if (elect_one()) {
+      if (p.probe) {  // (SF_GEMM_PROBE, measurement only: no loads, the MMA runs on stale tiles)
+        if (prank == 0 && elect_one()) mbar_arrive(&full[s]);
+      } else if (elect_one()) {
         uint8_t* st = smem + (size_t)s * stage_bytes;
         if constexpr (CG == 1) {
           if (!pre) {
@@ -372,6 +375,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     const uint32_t idesc = idesc_bf16_f32(kPair ? 2 * BM : BM, p.NT);
     const uint32_t a_off = (uint32_t)(BM * BK * 2) >> 4;           // B-operand tile offset (16 B units)
     const uint32_t sub_off = (uint32_t)(a_rows * BK * 2) >> 4;     // between activation sub-tiles
+    const bool two_sub = p.n_sub == 2;                              // (n_sub <= 2: T <= 512 per launch)
     int s = 0, gcnt = 0;
     uint32_t ph = 0;
     long long j = 0;  // units consumed
@@ -382,7 +386,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       mbar_wait(&acce[b], ((uint32_t)(seg / p.nbuf) & 1u) ^ 1u);
       tc_fence_after();
       if (lane == 0 && seg < 4) SF_TR(8 + 4 * seg);
-      const uint32_t dacc = tmem + (uint32_t)(b * cols);
+      const uint32_t dacc = tmem + (uint32_t)(b * cols), dacc1 = dacc + (uint32_t)p.NT;
       for (long long uu = u; uu < se; ++uu) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
@@ -392,18 +396,26 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         }
         ++j;
         if (elect_one()) {
+          // fully unrolled over (k step, sub-tile) with the operands formed once per stage: a runtime
+          // sub-tile loop costs more issue time per MMA than the tensor pipe needs at N <= 160
           const uint64_t dw = sw128_kmajor_desc(smem_u32(smem + (size_t)s * stage_bytes));
           const uint64_t da = dw + a_off;
+          const uint32_t acc0 = uu > u ? 1u : 0u;
+          auto issue = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+            if constexpr (CG == 1) umma_bf16(d, a, b, idesc, acc);
+            else umma_bf16_2sm(d, a, b, idesc, acc);
+          };
+          if (two_sub) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            for (int j = 0; j < p.n_sub; ++j) {
-              if constexpr (CG == 1)
-                umma_bf16(dacc + (uint32_t)(j * p.NT), dw + (uint64_t)(kk * 2), da + (uint64_t)(j * sub_off + kk * 2),
-                          idesc, (uu > u || kk > 0) ? 1u : 0u);
-              else
-                umma_bf16_2sm(dacc + (uint32_t)(j * p.NT), dw + (uint64_t)(kk * 2),
-                              da + (uint64_t)(j * sub_off + kk * 2), idesc, (uu > u || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              issue(dacc, dw + (uint64_t)(kk * 2), da + (uint64_t)(kk * 2), kk > 0 ? 1u : acc0);
+              issue(dacc1, dw + (uint64_t)(kk * 2), da + (uint64_t)(sub_off + kk * 2), kk > 0 ? 1u : acc0);
             }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              issue(dacc, dw + (uint64_t)(kk * 2), da + (uint64_t)(kk * 2), kk > 0 ? 1u : acc0);
+          }
           if (++gcnt == p.cgrp) {  // frees slots s-cgrp+1..s (in both CTAs of a pair)
             if constexpr (CG == 1) umma_commit(&empty[s]);
             else umma_commit_2sm(&empty[s], (uint16_t)(3u << pbase));
@@ -1213,6 +1225,7 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   p.K = K;
   p.Tp = (T + 31) / 32 * 32;
   tc_shape(T, &p.NT, &p.n_sub);
+  if (p.n_sub > 2) return cudaErrorInvalidValue;  // (callers split T > 512)
   p.kb_total = K / BK;
   p.n_tiles = N / (BM * CG);
   const long long U = (long long)p.n_tiles * p.kb_total;
@@ -1233,7 +1246,11 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
       p.cgrp = cg;
       break;
     }
+  static const int env_cg = getenv("SF_GEMM_CGRP") ? atoi(getenv("SF_GEMM_CGRP")) : 0;
+  if (env_cg >= 1 && env_cg <= p.stages) p.cgrp = env_cg;
   p.stages = (p.stages / p.cgrp) * p.cgrp;
+  static const int env_probe = getenv("SF_GEMM_PROBE") ? atoi(getenv("SF_GEMM_PROBE")) : 0;
+  p.probe = env_probe;
   p.epi = epi;
   p.partial = scratch.partial;
   p.flags = scratch.counters;
