@@ -96,6 +96,10 @@ struct SkParams {
   int NT, n_sub, stages, kb_total, n_tiles, G, nbuf, w_tiled, w_tma, stage_ok, bulk_ok, npre;
   int cgrp;  // ring slots released per tcgen05.commit
   int probe;  // measurement only (SF_GEMM_PROBE=1): the producer loads nothing
+  // three-slot accumulator rotation (two sub-tiles of NT <= 170 columns, one accumulator's worth of
+  // TMEM left over): piece g's sub-tile h lives in slot (2 g + h) % 3, so the next piece's MMA waits
+  // only for the first half of this piece's drain instead of all of it
+  int rot;
   int drain; // tile-entry cost of the stream-K partition (sk_begin)
   int park;  // park mid-range full tiles (T >= 64) for the final phase
   // chain (gate/up -> down in one launch, CHAIN instantiation): phase B's k-blocks, tiles, drain,
@@ -197,6 +201,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   uint64_t* acce = accf + 2;          // [2]
   uint64_t* fixb = acce + 2;           // bulk fixup loads (last-segment heads)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 3);
+  uint64_t* sempty = acce + 5;          // [3] (rot) slot released by both CTAs' 8 epilogue warps
   
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = kPair ? cluster_rank() : 0u;
@@ -234,6 +239,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       mbar_init(&acce[b], kPair ? 2 : 1);  // pair leader: both CTAs' epilogues release the accumulator
     }
     mbar_init(fixb, 1);
+    for (int x = 0; x < 3; ++x) mbar_init(&sempty[x], kPair ? 16 : 8);
     fence_barrier_init();
     SF_TR(125);
   }
@@ -383,10 +389,15 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       const long long u = seg < nseg ? seg_lo(seg) : segB_lo(seg - nseg);
       const long long se = seg < nseg ? seg_hi(seg) : segB_hi(seg - nseg);
       const int b = seg % p.nbuf;
-      mbar_wait(&acce[b], ((uint32_t)(seg / p.nbuf) & 1u) ^ 1u);
-      tc_fence_after();
+      if (!p.rot) {
+        mbar_wait(&acce[b], ((uint32_t)(seg / p.nbuf) & 1u) ^ 1u);
+        tc_fence_after();
+      }
       if (lane == 0 && seg < 4) SF_TR(8 + 4 * seg);
       const uint32_t dacc = tmem + (uint32_t)(b * cols), dacc1 = dacc + (uint32_t)p.NT;
+      // (rot) half-piece n = 2 seg + h -> slot n % 3; its previous use n - 3 must be drained
+      const int n0 = 2 * seg;
+      const uint32_t r0 = tmem + (uint32_t)((n0 % 3) * p.NT), r1 = tmem + (uint32_t)(((n0 + 1) % 3) * p.NT);
       for (long long uu = u; uu < se; ++uu) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
@@ -395,7 +406,31 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           if (j < 40) SF_TR(24 + (int)j);
         }
         ++j;
-        if (elect_one()) {
+        if (kPair && p.rot) {
+          const uint64_t dw = sw128_kmajor_desc(smem_u32(smem + (size_t)s * stage_bytes));
+          const uint64_t da = dw + a_off;
+          const uint32_t acc0 = uu > u ? 1u : 0u;
+          if (uu == u) {
+            mbar_wait(&sempty[n0 % 3], ((uint32_t)(n0 / 3) & 1u) ^ 1u);
+            tc_fence_after();
+          }
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              umma_bf16_2sm(r0, dw + (uint64_t)(kk * 2), da + (uint64_t)(kk * 2), idesc, kk > 0 ? 1u : acc0);
+          }
+          __syncwarp();
+          if (uu == u) {
+            mbar_wait(&sempty[(n0 + 1) % 3], ((uint32_t)((n0 + 1) / 3) & 1u) ^ 1u);
+            tc_fence_after();
+          }
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              umma_bf16_2sm(r1, dw + (uint64_t)(kk * 2), da + (uint64_t)(sub_off + kk * 2), idesc, kk > 0 ? 1u : acc0);
+            if (++gcnt == p.cgrp) umma_commit_2sm(&empty[s], (uint16_t)(3u << pbase));
+          }
+        } else if (elect_one()) {
           // fully unrolled over (k step, sub-tile) with the operands formed once per stage: a runtime
           // sub-tile loop costs more issue time per MMA than the tensor pipe needs at N <= 160
           const uint64_t dw = sw128_kmajor_desc(smem_u32(smem + (size_t)s * stage_bytes));
@@ -712,11 +747,29 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 
     // Epilogue of segment [u, se) of tile t from TMEM buffer b by ng groups (this thread: group
     // gid, barrier over nthr threads). final: every MMA of the CTA has completed (ring idle).
+    // (rot) this warp's TMEM reads of half-piece n = 2 seg + h are complete: release its slot
+    auto rot_release = [&](int n) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (prank == 0) mbar_arrive(&sempty[n % 3]);
+        else mbar_arrive_remote(&sempty[n % 3], pbase);
+      }
+    };
+    int ep_seg = 0;  // the segment being finished (rot slot mapping)
     auto segment_epilogue = [&](long long u, int t, long long se, int b, int gid, int ng, int nthr, bool final,
                                 int& defer_vt, bool phase_b) {
       const int kbs = phase_b ? kbB : kb;
       const long long ts = (long long)t * kbs, te = ts + kbs;
       const uint32_t t_row = tmem + (uint32_t)(b * cols) + ((uint32_t)(quad * 32) << 16);
+      // TMEM address of this thread's lane row at token column c0 (a 32-column chunk never straddles
+      // the two sub-tiles: NT % 32 == 0 under rot)
+      auto taddr = [&](int c0) -> uint32_t {
+        if (!p.rot) return t_row + (uint32_t)c0;
+        const int h = c0 >= p.NT ? 1 : 0;
+        return tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(((2 * ep_seg + h) % 3) * p.NT + c0 - h * p.NT);
+      };
+      const bool rel = p.rot && !final;  // (rot) release the slots as their columns are read
       const int vt = t * CG + (int)rank;  // 128-row tile index of this CTA's rows
       const bool is_full = (u == ts) && (se == te);
       const bool is_head = (u == ts) && !is_full;
@@ -735,12 +788,14 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
                          : (tail ? slot_base : defer_base);
         for (int c0 = gid * 32; c0 < p.T; c0 += cstep) {
           uint32_t r[32];
-          tmem_ld32_async(t_row + (uint32_t)c0, r);
+          tmem_ld32_async(taddr(c0), r);
           tmem_ld_wait();
+          if (rel && c0 < p.NT && c0 + cstep >= p.NT) rot_release(2 * ep_seg);  // last sub-tile-0 chunk read
 #pragma unroll
           for (int cc = 0; cc < 32; ++cc)
             if (c0 + cc < p.T) dst[(size_t)(c0 + cc) * BM + m] = __uint_as_float(r[cc]);
         }
+        if (rel) rot_release(2 * ep_seg + 1);
         if (tail) {
           __threadfence();
           named_sync(final ? 5 : 1, nthr);
@@ -775,7 +830,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         if (lead && final && P0 == 0) SF_TR(105);
         for (int c0 = P0 + gid * 32; c0 < P1; c0 += cstep) {
           uint32_t r[32];
-          tmem_ld32_async(t_row + (uint32_t)c0, r);
+          tmem_ld32_async(taddr(c0), r);
           tmem_ld_wait();
           if (lead && final && c0 < 2 * cstep) SF_TR(114 + 4 * (c0 / cstep));  // TMEM loaded
           float v[32];
@@ -828,6 +883,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           if (lead && final && c0 < 4 * cstep) SF_TR(107 + 2 * (c0 / cstep));  // stored
         }
         if (bulk) named_sync(final ? 5 : 1, nthr);  // smem pass consumed before the next one overwrites it
+      }
+      if (rel) {  // (not taken by construction under rot: every non-final piece is drained above)
+        rot_release(2 * ep_seg);
+        rot_release(2 * ep_seg + 1);
       }
       if (is_head) {
         named_sync(final ? 5 : 1, nthr);
@@ -899,11 +958,12 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         mbar_wait_sleep(&accf[b], (uint32_t)(seg / p.nbuf) & 1u);
         if (lead && seg < 4) SF_TR(8 + 4 * seg + 2);
         tc_fence_after();
+        ep_seg = seg;
         segment_epilogue(u, t, se, b, gid, ng, nthr, final, defer_vt, phase_b);
         if (!final) {
           tc_fence_before();
           named_sync(1, 256);
-          if (lead && seg < nseg_total - 1) {  // (the MMA never waits for the last buffer)
+          if (lead && seg < nseg_total - 1 && !p.rot) {  // (the MMA never waits for the last buffer)
             if (CG == 1 || prank == 0) mbar_arrive(&acce[b]);
             else mbar_arrive_remote(&acce[b], pbase);
           }
@@ -1269,12 +1329,24 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   if (!sk_fits(p.G, p.n_tiles, p.kb_total, p.drain)) return cudaErrorInvalidValue;
   p.park = (env_epi >> 4) & 1;
   p.stage_ok = (env_epi >> 1) & 7;
+  {  // three-slot accumulator rotation: every non-final piece must take the drain-to-partial path
+    static const int env_rot = getenv("SF_GEMM_ROT") ? atoi(getenv("SF_GEMM_ROT")) : 1;
+    const int m = epi.mode;
+    const bool stageable = m == EPI_STORE_ACT || m == EPI_STORE_F32 || m == EPI_SWIGLU_ACT || m == EPI_QKV_ROPE;
+    const int out_elt = m == EPI_STORE_F32 ? 4 : 2;
+    const bool can_stage = stageable && p.stage_ok && ((size_t)epi.ldo * out_elt) % 16 == 0 &&
+                           p.stages * stage_bytes >= 3 * 16384 + 64 * BM * 4;
+    p.rot = (env_rot && !chain && CG == 2 && p.n_sub == 2 && p.NT % 32 == 0 && 3 * p.NT <= 512 && p.nbuf == 1 && T >= 64 &&
+             (m == EPI_PARTIAL || (can_stage && p.park)))
+                ? 1
+                : 0;
+  }
   static const int trace_n = getenv("SF_GEMM_TRACE_N") ? atoi(getenv("SF_GEMM_TRACE_N")) : 0;
   if (trace_n && trace_n != N) p.trace = nullptr;  // trace one weight shape only
   if (!scratch.partial || scratch.partial_elems < (int64_t)2 * p.G * CG * p.Tp * BM || scratch.n_counters < p.G * CG)
     return cudaErrorInvalidValue;
   if (epi.mode == EPI_PARTIAL && p.n_tiles > p.G) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)p.stages * stage_bytes + 1024 + (2 * p.stages + 5) * 8 + 16;
+  const size_t smem = (size_t)p.stages * stage_bytes + 1024 + (2 * p.stages + 10) * 8;
   CUtensorMap mw, ma;
   memset(&mw, 0, sizeof(mw));
   static const int env_wtma = getenv("SF_GEMM_WTMA") ? atoi(getenv("SF_GEMM_WTMA")) : 0;
