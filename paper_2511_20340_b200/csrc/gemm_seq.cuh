@@ -389,22 +389,7 @@ gemm_seq_kernel(const __grid_constant__ SeqMaps maps, const __grid_constant__ Se
       const size_t ldo = (size_t)P.epi.ldo;
       const int f = vt_ * 64 + (m >> 1);
       __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(P.epi.out) + (size_t)c0 * ldo + f;
-#pragma unroll
-      for (int q0 = 0; q0 < 32; q0 += 8) {
-        if (q0 >= nq) break;  // (warp-uniform)
-        float uu[8], e[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) uu[j] = __shfl_down_sync(0xffffffffu, v[q0 + j], 1);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) e[j] = __expf(-v[q0 + j]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) e[j] = __fdividef(v[q0 + j], 1.f + e[j]) * uu[j];
-        if (!(lane & 1)) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (q0 + j < nq) o[(q0 + j) * ldo] = __float2bfloat16_rn(e[j]);
-        }
-      }
+      swiglu_pair(v, nq, lane, [&](int q, float y) { o[q * ldo] = __float2bfloat16_rn(y); });
     };
 
     constexpr int kPreT = 8;  // (small T) head pieces with one or two partners: partials loaded early
