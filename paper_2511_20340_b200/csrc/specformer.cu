@@ -678,7 +678,7 @@ static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const i
   return dbg_sync(h, "attention", launch_attention(h->bf, ap, h->st));
 }
 
-// Small verify blocks (T <= SF_SEQ_T, default 80: batch <= 16 at k = 4): the part of base layer l
+// Small verify blocks (T <= SF_SEQ_T; off by default, see seq_T): the part of base layer l
 // between two attentions -- O-proj + residual + RMS_ffn, gate/up SwiGLU, down + residual (+ tap) +
 // the next norm, and layer l+1's QKV with RoPE / KV append -- as ONE persistent launch
 // (gemm_seq_launch, csrc/gemm_seq.cuh) with the standalone launches' partition and arithmetic
@@ -686,7 +686,12 @@ static cudaError_t attn_layer(sf_handle* h, int layer, int T, int q_len, const i
 // switches call for the standalone path.
 static int seq_T() {
   const char* e = getenv("SF_SEQ_T");  // (read per call: tests compare both paths)
-  return e ? atoi(e) : 32;  // measured: faster up to T = 20 (B = 4 at k = 4), slower from T = 40
+  // Off by default (opt-in, SF_SEQ_T=80): it won 3-5% at B = 1..4 against the standalone launches
+  // while their MMA issue loop was the main-loop bound; with that loop fixed the standalone path is
+  // faster at every batch (7B, ms per step: B = 1 3.72 vs 4.15, B = 2 3.79 vs 4.23, B = 4 3.95 vs
+  // 4.47, B = 8 4.35 vs 5.23) -- the per-phase grid-wide dependencies now cost more than the launch
+  // boundaries they remove.
+  return e ? atoi(e) : 0;
 }
 static bool layer_seq(sf_handle* h, cudaError_t* err, int l, int T, int q_len, const int* pos0, float* tap,
                       const float* next_g) {
