@@ -580,13 +580,16 @@ static const int* taps_layers(int L, int* out4) {
 }
 
 // One attention sub-layer's "RoPE + append + attention" for rows (T, q_len, pos0) of layer `layer`.
-// bf16, head_dim 128, blocks of < 64 rows: RoPE and the paged K/V append run in the QKV GEMM's
-// epilogue (EPI_QKV_ROPE; one launch fewer per attention). Both paths rotate the same bf16-rounded
-// projections with the same operations, so the choice per T keeps every row's bits (batch
-// invariance); SF_ROPE_FUSE_T (read per call; tests) moves the threshold.
+// bf16, head_dim 128: RoPE and the paged K/V append can run in the QKV GEMM's epilogue (EPI_QKV_ROPE;
+// one launch fewer per attention) for blocks of < SF_ROPE_FUSE_T rows (read per call; tests). Both
+// paths rotate the same bf16-rounded projections with the same operations, so the choice per T keeps
+// every row's bits (batch invariance). Off by default: the partials + rope consumer form is faster at
+// every batch since the GEMM main loop got faster -- the fused form's head-tile fixup is a tail after
+// the last MMA (7B ms per step, consumer vs fused: B = 1 3.61 vs 3.72, B = 4 3.78 vs 3.94, B = 8 4.11
+// vs 4.35; B >= 13 already used the consumer).
 static bool fused_rope(const sf_handle* h, int T) {
   const char* e = getenv("SF_ROPE_FUSE_T");
-  const int thr = e ? atoi(e) : 64;
+  const int thr = e ? atoi(e) : 0;
   return h->bf && h->p.hd == 128 && T < thr;
 }
 
