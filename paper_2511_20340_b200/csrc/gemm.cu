@@ -1463,7 +1463,10 @@ bool gemm_partial_geom(int T, int N, int K, PartialGeom* g, int drain) {
 // sums, so a row streams at memory speed and a few rows (B = 1) still spread over many warps.
 constexpr int kRnMaxSeg = 16;  // k segments per 128-column tile (stream-K: <= G / n_tiles + 2)
 constexpr int kRnMaxTiles = 128;
-static int rn_ng(int d) {  // float4 groups per thread
+// float4 groups per thread: two where the width allows it (d = 4096: 512-thread rows, two resident per
+// SM -- a T = 320 block in about one wave instead of 2.2 with 1024-thread rows), else the fewest that fit
+static int rn_ng(int d) {
+  if (d % (4 * 2 * 32) == 0 && d / 8 <= 1024) return 2;
   for (int ng = 1; ng <= 4; ++ng)
     if (d % (4 * ng * 32) == 0 && d / (4 * ng) <= 1024) return ng;
   return 0;
@@ -1523,25 +1526,57 @@ __global__ void __launch_bounds__(1024) resid_norm_kernel(
     }
   }
   if (partial) {
+    if constexpr (NG == 2) {
+      // both column groups' segment loads in flight together (then the k-ordered sums per group)
+      const int n0 = col0 + 4 * tid, n1 = n0 + 4 * nthr;
+      const int vt0 = n0 / BM, vt1 = n1 / BM;
+      const int ns0 = seg_n[vt0], ns1 = seg_n[vt1], nsm = max(ns0, ns1);
+      const float* bp0 = partial + (size_t)src_row * BM + n0 % BM;
+      const float* bp1 = partial + (size_t)src_row * BM + n1 % BM;
+      for (int q0 = 0; q0 < nsm; q0 += 4) {
+        float4 pa[4], pb[4];
 #pragma unroll
-    for (int j = 0; j < NG; ++j) {
-      const int n = col0 + 4 * tid + 4 * nthr * j;
-      const int vt = n / BM, m = n % BM;
-      const int ns = seg_n[vt];
-      const float* bp = partial + (size_t)src_row * BM + m;
-      for (int q0 = 0; q0 < ns; q0 += kRnBatch) {
-        float4 pv[kRnBatch];
+        for (int q = 0; q < 4; ++q) {
+          if (q0 + q < ns0) pa[q] = __ldcg(reinterpret_cast<const float4*>(bp0 + seg_off[vt0][q0 + q]));
+          if (q0 + q < ns1) pb[q] = __ldcg(reinterpret_cast<const float4*>(bp1 + seg_off[vt1][q0 + q]));
+        }
 #pragma unroll
-        for (int q = 0; q < kRnBatch; ++q)
-          if (q0 + q < ns) pv[q] = __ldcg(reinterpret_cast<const float4*>(bp + seg_off[vt][q0 + q]));
-#pragma unroll
-        for (int q = 0; q < kRnBatch; ++q)
-          if (q0 + q < ns) {  // k order
-            x[j].x += pv[q].x;
-            x[j].y += pv[q].y;
-            x[j].z += pv[q].z;
-            x[j].w += pv[q].w;
+        for (int q = 0; q < 4; ++q) {  // k order
+          if (q0 + q < ns0) {
+            x[0].x += pa[q].x;
+            x[0].y += pa[q].y;
+            x[0].z += pa[q].z;
+            x[0].w += pa[q].w;
           }
+          if (q0 + q < ns1) {
+            x[1].x += pb[q].x;
+            x[1].y += pb[q].y;
+            x[1].z += pb[q].z;
+            x[1].w += pb[q].w;
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NG; ++j) {
+        const int n = col0 + 4 * tid + 4 * nthr * j;
+        const int vt = n / BM, m = n % BM;
+        const int ns = seg_n[vt];
+        const float* bp = partial + (size_t)src_row * BM + m;
+        for (int q0 = 0; q0 < ns; q0 += kRnBatch) {
+          float4 pv[kRnBatch];
+#pragma unroll
+          for (int q = 0; q < kRnBatch; ++q)
+            if (q0 + q < ns) pv[q] = __ldcg(reinterpret_cast<const float4*>(bp + seg_off[vt][q0 + q]));
+#pragma unroll
+          for (int q = 0; q < kRnBatch; ++q)
+            if (q0 + q < ns) {  // k order
+              x[j].x += pv[q].x;
+              x[j].y += pv[q].y;
+              x[j].z += pv[q].z;
+              x[j].w += pv[q].w;
+            }
+        }
       }
     }
   }
@@ -1796,7 +1831,10 @@ cudaError_t launch_rope_partial(const float* partial, const PartialGeom* g, int 
   if ((groups + H / CG - 1) / (H / CG) + 1 > kRnMaxSeg) return cudaErrorInvalidValue;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int grid = std::max(1, std::min(6 * sms, (T * H + 15) / 16));
+  // CTAs per SM: 4 = one resident wave at 64 registers (6 left a half-empty second wave: T = 320 13.4 ->
+  // 10.8 us per launch); small blocks need fewer CTAs than that anyway
+  static const int env_g = getenv("SF_ROPE_GRID") ? atoi(getenv("SF_ROPE_GRID")) : 4;
+  const int grid = std::max(1, std::min(std::max(1, env_g) * sms, (T * H + 15) / 16));
   return launch_k(rope_partial_kernel, dim3(grid), dim3(256), 0, st, partial, g->G, g->kb, g->drain, CG, H, g->T, T,
                   q_len, pos0, rope, Hq, Hkv, bt, pps, (__nv_bfloat16*)Kp, (__nv_bfloat16*)Vp, (__nv_bfloat16*)q_out);
 }
