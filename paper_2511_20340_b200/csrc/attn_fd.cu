@@ -73,7 +73,9 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
                                                         const __grid_constant__ CUtensorMap tmK4,
                                                         const __grid_constant__ CUtensorMap tmV4, AttnParams p,
                                                         int ntiles, int nseg_max, int seg_keys, int n_items,
-                                                        int split) {
+                                                        int split_arg) {
+  const int split = split_arg & 1;
+  const bool probe = (split_arg & 2) != 0;  // (SF_ATTN_PROBE, measurement only: stream the chunks, no math)
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   const uint32_t raw = smem_u32(sm_raw);
   uint8_t* sm = sm_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -252,6 +254,13 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
       if (c != it.c0 && c % seg_ch == 0) fold_segment();  // segment boundary (group schedule)
       const int st = seq % NST;
       mbar_wait(&full[st], (uint32_t)(seq / NST) & 1u);
+      if (probe) {  // (finite output: a state of one unit-weight zero row)
+        m_lo = m_hi = 0.f;
+        l_lo = l_hi = 1.f;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        continue;
+      }
       const uint32_t kb = sbase + st * STAGE_BYTES, vb = kb + KV_BYTES;
       const int kstart = c * CH + warp * 32;
       // S = Q K_w^T for this warp's 32 keys
@@ -548,8 +557,9 @@ cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
   if (!encode_kv_map(&mk, p.Kp, rows) || !encode_kv_map(&mv, p.Vp, rows)) return cudaErrorInvalidValue;
   if (!encode_kv_map4(&mk4, p.Kp, p.Hkv, p.n_pages) || !encode_kv_map4(&mv4, p.Vp, p.Hkv, p.n_pages))
     return cudaErrorInvalidValue;
+  static const int env_probe = getenv("SF_ATTN_PROBE") ? atoi(getenv("SF_ATTN_PROBE")) : 0;
   launch_k(attn_fd_kernel, dim3(grid), dim3(160), SMEM, s, mk, mv, mk4, mv4, p, ntiles, nseg_max, seg_keys, n_items,
-           split);
+           split | (env_probe ? 2 : 0));
   return cudaGetLastError();
 }
 
