@@ -1240,6 +1240,16 @@ static int max_groups(int cg) {
   return n;
 }
 
+// Stream-K groups of a weight shape: the co-resident groups, but at least kMinUnits (tile, k-block)
+// units per group -- small weights (the Small config's 0.6-5 MB GEMMs) otherwise split every tile over
+// dozens of groups and spend the launch in the fixup. A function of (N, K) and the device only (batch
+// invariance); every 7B / 13B shape keeps all 74 groups.
+static int sk_groups(int cg, long long n_tiles, int kb) {
+  static const int min_u = getenv("SF_GEMM_MINU") ? std::max(1, atoi(getenv("SF_GEMM_MINU"))) : 4;
+  const long long U = n_tiles * kb;
+  return (int)std::max<long long>(1, std::min<long long>(max_groups(cg), std::max<long long>(1, U / min_u)));
+}
+
 // CTA-pair mode halves each SM's share of the activation tile (the MMA reads the B operand from
 // both CTAs' shared memory), the L2->SM traffic that bounds the skinny GEMM at large T.
 // (A 4-CTA variant multicasting the activation between two pairs deadlocked in round 1 and was
@@ -1301,7 +1311,8 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
   p.kb_total = K / BK;
   p.n_tiles = N / (BM * CG);
   const long long U = (long long)p.n_tiles * p.kb_total;
-  p.G = (int)std::min<long long>(max_groups(CG), U);  // depends on (N, K) and the device only
+  p.G = sk_groups(CG, p.n_tiles, p.kb_total);  // depends on (N, K) and the device only
+  (void)U;
   const int cols = p.n_sub * p.NT;
   p.nbuf = (2 * cols <= 512) ? 2 : 1;
   p.tmem_cols = 32;
@@ -1375,7 +1386,7 @@ static cudaError_t launch_sk(const void* A, int lda, const void* W, bool w_tiled
       return cudaErrorInvalidValue;
     p.kbB = chain->K / BK;
     p.n_tilesB = chain->N / (BM * CG);
-    if (std::min<long long>(max_groups(CG), (long long)p.n_tilesB * p.kbB) != p.G || p.n_tilesB > p.G)
+    if (sk_groups(CG, p.n_tilesB, p.kbB) != p.G || p.n_tilesB > p.G)
       return cudaErrorInvalidValue;  // both phases on the same groups; phase B published as EPI_PARTIAL
     p.drainB = sk_drain(EPI_PARTIAL);
     if (!sk_fits(p.G, p.n_tilesB, p.kbB, p.drainB)) return cudaErrorInvalidValue;
@@ -1446,7 +1457,8 @@ bool gemm_partial_geom(int T, int N, int K, PartialGeom* g, int drain) {
   const int CG = gemm_cg(N, K);
   const int n_tiles = N / (BM * CG);
   const long long U = (long long)n_tiles * (K / BK);
-  const int G = (int)std::min<long long>(max_groups(CG), U);
+  const int G = sk_groups(CG, n_tiles, K / BK);
+  (void)U;
   if (n_tiles > G) return false;  // a group must touch at most 2 tiles
   g->G = G * CG;                  // slots are per CTA: consumer addresses (2 * group + which) * CG + rank
   g->kb = K / BK;

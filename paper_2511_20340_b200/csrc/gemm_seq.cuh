@@ -677,7 +677,7 @@ bool gemm_seq_supported(int T, const SeqStep* st, int n) {
       if (s.N % (2 * BM) || s.K % BK || gemm_cg(s.N, s.K) != 2) return false;
       if (s.epi.mode != EPI_PARTIAL && s.epi.mode != EPI_SWIGLU_ACT && s.epi.mode != EPI_QKV_ROPE) return false;
       const int n_tiles = s.N / (2 * BM), kb = s.K / BK;
-      const int G = (int)std::min<long long>(max_groups(2), (long long)n_tiles * kb);
+      const int G = sk_groups(2, n_tiles, kb);
       const int drain = s.epi.drain >= 0 ? s.epi.drain : sk_drain(s.epi.mode);
       if (!sk_fits(G, n_tiles, kb, drain)) return false;
       if (s.epi.mode == EPI_PARTIAL && n_tiles > G) return false;
@@ -686,7 +686,7 @@ bool gemm_seq_supported(int T, const SeqStep* st, int n) {
     } else {
       if (i == 0 || prev_mode != EPI_PARTIAL) return false;  // a consumer of the preceding EPI_PARTIAL GEMM
       {
-        const int n_tiles = prevN / (2 * BM), G = (int)std::min<long long>(max_groups(2), (long long)n_tiles * (st[i - 1].K / BK));
+        const int n_tiles = prevN / (2 * BM), G = sk_groups(2, n_tiles, st[i - 1].K / BK);
         if ((G + n_tiles - 1) / n_tiles + 1 > kRnMaxSeg || 2 * n_tiles > kRnMaxTiles) return false;
       }
       if (s.kind == SEQ_RESID_NORM && (s.d != prevN || !rn_ng(s.d) || rn_ng(s.d) > 2)) return false;
@@ -744,7 +744,7 @@ cudaError_t gemm_seq_launch(int T, const SeqStep* st, int n, const GemmScratch& 
       P.mode = s.epi.mode;
       P.kb = s.K / BK;
       P.n_tiles = s.N / (2 * BM);
-      P.G = (int)std::min<long long>(Gmax, (long long)P.n_tiles * P.kb);
+      P.G = sk_groups(2, P.n_tiles, P.kb);
       P.drain = s.epi.drain >= 0 ? s.epi.drain : sk_drain(s.epi.mode);
       P.map = nm;
       if (!make_map_tiled(&maps.w[nm], s.W, (long long)s.N * P.kb) || !make_map(&maps.a[nm], s.A, T, s.K, s.lda, p.NT / 2))
