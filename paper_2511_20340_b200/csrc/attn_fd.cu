@@ -3,8 +3,10 @@
 // Work: (sequence b, kv head, 16-row query tile) groups. Keys are cut into fixed SEG-key segments
 // (absolute positions) and the arithmetic is defined segment-wise:
 //   per segment s and warp w: an online softmax over w's 32-key slice of each of the segment's
-//     128-key chunks, starting fresh -> (m, l, O)_{s,w}   (S = Q K^T and O += P V by mma.sync bf16,
-//     masked keys excluded, P kept in registers);
+//     128-key chunks, starting fresh -> (m, l, O)_{s,w}   (S^T = K Q^T and O^T += V^T P^T by mma.sync
+//     bf16 with the keys as MMA rows and the tile's query rows as one or two 8-column n-tiles -- a
+//     decode block of <= 8 rows costs half the MMAs of a 16-row M tile; masked keys excluded, P^T
+//     transposed into the PV operand in registers with movmatrix);
 //   per warp: fold the segment states in order s = 0, 1, ...: M = max, f = 2^(m - M),
 //     l = l_a f_a + l_b f_b, O = O_a f_a + O_b f_b (explicitly rounded products);
 //   across warps: the same merge in the fixed order w = 0..3, then out = acc / L.
@@ -18,6 +20,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -49,6 +52,12 @@ SF_DEV void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_
       "{%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// transpose of an 8x8 b16 matrix held as the mma fragment layout (thread (g, t4): row g, columns 2 t4, +1)
+SF_DEV uint32_t movmatrix_trans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
 }
 SF_DEV uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -182,7 +191,10 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
     return;
   }
 
-  // ---- compute warps
+  // ---- compute warps. Keys are the MMA rows (S^T = K Q^T, O^T += V^T P^T): a 16-row query tile
+  // occupies one or two 8-column n-tiles, so a decode block of <= 8 rows (q_len (k+1) x G) costs half
+  // the MMAs of a 16-row M tile. A column's arithmetic never depends on the other columns or on the
+  // tile's row count (batch invariance, C23).
   const float scale_log2 = 0.08838834764831845f * 1.4426950408889634f;  // log2(e) / sqrt(128)
   int seq = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -192,62 +204,72 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
     const unsigned long long ti0 = g_kt.rec ? kt_now() : 0ull;
     const int r0 = it.qt * 16;
     const int nr = min(16, R - r0);
+    const bool two = nr > 8;  // (warp-uniform) the second 8-column n-tile holds rows
     const int base = p.pos0[it.b];
-    // Q fragments (rows g, g+8 of the tile) from the fp32 rotated queries
-    uint32_t qa[8][4];
+    // Q^T B fragments: query column q = nq*8 + g, dims kk*16 + 2 t4 (+1) and + 8 (bf16, rope_append's RNE)
+    uint32_t qb[2][8][2];
 #pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      const int r = g + 8 * hr;
+    for (int nq = 0; nq < 2; ++nq) {
+      const int r = nq * 8 + g;
       const bool ok = r < nr;
       const int rr = r0 + (ok ? r : 0), qi = rr / G, h = it.kvh * G + rr % G;
-      // bf16 rotated queries (rope_append rounded them RNE)
       const uint32_t* qrow = reinterpret_cast<const uint32_t*>(reinterpret_cast<const __nv_bfloat16*>(p.q) +
                                                                ((size_t)(it.b * p.q_len + qi) * p.Hq + h) * HD);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const int d0 = kk * 16 + 2 * t4;
-        qa[kk][hr] = ok ? qrow[d0 / 2] : 0u;
-        qa[kk][2 + hr] = ok ? qrow[(d0 + 8) / 2] : 0u;
+        qb[nq][kk][0] = ok ? qrow[d0 / 2] : 0u;
+        qb[nq][kk][1] = ok ? qrow[(d0 + 8) / 2] : 0u;
       }
     }
-    const int pos_lo = base + attn_row_last(p, (r0 + g) / G), pos_hi = base + attn_row_last(p, (r0 + g + 8) / G);
-    const bool row_lo = g < nr, row_hi = g + 8 < nr;
-    float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;  // log2-domain running max
-    float o[16][4];
+    // this thread's query columns q = nq*8 + 2 t4 + j: visibility bound (last visible key)
+    int posq[2][2];
+    bool okq[2][2];
 #pragma unroll
-    for (int nt = 0; nt < 16; ++nt)
+    for (int nq = 0; nq < 2; ++nq)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) o[nt][i] = 0.f;
-    // this warp's fold of its finished segments (starts empty: fold(empty, x) == x exactly)
-    float tm_lo = -INFINITY, tm_hi = -INFINITY, tl_lo = 0.f, tl_hi = 0.f;
-    float to[16][4];
-#pragma unroll
-    for (int nt = 0; nt < 16; ++nt)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) to[nt][i] = 0.f;
-    auto fold_segment = [&]() {
-      const float M_lo = fmaxf(tm_lo, m_lo), M_hi = fmaxf(tm_hi, m_hi);
-      const float ft_lo = (tm_lo == -INFINITY) ? 0.f : exp2f(tm_lo - M_lo);
-      const float fc_lo = (m_lo == -INFINITY) ? 0.f : exp2f(m_lo - M_lo);
-      const float ft_hi = (tm_hi == -INFINITY) ? 0.f : exp2f(tm_hi - M_hi);
-      const float fc_hi = (m_hi == -INFINITY) ? 0.f : exp2f(m_hi - M_hi);
-      tl_lo = __fadd_rn(__fmul_rn(tl_lo, ft_lo), __fmul_rn(l_lo, fc_lo));
-      tl_hi = __fadd_rn(__fmul_rn(tl_hi, ft_hi), __fmul_rn(l_hi, fc_hi));
-#pragma unroll
-      for (int nt = 0; nt < 16; ++nt) {
-        to[nt][0] = __fadd_rn(__fmul_rn(to[nt][0], ft_lo), __fmul_rn(o[nt][0], fc_lo));
-        to[nt][1] = __fadd_rn(__fmul_rn(to[nt][1], ft_lo), __fmul_rn(o[nt][1], fc_lo));
-        to[nt][2] = __fadd_rn(__fmul_rn(to[nt][2], ft_hi), __fmul_rn(o[nt][2], fc_hi));
-        to[nt][3] = __fadd_rn(__fmul_rn(to[nt][3], ft_hi), __fmul_rn(o[nt][3], fc_hi));
+      for (int j = 0; j < 2; ++j) {
+        const int q = nq * 8 + 2 * t4 + j;
+        okq[nq][j] = q < nr;
+        posq[nq][j] = base + attn_row_last(p, (r0 + min(q, nr - 1)) / G);
       }
-      tm_lo = M_lo;
-      tm_hi = M_hi;
-      m_lo = m_hi = -INFINITY;
-      l_lo = l_hi = 0.f;
+    float m[2][2], l[2][2], tm[2][2], tl[2][2];  // per column: running max (log2 domain), sum; folded
 #pragma unroll
-      for (int nt = 0; nt < 16; ++nt)
+    for (int nq = 0; nq < 2; ++nq)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) o[nt][i] = 0.f;
+      for (int j = 0; j < 2; ++j) m[nq][j] = tm[nq][j] = -INFINITY, l[nq][j] = tl[nq][j] = 0.f;
+    // O^T accumulators: m-tile md = dims md*16 .. +15, n-tile nq; [c]: (dim g | g+8, column 2 t4 | +1)
+    float o[8][2][4], to[8][2][4];
+#pragma unroll
+    for (int md = 0; md < 8; ++md)
+#pragma unroll
+      for (int nq = 0; nq < 2; ++nq)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[md][nq][i] = to[md][nq][i] = 0.f;
+    // this warp's fold of its finished segments (starts empty: fold(empty, x) == x exactly)
+    auto fold_segment = [&]() {
+#pragma unroll
+      for (int nq = 0; nq < 2; ++nq) {
+        if (nq == 1 && !two) break;  // (warp-uniform)
+        float ft[2], fc[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const float M = fmaxf(tm[nq][j], m[nq][j]);
+          ft[j] = (tm[nq][j] == -INFINITY) ? 0.f : exp2f(tm[nq][j] - M);
+          fc[j] = (m[nq][j] == -INFINITY) ? 0.f : exp2f(m[nq][j] - M);
+          tl[nq][j] = __fadd_rn(__fmul_rn(tl[nq][j], ft[j]), __fmul_rn(l[nq][j], fc[j]));
+          tm[nq][j] = M;
+          m[nq][j] = -INFINITY;
+          l[nq][j] = 0.f;
+        }
+#pragma unroll
+        for (int md = 0; md < 8; ++md)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            to[md][nq][i] = __fadd_rn(__fmul_rn(to[md][nq][i], ft[i & 1]), __fmul_rn(o[md][nq][i], fc[i & 1]));
+            o[md][nq][i] = 0.f;
+          }
+      }
     };
 
     for (int c = it.c0; c < it.c1; ++c, ++seq) {
@@ -255,103 +277,113 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
       const int st = seq % NST;
       mbar_wait(&full[st], (uint32_t)(seq / NST) & 1u);
       if (probe) {  // (finite output: a state of one unit-weight zero row)
-        m_lo = m_hi = 0.f;
-        l_lo = l_hi = 1.f;
+#pragma unroll
+        for (int nq = 0; nq < 2; ++nq)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) m[nq][j] = 0.f, l[nq][j] = 1.f;
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
         continue;
       }
       const uint32_t kb = sbase + st * STAGE_BYTES, vb = kb + KV_BYTES;
-      const int kstart = c * CH + warp * 32;
-      // S = Q K_w^T for this warp's 32 keys
-      float s[4][4];
+      // (one or two 8-column n-tiles: the chunk body instantiated per count, no work on an empty one)
+      auto chunk_body = [&](auto nq_count) {
+        constexpr int NQ = decltype(nq_count)::value;
+        const int kstart = c * CH + warp * 32;
+        const int mi = lane >> 3, ri = lane & 7;
+        // S^T = K_w Q^T: m-tiles mt (16 keys each of this warp's 32) x n-tiles nq, 8 k-steps of 16 dims
+        float s[2][2][4];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
+        for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) s[nt][i] = 0.f;
+          for (int nq = 0; nq < NQ; ++nq)
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const int key = warp * 32 + nt * 8 + (lane & 7);
+            for (int i = 0; i < 4; ++i) s[mt][nq][i] = 0.f;
 #pragma unroll
-        for (int kp = 0; kp < 4; ++kp) {
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4(kb + swz(key, kp * 4 + (lane >> 3)), b0, b1, b2, b3);
-          mma16816(s[nt], qa[2 * kp], b0, b1);
-          mma16816(s[nt], qa[2 * kp + 1], b2, b3);
+        for (int kk = 0; kk < 8; ++kk) {
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            uint32_t a[4];
+            ldsm_x4(kb + swz(warp * 32 + mt * 16 + (mi & 1) * 8 + ri, kk * 2 + (mi >> 1)), a[0], a[1], a[2], a[3]);
+            mma16816(s[mt][0], a, qb[0][kk][0], qb[0][kk][1]);
+            if (NQ == 2) mma16816(s[mt][1], a, qb[1][kk][0], qb[1][kk][1]);
+          }
         }
-      }
-      // mask, new running max (exact; masked entries excluded)
-      float cm_lo = -INFINITY, cm_hi = -INFINITY;
+        // mask, new running max per column (exact; masked entries excluded)
+        float cm[2][2];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
+        for (int nq = 0; nq < NQ; ++nq) cm[nq][0] = cm[nq][1] = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int key = kstart + nt * 8 + 2 * t4 + (i & 1);
-          const bool hi = i >= 2;
-          const bool vis = hi ? (row_hi && key <= pos_hi) : (row_lo && key <= pos_lo);
-          const float v = vis ? s[nt][i] * scale_log2 : -INFINITY;
-          s[nt][i] = v;
-          if (hi) cm_hi = fmaxf(cm_hi, v); else cm_lo = fmaxf(cm_lo, v);
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int key = kstart + mt * 16 + g + 8 * (i >> 1), j = i & 1;
+              const bool vis = okq[nq][j] && key <= posq[nq][j];
+              const float v = vis ? s[mt][nq][i] * scale_log2 : -INFINITY;
+              s[mt][nq][i] = v;
+              cm[nq][j] = fmaxf(cm[nq][j], v);
+            }
+        float af[2][2];
+#pragma unroll
+        for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+#pragma unroll
+            for (int off = 4; off <= 16; off <<= 1) cm[nq][j] = fmaxf(cm[nq][j], __shfl_xor_sync(0xffffffffu, cm[nq][j], off));
+            const float mn = fmaxf(m[nq][j], cm[nq][j]);
+            af[nq][j] = (mn == -INFINITY) ? 1.f : exp2f(m[nq][j] - mn);
+            m[nq][j] = mn;
+          }
+        // P^T and its column sums; P^T's 8x8 blocks transposed in registers into the PV B fragments
+        uint32_t pb[2][2][2];  // [mt = PV k-step][nq][b0 | b1]
+        float ps[2][2];
+#pragma unroll
+        for (int nq = 0; nq < NQ; ++nq) ps[nq][0] = ps[nq][1] = 0.f;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nq = 0; nq < NQ; ++nq) {
+            float e[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) e[i] = (s[mt][nq][i] == -INFINITY) ? 0.f : exp2f(s[mt][nq][i] - m[nq][i & 1]);
+            ps[nq][0] += e[0] + e[2];
+            ps[nq][1] += e[1] + e[3];
+            pb[mt][nq][0] = movmatrix_trans(pack_bf16(e[0], e[1]));  // keys mt*16 + 0..7
+            pb[mt][nq][1] = movmatrix_trans(pack_bf16(e[2], e[3]));  // keys mt*16 + 8..15
+          }
+#pragma unroll
+        for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+#pragma unroll
+            for (int off = 4; off <= 16; off <<= 1) ps[nq][j] += __shfl_xor_sync(0xffffffffu, ps[nq][j], off);
+            l[nq][j] = l[nq][j] * af[nq][j] + ps[nq][j];
+          }
+        // (no column of the warp raised its max: every factor is exactly 1 and the rescale is the identity)
+        if (!__all_sync(0xffffffffu, af[0][0] == 1.f && af[0][1] == 1.f && (NQ == 1 || (af[1][0] == 1.f && af[1][1] == 1.f)))) {
+#pragma unroll
+          for (int md = 0; md < 8; ++md)
+#pragma unroll
+            for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) o[md][nq][i] *= af[nq][i & 1];
         }
+        // O^T += V_w^T P^T: m-tiles md (16 dims) x 2 k-steps (16 keys) x n-tiles nq
 #pragma unroll
-      for (int off = 1; off <= 2; off <<= 1) {
-        cm_lo = fmaxf(cm_lo, __shfl_xor_sync(0xffffffffu, cm_lo, off));
-        cm_hi = fmaxf(cm_hi, __shfl_xor_sync(0xffffffffu, cm_hi, off));
-      }
-      const float mn_lo = fmaxf(m_lo, cm_lo), mn_hi = fmaxf(m_hi, cm_hi);
-      const float a_lo = (mn_lo == -INFINITY) ? 1.f : exp2f(m_lo - mn_lo);
-      const float a_hi = (mn_hi == -INFINITY) ? 1.f : exp2f(m_hi - mn_hi);
-      m_lo = mn_lo;
-      m_hi = mn_hi;
-      // P (bf16 A fragments straight from the S accumulators) and its row sums
-      uint32_t pa[2][4];
-      float ps_lo = 0.f, ps_hi = 0.f;
+        for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        float e[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float M = i >= 2 ? mn_hi : mn_lo;
-          e[i] = (s[nt][i] == -INFINITY) ? 0.f : exp2f(s[nt][i] - M);
+          for (int md = 0; md < 8; ++md) {
+            uint32_t a[4];
+            ldsm_x4_t(vb + swz(warp * 32 + mt * 16 + (mi >> 1) * 8 + ri, md * 2 + (mi & 1)), a[0], a[1], a[2], a[3]);
+            mma16816(o[md][0], a, pb[mt][0][0], pb[mt][0][1]);
+            if (NQ == 2) mma16816(o[md][1], a, pb[mt][1][0], pb[mt][1][1]);
+          }
         }
-        ps_lo += e[0] + e[1];
-        ps_hi += e[2] + e[3];
-        // k-step kk = nt/2 (16 keys): a0,a1 = n-tile 2kk (rows g, g+8); a2,a3 = n-tile 2kk+1
-        pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(e[0], e[1]);
-        pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(e[2], e[3]);
-      }
-#pragma unroll
-      for (int off = 1; off <= 2; off <<= 1) {
-        ps_lo += __shfl_xor_sync(0xffffffffu, ps_lo, off);
-        ps_hi += __shfl_xor_sync(0xffffffffu, ps_hi, off);
-      }
-      l_lo = l_lo * a_lo + ps_lo;
-      l_hi = l_hi * a_hi + ps_hi;
-      // (no row of the warp raised its max: every factor is exactly 1 and the rescale is the identity)
-      if (!__all_sync(0xffffffffu, a_lo == 1.f && a_hi == 1.f)) {
-#pragma unroll
-        for (int nt = 0; nt < 16; ++nt) {
-          o[nt][0] *= a_lo;
-          o[nt][1] *= a_lo;
-          o[nt][2] *= a_hi;
-          o[nt][3] *= a_hi;
-        }
-      }
-      // O += P V_w: 2 k-steps (this warp's 32 keys) x 16 n-tiles (128 dims)
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {
-        const uint32_t a[4] = {pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3]};
-#pragma unroll
-        for (int np = 0; np < 8; ++np) {
-          const int mi = lane >> 3, ri = lane & 7;
-          const int key = warp * 32 + kk * 16 + (mi & 1) * 8 + ri;
-          const int chunk = np * 2 + (mi >> 1);
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4_t(vb + swz(key, chunk), b0, b1, b2, b3);
-          mma16816(o[2 * np], a, b0, b1);
-          mma16816(o[2 * np + 1], a, b2, b3);
-        }
-      }
+      };
+      if (two) chunk_body(std::integral_constant<int, 2>{});
+      else chunk_body(std::integral_constant<int, 1>{});
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
     }
@@ -364,19 +396,23 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
     };
     if (split && it.nseg > 1) {
       // ---- segment schedule: publish this segment's four warp states
-      auto pub = [&](int r, int hsel) {
-        const size_t base = (row_slot(r) * p.nchunk_max + it.seg) * 4 + warp;
 #pragma unroll
-        for (int nt = 0; nt < 16; ++nt)
-          *reinterpret_cast<float2*>(p.part_o + base * HD + nt * 8 + 2 * t4) =
-              make_float2(to[nt][2 * hsel], to[nt][2 * hsel + 1]);
-        if (t4 == 0) {
-          p.part_ml[2 * base] = hsel ? tm_hi : tm_lo;
-          p.part_ml[2 * base + 1] = hsel ? tl_hi : tl_lo;
+      for (int nq = 0; nq < 2; ++nq)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int q = nq * 8 + 2 * t4 + j;
+          if (q >= nr) continue;
+          const size_t bq = (row_slot(q) * p.nchunk_max + it.seg) * 4 + warp;
+#pragma unroll
+          for (int md = 0; md < 8; ++md) {
+            p.part_o[bq * HD + md * 16 + g] = to[md][nq][j];
+            p.part_o[bq * HD + md * 16 + g + 8] = to[md][nq][2 + j];
+          }
+          if (g == 0) {
+            p.part_ml[2 * bq] = tm[nq][j];
+            p.part_ml[2 * bq + 1] = tl[nq][j];
+          }
         }
-      };
-      if (g < nr) pub(g, 0);
-      if (g + 8 < nr) pub(g + 8, 1);
       named_bar(1, 128);
       if (tid == 0) {
         int prev;
@@ -442,23 +478,23 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
       }
     } else {
       // ---- merge the 4 warp states in fixed order and normalise
-      if (g < nr) {  // (rows of the tile past the block's rows are never read)
 #pragma unroll
-        for (int nt = 0; nt < 16; ++nt)
-          *reinterpret_cast<float2*>(mrg + (warp * 16 + g) * HD + nt * 8 + 2 * t4) = make_float2(to[nt][0], to[nt][1]);
-      }
-      if (g + 8 < nr) {
+      for (int nq = 0; nq < 2; ++nq)
 #pragma unroll
-        for (int nt = 0; nt < 16; ++nt)
-          *reinterpret_cast<float2*>(mrg + (warp * 16 + g + 8) * HD + nt * 8 + 2 * t4) =
-              make_float2(to[nt][2], to[nt][3]);
-      }
-      if (t4 == 0) {
-        mrg_m[warp * 16 + g] = tm_lo;
-        mrg_m[warp * 16 + g + 8] = tm_hi;
-        mrg_l[warp * 16 + g] = tl_lo;
-        mrg_l[warp * 16 + g + 8] = tl_hi;
-      }
+        for (int j = 0; j < 2; ++j) {
+          const int q = nq * 8 + 2 * t4 + j;
+          if (q < nr) {  // (rows of the tile past the block's rows are never read)
+#pragma unroll
+            for (int md = 0; md < 8; ++md) {
+              mrg[(warp * 16 + q) * HD + md * 16 + g] = to[md][nq][j];
+              mrg[(warp * 16 + q) * HD + md * 16 + g + 8] = to[md][nq][2 + j];
+            }
+          }
+          if (g == 0) {
+            mrg_m[warp * 16 + q] = tm[nq][j];
+            mrg_l[warp * 16 + q] = tl[nq][j];
+          }
+        }
     }
     named_bar(1, 128);
     // per-row merge factors once (row r: thread r): M = max_w m_w, f_w = 2^(m_w - M), L = sum_w l_w f_w
