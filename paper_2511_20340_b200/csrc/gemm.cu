@@ -1475,25 +1475,30 @@ bool gemm_partial_geom(int T, int N, int K, PartialGeom* g, int drain) {
 // sums, so a row streams at memory speed and a few rows (B = 1) still spread over many warps.
 constexpr int kRnMaxSeg = 16;  // k segments per 128-column tile (stream-K: <= G / n_tiles + 2)
 constexpr int kRnMaxTiles = 128;
-// float4 groups per thread: two where the width allows it (d = 4096: 512-thread rows, two resident per
-// SM -- a T = 320 block in about one wave instead of 2.2 with 1024-thread rows), else the fewest that fit
+// float4 groups per virtual thread of the row's canonical reduction tree: the fewest that fit 1024
+// threads (the tree -- and so every bit -- depends on d only)
 static int rn_ng(int d) {
-  if (d % (4 * 2 * 32) == 0 && d / 8 <= 1024) return 2;
   for (int ng = 1; ng <= 4; ++ng)
     if (d % (4 * ng * 32) == 0 && d / (4 * ng) <= 1024) return ng;
   return 0;
 }
 
-template <int NG>
+// The canonical row kernel has nv = d / (4 NG) virtual threads; virtual thread v owns float4 column
+// groups v + nv j (j < NG), its sum of squares is an fma chain over them, a warp_sum per 32-thread
+// virtual warp and one final warp_sum over the virtual warps' sums. A launch runs it with F virtual
+// threads per real thread (v = tid + nthr f): F = 2 halves the threads of a row so two rows are
+// resident per SM at a 320-row block (one wave instead of 2.2); the arithmetic -- and every bit -- is
+// the same for either F, so F is chosen per launch (T) without breaking batch invariance.
+template <int NG, int F>
 __global__ void __launch_bounds__(1024) resid_norm_kernel(
     const float* __restrict__ partial, int G, int kb, int drain, int CG, int n_tiles_cta, int T, int rep, int d,
     const float* resid, const float* __restrict__ add, const float* __restrict__ bias, float* out, float* tap,
     const float* __restrict__ gamma, float eps, __nv_bfloat16* xn) {
-  constexpr int kRnBatch = 8 / NG;
+  constexpr int kRnBatch = (8 / NG) / F;  // partial loads in flight per column group
   __shared__ int seg_n[kRnMaxTiles];
   __shared__ int seg_off[kRnMaxTiles][kRnMaxSeg];  // slot * T * 128 (the tile's k segments, k order)
   __shared__ float red[32];
-  const int nthr = blockDim.x;
+  const int nthr = blockDim.x, nv = nthr * F;
   const int r = blockIdx.x;
   const int src_row = r / rep, col0 = (r % rep) * d;
   const int tid = threadIdx.x;
@@ -1516,115 +1521,105 @@ __global__ void __launch_bounds__(1024) resid_norm_kernel(
   pdl_wait();
   kt_.mark();
   pdl_trigger();
-  float4 x[NG];
-  float ss = 0.f;
+  float4 x[F][NG];
 #pragma unroll
-  for (int j = 0; j < NG; ++j) {
-    const int i = 4 * tid + 4 * nthr * j;  // column within the virtual row
-    x[j] = resid ? *reinterpret_cast<const float4*>(resid + (size_t)r * d + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-    if (add) {  // (tensor parallelism: the all-reduced row-parallel GEMM output)
-      const float4 a = *reinterpret_cast<const float4*>(add + (size_t)r * d + i);
-      x[j].x += a.x;
-      x[j].y += a.y;
-      x[j].z += a.z;
-      x[j].w += a.w;
+  for (int f = 0; f < F; ++f)
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+      const int i = 4 * (tid + nthr * f) + 4 * nv * j;  // column within the virtual row
+      x[f][j] = resid ? *reinterpret_cast<const float4*>(resid + (size_t)r * d + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (add) {  // (tensor parallelism: the all-reduced row-parallel GEMM output)
+        const float4 a = *reinterpret_cast<const float4*>(add + (size_t)r * d + i);
+        x[f][j].x += a.x;
+        x[f][j].y += a.y;
+        x[f][j].z += a.z;
+        x[f][j].w += a.w;
+      }
+      if (bias) {
+        const float4 bb = *reinterpret_cast<const float4*>(bias + col0 + i);
+        x[f][j].x += bb.x;
+        x[f][j].y += bb.y;
+        x[f][j].z += bb.z;
+        x[f][j].w += bb.w;
+      }
     }
-    if (bias) {
-      const float4 bb = *reinterpret_cast<const float4*>(bias + col0 + i);
-      x[j].x += bb.x;
-      x[j].y += bb.y;
-      x[j].z += bb.z;
-      x[j].w += bb.w;
-    }
-  }
   if (partial) {
-    if constexpr (NG == 2) {
-      // both column groups' segment loads in flight together (then the k-ordered sums per group)
-      const int n0 = col0 + 4 * tid, n1 = n0 + 4 * nthr;
-      const int vt0 = n0 / BM, vt1 = n1 / BM;
-      const int ns0 = seg_n[vt0], ns1 = seg_n[vt1], nsm = max(ns0, ns1);
-      const float* bp0 = partial + (size_t)src_row * BM + n0 % BM;
-      const float* bp1 = partial + (size_t)src_row * BM + n1 % BM;
-      for (int q0 = 0; q0 < nsm; q0 += 4) {
-        float4 pa[4], pb[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (q0 + q < ns0) pa[q] = __ldcg(reinterpret_cast<const float4*>(bp0 + seg_off[vt0][q0 + q]));
-          if (q0 + q < ns1) pb[q] = __ldcg(reinterpret_cast<const float4*>(bp1 + seg_off[vt1][q0 + q]));
-        }
+    for (int j = 0; j < NG; ++j) {
+      // the F column groups' segment loads in flight together, then each group's k-ordered sums
+      int vt[F], ns[F], nsm = 0;
+      const float* bp[F];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {  // k order
-          if (q0 + q < ns0) {
-            x[0].x += pa[q].x;
-            x[0].y += pa[q].y;
-            x[0].z += pa[q].z;
-            x[0].w += pa[q].w;
-          }
-          if (q0 + q < ns1) {
-            x[1].x += pb[q].x;
-            x[1].y += pb[q].y;
-            x[1].z += pb[q].z;
-            x[1].w += pb[q].w;
-          }
-        }
+      for (int f = 0; f < F; ++f) {
+        const int n = col0 + 4 * (tid + nthr * f) + 4 * nv * j;
+        vt[f] = n / BM;
+        ns[f] = seg_n[vt[f]];
+        nsm = max(nsm, ns[f]);
+        bp[f] = partial + (size_t)src_row * BM + n % BM;
       }
-    } else {
+      for (int q0 = 0; q0 < nsm; q0 += kRnBatch) {
+        float4 pv[F][kRnBatch];
 #pragma unroll
-      for (int j = 0; j < NG; ++j) {
-        const int n = col0 + 4 * tid + 4 * nthr * j;
-        const int vt = n / BM, m = n % BM;
-        const int ns = seg_n[vt];
-        const float* bp = partial + (size_t)src_row * BM + m;
-        for (int q0 = 0; q0 < ns; q0 += kRnBatch) {
-          float4 pv[kRnBatch];
+        for (int q = 0; q < kRnBatch; ++q)
 #pragma unroll
-          for (int q = 0; q < kRnBatch; ++q)
-            if (q0 + q < ns) pv[q] = __ldcg(reinterpret_cast<const float4*>(bp + seg_off[vt][q0 + q]));
+          for (int f = 0; f < F; ++f)
+            if (q0 + q < ns[f]) pv[f][q] = __ldcg(reinterpret_cast<const float4*>(bp[f] + seg_off[vt[f]][q0 + q]));
 #pragma unroll
-          for (int q = 0; q < kRnBatch; ++q)
-            if (q0 + q < ns) {  // k order
-              x[j].x += pv[q].x;
-              x[j].y += pv[q].y;
-              x[j].z += pv[q].z;
-              x[j].w += pv[q].w;
+        for (int q = 0; q < kRnBatch; ++q)
+#pragma unroll
+          for (int f = 0; f < F; ++f)
+            if (q0 + q < ns[f]) {  // k order
+              x[f][j].x += pv[f][q].x;
+              x[f][j].y += pv[f][q].y;
+              x[f][j].z += pv[f][q].z;
+              x[f][j].w += pv[f][q].w;
             }
-        }
       }
     }
   }
+  float ss[F];
 #pragma unroll
-  for (int j = 0; j < NG; ++j) {
-    const int i = 4 * tid + 4 * nthr * j;
-    if (out) *reinterpret_cast<float4*>(out + (size_t)r * d + i) = x[j];
-    if (tap) *reinterpret_cast<float4*>(tap + (size_t)r * d + i) = x[j];
-    ss = fmaf(x[j].x, x[j].x, ss);
-    ss = fmaf(x[j].y, x[j].y, ss);
-    ss = fmaf(x[j].z, x[j].z, ss);
-    ss = fmaf(x[j].w, x[j].w, ss);
+  for (int f = 0; f < F; ++f) {
+    ss[f] = 0.f;
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+      const int i = 4 * (tid + nthr * f) + 4 * nv * j;
+      if (out) *reinterpret_cast<float4*>(out + (size_t)r * d + i) = x[f][j];
+      if (tap) *reinterpret_cast<float4*>(tap + (size_t)r * d + i) = x[f][j];
+      ss[f] = fmaf(x[f][j].x, x[f][j].x, ss[f]);
+      ss[f] = fmaf(x[f][j].y, x[f][j].y, ss[f]);
+      ss[f] = fmaf(x[f][j].z, x[f][j].z, ss[f]);
+      ss[f] = fmaf(x[f][j].w, x[f][j].w, ss[f]);
+    }
   }
   if (!gamma) return;
-  // fixed reduction tree (depends on d only): warp shuffles, then warp 0 over the warp sums
-  ss = warp_sum(ss);
-  if ((tid & 31) == 0) red[tid >> 5] = ss;
+  // the canonical tree: a warp_sum per virtual warp, then warp 0 over the virtual warps' sums in order
+#pragma unroll
+  for (int f = 0; f < F; ++f) {
+    const float v = warp_sum(ss[f]);
+    if ((tid & 31) == 0) red[(tid >> 5) + (nthr >> 5) * f] = v;
+  }
   __syncthreads();
   if (tid < 32) {
-    float v = (tid < (nthr >> 5)) ? red[tid] : 0.f;
+    float v = (tid < (nv >> 5)) ? red[tid] : 0.f;
     v = warp_sum(v);
     if (tid == 0) red[0] = v;
   }
   __syncthreads();
   const float rs = 1.0f / sqrtf(red[0] / (float)d + eps);
 #pragma unroll
-  for (int j = 0; j < NG; ++j) {
-    const int i = 4 * tid + 4 * nthr * j;
-    const float4 gg = *reinterpret_cast<const float4*>(gamma + i);
-    __nv_bfloat162 lo = __floats2bfloat162_rn(x[j].x * rs * gg.x, x[j].y * rs * gg.y);
-    __nv_bfloat162 hi = __floats2bfloat162_rn(x[j].z * rs * gg.z, x[j].w * rs * gg.w);
-    uint2 pk;
-    pk.x = *reinterpret_cast<uint32_t*>(&lo);
-    pk.y = *reinterpret_cast<uint32_t*>(&hi);
-    *reinterpret_cast<uint2*>(xn + (size_t)r * d + i) = pk;
-  }
+  for (int f = 0; f < F; ++f)
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+      const int i = 4 * (tid + nthr * f) + 4 * nv * j;
+      const float4 gg = *reinterpret_cast<const float4*>(gamma + i);
+      __nv_bfloat162 lo = __floats2bfloat162_rn(x[f][j].x * rs * gg.x, x[f][j].y * rs * gg.y);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(x[f][j].z * rs * gg.z, x[f][j].w * rs * gg.w);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(xn + (size_t)r * d + i) = pk;
+    }
 }
 
 cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T, int rep, int d, const float* resid,
@@ -1645,17 +1640,24 @@ cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T,
     const int groups = G / CG;
     if ((groups + nt / CG - 1) / (nt / CG) + 1 > kRnMaxSeg) return cudaErrorInvalidValue;
   }
-  const dim3 grid(T * rep), block(d / (4 * ng));
+  const int nv = d / (4 * ng);  // the canonical tree's virtual threads
+  // more rows than SMs: half the threads per row (two virtual threads each) so two rows fit an SM
+  static const int env_f = getenv("SF_RN_FOLD") ? atoi(getenv("SF_RN_FOLD")) : -1;  // (tests: 1 / 2)
+  const bool fold = env_f >= 0 ? env_f == 2 : T * rep > num_sms();
+  const dim3 grid(T * rep);
+#define SF_RN(NGV)                                                                                                  \
+  return (fold && ng == 1 && nv % 64 == 0)                                                                          \
+             ? launch_k(resid_norm_kernel<NGV, 2>, grid, dim3(nv / 2), 0, st, partial, G, kb, drain, CG, nt, Tslot,  \
+                        rep, d, resid, add, bias, out, tap, gamma, eps, xn)                                          \
+             : launch_k(resid_norm_kernel<NGV, 1>, grid, dim3(nv), 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, \
+                        d, resid, add, bias, out, tap, gamma, eps, xn)
   switch (ng) {
-    case 1: return launch_k(resid_norm_kernel<1>, grid, block, 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, d, resid,
-                            add, bias, out, tap, gamma, eps, xn);
-    case 2: return launch_k(resid_norm_kernel<2>, grid, block, 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, d, resid,
-                            add, bias, out, tap, gamma, eps, xn);
-    case 3: return launch_k(resid_norm_kernel<3>, grid, block, 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, d, resid,
-                            add, bias, out, tap, gamma, eps, xn);
-    default: return launch_k(resid_norm_kernel<4>, grid, block, 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, d, resid,
-                             add, bias, out, tap, gamma, eps, xn);
+    case 1: SF_RN(1);
+    case 2: SF_RN(2);
+    case 3: SF_RN(3);
+    default: SF_RN(4);
   }
+#undef SF_RN
 }
 
 // Whether the fused consumer supports this (d, N, K): callers use the unfused path otherwise.

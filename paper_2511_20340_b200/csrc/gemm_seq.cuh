@@ -68,7 +68,6 @@ SF_DEV float* seq_ss(int* sy, int ph, int row) {  // [32] per-virtual-warp sums 
 static_assert(64 + kSeqMaxPhases * kSeqRows * (4 + 32) <= kSeqSyncInts, "sync block");
 
 SF_DEV int rn_ng_dev(int d) {  // float4 groups per virtual thread (rn_ng, device copy)
-  if (d % (4 * 2 * 32) == 0 && d / 8 <= 1024) return 2;
   for (int ng = 1; ng <= 4; ++ng)
     if (d % (4 * ng * 32) == 0 && d / (4 * ng) <= 1024) return ng;
   return 0;
