@@ -1382,17 +1382,31 @@ sf_status specformer_prefill(sf_handle* h, const int32_t* tokens, int32_t B, int
   // chunk rows per sequence for THIS batch (one 512-row GEMM pass per chunk; a handle sized for a large
   // batch prefills a small one in few chunks), within the plan's row capacity
   static const int pf_cap = getenv("SF_PF_CAP") ? atoi(getenv("SF_PF_CAP")) : 512;
-  const int C = std::max(p.k + 1, std::min(std::min(pf_cap, std::max(1, 512 / B)), p.R / B));
-  int Cc = 0;
-  for (int c0 = 0; c0 < P; c0 += C) {
-    Cc = std::min(C, P - c0);
-    SF_TRY(launch_build_prefill_rows(B, P, c0, Cc, h->prompt, h->tok_rows, h->pos0_pf, h->st));
-    SF_TRY(base_forward(h, B * Cc, Cc, h->pos0_pf, c0 + Cc, /*final_norm=*/false));
-    if (p.k > 0) SF_TRY(ctx_forward(h, B * Cc, Cc, h->pos0_pf, c0 + Cc));
+  // Sequence groups: Bg sequences per pass with as many rows each as a 512-row pass holds (P = 512: one
+  // sequence per pass), so each pass's attention reads one group's KV prefix (L2-resident) instead of
+  // every sequence's. The same rows, positions and weight passes as chunking all B sequences together
+  // (every row's arithmetic is independent of the block it runs in, C23): the same bits.
+  static const bool grouped = !getenv("SF_PF_GROUP") || atoi(getenv("SF_PF_GROUP")) != 0;
+  const int Bg = grouped ? std::max(1, std::min(B, std::max(1, std::min(pf_cap, p.R) / std::max(1, P)))) : B;
+  const int C = std::max(p.k + 1, std::min(std::min(pf_cap, std::max(1, 512 / Bg)), p.R / Bg));
+  int* bt_all = h->bt;
+  for (int b0 = 0; b0 < B; b0 += Bg) {
+    const int nb = std::min(Bg, B - b0);
+    h->bt = bt_all + (size_t)b0 * p.pps;  // the group's page-table rows as rows 0 .. nb - 1
+    int Cc = 0;
+    cudaError_t e = cudaSuccess;
+    for (int c0 = 0; c0 < P && e == cudaSuccess; c0 += C) {
+      Cc = std::min(C, P - c0);
+      e = launch_build_prefill_rows(nb, P, c0, Cc, h->prompt + (size_t)b0 * P, h->tok_rows, h->pos0_pf, h->st);
+      if (e == cudaSuccess) e = base_forward(h, nb * Cc, Cc, h->pos0_pf, c0 + Cc, /*final_norm=*/false);
+      if (e == cudaSuccess && p.k > 0) e = ctx_forward(h, nb * Cc, Cc, h->pos0_pf, c0 + Cc);
+    }
+    h->bt = bt_all;
+    SF_TRY(e);
+    // last prompt row per sequence: I_D row (draft input) and the final hidden state (LM head -> g0)
+    if (p.k > 0) SF_TRY(launch_gather_rows(h->ctx, Cc, nullptr, Cc - 1, nb, p.d, h->idrow + (size_t)b0 * p.d, h->st));
+    SF_TRY(launch_gather_rows(h->resid, Cc, nullptr, Cc - 1, nb, p.d, h->hlast + (size_t)b0 * p.d, h->st));
   }
-  // last prompt row per sequence: I_D row (draft input) and LM head -> g0
-  if (p.k > 0) SF_TRY(launch_gather_rows(h->ctx, Cc, nullptr, Cc - 1, B, p.d, h->idrow, h->st));
-  SF_TRY(launch_gather_rows(h->resid, Cc, nullptr, Cc - 1, B, p.d, h->hlast, h->st));
   SF_TRY(head_argmax(h, h->hlast, B, h->logits, h->g_pf));
   SF_TRY(launch_prefill_finish(B, P, h->g_pf, h->seq_len, h->n_prev, h->last_token, h->r_b, h->prompt_len, nullptr,
                                h->st));
