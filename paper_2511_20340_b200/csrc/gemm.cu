@@ -1642,7 +1642,8 @@ cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T,
   }
   const int nv = d / (4 * ng);  // the canonical tree's virtual threads
   // more rows than SMs: half the threads per row (two virtual threads each) so two rows fit an SM
-  static const int env_f = getenv("SF_RN_FOLD") ? atoi(getenv("SF_RN_FOLD")) : -1;  // (tests: 1 / 2)
+  const char* env_fs = getenv("SF_RN_FOLD");  // (read per launch: tests force 1 / 2)
+  const int env_f = env_fs ? atoi(env_fs) : -1;
   const bool fold = env_f >= 0 ? env_f == 2 : T * rep > num_sms();
   const dim3 grid(T * rep);
 #define SF_RN(NGV)                                                                                                  \

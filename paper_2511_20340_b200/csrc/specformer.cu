@@ -1386,7 +1386,8 @@ sf_status specformer_prefill(sf_handle* h, const int32_t* tokens, int32_t B, int
   // sequence per pass), so each pass's attention reads one group's KV prefix (L2-resident) instead of
   // every sequence's. The same rows, positions and weight passes as chunking all B sequences together
   // (every row's arithmetic is independent of the block it runs in, C23): the same bits.
-  static const bool grouped = !getenv("SF_PF_GROUP") || atoi(getenv("SF_PF_GROUP")) != 0;
+  const char* env_g = getenv("SF_PF_GROUP");  // (read per call: tests compare both)
+  const bool grouped = !env_g || atoi(env_g) != 0;
   const int Bg = grouped ? std::max(1, std::min(B, std::max(1, std::min(pf_cap, p.R) / std::max(1, P)))) : B;
   const int C = std::max(p.k + 1, std::min(std::min(pf_cap, std::max(1, 512 / Bg)), p.R / Bg));
   int* bt_all = h->bt;

@@ -564,3 +564,29 @@ def test_layer_seq_block_sizes_change_on_one_handle():
         big.profile(False)
         toks = [t for t in em.cpu().numpy().reshape(-1) if t >= 0]
         assert toks[:11] == ref[0][1:12], it
+
+
+# ------------------------------------------------------------------ launch shapes that must not change bits
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [W7D2.replace(name="7b-d2-b4", batch=4, prompt_len=200), GQA],
+                         ids=["7b_width", "gqa4"])
+def test_launch_shape_switches_bit_exact(cfg, monkeypatch):
+    """Per-launch shape choices that keep every row's arithmetic: the residual + RMSNorm consumer with one
+    or two virtual threads per real thread (SF_RN_FOLD 1 / 2: the canonical reduction tree either way) and
+    the prefill in sequence groups or all sequences per pass (SF_PF_GROUP 1 / 0). Logits, draft logits,
+    tokens and accept lengths are bit-identical across the four combinations, with ragged forced
+    acceptance (prompt 200: prefill groups of 2 sequences)."""
+    w, prompts = setup(cfg, seed=31, jitter=0.1)
+    k, n_steps = cfg.draft_len, 4
+    ar = run_gpu(cfg, w, prompts, n_steps * (k + 1) + k + 2, k=0)["tokens"]
+    slots = corrupt_slots(n_steps, cfg.batch, k, seed=11)
+    runs = []
+    for fold, group in (("1", "1"), ("2", "1"), ("1", "0"), ("2", "0")):
+        monkeypatch.setenv("SF_RN_FOLD", fold)
+        monkeypatch.setenv("SF_PF_GROUP", group)
+        runs.append(forced_run(cfg, w, prompts, n_steps, slots, ar))
+    for other in runs[1:]:
+        for s1, s2 in zip(runs[0]["steps"], other["steps"]):
+            for key in ("logits", "draft_logits", "greedy", "m", "emitted", "seq_len", "last_token"):
+                assert np.array_equal(s1[key], s2[key]), key
+    check_commit_integers(cfg, prompts, runs[0])
