@@ -147,10 +147,12 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
       const int kmax = item_of(item, it);
       for (int c = it.c0; c < it.c1; ++c, ++seq) {
         const int st = seq % NST;
-        mbar_wait(&empty[st], ((uint32_t)(seq / NST) & 1u) ^ 1u);
         const int kstart = c * CH;
         const int npages = (min(CH, kmax + 1 - kstart) + 15) / 16;
+        // the chunk's page-table entries are requested before waiting for the slot (the load's latency
+        // hides behind the wait instead of delaying the TMA issue once the slot is free)
         const int pg = (lane < npages) ? p.block_table[it.b * p.pages_per_seq + kstart / 16 + lane] : 0;
+        mbar_wait(&empty[st], ((uint32_t)(seq / NST) & 1u) ^ 1u);
         const int pg0 = __shfl_sync(0xffffffffu, pg, 0);
         // the chunk's pages are consecutive in the pool (the identity page table, and any run of a
         // permuted one): 4 TMA boxes of 8 pages x 16 keys x 64 dims instead of 32 one-page boxes

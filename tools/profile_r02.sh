@@ -15,6 +15,9 @@ CMD="python bench.py --batch 64 --steps 2 --warmup 3 --windows 1 --sweep none --
 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled \
     -k "regex:gemm_sk_kernel|attn_fd_kernel|resid_norm|rope_partial" -s 12 -c 6 -o $OUT/full_b64 -f $CMD > $OUT/ncu_full_b64.log 2>&1
 echo "full b64 rc=$?"
+ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled \
+    -k "regex:attn_fd_kernel" -s 2 -c 1 -o $OUT/full_attn_b64 -f $CMD > $OUT/ncu_full_attn_b64.log 2>&1
+echo "full attn b64 rc=$?"
 CMD1="python bench.py --batch 1 --steps 2 --warmup 3 --windows 1 --sweep none --no-cpu-baseline --forced-steps 0 --e2e-steps 2 --timeline-steps 0 --profile-steps 1"
 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled \
     -k "regex:gemm_sk_kernel|attn_fd_kernel" -s 8 -c 5 -o $OUT/full_b1 -f $CMD1 > $OUT/ncu_full_b1.log 2>&1
