@@ -26,7 +26,8 @@ SMALL = get_config("small")
 
 # ------------------------------------------------------------------ GEMM kernel parity
 @pytest.mark.parametrize("T,Nn,K", [(1, 128, 64), (5, 256, 128), (16, 384, 4096), (40, 768, 768), (77, 2304, 768),
-                                    (320, 4096, 4096), (600, 1024, 256), (8, 32000, 768), (257, 512, 11008)])
+                                    (320, 4096, 4096), (600, 1024, 256), (8, 32000, 768), (257, 512, 11008),
+                                    (384, 4096, 4096), (336, 2304, 768), (352, 512, 11008)])
 def test_gemm_bf16_tcgen05(T, Nn, K):
     g = torch.Generator().manual_seed(T * 7 + Nn + K)
     A = torch.randn(T, K, generator=g).to(torch.bfloat16)
@@ -37,6 +38,22 @@ def test_gemm_bf16_tcgen05(T, Nn, K):
     err = (out - ref).abs()
     tol = 2e-5 * (A.double().abs() @ W.double().abs().T) + 1e-6
     assert (err <= tol).all(), f"max err {err.max().item()} worst ratio {(err / tol).max().item()}"
+
+
+@pytest.mark.parametrize("Nn,K", [(4096, 4096), (22016, 4096), (512, 11008)])
+def test_gemm_rows_independent_of_block(Nn, K):
+    """Batch invariance of the tcgen05 GEMM across every accumulator shape: the rows of a 384-row block
+    (two 192-column sub-tiles, one accumulator), a 320-row block (two 160-column sub-tiles, rotating
+    through three TMEM slots), a 256-row block (one sub-tile, double-buffered) and a 16-row block are
+    bit-identical."""
+    g = torch.Generator().manual_seed(Nn + K)
+    A = torch.randn(384, K, generator=g).to(torch.bfloat16).cuda()
+    W = (0.02 * torch.randn(Nn, K, generator=g)).to(torch.bfloat16).cuda()
+    full = run_gemm(A, W)
+    for T in (320, 256, 16):
+        part = run_gemm(A[:T].contiguous(), W)
+        torch.cuda.synchronize()
+        assert torch.equal(part, full[:T]), T
 
 
 @pytest.mark.parametrize("T,Nn,K", [(1, 64, 16), (5, 512, 64), (33, 100, 70)])
