@@ -33,7 +33,12 @@ constexpr int CH = 128;
 constexpr int NST = 3;
 constexpr int KV_BYTES = CH * HD * 2;      // 32 KB
 constexpr int STAGE_BYTES = 2 * KV_BYTES;  // 64 KB
-constexpr int MERGE_BYTES = 4 * 16 * (HD + 2) * 4;  // per-warp O, m, l for the final merge
+constexpr int NW = kAttnWarps;      // compute warps
+constexpr int KPW = CH / NW;         // keys per warp slice of a chunk (one 16-key m-tile)
+constexpr int TR = kAttnTileRows;    // query rows per tile (one 8-column n-tile)
+constexpr int NTHR = (NW + 1) * 32;  // + the TMA producer warp
+static_assert(KPW == 16 && TR == 8, "one m-tile of keys and one n-tile of queries per warp");
+constexpr int MERGE_BYTES = NW * TR * (HD + 2) * 4;  // per-warp O, m, l for the final merge
 constexpr int SMEM = NST * STAGE_BYTES + MERGE_BYTES + 2 * NST * 8 + 1024 + 64 + 16;
 
 SF_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
@@ -76,23 +81,23 @@ struct Item {
 
 }  // namespace
 
-// item = (b * Hkv + kvh) * ntiles + qt. Warps 0..3 compute, warp 4 produces.
-__global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__ CUtensorMap tmK,
-                                                        const __grid_constant__ CUtensorMap tmV,
-                                                        const __grid_constant__ CUtensorMap tmK4,
-                                                        const __grid_constant__ CUtensorMap tmV4, AttnParams p,
-                                                        int ntiles, int nseg_max, int seg_keys, int n_items,
-                                                        int split_arg) {
+// item = (b * Hkv + kvh) * ntiles + qt. Warps 0..NW-1 compute, warp NW produces.
+__global__ void __launch_bounds__(NTHR, 1) attn_fd_kernel(const __grid_constant__ CUtensorMap tmK,
+                                                         const __grid_constant__ CUtensorMap tmV,
+                                                         const __grid_constant__ CUtensorMap tmK4,
+                                                         const __grid_constant__ CUtensorMap tmV4, AttnParams p,
+                                                         int ntiles, int nseg_max, int seg_keys, int n_items,
+                                                         int split_arg) {
   const int split = split_arg & 1;
   const bool probe = (split_arg & 2) != 0;  // (SF_ATTN_PROBE, measurement only: stream the chunks, no math)
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   const uint32_t raw = smem_u32(sm_raw);
   uint8_t* sm = sm_raw + (((raw + 1023u) & ~1023u) - raw);
   const uint32_t sbase = smem_u32(sm);
-  float* mrg = reinterpret_cast<float*>(sm + NST * STAGE_BYTES);  // [4][16][HD] O, then [4][16] m, l
-  float* mrg_m = mrg + 4 * 16 * HD;
-  float* mrg_l = mrg_m + 4 * 16;
-  uint64_t* full = reinterpret_cast<uint64_t*>(mrg_l + 4 * 16);
+  float* mrg = reinterpret_cast<float*>(sm + NST * STAGE_BYTES);  // [NW][TR][HD] O, then [NW][TR] m, l
+  float* mrg_m = mrg + NW * TR * HD;
+  float* mrg_l = mrg_m + NW * TR;
+  uint64_t* full = reinterpret_cast<uint64_t*>(mrg_l + NW * TR);
   uint64_t* empty = full + NST;
   int* mrg_flag = reinterpret_cast<int*>(empty + NST);
 
@@ -113,8 +118,8 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
     r /= ntiles;
     it.kvh = r % p.Hkv;
     it.b = r / p.Hkv;
-    const int r0 = it.qt * 16;
-    const int nr = min(16, R - r0);
+    const int r0 = it.qt * TR;
+    const int nr = min(TR, R - r0);
     const int kmax = min(p.pos0[it.b] + attn_row_last(p, min(p.q_len - 1, (r0 + nr - 1) / G)), p.max_key - 1);
     const int nch = kmax / CH + 1;
     it.nseg = (nch + seg_ch - 1) / seg_ch;
@@ -126,7 +131,7 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 4);  // one arrival per compute warp
+      mbar_init(&empty[s], NW);  // one arrival per compute warp
     }
     fence_barrier_init();
   }
@@ -139,7 +144,7 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
   kt_.mark();
   pdl_trigger();
 
-  if (warp == 4) {
+  if (warp == NW) {
     // ---- TMA producer
     int seq = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -154,10 +159,11 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
         const int pg = (lane < npages) ? p.block_table[it.b * p.pages_per_seq + kstart / 16 + lane] : 0;
         mbar_wait(&empty[st], ((uint32_t)(seq / NST) & 1u) ^ 1u);
         const int pg0 = __shfl_sync(0xffffffffu, pg, 0);
-        // the chunk's pages are consecutive in the pool (the identity page table, and any run of a
-        // permuted one): 4 TMA boxes of 8 pages x 16 keys x 64 dims instead of 32 one-page boxes
-        // (pages past the sequence's last key are masked; the pool is zero-initialised, so they are finite)
-        const bool run = __all_sync(0xffffffffu, lane >= npages || pg == pg0 + lane);
+        // a full chunk whose pages are consecutive in the pool (the identity page table, and any run of a
+        // permuted one): 4 TMA boxes of 8 pages x 16 keys x 64 dims instead of 32 one-page boxes. A tail
+        // chunk loads just its npages pages: boxes past the last key would be HBM bytes the math masks away
+        // (~16% of the KV stream at a 512-key prompt); the stale rows left in the slot are finite
+        const bool run = npages == 8 && __all_sync(0xffffffffu, lane >= npages || pg == pg0 + lane);
         if (run) {
           if (lane == 0) {
             mbar_arrive_expect_tx(&full[st], (uint32_t)(4 * 8 * 16 * 128));
@@ -193,199 +199,146 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
     return;
   }
 
-  // ---- compute warps. Keys are the MMA rows (S^T = K Q^T, O^T += V^T P^T): a 16-row query tile
-  // occupies one or two 8-column n-tiles, so a decode block of <= 8 rows (q_len (k+1) x G) costs half
-  // the MMAs of a 16-row M tile. A column's arithmetic never depends on the other columns or on the
-  // tile's row count (batch invariance, C23).
+  // ---- compute warps. Keys are the MMA rows (S^T = K Q^T, O^T += V^T P^T): warp w's 16 keys of a chunk
+  // are one m-tile, the tile's <= 8 query rows one 8-column n-tile. A column's arithmetic never depends
+  // on the other columns or on the tile's row count (batch invariance, C23).
   const float scale_log2 = 0.08838834764831845f * 1.4426950408889634f;  // log2(e) / sqrt(128)
+  const int mi = lane >> 3, ri = lane & 7;
   int seq = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     Item it;
     item_of(item, it);
     if (it.c0 >= it.c1) continue;  // segment beyond this group's keys
     const unsigned long long ti0 = g_kt.rec ? kt_now() : 0ull;
-    const int r0 = it.qt * 16;
-    const int nr = min(16, R - r0);
-    const bool two = nr > 8;  // (warp-uniform) the second 8-column n-tile holds rows
+    const int r0 = it.qt * TR;
+    const int nr = min(TR, R - r0);
     const int base = p.pos0[it.b];
-    // Q^T B fragments: query column q = nq*8 + g, dims kk*16 + 2 t4 (+1) and + 8 (bf16, rope_append's RNE)
-    uint32_t qb[2][8][2];
-#pragma unroll
-    for (int nq = 0; nq < 2; ++nq) {
-      const int r = nq * 8 + g;
-      const bool ok = r < nr;
-      const int rr = r0 + (ok ? r : 0), qi = rr / G, h = it.kvh * G + rr % G;
+    // Q^T B fragments: query column q = g, dims kk*16 + 2 t4 (+1) and + 8 (bf16, rope_append's RNE)
+    uint32_t qb[8][2];
+    {
+      const bool ok = g < nr;
+      const int rr = r0 + (ok ? g : 0), qi = rr / G, h = it.kvh * G + rr % G;
       const uint32_t* qrow = reinterpret_cast<const uint32_t*>(reinterpret_cast<const __nv_bfloat16*>(p.q) +
                                                                ((size_t)(it.b * p.q_len + qi) * p.Hq + h) * HD);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const int d0 = kk * 16 + 2 * t4;
-        qb[nq][kk][0] = ok ? qrow[d0 / 2] : 0u;
-        qb[nq][kk][1] = ok ? qrow[(d0 + 8) / 2] : 0u;
+        qb[kk][0] = ok ? qrow[d0 / 2] : 0u;
+        qb[kk][1] = ok ? qrow[(d0 + 8) / 2] : 0u;
       }
     }
-    // this thread's query columns q = nq*8 + 2 t4 + j: visibility bound (last visible key)
-    int posq[2][2];
-    bool okq[2][2];
+    // this thread's query columns q = 2 t4 + j: visibility bound (last visible key)
+    int posq[2];
+    bool okq[2];
 #pragma unroll
-    for (int nq = 0; nq < 2; ++nq)
+    for (int j = 0; j < 2; ++j) {
+      const int q = 2 * t4 + j;
+      okq[j] = q < nr;
+      posq[j] = base + attn_row_last(p, (r0 + min(q, nr - 1)) / G);
+    }
+    // the last key any column of the tile sees: a warp slice past it is fully masked, and its chunk step
+    // would leave (m, l, O) unchanged -- the warp skips it
+    int wlast = max(okq[0] ? posq[0] : -1, okq[1] ? posq[1] : -1);
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int q = nq * 8 + 2 * t4 + j;
-        okq[nq][j] = q < nr;
-        posq[nq][j] = base + attn_row_last(p, (r0 + min(q, nr - 1)) / G);
-      }
-    float m[2][2], l[2][2], tm[2][2], tl[2][2];  // per column: running max (log2 domain), sum; folded
+    for (int off = 1; off <= 16; off <<= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, off));
+    float m[2], l[2], tm[2], tl[2];  // per column: running max (log2 domain), sum; folded
 #pragma unroll
-    for (int nq = 0; nq < 2; ++nq)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) m[nq][j] = tm[nq][j] = -INFINITY, l[nq][j] = tl[nq][j] = 0.f;
-    // O^T accumulators: m-tile md = dims md*16 .. +15, n-tile nq; [c]: (dim g | g+8, column 2 t4 | +1)
-    float o[8][2][4], to[8][2][4];
+    for (int j = 0; j < 2; ++j) m[j] = tm[j] = -INFINITY, l[j] = tl[j] = 0.f;
+    // O^T accumulators: m-tile md = dims md*16 .. +15; [c]: (dim g | g+8, column 2 t4 | +1)
+    float o[8][4], to[8][4];
 #pragma unroll
     for (int md = 0; md < 8; ++md)
 #pragma unroll
-      for (int nq = 0; nq < 2; ++nq)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) o[md][nq][i] = to[md][nq][i] = 0.f;
+      for (int i = 0; i < 4; ++i) o[md][i] = to[md][i] = 0.f;
     // this warp's fold of its finished segments (starts empty: fold(empty, x) == x exactly)
     auto fold_segment = [&]() {
+      float ft[2], fc[2];
 #pragma unroll
-      for (int nq = 0; nq < 2; ++nq) {
-        if (nq == 1 && !two) break;  // (warp-uniform)
-        float ft[2], fc[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const float M = fmaxf(tm[nq][j], m[nq][j]);
-          ft[j] = (tm[nq][j] == -INFINITY) ? 0.f : exp2f(tm[nq][j] - M);
-          fc[j] = (m[nq][j] == -INFINITY) ? 0.f : exp2f(m[nq][j] - M);
-          tl[nq][j] = __fadd_rn(__fmul_rn(tl[nq][j], ft[j]), __fmul_rn(l[nq][j], fc[j]));
-          tm[nq][j] = M;
-          m[nq][j] = -INFINITY;
-          l[nq][j] = 0.f;
-        }
-#pragma unroll
-        for (int md = 0; md < 8; ++md)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            to[md][nq][i] = __fadd_rn(__fmul_rn(to[md][nq][i], ft[i & 1]), __fmul_rn(o[md][nq][i], fc[i & 1]));
-            o[md][nq][i] = 0.f;
-          }
+      for (int j = 0; j < 2; ++j) {
+        const float M = fmaxf(tm[j], m[j]);
+        ft[j] = (tm[j] == -INFINITY) ? 0.f : exp2f(tm[j] - M);
+        fc[j] = (m[j] == -INFINITY) ? 0.f : exp2f(m[j] - M);
+        tl[j] = __fadd_rn(__fmul_rn(tl[j], ft[j]), __fmul_rn(l[j], fc[j]));
+        tm[j] = M;
+        m[j] = -INFINITY;
+        l[j] = 0.f;
       }
+#pragma unroll
+      for (int md = 0; md < 8; ++md)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          to[md][i] = __fadd_rn(__fmul_rn(to[md][i], ft[i & 1]), __fmul_rn(o[md][i], fc[i & 1]));
+          o[md][i] = 0.f;
+        }
     };
 
     for (int c = it.c0; c < it.c1; ++c, ++seq) {
       if (c != it.c0 && c % seg_ch == 0) fold_segment();  // segment boundary (group schedule)
       const int st = seq % NST;
       mbar_wait(&full[st], (uint32_t)(seq / NST) & 1u);
+      const int kstart = c * CH + warp * KPW;
       if (probe) {  // (finite output: a state of one unit-weight zero row)
 #pragma unroll
-        for (int nq = 0; nq < 2; ++nq)
+        for (int j = 0; j < 2; ++j) m[j] = 0.f, l[j] = 1.f;
+      } else if (kstart <= wlast) {  // (warp-uniform)
+        const uint32_t kb = sbase + st * STAGE_BYTES, vb = kb + KV_BYTES;
+        // S^T = K_w Q^T: 16 keys x 8 columns, 8 k-steps of 16 dims (two independent accumulator chains)
+        float s[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int j = 0; j < 2; ++j) m[nq][j] = 0.f, l[nq][j] = 1.f;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
-        continue;
-      }
-      const uint32_t kb = sbase + st * STAGE_BYTES, vb = kb + KV_BYTES;
-      // (one or two 8-column n-tiles: the chunk body instantiated per count, no work on an empty one)
-      auto chunk_body = [&](auto nq_count) {
-        constexpr int NQ = decltype(nq_count)::value;
-        const int kstart = c * CH + warp * 32;
-        const int mi = lane >> 3, ri = lane & 7;
-        // S^T = K_w Q^T: m-tiles mt (16 keys each of this warp's 32) x n-tiles nq, 8 k-steps of 16 dims
-        float s[2][2][4];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int nq = 0; nq < NQ; ++nq)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) s[mt][nq][i] = 0.f;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt) {
-            uint32_t a[4];
-            ldsm_x4(kb + swz(warp * 32 + mt * 16 + (mi & 1) * 8 + ri, kk * 2 + (mi >> 1)), a[0], a[1], a[2], a[3]);
-            mma16816(s[mt][0], a, qb[0][kk][0], qb[0][kk][1]);
-            if (NQ == 2) mma16816(s[mt][1], a, qb[1][kk][0], qb[1][kk][1]);
-          }
+        for (int kk = 0; kk < 8; kk += 2) {
+          uint32_t a[4], a2[4];
+          ldsm_x4(kb + swz(warp * KPW + (mi & 1) * 8 + ri, kk * 2 + (mi >> 1)), a[0], a[1], a[2], a[3]);
+          ldsm_x4(kb + swz(warp * KPW + (mi & 1) * 8 + ri, kk * 2 + 2 + (mi >> 1)), a2[0], a2[1], a2[2], a2[3]);
+          mma16816(s, a, qb[kk][0], qb[kk][1]);
+          mma16816(s2, a2, qb[kk + 1][0], qb[kk + 1][1]);
         }
         // mask, new running max per column (exact; masked entries excluded)
-        float cm[2][2];
+        float cm[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-        for (int nq = 0; nq < NQ; ++nq) cm[nq][0] = cm[nq][1] = -INFINITY;
+        for (int i = 0; i < 4; ++i) {
+          const int key = kstart + g + 8 * (i >> 1), j = i & 1;
+          const bool vis = okq[j] && key <= posq[j];
+          const float v = vis ? (s[i] + s2[i]) * scale_log2 : -INFINITY;
+          s[i] = v;
+          cm[j] = fmaxf(cm[j], v);
+        }
+        float af[2];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int j = 0; j < 2; ++j) {
 #pragma unroll
-          for (int nq = 0; nq < NQ; ++nq)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int key = kstart + mt * 16 + g + 8 * (i >> 1), j = i & 1;
-              const bool vis = okq[nq][j] && key <= posq[nq][j];
-              const float v = vis ? s[mt][nq][i] * scale_log2 : -INFINITY;
-              s[mt][nq][i] = v;
-              cm[nq][j] = fmaxf(cm[nq][j], v);
-            }
-        float af[2][2];
-#pragma unroll
-        for (int nq = 0; nq < NQ; ++nq)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-#pragma unroll
-            for (int off = 4; off <= 16; off <<= 1) cm[nq][j] = fmaxf(cm[nq][j], __shfl_xor_sync(0xffffffffu, cm[nq][j], off));
-            const float mn = fmaxf(m[nq][j], cm[nq][j]);
-            af[nq][j] = (mn == -INFINITY) ? 1.f : exp2f(m[nq][j] - mn);
-            m[nq][j] = mn;
-          }
+          for (int off = 4; off <= 16; off <<= 1) cm[j] = fmaxf(cm[j], __shfl_xor_sync(0xffffffffu, cm[j], off));
+          const float mn = fmaxf(m[j], cm[j]);
+          af[j] = (mn == -INFINITY) ? 1.f : exp2f(m[j] - mn);
+          m[j] = mn;
+        }
         // P^T and its column sums; P^T's 8x8 blocks transposed in registers into the PV B fragments
-        uint32_t pb[2][2][2];  // [mt = PV k-step][nq][b0 | b1]
-        float ps[2][2];
+        float e[4];
 #pragma unroll
-        for (int nq = 0; nq < NQ; ++nq) ps[nq][0] = ps[nq][1] = 0.f;
+        for (int i = 0; i < 4; ++i) e[i] = (s[i] == -INFINITY) ? 0.f : exp2f(s[i] - m[i & 1]);
+        float ps[2] = {e[0] + e[2], e[1] + e[3]};
+        const uint32_t pb0 = movmatrix_trans(pack_bf16(e[0], e[1]));  // keys 0..7 of the slice
+        const uint32_t pb1 = movmatrix_trans(pack_bf16(e[2], e[3]));  // keys 8..15
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int j = 0; j < 2; ++j) {
 #pragma unroll
-          for (int nq = 0; nq < NQ; ++nq) {
-            float e[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) e[i] = (s[mt][nq][i] == -INFINITY) ? 0.f : exp2f(s[mt][nq][i] - m[nq][i & 1]);
-            ps[nq][0] += e[0] + e[2];
-            ps[nq][1] += e[1] + e[3];
-            pb[mt][nq][0] = movmatrix_trans(pack_bf16(e[0], e[1]));  // keys mt*16 + 0..7
-            pb[mt][nq][1] = movmatrix_trans(pack_bf16(e[2], e[3]));  // keys mt*16 + 8..15
-          }
-#pragma unroll
-        for (int nq = 0; nq < NQ; ++nq)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-#pragma unroll
-            for (int off = 4; off <= 16; off <<= 1) ps[nq][j] += __shfl_xor_sync(0xffffffffu, ps[nq][j], off);
-            l[nq][j] = l[nq][j] * af[nq][j] + ps[nq][j];
-          }
+          for (int off = 4; off <= 16; off <<= 1) ps[j] += __shfl_xor_sync(0xffffffffu, ps[j], off);
+          l[j] = l[j] * af[j] + ps[j];
+        }
         // (no column of the warp raised its max: every factor is exactly 1 and the rescale is the identity)
-        if (!__all_sync(0xffffffffu, af[0][0] == 1.f && af[0][1] == 1.f && (NQ == 1 || (af[1][0] == 1.f && af[1][1] == 1.f)))) {
+        if (!__all_sync(0xffffffffu, af[0] == 1.f && af[1] == 1.f)) {
 #pragma unroll
           for (int md = 0; md < 8; ++md)
 #pragma unroll
-            for (int nq = 0; nq < NQ; ++nq)
-#pragma unroll
-              for (int i = 0; i < 4; ++i) o[md][nq][i] *= af[nq][i & 1];
+            for (int i = 0; i < 4; ++i) o[md][i] *= af[i & 1];
         }
-        // O^T += V_w^T P^T: m-tiles md (16 dims) x 2 k-steps (16 keys) x n-tiles nq
+        // O^T += V_w^T P^T: m-tiles md (16 dims), one k-step (the slice's 16 keys)
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-#pragma unroll
-          for (int md = 0; md < 8; ++md) {
-            uint32_t a[4];
-            ldsm_x4_t(vb + swz(warp * 32 + mt * 16 + (mi >> 1) * 8 + ri, md * 2 + (mi & 1)), a[0], a[1], a[2], a[3]);
-            mma16816(o[md][0], a, pb[mt][0][0], pb[mt][0][1]);
-            if (NQ == 2) mma16816(o[md][1], a, pb[mt][1][0], pb[mt][1][1]);
-          }
+        for (int md = 0; md < 8; ++md) {
+          uint32_t a[4];
+          ldsm_x4_t(vb + swz(warp * KPW + (mi >> 1) * 8 + ri, md * 2 + (mi & 1)), a[0], a[1], a[2], a[3]);
+          mma16816(o[md], a, pb0, pb1);
         }
-      };
-      if (two) chunk_body(std::integral_constant<int, 2>{});
-      else chunk_body(std::integral_constant<int, 1>{});
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
     }
@@ -397,134 +350,131 @@ __global__ void __launch_bounds__(160, 1) attn_fd_kernel(const __grid_constant__
       return (size_t)(it.b * p.q_len + qi) * p.Hq + h;
     };
     if (split && it.nseg > 1) {
-      // ---- segment schedule: publish this segment's four warp states
+      // ---- segment schedule: publish this segment's warp states
 #pragma unroll
-      for (int nq = 0; nq < 2; ++nq)
+      for (int j = 0; j < 2; ++j) {
+        const int q = 2 * t4 + j;
+        if (q >= nr) continue;
+        const size_t bq = (row_slot(q) * p.nchunk_max + it.seg) * NW + warp;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int q = nq * 8 + 2 * t4 + j;
-          if (q >= nr) continue;
-          const size_t bq = (row_slot(q) * p.nchunk_max + it.seg) * 4 + warp;
-#pragma unroll
-          for (int md = 0; md < 8; ++md) {
-            p.part_o[bq * HD + md * 16 + g] = to[md][nq][j];
-            p.part_o[bq * HD + md * 16 + g + 8] = to[md][nq][2 + j];
-          }
-          if (g == 0) {
-            p.part_ml[2 * bq] = tm[nq][j];
-            p.part_ml[2 * bq + 1] = tl[nq][j];
-          }
+        for (int md = 0; md < 8; ++md) {
+          p.part_o[bq * HD + md * 16 + g] = to[md][j];
+          p.part_o[bq * HD + md * 16 + g + 8] = to[md][2 + j];
         }
-      named_bar(1, 128);
+        if (g == 0) {
+          p.part_ml[2 * bq] = tm[j];
+          p.part_ml[2 * bq + 1] = tl[j];
+        }
+      }
+      named_bar(1, NW * 32);
       if (tid == 0) {
         int prev;
         asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(p.seg_cnt + group) : "memory");
         mrg_flag[0] = prev == it.nseg - 1;
         if (prev == it.nseg - 1) p.seg_cnt[group] = 0;  // re-arm for the next launch
       }
-      named_bar(1, 128);
+      named_bar(1, NW * 32);
       if (!mrg_flag[0]) continue;
       // the group's last segment: fold every warp slot's segment states in segment order (the same
       // operations as the in-register fold). Step factors per (warp, row) first (one thread each),
-      // then every thread (one dimension) streams the O values, all segments of 4 (warp, row)
-      // pairs in flight at a time.
+      // then every thread (one dimension, one parity of the (warp, row) pairs) streams the O values,
+      // all segments of 4 pairs in flight at a time.
       constexpr int SMAX = 8;
-      float* fa_s = mrg;                   // [4][16][SMAX] factor of the running state, then
-      float* fb_s = mrg + 4 * 16 * SMAX;   // of segment s; the O fold overwrites mrg[] afterwards
+      float* fa_s = mrg;                    // [NW][TR][SMAX] factor of the running state, then
+      float* fb_s = mrg + NW * TR * SMAX;   // of segment s; the O fold overwrites mrg[] afterwards
       const int nsg = min(it.nseg, SMAX);
-      if (tid < 4 * nr) {
+      if (tid < NW * nr) {
         const int w = tid / nr, r = tid % nr;
         const size_t s0 = row_slot(r) * p.nchunk_max;
         float m = -INFINITY, l = 0.f;
         for (int sg = 0; sg < nsg; ++sg) {
-          const size_t bs = (s0 + sg) * 4 + w;
+          const size_t bs = (s0 + sg) * NW + w;
           const float ms = __ldcg(&p.part_ml[2 * bs]), ls = __ldcg(&p.part_ml[2 * bs + 1]);
           const float M = fmaxf(m, ms);
           const float fa = (m == -INFINITY) ? 0.f : exp2f(m - M);
           const float fb = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
           l = __fadd_rn(__fmul_rn(l, fa), __fmul_rn(ls, fb));
           m = M;
-          fa_s[(w * 16 + r) * SMAX + sg] = fa;
-          fb_s[(w * 16 + r) * SMAX + sg] = fb;
+          fa_s[(w * TR + r) * SMAX + sg] = fa;
+          fb_s[(w * TR + r) * SMAX + sg] = fb;
         }
-        mrg_m[w * 16 + r] = m;
-        mrg_l[w * 16 + r] = l;
+        mrg_m[w * TR + r] = m;
+        mrg_l[w * TR + r] = l;
       }
-      named_bar(1, 128);
-      float Ofold[64];  // (warp, row) pairs x this thread's dimension d = tid
-      for (int q0 = 0; q0 < 4 * nr; q0 += 4) {
+      named_bar(1, NW * 32);
+      const int d = tid & (HD - 1), par = tid >> 7;  // dimension, pair parity
+      const int npair = NW * nr;                      // (warp, row) pairs q = w nr + r
+      float Ofold[NW * TR / 2];
+      for (int i0 = 0; 2 * i0 < npair; i0 += 4) {
         float Os[4][SMAX];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int q = min(q0 + j, 4 * nr - 1), w = q / nr, r = q % nr;
+          const int q = min(2 * (i0 + j) + par, npair - 1), w = q / nr, r = q % nr;
           const size_t s0 = row_slot(r) * p.nchunk_max;
 #pragma unroll
           for (int sg = 0; sg < SMAX; ++sg)
-            Os[j][sg] = (sg < nsg) ? __ldcg(&p.part_o[((s0 + sg) * 4 + w) * HD + tid]) : 0.f;
+            Os[j][sg] = (sg < nsg) ? __ldcg(&p.part_o[((s0 + sg) * NW + w) * HD + d]) : 0.f;
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int q = min(q0 + j, 4 * nr - 1), w = q / nr, r = q % nr;
+          const int q = min(2 * (i0 + j) + par, npair - 1), w = q / nr, r = q % nr;
           float O = 0.f;
 #pragma unroll
           for (int sg = 0; sg < SMAX; ++sg)
             if (sg < nsg)
-              O = __fadd_rn(__fmul_rn(O, fa_s[(w * 16 + r) * SMAX + sg]), __fmul_rn(Os[j][sg], fb_s[(w * 16 + r) * SMAX + sg]));
-          if (q0 + j < 4 * nr) Ofold[q0 + j] = O;
+              O = __fadd_rn(__fmul_rn(O, fa_s[(w * TR + r) * SMAX + sg]), __fmul_rn(Os[j][sg], fb_s[(w * TR + r) * SMAX + sg]));
+          if (i0 + j < NW * TR / 2) Ofold[i0 + j] = O;
         }
       }
-      named_bar(1, 128);  // factors consumed before mrg[] is overwritten
-      for (int q = 0; q < 4 * nr; ++q) {
-        const int w = q / nr, r = q % nr;
-        mrg[(w * 16 + r) * HD + tid] = Ofold[q];
+      named_bar(1, NW * 32);  // factors consumed before mrg[] is overwritten
+      for (int i = 0; 2 * i + par < npair; ++i) {
+        const int q = 2 * i + par, w = q / nr, r = q % nr;
+        mrg[(w * TR + r) * HD + d] = Ofold[i];
       }
     } else {
-      // ---- merge the 4 warp states in fixed order and normalise
+      // ---- the warp states, for the merge in fixed order
 #pragma unroll
-      for (int nq = 0; nq < 2; ++nq)
+      for (int j = 0; j < 2; ++j) {
+        const int q = 2 * t4 + j;
+        if (q < nr) {  // (rows of the tile past the block's rows are never read)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int q = nq * 8 + 2 * t4 + j;
-          if (q < nr) {  // (rows of the tile past the block's rows are never read)
-#pragma unroll
-            for (int md = 0; md < 8; ++md) {
-              mrg[(warp * 16 + q) * HD + md * 16 + g] = to[md][nq][j];
-              mrg[(warp * 16 + q) * HD + md * 16 + g + 8] = to[md][nq][2 + j];
-            }
+          for (int md = 0; md < 8; ++md) {
+            mrg[(warp * TR + q) * HD + md * 16 + g] = to[md][j];
+            mrg[(warp * TR + q) * HD + md * 16 + g + 8] = to[md][2 + j];
           }
           if (g == 0) {
-            mrg_m[warp * 16 + q] = tm[nq][j];
-            mrg_l[warp * 16 + q] = tl[nq][j];
+            mrg_m[warp * TR + q] = tm[j];
+            mrg_l[warp * TR + q] = tl[j];
           }
         }
+      }
     }
-    named_bar(1, 128);
+    named_bar(1, NW * 32);
     // per-row merge factors once (row r: thread r): M = max_w m_w, f_w = 2^(m_w - M), L = sum_w l_w f_w
     // (same values and order as forming them per element)
     if (tid < nr) {
       const int r = tid;
       float M = -INFINITY;
 #pragma unroll
-      for (int w = 0; w < 4; ++w) M = fmaxf(M, mrg_m[w * 16 + r]);
+      for (int w = 0; w < NW; ++w) M = fmaxf(M, mrg_m[w * TR + r]);
       float L = 0.f;
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const float f = (mrg_m[w * 16 + r] == -INFINITY) ? 0.f : exp2f(mrg_m[w * 16 + r] - M);
-        L += mrg_l[w * 16 + r] * f;
-        mrg_m[w * 16 + r] = f;
+      for (int w = 0; w < NW; ++w) {
+        const float f = (mrg_m[w * TR + r] == -INFINITY) ? 0.f : exp2f(mrg_m[w * TR + r] - M);
+        L += mrg_l[w * TR + r] * f;
+        mrg_m[w * TR + r] = f;
       }
       mrg_l[r] = L;
-      mrg_l[16 + r] = M;
     }
-    named_bar(1, 128);
-    for (int e = tid; e < nr * HD; e += 128) {
+    named_bar(1, NW * 32);
+    for (int e = tid; e < nr * HD; e += NW * 32) {
       const int r = e / HD, d = e % HD;
       float acc = 0.f;
 #pragma unroll
-      for (int w = 0; w < 4; ++w) acc += mrg[(w * 16 + r) * HD + d] * mrg_m[w * 16 + r];
+      for (int w = 0; w < NW; ++w) acc += mrg[(w * TR + r) * HD + d] * mrg_m[w * TR + r];
       reinterpret_cast<__nv_bfloat16*>(p.out)[row_slot(r) * HD + d] = __float2bfloat16_rn(acc / mrg_l[r]);
     }
-    named_bar(1, 128);
+    named_bar(1, NW * 32);
     if (tid == 0 && g_kt.rec) kt_item((uint32_t)(it.seg | (it.nseg << 8) | ((it.c1 - it.c0) << 16)), ti0, ti1, kt_now());
   }
 }
@@ -575,7 +525,7 @@ cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
     attr = true;
   }
   const int G = p.Hq / p.Hkv;
-  const int ntiles = (p.q_len * G + 15) / 16;
+  const int ntiles = (p.q_len * G + TR - 1) / TR;
   // segment size override (tests exercise the multi-segment fold at short contexts; read per launch)
   const int env_seg = getenv("SF_ATTN_SEG") ? atoi(getenv("SF_ATTN_SEG")) : 0;
   const int seg_keys = (env_seg >= CH && env_seg % CH == 0) ? env_seg : kAttnSeg;
@@ -596,7 +546,7 @@ cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
   if (!encode_kv_map4(&mk4, p.Kp, p.Hkv, p.n_pages) || !encode_kv_map4(&mv4, p.Vp, p.Hkv, p.n_pages))
     return cudaErrorInvalidValue;
   static const int env_probe = getenv("SF_ATTN_PROBE") ? atoi(getenv("SF_ATTN_PROBE")) : 0;
-  launch_k(attn_fd_kernel, dim3(grid), dim3(160), SMEM, s, mk, mv, mk4, mv4, p, ntiles, nseg_max, seg_keys, n_items,
+  launch_k(attn_fd_kernel, dim3(grid), dim3(NTHR), SMEM, s, mk, mv, mk4, mv4, p, ntiles, nseg_max, seg_keys, n_items,
            split | (env_probe ? 2 : 0));
   return cudaGetLastError();
 }

@@ -31,6 +31,8 @@ __host__ __device__ inline int attn_row_last(const AttnParams& p, int qi) { retu
 
 constexpr int kAttnChunk = 128;  // fixed absolute key-chunk size (split-KV boundaries, C23)
 constexpr int kAttnSeg = 2048;   // flash-decoding key segment (fixed absolute bounds; defines the arithmetic)
+constexpr int kAttnTileRows = 8; // bf16 flash-decoding query tile: (query, head) rows per work item
+constexpr int kAttnWarps = 8;    // its compute warps: warp w owns keys [16 w, 16 w + 16) of every 128-key chunk
 
 // act dtype: bf16 (is_bf16) or fp32.
 cudaError_t launch_rope_table(float2* table, int max_seq, int hd, float theta, cudaStream_t s);

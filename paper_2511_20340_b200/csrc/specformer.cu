@@ -227,11 +227,12 @@ Plan make_plan(const sf_config* c) {
   p.o_hlast = take((int64_t)p.B * p.d * 4);
   p.o_logits = take((int64_t)p.rows_v * p.V * 4);
   p.o_dlogits = take((int64_t)p.rows_d * p.V * 4);
-  p.o_apo = take((int64_t)p.R * p.Hq * p.nchunk * 4 * p.hd * 4);
-  p.o_apml = take((int64_t)p.R * p.Hq * p.nchunk * 4 * 2 * 4);
-  // split-KV arrival counters: one per (sequence, kv head, 16-row query tile) at the longest block
-  p.n_acnt = std::max<int64_t>((int64_t)p.B * p.Hkv * ((std::max(p.k + 1, p.C_pf) * (p.Hq / p.Hkv) + 15) / 16),
-                               (int64_t)p.Hkv * ((p.R * (p.Hq / p.Hkv) + 15) / 16 + 1));  // (one long sequence)
+  p.o_apo = take((int64_t)p.R * p.Hq * p.nchunk * kAttnWarps * p.hd * 4);
+  p.o_apml = take((int64_t)p.R * p.Hq * p.nchunk * kAttnWarps * 2 * 4);
+  // split-KV arrival counters: one per (sequence, kv head, query tile) at the longest block
+  constexpr int TR = kAttnTileRows;
+  p.n_acnt = std::max<int64_t>((int64_t)p.B * p.Hkv * ((std::max(p.k + 1, p.C_pf) * (p.Hq / p.Hkv) + TR - 1) / TR),
+                               (int64_t)p.Hkv * ((p.R * (p.Hq / p.Hkv) + TR - 1) / TR + 1));  // (one long sequence)
   p.o_acnt = take(p.n_acnt * 4);
   p.o_gpart = take(p.gpart_elems * 4);
   p.o_gcnt = take(4096 * 4);
