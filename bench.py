@@ -247,6 +247,8 @@ def run_ours(args, cfg):
     torch.cuda.empty_cache()
     if tp > 1:
         eng.attach_nccl(tpmod.share_unique_id(nccl_unique_id, rank), tp, rank)
+        if args.tp_fused:  # NEXT-3: row-parallel all-reduce fused into the norm consumer over peer memory
+            eng.attach_xch(tpmod.share_xch_handles(eng.xch_handle(), rank, tp))
         prompts = make_prompts(B, P, cfg.vocab)  # every rank: the same global batch
     else:
         prompts = dp.shard_rows(make_prompts(B * world, P, cfg.vocab), rank, world)  # weak scaling
@@ -611,7 +613,7 @@ def run_ours(args, cfg):
             "config": {"workload": f"{cfg.name}-shaped SpecFormer decode step (draft+verify+accept), "
                                    f"batch {B}/GPU, k {k}, prompt {P}",
                        "model": cfg.name, "batch_per_gpu": B if tp == 1 else B / tp, "global_batch": B * world // tp,
-                       "draft_len": k, "prompt_len": P, "parallelism": f"tp{tp}" if tp > 1 else f"dp{world}",
+                       "draft_len": k, "prompt_len": P, "parallelism": (f"tp{tp}" + ("-fused" if args.tp_fused else "")) if tp > 1 else f"dp{world}",
                        "cuda_graph": True, "logits": "not stored (fused LM-head argmax)" if no_logits else "stored",
                        "l2": "inputs larger than L2 (14 GB weights + KV per step)",
                        "timing": f"median of {n_win} windows of {K} steps, each after a fresh prefill + {W} warm-up steps"},
@@ -661,6 +663,8 @@ def main():
     ap.add_argument("--forced-steps", type=int, default=32)
     ap.add_argument("--tp", action="store_true", help="N > 1: split one model over the ranks (tensor parallelism; "
                                                       "the default for --config 70b) instead of one batch per rank")
+    ap.add_argument("--tp-fused", action="store_true", help="with --tp: the NEXT-3 fused peer-memory all-reduce "
+                    "(CUDA IPC exchange regions) instead of NCCL for the row-parallel outputs")
     ap.add_argument("--timeline-steps", type=int, default=2, help="graph steps replayed with the kernel timeline on")
     ap.add_argument("--draft-len", type=int, default=None, help="override k (13B sweep: 4 / 6 / 8)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

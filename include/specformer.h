@@ -275,6 +275,32 @@ sf_local_group* sf_local_group_create(int32_t n);
 void sf_local_group_destroy(sf_local_group* g);
 sf_status sf_local_group_attach(sf_handle* h, sf_local_group* g, int32_t rank);
 
+/* ---- NEXT-3: the row-parallel all-reduce fused into the residual + RMSNorm consumer, over peer memory
+ * (PAPER P91-95: at large batch the step is compute-bound, so the ~2 L + 5
+ * all-reduces per step must not sit on the critical path as separate collective launches).
+ * Each rank owns an exchange region (library-allocated, 256 B of flags + two bf16 [R, d] slots, R the
+ * handle's largest row block). A row-parallel GEMM (base O / down, context W_D / O, draft O / down)
+ * stores its bf16 output straight into this rank's slot of the coming epoch (double-buffered, chosen
+ * on the device by the epoch counter), a one-warp kernel increments the epoch and publishes it with a
+ * system-scope release into every peer's flags, and the consumer on every rank waits (system-scope
+ * acquire, bounded at 5 s -> SF_ERR_NCCL at specformer_sync) for all peers' flags, then adds the ranks'
+ * slots to the fp32 residual in rank order 0..tp-1 (every rank: the same values in the same order,
+ * hence the same bits) before the norm. Replaces the NCCL all-reduce of the row-parallel outputs
+ * (the argmax max still uses the attached collective). Attach after the collective and before the
+ * first prefill; every rank must attach. bf16 handles with 2 <= tp_size <= 8 only
+ * (SF_ERR_UNSUPPORTED / SF_ERR_STATE otherwise). */
+/* This rank's exchange region as a 64-byte cudaIpcMemHandle_t (allocates the region on first use). */
+sf_status sf_tp_xch_handle(sf_handle* h, uint8_t* out_64);
+/* One process per GPU: handles_64xtp = every rank's sf_tp_xch_handle bytes in rank order (this rank's
+ * entry is not opened). Opens the peers' regions with cudaIpcOpenMemHandle (lazy peer access);
+ * captured by SF_FLAG_CUDA_GRAPH. Errors: SF_ERR_CUDA (a peer region cannot be mapped), SF_ERR_STATE. */
+sf_status sf_tp_xch_attach(sf_handle* h, const uint8_t* handles_64xtp);
+/* Local group (one process, one device, tests): the ranks' regions are shared directly; after every
+ * epoch signal the ranks meet at a host barrier, so no rank's kernel ever waits on another rank's
+ * kernel (the flag waits are satisfied before the consumer starts). Every rank calls it (it blocks
+ * until all have); needs sf_local_group_attach with the same group first. */
+sf_status sf_local_group_xch_attach(sf_handle* h, sf_local_group* g);
+
 #ifdef __cplusplus
 }
 #endif

@@ -77,6 +77,9 @@ SIGNATURES = [
     ("sf_local_group_create", _P, [C.c_int32]),
     ("sf_local_group_destroy", None, [_P]),
     ("sf_local_group_attach", C.c_int, [_P, _P, C.c_int32]),
+    ("sf_tp_xch_handle", C.c_int, [_P, _P]),
+    ("sf_tp_xch_attach", C.c_int, [_P, _P]),
+    ("sf_local_group_xch_attach", C.c_int, [_P, _P]),
 ]
 
 

@@ -528,6 +528,14 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     const bool lead = threadIdx.x == 128;  // first epilogue thread: flags, barriers' single-thread work
     constexpr int mode = MODE;
     const size_t ldo = (size_t)p.epi.ldo;
+    // the output base (a device-selected exchange slot for the fused TP all-reduce; read when storing,
+    // after this thread's grid-dependency wait: the selecting counter is written two launches earlier)
+    auto eout = [&]() -> uint8_t* {
+      uint8_t* o = reinterpret_cast<uint8_t*>(p.epi.out);
+      if (p.epi.out_sel)
+        o += (size_t)((*(volatile const int*)p.epi.out_sel + 1) & 1) * (size_t)p.epi.out_sel_stride * 2;
+      return o;
+    };
     // smem ring reuse once every MMA of the CTA has completed (final phase): partial staging
     // [0, ring - 48 KB) and three 16 KB output staging buffers at the end
     constexpr int kStageBytes = 16384;
@@ -678,7 +686,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       named_sync(2 + gid, 128);
       if (lead && c0 < 2 * 96) SF_TR(116 + 4 * (c0 / 96));  // staged in smem
       const int col0 = mode == EPI_SWIGLU_ACT ? vt_ * 64 : vt_ * BM;
-      uint8_t* gbase = reinterpret_cast<uint8_t*>(p.epi.out) + ((size_t)c0 * ldo + col0) * out_elt;
+      uint8_t* gbase = eout() + ((size_t)c0 * ldo + col0) * out_elt;
       const int vpr = rowb / 16, ht = quad * 32 + lane;
       for (int i = ht; i < nq * vpr; i += 128) {
         const int q = i / vpr, x = i % vpr;
@@ -701,7 +709,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       }
       const int n = vt_ * BM + m;
       if (mode == EPI_STORE_ACT) {
-        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.epi.out) + (size_t)c0 * ldo + n;
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(eout()) + (size_t)c0 * ldo + n;
 #pragma unroll
         for (int q = 0; q < 32; ++q)
           if (q < nq) o[q * ldo] = __float2bfloat16_rn(v[q]);
@@ -1493,7 +1501,7 @@ template <int NG, int F>
 __global__ void __launch_bounds__(1024) resid_norm_kernel(
     const float* __restrict__ partial, int G, int kb, int drain, int CG, int n_tiles_cta, int T, int rep, int d,
     const float* resid, const float* __restrict__ add, const float* __restrict__ bias, float* out, float* tap,
-    const float* __restrict__ gamma, float eps, __nv_bfloat16* xn) {
+    const float* __restrict__ gamma, float eps, __nv_bfloat16* xn, TpSrc tp) {
   constexpr int kRnBatch = (8 / NG) / F;  // partial loads in flight per column group
   __shared__ int seg_n[kRnMaxTiles];
   __shared__ int seg_off[kRnMaxTiles][kRnMaxSeg];  // slot * T * 128 (the tile's k segments, k order)
@@ -1521,6 +1529,30 @@ __global__ void __launch_bounds__(1024) resid_norm_kernel(
   pdl_wait();
   kt_.mark();
   pdl_trigger();
+  __shared__ int tp_epoch;
+  if (tp.n > 0) {
+    // NEXT-3: every peer has published this epoch's slot (system-scope acquire of the flag it wrote
+    // into this rank's region after its GEMM); bounded, so a missing peer cannot hang the device
+    if (tid == 0) {
+      const int e = *(volatile const int*)tp.ctr;
+      const unsigned long long t0 = gtimer();
+      for (int q = 0; q < tp.n; ++q) {
+        if (q == tp.own) continue;
+        int f;
+        for (;;) {
+          asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(f) : "l"(tp.flags + q) : "memory");
+          if (f >= e) break;
+          if (gtimer() - t0 > 5000000000ull) {  // 5 s
+            atomicOr(tp.err, 4);  // (specformer_sync: SF_ERR_NCCL)
+            break;
+          }
+          __nanosleep(64);
+        }
+      }
+      tp_epoch = e;
+    }
+    __syncthreads();
+  }
   float4 x[F][NG];
 #pragma unroll
   for (int f = 0; f < F; ++f)
@@ -1534,6 +1566,23 @@ __global__ void __launch_bounds__(1024) resid_norm_kernel(
         x[f][j].y += a.y;
         x[f][j].z += a.z;
         x[f][j].w += a.w;
+      }
+      if (tp.n > 0) {  // (NEXT-3: the ranks' bf16 GEMM outputs, read over peer memory, summed in rank order)
+        const size_t off = (size_t)(tp_epoch & 1) * (size_t)tp.slot_elems + (size_t)r * d + i;
+        uint2 raw[kTpMax];
+#pragma unroll
+        for (int q = 0; q < kTpMax; ++q)
+          if (q < tp.n) raw[q] = __ldcg(reinterpret_cast<const uint2*>(tp.slot[q] + off));
+#pragma unroll
+        for (int q = 0; q < kTpMax; ++q)
+          if (q < tp.n) {
+            const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[q].x));
+            const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[q].y));
+            x[f][j].x += lo.x;
+            x[f][j].y += lo.y;
+            x[f][j].z += hi.x;
+            x[f][j].w += hi.y;
+          }
       }
       if (bias) {
         const float4 bb = *reinterpret_cast<const float4*>(bias + col0 + i);
@@ -1624,8 +1673,13 @@ __global__ void __launch_bounds__(1024) resid_norm_kernel(
 
 cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T, int rep, int d, const float* resid,
                               const float* add, const float* bias, float* out, float* tap, const float* gamma,
-                              float eps, __nv_bfloat16* xn, cudaStream_t st) {
+                              float eps, __nv_bfloat16* xn, cudaStream_t st, const TpSrc* tps) {
   if (T * rep <= 0) return cudaSuccess;
+  TpSrc tp;
+  if (tps) {
+    if (tps->n < 1 || tps->n > kTpMax || rep != 1 || partial) return cudaErrorInvalidValue;
+    tp = *tps;
+  }
   const int ng = rn_ng(d);
   if (!ng) return cudaErrorInvalidValue;
   int G = 1, kb = 1, CG = 1, nt = 1, Tslot = T, drain = 0;
@@ -1649,9 +1703,9 @@ cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T,
 #define SF_RN(NGV)                                                                                                  \
   return (fold && ng == 1 && nv % 64 == 0)                                                                          \
              ? launch_k(resid_norm_kernel<NGV, 2>, grid, dim3(nv / 2), 0, st, partial, G, kb, drain, CG, nt, Tslot,  \
-                        rep, d, resid, add, bias, out, tap, gamma, eps, xn)                                          \
+                        rep, d, resid, add, bias, out, tap, gamma, eps, xn, tp)                                      \
              : launch_k(resid_norm_kernel<NGV, 1>, grid, dim3(nv), 0, st, partial, G, kb, drain, CG, nt, Tslot, rep, \
-                        d, resid, add, bias, out, tap, gamma, eps, xn)
+                        d, resid, add, bias, out, tap, gamma, eps, xn, tp)
   switch (ng) {
     case 1: SF_RN(1);
     case 2: SF_RN(2);
@@ -1659,6 +1713,29 @@ cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T,
     default: SF_RN(4);
   }
 #undef SF_RN
+}
+
+// NEXT-3 epoch publication: one warp. The GEMM that wrote this epoch's slot has completed (stream
+// order); the system-scope fence orders its stores before the flags the peers acquire.
+__global__ void tp_signal_kernel(int* ctr, TpPeers pf, int n, int own) {
+  __shared__ int e;
+  if (threadIdx.x == 0) {
+    e = *ctr + 1;
+    *ctr = e;
+    __threadfence_system();
+  }
+  __syncthreads();
+  const int q = threadIdx.x;
+  if (q < n && q != own)
+    asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(pf.p[q] + own), "r"(e) : "memory");
+}
+
+cudaError_t launch_tp_signal(int* ctr, int* const* peer_flags, int n, int own, cudaStream_t s) {
+  if (n < 1 || n > kTpMax || own < 0 || own >= n) return cudaErrorInvalidValue;
+  TpPeers pf;
+  for (int q = 0; q < n; ++q) pf.p[q] = peer_flags[q];
+  tp_signal_kernel<<<1, 32, 0, s>>>(ctr, pf, n, own);
+  return cudaGetLastError();
 }
 
 // Whether the fused consumer supports this (d, N, K): callers use the unfused path otherwise.

@@ -55,7 +55,32 @@ struct GemmEpi {
   unsigned long long* amax = nullptr;
   unsigned amax_v0 = 0;
   int* amax_err = nullptr;
+  // EPI_STORE_ACT into a double-buffered slot chosen on the device (NEXT-3, the fused tensor-parallel
+  // all-reduce): the rows go to out + ((*out_sel + 1) & 1) * out_sel_stride elements -- the slot of the
+  // all-reduce whose epoch the next tp_signal launch will publish (*out_sel + 1)
+  const int* out_sel = nullptr;
+  long long out_sel_stride = 0;
 };
+
+// NEXT-3: the peers' exchange slots a fused residual + norm consumer sums (tensor parallelism over
+// peer memory, include/specformer.h sf_tp_xch_*). Rank q's slot for epoch e is slot[q] +
+// (e & 1) * slot_elems ([T, d] bf16, the rank's row-parallel GEMM output); flags[q] holds the last
+// epoch rank q published into THIS rank's region, *ctr this rank's current epoch.
+constexpr int kTpMax = 8;
+struct TpSrc {
+  const __nv_bfloat16* slot[kTpMax];
+  const int* ctr = nullptr;
+  const int* flags = nullptr;
+  int* err = nullptr;         // sticky: a peer's flag did not arrive within the time limit
+  long long slot_elems = 0;
+  int n = 0;                  // ranks (0: off)
+  int own = 0;
+};
+struct TpPeers {
+  int* p[kTpMax];
+};
+// rank `own` publishes its next epoch: ++*ctr, then (system-scope release) peer_flags[q][own] = epoch
+cudaError_t launch_tp_signal(int* ctr, int* const* peer_flags, int n, int own, cudaStream_t s);
 
 struct GemmScratch {
   float* partial = nullptr;   // split-K partials
@@ -94,13 +119,14 @@ bool gemm_partial_geom(int T, int N, int K, PartialGeom* g, int drain = -1);
 // Fused consumer of EPI_PARTIAL (and plain residual/norm): for virtual row r (T*rep rows, source
 // row r / rep, columns [(r % rep) * d, +d) of the GEMM output):
 //   x = (resid ? resid[r] : 0) + (add ? add[r] : 0) + (bias ? bias[col] : 0) + sum_k-segments partial
+//   (tp: + sum over the ranks q = 0, 1, .. of the bf16 exchange slots, after waiting for their epoch)
 //   (fixed order; partial may be null -- add carries a tensor-parallel all-reduced GEMM output)
 //   out[r] = x (fp32, out may alias resid); tap[r] = x (optional);
 //   xn[r] = bf16(x / sqrt(mean(x^2) + eps) * gamma) (optional, gamma != null)
 bool resid_norm_supported(int d, int T, int N, int K);
 cudaError_t launch_resid_norm(const float* partial, const PartialGeom* g, int T, int rep, int d, const float* resid,
                               const float* add, const float* bias, float* out, float* tap, const float* gamma,
-                              float eps, __nv_bfloat16* xn, cudaStream_t s);
+                              float eps, __nv_bfloat16* xn, cudaStream_t s, const TpSrc* tp = nullptr);
 
 // Gate/up (SwiGLU, rows interleaved) -> down in ONE launch: phase A computes act = SwiGLU(A . WA^T)
 // [T, NA/2] and publishes each finished 128-row tile; phase B (down, NB rows, K = NA/2) streams its

@@ -298,6 +298,16 @@ struct sf_handle {
     bool graph_safe = false;  // only device work is enqueued (NCCL): decode_steps may capture it
   } coll;
   void* nccl_comm = nullptr;
+  // NEXT-3 fused TP all-reduce over peer memory: this rank's exchange region ([0, 128) the epochs the
+  // peers published into it, [128] this rank's epoch counter, [256 ..) two bf16 [R, d] slots), the
+  // peers' regions (mapped through CUDA IPC, or direct pointers in a local group), mode 0 off / 1 IPC /
+  // 2 local group (eager: a host barrier after every signal, so no kernel waits on another rank's)
+  char* xch = nullptr;
+  size_t xch_bytes = 0;
+  char* xpeer[kTpMax] = {};
+  bool xopened[kTpMax] = {};
+  int xmode = 0;
+  void* xgroup = nullptr;  // (mode 2) the sf_local_group
   int *tok_rows, *pos0_pf, *seq_len, *n_prev, *last_token, *r_b, *prompt_len, *draft, *greedy, *accept_len,
       *emitted, *err, *step_counter, *g_pf, *prompt, *d_logcap;
   // state
@@ -494,9 +504,42 @@ static cudaError_t tp_max(sf_handle* h, unsigned long long* buf, int64_t n) {
   return h->coll.max_u64(h->coll.ctx, buf, n, h->st);
 }
 
+static constexpr size_t kXchHead = 256;  // flags [0, 128), epoch counter at 128
+static void local_xch_barrier(sf_handle* h);
+
 static bool gemm_resid_norm(sf_handle* h, cudaError_t* err, const void* A, int lda, const void* W, int T, int N,
                             int K, int rep, const float* resid, const float* bias, float* out, float* tap,
                             const float* gamma, bool row_parallel = false) {
+  if (row_parallel && h->p.tp > 1 && h->xmode && rep == 1 && N == h->p.d) {
+    // NEXT-3: the GEMM stores its bf16 output straight into this rank's exchange slot of the coming
+    // epoch, tp_signal publishes the epoch to every peer, and the residual + norm consumer sums the
+    // ranks' slots in rank order over peer memory (the all-reduce fused into the consumer; no NCCL
+    // launch, no fp32 round trip). Every rank adds the same values in the same order: same bits.
+    const Plan& p = h->p;
+    int* ctr = (int*)(h->xch + 128);
+    GemmEpi ep = epi_act(h->xch + kXchHead, N);
+    ep.out_sel = ctr;
+    ep.out_sel_stride = (long long)p.R * p.d;
+    if ((*err = gemm(h, A, lda, W, T, N, K, ep)) != cudaSuccess) return true;
+    int* pf[kTpMax];
+    for (int q = 0; q < p.tp; ++q) pf[q] = (int*)h->xpeer[q];
+    h->launches += 2;
+    if ((*err = launch_tp_signal(ctr, pf, p.tp, p.tp_rank, h->st)) != cudaSuccess) return true;
+    if (h->xmode == 2) local_xch_barrier(h);
+    TpSrc ts;
+    for (int q = 0; q < p.tp; ++q) ts.slot[q] = (const __nv_bfloat16*)(h->xpeer[q] + kXchHead);
+    ts.ctr = ctr;
+    ts.flags = (const int*)h->xch;
+    ts.err = h->err;
+    ts.slot_elems = (long long)p.R * p.d;
+    ts.n = p.tp;
+    ts.own = p.tp_rank;
+    ProfScope ps(h, 2, (double)T * N * (2.0 * p.tp + 4.0 * 2));
+    *err = dbg_sync(h, "resid_norm(tp fused)", launch_resid_norm(nullptr, nullptr, T, rep, p.d, resid, nullptr, bias, out,
+                                                                 tap, gamma, h->c.rms_eps,
+                                                                 gamma ? (__nv_bfloat16*)h->xn : nullptr, h->st, &ts));
+    return true;
+  }
   if (row_parallel && h->p.tp > 1) {
     if ((*err = gemm(h, A, lda, W, T, N, K, epi_f32(h->tpbuf, N))) != cudaSuccess) return true;
     if ((*err = tp_sum(h, h->tpbuf, (int64_t)T * N)) != cudaSuccess) return true;
@@ -1049,6 +1092,8 @@ struct sf_local_group {
   std::vector<cudaEvent_t> ev_in, ev_mid;
   std::vector<void*> tmp;
   std::vector<size_t> tmp_bytes;
+  std::vector<char*> xch;          // NEXT-3: the ranks' exchange regions
+  std::vector<cudaEvent_t> ev_x;   // and their signal events
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     const int64_t g = gen;
@@ -1088,6 +1133,16 @@ static cudaError_t local_reduce(void* ctx, void* buf, int64_t n, int mode, cudaS
   if (e == cudaSuccess) e = cudaMemcpyAsync(buf, g->tmp[r], bytes, cudaMemcpyDeviceToDevice, s);
   g->barrier();
   return e;
+}
+// (local group, fused TP all-reduce) every rank's epoch signal has executed before any rank's
+// consumer starts: its flag waits are then already satisfied, no kernel waits on another rank's
+static void local_xch_barrier(sf_handle* h) {
+  sf_local_group* g = (sf_local_group*)h->xgroup;
+  const int r = h->p.tp_rank;
+  cudaEventRecord(g->ev_x[r], h->st);
+  g->barrier();
+  for (int q = 0; q < g->n; ++q) cudaStreamWaitEvent(h->st, g->ev_x[q], 0);
+  g->barrier();  // (every wait enqueued before any rank re-records its event)
 }
 static cudaError_t local_sum_f32(void* ctx, float* buf, int64_t n, cudaStream_t s) {
   return local_reduce(ctx, buf, n, 0, s);
@@ -1667,6 +1722,7 @@ sf_status specformer_sync(sf_handle* h) {
   SF_TRY(cudaMemcpy(&err, h->err, 4, cudaMemcpyDeviceToHost));
   if (err & 1) return set_err(h, SF_ERR_NONFINITE, "non-finite logits");
   if (err & 2) return set_err(h, SF_ERR_CAPACITY, "KV page pool exhausted");
+  if (err & 4) return set_err(h, SF_ERR_NCCL, "tensor-parallel exchange: a peer's epoch flag did not arrive within 5 s");
 #ifdef SF_WITH_NCCL
   if (h->nccl_comm) {  // asynchronous communicator errors (a peer failed, a network / NVLink error)
     ncclResult_t ar = ncclSuccess;
@@ -1692,6 +1748,9 @@ void specformer_destroy(sf_handle* h) {
   if (h->nccl_comm) ncclCommDestroy((ncclComm_t)h->nccl_comm);
 #endif
   if (h->coll.sum_f32 == local_sum_f32) delete (LocalCtx*)h->coll.ctx;
+  for (int q = 0; q < kTpMax; ++q)
+    if (h->xopened[q]) cudaIpcCloseMemHandle(h->xpeer[q]);
+  if (h->xch) cudaFree(h->xch);
   delete h;
 }
 
@@ -1740,9 +1799,12 @@ sf_local_group* sf_local_group_create(int32_t n) {
   g->tmp_bytes.assign(n, 0);
   g->ev_in.resize(n);
   g->ev_mid.resize(n);
+  g->ev_x.resize(n);
+  g->xch.assign(n, nullptr);
   for (int i = 0; i < n; ++i) {
     cudaEventCreateWithFlags(&g->ev_in[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&g->ev_mid[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&g->ev_x[i], cudaEventDisableTiming);
   }
   return g;
 }
@@ -1753,6 +1815,7 @@ void sf_local_group_destroy(sf_local_group* g) {
   for (int i = 0; i < g->n; ++i) {
     cudaEventDestroy(g->ev_in[i]);
     cudaEventDestroy(g->ev_mid[i]);
+    cudaEventDestroy(g->ev_x[i]);
     if (g->tmp[i]) cudaFree(g->tmp[i]);
   }
   delete g;
@@ -1767,6 +1830,76 @@ sf_status sf_local_group_attach(sf_handle* h, sf_local_group* g, int32_t rank) {
   h->coll.max_u64 = local_max_u64;
   h->coll.ctx = new LocalCtx{g, rank};
   h->coll.graph_safe = false;
+  return SF_OK;
+}
+
+// ---- NEXT-3: the fused TP all-reduce's exchange regions
+static sf_status xch_alloc(sf_handle* h) {
+  if (h->p.tp < 2 || h->p.tp > kTpMax) return set_err(h, SF_ERR_STATE, "exchange regions need 2 <= tp_size <= 8");
+  if (!h->bf) return set_err(h, SF_ERR_UNSUPPORTED, "the fused TP all-reduce is bf16 only");
+  if (h->state != ST_INIT) return set_err(h, SF_ERR_STATE, "attach the exchange before the first prefill");
+  if (h->xch) return SF_OK;
+  const size_t bytes = kXchHead + (size_t)2 * h->p.R * h->p.d * 2;
+  void* x = nullptr;
+  SF_TRY(cudaMalloc(&x, bytes));
+  SF_TRY(cudaMemset(x, 0, bytes));
+  SF_TRY(cudaDeviceSynchronize());
+  h->xch = (char*)x;
+  h->xch_bytes = bytes;
+  return SF_OK;
+}
+
+sf_status sf_tp_xch_handle(sf_handle* h, uint8_t* out_64) {
+  if (!h || !out_64) return SF_ERR_ARG;
+  const sf_status s = xch_alloc(h);
+  if (s != SF_OK) return s;
+  cudaIpcMemHandle_t ih;
+  static_assert(sizeof(ih) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  SF_TRY(cudaIpcGetMemHandle(&ih, h->xch));
+  memcpy(out_64, &ih, 64);
+  return SF_OK;
+}
+
+sf_status sf_tp_xch_attach(sf_handle* h, const uint8_t* handles) {
+  if (!h || !handles) return SF_ERR_ARG;
+  if (h->xmode) return set_err(h, SF_ERR_STATE, "an exchange is already attached");
+  const sf_status s = xch_alloc(h);
+  if (s != SF_OK) return s;
+  const int tp = h->p.tp, r = h->p.tp_rank;
+  for (int q = 0; q < tp; ++q) {
+    if (q == r) {
+      h->xpeer[q] = h->xch;
+      continue;
+    }
+    cudaIpcMemHandle_t ih;
+    memcpy(&ih, handles + 64 * q, 64);
+    void* ptr = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&ptr, ih, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (int j = 0; j < q; ++j)
+        if (h->xopened[j]) cudaIpcCloseMemHandle(h->xpeer[j]), h->xopened[j] = false, h->xpeer[j] = nullptr;
+      return set_err(h, SF_ERR_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    }
+    h->xpeer[q] = (char*)ptr;
+    h->xopened[q] = true;
+  }
+  h->xmode = 1;
+  return SF_OK;
+}
+
+sf_status sf_local_group_xch_attach(sf_handle* h, sf_local_group* g) {
+  if (!h || !g) return SF_ERR_ARG;
+  if (h->coll.sum_f32 != local_sum_f32 || ((LocalCtx*)h->coll.ctx)->g != g)
+    return set_err(h, SF_ERR_STATE, "attach the local group (sf_local_group_attach) first");
+  if (h->xmode) return set_err(h, SF_ERR_STATE, "an exchange is already attached");
+  const sf_status s = xch_alloc(h);
+  if (s != SF_OK) return s;
+  g->xch[h->p.tp_rank] = h->xch;
+  g->barrier();  // every rank's region registered
+  for (int q = 0; q < g->n; ++q) h->xpeer[q] = g->xch[q];
+  g->barrier();
+  h->xgroup = g;
+  h->xmode = 2;
   return SF_OK;
 }
 

@@ -296,6 +296,24 @@ class Engine:
         self._group = group  # keep alive
         self._check(self.lib.sf_local_group_attach(self.h, group.g, rank), "sf_local_group_attach")
 
+    def xch_handle(self) -> bytes:
+        """NEXT-3: this rank's exchange region as 64 IPC-handle bytes (tp.share_xch_handles gathers them)."""
+        buf = (C.c_uint8 * 64)()
+        self._check(self.lib.sf_tp_xch_handle(self.h, buf), "sf_tp_xch_handle")
+        return bytes(buf)
+
+    def attach_xch(self, handles: list[bytes]):
+        """NEXT-3 (one process per GPU): map the peers' exchange regions; the row-parallel all-reduce then
+        runs fused into the residual + norm consumer over peer memory."""
+        if len(handles) != self.cfg.tp_size or any(len(x) != 64 for x in handles):
+            raise ValueError("one 64-byte handle per rank, in rank order")
+        buf = (C.c_uint8 * (64 * len(handles))).from_buffer_copy(b"".join(handles))
+        self._check(self.lib.sf_tp_xch_attach(self.h, buf), "sf_tp_xch_attach")
+
+    def attach_local_xch(self):
+        """NEXT-3 on a local group (tests): every rank's thread calls it after attach_local_group."""
+        self._check(self.lib.sf_local_group_xch_attach(self.h, self._group.g), "sf_local_group_xch_attach")
+
     def kernel_launches(self) -> int:
         return int(self.lib.specformer_kernel_launches(self.h))
 

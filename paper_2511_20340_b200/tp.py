@@ -19,6 +19,22 @@ def share_unique_id(make_id, rank: int) -> bytes:
     return obj[0]
 
 
+def share_xch_handles(own: bytes, rank: int, world: int) -> list[bytes]:
+    """NEXT-3: all-gather every rank's 64-byte exchange-region handle (Engine.xch_handle), in rank
+    order, for Engine.attach_xch. Only the host carries the handles; the data path never touches
+    torch.distributed."""
+    if len(own) != 64:
+        raise ValueError("an exchange handle is 64 bytes")
+    if world == 1:
+        return [own]
+    out = [None] * world
+    dist.all_gather_object(out, (rank, own))
+    got = dict(out)
+    if sorted(got) != list(range(world)):
+        raise RuntimeError(f"exchange handles from ranks {sorted(got)}, expected 0..{world - 1}")
+    return [got[q] for q in range(world)]
+
+
 class LazyWeights(Mapping):
     """A weight dict whose tensors are drawn on access (synth.make_weights with names={name}), so a
     rank never holds more than one full tensor besides its packed slices (70B: 141 GB of bf16)."""

@@ -111,3 +111,43 @@ def test_tp_unique_id_broadcast_gloo():
         assert uid == bytes(range(128))
         assert ncalls == (1 if rank == 0 else 0)  # make_id on rank 0 only (counted before the draw)
         assert b == "B" and names == ["a", "b"] and n == 2
+
+
+def _xch_worker(rank, world, port, out_q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2511_20340_b200 import tp as tpmod
+        own = bytes([rank + 1]) * 64
+        hs = tpmod.share_xch_handles(own, rank, world)
+        bad = None
+        try:
+            tpmod.share_xch_handles(b"x", rank, world)
+        except ValueError as e:
+            bad = str(e)
+        out_q.put((rank, hs, bad))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def test_tp_xch_handles_allgather_gloo():
+    """NEXT-3 host plumbing: every rank receives all ranks' 64-byte exchange handles in rank order
+    (what sf_tp_xch_attach expects); a malformed handle is refused before any collective."""
+    world = 3
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_xch_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [bytes([r + 1]) * 64 for r in range(world)]
+    for rank, hs, bad in res:
+        assert hs == want
+        assert bad and "64 bytes" in bad
