@@ -18,9 +18,9 @@ for B in (64, 16, 1):
     out[f"7b_b{B}"] = t
     shutil.copy(f"{src}/ktrace_b{B}.txt", f"profiles/r02/ktrace_7b_b{B}.txt")
 json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
-for n in ("b64", "b1"):
+for n in ("b64", "b1", "attn_b64"):
     r = subprocess.run(["python", "tools/ncu_full_summary.py", f"{src}/full_{n}.ncu-rep"], capture_output=True, text=True)
-    open(f"profiles/r02/full_7b_{n}.txt", "w").write(r.stdout)
+    open(f"profiles/r02/full_7b_{n}.txt".replace("full_7b_attn_b64", "full_7b_b64_attn"), "w").write(r.stdout)
 shutil.copy(f"{src}/bench_default.json", "profiles/r02/bench/bench_7b_default.json")
 d = json.loads(open(f"{src}/bench_default.json").read().strip().splitlines()[-1])
 print("B64", round(d["value"]), round(d["ms_per_step"], 3), [round(x, 1) for x in d["windows"]["ms"]],
