@@ -35,10 +35,10 @@ constexpr int KV_BYTES = CH * HD * 2;      // 32 KB
 constexpr int STAGE_BYTES = 2 * KV_BYTES;  // 64 KB
 constexpr int NW = kAttnWarps;      // compute warps
 constexpr int KPW = CH / NW;         // keys per warp slice of a chunk (one 16-key m-tile)
-constexpr int TR = kAttnTileRows;    // query rows per tile (one 8-column n-tile)
 constexpr int NTHR = (NW + 1) * 32;  // + the TMA producer warp
-static_assert(KPW == 16 && TR == 8, "one m-tile of keys and one n-tile of queries per warp");
-constexpr int MERGE_BYTES = NW * TR * (HD + 2) * 4;  // per-warp O, m, l for the final merge
+static_assert(KPW == 16, "one m-tile of keys per warp");
+constexpr int kFoldSeg = 64;  // key segments one row can span (the fold's factor table in the merge buffer)
+constexpr int MERGE_BYTES = NW * 8 * (HD + 2) * 4;  // per-warp O, m, l of 8 rows for the final merge
 constexpr int SMEM = NST * STAGE_BYTES + MERGE_BYTES + 2 * NST * 8 + 1024 + 64 + 16;
 
 SF_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
@@ -81,7 +81,10 @@ struct Item {
 
 }  // namespace
 
-// item = (b * Hkv + kvh) * ntiles + qt. Warps 0..NW-1 compute, warp NW produces.
+// item = (b * Hkv + kvh) * ntiles + qt. Warps 0..NW-1 compute, warp NW produces. NQ: 8-column n-tiles per
+// query tile (tiles of 8 NQ rows; 2 when a sequence's (query, head) rows exceed 8, so each (sequence, kv
+// head) streams its keys once for up to 16 rows)
+template <int NQ>
 __global__ void __launch_bounds__(NTHR, 1) attn_fd_kernel(const __grid_constant__ CUtensorMap tmK,
                                                          const __grid_constant__ CUtensorMap tmV,
                                                          const __grid_constant__ CUtensorMap tmK4,
@@ -94,10 +97,11 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fd_kernel(const __grid_constant_
   const uint32_t raw = smem_u32(sm_raw);
   uint8_t* sm = sm_raw + (((raw + 1023u) & ~1023u) - raw);
   const uint32_t sbase = smem_u32(sm);
-  float* mrg = reinterpret_cast<float*>(sm + NST * STAGE_BYTES);  // [NW][TR][HD] O, then [NW][TR] m, l
-  float* mrg_m = mrg + NW * TR * HD;
-  float* mrg_l = mrg_m + NW * TR;
-  uint64_t* full = reinterpret_cast<uint64_t*>(mrg_l + NW * TR);
+  constexpr int TT = 8 * NQ;  // query rows per tile
+  float* mrg = reinterpret_cast<float*>(sm + NST * STAGE_BYTES);  // [NW][8][HD] O, then [NW][8] m, l
+  float* mrg_m = mrg + NW * 8 * HD;
+  float* mrg_l = mrg_m + NW * 8;
+  uint64_t* full = reinterpret_cast<uint64_t*>(mrg_l + NW * 8);
   uint64_t* empty = full + NST;
   int* mrg_flag = reinterpret_cast<int*>(empty + NST);
 
@@ -118,8 +122,8 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fd_kernel(const __grid_constant_
     r /= ntiles;
     it.kvh = r % p.Hkv;
     it.b = r / p.Hkv;
-    const int r0 = it.qt * TR;
-    const int nr = min(TR, R - r0);
+    const int r0 = it.qt * TT;
+    const int nr = min(TT, R - r0);
     const int kmax = min(p.pos0[it.b] + attn_row_last(p, min(p.q_len - 1, (r0 + nr - 1) / G)), p.max_key - 1);
     const int nch = kmax / CH + 1;
     it.nseg = (nch + seg_ch - 1) / seg_ch;
@@ -200,8 +204,9 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fd_kernel(const __grid_constant_
   }
 
   // ---- compute warps. Keys are the MMA rows (S^T = K Q^T, O^T += V^T P^T): warp w's 16 keys of a chunk
-  // are one m-tile, the tile's <= 8 query rows one 8-column n-tile. A column's arithmetic never depends
-  // on the other columns or on the tile's row count (batch invariance, C23).
+  // are one m-tile, the tile's query rows one (NQ = 1) or two (NQ = 2) 8-column n-tiles sharing the K / V
+  // fragments. A column's arithmetic never depends on the other columns, the n-tile count or the tile's
+  // row count (batch invariance, C23; the same bits for 8- and 16-row tiles).
   const float scale_log2 = 0.08838834764831845f * 1.4426950408889634f;  // log2(e) / sqrt(128)
   const int mi = lane >> 3, ri = lane & 7;
   int seq = 0;
@@ -210,271 +215,315 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fd_kernel(const __grid_constant_
     item_of(item, it);
     if (it.c0 >= it.c1) continue;  // segment beyond this group's keys
     const unsigned long long ti0 = g_kt.rec ? kt_now() : 0ull;
-    const int r0 = it.qt * TR;
-    const int nr = min(TR, R - r0);
+    const int r0 = it.qt * TT;
+    const int nr = min(TT, R - r0);
+    const bool two = NQ == 2 && nr > 8;  // (warp-uniform) the second n-tile holds rows
     const int base = p.pos0[it.b];
-    // Q^T B fragments: query column q = g, dims kk*16 + 2 t4 (+1) and + 8 (bf16, rope_append's RNE)
-    uint32_t qb[8][2];
-    {
-      const bool ok = g < nr;
-      const int rr = r0 + (ok ? g : 0), qi = rr / G, h = it.kvh * G + rr % G;
+    // Q^T B fragments: query column q = nq*8 + g, dims kk*16 + 2 t4 (+1) and + 8 (bf16, rope_append's RNE)
+    uint32_t qb[NQ][8][2];
+#pragma unroll
+    for (int nq = 0; nq < NQ; ++nq) {
+      const int r = nq * 8 + g;
+      const bool ok = r < nr;
+      const int rr = r0 + (ok ? r : 0), qi = rr / G, h = it.kvh * G + rr % G;
       const uint32_t* qrow = reinterpret_cast<const uint32_t*>(reinterpret_cast<const __nv_bfloat16*>(p.q) +
                                                                ((size_t)(it.b * p.q_len + qi) * p.Hq + h) * HD);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const int d0 = kk * 16 + 2 * t4;
-        qb[kk][0] = ok ? qrow[d0 / 2] : 0u;
-        qb[kk][1] = ok ? qrow[(d0 + 8) / 2] : 0u;
+        qb[nq][kk][0] = ok ? qrow[d0 / 2] : 0u;
+        qb[nq][kk][1] = ok ? qrow[(d0 + 8) / 2] : 0u;
       }
     }
-    // this thread's query columns q = 2 t4 + j: visibility bound (last visible key)
-    int posq[2];
-    bool okq[2];
+    // this thread's query columns q = nq*8 + 2 t4 + j: visibility bound (last visible key)
+    int posq[NQ][2];
+    bool okq[NQ][2];
+    int wlast = -1;  // the last key any column of the tile sees: a warp slice past it is skipped (its
+                     // chunk step would leave (m, l, O) unchanged)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int q = 2 * t4 + j;
-      okq[j] = q < nr;
-      posq[j] = base + attn_row_last(p, (r0 + min(q, nr - 1)) / G);
-    }
-    // the last key any column of the tile sees: a warp slice past it is fully masked, and its chunk step
-    // would leave (m, l, O) unchanged -- the warp skips it
-    int wlast = max(okq[0] ? posq[0] : -1, okq[1] ? posq[1] : -1);
+    for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int q = nq * 8 + 2 * t4 + j;
+        okq[nq][j] = q < nr;
+        posq[nq][j] = base + attn_row_last(p, (r0 + min(q, nr - 1)) / G);
+        if (okq[nq][j]) wlast = max(wlast, posq[nq][j]);
+      }
 #pragma unroll
     for (int off = 1; off <= 16; off <<= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, off));
-    float m[2], l[2], tm[2], tl[2];  // per column: running max (log2 domain), sum; folded
+    float m[NQ][2], l[NQ][2];  // per column: running max (log2 domain), sum
 #pragma unroll
-    for (int j = 0; j < 2; ++j) m[j] = tm[j] = -INFINITY, l[j] = tl[j] = 0.f;
-    // O^T accumulators: m-tile md = dims md*16 .. +15; [c]: (dim g | g+8, column 2 t4 | +1)
-    float o[8][4], to[8][4];
+    for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) m[nq][j] = -INFINITY, l[nq][j] = 0.f;
+    // O^T accumulators: m-tile md = dims md*16 .. +15, n-tile nq; [c]: (dim g | g+8, column 2 t4 | +1)
+    float o[8][NQ][4];
 #pragma unroll
     for (int md = 0; md < 8; ++md)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) o[md][i] = to[md][i] = 0.f;
-    // this warp's fold of its finished segments (starts empty: fold(empty, x) == x exactly)
-    auto fold_segment = [&]() {
-      float ft[2], fc[2];
+      for (int nq = 0; nq < NQ; ++nq)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const float M = fmaxf(tm[j], m[j]);
-        ft[j] = (tm[j] == -INFINITY) ? 0.f : exp2f(tm[j] - M);
-        fc[j] = (m[j] == -INFINITY) ? 0.f : exp2f(m[j] - M);
-        tl[j] = __fadd_rn(__fmul_rn(tl[j], ft[j]), __fmul_rn(l[j], fc[j]));
-        tm[j] = M;
-        m[j] = -INFINITY;
-        l[j] = 0.f;
-      }
+        for (int i = 0; i < 4; ++i) o[md][nq][i] = 0.f;
+    const auto row_slot = [&](int r) {  // (token, head) of tile row r
+      const int rr = r0 + r, qi = rr / G, h = it.kvh * G + rr % G;
+      return (size_t)(it.b * p.q_len + qi) * p.Hq + h;
+    };
+    // a finished key segment's warp state -> the partial buffer (folded in segment order at the end), and a
+    // fresh state for the next segment
+    auto publish_segment = [&](int sgi) {
+#pragma unroll
+      for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int q = nq * 8 + 2 * t4 + j;
+          if (q < nr) {
+            const size_t bq = (row_slot(q) * p.nchunk_max + sgi) * NW + warp;
+#pragma unroll
+            for (int md = 0; md < 8; ++md) {
+              p.part_o[bq * HD + md * 16 + g] = o[md][nq][j];
+              p.part_o[bq * HD + md * 16 + g + 8] = o[md][nq][2 + j];
+            }
+            if (g == 0) {
+              p.part_ml[2 * bq] = m[nq][j];
+              p.part_ml[2 * bq + 1] = l[nq][j];
+            }
+          }
+          m[nq][j] = -INFINITY;
+          l[nq][j] = 0.f;
+        }
 #pragma unroll
       for (int md = 0; md < 8; ++md)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          to[md][i] = __fadd_rn(__fmul_rn(to[md][i], ft[i & 1]), __fmul_rn(o[md][i], fc[i & 1]));
-          o[md][i] = 0.f;
-        }
+        for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) o[md][nq][i] = 0.f;
     };
 
     for (int c = it.c0; c < it.c1; ++c, ++seq) {
-      if (c != it.c0 && c % seg_ch == 0) fold_segment();  // segment boundary (group schedule)
+      if (c != it.c0 && c % seg_ch == 0) publish_segment(c / seg_ch - 1);  // segment boundary (group schedule)
       const int st = seq % NST;
       mbar_wait(&full[st], (uint32_t)(seq / NST) & 1u);
       const int kstart = c * CH + warp * KPW;
       if (probe) {  // (finite output: a state of one unit-weight zero row)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) m[j] = 0.f, l[j] = 1.f;
+        for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) m[nq][j] = 0.f, l[nq][j] = 1.f;
       } else if (kstart <= wlast) {  // (warp-uniform)
         const uint32_t kb = sbase + st * STAGE_BYTES, vb = kb + KV_BYTES;
-        // S^T = K_w Q^T: 16 keys x 8 columns, 8 k-steps of 16 dims (two independent accumulator chains)
-        float s[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+        // S^T = K_w Q^T: 16 keys x 8 columns per n-tile, 8 k-steps of 16 dims (two accumulator chains)
+        float s[NQ][4], s2[NQ][4];
+#pragma unroll
+        for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) s[nq][i] = s2[nq][i] = 0.f;
 #pragma unroll
         for (int kk = 0; kk < 8; kk += 2) {
           uint32_t a[4], a2[4];
           ldsm_x4(kb + swz(warp * KPW + (mi & 1) * 8 + ri, kk * 2 + (mi >> 1)), a[0], a[1], a[2], a[3]);
           ldsm_x4(kb + swz(warp * KPW + (mi & 1) * 8 + ri, kk * 2 + 2 + (mi >> 1)), a2[0], a2[1], a2[2], a2[3]);
-          mma16816(s, a, qb[kk][0], qb[kk][1]);
-          mma16816(s2, a2, qb[kk + 1][0], qb[kk + 1][1]);
+#pragma unroll
+          for (int nq = 0; nq < NQ; ++nq) {
+            if (nq == 1 && !two) break;
+            mma16816(s[nq], a, qb[nq][kk][0], qb[nq][kk][1]);
+            mma16816(s2[nq], a2, qb[nq][kk + 1][0], qb[nq][kk + 1][1]);
+          }
         }
-        // mask, new running max per column (exact; masked entries excluded)
-        float cm[2] = {-INFINITY, -INFINITY};
+        uint32_t pb[NQ][2];
+        bool resc = false;  // some column of the warp raised its max
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int key = kstart + g + 8 * (i >> 1), j = i & 1;
-          const bool vis = okq[j] && key <= posq[j];
-          const float v = vis ? (s[i] + s2[i]) * scale_log2 : -INFINITY;
-          s[i] = v;
-          cm[j] = fmaxf(cm[j], v);
+        for (int nq = 0; nq < NQ; ++nq) {
+          if (nq == 1 && !two) break;
+          // mask, new running max per column (exact; masked entries excluded)
+          float cm[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int key = kstart + g + 8 * (i >> 1), j = i & 1;
+            const bool vis = okq[nq][j] && key <= posq[nq][j];
+            const float v = vis ? (s[nq][i] + s2[nq][i]) * scale_log2 : -INFINITY;
+            s[nq][i] = v;
+            cm[j] = fmaxf(cm[j], v);
+          }
+          float af[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+#pragma unroll
+            for (int off = 4; off <= 16; off <<= 1) cm[j] = fmaxf(cm[j], __shfl_xor_sync(0xffffffffu, cm[j], off));
+            const float mn = fmaxf(m[nq][j], cm[j]);
+            af[j] = (mn == -INFINITY) ? 1.f : exp2f(m[nq][j] - mn);
+            m[nq][j] = mn;
+          }
+          // P^T and its column sums; P^T's 8x8 blocks transposed in registers into the PV B fragments
+          float e[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) e[i] = (s[nq][i] == -INFINITY) ? 0.f : exp2f(s[nq][i] - m[nq][i & 1]);
+          float ps[2] = {e[0] + e[2], e[1] + e[3]};
+          pb[nq][0] = movmatrix_trans(pack_bf16(e[0], e[1]));  // keys 0..7 of the slice
+          pb[nq][1] = movmatrix_trans(pack_bf16(e[2], e[3]));  // keys 8..15
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+#pragma unroll
+            for (int off = 4; off <= 16; off <<= 1) ps[j] += __shfl_xor_sync(0xffffffffu, ps[j], off);
+            l[nq][j] = l[nq][j] * af[j] + ps[j];
+          }
+          // (no column of the warp raised its max: every factor is exactly 1 and the rescale is the identity)
+          if (!__all_sync(0xffffffffu, af[0] == 1.f && af[1] == 1.f)) {
+            resc = true;
+#pragma unroll
+            for (int md = 0; md < 8; ++md)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) o[md][nq][i] *= af[i & 1];
+          }
         }
-        float af[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-#pragma unroll
-          for (int off = 4; off <= 16; off <<= 1) cm[j] = fmaxf(cm[j], __shfl_xor_sync(0xffffffffu, cm[j], off));
-          const float mn = fmaxf(m[j], cm[j]);
-          af[j] = (mn == -INFINITY) ? 1.f : exp2f(m[j] - mn);
-          m[j] = mn;
-        }
-        // P^T and its column sums; P^T's 8x8 blocks transposed in registers into the PV B fragments
-        float e[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) e[i] = (s[i] == -INFINITY) ? 0.f : exp2f(s[i] - m[i & 1]);
-        float ps[2] = {e[0] + e[2], e[1] + e[3]};
-        const uint32_t pb0 = movmatrix_trans(pack_bf16(e[0], e[1]));  // keys 0..7 of the slice
-        const uint32_t pb1 = movmatrix_trans(pack_bf16(e[2], e[3]));  // keys 8..15
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-#pragma unroll
-          for (int off = 4; off <= 16; off <<= 1) ps[j] += __shfl_xor_sync(0xffffffffu, ps[j], off);
-          l[j] = l[j] * af[j] + ps[j];
-        }
-        // (no column of the warp raised its max: every factor is exactly 1 and the rescale is the identity)
-        if (!__all_sync(0xffffffffu, af[0] == 1.f && af[1] == 1.f)) {
-#pragma unroll
-          for (int md = 0; md < 8; ++md)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) o[md][i] *= af[i & 1];
-        }
-        // O^T += V_w^T P^T: m-tiles md (16 dims), one k-step (the slice's 16 keys)
+        (void)resc;
+        // O^T += V_w^T P^T: m-tiles md (16 dims), one k-step (the slice's 16 keys), n-tiles nq
 #pragma unroll
         for (int md = 0; md < 8; ++md) {
           uint32_t a[4];
           ldsm_x4_t(vb + swz(warp * KPW + (mi >> 1) * 8 + ri, md * 2 + (mi & 1)), a[0], a[1], a[2], a[3]);
-          mma16816(o[md], a, pb0, pb1);
+#pragma unroll
+          for (int nq = 0; nq < NQ; ++nq) {
+            if (nq == 1 && !two) break;
+            mma16816(o[md][nq], a, pb[nq][0], pb[nq][1]);
+          }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
     }
     const unsigned long long ti1 = g_kt.rec ? kt_now() : 0ull;
-    fold_segment();
     const int group = (it.b * p.Hkv + it.kvh) * ntiles + it.qt;
-    auto row_slot = [&](int r) {  // (token, head) of tile row r
-      const int rr = r0 + r, qi = rr / G, h = it.kvh * G + rr % G;
-      return (size_t)(it.b * p.q_len + qi) * p.Hq + h;
-    };
-    if (split && it.nseg > 1) {
-      // ---- segment schedule: publish this segment's warp states
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int q = 2 * t4 + j;
-        if (q >= nr) continue;
-        const size_t bq = (row_slot(q) * p.nchunk_max + it.seg) * NW + warp;
-#pragma unroll
-        for (int md = 0; md < 8; ++md) {
-          p.part_o[bq * HD + md * 16 + g] = to[md][j];
-          p.part_o[bq * HD + md * 16 + g + 8] = to[md][2 + j];
+    // several segments: each one's warp states are in the partial buffer, folded below in segment order
+    // (the split schedule's CTA that completes the group, or the group's own CTA)
+    const bool multi = it.nseg > 1;
+    if (multi) {
+      publish_segment(split ? it.seg : it.nseg - 1);
+      if (split) {
+        named_bar(1, NW * 32);
+        if (tid == 0) {
+          int prev;
+          asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(p.seg_cnt + group) : "memory");
+          mrg_flag[0] = prev == it.nseg - 1;
+          if (prev == it.nseg - 1) p.seg_cnt[group] = 0;  // re-arm for the next launch
         }
-        if (g == 0) {
-          p.part_ml[2 * bq] = tm[j];
-          p.part_ml[2 * bq + 1] = tl[j];
-        }
+        named_bar(1, NW * 32);
+        if (!mrg_flag[0]) continue;
+      } else {
+        __threadfence();
+        named_bar(1, NW * 32);
       }
-      named_bar(1, NW * 32);
-      if (tid == 0) {
-        int prev;
-        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(p.seg_cnt + group) : "memory");
-        mrg_flag[0] = prev == it.nseg - 1;
-        if (prev == it.nseg - 1) p.seg_cnt[group] = 0;  // re-arm for the next launch
-      }
-      named_bar(1, NW * 32);
-      if (!mrg_flag[0]) continue;
-      // the group's last segment: fold every warp slot's segment states in segment order (the same
-      // operations as the in-register fold). Step factors per (warp, row) first (one thread each),
-      // then every thread (one dimension, one parity of the (warp, row) pairs) streams the O values,
-      // all segments of 4 pairs in flight at a time.
-      constexpr int SMAX = 8;
-      float* fa_s = mrg;                    // [NW][TR][SMAX] factor of the running state, then
-      float* fb_s = mrg + NW * TR * SMAX;   // of segment s; the O fold overwrites mrg[] afterwards
-      const int nsg = min(it.nseg, SMAX);
-      if (tid < NW * nr) {
-        const int w = tid / nr, r = tid % nr;
-        const size_t s0 = row_slot(r) * p.nchunk_max;
-        float m = -INFINITY, l = 0.f;
-        for (int sg = 0; sg < nsg; ++sg) {
-          const size_t bs = (s0 + sg) * NW + w;
-          const float ms = __ldcg(&p.part_ml[2 * bs]), ls = __ldcg(&p.part_ml[2 * bs + 1]);
-          const float M = fmaxf(m, ms);
-          const float fa = (m == -INFINITY) ? 0.f : exp2f(m - M);
-          const float fb = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
-          l = __fadd_rn(__fmul_rn(l, fa), __fmul_rn(ls, fb));
-          m = M;
-          fa_s[(w * TR + r) * SMAX + sg] = fa;
-          fb_s[(w * TR + r) * SMAX + sg] = fb;
-        }
-        mrg_m[w * TR + r] = m;
-        mrg_l[w * TR + r] = l;
-      }
-      named_bar(1, NW * 32);
-      const int d = tid & (HD - 1), par = tid >> 7;  // dimension, pair parity
-      const int npair = NW * nr;                      // (warp, row) pairs q = w nr + r
-      float Ofold[NW * TR / 2];
-      for (int i0 = 0; 2 * i0 < npair; i0 += 4) {
-        float Os[4][SMAX];
+    }
+    // ---- the merge, one 8-row half of the tile at a time through the 8-row merge buffer: the warp
+    // states (or, for the group's last segment, every warp slot's segment states folded in segment
+    // order -- the same operations as the in-register fold), then the fixed-order merge and normalise
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int q = min(2 * (i0 + j) + par, npair - 1), w = q / nr, r = q % nr;
-          const size_t s0 = row_slot(r) * p.nchunk_max;
-#pragma unroll
-          for (int sg = 0; sg < SMAX; ++sg)
-            Os[j][sg] = (sg < nsg) ? __ldcg(&p.part_o[((s0 + sg) * NW + w) * HD + d]) : 0.f;
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int q = min(2 * (i0 + j) + par, npair - 1), w = q / nr, r = q % nr;
-          float O = 0.f;
-#pragma unroll
-          for (int sg = 0; sg < SMAX; ++sg)
-            if (sg < nsg)
-              O = __fadd_rn(__fmul_rn(O, fa_s[(w * TR + r) * SMAX + sg]), __fmul_rn(Os[j][sg], fb_s[(w * TR + r) * SMAX + sg]));
-          if (i0 + j < NW * TR / 2) Ofold[i0 + j] = O;
-        }
-      }
-      named_bar(1, NW * 32);  // factors consumed before mrg[] is overwritten
-      for (int i = 0; 2 * i + par < npair; ++i) {
-        const int q = 2 * i + par, w = q / nr, r = q % nr;
-        mrg[(w * TR + r) * HD + d] = Ofold[i];
-      }
-    } else {
-      // ---- the warp states, for the merge in fixed order
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int q = 2 * t4 + j;
-        if (q < nr) {  // (rows of the tile past the block's rows are never read)
-#pragma unroll
-          for (int md = 0; md < 8; ++md) {
-            mrg[(warp * TR + q) * HD + md * 16 + g] = to[md][j];
-            mrg[(warp * TR + q) * HD + md * 16 + g + 8] = to[md][2 + j];
+    for (int hf = 0; hf < NQ; ++hf) {
+      if (hf == 1 && !two) break;
+      const int rb = hf * 8, nh = min(8, nr - rb);  // rows [rb, rb + nh) of the tile
+      if (multi) {
+        // step factors per (warp, row) first (one thread each), then every thread (one dimension, one
+        // parity of the (warp, row) pairs) folds the O values of 4 pairs, 8 segments' loads in flight
+        float* fa_s = mrg;                   // [NW][8][kFoldSeg] factor of the running state, then
+        float* fb_s = mrg + NW * 8 * kFoldSeg;  // of segment s; the O fold overwrites mrg[] afterwards
+        const int nsg = it.nseg;
+        if (tid < NW * nh) {
+          const int w = tid / nh, r = tid % nh;
+          const size_t s0 = row_slot(rb + r) * p.nchunk_max;
+          float m_ = -INFINITY, l_ = 0.f;
+          for (int sg = 0; sg < nsg; ++sg) {
+            const size_t bs = (s0 + sg) * NW + w;
+            const float ms = __ldcg(&p.part_ml[2 * bs]), ls = __ldcg(&p.part_ml[2 * bs + 1]);
+            const float M = fmaxf(m_, ms);
+            const float fa = (m_ == -INFINITY) ? 0.f : exp2f(m_ - M);
+            const float fb = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
+            l_ = __fadd_rn(__fmul_rn(l_, fa), __fmul_rn(ls, fb));
+            m_ = M;
+            fa_s[(w * 8 + r) * kFoldSeg + sg] = fa;
+            fb_s[(w * 8 + r) * kFoldSeg + sg] = fb;
           }
-          if (g == 0) {
-            mrg_m[warp * TR + q] = tm[j];
-            mrg_l[warp * TR + q] = tl[j];
+          mrg_m[w * 8 + r] = m_;
+          mrg_l[w * 8 + r] = l_;
+        }
+        named_bar(1, NW * 32);
+        const int d = tid & (HD - 1), par = tid >> 7;  // dimension, pair parity
+        const int npair = NW * nh;                      // (warp, row) pairs q = w nh + r
+        float Ofold[NW * 8 / 2];
+        for (int i0 = 0; 2 * i0 < npair; i0 += 4) {
+          float O[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int sg0 = 0; sg0 < nsg; sg0 += 8) {
+            float Os[4][8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int q = min(2 * (i0 + j) + par, npair - 1), w = q / nh, r = q % nh;
+              const size_t s0 = row_slot(rb + r) * p.nchunk_max;
+#pragma unroll
+              for (int sg = 0; sg < 8; ++sg)
+                Os[j][sg] = (sg0 + sg < nsg) ? __ldcg(&p.part_o[((s0 + sg0 + sg) * NW + w) * HD + d]) : 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int q = min(2 * (i0 + j) + par, npair - 1), w = q / nh, r = q % nh;
+              const float* fa = fa_s + (w * 8 + r) * kFoldSeg + sg0;
+              const float* fb = fb_s + (w * 8 + r) * kFoldSeg + sg0;
+#pragma unroll
+              for (int sg = 0; sg < 8; ++sg)
+                if (sg0 + sg < nsg) O[j] = __fadd_rn(__fmul_rn(O[j], fa[sg]), __fmul_rn(Os[j][sg], fb[sg]));
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (i0 + j < NW * 8 / 2) Ofold[i0 + j] = O[j];
+        }
+        named_bar(1, NW * 32);  // factors consumed before mrg[] is overwritten
+        for (int i = 0; 2 * i + par < npair; ++i) {
+          const int q = 2 * i + par, w = q / nh, r = q % nh;
+          mrg[(w * 8 + r) * HD + d] = Ofold[i];
+        }
+      } else {
+        // this warp's states of the half's rows (one segment: a fold from the empty state is the identity)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int q = 2 * t4 + j;
+          if (q < nh) {  // (rows of the tile past the block's rows are never read)
+#pragma unroll
+            for (int md = 0; md < 8; ++md) {
+              mrg[(warp * 8 + q) * HD + md * 16 + g] = o[md][hf][j];
+              mrg[(warp * 8 + q) * HD + md * 16 + g + 8] = o[md][hf][2 + j];
+            }
+            if (g == 0) {
+              mrg_m[warp * 8 + q] = m[hf][j];
+              mrg_l[warp * 8 + q] = l[hf][j];
+            }
           }
         }
       }
-    }
-    named_bar(1, NW * 32);
-    // per-row merge factors once (row r: thread r): M = max_w m_w, f_w = 2^(m_w - M), L = sum_w l_w f_w
-    // (same values and order as forming them per element)
-    if (tid < nr) {
-      const int r = tid;
-      float M = -INFINITY;
+      named_bar(1, NW * 32);
+      // per-row merge factors once (row r: thread r): M = max_w m_w, f_w = 2^(m_w - M), L = sum_w l_w f_w
+      // (same values and order as forming them per element)
+      if (tid < nh) {
+        const int r = tid;
+        float M = -INFINITY;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) M = fmaxf(M, mrg_m[w * TR + r]);
-      float L = 0.f;
+        for (int w = 0; w < NW; ++w) M = fmaxf(M, mrg_m[w * 8 + r]);
+        float L = 0.f;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const float f = (mrg_m[w * TR + r] == -INFINITY) ? 0.f : exp2f(mrg_m[w * TR + r] - M);
-        L += mrg_l[w * TR + r] * f;
-        mrg_m[w * TR + r] = f;
+        for (int w = 0; w < NW; ++w) {
+          const float f = (mrg_m[w * 8 + r] == -INFINITY) ? 0.f : exp2f(mrg_m[w * 8 + r] - M);
+          L += mrg_l[w * 8 + r] * f;
+          mrg_m[w * 8 + r] = f;
+        }
+        mrg_l[r] = L;
       }
-      mrg_l[r] = L;
-    }
-    named_bar(1, NW * 32);
-    for (int e = tid; e < nr * HD; e += NW * 32) {
-      const int r = e / HD, d = e % HD;
-      float acc = 0.f;
+      named_bar(1, NW * 32);
+      for (int e = tid; e < nh * HD; e += NW * 32) {
+        const int r = e / HD, d = e % HD;
+        float acc = 0.f;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) acc += mrg[(w * TR + r) * HD + d] * mrg_m[w * TR + r];
-      reinterpret_cast<__nv_bfloat16*>(p.out)[row_slot(r) * HD + d] = __float2bfloat16_rn(acc / mrg_l[r]);
+        for (int w = 0; w < NW; ++w) acc += mrg[(w * 8 + r) * HD + d] * mrg_m[w * 8 + r];
+        reinterpret_cast<__nv_bfloat16*>(p.out)[row_slot(rb + r) * HD + d] = __float2bfloat16_rn(acc / mrg_l[r]);
+      }
+      named_bar(1, NW * 32);
     }
-    named_bar(1, NW * 32);
     if (tid == 0 && g_kt.rec) kt_item((uint32_t)(it.seg | (it.nseg << 8) | ((it.c1 - it.c0) << 16)), ti0, ti1, kt_now());
   }
 }
@@ -518,19 +567,25 @@ cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
   static bool attr = false;
   static int num_sms = 148;
   if (!attr) {
-    cudaFuncSetAttribute(attn_fd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(attn_fd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(attn_fd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     attr = true;
   }
   const int G = p.Hq / p.Hkv;
-  const int ntiles = (p.q_len * G + TR - 1) / TR;
+  // 16-row tiles (two n-tiles) when a sequence's (query, head) rows exceed 8 -- 13B at k = 8, GQA -- so
+  // its keys are streamed once per 16 rows; the same per-column arithmetic either way (bit-identical).
+  // SF_ATTN_NQ=1 forces 8-row tiles (tests)
+  static const int env_nq = getenv("SF_ATTN_NQ") ? atoi(getenv("SF_ATTN_NQ")) : 0;
+  const int NQ = (p.q_len * G > 8 && env_nq != 1) ? 2 : 1;
+  const int ntiles = (p.q_len * G + 8 * NQ - 1) / (8 * NQ);
   // segment size override (tests exercise the multi-segment fold at short contexts; read per launch)
   const int env_seg = getenv("SF_ATTN_SEG") ? atoi(getenv("SF_ATTN_SEG")) : 0;
   const int seg_keys = (env_seg >= CH && env_seg % CH == 0) ? env_seg : kAttnSeg;
   const int nseg_max = (p.max_key + seg_keys - 1) / seg_keys;
-  if (nseg_max > p.nchunk_max || !p.seg_cnt) return cudaErrorInvalidValue;
+  if (nseg_max > p.nchunk_max || nseg_max > kFoldSeg || !p.seg_cnt) return cudaErrorInvalidValue;
   // schedule (the arithmetic is the same): a CTA per (group, segment) when the groups alone would
   // leave most SMs idle, else a CTA per group folding its segments in registers
   const int n_groups = p.B * p.Hkv * ntiles;
@@ -546,7 +601,7 @@ cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
   if (!encode_kv_map4(&mk4, p.Kp, p.Hkv, p.n_pages) || !encode_kv_map4(&mv4, p.Vp, p.Hkv, p.n_pages))
     return cudaErrorInvalidValue;
   static const int env_probe = getenv("SF_ATTN_PROBE") ? atoi(getenv("SF_ATTN_PROBE")) : 0;
-  launch_k(attn_fd_kernel, dim3(grid), dim3(NTHR), SMEM, s, mk, mv, mk4, mv4, p, ntiles, nseg_max, seg_keys, n_items,
+  launch_k(NQ == 2 ? attn_fd_kernel<2> : attn_fd_kernel<1>, dim3(grid), dim3(NTHR), SMEM, s, mk, mv, mk4, mv4, p, ntiles, nseg_max, seg_keys, n_items,
            split | (env_probe ? 2 : 0));
   return cudaGetLastError();
 }
