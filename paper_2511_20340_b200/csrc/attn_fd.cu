@@ -578,7 +578,7 @@ cudaError_t launch_attention_fd(const AttnParams& p, cudaStream_t s) {
   // 16-row tiles (two n-tiles) when a sequence's (query, head) rows exceed 8 -- 13B at k = 8, GQA -- so
   // its keys are streamed once per 16 rows; the same per-column arithmetic either way (bit-identical).
   // SF_ATTN_NQ=1 forces 8-row tiles (tests)
-  static const int env_nq = getenv("SF_ATTN_NQ") ? atoi(getenv("SF_ATTN_NQ")) : 0;
+  const int env_nq = getenv("SF_ATTN_NQ") ? atoi(getenv("SF_ATTN_NQ")) : 0;  // (read per launch: tests compare)
   const int NQ = (p.q_len * G > 8 && env_nq != 1) ? 2 : 1;
   const int ntiles = (p.q_len * G + 8 * NQ - 1) / (8 * NQ);
   // segment size override (tests exercise the multi-segment fold at short contexts; read per launch)

@@ -618,17 +618,20 @@ def test_layer_seq_block_sizes_change_on_one_handle():
 def test_launch_shape_switches_bit_exact(cfg, monkeypatch):
     """Per-launch shape choices that keep every row's arithmetic: the residual + RMSNorm consumer with one
     or two virtual threads per real thread (SF_RN_FOLD 1 / 2: the canonical reduction tree either way) and
-    the prefill in sequence groups or all sequences per pass (SF_PF_GROUP 1 / 0). Logits, draft logits,
-    tokens and accept lengths are bit-identical across the four combinations, with ragged forced
+    the prefill in sequence groups or all sequences per pass (SF_PF_GROUP 1 / 0), and attention query tiles
+    of 16 rows (two n-tiles, the default when a sequence's (query, head) rows exceed 8) or 8 (SF_ATTN_NQ=1).
+    Logits, draft logits,
+    tokens and accept lengths are bit-identical across the combinations, with ragged forced
     acceptance (prompt 200: prefill groups of 2 sequences)."""
     w, prompts = setup(cfg, seed=31, jitter=0.1)
     k, n_steps = cfg.draft_len, 4
     ar = run_gpu(cfg, w, prompts, n_steps * (k + 1) + k + 2, k=0)["tokens"]
     slots = corrupt_slots(n_steps, cfg.batch, k, seed=11)
     runs = []
-    for fold, group in (("1", "1"), ("2", "1"), ("1", "0"), ("2", "0")):
+    for fold, group, nq in (("1", "1", "0"), ("2", "1", "0"), ("1", "0", "0"), ("2", "0", "0"), ("1", "1", "1")):
         monkeypatch.setenv("SF_RN_FOLD", fold)
         monkeypatch.setenv("SF_PF_GROUP", group)
+        monkeypatch.setenv("SF_ATTN_NQ", nq)  # 1: 8-row attention tiles only (GQA: 16-row tiles by default)
         runs.append(forced_run(cfg, w, prompts, n_steps, slots, ar))
     for other in runs[1:]:
         for s1, s2 in zip(runs[0]["steps"], other["steps"]):
