@@ -498,29 +498,34 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fd_kernel(const __grid_constant_
         }
       }
       named_bar(1, NW * 32);
-      // per-row merge factors once (row r: thread r): M = max_w m_w, f_w = 2^(m_w - M), L = sum_w l_w f_w
-      // (same values and order as forming them per element)
-      if (tid < nh) {
-        const int r = tid;
-        float M = -INFINITY;
+      // warp r merges row r (the 8 compute warps <-> the half's <= 8 rows): lanes 0..NW-1 hold warp slot
+      // w's m / l and form f_w = 2^(m_w - M), M = max_w m_w; L = sum_w l_w f_w and every output dimension
+      // acc = sum_w O_w f_w are accumulated in the fixed order w = 0, 1, .. (lane l: dims 4l .. 4l + 3)
+      if (warp < nh) {
+        const int r = warp;
+        const float mw = lane < NW ? mrg_m[lane * 8 + r] : -INFINITY;
+        float M = mw;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) M = fmaxf(M, mrg_m[w * 8 + r]);
-        float L = 0.f;
+        for (int off = 1; off < NW; off <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+        const float f = (lane < NW && mw != -INFINITY) ? exp2f(mw - M) : 0.f;
+        const float lw = lane < NW ? mrg_l[lane * 8 + r] : 0.f;
+        float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
-          const float f = (mrg_m[w * 8 + r] == -INFINITY) ? 0.f : exp2f(mrg_m[w * 8 + r] - M);
-          L += mrg_l[w * 8 + r] * f;
-          mrg_m[w * 8 + r] = f;
+          const float fw = __shfl_sync(0xffffffffu, f, w);
+          L += __shfl_sync(0xffffffffu, lw, w) * fw;
+          const float4 v = *reinterpret_cast<const float4*>(mrg + (w * 8 + r) * HD + 4 * lane);
+          acc[0] += v.x * fw;
+          acc[1] += v.y * fw;
+          acc[2] += v.z * fw;
+          acc[3] += v.w * fw;
         }
-        mrg_l[r] = L;
-      }
-      named_bar(1, NW * 32);
-      for (int e = tid; e < nh * HD; e += NW * 32) {
-        const int r = e / HD, d = e % HD;
-        float acc = 0.f;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) acc += mrg[(w * 8 + r) * HD + d] * mrg_m[w * 8 + r];
-        reinterpret_cast<__nv_bfloat16*>(p.out)[row_slot(rb + r) * HD + d] = __float2bfloat16_rn(acc / mrg_l[r]);
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(acc[0] / L, acc[1] / L);
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(acc[2] / L, acc[3] / L);
+        uint2 pk;
+        pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + row_slot(rb + r) * HD + 4 * lane) = pk;
       }
       named_bar(1, NW * 32);
     }

@@ -14,6 +14,8 @@ from paper_2511_20340_b200.timeline import REC, critical_path, name
 
 def main():
     cfg = get_config(os.environ.get("CFG", "7b"))
+    if os.environ.get("K"):
+        cfg = cfg.replace(draft_len=int(os.environ["K"]))
     B = int(os.environ.get("B", "64")); steps = int(os.environ.get("STEPS", "2"))
     w = make_weights(cfg, seed=0, device="cuda")
     eng = Engine(EngineConfig.from_model(cfg, max_batch=B, max_seq=cfg.prompt_len + 32 * (cfg.draft_len + 1),
