@@ -293,6 +293,20 @@ def test_attention_segments_fold(cfg, monkeypatch):
         assert np.array_equal(s1["logits"], s2["logits"])
 
 
+def test_attention_many_segments_fold(monkeypatch):
+    """A context of more than 8 key segments (SF_ATTN_SEG=128, 1200-key prompts: 10 segments): the split
+    schedule is off (it holds <= 8), so the group's own CTA publishes every segment's warp states and folds
+    them in segment order, 8 segments' loads per batch (two batches here). Oracle parity at the bf16
+    tolerance and GPU SD == GPU AR."""
+    monkeypatch.setenv("SF_ATTN_SEG", "128")
+    cfg = MID.replace(name="mid-long", batch=2, prompt_len=1200, gen_len=10)
+    w, prompts = setup(cfg, seed=9, jitter=0.1)
+    res = run_gpu(cfg, w, prompts, cfg.gen_len, want_logits=True)
+    assert _check_bf16(cfg, w, prompts, res, seqs=(0,)) > 4
+    ar = run_gpu(cfg, w, prompts, cfg.gen_len, k=0)
+    assert ar["tokens"] == res["tokens"]
+
+
 @pytest.mark.parametrize("cfg", [MID, GQA], ids=["mha128", "gqa4"])
 def test_fused_rope_epilogue_bit_exact(cfg, monkeypatch):
     """The QKV GEMM's fused RoPE / paged-append epilogue (small blocks) and the separate RoPE kernel
