@@ -144,64 +144,80 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fd_kernel(const __grid_constant_
     reinterpret_cast<uint4*>(sm)[i] = make_uint4(0u, 0u, 0u, 0u);
   fence_proxy_async();
   __syncthreads();
-  pdl_wait();  // queries, lengths and the new KV rows come from the previous kernels
-  kt_.mark();
-  pdl_trigger();
 
   if (warp == NW) {
-    // ---- TMA producer
+    // ---- TMA producer. Chunk c of item it into ring slot st (sequence number sq of this CTA's chunks)
+    auto issue = [&](const Item& it, int kmax, int c, int sq, bool wait_slot) {
+      const int st = sq % NST;
+      const int kstart = c * CH;
+      const int npages = (min(CH, kmax + 1 - kstart) + 15) / 16;
+      // the chunk's page-table entries are requested before waiting for the slot (the load's latency
+      // hides behind the wait instead of delaying the TMA issue once the slot is free)
+      const int pg = (lane < npages) ? p.block_table[it.b * p.pages_per_seq + kstart / 16 + lane] : 0;
+      if (wait_slot) mbar_wait(&empty[st], ((uint32_t)(sq / NST) & 1u) ^ 1u);
+      const int pg0 = __shfl_sync(0xffffffffu, pg, 0);
+      // a full chunk whose pages are consecutive in the pool (the identity page table, and any run of a
+      // permuted one): 4 TMA boxes of 8 pages x 16 keys x 64 dims instead of 32 one-page boxes. A tail
+      // chunk loads just its npages pages: boxes past the last key would be HBM bytes the math masks away
+      // (~16% of the KV stream at a 512-key prompt); the stale rows left in the slot are finite
+      const bool run = npages == 8 && __all_sync(0xffffffffu, lane >= npages || pg == pg0 + lane);
+      if (run) {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[st], (uint32_t)(4 * 8 * 16 * 128));
+          uint8_t* kb = sm + st * STAGE_BYTES;
+          uint8_t* vb = kb + KV_BYTES;
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            tma_load_4d(kb + hf * (CH * 128), &tmK4, &full[st], hf * 64, 0, it.kvh, pg0, kEvictFirst);
+            tma_load_4d(vb + hf * (CH * 128), &tmV4, &full[st], hf * 64, 0, it.kvh, pg0, kEvictFirst);
+          }
+        }
+        __syncwarp();
+        return;
+      }
+      if (lane == 0) mbar_arrive_expect_tx(&full[st], (uint32_t)(npages * 4 * 16 * 128));
+      __syncwarp();
+      for (int i = 0; i < npages; ++i) {
+        const int blk = __shfl_sync(0xffffffffu, pg, i);
+        if (lane == 0) {
+          const int row = (blk * p.Hkv + it.kvh) * 16;
+          uint8_t* kb = sm + st * STAGE_BYTES;
+          uint8_t* vb = kb + KV_BYTES;
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            tma_load_2d(kb + hf * (CH * 128) + i * 16 * 128, &tmK, &full[st], hf * 64, row, kEvictFirst);
+            tma_load_2d(vb + hf * (CH * 128) + i * 16 * 128, &tmV, &full[st], hf * 64, row, kEvictFirst);
+          }
+        }
+      }
+      __syncwarp();
+    };
+    // Before the grid dependency resolves: the first item's leading chunks whose keys all precede its
+    // sequence's first new row. They hold only KV rows written by earlier steps; the previous kernel (the
+    // RoPE / append step) writes rows pos0 .. only. pos0 and the page table come from launches at least two
+    // back, complete once this kernel runs (PDL: the previous kernel passed its own dependency wait).
+    int pre = 0;
+    if ((int)blockIdx.x < n_items) {
+      Item it;
+      const int kmax = item_of(blockIdx.x, it);
+      const int base = p.pos0[it.b];
+      for (int c = it.c0; c < it.c1 && pre < NST && (c + 1) * CH <= base; ++c, ++pre) issue(it, kmax, c, pre, false);
+    }
+    pdl_wait();  // the new KV rows (and, for the compute warps, the queries) come from the previous kernel
+    kt_.mark();
+    pdl_trigger();
     int seq = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       Item it;
       const int kmax = item_of(item, it);
-      for (int c = it.c0; c < it.c1; ++c, ++seq) {
-        const int st = seq % NST;
-        const int kstart = c * CH;
-        const int npages = (min(CH, kmax + 1 - kstart) + 15) / 16;
-        // the chunk's page-table entries are requested before waiting for the slot (the load's latency
-        // hides behind the wait instead of delaying the TMA issue once the slot is free)
-        const int pg = (lane < npages) ? p.block_table[it.b * p.pages_per_seq + kstart / 16 + lane] : 0;
-        mbar_wait(&empty[st], ((uint32_t)(seq / NST) & 1u) ^ 1u);
-        const int pg0 = __shfl_sync(0xffffffffu, pg, 0);
-        // a full chunk whose pages are consecutive in the pool (the identity page table, and any run of a
-        // permuted one): 4 TMA boxes of 8 pages x 16 keys x 64 dims instead of 32 one-page boxes. A tail
-        // chunk loads just its npages pages: boxes past the last key would be HBM bytes the math masks away
-        // (~16% of the KV stream at a 512-key prompt); the stale rows left in the slot are finite
-        const bool run = npages == 8 && __all_sync(0xffffffffu, lane >= npages || pg == pg0 + lane);
-        if (run) {
-          if (lane == 0) {
-            mbar_arrive_expect_tx(&full[st], (uint32_t)(4 * 8 * 16 * 128));
-            uint8_t* kb = sm + st * STAGE_BYTES;
-            uint8_t* vb = kb + KV_BYTES;
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-              tma_load_4d(kb + hf * (CH * 128), &tmK4, &full[st], hf * 64, 0, it.kvh, pg0, kEvictFirst);
-              tma_load_4d(vb + hf * (CH * 128), &tmV4, &full[st], hf * 64, 0, it.kvh, pg0, kEvictFirst);
-            }
-          }
-          __syncwarp();
-          continue;
-        }
-        if (lane == 0) mbar_arrive_expect_tx(&full[st], (uint32_t)(npages * 4 * 16 * 128));
-        __syncwarp();
-        for (int i = 0; i < npages; ++i) {
-          const int blk = __shfl_sync(0xffffffffu, pg, i);
-          if (lane == 0) {
-            const int row = (blk * p.Hkv + it.kvh) * 16;
-            uint8_t* kb = sm + st * STAGE_BYTES;
-            uint8_t* vb = kb + KV_BYTES;
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-              tma_load_2d(kb + hf * (CH * 128) + i * 16 * 128, &tmK, &full[st], hf * 64, row, kEvictFirst);
-              tma_load_2d(vb + hf * (CH * 128) + i * 16 * 128, &tmV, &full[st], hf * 64, row, kEvictFirst);
-            }
-          }
-        }
-        __syncwarp();
-      }
+      for (int c = it.c0; c < it.c1; ++c, ++seq)
+        if (seq >= pre) issue(it, kmax, c, seq, true);
     }
     return;
   }
+  pdl_wait();  // queries, lengths and the new KV rows come from the previous kernels
+  kt_.mark();
+  pdl_trigger();
 
   // ---- compute warps. Keys are the MMA rows (S^T = K Q^T, O^T += V^T P^T): warp w's 16 keys of a chunk
   // are one m-tile, the tile's query rows one (NQ = 1) or two (NQ = 2) 8-column n-tiles sharing the K / V
