@@ -89,7 +89,8 @@ typedef struct {
                           decoding through verify_step + accept_commit (no draft head), used by
                           the GPU SD == AR losslessness test.                               */
   int32_t max_batch;   /* B_max sequences handled by this handle                          */
-  int32_t max_seq;     /* per-sequence KV capacity (positions), multiple of kv_block      */
+  int32_t max_seq;     /* per-sequence KV capacity (positions), multiple of kv_block;
+                          <= 131072 for bf16 head_dim 128 (64 attention key segments of 2048) */
   int32_t kv_block;    /* paged-KV page size in tokens; must be 16                        */
   float rope_theta;    /* 10000 (reading C5)                                               */
   float rms_eps;       /* 1e-6 (reading C3)                                                */

@@ -55,6 +55,8 @@ bool valid_config(const sf_config* c, std::string* why) {
   if (c->max_batch < 1 || c->max_batch > 1024) return fail("max_batch must be in [1, 1024]");
   if (c->kv_block != 16) return fail("kv_block must be 16");
   if (c->max_seq < 16 || c->max_seq % 16) return fail("max_seq must be a positive multiple of 16");
+  // (bf16 flash-decoding attention: a row folds at most 64 key segments of kAttnSeg keys)
+  if (c->dtype == SF_BF16 && c->head_dim == 128 && c->max_seq > 64 * kAttnSeg) return fail("max_seq must be <= 131072");
   if (!(c->rms_eps > 0.f)) return fail("rms_eps must be > 0");
   if (!(c->rope_theta > 0.f)) return fail("rope_theta must be > 0");
   if (c->dtype != SF_FP32 && c->dtype != SF_BF16) return fail("dtype must be SF_FP32 or SF_BF16");

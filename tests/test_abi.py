@@ -90,6 +90,12 @@ def test_bf16_shape_constraints(lib):
     c = _c("small")
     c.vocab = 32001
     assert lib.sf_weights_bytes(C.byref(c)) == -1
+    # bf16 head_dim 128: the flash-decoding attention folds at most 64 key segments of 2048 keys
+    c = _c("7b")
+    c.max_seq = 64 * 2048
+    assert lib.sf_workspace_bytes(C.byref(c)) > 0
+    c.max_seq = 64 * 2048 + 16
+    assert lib.sf_workspace_bytes(C.byref(c)) == -1
 
 
 def test_null_handle_calls(lib):
